@@ -1,0 +1,387 @@
+#!/usr/bin/env python
+"""Benchmark of the quadratic-layer hot path (BASELINE.json metric).
+
+Default workload (N=1): BASELINE config 2 -- one quadratic conv layer
+(proposed neuron), NCHW 128x64x32x32 -> 64, 3x3/s1/p1, bf16, forward +
+backward. A "step" = pack weights + forward + backward (weight, bias and
+input gradients) over one batch. Metric: algorithmic TFLOP/s
+(9 GEMMs x 2*M*K*N: 86.97 GFLOP per step).
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling, every rank runs its own
+batch-128 step and the weight/bias gradients are all-reduced (mean) over NCCL
+each step -- the one real exchange of data-parallel training.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload c2|c1|c5_64x56|...]
+
+``--impl reference`` times the reference algorithm on the host CPU (the
+oracle port of the reference's numpy path; the reference is pure Python and
+is not installable on the GPU box) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (family, kind, N, C, F, H, W, r, s, p, dtype)
+    "c2": ("proposed", "conv", 128, 64, 64, 32, 32, 3, 1, 1, "bf16"),
+    "c2_fp32": ("proposed", "conv", 128, 64, 64, 32, 32, 3, 1, 1, "fp32"),
+    "c1": ("proposed", "fc", 256, 512, 512, 1, 1, 1, 1, 0, "fp32"),
+    "c5_proposed_64x56": ("proposed", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
+    "c5_proposed_128x28": ("proposed", "conv", 64, 128, 128, 28, 28, 3, 1, 1, "bf16"),
+    "c5_proposed_256x14": ("proposed", "conv", 64, 256, 256, 14, 14, 3, 1, 1, "bf16"),
+    "c5_proposed_512x7": ("proposed", "conv", 64, 512, 512, 7, 7, 3, 1, 1, "bf16"),
+    "c5_t4_64x56": ("t4", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
+    "c5_t2lin_64x56": ("t2_linear", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
+    "c5_t4_512x7": ("t4", "conv", 64, 512, 512, 7, 7, 3, 1, 1, "bf16"),
+    "c5_t2lin_512x7": ("t2_linear", "conv", 64, 512, 512, 7, 7, 3, 1, 1, "bf16"),
+}
+METRIC = "quadratic_conv_fwd_bwd_tflops"
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            pk = json.load(fh)
+        return {"bf16": pk["bf16_tflops"], "bf16_sustained": pk["bf16_tflops_sustained"],
+                "hbm": pk["hbm_gbs"], "src": "measured"}
+    except Exception:  # noqa: BLE001
+        return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "src": "fallback"}
+
+
+def make_spec(wl):
+    from paper_2204_01701_b200.spec import QuadraticLayerSpec
+    fam, kind, n, c, f, h, w, r, s, p, _ = wl
+    return QuadraticLayerSpec(kind=kind, family=fam, in_dim=c, out_dim=f, kernel=r, stride=s,
+                              pad=p)
+
+
+def flops_of(wl, n=None):
+    from paper_2204_01701_b200.spec import gemm_flops
+    fam, kind, n0, c, f, h, w, r, s, p, _ = wl
+    return gemm_flops(make_spec(wl), n if n is not None else n0, h, w)
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ---------------------------------------------------------------------------
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:  # noqa: BLE001
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:  # noqa: BLE001
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# CPU side: the reference algorithm (oracle port of the reference's numpy path)
+# ---------------------------------------------------------------------------
+def cpu_sample(wl, batch, reps):
+    """Time reference forward + symbolic_backward (fp64 numpy, all host
+    threads) on `batch` samples; returns (best seconds, flops)."""
+    from oracle import quadra_oracle as Q
+    fam, kind, n, c, f, h, w, r, s, p, _ = wl
+    x, P, g = Q.synthetic_layer(fam, kind, batch, c, f, h, w, r, s, p, seed=0)
+    geo = Q.Geometry(kind, r, s, p)
+    best = None
+    for _ in range(reps):
+        t0 = time.perf_counter()
+        y, a, b = Q.forward(fam, geo, P, x)
+        Q.symbolic_backward(fam, geo, P, x, a, b, g)
+        dt = time.perf_counter() - t0
+        best = dt if best is None else min(best, dt)
+    return best, flops_of(wl, batch)
+
+
+def cpu_batch_for(wl):
+    """Bounded CPU sample: ~1-3 s per repetition on a few host cores."""
+    fam, kind, n, c, f, h, w, r, s, p, _ = wl
+    if kind == "fc":
+        return n
+    per_sample = flops_of(wl, 1)
+    return max(1, min(n, int(6e9 // per_sample)))
+
+
+def run_reference(args, wl, wl_name):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    cores = os.cpu_count()
+    batch = cpu_batch_for(wl)
+    times = []
+    flops = flops_of(wl, batch)
+    for i in range(args.warmup + args.steps):
+        t, _ = cpu_sample(wl, batch, 1)
+        if i >= args.warmup:
+            times.append(t)
+    mean = sum(times) / len(times)
+    value = flops / mean / 1e12
+    sample = (f"{wl_name} at batch {batch} of {wl[2]} (fp64 numpy/BLAS reference algorithm: "
+              f"im2col + GEMM + col2im), mean of {args.steps} steps")
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": mean * 1e3 * wl[2] / batch, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config_of(wl, wl_name, args.gpus),
+           "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
+def config_of(wl, name, ngpu):
+    fam, kind, n, c, f, h, w, r, s, p, dt = wl
+    return {"workload": f"{name}: {fam} {kind} {n}x{c}x{h}x{w} -> {f}, k{r} s{s} p{p}, {dt}",
+            "family": fam, "global_batch": n * ngpu, "per_gpu_batch": n,
+            "parallelism": f"dp{ngpu}",
+            "l2": "flushed between timed steps (256 MiB write, untimed)",
+            "flops_per_step_per_gpu": flops_of(wl)}
+
+
+# ---------------------------------------------------------------------------
+# GPU side
+# ---------------------------------------------------------------------------
+def run_ours(args, wl, wl_name):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_01701_b200 import _lib, neurons
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    fam, kind, n, c, f, h, w, r, s, p, dts = wl
+    dt = torch.bfloat16 if dts == "bf16" else torch.float32
+    spec = make_spec(wl)
+
+    from oracle import quadra_oracle as Q  # seeded input generator only (not timed)
+    x64, P64, g64 = Q.synthetic_layer(fam, kind, n, c, f, h, w, r, s, p, seed=rank)
+    x = torch.as_tensor(x64, device=dev).to(dt)
+    gy = torch.as_tensor(g64, device=dev).to(dt)
+    if kind == "conv":
+        x = x.contiguous(memory_format=torch.channels_last)
+        gy = gy.contiguous(memory_format=torch.channels_last)
+    params = {k_: torch.as_tensor(v, dtype=torch.float32, device=dev) for k_, v in P64.items()}
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(want_dx=True, want_dw=True):
+        y, cache = neurons.forward(spec, params, x, dtype=dt)
+        grads, dx = neurons.symbolic_backward(spec, params, cache, gy, want_dx=want_dx,
+                                              want_dw=want_dw)
+        if world > 1 and want_dw:
+            flat = torch.cat([t_.reshape(-1) for t_ in grads.values()])
+            dist.all_reduce(flat)
+            flat.div_(world)
+        return y, grads, dx
+
+    def timed(fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+               for _ in range(k)]
+        for i in range(k):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            fn()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps)
+    launches = _lib.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    total_ms = sum(ms)
+    if world > 1:
+        tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        total_ms = float(tt.item())
+    ms_step = total_ms / args.steps
+    flops = flops_of(wl)
+    value = world * flops / (ms_step * 1e-3) / 1e12
+
+    # ---- per-kernel phases (roofline of the dominant kernel) ----
+    pk = load_peaks()
+    phase = {}
+    if True:  # every rank (keeps the collectives below in step)
+        def fwd_only():
+            neurons.forward(spec, params, x, dtype=dt)
+        y0, cache0 = neurons.forward(spec, params, x, dtype=dt)
+
+        def dgrad_only():
+            neurons.symbolic_backward(spec, params, cache0, gy, want_dx=True, want_dw=False)
+
+        def wgrad_only():
+            neurons.symbolic_backward(spec, params, cache0, gy, want_dx=False, want_dw=True)
+        for _ in range(3):
+            fwd_only(); dgrad_only(); wgrad_only()
+        torch.cuda.synchronize()
+        per_gemm_set = flops / 3  # fprop / dgrad / wgrad each carry one third
+        for name, fn in (("fprop", fwd_only), ("dgrad", dgrad_only), ("wgrad", wgrad_only)):
+            t = timed(fn, max(5, args.steps))
+            phase[name] = {"ms": sum(t) / len(t), "tflops": per_gemm_set / (sum(t) / len(t) * 1e-3) / 1e12}
+    dom = max(phase, key=lambda k_: phase[k_]["ms"])
+    roof = {"bound": "tensor", "kernel": dom, "achieved": phase[dom]["tflops"], "peak": pk["bf16"],
+            "unit": "TFLOP/s", "frac": phase[dom]["tflops"] / pk["bf16"], "traffic": None,
+            "peak_src": f"{pk['src']} bf16 dense (burst); sustained {pk['bf16_sustained']}",
+            "phases": phase}
+    if dts != "bf16":
+        roof["note"] = "fp32 runs on the CUDA-core (FFMA) path; the bf16 peak is the denominator"
+
+    # ---- end to end through the public API with host buffers ----
+    x_h = x.detach().cpu().pin_memory()
+    g_h = gy.detach().cpu().pin_memory()
+    w_h = {k_: v.detach().cpu().pin_memory() for k_, v in params.items()}
+    dx_h = torch.empty(x.shape, dtype=dt).pin_memory()
+    gr_h = {k_: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k_, v in params.items()}
+
+    def e2e_step():
+        xd = x_h.to(dev, non_blocking=True)
+        gd = g_h.to(dev, non_blocking=True)
+        pd = {k_: v.to(dev, non_blocking=True) for k_, v in w_h.items()}
+        yy, cc = neurons.forward(spec, pd, xd, dtype=dt)
+        grads, dxx = neurons.symbolic_backward(spec, pd, cc, gd)
+        dx_h.copy_(dxx.contiguous() if kind == "fc" else dxx.permute(0, 1, 2, 3).contiguous(),
+                   non_blocking=True)
+        for k_, v in grads.items():
+            gr_h[k_].copy_(v, non_blocking=True)
+    for _ in range(2):
+        e2e_step()
+    torch.cuda.synchronize()
+    e2e_ms = timed(e2e_step, args.steps)
+    e2e_step_ms = sum(e2e_ms) / len(e2e_ms)
+    if world > 1:
+        tt = torch.tensor([e2e_step_ms], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e2e_step_ms = float(tt.item())
+    h2d = x_h.numel() * x_h.element_size() + g_h.numel() * g_h.element_size() + sum(
+        v.numel() * 4 for v in w_h.values())
+    d2h = dx_h.numel() * dx_h.element_size() + sum(v.numel() * 4 for v in gr_h.values())
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    # ---- CPU baseline on rank 0 at N=1, bounded sample ----
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        batch = cpu_batch_for(wl)
+        t_cpu, fl = cpu_sample(wl, batch, 2)
+        cpu = {"value": fl / t_cpu / 1e12, "unit": "TFLOP/s", "cores": os.cpu_count(),
+               "kind": "port",
+               "sample": f"{wl_name} at batch {batch} of {n}, fp64 numpy reference algorithm "
+                         f"(im2col+GEMM+col2im), best of 2, {t_cpu:.2f} s"}
+    out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": dts, "data": "synthetic (seeded N(0,1) x and dy, Kaiming-uniform W, b=0)",
+           "config": config_of(wl, wl_name, world),
+           "roofline": roof, "cpu_baseline": cpu,
+           "e2e": {"value": world * flops / (e2e_step_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
+                   "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": h2d,
+                   "d2h_bytes_per_step": d2h},
+           "gpu_launches": launches, "launches_per_step": launches / args.steps,
+           "clocks": clk.summary(),
+           "path": "tcgen05" if neurons.device_path(spec, x.shape, dt) == 1 else "cuda-core"}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    wl = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, wl, args.workload)
+    return run_ours(args, wl, args.workload)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

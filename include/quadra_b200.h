@@ -1,0 +1,127 @@
+/*
+ * quadra_b200.h -- C ABI of the B200-native quadratic-layer hot path.
+ *
+ * The reference (QuadraLib, /root/reference/pkg/src/quadra) is a pure-Python
+ * numpy library with no FFI; its hot-path interface is the Python pair
+ *
+ *   neurons.forward(spec, params, x) -> (y, LayerCache(x, a, b))
+ *       /root/reference/pkg/src/quadra/neurons.py:235-276
+ *   neurons.symbolic_backward(spec, params, cache, dy) -> ({role: dW}, dx)
+ *       /root/reference/pkg/src/quadra/neurons.py:295-445
+ *
+ * plus the integer helpers validate_spec / param_shapes / conv_out_size
+ * (neurons.py:50-107, tensor.py:279-280). Each entry point below replaces one
+ * of those (cited per function); the Python package
+ * paper_2204_01701_b200.neurons binds them with ctypes and keeps the
+ * reference's Python signatures.
+ *
+ * Conventions: every tensor pointer is DEVICE memory, caller-allocated;
+ * every call is stream-ordered on `stream` with no host synchronisation and
+ * no allocation inside. Activations are NHWC (channels_last; fc = (N, C)) in
+ * the descriptor's dtype; weights and weight/bias gradients are fp32 in the
+ * reference layouts (conv (F, C, r, r); fc (in, out) = (C, F)).
+ */
+#ifndef QUADRA_B200_H
+#define QUADRA_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* family tags: reference neurons.py:40-41 (+ t2_linear) */
+enum {
+  QD_FAM_FIRST_ORDER = 0, /* W x + b                                  */
+  QD_FAM_T2 = 1,          /* Wa (x*x)                                 */
+  QD_FAM_T4 = 2,          /* (Wa x) * (Wb x)                          */
+  QD_FAM_PROPOSED = 3,    /* (Wa x + ba) * (Wb x + bb) + (Wc x + bc)  */
+  QD_FAM_T2_LINEAR = 4    /* Wa (x*x) + Wc x                          */
+};
+enum { QD_KIND_FC = 0, QD_KIND_CONV = 1 };
+enum { QD_F32 = 0, QD_BF16 = 1 };
+
+/* status codes; the Python layer re-raises the reference exception classes
+ * (errors.py:8-38): CONFIG->ConfigError, DIM->DimensionError,
+ * INTEGRITY->IntegrityError, CUDA/UNSUPPORTED/ARG->DeviceError */
+enum {
+  QD_OK = 0,
+  QD_ERR_CONFIG = 1,
+  QD_ERR_DIM = 2,
+  QD_ERR_INTEGRITY = 3,
+  QD_ERR_CUDA = 4,
+  QD_ERR_UNSUPPORTED = 5,
+  QD_ERR_ARG = 6
+};
+
+/* flags */
+#define QD_FLAG_NO_DX 1u      /* backward: skip the input gradient        */
+#define QD_FLAG_FORCE_SIMT 2u /* use the generic CUDA-core kernels even    \
+                                 where a tcgen05 kernel exists (tests)     */
+#define QD_FLAG_NO_DW 4u      /* backward: skip weight and bias gradients  \
+                                 (frozen layers; per-kernel timing)        */
+
+typedef struct {
+  int family, kind, dtype;
+  int N, C, H, W; /* input  (fc: H = W = 1)                            */
+  int F;          /* output channels / features                        */
+  int r, stride, pad;
+  unsigned flags;
+} qd_desc;
+
+/* Replaces validate_spec + _check_x + _check_conv_pre
+ * (neurons.py:50-77, :212-220; tensor.py:334-352) for the device path. */
+int qd_validate(const qd_desc* d);
+
+/* conv_out_size semantics, tensor.py:279-280. */
+int qd_out_shape(const qd_desc* d, int* OH, int* OW);
+
+/* Bytes of the packed-weight buffer and of the scratch workspace one layer
+ * needs (forward and backward share it). */
+size_t qd_pack_bytes(const qd_desc* d);
+size_t qd_workspace_bytes(const qd_desc* d);
+
+/* Cast + re-layout the fp32 reference-layout weights of the branches into
+ * the kernels' packed layouts (fprop [Wa;Wb;Wc] K-major, dgrad flipped).
+ * w[i] are the family's weight roles in order: proposed (Wa, Wb, Wc),
+ * t4 (Wa, Wb), t2 (Wa), first_order (W), t2_linear (Wa, Wc). Unused = NULL.
+ * Replaces the implicit W.reshape(f,-1) of tensor.py:317, :329. */
+int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack,
+                    void* stream);
+
+/* Forward: neurons.forward (neurons.py:235-276).
+ * bias[i]: fp32 (F) per role (proposed ba, bb, bc; first_order b; else NULL).
+ * y: output NHWC; a_cache/b_cache: the LayerCache a, b (proposed/t4, NHWC,
+ * dtype) -- may be NULL when not needed by the family. */
+int qd_forward(const qd_desc* d, const void* x, const void* wpack,
+               const float* const bias[3], void* y, void* a_cache,
+               void* b_cache, void* workspace, void* stream);
+
+/* Backward: neurons.symbolic_backward (neurons.py:295-445).
+ * dW[i]: fp32 reference-layout gradient per weight role (same order as
+ * qd_pack_weights); db[i]: fp32 (F) per bias role; dx NHWC (may be NULL with
+ * QD_FLAG_NO_DX). */
+int qd_backward(const qd_desc* d, const void* x, const void* wpack,
+                const void* a_cache, const void* b_cache, const void* dy,
+                void* dx, float* const dW[3], float* const db[3],
+                void* workspace, void* stream);
+
+/* Which implementation qd_forward / qd_backward will use for d:
+ * 0 = generic CUDA-core (SIMT) kernels, 1 = tcgen05/TMA kernels. */
+int qd_path(const qd_desc* d);
+
+const char* qd_error_string(int status);
+const char* qd_last_error(void); /* detail of the last failure (thread-local) */
+
+/* Number of kernels this library has launched since load (benchmarks report
+ * it as gpu_launches). */
+unsigned long long qd_launch_count(void);
+
+/* Library version string. */
+const char* qd_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QUADRA_B200_H */

@@ -1,0 +1,114 @@
+"""ctypes binding of libquadra_b200.so (the C ABI in include/quadra_b200.h).
+
+The shared library is built in-tree (``python __graft_entry__.py`` or
+``make -C paper_2204_01701_b200/csrc``). There is no fallback: if it is
+missing or cannot be loaded, every device entry point raises DeviceError.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import threading
+
+from .errors import ConfigError, DeviceError, DimensionError, IntegrityError
+
+LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libquadra_b200.so")
+
+FAMILY_CODE = {"first_order": 0, "t2": 1, "t4": 2, "proposed": 3, "t2_linear": 4}
+KIND_CODE = {"fc": 0, "conv": 1}
+F32, BF16 = 0, 1
+
+QD_OK, QD_ERR_CONFIG, QD_ERR_DIM, QD_ERR_INTEGRITY = 0, 1, 2, 3
+QD_ERR_CUDA, QD_ERR_UNSUPPORTED, QD_ERR_ARG = 4, 5, 6
+FLAG_NO_DX, FLAG_FORCE_SIMT, FLAG_NO_DW = 1, 2, 4
+
+EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
+           "qd_pack_weights", "qd_forward", "qd_backward", "qd_path",
+           "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version")
+
+
+class QdDesc(ctypes.Structure):
+    _fields_ = [("family", ctypes.c_int), ("kind", ctypes.c_int), ("dtype", ctypes.c_int),
+                ("N", ctypes.c_int), ("C", ctypes.c_int), ("H", ctypes.c_int),
+                ("W", ctypes.c_int), ("F", ctypes.c_int), ("r", ctypes.c_int),
+                ("stride", ctypes.c_int), ("pad", ctypes.c_int), ("flags", ctypes.c_uint)]
+
+
+_lock = threading.Lock()
+_lib = None
+
+
+def load():
+    """Load (once) and return the ctypes handle; raises DeviceError."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(
+                f"{LIB_PATH} is not built; run `python __graft_entry__.py` (build) first "
+                "-- there is no CPU fallback")
+        try:
+            lib = ctypes.CDLL(LIB_PATH)
+        except OSError as e:  # pragma: no cover - depends on the box
+            raise DeviceError(f"cannot load {LIB_PATH}: {e}") from e
+        P = ctypes.POINTER
+        vp = ctypes.c_void_p
+        fp3 = ctypes.c_void_p * 3
+        lib.qd_validate.argtypes = [P(QdDesc)]
+        lib.qd_validate.restype = ctypes.c_int
+        lib.qd_out_shape.argtypes = [P(QdDesc), P(ctypes.c_int), P(ctypes.c_int)]
+        lib.qd_out_shape.restype = ctypes.c_int
+        lib.qd_pack_bytes.argtypes = [P(QdDesc)]
+        lib.qd_pack_bytes.restype = ctypes.c_size_t
+        lib.qd_workspace_bytes.argtypes = [P(QdDesc)]
+        lib.qd_workspace_bytes.restype = ctypes.c_size_t
+        lib.qd_pack_weights.argtypes = [P(QdDesc), fp3, vp, vp]
+        lib.qd_pack_weights.restype = ctypes.c_int
+        lib.qd_forward.argtypes = [P(QdDesc), vp, vp, fp3, vp, vp, vp, vp, vp]
+        lib.qd_forward.restype = ctypes.c_int
+        lib.qd_backward.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, fp3, fp3, vp, vp]
+        lib.qd_backward.restype = ctypes.c_int
+        lib.qd_path.argtypes = [P(QdDesc)]
+        lib.qd_path.restype = ctypes.c_int
+        lib.qd_error_string.argtypes = [ctypes.c_int]
+        lib.qd_error_string.restype = ctypes.c_char_p
+        lib.qd_last_error.argtypes = []
+        lib.qd_last_error.restype = ctypes.c_char_p
+        lib.qd_launch_count.argtypes = []
+        lib.qd_launch_count.restype = ctypes.c_ulonglong
+        lib.qd_version.argtypes = []
+        lib.qd_version.restype = ctypes.c_char_p
+        _lib = lib
+        return lib
+
+
+def raise_for(status, what=""):
+    """Map a QD status to the reference exception classes."""
+    if status == QD_OK:
+        return
+    lib = load()
+    msg = lib.qd_last_error().decode(errors="replace")
+    if what:
+        msg = f"{what}: {msg}"
+    if status == QD_ERR_CONFIG:
+        raise ConfigError(msg)
+    if status == QD_ERR_DIM:
+        raise DimensionError(msg)
+    if status == QD_ERR_INTEGRITY:
+        raise IntegrityError(msg)
+    raise DeviceError(f"{lib.qd_error_string(status).decode()}: {msg}")
+
+
+def ptr3(*ptrs):
+    arr = (ctypes.c_void_p * 3)()
+    for i, p in enumerate(ptrs[:3]):
+        arr[i] = p if p else None
+    return arr
+
+
+def launch_count():
+    return int(load().qd_launch_count())

@@ -1,0 +1,210 @@
+// C-ABI entry points of libquadra_b200.so (declared in include/quadra_b200.h).
+// Validation mirrors the reference's error conventions; dispatch picks the
+// tcgen05 kernels when the shape tiles onto them and the generic CUDA-core
+// kernels otherwise. There is no host fallback.
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+#include <atomic>
+#include "qd_kernels.h"
+
+namespace qd {
+
+static std::atomic<unsigned long long> g_launches{0};
+static thread_local char g_err[512] = "";
+
+void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+int set_error(int status, const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+  return status;
+}
+
+int check_launch(const char* what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return set_error(QD_ERR_CUDA, "%s: %s", what, cudaGetErrorString(e));
+  return QD_OK;
+}
+
+static size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
+
+Workspace plan_workspace(const Plan& P, int path) {
+  Workspace L;
+  memset(&L, 0, sizeof(L));
+  size_t es = P.dtype == QD_BF16 ? 2 : 4;
+  if (path == 0) {
+    size_t a = (size_t)P.Mout * P.nb * P.F, b = (size_t)P.Min * P.Cd;
+    L.sz_P = (a > b ? a : b) * 4;
+  }
+  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4) L.sz_D = (size_t)P.Mout * P.Jd * es;
+  if (path == 0) {
+    long long tiles = (long long)((P.Jd + 63) / 64) * ((P.Kf + 63) / 64);
+    long long S = (2 * 148 + tiles - 1) / tiles;
+    long long cap = P.Mout / 256;
+    if (cap < 1) cap = 1;
+    if (S > cap) S = cap;
+    if (S < 1) S = 1;
+    L.wg_split = (int)S;
+  } else {
+    L.wg_split = tc_wgrad_split(P);
+  }
+  L.sz_WG = (size_t)L.wg_split * P.Jd * P.Kf * 4;
+  long long bs = (P.Mout + 255) / 256;
+  if (bs > 2 * 148) bs = 2 * 148;
+  if (bs < 1) bs = 1;
+  L.bs_split = (int)bs;
+  L.sz_BS = (size_t)L.bs_split * P.Jd * 4;
+  if (path == 1 && P.sq) L.sz_XS = (size_t)P.Min * P.C * es;
+  size_t off = 0;
+  L.off_P = off; off = align_up(off + L.sz_P);
+  L.off_D = off; off = align_up(off + L.sz_D);
+  L.off_WG = off; off = align_up(off + L.sz_WG);
+  L.off_BS = off; off = align_up(off + L.sz_BS);
+  L.off_XS = off; off = align_up(off + L.sz_XS);
+  L.total = off;
+  return L;
+}
+
+static int validate(const qd_desc* d) {
+  if (!d) return set_error(QD_ERR_ARG, "null descriptor");
+  if (d->family < 0 || d->family > QD_FAM_T2_LINEAR)
+    return set_error(QD_ERR_CONFIG, "unknown family %d", d->family);
+  if (d->kind != QD_KIND_FC && d->kind != QD_KIND_CONV)
+    return set_error(QD_ERR_CONFIG, "unknown layer kind %d", d->kind);
+  if (d->dtype != QD_F32 && d->dtype != QD_BF16)
+    return set_error(QD_ERR_CONFIG, "unknown dtype %d", d->dtype);
+  if (d->C < 1 || d->F < 1)
+    return set_error(QD_ERR_CONFIG, "layer dims must be positive: %d->%d", d->C, d->F);
+  if (d->N < 1 || d->H < 1 || d->W < 1)
+    return set_error(QD_ERR_DIM, "tensor dimensions must be positive, got (%d, %d, %d, %d)", d->N,
+                     d->C, d->H, d->W);
+  if (d->kind == QD_KIND_FC) {
+    if (d->r != 1 || d->stride != 1 || d->pad != 0)
+      return set_error(QD_ERR_CONFIG, "fc layers must use k=1 s=1 p=0");
+    if (d->H != 1 || d->W != 1) return set_error(QD_ERR_DIM, "fc input must be (N, C)");
+  } else {
+    if (d->r < 1 || d->stride < 1 || d->pad < 0)
+      return set_error(QD_ERR_CONFIG, "bad conv geometry k=%d s=%d p=%d", d->r, d->stride, d->pad);
+    if (d->r > d->H + 2 * d->pad || d->r > d->W + 2 * d->pad)
+      return set_error(QD_ERR_DIM, "kernel %d larger than padded input (%d, %d, %d, %d) with pad %d",
+                       d->r, d->N, d->C, d->H, d->W, d->pad);
+  }
+  long long elems = (long long)d->N * d->C * d->H * d->W;
+  if (elems >= (1LL << 40)) return set_error(QD_ERR_DIM, "input too large");
+  return QD_OK;
+}
+
+}  // namespace qd
+
+using namespace qd;
+
+extern "C" {
+
+int qd_validate(const qd_desc* d) { return validate(d); }
+
+int qd_out_shape(const qd_desc* d, int* OH, int* OW) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  if (OH) *OH = P.OH;
+  if (OW) *OW = P.OW;
+  return QD_OK;
+}
+
+size_t qd_pack_bytes(const qd_desc* d) {
+  if (validate(d)) return 0;
+  Plan P = make_plan(*d);
+  size_t es = P.dtype == QD_BF16 ? 2 : 4;
+  return (pack_fprop_elems(P) + pack_dgrad_elems(P)) * es;
+}
+
+int qd_path(const qd_desc* d) {
+  if (validate(d)) return -1;
+  Plan P = make_plan(*d);
+  return tc_supported(P, d->flags) ? 1 : 0;
+}
+
+size_t qd_workspace_bytes(const qd_desc* d) {
+  if (validate(d)) return 0;
+  Plan P = make_plan(*d);
+  return plan_workspace(P, tc_supported(P, d->flags) ? 1 : 0).total;
+}
+
+int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  for (int i = 0; i < P.nroles; ++i)
+    if (!w || !w[i]) return set_error(QD_ERR_ARG, "weight role %d is NULL", i);
+  if (!wpack) return set_error(QD_ERR_ARG, "wpack is NULL");
+  launch_pack(P, w, wpack, (cudaStream_t)stream);
+  return check_launch("pack weights");
+}
+
+int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* const bias[3],
+               void* y, void* a_cache, void* b_cache, void* workspace, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  if (!x || !wpack || !y) return set_error(QD_ERR_ARG, "null tensor pointer");
+  for (int i = 0; i < P.nbias; ++i)
+    if (!bias || !bias[i]) return set_error(QD_ERR_ARG, "bias role %d is NULL", i);
+  bool cache = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  if (cache && (!a_cache || !b_cache))
+    return set_error(QD_ERR_ARG, "family caches a and b: a_cache/b_cache must be given");
+  const float* nob[3] = {nullptr, nullptr, nullptr};
+  const float* const* bs = bias ? bias : nob;
+  int path = tc_supported(P, d->flags) ? 1 : 0;
+  Workspace L = plan_workspace(P, path);
+  if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (path == 1) return tc_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
+  return simt_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
+}
+
+int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* a_cache,
+                const void* b_cache, const void* dy, void* dx, float* const dW[3],
+                float* const db[3], void* workspace, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  if (!x || !wpack || !dy) return set_error(QD_ERR_ARG, "null tensor pointer");
+  bool cache = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  if (cache && (!a_cache || !b_cache))
+    return set_error(QD_ERR_INTEGRITY, "cache for this family must hold a and b");
+  if (!(d->flags & QD_FLAG_NO_DX) && !dx) return set_error(QD_ERR_ARG, "dx is NULL");
+  float* nof[3] = {nullptr, nullptr, nullptr};
+  float* const* w = (dW && !(d->flags & QD_FLAG_NO_DW)) ? dW : nof;
+  float* const* b = (db && !(d->flags & QD_FLAG_NO_DW)) ? db : nof;
+  int path = tc_supported(P, d->flags) ? 1 : 0;
+  Workspace L = plan_workspace(P, path);
+  if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
+  void* dxp = (d->flags & QD_FLAG_NO_DX) ? nullptr : dx;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (path == 1) return tc_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
+  return simt_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
+}
+
+const char* qd_error_string(int status) {
+  switch (status) {
+    case QD_OK: return "ok";
+    case QD_ERR_CONFIG: return "ConfigError";
+    case QD_ERR_DIM: return "DimensionError";
+    case QD_ERR_INTEGRITY: return "IntegrityError";
+    case QD_ERR_CUDA: return "CUDA error";
+    case QD_ERR_UNSUPPORTED: return "unsupported on this device path";
+    case QD_ERR_ARG: return "invalid argument";
+  }
+  return "unknown status";
+}
+
+const char* qd_last_error(void) { return g_err; }
+
+unsigned long long qd_launch_count(void) { return g_launches.load(); }
+
+const char* qd_version(void) { return "quadra_b200 0.1.0 (sm_100a)"; }
+
+}  // extern "C"

@@ -1,0 +1,61 @@
+// Host launchers shared between the translation units of libquadra_b200.so.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+#include "qd_common.cuh"
+
+namespace qd {
+
+// ---- bookkeeping -----------------------------------------------------------
+void count_launch(int n = 1);
+int set_error(int status, const char* fmt, ...);
+int check_launch(const char* what);
+
+// ---- workspace layout ------------------------------------------------------
+struct Workspace {
+  size_t total;
+  size_t off_P, sz_P;      // SIMT fprop / dgrad fp32 GEMM output
+  size_t off_D, sz_D;      // backward operand D (dtype), proposed/t4
+  size_t off_WG, sz_WG;    // wgrad split-K partials (fp32)
+  size_t off_BS, sz_BS;    // bias-sum partials (fp32)
+  size_t off_XS, sz_XS;    // squared input (dtype), t2/t2_linear tcgen05 path
+  int wg_split;            // number of wgrad partials
+  int bs_split;            // number of bias-sum partials
+};
+Workspace plan_workspace(const Plan& P, int path);
+
+// ---- packing (both paths) --------------------------------------------------
+size_t pack_fprop_elems(const Plan& P);
+size_t pack_dgrad_elems(const Plan& P);
+void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st);
+
+// ---- generic CUDA-core path ------------------------------------------------
+int simt_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3],
+                 void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st);
+int simt_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b,
+                  const void* dy, void* dx, float* const dW[3], float* const db[3], char* ws,
+                  const Workspace& L, cudaStream_t st);
+
+// ---- shared backward pieces (elementwise / reductions) ---------------------
+// D = [dy*b | dy*a | dy] (proposed) or [dy*b | dy*a] (t4), plus column-sum
+// partials of D (or of dy) for the bias gradients.
+void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const void* b,
+                         void* D, float* bsum_part, int bs_split, cudaStream_t st);
+void launch_bias_finish(const Plan& P, const float* bsum_part, int bs_split,
+                        float* const db[3], cudaStream_t st);
+// sum the wgrad partials [S][Jd][Kf] and scatter into reference layouts
+void launch_wgrad_finish(const Plan& P, const float* part, int S, float* const dW[3],
+                         cudaStream_t st);
+void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st);
+
+// ---- tcgen05 path ----------------------------------------------------------
+bool tc_supported(const Plan& P, unsigned flags);
+int tc_wgrad_split(const Plan& P);
+int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3],
+               void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st);
+// dW[0] == nullptr skips the weight/bias gradient GEMM (QD_FLAG_NO_DW)
+int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b,
+                const void* dy, void* dx, float* const dW[3], float* const db[3], char* ws,
+                const Workspace& L, cudaStream_t st);
+
+}  // namespace qd

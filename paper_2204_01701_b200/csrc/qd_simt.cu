@@ -1,0 +1,436 @@
+// Generic CUDA-core kernels: weight packing, the elementwise/reduction pieces
+// of the backward pass (shared with the tcgen05 path), and a fully general
+// implicit-GEMM fallback that covers every geometry (any stride/pad/kernel,
+// any channel count, fp32 and bf16). The fallback is the fp32 path (exact
+// FFMA accumulation) and the path for shapes the tcgen05 kernels do not
+// tile; it is never a CPU path.
+//
+// Math follows the reference closed forms (neurons.py:235-276 forward,
+// neurons.py:295-445 backward) with the conv lowered as an implicit GEMM
+// instead of materialising the patch matrix (tensor.py:283-331).
+#include <stdio.h>
+#include "qd_kernels.h"
+
+namespace qd {
+
+// ---------------------------------------------------------------------------
+// packing
+// ---------------------------------------------------------------------------
+size_t pack_fprop_elems(const Plan& P) { return (size_t)P.nb * P.F * P.Kf; }
+size_t pack_dgrad_elems(const Plan& P) { return (size_t)P.Cd * P.Kd; }
+
+template <typename T>
+__global__ void pack_fprop_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
+  const float* w[3] = {w0, w1, w2};
+  long long total = (long long)P.nb * P.F * P.Kf;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int R = (int)(i / P.Kf), k = (int)(i % P.Kf);
+    int grp = P.nb * P.FT;
+    int tile = R / grp, rem = R % grp;
+    int br = rem / P.FT, f = tile * P.FT + rem % P.FT;
+    int role = br, kk = k;
+    if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+    int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
+    float v;
+    if (P.kind == QD_KIND_FC) v = w[role][(size_t)c * P.F + f];
+    else v = w[role][(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+    out[i] = cvt<T>(v);
+  }
+}
+
+// dgrad weights: Wd[c'][e*Jd + j], e = flipped tap (ey,ex) -> (r-1-ey, r-1-ex)
+template <typename T>
+__global__ void pack_dgrad_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
+  const float* w[3] = {w0, w1, w2};
+  long long total = (long long)P.Cd * P.Kd;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int cp = (int)(i / P.Kd), k = (int)(i % P.Kd);
+    int e = k / P.Jd, j = k % P.Jd;
+    int ey = e / P.r, ex = e % P.r, dy = P.r - 1 - ey, dx = P.r - 1 - ex;
+    int role, f, c;
+    if (P.sq == 2) { role = cp / P.C; c = cp % P.C; f = j; }
+    else { role = j / P.F; f = j % P.F; c = cp; }
+    float v;
+    if (P.kind == QD_KIND_FC) v = w[role][(size_t)c * P.F + f];
+    else v = w[role][(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+    out[i] = cvt<T>(v);
+  }
+}
+
+static inline int grid_for(long long n, int bs = 256, int cap = 148 * 16) {
+  long long g = (n + bs - 1) / bs;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return (int)g;
+}
+
+void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
+  long long nf = (long long)pack_fprop_elems(P), nd = (long long)pack_dgrad_elems(P);
+  if (P.dtype == QD_BF16) {
+    bf16* o = (bf16*)wpack;
+    pack_fprop_kernel<bf16><<<grid_for(nf), 256, 0, st>>>(P, w[0], w[1], w[2], o);
+    pack_dgrad_kernel<bf16><<<grid_for(nd), 256, 0, st>>>(P, w[0], w[1], w[2], o + nf);
+  } else {
+    float* o = (float*)wpack;
+    pack_fprop_kernel<float><<<grid_for(nf), 256, 0, st>>>(P, w[0], w[1], w[2], o);
+    pack_dgrad_kernel<float><<<grid_for(nd), 256, 0, st>>>(P, w[0], w[1], w[2], o + nf);
+  }
+  count_launch(2);
+}
+
+// ---------------------------------------------------------------------------
+// generic tiled SIMT GEMM:  out[s][m][n] = sum_{k in split s} A(m,k) * B(n,k)
+// ---------------------------------------------------------------------------
+constexpr int SG_BM = 64, SG_BN = 64, SG_BK = 16;
+
+template <class LA, class LB>
+__global__ void __launch_bounds__(256) simt_gemm_kernel(LA la, LB lb, int M, int N, long long K,
+                                                        long long kper, float* out) {
+  __shared__ float As[SG_BK][SG_BM + 4];
+  __shared__ float Bs[SG_BK][SG_BN + 4];
+  int m0 = blockIdx.x * SG_BM, n0 = blockIdx.y * SG_BN, s = blockIdx.z;
+  long long kb = (long long)s * kper, ke = kb + kper;
+  if (ke > K) ke = K;
+  int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  float acc[4][4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j] = 0.f;
+  for (long long k0 = kb; k0 < ke; k0 += SG_BK) {
+    for (int i = threadIdx.x; i < SG_BM * SG_BK; i += 256) {
+      int mm = i % SG_BM, kk = i / SG_BM;
+      int m = m0 + mm;
+      long long k = k0 + kk;
+      As[kk][mm] = (m < M && k < ke) ? la(m, k) : 0.f;
+    }
+    for (int i = threadIdx.x; i < SG_BN * SG_BK; i += 256) {
+      int nn = i % SG_BN, kk = i / SG_BN;
+      int n = n0 + nn;
+      long long k = k0 + kk;
+      Bs[kk][nn] = (n < N && k < ke) ? lb(n, k) : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < SG_BK; ++kk) {
+      float av[4], bv[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) av[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bv[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], bv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  float* o = out + (size_t)s * M * N;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      int n = n0 + tx * 4 + j;
+      if (n < N) o[(size_t)m * N + n] = acc[i][j];
+    }
+  }
+}
+
+template <class LA, class LB>
+static void simt_gemm(LA la, LB lb, int M, int N, long long K, int split, float* out, cudaStream_t st) {
+  long long kper = (K + split - 1) / split;
+  kper = (kper + SG_BK - 1) / SG_BK * SG_BK;
+  dim3 grid((M + SG_BM - 1) / SG_BM, (N + SG_BN - 1) / SG_BN, split);
+  simt_gemm_kernel<<<grid, 256, 0, st>>>(la, lb, M, N, K, kper, out);
+  count_launch();
+}
+
+// fprop A: implicit im2col of x (optionally squared), m = output pixel
+template <typename T>
+struct FpropA {
+  const T* x; int H, W, C, OH, OW, r, s, p, K0, sq;
+  __device__ float operator()(int m, long long kl) const {
+    int k = (int)kl;
+    int ow = m % OW, t = m / OW, oh = t % OH, n = t / OH;
+    bool square = (sq == 1) || (sq == 2 && k < K0);
+    int kk = k % K0;
+    int tap = kk / C, c = kk % C, dy = tap / r, dx = tap % r;
+    int h = oh * s + dy - p, w = ow * s + dx - p;
+    if (h < 0 || h >= H || w < 0 || w >= W) return 0.f;
+    float v = ld(x + (((size_t)n * H + h) * W + w) * C + c);
+    return square ? v * v : v;
+  }
+};
+// fprop B: GEMM column n = br*F + f -> packed row
+template <typename T>
+struct FpropB {
+  const T* wf; int F, nb, FT, Kf;
+  __device__ float operator()(int n, long long k) const {
+    int br = n / F, f = n % F;
+    return ld(wf + (size_t)fprop_row(br, f, nb, FT) * Kf + k);
+  }
+};
+// dgrad A: transposed-conv gather of D, m = input pixel, k = (e, j)
+template <typename T>
+struct DgradA {
+  const T* D; int H, W, OH, OW, r, s, p, Jd;
+  __device__ float operator()(int m, long long kl) const {
+    int k = (int)kl;
+    int w = m % W, t = m / W, h = t % H, n = t / H;
+    int e = k / Jd, j = k % Jd;
+    int dy = r - 1 - e / r, dx = r - 1 - e % r;
+    int th = h + p - dy, tw = w + p - dx;
+    if (th < 0 || tw < 0 || th % s || tw % s) return 0.f;
+    int oh = th / s, ow = tw / s;
+    if (oh >= OH || ow >= OW) return 0.f;
+    return ld(D + (((size_t)n * OH + oh) * OW + ow) * Jd + j);
+  }
+};
+template <typename T>
+struct RowMajorB {  // B(n, k) = w[n*K + k]
+  const T* w; long long K;
+  __device__ float operator()(int n, long long k) const { return ld(w + (size_t)n * K + k); }
+};
+// wgrad A: A(j, pixel) = D[pixel][j]
+template <typename T>
+struct WgradA {
+  const T* D; int Jd;
+  __device__ float operator()(int j, long long q) const { return ld(D + (size_t)q * Jd + j); }
+};
+// wgrad B: B(kw, pixel) = im2col(x or x*x)[pixel][kw]
+template <typename T>
+struct WgradB {
+  FpropA<T> a;
+  __device__ float operator()(int kw, long long q) const { return a((int)q, kw); }
+};
+
+// ---------------------------------------------------------------------------
+// elementwise / reduction pieces
+// ---------------------------------------------------------------------------
+template <typename T>
+__global__ void fwd_epilogue_kernel(Plan P, const float* G, const float* b0, const float* b1,
+                                    const float* b2, T* y, T* a, T* b) {
+  long long total = P.Mout * P.F;
+  int NG = P.nb * P.F;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long m = i / P.F;
+    int f = (int)(i % P.F);
+    const float* g = G + m * NG;
+    float out;
+    if (P.family == QD_FAM_PROPOSED) {
+      float av = g[f] + b0[f], bv = g[P.F + f] + b1[f];
+      out = av * bv + (g[2 * P.F + f] + b2[f]);
+      a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
+    } else if (P.family == QD_FAM_T4) {
+      float av = g[f], bv = g[P.F + f];
+      out = av * bv;
+      a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
+    } else if (P.family == QD_FAM_FIRST_ORDER) {
+      out = g[f] + b0[f];
+    } else {
+      out = g[f];
+    }
+    y[i] = cvt<T>(out);
+  }
+}
+
+// D = [dy*b | dy*a | dy] / [dy*b | dy*a]; column partial sums of D (fp32 products)
+// or of dy (t2 / t2_linear / first_order) for the bias gradients.
+template <typename T>
+__global__ void bwd_prologue_kernel(Plan P, const T* dy, const T* a, const T* b, T* D,
+                                    float* part, long long rows_per) {
+  int s = blockIdx.x;
+  long long r0 = (long long)s * rows_per, r1 = r0 + rows_per;
+  if (r1 > P.Mout) r1 = P.Mout;
+  bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  int F = P.F;
+  for (int f = threadIdx.x; f < F; f += blockDim.x) {
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    for (long long m = r0; m < r1; ++m) {
+      size_t i = (size_t)m * F + f;
+      float g = ld(dy + i);
+      if (mat) {
+        float av = ld(a + i), bv = ld(b + i);
+        float d0 = g * bv, d1 = g * av;
+        T* drow = D + (size_t)m * P.Jd;
+        drow[f] = cvt<T>(d0);
+        drow[F + f] = cvt<T>(d1);
+        if (P.family == QD_FAM_PROPOSED) drow[2 * F + f] = cvt<T>(g);
+        s0 += d0; s1 += d1; s2 += g;
+      } else {
+        s0 += g;
+      }
+    }
+    float* o = part + (size_t)s * P.Jd;
+    if (P.family == QD_FAM_PROPOSED) { o[f] = s0; o[F + f] = s1; o[2 * F + f] = s2; }
+    else if (P.family == QD_FAM_T4) { o[f] = s0; o[F + f] = s1; }
+    else o[f] = s0;
+  }
+}
+
+void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const void* b, void* D,
+                         float* part, int split, cudaStream_t st) {
+  long long rows_per = (P.Mout + split - 1) / split;
+  int threads = P.F >= 256 ? 256 : ((P.F + 31) / 32) * 32;
+  if (P.dtype == QD_BF16)
+    bwd_prologue_kernel<bf16><<<split, threads, 0, st>>>(P, (const bf16*)dy, (const bf16*)a,
+                                                         (const bf16*)b, (bf16*)D, part, rows_per);
+  else
+    bwd_prologue_kernel<float><<<split, threads, 0, st>>>(P, (const float*)dy, (const float*)a,
+                                                          (const float*)b, (float*)D, part, rows_per);
+  count_launch();
+}
+
+// bias gradient per role: proposed ba <- sum(dy*b) (block 0), bb <- sum(dy*a)
+// (block 1), bc <- sum(dy) (block 2); first_order b <- sum(dy). Fixed-order sum.
+__global__ void bias_finish_kernel(Plan P, const float* part, int S, float* d0, float* d1, float* d2) {
+  int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= P.Jd) return;
+  float acc = 0.f;
+  for (int s = 0; s < S; ++s) acc += part[(size_t)s * P.Jd + j];
+  int role = j / P.F, f = j % P.F;
+  float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
+  if (dst) dst[f] = acc;
+}
+
+void launch_bias_finish(const Plan& P, const float* part, int S, float* const db[3], cudaStream_t st) {
+  if (P.nbias == 0) return;
+  bias_finish_kernel<<<(P.Jd + 127) / 128, 128, 0, st>>>(P, part, S, db[0], db[1], db[2]);
+  count_launch();
+}
+
+// wgrad partials [S][Jd][Kf] -> reference layouts
+__global__ void wgrad_finish_kernel(Plan P, const float* part, int S, float* w0, float* w1, float* w2) {
+  long long total = (long long)P.Jd * P.Kf;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    int j = (int)(i / P.Kf), k = (int)(i % P.Kf);
+    float acc = 0.f;
+    for (int s = 0; s < S; ++s) acc += part[(size_t)s * total + i];
+    int role, f = j % P.F, kk = k;
+    if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+    else role = j / P.F;
+    int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
+    float* dst = role == 0 ? w0 : (role == 1 ? w1 : w2);
+    if (!dst) continue;
+    if (P.kind == QD_KIND_FC) dst[(size_t)c * P.F + f] = acc;
+    else dst[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx] = acc;
+  }
+}
+
+void launch_wgrad_finish(const Plan& P, const float* part, int S, float* const dW[3], cudaStream_t st) {
+  long long total = (long long)P.Jd * P.Kf;
+  wgrad_finish_kernel<<<grid_for(total), 256, 0, st>>>(P, part, S, dW[0], dW[1], dW[2]);
+  count_launch();
+}
+
+template <typename T>
+__global__ void square_kernel(const T* x, T* xs, long long n) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float v = ld(x + i);
+    xs[i] = cvt<T>(v * v);
+  }
+}
+
+void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st) {
+  long long n = P.Min * P.C;
+  if (P.dtype == QD_BF16) square_kernel<bf16><<<grid_for(n), 256, 0, st>>>((const bf16*)x, (bf16*)xs, n);
+  else square_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)x, (float*)xs, n);
+  count_launch();
+}
+
+// dgrad epilogue: dx = Q (first_order/t4/proposed), 2 x Q (t2),
+// 2 x Q[:, :C] + Q[:, C:] (t2_linear)  -- neurons.py:400-405 "t = ds*x; dx = t + t"
+template <typename T>
+__global__ void dgrad_epilogue_kernel(Plan P, const float* Q, const T* x, T* dx) {
+  long long total = P.Min * P.C;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    long long m = i / P.C;
+    int c = (int)(i % P.C);
+    float v;
+    if (P.sq == 0) v = Q[i];
+    else {
+      float t = Q[m * P.Cd + c] * ld(x + i);
+      v = t + t;
+      if (P.sq == 2) v += Q[m * P.Cd + P.C + c];
+    }
+    dx[i] = cvt<T>(v);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// full SIMT forward / backward
+// ---------------------------------------------------------------------------
+template <typename T>
+static int simt_forward_t(const Plan& P, const T* x, const T* wf, const float* const bias[3], T* y,
+                          T* a, T* b, char* ws, const Workspace& L, cudaStream_t st) {
+  float* G = (float*)(ws + L.off_P);
+  FpropA<T> la{x, P.H, P.W, P.C, P.OH, P.OW, P.r, P.s, P.p, P.K0, P.sq};
+  FpropB<T> lb{wf, P.F, P.nb, P.FT, P.Kf};
+  simt_gemm(la, lb, (int)P.Mout, P.nb * P.F, P.Kf, 1, G, st);
+  long long total = P.Mout * P.F;
+  fwd_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, G, bias[0], bias[1], bias[2], y, a, b);
+  count_launch();
+  return check_launch("simt forward");
+}
+
+int simt_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3],
+                 void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st) {
+  if (P.dtype == QD_BF16)
+    return simt_forward_t<bf16>(P, (const bf16*)x, (const bf16*)wpack, bias, (bf16*)y, (bf16*)a,
+                                (bf16*)b, ws, L, st);
+  return simt_forward_t<float>(P, (const float*)x, (const float*)wpack, bias, (float*)y, (float*)a,
+                               (float*)b, ws, L, st);
+}
+
+template <typename T>
+static int simt_backward_t(const Plan& P, const T* x, const T* wpack, const T* a, const T* b,
+                           const T* dy, T* dx, float* const dW[3], float* const db[3], char* ws,
+                           const Workspace& L, cudaStream_t st, bool want_dx) {
+  const T* wd = wpack + pack_fprop_elems(P);
+  float* bpart = (float*)(ws + L.off_BS);
+  const T* D = dy;
+  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4) D = (const T*)(ws + L.off_D);
+  launch_bwd_prologue(P, dy, a, b, (void*)D, bpart, L.bs_split, st);
+  if (db[0]) launch_bias_finish(P, bpart, L.bs_split, db, st);
+  if (dW[0]) {
+    // wgrad: [Jd][Kf] = D^T * im2col(x | x*x), split over pixels
+    float* part = (float*)(ws + L.off_WG);
+    WgradA<T> wa{D, P.Jd};
+    WgradB<T> wb{FpropA<T>{x, P.H, P.W, P.C, P.OH, P.OW, P.r, P.s, P.p, P.K0, P.sq}};
+    simt_gemm(wa, wb, P.Jd, P.Kf, P.Mout, L.wg_split, part, st);
+    launch_wgrad_finish(P, part, L.wg_split, dW, st);
+  }
+  if (want_dx) {
+    float* Q = (float*)(ws + L.off_P);
+    DgradA<T> da{D, P.H, P.W, P.OH, P.OW, P.r, P.s, P.p, P.Jd};
+    RowMajorB<T> dbm{wd, P.Kd};
+    simt_gemm(da, dbm, (int)P.Min, P.Cd, P.Kd, 1, Q, st);
+    long long total = P.Min * P.C;
+    dgrad_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, Q, x, dx);
+    count_launch();
+  }
+  return check_launch("simt backward");
+}
+
+int simt_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b,
+                  const void* dy, void* dx, float* const dW[3], float* const db[3], char* ws,
+                  const Workspace& L, cudaStream_t st) {
+  bool want_dx = dx != nullptr;
+  if (P.dtype == QD_BF16)
+    return simt_backward_t<bf16>(P, (const bf16*)x, (const bf16*)wpack, (const bf16*)a,
+                                 (const bf16*)b, (const bf16*)dy, (bf16*)dx, dW, db, ws, L, st,
+                                 want_dx);
+  return simt_backward_t<float>(P, (const float*)x, (const float*)wpack, (const float*)a,
+                                (const float*)b, (const float*)dy, (float*)dx, dW, db, ws, L, st,
+                                want_dx);
+}
+
+}  // namespace qd

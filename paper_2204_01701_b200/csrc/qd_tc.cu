@@ -1,0 +1,822 @@
+// tcgen05 / TMEM / TMA kernels for the quadratic conv (and fc as a 1x1 conv
+// over an N x 1 x 1 grid), bf16 operands, fp32 accumulation in TMEM.
+//
+//  K1  conv_gemm<EPI_PROPOSED|EPI_T4|EPI_PLAIN>  fprop: one implicit GEMM over
+//      the branch-interleaved [Wa;Wb;Wc] weights; A tiles are 4-D TMA boxes of
+//      the NHWC activations shifted per filter tap (OOB zero fill = padding);
+//      the a*b + c + bias epilogue runs on the TMEM accumulator in registers
+//      and the y / a / b tiles leave through TMA stores. The raw Wa.x, Wb.x,
+//      Wc.x and a*b never reach HBM (neurons.py:268-274).
+//  K3  conv_gemm<EPI_PLAIN|EPI_SQ>  stride-1 dgrad: the same kernel run as a
+//      conv of D = [dy*b | dy*a | dy] with the flipped packed weights, so
+//      dX = Wa^T(dy*b) + Wb^T(dy*a) + Wc^T dy is ONE GEMM with K = r*r*3F
+//      (neurons.py:433-444); t2's "t = ds*x; dx = t + t" (:400-405) is the
+//      EPI_SQ epilogue.
+//  K4  wgrad: dW^T tiles = im2col(x)^T . D with both operands MN-major
+//      straight from TMA boxes, split over pixels into fp32 partials that a
+//      fixed-order reduce folds into the reference layouts (deterministic).
+//
+// Warp roles (256 threads): w0 TMA producer, w1 MMA issuer (one lane),
+// w2 TMEM allocator, w4-7 epilogue (TMEM lane quarter = warp % 4).
+// Persistent over output tiles, TMEM accumulators double-buffered so the
+// epilogue of tile i overlaps the main loop of tile i+1.
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <string.h>
+#include "qd_kernels.h"
+#include "qd_ptx.cuh"
+
+namespace qd {
+
+enum { EPI_PROPOSED = 0, EPI_T4 = 1, EPI_PLAIN = 2, EPI_SQ = 3 };
+
+struct ConvArgs {
+  int tiles_w, tiles_h, tiles_nn, total_tiles;
+  int Wb, Hb, Nb, box_rows;
+  int OHg, OWg, Ng;         // output grid (epilogue validity)
+  int r, pad_eff, cblks;    // taps, shift, 64-channel blocks of the A tensor
+  int kb_half, dual;        // k-blocks per A map; dual = second half from map A1 (t2_linear)
+  int b_rs_tile, b_rs_blk;  // B row offset per N tile / per 64-row block
+  int out_c_tile;           // output channel offset per N tile
+  int Cout;                 // channels of the output tensor (and of x for EPI_SQ)
+  const float* bias0;
+  const float* bias1;
+  const float* bias2;
+  const bf16* xres;         // x (NHWC) for EPI_SQ
+};
+
+template <int EPI, int NB>
+struct ConvCfg {
+  static constexpr int A_BYTES = 128 * 128;
+  static constexpr int B_BYTES = NB * 64 * 128;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int NOUT = (EPI == EPI_PROPOSED || EPI == EPI_T4) ? 3 : (EPI == EPI_PLAIN ? NB : 1);
+  static constexpr int STG = NOUT * 128 * 128;
+  static constexpr int BUDGET = 220 * 1024;
+  static constexpr int S0 = (BUDGET - STG - 1024) / STAGE;
+  static constexpr int STAGES = S0 > 6 ? 6 : S0;
+  static constexpr int SMEM = 1024 /*align slack*/ + STAGES * STAGE + STG + 1024 /*barriers*/;
+  static constexpr int ACC_COLS = NB * 64;
+};
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+
+// write 16 fp32 values (channels 16j..16j+15 of a 64-channel row) as bf16 into a
+// SWIZZLE_128B staging tile: 16-B chunk q of row `row` lives at chunk q ^ (row & 7)
+__device__ __forceinline__ void stage_store16(uint8_t* tile, int row, int j, const float* v) {
+  uint4 lo, hi;
+  lo.x = pack_bf16x2(v[0], v[1]);   lo.y = pack_bf16x2(v[2], v[3]);
+  lo.z = pack_bf16x2(v[4], v[5]);   lo.w = pack_bf16x2(v[6], v[7]);
+  hi.x = pack_bf16x2(v[8], v[9]);   hi.y = pack_bf16x2(v[10], v[11]);
+  hi.z = pack_bf16x2(v[12], v[13]); hi.w = pack_bf16x2(v[14], v[15]);
+  uint8_t* rowp = tile + row * 128;
+  int q0 = 2 * j, q1 = 2 * j + 1;
+  *reinterpret_cast<uint4*>(rowp + ((q0 ^ (row & 7)) << 4)) = lo;
+  *reinterpret_cast<uint4*>(rowp + ((q1 ^ (row & 7)) << 4)) = hi;
+}
+
+template <int EPI, int NB>
+__global__ void __launch_bounds__(256, 1)
+    conv_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
+                     const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapO0,
+                     const __grid_constant__ CUtensorMap mapO1, const __grid_constant__ CUtensorMap mapO2,
+                     const ConvArgs args) {
+  using Cfg = ConvCfg<EPI, NB>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint8_t* sOut = sB + STAGES * Cfg::B_BYTES;
+  uint64_t* full = (uint64_t*)(sOut + Cfg::STG);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&mapA0);
+    ptx::prefetch_tmap(&mapA1);
+    ptx::prefetch_tmap(&mapB);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 4);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(tmem_slot, 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  const int KB = args.kb_half * (args.dual ? 2 : 1);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // ===== TMA producer =====
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t bytes = (uint32_t)(args.box_rows * 128 + Cfg::B_BYTES);
+      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+        int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
+        int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
+        int tn = mt / (args.tiles_w * args.tiles_h);
+        int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
+        for (int kb = 0; kb < KB; ++kb) {
+          ptx::mbar_wait(&empty[stage], phase ^ 1);
+          ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+          int half = kb / args.kb_half, kk = kb % args.kb_half;
+          int tap = kk / args.cblks, cb = kk % args.cblks;
+          int ey = tap / args.r, ex = tap % args.r;
+          const CUtensorMap* ma = half ? &mapA1 : &mapA0;
+          ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, w0 + ex - args.pad_eff,
+                           h0 + ey - args.pad_eff, n0);
+#pragma unroll
+          for (int i = 0; i < NB; ++i)
+            ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, kb * 64,
+                             ntile * args.b_rs_tile + i * args.b_rs_blk);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ===== MMA issuer =====
+      constexpr uint32_t IDESC = ptx::idesc_bf16(128, NB * 64, false, false);
+      int stage = 0;
+      uint32_t phase = 0;
+      int it = 0;
+      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+        int as = it & 1;
+        uint32_t aph = (it >> 1) & 1;
+        ptx::mbar_wait(&tempty[as], aph ^ 1);
+        ptx::tc_fence_after();
+        uint32_t d_tmem = tmem_base + as * Cfg::ACC_COLS;
+        for (int kb = 0; kb < KB; ++kb) {
+          ptx::mbar_wait(&full[stage], phase);
+          ptx::tc_fence_after();
+          uint32_t a0 = ptx::smem_u32(sA + stage * Cfg::A_BYTES);
+          uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint64_t ad = ptx::sw128_desc(a0 + k * 32, 16, 1024);
+            uint64_t bd = ptx::sw128_desc(b0 + k * 32, 16, 1024);
+            ptx::mma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+          }
+          ptx::mma_commit(&empty[stage]);
+          if (++stage == STAGES) { stage = 0; phase ^= 1; }
+        }
+        ptx::mma_commit(&tfull[as]);
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue =====
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int etid = threadIdx.x - 128;
+    int it = 0;
+    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+      int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
+      int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
+      int tn = mt / (args.tiles_w * args.tiles_h);
+      int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
+      int as = it & 1;
+      uint32_t aph = (it >> 1) & 1;
+      // previous tile's TMA stores must have finished reading the staging tiles
+      if (etid == 0) ptx::bulk_wait_read0();
+      ptx::named_bar_sync(1, 128);
+      ptx::mbar_wait(&tfull[as], aph);
+      ptx::tc_fence_after();
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::ACC_COLS;
+      const int c_base = ntile * args.out_c_tile;
+      // pixel of this row (for EPI_SQ's x operand)
+      bool valid = false;
+      size_t pix = 0;
+      if (EPI == EPI_SQ) {
+        int ww = row % args.Wb, hh = (row / args.Wb) % args.Hb, nn = row / (args.Wb * args.Hb);
+        int n = n0 + nn, h = h0 + hh, w = w0 + ww;
+        valid = row < args.box_rows && n < args.Ng && h < args.OHg && w < args.OWg;
+        pix = ((size_t)n * args.OHg + h) * args.OWg + w;
+      }
+#pragma unroll 1
+      for (int j = 0; j < 4; ++j) {
+        float v[NB][16];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) ptx::tmem_ld16(tbase + i * 64 + j * 16, v[i]);
+        ptx::tmem_wait_ld();
+        if (EPI == EPI_PROPOSED || EPI == EPI_T4) {
+          float y[16], a[16], b[16];
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            int c = c_base + j * 16 + e;
+            if (EPI == EPI_PROPOSED) {
+              a[e] = v[0][e] + __ldg(args.bias0 + c);
+              b[e] = v[1][e] + __ldg(args.bias1 + c);
+              y[e] = fmaf(a[e], b[e], v[2 % NB][e] + __ldg(args.bias2 + c));
+            } else {
+              a[e] = v[0][e];
+              b[e] = v[1 % NB][e];
+              y[e] = a[e] * b[e];
+            }
+          }
+          stage_store16(sOut, row, j, y);
+          stage_store16(sOut + 16384, row, j, a);
+          stage_store16(sOut + 32768, row, j, b);
+        } else if (EPI == EPI_PLAIN) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) {
+            if (args.bias0) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) v[i][e] += __ldg(args.bias0 + c_base + i * 64 + j * 16 + e);
+            }
+            stage_store16(sOut + i * 16384, row, j, v[i]);
+          }
+        } else {  // EPI_SQ: dx = 2 x acc0 (+ acc1)
+          float o[16];
+          float xv[16];
+          if (valid) {
+            const uint4* xp = reinterpret_cast<const uint4*>(args.xres + pix * args.Cout + c_base + j * 16);
+            uint4 u0 = __ldg(xp), u1 = __ldg(xp + 1);
+            const __nv_bfloat162* h0p = reinterpret_cast<const __nv_bfloat162*>(&u0);
+            const __nv_bfloat162* h1p = reinterpret_cast<const __nv_bfloat162*>(&u1);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              float2 f0 = __bfloat1622float2(h0p[e]);
+              float2 f1 = __bfloat1622float2(h1p[e]);
+              xv[2 * e] = f0.x; xv[2 * e + 1] = f0.y;
+              xv[8 + 2 * e] = f1.x; xv[8 + 2 * e + 1] = f1.y;
+            }
+          } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) xv[e] = 0.f;
+          }
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            float tt = v[0][e] * xv[e];
+            o[e] = tt + tt;
+            if (NB == 2) o[e] += v[NB - 1][e];
+          }
+          stage_store16(sOut, row, j, o);
+        }
+      }
+      // accumulator drained: hand it back to the MMA warp
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+      ptx::fence_proxy_async_smem();
+      ptx::named_bar_sync(1, 128);
+      if (etid == 0) {
+        if (EPI == EPI_PROPOSED || EPI == EPI_T4) {
+          ptx::tma_store_4d(&mapO0, sOut, c_base, w0, h0, n0);
+          ptx::tma_store_4d(&mapO1, sOut + 16384, c_base, w0, h0, n0);
+          ptx::tma_store_4d(&mapO2, sOut + 32768, c_base, w0, h0, n0);
+        } else if (EPI == EPI_PLAIN) {
+#pragma unroll
+          for (int i = 0; i < NB; ++i) ptx::tma_store_4d(&mapO0, sOut + i * 16384, c_base + i * 64, w0, h0, n0);
+        } else {
+          ptx::tma_store_4d(&mapO0, sOut, c_base, w0, h0, n0);
+        }
+        ptx::bulk_commit();
+      }
+    }
+    if (etid == 0) ptx::bulk_wait0();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4 wgrad
+// ---------------------------------------------------------------------------
+struct WgArgs {
+  int mtiles, ntiles, splits;
+  int pb_w, pb_h, pb_n;                 // pixel box (product 64)
+  int pt_w, pt_h, ptiles;               // pixel tiles along w, h; total
+  int r, pad, cblks, kb_half, nkb;      // 64-row k-block decode
+  int Jd, Kf;
+  float* part;                          // [splits][Jd][Kf]
+};
+
+template <int NBLK>
+struct WgCfg {
+  static constexpr int A_BYTES = 2 * 8192;
+  static constexpr int B_BYTES = NBLK * 8192;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int S0 = (220 * 1024 - 2048) / STAGE;
+  static constexpr int STAGES = S0 > 8 ? 8 : S0;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 1024;
+  static constexpr int TCOLS = NBLK * 64 <= 32 ? 32 : (NBLK * 64 <= 64 ? 64 : (NBLK * 64 <= 128 ? 128 : 256));
+};
+
+template <int NBLK>
+__global__ void __launch_bounds__(256, 1)
+    wgrad_kernel(const __grid_constant__ CUtensorMap mapX0, const __grid_constant__ CUtensorMap mapX1,
+                 const __grid_constant__ CUtensorMap mapD, const WgArgs args) {
+  using Cfg = WgCfg<NBLK>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = (uint64_t*)(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int b = blockIdx.x;
+  const int ntile = b % args.ntiles;
+  b /= args.ntiles;
+  const int mtile = b % args.mtiles;
+  const int split = b / args.mtiles;
+  const int p_beg = (int)((long long)split * args.ptiles / args.splits);
+  const int p_end = (int)((long long)(split + 1) * args.ptiles / args.splits);
+  const int nA = (2 * mtile + 1 < args.nkb) ? 2 : 1;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&mapX0);
+    ptx::prefetch_tmap(&mapX1);
+    ptx::prefetch_tmap(&mapD);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(tmem_slot, Cfg::TCOLS);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t bytes = (uint32_t)(nA * 8192 + Cfg::B_BYTES);
+      for (int pt = p_beg; pt < p_end; ++pt) {
+        int tw = pt % args.pt_w, th = (pt / args.pt_w) % args.pt_h, tn = pt / (args.pt_w * args.pt_h);
+        int w0 = tw * args.pb_w, h0 = th * args.pb_h, n0 = tn * args.pb_n;
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+        for (int a = 0; a < nA; ++a) {
+          int kb = 2 * mtile + a;
+          int half = kb / args.kb_half, kk = kb % args.kb_half;
+          int tap = kk / args.cblks, cb = kk % args.cblks;
+          int ey = tap / args.r, ex = tap % args.r;
+          ptx::tma_load_4d(half ? &mapX1 : &mapX0, &full[stage], sA + stage * Cfg::A_BYTES + a * 8192, cb * 64,
+                           w0 + ex - args.pad, h0 + ey - args.pad, n0);
+        }
+#pragma unroll
+        for (int i = 0; i < NBLK; ++i)
+          ptx::tma_load_4d(&mapD, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192,
+                           (ntile * NBLK + i) * 64, w0, h0, n0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16(128, NBLK * 64, true, true);
+      int stage = 0;
+      uint32_t phase = 0;
+      bool first = true;
+      for (int pt = p_beg; pt < p_end; ++pt) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        uint32_t a0 = ptx::smem_u32(sA + stage * Cfg::A_BYTES);
+        uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::B_BYTES);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          // 16 pixels (K) per MMA = two 8-row groups of 128 B
+          uint64_t ad = ptx::sw128_desc(a0 + k * 2048, 8192, 1024);
+          uint64_t bd = ptx::sw128_desc(b0 + k * 2048, 8192, 1024);
+          ptx::mma_bf16(tmem_base, ad, bd, IDESC, (first && k == 0) ? 0u : 1u);
+        }
+        first = false;
+        ptx::mma_commit(&empty[stage]);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      ptx::mma_commit(done);
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int kglob = mtile * 128 + row;
+    const bool has_work = p_end > p_beg;
+    if (has_work) {
+      ptx::mbar_wait(done, 0);
+      ptx::tc_fence_after();
+    }
+    const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16);
+    float* dst = args.part + (size_t)split * args.Jd * args.Kf;
+#pragma unroll 1
+    for (int c = 0; c < NBLK * 64; c += 16) {
+      float v[16];
+      if (has_work) {
+        ptx::tmem_ld16(tbase + c, v);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+      }
+      if (kglob < args.Kf && row < nA * 64) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          int j = ntile * NBLK * 64 + c + e;
+          dst[(size_t)j * args.Kf + kglob] = v[e];
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, Cfg::TCOLS);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// vectorised backward prologue for the tcgen05 path:
+// D = [dy*b | dy*a | dy] (proposed) / [dy*b | dy*a] (t4) in bf16 plus
+// fixed-order column partial sums (bias gradients) of the fp32 products.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf16* __restrict__ dy,
+                                                               const bf16* __restrict__ a,
+                                                               const bf16* __restrict__ b, bf16* __restrict__ D,
+                                                               float* __restrict__ part, long long rows_per) {
+  const int F = P.F, chunks = F / 8;
+  const int lanes = 256 / chunks;  // rows processed concurrently
+  const int ch = threadIdx.x % chunks, rl = threadIdx.x / chunks;
+  const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  const bool prop = P.family == QD_FAM_PROPOSED;
+  long long r0 = (long long)blockIdx.x * rows_per, r1 = r0 + rows_per;
+  if (r1 > P.Mout) r1 = P.Mout;
+  float s0[8], s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s0[e] = s1[e] = s2[e] = 0.f;
+  if (rl < lanes) {
+    for (long long m = r0 + rl; m < r1; m += lanes) {
+      size_t off = (size_t)m * F + ch * 8;
+      uint4 gu = __ldg(reinterpret_cast<const uint4*>(dy + off));
+      const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
+      if (mat) {
+        uint4 au = __ldg(reinterpret_cast<const uint4*>(a + off));
+        uint4 bu = __ldg(reinterpret_cast<const uint4*>(b + off));
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&au);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bu);
+        uint4 d0, d1;
+        uint32_t* d0p = reinterpret_cast<uint32_t*>(&d0);
+        uint32_t* d1p = reinterpret_cast<uint32_t*>(&d1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 g = __bfloat1622float2(g2[e]), av = __bfloat1622float2(a2[e]), bv = __bfloat1622float2(b2[e]);
+          float x0 = g.x * bv.x, x1 = g.y * bv.y, y0 = g.x * av.x, y1 = g.y * av.y;
+          d0p[e] = pack_bf16x2(x0, x1);
+          d1p[e] = pack_bf16x2(y0, y1);
+          s0[2 * e] += x0; s0[2 * e + 1] += x1;
+          s1[2 * e] += y0; s1[2 * e + 1] += y1;
+          s2[2 * e] += g.x; s2[2 * e + 1] += g.y;
+        }
+        bf16* drow = D + (size_t)m * P.Jd + ch * 8;
+        *reinterpret_cast<uint4*>(drow) = d0;
+        *reinterpret_cast<uint4*>(drow + F) = d1;
+        if (prop) *reinterpret_cast<uint4*>(drow + 2 * F) = gu;
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 g = __bfloat1622float2(g2[e]);
+          s0[2 * e] += g.x; s0[2 * e + 1] += g.y;
+        }
+      }
+    }
+  }
+  // reduce over the row lanes of this block in a fixed order
+  __shared__ float red[256][9];
+  const int nsum = mat ? (prop ? 3 : 2) : 1;
+  for (int sidx = 0; sidx < nsum; ++sidx) {
+    float* src = sidx == 0 ? s0 : (sidx == 1 ? s1 : s2);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[threadIdx.x][e] = src[e];
+    __syncthreads();
+    for (int tcol = threadIdx.x; tcol < chunks * 8; tcol += 256) {
+      int c = tcol / 8, e = tcol % 8;
+      float acc = 0.f;
+      for (int l = 0; l < lanes; ++l) acc += red[l * chunks + c][e];
+      int jcol = sidx * F + c * 8 + e;
+      // proposed/t4: block 0 = sum(dy*b), 1 = sum(dy*a), 2 = sum(dy); else block 0 = sum(dy)
+      part[(size_t)blockIdx.x * P.Jd + jcol] = acc;
+    }
+    __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+static int g_num_sms = 0;
+static int g_arch_ok = -1;
+
+static bool init_driver() {
+  if (g_arch_ok >= 0) return g_arch_ok == 1;
+  int dev = 0;
+  cudaDeviceProp prop;
+  g_arch_ok = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) { cudaGetLastError(); return false; }
+  if (cudaGetDeviceProperties(&prop, dev) != cudaSuccess) { cudaGetLastError(); return false; }
+  g_num_sms = prop.multiProcessorCount;
+  if (prop.major != 10) return false;
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess || !fn) {
+    cudaGetLastError();
+    return false;
+  }
+  g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  g_arch_ok = 1;
+  return true;
+}
+
+bool tc_supported(const Plan& P, unsigned flags) {
+  if (flags & QD_FLAG_FORCE_SIMT) return false;
+  if (P.dtype != QD_BF16) return false;
+  if (P.C % 64 || P.F % 64) return false;
+  if (P.s != 1) return false;
+  if (P.OH < 1 || P.OW < 1) return false;
+  return init_driver();
+}
+
+static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint32_t* box) {
+  cuuint64_t strides[4];
+  cuuint64_t acc = dims[0] * 2;
+  for (int i = 1; i < rank; ++i) {
+    strides[i - 1] = acc;
+    acc *= dims[i];
+  }
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(QD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+  return QD_OK;
+}
+
+// NHWC activation map with a (64, Wb, Hb, Nb) box
+static int map_act(CUtensorMap* m, const void* p, int Cch, int W, int H, int N, int Wb, int Hb, int Nb) {
+  cuuint64_t dims[4] = {(cuuint64_t)Cch, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+  cuuint32_t box[4] = {64, (cuuint32_t)Wb, (cuuint32_t)Hb, (cuuint32_t)Nb};
+  return make_map(m, p, 4, dims, box);
+}
+static int map_rows(CUtensorMap* m, const void* p, int K, int rows) {
+  cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
+  cuuint32_t box[2] = {64, 64};
+  return make_map(m, p, 2, dims, box);
+}
+
+struct Box { int Wb, Hb, Nb, tw, th, tn; };
+
+// choose the (Wb, Hb, Nb) pixel box with Wb*Hb*Nb <= cap that covers the grid
+// with the fewest tiles (ties: wider boxes, longer TMA rows)
+static Box choose_box(int W, int H, int N, int cap, bool exact) {
+  Box best{1, 1, 1, W, H, N};
+  long long best_tiles = -1;
+  if (exact) {
+    // box product must be exactly `cap` (a power of two); dims may overhang the
+    // tensor (TMA zero-fills), so any grid works
+    for (int wb = cap; wb >= 1; wb /= 2)
+      for (int hb = cap / wb; hb >= 1; hb /= 2) {
+        int nb = cap / (wb * hb);
+        long long tiles = (long long)((W + wb - 1) / wb) * ((H + hb - 1) / hb) * ((N + nb - 1) / nb);
+        if (best_tiles < 0 || tiles < best_tiles) {
+          best_tiles = tiles;
+          best = Box{wb, hb, nb, (W + wb - 1) / wb, (H + hb - 1) / hb, (N + nb - 1) / nb};
+        }
+      }
+    return best;
+  }
+  for (int wb = (W < cap ? W : cap); wb >= 1; --wb) {
+    for (int hb = (H < cap / wb ? H : cap / wb); hb >= 1; --hb) {
+      int nb = cap / (wb * hb);
+      if (nb > N) nb = N;
+      if (nb < 1) continue;
+      if (nb > 256 || wb > 256 || hb > 256) continue;
+      if (exact && wb * hb * nb != cap) continue;
+      long long tiles = (long long)((W + wb - 1) / wb) * ((H + hb - 1) / hb) * ((N + nb - 1) / nb);
+      if (best_tiles < 0 || tiles < best_tiles) {
+        best_tiles = tiles;
+        best = Box{wb, hb, nb, (W + wb - 1) / wb, (H + hb - 1) / hb, (N + nb - 1) / nb};
+      }
+    }
+  }
+  return best;
+}
+
+template <int EPI, int NB>
+static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const CUtensorMap& O0,
+                       const CUtensorMap& O1, const CUtensorMap& O2, const ConvArgs& args, cudaStream_t st) {
+  using Cfg = ConvCfg<EPI, NB>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(conv_gemm_kernel<EPI, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr = true;
+  }
+  int grid = args.total_tiles < g_num_sms ? args.total_tiles : g_num_sms;
+  conv_gemm_kernel<EPI, NB><<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
+  count_launch();
+  return check_launch("conv_gemm");
+}
+
+template <int NBLK>
+static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUtensorMap& Dm, const WgArgs& args,
+                        cudaStream_t st) {
+  using Cfg = WgCfg<NBLK>;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(wgrad_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    attr = true;
+  }
+  int grid = args.mtiles * args.ntiles * args.splits;
+  wgrad_kernel<NBLK><<<grid, 256, Cfg::SMEM, st>>>(X0, X1, Dm, args);
+  count_launch();
+  return check_launch("wgrad");
+}
+
+static int wgrad_ntile_blocks(int Jd) {
+  int nb = Jd / 64;
+  for (int c = 4; c >= 1; --c)
+    if (nb % c == 0) return c;
+  return 1;
+}
+
+int tc_wgrad_split(const Plan& P) {
+  int nkb = P.Kf / 64;
+  int mtiles = (nkb + 1) / 2;
+  int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P.Jd);
+  Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
+  long long ptiles = (long long)pb.tw * pb.th * pb.tn;
+  int sms = g_num_sms > 0 ? g_num_sms : 148;
+  long long S = (sms + mtiles * ntiles - 1) / (mtiles * ntiles);
+  long long cap = ptiles / 4;
+  if (cap < 1) cap = 1;
+  if (S > cap) S = cap;
+  if (S < 1) S = 1;
+  return (int)S;
+}
+
+// generic conv-GEMM launch (fprop or dgrad)
+static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N,
+                    int OWg, int OHg, int pad_eff, int r, int dual, const void* wmat, int wrows, int wK,
+                    int b_rs_tile, int b_rs_blk, int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2,
+                    int Cout, const float* const bias[3], const void* xres, cudaStream_t st) {
+  Box bx = choose_box(OWg, OHg, N, 128, false);
+  CUtensorMap A0, A1, B, O0, O1, O2;
+  int rc;
+  if ((rc = map_act(&A0, a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
+  if ((rc = map_act(&A1, a1 ? a1 : a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
+  if ((rc = map_rows(&B, wmat, wK, wrows))) return rc;
+  if ((rc = map_act(&O0, o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
+  if ((rc = map_act(&O1, o1 ? o1 : o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
+  if ((rc = map_act(&O2, o2 ? o2 : o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
+  ConvArgs g;
+  memset(&g, 0, sizeof(g));
+  g.tiles_w = bx.tw; g.tiles_h = bx.th; g.tiles_nn = tiles_nn;
+  g.total_tiles = bx.tw * bx.th * bx.tn * tiles_nn;
+  g.Wb = bx.Wb; g.Hb = bx.Hb; g.Nb = bx.Nb; g.box_rows = bx.Wb * bx.Hb * bx.Nb;
+  g.OHg = OHg; g.OWg = OWg; g.Ng = N;
+  g.r = r; g.pad_eff = pad_eff; g.cblks = Cin / 64;
+  g.kb_half = r * r * (Cin / 64); g.dual = dual;
+  g.b_rs_tile = b_rs_tile; g.b_rs_blk = b_rs_blk; g.out_c_tile = out_c_tile; g.Cout = Cout;
+  g.bias0 = bias[0]; g.bias1 = bias[1]; g.bias2 = bias[2];
+  g.xres = (const bf16*)xres;
+  if (epi == EPI_PROPOSED) return launch_conv<EPI_PROPOSED, 3>(A0, A1, B, O0, O1, O2, g, st);
+  if (epi == EPI_T4) return launch_conv<EPI_T4, 2>(A0, A1, B, O0, O1, O2, g, st);
+  if (epi == EPI_PLAIN) {
+    if (nbk == 4) return launch_conv<EPI_PLAIN, 4>(A0, A1, B, O0, O1, O2, g, st);
+    if (nbk == 2) return launch_conv<EPI_PLAIN, 2>(A0, A1, B, O0, O1, O2, g, st);
+    return launch_conv<EPI_PLAIN, 1>(A0, A1, B, O0, O1, O2, g, st);
+  }
+  if (nbk == 2) return launch_conv<EPI_SQ, 2>(A0, A1, B, O0, O1, O2, g, st);
+  return launch_conv<EPI_SQ, 1>(A0, A1, B, O0, O1, O2, g, st);
+}
+
+static int plain_blocks(int ch) { return ch % 256 == 0 ? 4 : (ch % 128 == 0 ? 2 : 1); }
+
+int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
+               void* b, char* ws, const Workspace& L, cudaStream_t st) {
+  const void* a0 = x;
+  const void* a1 = nullptr;
+  if (P.sq) {
+    void* xs = ws + L.off_XS;
+    launch_square(P, x, xs, st);
+    a0 = xs;
+    if (P.sq == 2) a1 = x;
+  }
+  const float* nb3[3] = {bias[0], bias[1], bias[2]};
+  int epi, nbk, tiles_nn, b_rs_tile, out_c_tile;
+  if (P.family == QD_FAM_PROPOSED) { epi = EPI_PROPOSED; nbk = 3; }
+  else if (P.family == QD_FAM_T4) { epi = EPI_T4; nbk = 2; }
+  else { epi = EPI_PLAIN; nbk = plain_blocks(P.F); }
+  if (epi == EPI_PLAIN) {
+    tiles_nn = P.F / (64 * nbk); b_rs_tile = 64 * nbk; out_c_tile = 64 * nbk;
+    if (P.family != QD_FAM_FIRST_ORDER) nb3[0] = nullptr;
+  } else {
+    tiles_nn = P.F / 64; b_rs_tile = nbk * 64; out_c_tile = 64;
+  }
+  return run_conv(epi, nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
+                  P.nb * P.F, P.Kf, b_rs_tile, 64, tiles_nn, out_c_tile, y, a, b, P.F, nb3, nullptr, st);
+}
+
+int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
+                void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L,
+                cudaStream_t st) {
+  const bf16* wd = (const bf16*)wpack + pack_fprop_elems(P);
+  const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  const bf16* D = (const bf16*)dy;
+  float* bpart = (float*)(ws + L.off_BS);
+  if (mat || P.nbias) {
+    long long rows_per = (P.Mout + L.bs_split - 1) / L.bs_split;
+    bf16* Dw = mat ? (bf16*)(ws + L.off_D) : nullptr;
+    bwd_prologue_vec_kernel<<<L.bs_split, 256, 0, st>>>(P, (const bf16*)dy, (const bf16*)a, (const bf16*)b, Dw,
+                                                        bpart, rows_per);
+    count_launch();
+    if (mat) D = Dw;
+    if (db[0]) launch_bias_finish(P, bpart, L.bs_split, db, st);
+  }
+  int rc;
+  // ---- wgrad ----
+  if (dW[0]) {
+    const void* x0 = x;
+    const void* x1 = x;
+    if (P.sq) {
+      void* xs = ws + L.off_XS;
+      launch_square(P, x, xs, st);
+      x0 = xs;
+    }
+    Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
+    CUtensorMap X0, X1, Dm;
+    if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
+    if ((rc = map_act(&X1, x1, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
+    if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
+    WgArgs g;
+    memset(&g, 0, sizeof(g));
+    int nblk = wgrad_ntile_blocks(P.Jd);
+    g.nkb = P.Kf / 64;
+    g.mtiles = (g.nkb + 1) / 2;
+    g.ntiles = (P.Jd / 64) / nblk;
+    g.splits = L.wg_split;
+    g.pb_w = pb.Wb; g.pb_h = pb.Hb; g.pb_n = pb.Nb;
+    g.pt_w = pb.tw; g.pt_h = pb.th; g.ptiles = pb.tw * pb.th * pb.tn;
+    g.r = P.r; g.pad = P.p; g.cblks = P.C / 64; g.kb_half = P.K0 / 64;
+    g.Jd = P.Jd; g.Kf = P.Kf;
+    g.part = (float*)(ws + L.off_WG);
+    if (nblk == 4) rc = launch_wgrad<4>(X0, X1, Dm, g, st);
+    else if (nblk == 3) rc = launch_wgrad<3>(X0, X1, Dm, g, st);
+    else if (nblk == 2) rc = launch_wgrad<2>(X0, X1, Dm, g, st);
+    else rc = launch_wgrad<1>(X0, X1, Dm, g, st);
+    if (rc) return rc;
+    launch_wgrad_finish(P, g.part, g.splits, dW, st);
+  }
+  // ---- dgrad (stride 1: a conv of D with the flipped packed weights) ----
+  if (dx) {
+    const float* nob[3] = {nullptr, nullptr, nullptr};
+    int pad_eff = P.r - 1 - P.p;
+    if (P.sq == 0) {
+      int nbk = plain_blocks(P.C);
+      rc = run_conv(EPI_PLAIN, nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
+                    64 * nbk, 64, P.C / (64 * nbk), 64 * nbk, dx, nullptr, nullptr, P.C, nob, nullptr, st);
+    } else if (P.sq == 1) {
+      rc = run_conv(EPI_SQ, 1, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd, 64,
+                    64, P.C / 64, 64, dx, nullptr, nullptr, P.C, nob, x, st);
+    } else {
+      rc = run_conv(EPI_SQ, 2, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd, 64,
+                    P.C, P.C / 64, 64, dx, nullptr, nullptr, P.C, nob, x, st);
+    }
+    if (rc) return rc;
+  }
+  return check_launch("tc backward");
+}
+
+}  // namespace qd

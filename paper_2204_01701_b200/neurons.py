@@ -1,0 +1,283 @@
+"""Drop-in quadratic-layer API on the B200 kernels.
+
+Same names and argument meaning as the reference's ``quadra.neurons``:
+
+* ``forward(spec, params, x) -> (y, LayerCache)``     neurons.py:235-276
+* ``symbolic_backward(spec, params, cache, dy) -> (grads, dx)``  neurons.py:295-445
+* ``validate_spec``, ``param_shapes``, ``cache_names``, ``count_*``,
+  ``init_params``                                        neurons.py:50-186
+* ``SYMBOLIC_BACKWARD`` family -> rule registry          tensor.py:598, neurons.py:462-463
+
+Differences a caller sees: tensors are torch tensors on the GPU instead of
+``quadra.Tensor`` (numpy inputs and objects with a ``.data`` ndarray are
+accepted and moved to the device); arithmetic is fp32 or bf16 instead of
+fp64 (``dtype=``, default: x's dtype, fp64 -> fp32); conv activations use the
+channels_last memory format (logical NCHW shape is kept). Errors raise the
+reference exception classes with the reference messages. Every call runs the
+CUDA kernels of libquadra_b200.so; nothing here computes on the CPU.
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DimensionError, IntegrityError
+from .spec import (DEVICE_FAMILIES, FAMILIES, KINDS, QUADRATIC_FAMILIES, T1_FAMILIES,  # noqa: F401
+                   QuadraticLayerSpec, cache_names, conv_out_size, count_macs, count_params,
+                   count_weights, fan_in, output_spatial, param_shapes, validate_device_spec,
+                   validate_spec)
+
+# weight roles in GEMM-branch order and bias roles, per family (the C ABI's
+# w[0..2] / bias[0..2] slots)
+WEIGHT_ROLES = {"proposed": ("Wa", "Wb", "Wc"), "t4": ("Wa", "Wb"), "t2": ("Wa",),
+                "first_order": ("W",), "t2_linear": ("Wa", "Wc")}
+BIAS_ROLES = {"proposed": ("ba", "bb", "bc"), "first_order": ("b",)}
+# gradient dict order of the reference symbolic_backward (neurons.py:380-391, :433-444)
+GRAD_ORDER = {"proposed": ("bc", "Wc", "bb", "Wb", "ba", "Wa"), "t4": ("Wb", "Wa"),
+              "t2": ("Wa",), "first_order": ("b", "W"), "t2_linear": ("Wa", "Wc")}
+
+_DAMPED_SECOND_FACTOR = ("t4", "t2and4", "proposed")
+
+
+@dataclass
+class LayerCache:
+    """Minimal forward values retained for the closed-form backward.
+
+    Fields of the reference LayerCache (neurons.py:201-209) plus the device
+    descriptor and the packed weights the forward used.
+    """
+    family: str
+    kind: str
+    x: torch.Tensor
+    a: torch.Tensor | None
+    b: torch.Tensor | None
+    y_shape: tuple
+    desc: object = field(default=None, repr=False)
+    wpack: torch.Tensor | None = field(default=None, repr=False)
+    pack_key: tuple = field(default=(), repr=False)
+
+
+def _device():
+    if not torch.cuda.is_available():
+        from .errors import DeviceError
+        raise DeviceError("no CUDA device: the quadratic-layer kernels run only on the GPU")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _as_device(t):
+    if isinstance(t, torch.Tensor):
+        return t if t.is_cuda else t.to(_device())
+    if hasattr(t, "data") and isinstance(getattr(t, "data"), np.ndarray):
+        t = t.data
+    return torch.as_tensor(np.asarray(t), device=_device())
+
+
+def _compute_dtype(x, dtype):
+    if dtype is not None:
+        dt = dtype
+    else:
+        dt = x.dtype
+        if dt == torch.float64:
+            dt = torch.float32
+    if dt not in (torch.float32, torch.bfloat16):
+        raise DimensionError(f"unsupported compute dtype {dt}; use float32 or bfloat16")
+    return dt
+
+
+def _check_x(spec, x):
+    """neurons.py:212-220."""
+    if spec.kind == "fc":
+        if x.ndim != 2 or x.shape[1] != spec.in_dim:
+            raise DimensionError(f"layer expects (N, {spec.in_dim}) input, got {tuple(x.shape)}")
+    else:
+        if x.ndim != 4 or x.shape[1] != spec.in_dim:
+            raise DimensionError(
+                f"layer expects (N, {spec.in_dim}, H, W) input, got {tuple(x.shape)}")
+
+
+def make_desc(spec, x_shape, dtype, flags=0):
+    d = _lib.QdDesc()
+    d.family = _lib.FAMILY_CODE[spec.family]
+    d.kind = _lib.KIND_CODE[spec.kind]
+    d.dtype = _lib.BF16 if dtype == torch.bfloat16 else _lib.F32
+    d.N = int(x_shape[0])
+    d.C = int(x_shape[1])
+    d.H = int(x_shape[2]) if spec.kind == "conv" else 1
+    d.W = int(x_shape[3]) if spec.kind == "conv" else 1
+    d.F = spec.out_dim
+    d.r, d.stride, d.pad = spec.kernel, spec.stride, spec.pad
+    d.flags = flags
+    return d
+
+
+def _layout(t, kind):
+    return t.contiguous(memory_format=torch.channels_last) if kind == "conv" else t.contiguous()
+
+
+def _weights(spec, params):
+    shapes = param_shapes(spec)
+    out = {}
+    for role, shape in shapes.items():
+        if role not in params:
+            raise DimensionError(f"missing parameter {role!r} for family {spec.family}")
+        t = _as_device(params[role])
+        if tuple(t.shape) != tuple(shape):
+            raise DimensionError(f"parameter {role} has shape {tuple(t.shape)}, expected {shape}")
+        out[role] = t
+    return out
+
+
+def _pack_key(ws):
+    return tuple((id(t), t._version, t.data_ptr()) for t in ws)
+
+
+def _pack(spec, desc, params):
+    lib = _lib.load()
+    roles = WEIGHT_ROLES[spec.family]
+    P = _weights(spec, params)
+    ws = [P[r].detach().to(torch.float32).contiguous() for r in roles]
+    nbytes = lib.qd_pack_bytes(ctypes.byref(desc))
+    if nbytes == 0:
+        _lib.raise_for(lib.qd_validate(ctypes.byref(desc)), "pack")
+    wpack = torch.empty(nbytes, dtype=torch.uint8, device=ws[0].device)
+    st = lib.qd_pack_weights(ctypes.byref(desc), _lib.ptr3(*[w.data_ptr() for w in ws]),
+                             wpack.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_pack_weights")
+    biases = [P[r].detach().to(torch.float32).contiguous() for r in BIAS_ROLES.get(spec.family, ())]
+    return wpack, _pack_key([P[r] for r in roles]), biases, ws
+
+
+def _workspace(desc, device):
+    n = _lib.load().qd_workspace_bytes(ctypes.byref(desc))
+    return torch.empty(max(n, 1), dtype=torch.uint8, device=device)
+
+
+def forward(spec, params, x, *, dtype=None, flags=0):
+    """Evaluate one layer on the GPU; returns (y, LayerCache). neurons.py:235-276."""
+    validate_device_spec(spec)
+    lib = _lib.load()
+    x = _as_device(x)
+    _check_x(spec, x)
+    cdt = _compute_dtype(x, dtype)
+    x = _layout(x.detach().to(cdt), spec.kind)
+    desc = make_desc(spec, x.shape, cdt, flags)
+    _lib.raise_for(lib.qd_validate(ctypes.byref(desc)))
+    oh, ow = ctypes.c_int(), ctypes.c_int()
+    lib.qd_out_shape(ctypes.byref(desc), ctypes.byref(oh), ctypes.byref(ow))
+    wpack, key, biases, _ = _pack(spec, desc, params)
+    if spec.kind == "conv":
+        yshape = (x.shape[0], spec.out_dim, oh.value, ow.value)
+        mk = lambda: torch.empty(yshape, dtype=cdt, device=x.device,  # noqa: E731
+                                 memory_format=torch.channels_last)
+    else:
+        yshape = (x.shape[0], spec.out_dim)
+        mk = lambda: torch.empty(yshape, dtype=cdt, device=x.device)  # noqa: E731
+    y = mk()
+    a = b = None
+    if spec.family in ("proposed", "t4"):
+        a, b = mk(), mk()
+    ws = _workspace(desc, x.device)
+    st = lib.qd_forward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
+                        _lib.ptr3(*[t.data_ptr() for t in biases]), y.data_ptr(),
+                        a.data_ptr() if a is not None else None,
+                        b.data_ptr() if b is not None else None, ws.data_ptr(),
+                        torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_forward")
+    return y, LayerCache(spec.family, spec.kind, x, a, b, tuple(y.shape), desc, wpack, key)
+
+
+def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True):
+    """Closed-form gradients on the GPU; returns ({role: grad}, dx).
+
+    neurons.py:295-445 -- same checks (IntegrityError for a cache of another
+    family/kind or a dy of the wrong shape), same roles, reference layouts.
+    Weight/bias gradients are fp32; dx has the compute dtype (None when
+    want_dx is False).
+    """
+    if cache.family != spec.family or cache.kind != spec.kind:
+        raise IntegrityError(
+            f"cache for {cache.family}/{cache.kind} used with {spec.family}/{spec.kind} layer")
+    validate_device_spec(spec)
+    lib = _lib.load()
+    g = _as_device(dy.data if hasattr(dy, "data") and not isinstance(dy, torch.Tensor) else dy)
+    if tuple(g.shape) != tuple(cache.y_shape):
+        raise IntegrityError(
+            f"output gradient shape {tuple(g.shape)} does not match forward {tuple(cache.y_shape)}")
+    _check_x(spec, cache.x)
+    x = cache.x
+    cdt = x.dtype
+    g = _layout(g.detach().to(cdt), spec.kind)
+    flags = cache.desc.flags if cache.desc is not None else 0
+    if not want_dx:
+        flags |= _lib.FLAG_NO_DX
+    if not want_dw:
+        flags |= _lib.FLAG_NO_DW
+    desc = make_desc(spec, x.shape, cdt, flags)
+    P = _weights(spec, params)
+    roles = WEIGHT_ROLES[spec.family]
+    if cache.wpack is not None and cache.pack_key == _pack_key([P[r] for r in roles]):
+        wpack = cache.wpack
+    else:
+        wpack = _pack(spec, desc, params)[0]
+    dev = x.device
+    shapes = param_shapes(spec)
+    grads = {role: torch.empty(shapes[role], dtype=torch.float32, device=dev)
+             for role in GRAD_ORDER[spec.family]}
+    dx = torch.empty_like(x) if want_dx else None  # preserves channels_last
+    ws = _workspace(desc, dev)
+    st = lib.qd_backward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
+                         cache.a.data_ptr() if cache.a is not None else None,
+                         cache.b.data_ptr() if cache.b is not None else None,
+                         g.data_ptr(), dx.data_ptr() if dx is not None else None,
+                         _lib.ptr3(*[grads[r].data_ptr() for r in roles]),
+                         _lib.ptr3(*[grads[r].data_ptr() for r in BIAS_ROLES.get(spec.family, ())]),
+                         ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_backward")
+    return grads, dx
+
+
+def device_path(spec, x_shape, dtype=torch.bfloat16, flags=0):
+    """0 = generic CUDA-core kernels, 1 = tcgen05/TMA kernels."""
+    desc = make_desc(spec, x_shape, dtype, flags)
+    p = _lib.load().qd_path(ctypes.byref(desc))
+    if p < 0:
+        _lib.raise_for(_lib.load().qd_validate(ctypes.byref(desc)))
+    return p
+
+
+def init_params(spec, rng, device=None):
+    """Fan-in-scaled normal init, product second factor damped x0.1, zero biases.
+
+    Same draws, in the same order, as the reference init_params
+    (neurons.py:132-147) given the same numpy Generator; returns fp32 torch
+    tensors on the GPU.
+    """
+    shapes = param_shapes(spec)
+    std = np.sqrt(2.0 / fan_in(spec))
+    dev = device or _device()
+    out = {}
+    for role, shape in shapes.items():
+        if role.startswith("b"):
+            arr = np.zeros(shape)
+        elif role == "Wq":
+            arr = rng.normal(0.0, 1.0 / spec.in_dim, size=shape)
+        elif role == "Wb" and spec.family in _DAMPED_SECOND_FACTOR:
+            arr = rng.normal(0.0, 0.1 * std, size=shape)
+        else:
+            arr = rng.normal(0.0, std, size=shape)
+        out[role] = torch.as_tensor(arr, dtype=torch.float32, device=dev)
+    return out
+
+
+def _symbolic_rule(spec, params, cache, g):
+    return symbolic_backward(spec, params, cache, g)
+
+
+# family -> closed-form backward rule (reference registry tensor.py:598,
+# populated at import like neurons.py:462-463)
+SYMBOLIC_BACKWARD = {fam: _symbolic_rule for fam in DEVICE_FAMILIES}

@@ -1,0 +1,115 @@
+"""torch.nn modules over the quadratic-layer kernels.
+
+The reference records a quadratic layer as ONE symbolic tape node whose
+backward is the closed form (neurons.py:466-477, tensor.py:601-609); here that
+node is a ``torch.autograd.Function`` whose backward calls
+``neurons.symbolic_backward`` -- the paper's own "hybrid back-propagation"
+design. Parameters keep the reference role names
+(``Wa, Wb, Wc, ba, bb, bc``) and layouts (conv (F, C, r, r); fc (in, out)),
+mirroring the paper's ``qua.type#()`` module API.
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+from torch import nn
+
+from . import neurons
+from .spec import QuadraticLayerSpec, fan_in, param_shapes, validate_device_spec
+
+
+class QuadFunction(torch.autograd.Function):
+    """y = layer(x; params) with the closed-form backward (one tape node)."""
+
+    @staticmethod
+    def forward(ctx, spec, dtype, x, *tensors):
+        roles = tuple(param_shapes(spec).keys())
+        params = dict(zip(roles, tensors))
+        y, cache = neurons.forward(spec, params, x, dtype=dtype)
+        ctx.spec, ctx.roles, ctx.params, ctx.cache = spec, roles, params, cache
+        ctx.x_dtype = x.dtype
+        return y
+
+    @staticmethod
+    def backward(ctx, gy):
+        want_dx = ctx.needs_input_grad[2]
+        grads, dx = neurons.symbolic_backward(ctx.spec, ctx.params, ctx.cache, gy,
+                                              want_dx=want_dx)
+        if dx is not None and dx.dtype != ctx.x_dtype:
+            dx = dx.to(ctx.x_dtype)
+        ctx.cache = None
+        return (None, None, dx) + tuple(grads[r] for r in ctx.roles)
+
+
+def quadratic(spec, params, x, dtype=None):
+    """Autograd-tracked layer call; ``params`` maps role -> tensor."""
+    roles = tuple(param_shapes(spec).keys())
+    return QuadFunction.apply(spec, dtype, x, *[params[r] for r in roles])
+
+
+def _reset(module, spec, generator=None, init="reference"):
+    """'reference': neurons.py:132-147 semantics (normal sqrt(2/fan_in), Wb x0.1,
+    zero bias); 'kaiming_uniform': U(+-sqrt(6/fan_in)) for every weight, zero
+    bias (BASELINE.json configs)."""
+    fi = fan_in(spec)
+    with torch.no_grad():
+        for role in param_shapes(spec):
+            p = getattr(module, role)
+            if role.startswith("b"):
+                p.zero_()
+            elif init == "kaiming_uniform":
+                bound = math.sqrt(6.0 / fi)
+                p.uniform_(-bound, bound, generator=generator)
+            else:
+                std = math.sqrt(2.0 / fi)
+                if role == "Wb" and spec.family in ("t4", "t2and4", "proposed"):
+                    std *= 0.1
+                p.normal_(0.0, std, generator=generator)
+
+
+class _QuadBase(nn.Module):
+    def __init__(self, spec, compute_dtype=torch.bfloat16, init="reference", device=None,
+                 generator=None):
+        super().__init__()
+        validate_device_spec(spec)
+        self.spec = spec
+        self.compute_dtype = compute_dtype
+        for role, shape in param_shapes(spec).items():
+            self.register_parameter(role, nn.Parameter(
+                torch.empty(shape, dtype=torch.float32, device=device)))
+        _reset(self, spec, generator, init)
+
+    def params(self):
+        return {role: getattr(self, role) for role in param_shapes(self.spec)}
+
+    def forward(self, x):
+        roles = tuple(param_shapes(self.spec).keys())
+        return QuadFunction.apply(self.spec, self.compute_dtype, x,
+                                  *[getattr(self, r) for r in roles])
+
+    def extra_repr(self):
+        return self.spec.describe() + f" dtype={self.compute_dtype}"
+
+
+class QuadConv2d(_QuadBase):
+    """Quadratic conv: family in {proposed, t4, t2, t2_linear, first_order}."""
+
+    def __init__(self, in_channels, out_channels, kernel_size=3, stride=1, padding=0,
+                 family="proposed", compute_dtype=torch.bfloat16, init="reference",
+                 device=None, generator=None):
+        spec = QuadraticLayerSpec(kind="conv", family=family, in_dim=in_channels,
+                                  out_dim=out_channels, kernel=kernel_size, stride=stride,
+                                  pad=padding)
+        super().__init__(spec, compute_dtype, init, device, generator)
+
+
+class QuadLinear(_QuadBase):
+    """Quadratic fc layer; weights stored (in, out) like the reference."""
+
+    def __init__(self, in_features, out_features, family="proposed",
+                 compute_dtype=torch.bfloat16, init="reference", device=None, generator=None):
+        spec = QuadraticLayerSpec(kind="fc", family=family, in_dim=in_features,
+                                  out_dim=out_features)
+        super().__init__(spec, compute_dtype, init, device, generator)

@@ -1,0 +1,233 @@
+"""GPU parity: the CUDA kernels (through the C ABI) vs the CPU oracle.
+
+Tolerances (BASELINE.json north_star): rel_err (reference tests/oracles.py:98-102)
+<= 1e-4 for fp32, <= 2e-2 for bf16; the oracle consumes the SAME cast input
+values upcast to fp64, so the comparison measures kernel error only.
+"""
+import numpy as np
+import pytest
+import torch
+
+from conftest import golden_index, load_case
+from oracle import quadra_oracle as Q
+
+pytestmark = pytest.mark.gpu
+
+TOL = {torch.float32: 1e-4, torch.bfloat16: 2e-2}
+
+
+def _spec(family, kind, c, f, k=1, s=1, p=0):
+    from paper_2204_01701_b200.spec import QuadraticLayerSpec
+    return QuadraticLayerSpec(kind=kind, family=family, in_dim=c, out_dim=f, kernel=k, stride=s,
+                              pad=p)
+
+
+def _q(a, dtype):
+    """Round an fp64 array to the run dtype and back (what the kernel sees)."""
+    return torch.as_tensor(a).to(dtype).to(torch.float64).numpy()
+
+
+def run_device(family, kind, x, P, g, dtype, k=1, s=1, p=0, flags=0):
+    from paper_2204_01701_b200 import neurons
+    c = x.shape[1]
+    f = g.shape[1]
+    spec = _spec(family, kind, c, f, k, s, p)
+    dev = torch.device("cuda")
+    xt = torch.as_tensor(x, device=dev).to(dtype)
+    params = {r: torch.as_tensor(v, dtype=torch.float32, device=dev) for r, v in P.items()}
+    y, cache = neurons.forward(spec, params, xt, dtype=dtype, flags=flags)
+    grads, dx = neurons.symbolic_backward(spec, params, cache, torch.as_tensor(g, device=dev).to(dtype))
+    torch.cuda.synchronize()
+    cv = lambda t: None if t is None else t.detach().to(torch.float64).cpu().numpy()  # noqa: E731
+    return (cv(y), cv(cache.a), cv(cache.b), {r: cv(v) for r, v in grads.items()}, cv(dx),
+            neurons.device_path(spec, x.shape, dtype, flags))
+
+
+def check_against_oracle(family, kind, x, P, g, dtype, k=1, s=1, p=0, flags=0, tol=None):
+    """Run device + oracle on identical (dtype-rounded) inputs; assert parity."""
+    tol = tol or TOL[dtype]
+    xq = _q(x, dtype)
+    gq = _q(g, dtype)
+    # weights are fp32 masters, cast to the compute dtype by the packer
+    Pq = {r: (_q(v, dtype) if not r.startswith("b") else _q(v, torch.float32)) for r, v in P.items()}
+    y, a, b, grads, dx, path = run_device(family, kind, xq, P, gq, dtype, k, s, p, flags)
+    geo = Q.Geometry(kind, k, s, p)
+    ry, ra, rb = Q.forward(family, geo, Pq, xq)
+    assert Q.rel_err(y, ry) <= tol, ("y", Q.rel_err(y, ry))
+    if ra is not None:
+        assert Q.rel_err(a, ra) <= tol and Q.rel_err(b, rb) <= tol
+    # oracle backward uses the kernel's own (rounded) a, b cache like the reference
+    ca = a if a is not None else None
+    cb = b if b is not None else None
+    rg, rdx = Q.symbolic_backward(family, geo, Pq, xq, ca, cb, gq)
+    assert Q.rel_err(dx, rdx) <= tol, ("dx", Q.rel_err(dx, rdx))
+    assert set(grads) == set(rg)
+    for role in rg:
+        assert Q.rel_err(grads[role], rg[role]) <= tol, (role, Q.rel_err(grads[role], rg[role]))
+    return path
+
+
+GOLD = golden_index()["layers"]
+
+
+@pytest.mark.parametrize("case", GOLD, ids=[c["file"] for c in GOLD])
+def test_golden_cases_fp32(case):
+    """Every reference golden case (incl. k3/s2/p1 and k2/s1/p0) in fp32 against
+    the REFERENCE's own outputs."""
+    z = load_case(case["file"])
+    P = {k[2:]: v for k, v in z.items() if k.startswith("P_")}
+    y, a, b, grads, dx, _ = run_device(case["family"], case["kind"], z["x"], P, z["g"],
+                                       torch.float32, case["k"], case["s"], case["p"])
+    assert Q.rel_err(y, z["y"]) <= 1e-4
+    assert Q.rel_err(dx, z["dx"]) <= 1e-4
+    for role in grads:
+        assert Q.rel_err(grads[role], z["G_" + role]) <= 1e-4, role
+
+
+@pytest.mark.parametrize("case", GOLD, ids=[c["file"] for c in GOLD])
+def test_golden_cases_bf16(case):
+    z = load_case(case["file"])
+    P = {k[2:]: v for k, v in z.items() if k.startswith("P_")}
+    check_against_oracle(case["family"], case["kind"], z["x"], P, z["g"], torch.bfloat16,
+                         case["k"], case["s"], case["p"])
+
+
+# shapes that tile onto the tcgen05 kernels (C, F multiples of 64, stride 1)
+TC_CASES = [
+    # family, kind, n, c, f, h, w, k, s, p
+    ("proposed", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("proposed", "conv", 3, 64, 128, 10, 12, 3, 1, 1),
+    ("proposed", "conv", 2, 128, 64, 6, 6, 1, 1, 0),
+    ("proposed", "conv", 2, 64, 64, 9, 7, 2, 1, 0),
+    ("proposed", "conv", 8, 64, 64, 32, 32, 3, 1, 1),       # BASELINE C2 geometry, batch 8
+    ("proposed", "conv", 4, 256, 256, 7, 7, 3, 1, 1),       # C5 512@7-like, dgrad N=256
+    ("t4", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("t4", "conv", 2, 64, 128, 11, 9, 3, 1, 1),
+    ("t2", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("t2_linear", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("t2_linear", "conv", 2, 128, 64, 5, 6, 3, 1, 1),
+    ("first_order", "conv", 2, 64, 128, 8, 8, 3, 1, 1),
+    ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
+    ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
+    ("t2_linear", "fc", 64, 128, 64, 1, 1, 1, 1, 0),
+]
+
+
+@pytest.mark.parametrize("case", TC_CASES, ids=[f"{c[0]}-{c[1]}-{c[3]}x{c[4]}-{c[5]}x{c[6]}-k{c[7]}p{c[9]}"
+                                               for c in TC_CASES])
+def test_tcgen05_path_parity(case):
+    fam, kind, n, c, f, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, kind, n, c, f, h, w, k, s, p, seed=7, random_bias=True)
+    path = check_against_oracle(fam, kind, x, P, g, torch.bfloat16, k, s, p)
+    assert path == 1, "expected the tcgen05 kernels for this shape"
+
+
+@pytest.mark.parametrize("case", TC_CASES[:4] + TC_CASES[8:10], ids=str)
+def test_tcgen05_matches_cuda_core_path(case):
+    """Same bf16 inputs through the tcgen05 kernels and the CUDA-core kernels."""
+    from paper_2204_01701_b200 import _lib
+    fam, kind, n, c, f, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, kind, n, c, f, h, w, k, s, p, seed=11, random_bias=True)
+    xq, gq = _q(x, torch.bfloat16), _q(g, torch.bfloat16)
+    r1 = run_device(fam, kind, xq, P, gq, torch.bfloat16, k, s, p)
+    r0 = run_device(fam, kind, xq, P, gq, torch.bfloat16, k, s, p, flags=_lib.FLAG_FORCE_SIMT)
+    assert r1[5] == 1 and r0[5] == 0
+    assert Q.rel_err(r1[0], r0[0]) <= 1e-2
+    assert Q.rel_err(r1[4], r0[4]) <= 1e-2
+    for role in r1[3]:
+        assert Q.rel_err(r1[3][role], r0[3][role]) <= 1e-2, role
+
+
+def test_c1_fc_fp32():
+    """BASELINE config 1: fc 256x512->512, fp32, Kaiming-uniform, b=0."""
+    x, P, g = Q.synthetic_layer("proposed", "fc", 256, 512, 512, seed=0)
+    check_against_oracle("proposed", "fc", x, P, g, torch.float32)
+
+
+def test_variants_fp32_conv():
+    for fam in ("proposed", "t4", "t2", "t2_linear", "first_order"):
+        x, P, g = Q.synthetic_layer(fam, "conv", 2, 5, 6, 7, 6, 3, 2, 1, seed=3, random_bias=True)
+        check_against_oracle(fam, "conv", x, P, g, torch.float32, 3, 2, 1)
+
+
+def test_c2_full_batch_properties():
+    """BASELINE config 2 at full size (128x64x32x32 -> 64, bf16): per-sample
+    outputs vs the oracle on a slice, and batch-linearity of dW/db."""
+    from paper_2204_01701_b200 import neurons
+    fam, n = "proposed", 128
+    x, P, g = Q.synthetic_layer(fam, "conv", n, 64, 64, 32, 32, 3, 1, 1, seed=0)
+    dt = torch.bfloat16
+    xq, gq = _q(x, dt), _q(g, dt)
+    y, a, b, grads, dx, path = run_device(fam, "conv", xq, P, gq, dt, 3, 1, 1)
+    assert path == 1
+    assert np.isfinite(y).all() and np.isfinite(dx).all()
+    geo = Q.Geometry("conv", 3, 1, 1)
+    Pq = {r: (_q(v, dt) if not r.startswith("b") else v) for r, v in P.items()}
+    sl = slice(0, 4)
+    ry, ra, rb = Q.forward(fam, geo, Pq, xq[sl])
+    assert Q.rel_err(y[sl], ry) <= 2e-2
+    _, rdx = Q.symbolic_backward(fam, geo, Pq, xq[sl], a[sl], b[sl], gq[sl])
+    assert Q.rel_err(dx[sl], rdx) <= 2e-2
+    h = n // 2
+    _, _, _, g1, _, _ = run_device(fam, "conv", xq[:h], P, gq[:h], dt, 3, 1, 1)
+    _, _, _, g2, _, _ = run_device(fam, "conv", xq[h:], P, gq[h:], dt, 3, 1, 1)
+    for role in grads:
+        assert Q.rel_err(grads[role], g1[role] + g2[role]) <= 1e-2, role
+
+
+def test_deterministic_replay():
+    """Bitwise-identical outputs and gradients on replay."""
+    x, P, g = Q.synthetic_layer("proposed", "conv", 4, 64, 64, 16, 16, 3, 1, 1, seed=5)
+    r1 = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    r2 = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    assert (r1[0] == r2[0]).all() and (r1[4] == r2[4]).all()
+    for role in r1[3]:
+        assert (r1[3][role] == r2[3][role]).all()
+
+
+def test_error_conventions_on_device():
+    from paper_2204_01701_b200 import neurons
+    from paper_2204_01701_b200.errors import DimensionError, IntegrityError
+    dev = torch.device("cuda")
+    s1 = _spec("t4", "fc", 3, 2)
+    s2 = _spec("proposed", "fc", 3, 2)
+    p1 = {"Wa": torch.randn(3, 2, device=dev), "Wb": torch.randn(3, 2, device=dev)}
+    _, cache = neurons.forward(s1, p1, torch.randn(2, 3, device=dev))
+    with pytest.raises(IntegrityError):
+        neurons.symbolic_backward(s2, p1, cache, torch.zeros(2, 2, device=dev))
+    with pytest.raises(IntegrityError):
+        neurons.symbolic_backward(s1, p1, cache, torch.zeros(2, 5, device=dev))
+    with pytest.raises(DimensionError):
+        neurons.forward(s1, p1, torch.randn(2, 4, device=dev))
+    sc = _spec("proposed", "conv", 1, 1, 5, 1, 0)
+    pc = {r: torch.randn(*sh, device=dev) for r, sh in
+          __import__("paper_2204_01701_b200.spec", fromlist=["x"]).param_shapes(sc).items()}
+    with pytest.raises(DimensionError):
+        neurons.forward(sc, pc, torch.randn(1, 1, 3, 3, device=dev))
+
+
+def test_autograd_module_matches_functional():
+    from paper_2204_01701_b200 import neurons
+    from paper_2204_01701_b200.nn import QuadConv2d
+    torch.manual_seed(0)
+    m = QuadConv2d(64, 64, 3, 1, 1, device="cuda")
+    x = torch.randn(2, 64, 8, 8, device="cuda", dtype=torch.bfloat16,
+                    requires_grad=True).contiguous(memory_format=torch.channels_last)
+    x.retain_grad()
+    y = m(x)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    y2, cache = neurons.forward(m.spec, m.params(), x.detach())
+    grads, dx = neurons.symbolic_backward(m.spec, m.params(), cache, gy)
+    assert torch.equal(y, y2)
+    assert torch.equal(x.grad, dx)
+    for role, g in grads.items():
+        assert torch.equal(getattr(m, role).grad, g)
+
+
+def test_kernels_launch_counter():
+    from paper_2204_01701_b200 import _lib
+    before = _lib.launch_count()
+    x, P, g = Q.synthetic_layer("proposed", "conv", 2, 64, 64, 8, 8, 3, 1, 1)
+    run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    assert _lib.launch_count() > before
