@@ -19,46 +19,6 @@ namespace qd {
 size_t pack_fprop_elems(const Plan& P) { return (size_t)P.nb * P.F * P.Kf; }
 size_t pack_dgrad_elems(const Plan& P) { return (size_t)P.Cd * P.Kd; }
 
-template <typename T>
-__global__ void pack_fprop_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
-  const float* w[3] = {w0, w1, w2};
-  long long total = (long long)P.nb * P.F * P.Kf;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    int R = (int)(i / P.Kf), k = (int)(i % P.Kf);
-    int grp = P.nb * P.FT;
-    int tile = R / grp, rem = R % grp;
-    int br = rem / P.FT, f = tile * P.FT + rem % P.FT;
-    int role = br, kk = k;
-    if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
-    int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
-    float v;
-    if (P.kind == QD_KIND_FC) v = w[role][(size_t)c * P.F + f];
-    else v = w[role][(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
-    out[i] = cvt<T>(v);
-  }
-}
-
-// dgrad weights: Wd[c'][e*Jd + j], e = flipped tap (ey,ex) -> (r-1-ey, r-1-ex)
-template <typename T>
-__global__ void pack_dgrad_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
-  const float* w[3] = {w0, w1, w2};
-  long long total = (long long)P.Cd * P.Kd;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    int cp = (int)(i / P.Kd), k = (int)(i % P.Kd);
-    int e = k / P.Jd, j = k % P.Jd;
-    int ey = e / P.r, ex = e % P.r, dy = P.r - 1 - ey, dx = P.r - 1 - ex;
-    int role, f, c;
-    if (P.sq == 2) { role = cp / P.C; c = cp % P.C; f = j; }
-    else { role = j / P.F; f = j % P.F; c = cp; }
-    float v;
-    if (P.kind == QD_KIND_FC) v = w[role][(size_t)c * P.F + f];
-    else v = w[role][(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
-    out[i] = cvt<T>(v);
-  }
-}
-
 static inline int grid_for(long long n, int bs = 256, int cap = 148 * 16) {
   long long g = (n + bs - 1) / bs;
   if (g > cap) g = cap;
@@ -66,18 +26,49 @@ static inline int grid_for(long long n, int bs = 256, int cap = 148 * 16) {
   return (int)g;
 }
 
+template <typename T>
+__global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
+  // blocks [0, nfb) pack the fprop layout, the rest the dgrad layout
+  long long nf = (long long)P.nb * P.F * P.Kf;
+  int nfb = (int)((nf + 255) / 256);
+  if ((int)blockIdx.x < nfb) {
+    long long i = (long long)blockIdx.x * 256 + threadIdx.x;
+    if (i >= nf) return;
+    int R = (int)(i / P.Kf), k = (int)(i % P.Kf);
+    int grp = P.nb * P.FT;
+    int tile = R / grp, rem = R % grp;
+    int br = rem / P.FT, f = tile * P.FT + rem % P.FT;
+    int role = br, kk = k;
+    if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+    int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
+    const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+    float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                     : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+    out[i] = cvt<T>(v);
+  } else {
+    long long i = (long long)(blockIdx.x - nfb) * 256 + threadIdx.x;
+    if (i >= (long long)P.Cd * P.Kd) return;
+    int cp = (int)(i / P.Kd), k = (int)(i % P.Kd);
+    int e = k / P.Jd, j = k % P.Jd;
+    int ey = e / P.r, ex = e % P.r, dy = P.r - 1 - ey, dx = P.r - 1 - ex;
+    int role, f, c;
+    if (P.sq == 2) { role = cp / P.C; c = cp % P.C; f = j; }
+    else { role = j / P.F; f = j % P.F; c = cp; }
+    const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+    float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                     : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+    out[nf + i] = cvt<T>(v);
+  }
+}
+
 void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
   long long nf = (long long)pack_fprop_elems(P), nd = (long long)pack_dgrad_elems(P);
-  if (P.dtype == QD_BF16) {
-    bf16* o = (bf16*)wpack;
-    pack_fprop_kernel<bf16><<<grid_for(nf), 256, 0, st>>>(P, w[0], w[1], w[2], o);
-    pack_dgrad_kernel<bf16><<<grid_for(nd), 256, 0, st>>>(P, w[0], w[1], w[2], o + nf);
-  } else {
-    float* o = (float*)wpack;
-    pack_fprop_kernel<float><<<grid_for(nf), 256, 0, st>>>(P, w[0], w[1], w[2], o);
-    pack_dgrad_kernel<float><<<grid_for(nd), 256, 0, st>>>(P, w[0], w[1], w[2], o + nf);
-  }
-  count_launch(2);
+  int blocks = (int)((nf + 255) / 256 + (nd + 255) / 256);
+  if (P.dtype == QD_BF16)
+    pack_all_kernel<bf16><<<blocks, 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack);
+  else
+    pack_all_kernel<float><<<blocks, 256, 0, st>>>(P, w[0], w[1], w[2], (float*)wpack);
+  count_launch();
 }
 
 // ---------------------------------------------------------------------------
@@ -287,20 +278,31 @@ void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const voi
 }
 
 // bias gradient per role: proposed ba <- sum(dy*b) (block 0), bb <- sum(dy*a)
-// (block 1), bc <- sum(dy) (block 2); first_order b <- sum(dy). Fixed-order sum.
-__global__ void bias_finish_kernel(Plan P, const float* part, int S, float* d0, float* d1, float* d2) {
-  int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= P.Jd) return;
+// (block 1), bc <- sum(dy) (block 2); first_order b <- sum(dy).
+// One block per 32 columns; 8 row-groups sum strided partials, then a
+// fixed-order combine (deterministic).
+__global__ void __launch_bounds__(256) bias_finish_kernel(Plan P, const float* part, int S, float* d0,
+                                                          float* d1, float* d2) {
+  __shared__ float red[8][33];
+  int col = threadIdx.x % 32, grp = threadIdx.x / 32;
+  int j = blockIdx.x * 32 + col;
   float acc = 0.f;
-  for (int s = 0; s < S; ++s) acc += part[(size_t)s * P.Jd + j];
-  int role = j / P.F, f = j % P.F;
-  float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
-  if (dst) dst[f] = acc;
+  if (j < P.Jd)
+    for (int s = grp; s < S; s += 8) acc += part[(size_t)s * P.Jd + j];
+  red[grp][col] = acc;
+  __syncthreads();
+  if (grp == 0 && j < P.Jd) {
+    float t = 0.f;
+    for (int g = 0; g < 8; ++g) t += red[g][col];
+    int role = j / P.F, f = j % P.F;
+    float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
+    if (dst) dst[f] = t;
+  }
 }
 
 void launch_bias_finish(const Plan& P, const float* part, int S, float* const db[3], cudaStream_t st) {
   if (P.nbias == 0) return;
-  bias_finish_kernel<<<(P.Jd + 127) / 128, 128, 0, st>>>(P, part, S, db[0], db[1], db[2]);
+  bias_finish_kernel<<<(P.Jd + 31) / 32, 256, 0, st>>>(P, part, S, db[0], db[1], db[2]);
   count_launch();
 }
 

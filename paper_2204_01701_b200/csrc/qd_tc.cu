@@ -678,7 +678,8 @@ int tc_wgrad_split(const Plan& P) {
   Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
   long long ptiles = (long long)pb.tw * pb.th * pb.tn;
   int sms = g_num_sms > 0 ? g_num_sms : 148;
-  long long S = (sms + mtiles * ntiles - 1) / (mtiles * ntiles);
+  // one wave: every CTA holds ~200 KB of smem, so > #SMs CTAs would run a tail wave
+  long long S = sms / (mtiles * ntiles);
   long long cap = ptiles / 4;
   if (cap < 1) cap = 1;
   if (S > cap) S = cap;
