@@ -256,13 +256,33 @@ def run_ours(args, wl, wl_name):
     for _ in range(args.warmup):
         step()
     torch.cuda.synchronize()
+    # kernels of ours per step (counted on an eager step; graph replays launch the same set)
+    l0 = _lib.launch_count()
+    step()
+    torch.cuda.synchronize()
+    per_step_launches = _lib.launch_count() - l0
+    run = step
+    if not args.no_graph:
+        # the whole step (pack + fwd + bwd [+ gradient all-reduce]) as one CUDA graph:
+        # no host launch gaps between the ~8 kernels
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step()
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+        run = graph.replay
+        for _ in range(args.warmup):
+            run()
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    l0 = _lib.launch_count()
     with ClockSampler(local) as clk:
-        ms = timed(step, args.steps)
-    launches = _lib.launch_count() - l0
+        ms = timed(run, args.steps)
+    launches = per_step_launches * args.steps
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
@@ -353,7 +373,7 @@ def run_ours(args, wl, wl_name):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": dts, "data": "synthetic (seeded N(0,1) x and dy, Kaiming-uniform W, b=0)",
-           "config": config_of(wl, wl_name, world),
+           "config": dict(config_of(wl, wl_name, world), cuda_graph=not args.no_graph),
            "roofline": roof, "cpu_baseline": cpu,
            "e2e": {"value": world * flops / (e2e_step_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                    "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": h2d,
@@ -375,6 +395,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     wl = WORKLOADS[args.workload]

@@ -61,6 +61,8 @@ enum {
                                  where a tcgen05 kernel exists (tests)     */
 #define QD_FLAG_NO_DW 4u      /* backward: skip weight and bias gradients  \
                                  (frozen layers; per-kernel timing)        */
+#define QD_FLAG_TC_V1 8u      /* tcgen05 path without the CTA-pair / halo \
+                                 conv kernel (tests compare the two)       */
 
 typedef struct {
   int family, kind, dtype;

@@ -21,7 +21,7 @@ F32, BF16 = 0, 1
 
 QD_OK, QD_ERR_CONFIG, QD_ERR_DIM, QD_ERR_INTEGRITY = 0, 1, 2, 3
 QD_ERR_CUDA, QD_ERR_UNSUPPORTED, QD_ERR_ARG = 4, 5, 6
-FLAG_NO_DX, FLAG_FORCE_SIMT, FLAG_NO_DW = 1, 2, 4
+FLAG_NO_DX, FLAG_FORCE_SIMT, FLAG_NO_DW, FLAG_TC_V1 = 1, 2, 4, 8
 
 EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_pack_weights", "qd_forward", "qd_backward", "qd_path",

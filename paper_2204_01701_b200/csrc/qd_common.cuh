@@ -28,6 +28,7 @@ struct Plan {
   int Kd;          // dgrad K: r*r*Jd
   int nroles;      // weight roles
   int nbias;       // bias roles
+  unsigned flags;  // qd_desc flags
 };
 
 __host__ __device__ inline int conv_out(int size, int r, int s, int p) {
@@ -41,6 +42,7 @@ inline Plan make_plan(const qd_desc& d) {
   P.family = d.family; P.kind = d.kind; P.dtype = d.dtype;
   P.N = d.N; P.C = d.C; P.H = d.H; P.W = d.W; P.F = d.F;
   P.r = d.r; P.s = d.stride; P.p = d.pad;
+  P.flags = d.flags;
   P.OH = conv_out(P.H, P.r, P.s, P.p);
   P.OW = conv_out(P.W, P.r, P.s, P.p);
   P.Min = (long long)P.N * P.H * P.W;

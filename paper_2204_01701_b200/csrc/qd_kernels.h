@@ -46,11 +46,23 @@ void launch_bias_finish(const Plan& P, const float* bsum_part, int bs_split,
 // sum the wgrad partials [S][Jd][Kf] and scatter into reference layouts
 void launch_wgrad_finish(const Plan& P, const float* part, int S, float* const dW[3],
                          cudaStream_t st);
+// tcgen05 path: wgrad partial fold + bias partial fold in one launch (Kf % 4 == 0)
+void launch_bwd_finish(const Plan& P, const float* wpart, int S, float* const dW[3], const float* bpart, int SB,
+                       float* const db[3], cudaStream_t st);
 void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st);
 
 // ---- tcgen05 path ----------------------------------------------------------
 bool tc_supported(const Plan& P, unsigned flags);
 int tc_wgrad_split(const Plan& P);
+// v2 wgrad with halo reuse (qd_tc2.cu); wgrad2_split() == 0 when not eligible
+int wgrad2_split(const Plan& P);
+int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
+               cudaStream_t st);
+// v2 stride-1 conv on CTA pairs (qd_tc2.cu); QD_ERR_UNSUPPORTED if the shape does not fit
+int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
+              int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
+              int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
+              const void* xres, cudaStream_t st);
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3],
                void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st);
 // dW[0] == nullptr skips the weight/bias gradient GEMM (QD_FLAG_NO_DW)

@@ -142,6 +142,27 @@ __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo_byte
   d |= (uint64_t)2 << 61;  // SWIZZLE_128B
   return d;
 }
+// Split form for issue loops: the high word (SBO, version, layout) is fixed
+// per operand, the low word (start address >> 4 | LBO >> 4 << 16) advances by
+// (byte offset >> 4); keeps the per-MMA work to one add on uniform registers.
+__host__ __device__ constexpr uint32_t sw128_desc_hi(uint32_t sbo_bytes) {
+  return ((sbo_bytes >> 4) & 0x3FFF) | (1u << 14) | (2u << 29);
+}
+__device__ __forceinline__ uint32_t sw128_desc_lo(uint32_t saddr, uint32_t lbo_bytes) {
+  return ((saddr >> 4) & 0x3FFF) | (((lbo_bytes >> 4) & 0x3FFF) << 16);
+}
+__device__ __forceinline__ uint64_t mk_desc(uint32_t hi, uint32_t lo) { return ((uint64_t)hi << 32) | lo; }
+
+// one elected lane of a converged warp (the MMA/TMA issue loops run on the
+// whole warp so descriptor arithmetic stays on the uniform datapath)
+__device__ __forceinline__ bool elect_one() {
+  uint32_t p;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\telect.sync _|P, 0xffffffff;\n\tselp.u32 %0, 1, 0, P;\n\t}"
+      : "=r"(p));
+  return p != 0;
+}
+
 // Instruction descriptor: kind::f16, A = B = bf16, D = f32, dense.
 __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N, bool a_mn_major, bool b_mn_major) {
   return (1u << 4)                                // D format f32

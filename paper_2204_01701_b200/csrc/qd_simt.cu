@@ -436,3 +436,70 @@ int simt_backward(const Plan& P, const void* x, const void* wpack, const void* a
 }
 
 }  // namespace qd
+
+namespace qd {
+// One launch folds both fixed-order reductions of the backward pass:
+// blocks [0, nwb) sum the wgrad split-K partials (4 elements per thread) and
+// scatter them into the reference layouts; the rest sum the bias partials.
+__global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __restrict__ wpart, int S,
+                                                         float* w0, float* w1, float* w2,
+                                                         const float* __restrict__ bpart, int SB, float* d0,
+                                                         float* d1, float* d2, int nwb) {
+  if ((int)blockIdx.x < nwb) {
+    if (!w0) return;
+    const long long total = (long long)P.Jd * P.Kf;
+    long long i4 = ((long long)blockIdx.x * 256 + threadIdx.x) * 4;
+    if (i4 >= total) return;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    const float4* src = reinterpret_cast<const float4*>(wpart + i4);
+    const long long stride4 = total / 4;
+#pragma unroll 4
+    for (int s = 0; s < S; ++s) {
+      float4 v = __ldg(src + s * stride4);
+      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    }
+    float av[4] = {acc.x, acc.y, acc.z, acc.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      long long i = i4 + e;
+      int j = (int)(i / P.Kf), k = (int)(i % P.Kf);
+      int role, f = j % P.F, kk = k;
+      if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+      else role = j / P.F;
+      int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
+      float* dst = role == 0 ? w0 : (role == 1 ? w1 : w2);
+      if (!dst) continue;
+      if (P.kind == QD_KIND_FC) dst[(size_t)c * P.F + f] = av[e];
+      else dst[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx] = av[e];
+    }
+  } else {
+    if (P.nbias == 0 || !d0) return;
+    __shared__ float red[8][33];
+    int col = threadIdx.x % 32, grp = threadIdx.x / 32;
+    int j = ((int)blockIdx.x - nwb) * 32 + col;
+    float acc = 0.f;
+    if (j < P.Jd)
+      for (int s = grp; s < SB; s += 8) acc += bpart[(size_t)s * P.Jd + j];
+    red[grp][col] = acc;
+    __syncthreads();
+    if (grp == 0 && j < P.Jd) {
+      float t = 0.f;
+      for (int gq = 0; gq < 8; ++gq) t += red[gq][col];
+      int role = j / P.F, f = j % P.F;
+      float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
+      if (dst) dst[f] = t;
+    }
+  }
+}
+
+void launch_bwd_finish(const Plan& P, const float* wpart, int S, float* const dW[3], const float* bpart, int SB,
+                       float* const db[3], cudaStream_t st) {
+  long long total = (long long)P.Jd * P.Kf;  // Kf is a multiple of 64 on the tcgen05 path
+  int nwb = dW[0] ? (int)((total / 4 + 255) / 256) : 0;
+  int nbb = (P.nbias && db[0]) ? (P.Jd + 31) / 32 : 0;
+  if (nwb + nbb == 0) return;
+  bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1], db[2],
+                                                nwb);
+  count_launch();
+}
+}  // namespace qd

@@ -153,34 +153,38 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ===== MMA issuer =====
-      constexpr uint32_t IDESC = ptx::idesc_bf16(128, NB * 64, false, false);
-      int stage = 0;
-      uint32_t phase = 0;
-      int it = 0;
-      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
-        int as = it & 1;
-        uint32_t aph = (it >> 1) & 1;
-        ptx::mbar_wait(&tempty[as], aph ^ 1);
+    // ===== MMA issuer: warp-wide loop (uniform datapath), one elected lane issues =====
+    constexpr uint32_t IDESC = ptx::idesc_bf16(128, NB * 64, false, false);
+    constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
+    const bool leader = ptx::elect_one();
+    const uint32_t a_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sA), 16);
+    const uint32_t b_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sB), 16);
+    int stage = 0;
+    uint32_t phase = 0;
+    int it = 0;
+    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+      int as = it & 1;
+      uint32_t aph = (it >> 1) & 1;
+      ptx::mbar_wait(&tempty[as], aph ^ 1);
+      ptx::tc_fence_after();
+      uint32_t d_tmem = tmem_base + as * Cfg::ACC_COLS;
+      for (int kb = 0; kb < KB; ++kb) {
+        ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
-        uint32_t d_tmem = tmem_base + as * Cfg::ACC_COLS;
-        for (int kb = 0; kb < KB; ++kb) {
-          ptx::mbar_wait(&full[stage], phase);
-          ptx::tc_fence_after();
-          uint32_t a0 = ptx::smem_u32(sA + stage * Cfg::A_BYTES);
-          uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::B_BYTES);
+        const uint32_t a_lo = a_lo0 + stage * (Cfg::A_BYTES >> 4);
+        const uint32_t b_lo = b_lo0 + stage * (Cfg::B_BYTES >> 4);
+        if (leader) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint64_t ad = ptx::sw128_desc(a0 + k * 32, 16, 1024);
-            uint64_t bd = ptx::sw128_desc(b0 + k * 32, 16, 1024);
-            ptx::mma_bf16(d_tmem, ad, bd, IDESC, (kb | k) != 0);
-          }
+          for (int k = 0; k < 4; ++k)
+            ptx::mma_bf16(d_tmem, ptx::mk_desc(DHI, a_lo + 2 * k), ptx::mk_desc(DHI, b_lo + 2 * k), IDESC,
+                          (kb | k) != 0);
           ptx::mma_commit(&empty[stage]);
-          if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
-        ptx::mma_commit(&tfull[as]);
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
+      if (leader) ptx::mma_commit(&tfull[as]);
+      __syncwarp();
     }
   } else if (warp >= 4) {
     // ===== epilogue =====
@@ -396,29 +400,33 @@ __global__ void __launch_bounds__(256, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IDESC = ptx::idesc_bf16(128, NBLK * 64, true, true);
-      int stage = 0;
-      uint32_t phase = 0;
-      bool first = true;
-      for (int pt = p_beg; pt < p_end; ++pt) {
-        ptx::mbar_wait(&full[stage], phase);
-        ptx::tc_fence_after();
-        uint32_t a0 = ptx::smem_u32(sA + stage * Cfg::A_BYTES);
-        uint32_t b0 = ptx::smem_u32(sB + stage * Cfg::B_BYTES);
+    // warp-wide loop, elected lane issues (descriptors stay on the uniform datapath)
+    constexpr uint32_t IDESC = ptx::idesc_bf16(128, NBLK * 64, true, true);
+    constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
+    const bool leader = ptx::elect_one();
+    const uint32_t a_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sA), 8192);
+    const uint32_t b_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sB), 8192);
+    int stage = 0;
+    uint32_t phase = 0;
+    uint32_t accum = 0;
+    for (int pt = p_beg; pt < p_end; ++pt) {
+      ptx::mbar_wait(&full[stage], phase);
+      ptx::tc_fence_after();
+      const uint32_t a_lo = a_lo0 + stage * (Cfg::A_BYTES >> 4);
+      const uint32_t b_lo = b_lo0 + stage * (Cfg::B_BYTES >> 4);
+      if (leader) {
 #pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          // 16 pixels (K) per MMA = two 8-row groups of 128 B
-          uint64_t ad = ptx::sw128_desc(a0 + k * 2048, 8192, 1024);
-          uint64_t bd = ptx::sw128_desc(b0 + k * 2048, 8192, 1024);
-          ptx::mma_bf16(tmem_base, ad, bd, IDESC, (first && k == 0) ? 0u : 1u);
-        }
-        first = false;
+        for (int k = 0; k < 4; ++k)  // 16 pixels (K) per MMA = two 8-row groups of 128 B
+          ptx::mma_bf16(tmem_base, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, b_lo + 128 * k), IDESC,
+                        accum | (uint32_t)k);
         ptx::mma_commit(&empty[stage]);
-        if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      ptx::mma_commit(done);
+      accum = 1;
+      __syncwarp();
+      if (++stage == STAGES) { stage = 0; phase ^= 1; }
     }
+    if (leader) ptx::mma_commit(done);
+    __syncwarp();
   } else if (warp >= 4) {
     const int q = warp & 3;
     const int row = q * 32 + lane;
@@ -560,6 +568,9 @@ static bool init_driver() {
   return true;
 }
 
+PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() { return g_encode; }
+int tc_num_sms() { return g_num_sms > 0 ? g_num_sms : 148; }
+
 bool tc_supported(const Plan& P, unsigned flags) {
   if (flags & QD_FLAG_FORCE_SIMT) return false;
   if (P.dtype != QD_BF16) return false;
@@ -672,6 +683,10 @@ static int wgrad_ntile_blocks(int Jd) {
 }
 
 int tc_wgrad_split(const Plan& P) {
+  if (!(P.flags & QD_FLAG_TC_V1)) {
+    int s2 = wgrad2_split(P);
+    if (s2 > 0) return s2;
+  }
   int nkb = P.Kf / 64;
   int mtiles = (nkb + 1) / 2;
   int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P.Jd);
@@ -746,6 +761,11 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
   } else {
     tiles_nn = P.F / 64; b_rs_tile = nbk * 64; out_c_tile = 64;
   }
+  if (!(P.flags & QD_FLAG_TC_V1)) {
+    int rc2 = run_conv2(epi, nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
+                        P.nb * P.F, P.Kf, b_rs_tile, 64, tiles_nn, out_c_tile, y, a, b, P.F, nb3, nullptr, st);
+    if (rc2 != QD_ERR_UNSUPPORTED) return rc2;
+  }
   return run_conv(epi, nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
                   P.nb * P.F, P.Kf, b_rs_tile, 64, tiles_nn, out_c_tile, y, a, b, P.F, nb3, nullptr, st);
 }
@@ -764,7 +784,6 @@ int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
                                                         bpart, rows_per);
     count_launch();
     if (mat) D = Dw;
-    if (db[0]) launch_bias_finish(P, bpart, L.bs_split, db, st);
   }
   int rc;
   // ---- wgrad ----
@@ -776,6 +795,14 @@ int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
       launch_square(P, x, xs, st);
       x0 = xs;
     }
+    rc = QD_ERR_UNSUPPORTED;
+    if (!(P.flags & QD_FLAG_TC_V1) && wgrad2_split(P) == L.wg_split)
+      rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st);
+    if (rc == QD_OK) {
+      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, dW, bpart, L.bs_split, db, st);
+    } else if (rc != QD_ERR_UNSUPPORTED) {
+      return rc;
+    } else {
     Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
     CUtensorMap X0, X1, Dm;
     if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
@@ -798,23 +825,29 @@ int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
     else if (nblk == 2) rc = launch_wgrad<2>(X0, X1, Dm, g, st);
     else rc = launch_wgrad<1>(X0, X1, Dm, g, st);
     if (rc) return rc;
-    launch_wgrad_finish(P, g.part, g.splits, dW, st);
+    launch_bwd_finish(P, g.part, g.splits, dW, bpart, L.bs_split, db, st);
+    }
+  } else if (db[0] && (mat || P.nbias)) {
+    launch_bias_finish(P, bpart, L.bs_split, db, st);
   }
   // ---- dgrad (stride 1: a conv of D with the flipped packed weights) ----
   if (dx) {
     const float* nob[3] = {nullptr, nullptr, nullptr};
     int pad_eff = P.r - 1 - P.p;
-    if (P.sq == 0) {
-      int nbk = plain_blocks(P.C);
-      rc = run_conv(EPI_PLAIN, nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
-                    64 * nbk, 64, P.C / (64 * nbk), 64 * nbk, dx, nullptr, nullptr, P.C, nob, nullptr, st);
-    } else if (P.sq == 1) {
-      rc = run_conv(EPI_SQ, 1, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd, 64,
-                    64, P.C / 64, 64, dx, nullptr, nullptr, P.C, nob, x, st);
-    } else {
-      rc = run_conv(EPI_SQ, 2, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd, 64,
-                    P.C, P.C / 64, 64, dx, nullptr, nullptr, P.C, nob, x, st);
-    }
+    int epi = P.sq == 0 ? EPI_PLAIN : EPI_SQ;
+    int nbk = P.sq == 0 ? plain_blocks(P.C) : (P.sq == 1 ? 1 : 2);
+    int tiles_nn = P.sq == 0 ? P.C / (64 * nbk) : P.C / 64;
+    int b_rs_tile = P.sq == 0 ? 64 * nbk : 64;
+    int b_rs_blk = P.sq == 2 ? P.C : 64;
+    int out_c_tile = P.sq == 0 ? 64 * nbk : 64;
+    const void* xr = P.sq ? x : nullptr;
+    rc = QD_ERR_UNSUPPORTED;
+    if (!(P.flags & QD_FLAG_TC_V1))
+      rc = run_conv2(epi, nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
+                     b_rs_tile, b_rs_blk, tiles_nn, out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
+    if (rc == QD_ERR_UNSUPPORTED)
+      rc = run_conv(epi, nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
+                    b_rs_tile, b_rs_blk, tiles_nn, out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
     if (rc) return rc;
   }
   return check_launch("tc backward");

@@ -1,0 +1,913 @@
+// K1/K3 v2: stride-1 implicit-GEMM conv on CTA pairs (cta_group::2) with
+// halo reuse. Used for fprop (A = x) and dgrad (A = D, flipped weights) when
+// r >= 2, channels are multiples of 64 and the image is wide enough.
+//
+// Tiling. Each image's output grid is walked in the "padded flat" index
+// q = oh * Wp + ow (Wp = W + 2 pe): output (oh, ow) reads padded input rows
+// q + ey * Wp + ex, so a tile of 128 consecutive q needs ONE halo box of whole
+// padded rows (4-D TMA box {64 ch, Wp, HR, 1}, OOB zero fill = the padding),
+// and every filter tap is the same smem tile read through a descriptor
+// shifted by ey*Wp + ex rows -- SWIZZLE_128B is address based on sm_100a
+// (profiles/r1_probe_sw128_row_shift.log), so row shifts need no re-layout.
+// The last r-1 columns of each padded row are junk outputs and are not stored.
+//
+// Pairs. The two CTAs of a cluster take the same tile index of images 2p and
+// 2p+1 (identical halo geometry, so one descriptor address serves both) and
+// issue M = 256 MMAs: CTA r holds A rows 128r.. and N rows [r N/2, (r+1) N/2)
+// of B (profiles/r1_probe_2cta.log). When half of B fits in smem (C = F = 64:
+// 108 KB) it is loaded once per CTA and stays resident; otherwise B streams
+// per (tap, channel block) through a ring.
+//
+// Epilogue. Per warp, TMEM rows -> registers (a*b + c + bias, or 2 x acc) ->
+// swizzled 4 KB warp staging -> 16-B coalesced global stores that skip the
+// junk columns; TMEM accumulators are double-buffered so this overlaps the
+// next tile's main loop.
+#include <cudaTypedefs.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+#include "qd_kernels.h"
+#include "qd_ptx.cuh"
+
+namespace qd {
+
+enum { E2_PROPOSED = 0, E2_T4 = 1, E2_PLAIN = 2, E2_SQ = 3 };
+
+struct C2Args {
+  int N, Cin, Win, Hin;
+  int OHg, OWg;
+  int pe, r, Wp, HR;
+  int T_img, tiles_nn, total;
+  int cblks, ablocks, KBtot;
+  int resident;
+  int b_rs_tile, b_rs_blk, b_contig;
+  int Cout, out_c_tile;
+  uint32_t halo_bytes, halo_tx, b_stage_bytes;
+  int b_slots, a_slots, stg_tiles;
+  int nbias;  // bias vectors staged in smem (3 proposed, 1 first_order, else 0), Cout floats each
+  int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
+  unsigned long long* trace;  // QD_TRACE (dev only): per-role clock64 timeline of cluster 0
+  const float* bias0;
+  const float* bias1;
+  const float* bias2;
+  bf16* out0;
+  bf16* out1;
+  bf16* out2;
+  const bf16* xres;
+};
+
+namespace c2 {
+// dev-only timeline: slot = (role * 64 + tile) * 16 + event, CTA 0 only
+#define C2_TRACE(role, tile, ev)                                                                  \
+  do {                                                                                            \
+    if (g.trace && blockIdx.x == 0 && (tile) < 64)                                                \
+      g.trace[((role) * 64 + (tile)) * 16 + (ev)] = (unsigned long long)clock64();                \
+  } while (0)
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ uint32_t peer0(const void* p) { return ptx::smem_u32(p) & 0xFEFFFFFFu; }
+__device__ __forceinline__ void tma4_cg2(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1, int c2,
+                                         int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(m), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void tma2_cg2(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(dst)),
+      "l"(m), "r"(bar), "r"(c0), "r"(c1)
+      : "memory");
+}
+__device__ __forceinline__ void mma_cg2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+      "l"(a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          ptx::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+// TMEM hand-back: no memory is published through this barrier (the TMEM
+// reads are ordered by tcgen05.wait::ld + fence::before_thread_sync), so a
+// relaxed arrive -- a release would first drain this warp's outstanding
+// global stores of the previous tile (profiled: the MMA warp stalled on it).
+__device__ __forceinline__ void arrive_remote(uint32_t addr) {
+  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t*>(&h);
+}
+// 16 values (channels 16j..16j+15) of warp-local row `row` into a 32x128 B
+// staging tile, 16-B chunk q stored at q ^ (row & 7) (bank-conflict free)
+__device__ __forceinline__ void stage16(uint8_t* tile, int row, int j, const float* v) {
+  uint4 lo, hi;
+  lo.x = pack2(v[0], v[1]);   lo.y = pack2(v[2], v[3]);   lo.z = pack2(v[4], v[5]);   lo.w = pack2(v[6], v[7]);
+  hi.x = pack2(v[8], v[9]);   hi.y = pack2(v[10], v[11]); hi.z = pack2(v[12], v[13]); hi.w = pack2(v[14], v[15]);
+  uint8_t* rp = tile + row * 128;
+  *reinterpret_cast<uint4*>(rp + (((2 * j) ^ (row & 7)) << 4)) = lo;
+  *reinterpret_cast<uint4*>(rp + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
+}
+}  // namespace c2
+
+// coalesced store of one 32 x 128 B warp staging tile: 4 rows (512 B) per instruction
+template <int EPI>
+__device__ __forceinline__ void c2_store_pass(const C2Args& g, const uint8_t* st, int o, int c_base, int pix,
+                                              int lane) {
+  bf16* dst = (EPI == E2_PROPOSED || EPI == E2_T4) ? (o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2)) : g.out0;
+  const int ch = (EPI == E2_PLAIN) ? c_base + o * 64 : c_base;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    int Rw = 4 * i + (lane >> 3), c = lane & 7;
+    int rp = __shfl_sync(0xffffffffu, pix, Rw);
+    uint4 val = *reinterpret_cast<const uint4*>(st + Rw * 128 + ((c ^ (Rw & 7)) << 4));
+    if (rp >= 0) *reinterpret_cast<uint4*>(dst + (size_t)rp * g.Cout + ch + c * 8) = val;
+  }
+}
+
+template <int EPI, int NB, int R>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    conv2_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
+                 const __grid_constant__ CUtensorMap mB, const C2Args g) {
+  // output "passes": proposed/t4 write y, a, b; plain writes NB 64-channel blocks
+  constexpr int NPASS = (EPI == E2_PROPOSED || EPI == E2_T4) ? 3 : (EPI == E2_PLAIN ? NB : 1);
+  constexpr int ACC = NB * 64;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sHalo = sm;
+  uint8_t* sB = sHalo + g.a_slots * g.halo_bytes;
+  uint8_t* sStg = sB + g.b_slots * g.b_stage_bytes;
+  float* sBias = (float*)(sStg + 4 * g.stg_tiles * 4096);
+  uint64_t* afull = (uint64_t*)(sBias + g.nbias * g.Cout);
+  uint64_t* aempty = afull + 4;
+  uint64_t* tfull = aempty + 4;
+  uint64_t* tempty = tfull + 2;
+  uint64_t* bres = tempty + 2;
+  uint64_t* bfull = bres + 1;
+  uint64_t* bempty = bfull + g.b_slots;
+  uint32_t* tslot = (uint32_t*)(bempty + g.b_slots);
+
+  const uint32_t rank = c2::cluster_rank();
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+  const int r = R > 0 ? R : g.r;
+  const int rr = r * r;
+
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(&mA0);
+    ptx::prefetch_tmap(&mA1);
+    ptx::prefetch_tmap(&mB);
+    for (int i = 0; i < 4; ++i) {
+      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&aempty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(&tfull[i], 1);
+      ptx::mbar_init(&tempty[i], 8);
+    }
+    ptx::mbar_init(bres, 1);
+    for (int i = 0; i < g.b_slots; ++i) {
+      ptx::mbar_init(&bfull[i], 1);
+      ptx::mbar_init(&bempty[i], 1);
+    }
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(ptx::smem_u32(tslot)),
+                 "r"(512)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  ptx::tc_fence_before();
+  c2::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    // ===== TMA producer (whole warp loops, one elected lane issues; both CTAs,
+    // completions land on CTA0's barriers) =====
+    const int half_rows = NB * 32;
+    const bool leader = ptx::elect_one();
+    auto brow = [&](int j) {
+      return g.b_contig ? j * g.b_rs_tile + (int)rank * half_rows : j * g.b_rs_tile + (int)rank * g.b_rs_blk;
+    };
+    if (g.resident && leader) {
+      if (rank == 0) ptx::mbar_arrive_expect_tx(bres, 2u * g.KBtot * g.b_stage_bytes);
+      for (int kb = 0; kb < g.KBtot; ++kb)
+        c2::tma2_cg2(&mB, c2::peer0(bres), sB + kb * g.b_stage_bytes, kb * 64, brow(0));
+    }
+    int as = 0, bs = 0;
+    uint32_t aph = 0, bph = 0;
+    int it = 0;
+    for (int w = cluster; w < g.total; w += nclusters, ++it) {
+      int j = w % g.tiles_nn, rest = w / g.tiles_nn;
+      int t = rest % g.T_img, p = rest / g.T_img;
+      int n = 2 * p + (int)rank;
+      int hq_lo = (128 * t) / g.Wp;
+      for (int ab = 0; ab < g.ablocks; ++ab) {
+        int half = ab / g.cblks, cb = ab % g.cblks;
+        if (leader) C2_TRACE(0, it, 2 * ab);
+        ptx::mbar_wait(&aempty[as], aph ^ 1);
+        if (leader) {
+          C2_TRACE(0, it, 2 * ab + 1);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&afull[as], 2u * g.halo_tx);
+          c2::tma4_cg2(half ? &mA1 : &mA0, c2::peer0(&afull[as]), sHalo + as * g.halo_bytes, cb * 64, -g.pe,
+                       hq_lo - g.pe, n);
+        }
+        if (++as == g.a_slots) { as = 0; aph ^= 1; }
+        if (!g.resident) {
+          for (int tap = 0; tap < rr; ++tap) {
+            int kbi = (half * rr + tap) * g.cblks + cb;
+            ptx::mbar_wait(&bempty[bs], bph ^ 1);
+            if (leader) {
+              if (rank == 0) ptx::mbar_arrive_expect_tx(&bfull[bs], 2u * g.b_stage_bytes);
+              c2::tma2_cg2(&mB, c2::peer0(&bfull[bs]), sB + bs * g.b_stage_bytes, kbi * 64, brow(j));
+            }
+            if (++bs == g.b_slots) { bs = 0; bph ^= 1; }
+          }
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // ===== MMA issuer (CTA0 only, M = 256 over the pair); warp-wide loop,
+      // descriptors on the uniform datapath, one elected lane issues =====
+      constexpr uint32_t IDESC = ptx::idesc_bf16(256, ACC, false, false);
+      constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
+      const bool leader = ptx::elect_one();
+      if (g.resident) {
+        ptx::mbar_wait(bres, 0);
+        ptx::tc_fence_after();
+      }
+      const uint32_t halo_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sHalo), 16);
+      const uint32_t b_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sB), 16);
+      const uint32_t halo_step = g.halo_bytes >> 4, b_step = g.b_stage_bytes >> 4;
+      const uint32_t wp8 = (uint32_t)g.Wp * 8;
+      int as = 0, bs = 0;
+      uint32_t aph = 0, bph = 0;
+      int it = 0;
+      for (int w = cluster; w < g.total; w += nclusters, ++it) {
+        int rest = w / g.tiles_nn;
+        int t = rest % g.T_img;
+        int q0 = 128 * t;
+        int row_off = q0 - (q0 / g.Wp) * g.Wp;
+        int acs = it & 1;
+        uint32_t tph = (it >> 1) & 1;
+        if (leader) C2_TRACE(1, it, 0);
+        ptx::mbar_wait(&tempty[acs], tph ^ 1);
+        if (leader) C2_TRACE(1, it, 1);
+        ptx::tc_fence_after();
+        const uint32_t d = tmem + acs * ACC;
+        uint32_t accum = 0;
+        for (int ab = 0; ab < g.ablocks; ++ab) {
+          int half = ab / g.cblks, cb = ab % g.cblks;
+          ptx::mbar_wait(&afull[as], aph);
+          if (leader) C2_TRACE(1, it, 2 + ab);
+          ptx::tc_fence_after();
+          const uint32_t a_lo = halo_lo0 + as * halo_step + row_off * 8;
+          if (g.resident && !(g.dbg & 2)) {
+            // all taps of this channel block back to back (B resident: no waits)
+            const uint32_t bb = b_lo0 + (half * rr * g.cblks + cb) * b_step;
+            const uint32_t tap_b = g.cblks * b_step;
+            if (leader) {
+              if (R > 0) {
+#pragma unroll
+                for (int ey = 0; ey < R; ++ey)
+#pragma unroll
+                  for (int ex = 0; ex < R; ++ex) {
+                    const uint32_t at = a_lo + ey * wp8 + ex * 8, bt = bb + (ey * R + ex) * tap_b;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                      c2::mma_cg2(d, ptx::mk_desc(DHI, at + 2 * k), ptx::mk_desc(DHI, bt + 2 * k), IDESC, accum);
+                      accum = 1;
+                    }
+                  }
+              } else {
+                for (int ey = 0; ey < r; ++ey)
+                  for (int ex = 0; ex < r; ++ex) {
+                    const uint32_t at = a_lo + ey * wp8 + ex * 8, bt = bb + (ey * r + ex) * tap_b;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                      c2::mma_cg2(d, ptx::mk_desc(DHI, at + 2 * k), ptx::mk_desc(DHI, bt + 2 * k), IDESC, accum);
+                      accum = 1;
+                    }
+                  }
+              }
+            }
+            accum = 1;
+            __syncwarp();
+          } else {
+            for (int ey = 0; ey < r; ++ey) {
+              for (int ex = 0; ex < r; ++ex) {
+                uint32_t b_lo;
+                if (g.resident) {
+                  b_lo = b_lo0 + ((half * rr + ey * r + ex) * g.cblks + cb) * b_step;
+                } else {
+                  ptx::mbar_wait(&bfull[bs], bph);
+                  ptx::tc_fence_after();
+                  b_lo = b_lo0 + bs * b_step;
+                }
+                const uint32_t at = a_lo + ey * wp8 + ex * 8;
+                if (leader && !(g.dbg & 2)) {
+#pragma unroll
+                  for (int k = 0; k < 4; ++k)
+                    c2::mma_cg2(d, ptx::mk_desc(DHI, at + 2 * k), ptx::mk_desc(DHI, b_lo + 2 * k), IDESC,
+                                accum | (uint32_t)k);
+                }
+                accum = 1;
+                __syncwarp();
+                if (!g.resident) {
+                  if (leader) c2::commit_mc(&bempty[bs]);
+                  if (++bs == g.b_slots) { bs = 0; bph ^= 1; }
+                }
+              }
+            }
+          }
+          if (leader) c2::commit_mc(&aempty[as]);
+          if (++as == g.a_slots) { as = 0; aph ^= 1; }
+        }
+        if (leader) c2::commit_mc(&tfull[acs]);
+        if (leader) C2_TRACE(1, it, 15);
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 4) {
+    // ===== epilogue (both CTAs, own TMEM rows); one 4 KB staging tile per warp,
+    // one output pass at a time =====
+    const int q = warp & 3;
+    {
+      // every bias of the layer into smem once; read back as float4 broadcasts
+      const int et = threadIdx.x - 128;
+      for (int i = et; i < g.nbias * g.Cout; i += 128) {
+        int role = i / g.Cout, c = i - role * g.Cout;
+        const float* src = role == 0 ? g.bias0 : (role == 1 ? g.bias1 : g.bias2);
+        sBias[i] = __ldg(src + c);
+      }
+      ptx::named_bar_sync(1, 128);
+    }
+    uint8_t* stg = sStg + q * g.stg_tiles * 4096;
+    const bool multi = g.stg_tiles > 1;
+    const uint32_t tempty0 = c2::peer0(&tempty[0]);
+    int it = 0;
+    for (int w = cluster; w < g.total; w += nclusters, ++it) {
+      int j = w % g.tiles_nn, rest = w / g.tiles_nn;
+      int t = rest % g.T_img, p = rest / g.T_img;
+      int n = 2 * p + (int)rank;
+      int acs = it & 1;
+      uint32_t tph = (it >> 1) & 1;
+      int qq = 128 * t + q * 32 + lane;
+      int hq = qq / g.Wp, wq = qq - hq * g.Wp;
+      bool valid = n < g.N && hq < g.OHg && wq < g.OWg;
+      int pix = valid ? (n * g.OHg + hq) * g.OWg + wq : -1;
+      const int c_base = j * g.out_c_tile;
+      if (q == 0 && lane == 0) C2_TRACE(2, it, 0);
+      ptx::mbar_wait(&tfull[acs], tph);
+      if (q == 0 && lane == 0) C2_TRACE(2, it, 1);
+      ptx::tc_fence_after();
+      if (g.dbg & 1) {
+        __syncwarp();
+        if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
+        continue;
+      }
+      const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acs * ACC;
+#pragma unroll 1
+      for (int o = 0; o < NPASS; ++o) {
+#pragma unroll 1
+        for (int jj = 0; jj < 4; ++jj) {
+          float out[16];
+          const int c0 = c_base + jj * 16;
+          if (EPI == E2_PROPOSED || EPI == E2_T4) {
+            float va[16], vb[16];
+            if (o != 2) ptx::tmem_ld16(tb + jj * 16, va);            // a
+            if (o != 1) ptx::tmem_ld16(tb + 64 + jj * 16, vb);       // b
+            float vc[16];
+            if (EPI == E2_PROPOSED && o == 0) ptx::tmem_ld16(tb + 128 + jj * 16, vc);
+            // biases: 16 channels as 4 x float4 per role, loaded together (a per-element
+            // __ldg chain serialised at ~86 cycles each -- traced)
+            float ba[16], bbv[16], bc[16];
+            if (EPI == E2_PROPOSED) {
+              const float4* pa = reinterpret_cast<const float4*>(sBias + c0);
+              const float4* pb = reinterpret_cast<const float4*>(sBias + g.Cout + c0);
+              const float4* pc = reinterpret_cast<const float4*>(sBias + 2 * g.Cout + c0);
+#pragma unroll
+              for (int v4 = 0; v4 < 4; ++v4) {
+                float4 x0 = pa[v4], x1 = pb[v4], x2 = pc[v4];
+                ba[4 * v4] = x0.x; ba[4 * v4 + 1] = x0.y; ba[4 * v4 + 2] = x0.z; ba[4 * v4 + 3] = x0.w;
+                bbv[4 * v4] = x1.x; bbv[4 * v4 + 1] = x1.y; bbv[4 * v4 + 2] = x1.z; bbv[4 * v4 + 3] = x1.w;
+                bc[4 * v4] = x2.x; bc[4 * v4 + 1] = x2.y; bc[4 * v4 + 2] = x2.z; bc[4 * v4 + 3] = x2.w;
+              }
+            }
+            ptx::tmem_wait_ld();
+            if (EPI == E2_PROPOSED) {
+              if (o == 0) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) out[e] = fmaf(va[e] + ba[e], vb[e] + bbv[e], vc[e] + bc[e]);
+              } else if (o == 1) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) out[e] = va[e] + ba[e];
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) out[e] = vb[e] + bbv[e];
+              }
+            } else {
+              if (o == 0) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) out[e] = va[e] * vb[e];
+              } else if (o == 1) {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) out[e] = va[e];
+              } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) out[e] = vb[e];
+              }
+            }
+          } else if (EPI == E2_PLAIN) {
+            ptx::tmem_ld16(tb + o * 64 + jj * 16, out);
+            float bz[16];
+            if (g.nbias) {
+              const float4* pz = reinterpret_cast<const float4*>(sBias + c0 + o * 64);
+#pragma unroll
+              for (int v4 = 0; v4 < 4; ++v4) {
+                float4 x0 = pz[v4];
+                bz[4 * v4] = x0.x; bz[4 * v4 + 1] = x0.y; bz[4 * v4 + 2] = x0.z; bz[4 * v4 + 3] = x0.w;
+              }
+            }
+            ptx::tmem_wait_ld();
+            if (g.nbias) {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) out[e] += bz[e];
+            }
+          } else {  // E2_SQ: dx = 2 x acc0 (+ acc1)
+            float v0[16], v1[16], xv[16];
+            ptx::tmem_ld16(tb + jj * 16, v0);
+            if (NB == 2) ptx::tmem_ld16(tb + 64 + jj * 16, v1);
+            if (valid) {
+              const uint4* xp = reinterpret_cast<const uint4*>(g.xres + (size_t)pix * g.Cout + c0);
+              uint4 u0 = __ldg(xp), u1 = __ldg(xp + 1);
+              const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
+              const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                float2 f0 = __bfloat1622float2(h0[e]), f1 = __bfloat1622float2(h1[e]);
+                xv[2 * e] = f0.x; xv[2 * e + 1] = f0.y; xv[8 + 2 * e] = f1.x; xv[9 + 2 * e] = f1.y;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 16; ++e) xv[e] = 0.f;
+            }
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              float tt = v0[e] * xv[e];
+              out[e] = tt + tt;
+              if (NB == 2) out[e] += v1[e];
+            }
+          }
+          c2::stage16(stg + (multi ? o * 4096 : 0), lane, jj, out);
+        }
+        if (q == 0 && lane == 0) C2_TRACE(2, it, 4 + 2 * o);
+        if (o == NPASS - 1) {
+          // every TMEM read of this tile is done -> hand the accumulator back
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
+          if (q == 0 && lane == 0) C2_TRACE(2, it, 2);
+        }
+        if (!multi) {
+          __syncwarp();
+          c2_store_pass<EPI>(g, stg, o, c_base, pix, lane);
+          __syncwarp();
+          if (q == 0 && lane == 0) C2_TRACE(2, it, 5 + 2 * o);
+        }
+      }
+      if (multi) {
+        __syncwarp();
+#pragma unroll 1
+        for (int o = 0; o < NPASS; ++o) c2_store_pass<EPI>(g, stg + o * 4096, o, c_base, pix, lane);
+        __syncwarp();
+      }
+      if (q == 0 && lane == 0) C2_TRACE(2, it, 3);
+    }
+  }
+  ptx::tc_fence_before();
+  c2::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
+  }
+}
+
+// ---------------------------------------------------------------------------
+// host
+// ---------------------------------------------------------------------------
+static unsigned long long* g_trace = nullptr;
+static unsigned long long* trace_buffer() {
+  if (!g_trace) {
+    cudaMalloc(&g_trace, 3 * 64 * 16 * sizeof(unsigned long long));
+  }
+  cudaMemset(g_trace, 0, 3 * 64 * 16 * sizeof(unsigned long long));
+  return g_trace;
+}
+}  // namespace qd
+// dev-only: copy the last QD_TRACE timeline (3 roles x 64 tiles x 16 events, clock64)
+extern "C" int qd_debug_trace_copy(unsigned long long* host) {
+  if (!qd::g_trace) return -1;
+  cudaDeviceSynchronize();
+  return (int)cudaMemcpy(host, qd::g_trace, 3 * 64 * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
+namespace qd {
+extern PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn();
+extern int tc_num_sms();
+
+struct C2Plan {
+  bool ok;
+  C2Args g;
+  size_t smem;
+};
+
+static int c2_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint32_t* box) {
+  cuuint64_t strides[4];
+  cuuint64_t acc = dims[0] * 2;
+  for (int i = 1; i < rank; ++i) {
+    strides[i - 1] = acc;
+    acc *= dims[i];
+  }
+  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  CUresult r = tc_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box,
+                              es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                              CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return set_error(QD_ERR_CUDA, "cuTensorMapEncodeTiled (conv2) failed (%d)", (int)r);
+  return QD_OK;
+}
+
+// geometry + smem plan; ok=false if this conv does not fit the v2 kernel
+static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int NB, int NOUT,
+                      int tiles_nn, int Cout, int nbias) {
+  C2Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  C2Args& g = pl.g;
+  if (r < 2 || Cin % 64 || Cout % 64) return pl;
+  int Wp = Win + 2 * pe;
+  if (OWg != Wp - r + 1 || Wp > 256 || OWg < 12) return pl;
+  int T_img = (OHg * Wp + 127) / 128;
+  int HR = 0;
+  for (int t = 0; t < T_img; ++t) {
+    int q0 = 128 * t, lo = q0 / Wp, hi = (q0 + 127 + (r - 1) * Wp + (r - 1)) / Wp;
+    if (hi - lo + 1 > HR) HR = hi - lo + 1;
+  }
+  if (HR > 256) return pl;
+  uint32_t halo_tx = (uint32_t)Wp * HR * 128;
+  uint32_t halo = (halo_tx + 1023) / 1024 * 1024;
+  if (halo > 64 * 1024) return pl;
+  int cblks = Cin / 64;
+  int ablocks = cblks * (dual ? 2 : 1);
+  int KBtot = ablocks * r * r;
+  uint32_t bstage = NB * 32 * 128;
+  // staging: one 4 KB tile per warp per output pass (single epilogue pass over TMEM,
+  // stores after the hand-back) when smem allows, else one tile reused per pass
+  int stg_tiles = NOUT;
+  {
+    const char* e = getenv("QD_C2_STG");
+    if (e) stg_tiles = atoi(e) > 1 ? NOUT : 1;
+  }
+  const size_t bias_bytes = (size_t)nbias * Cout * 4;
+  const size_t fixed0 = 1024 + 4 * (size_t)stg_tiles * 4096 + bias_bytes + 1024;  // slack, staging, biases, barriers
+  const size_t limit = 227 * 1024;
+  int resident = 0, slots, aslots = 0;
+  // prefer resident B with >= 3 halo buffers; else stream B with a 4-deep halo ring
+  if (tiles_nn == 1 && KBtot <= 48) {
+    size_t rest = limit - fixed0 - (size_t)KBtot * bstage;
+    if ((long long)rest >= 2 * (long long)halo) {
+      resident = 1;
+      slots = KBtot;
+      aslots = (int)(rest / halo);
+      if (aslots > 4) aslots = 4;
+    }
+  }
+  if (!resident) {
+    aslots = 4;
+    while (aslots > 2 && fixed0 + (size_t)aslots * halo + 4 * (size_t)bstage > limit) --aslots;
+    if (fixed0 + (size_t)aslots * halo + 2 * (size_t)bstage > limit) return pl;
+    slots = (int)((limit - fixed0 - (size_t)aslots * halo) / bstage);
+    if (slots > 8) slots = 8;
+  }
+  const size_t fixed = fixed0 + (size_t)aslots * halo;
+  g.N = N; g.Cin = Cin; g.Win = Win; g.Hin = Hin; g.OHg = OHg; g.OWg = OWg;
+  g.pe = pe; g.r = r; g.Wp = Wp; g.HR = HR;
+  g.T_img = T_img; g.tiles_nn = tiles_nn; g.total = ((N + 1) / 2) * T_img * tiles_nn;
+  g.cblks = cblks; g.ablocks = ablocks; g.KBtot = KBtot; g.resident = resident;
+  g.halo_bytes = halo; g.halo_tx = halo_tx; g.b_stage_bytes = bstage; g.b_slots = slots; g.a_slots = aslots; g.stg_tiles = stg_tiles; g.nbias = nbias;
+  g.Cout = Cout;
+  pl.smem = fixed + (size_t)slots * bstage;
+  pl.ok = true;
+  return pl;
+}
+
+template <int EPI, int NB, int R>
+static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
+                       cudaStream_t st) {
+  static int attr_smem = 0;
+  if ((int)pl.smem > attr_smem) {
+    cudaFuncSetAttribute(conv2_kernel<EPI, NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    attr_smem = (int)pl.smem;
+  }
+  int clusters = tc_num_sms() / 2;
+  if (pl.g.total < clusters) clusters = pl.g.total;
+  conv2_kernel<EPI, NB, R><<<2 * clusters, 256, pl.smem, st>>>(A0, A1, B, pl.g);
+  count_launch();
+  return check_launch("conv2");
+}
+template <int EPI, int NB>
+static int c2_launch(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
+                     cudaStream_t st) {
+  if (pl.g.r == 3) return c2_launch_r<EPI, NB, 3>(A0, A1, B, pl, st);
+  return c2_launch_r<EPI, NB, 0>(A0, A1, B, pl, st);
+}
+
+// fprop / dgrad entry: returns QD_ERR_UNSUPPORTED when the geometry does not
+// fit (the caller then uses the v1 kernel)
+int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
+              int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
+              int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
+              const void* xres, cudaStream_t st) {
+  int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
+  int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
+  C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
+  if (!pl.ok) return QD_ERR_UNSUPPORTED;
+  C2Args& g = pl.g;
+  g.b_rs_tile = b_rs_tile;
+  g.b_rs_blk = b_rs_blk;
+  g.b_contig = (b_rs_blk == 64) ? 1 : 0;
+  if (!g.b_contig && nbk != 2) return QD_ERR_UNSUPPORTED;
+  g.out_c_tile = out_c_tile;
+  {
+    const char* e = getenv("QD_DEBUG");
+    g.dbg = e ? atoi(e) : 0;
+    g.trace = getenv("QD_TRACE") ? trace_buffer() : nullptr;
+  }
+  g.bias0 = bias[0]; g.bias1 = bias[1]; g.bias2 = bias[2];
+  g.out0 = (bf16*)o0; g.out1 = (bf16*)o1; g.out2 = (bf16*)o2;
+  g.xres = (const bf16*)xres;
+  CUtensorMap A0, A1, B;
+  int rc;
+  cuuint64_t dA[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)N};
+  cuuint32_t bA[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.HR, 1};
+  if ((rc = c2_map(&A0, a0, 4, dA, bA))) return rc;
+  if ((rc = c2_map(&A1, a1 ? a1 : a0, 4, dA, bA))) return rc;
+  cuuint64_t dB[2] = {(cuuint64_t)wK, (cuuint64_t)wrows};
+  cuuint32_t bB[2] = {64, (cuuint32_t)(nbk * 32)};
+  if ((rc = c2_map(&B, wmat, 2, dB, bB))) return rc;
+  if (epi == E2_PROPOSED) return c2_launch<E2_PROPOSED, 3>(A0, A1, B, pl, st);
+  if (epi == E2_T4) return c2_launch<E2_T4, 2>(A0, A1, B, pl, st);
+  if (epi == E2_PLAIN) {
+    if (nbk == 4) return c2_launch<E2_PLAIN, 4>(A0, A1, B, pl, st);
+    if (nbk == 2) return c2_launch<E2_PLAIN, 2>(A0, A1, B, pl, st);
+    return c2_launch<E2_PLAIN, 1>(A0, A1, B, pl, st);
+  }
+  if (nbk == 2) return c2_launch<E2_SQ, 2>(A0, A1, B, pl, st);
+  return c2_launch<E2_SQ, 1>(A0, A1, B, pl, st);
+}
+
+
+// ===========================================================================
+// K4 v2: wgrad with halo reuse.
+//   dW^T[(tap, c)][j] = sum_q x_pad[q + off(tap)][c] * D[q][j]
+// over the same padded-flat q of conv2. Per stage: one D box {64 j, Wp, RD}
+// (columns >= OW are out of bounds -> 0, so junk q contribute nothing) and one
+// x halo box {64 c, Wp, RX}. A = x^T (MN-major): M = 128 rows = TWO taps, the
+// second tap's 64-channel atom being the same halo shifted by
+// off(t1) - off(t0) rows (LBO = that shift; overlapping atoms are legal,
+// profiles/r1_probe_lbo_overlap_and_tma_dst.log). B = D (MN-major, N = 64 j).
+// All r*r taps accumulate in one CTA: ceil(r*r/2) accumulators x 64 columns.
+// Output: fp32 split-K partials [S][Jd][Kf], folded by wgrad_finish.
+// ===========================================================================
+struct W2Args {
+  int N, OHg, OWg, Jd, Kf, K0, C;
+  int pe, r, Wp, RD, RX;
+  int T_img, cblks, ablocks, jtiles, splits;
+  uint32_t d_tx, x_tx, d_bytes, x_bytes;
+  int stages;
+  float* part;
+};
+
+__global__ void __launch_bounds__(256, 1)
+    wgrad2_kernel(const __grid_constant__ CUtensorMap mX0, const __grid_constant__ CUtensorMap mX1,
+                  const __grid_constant__ CUtensorMap mD, const W2Args g) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t stage_bytes = g.d_bytes + g.x_bytes;
+  uint64_t* full = (uint64_t*)(sm + g.stages * stage_bytes);
+  uint64_t* empty = full + g.stages;
+  uint64_t* done = empty + g.stages;
+  uint32_t* tslot = (uint32_t*)(done + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  int b = blockIdx.x;
+  const int jt = b % g.jtiles;
+  b /= g.jtiles;
+  const int ab = b % g.ablocks;
+  const int split = b / g.ablocks;
+  const int half = ab / g.cblks, cb = ab % g.cblks;
+  const int nblk = g.N * g.T_img;
+  const int q_beg = (int)((long long)split * nblk / g.splits);
+  const int q_end = (int)((long long)(split + 1) * nblk / g.splits);
+  const int rr = g.r * g.r;
+  const int npairs = (rr + 1) / 2;
+
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(&mX0);
+    ptx::prefetch_tmap(&mX1);
+    ptx::prefetch_tmap(&mD);
+    for (int i = 0; i < g.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(tslot, 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    const bool leader = ptx::elect_one();
+    int st = 0;
+    uint32_t ph = 0;
+    for (int qb = q_beg; qb < q_end; ++qb) {
+      int n = qb / g.T_img, t = qb % g.T_img;
+      int hq_lo = (128 * t) / g.Wp;
+      ptx::mbar_wait(&empty[st], ph ^ 1);
+      if (leader) {
+        uint8_t* s = sm + st * stage_bytes;
+        ptx::mbar_arrive_expect_tx(&full[st], g.d_tx + g.x_tx);
+        ptx::tma_load_4d(&mD, &full[st], s, jt * 64, 0, hq_lo, n);
+        ptx::tma_load_4d(half ? &mX1 : &mX0, &full[st], s + g.d_bytes, cb * 64, -g.pe, hq_lo - g.pe, n);
+      }
+      __syncwarp();
+      if (++st == g.stages) { st = 0; ph ^= 1; }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t IDESC = ptx::idesc_bf16(128, 64, true, true);
+    constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
+    const bool leader = ptx::elect_one();
+    const uint32_t s_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sm), 0);
+    int st = 0;
+    uint32_t ph = 0;
+    uint32_t accum = 0;
+    for (int qb = q_beg; qb < q_end; ++qb) {
+      int t = qb % g.T_img;
+      int q0 = 128 * t;
+      int row_off = q0 - (q0 / g.Wp) * g.Wp;
+      ptx::mbar_wait(&full[st], ph);
+      ptx::tc_fence_after();
+      const uint32_t d_lo = s_lo0 + st * (stage_bytes >> 4) + row_off * 8;
+      const uint32_t x_lo = s_lo0 + st * (stage_bytes >> 4) + (g.d_bytes >> 4) + row_off * 8;
+      if (leader) {
+        for (int p = 0; p < npairs; ++p) {
+          int t0 = 2 * p, t1 = (2 * p + 1 < rr) ? 2 * p + 1 : 2 * p;
+          int o0 = (t0 / g.r) * g.Wp + t0 % g.r, o1 = (t1 / g.r) * g.Wp + t1 % g.r;
+          // A: MN-major, atom 1 = atom 0 shifted by (o1 - o0) rows -> LBO field
+          const uint32_t a_lo = x_lo + o0 * 8 + ((uint32_t)((o1 - o0) * 8) << 16);
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::mma_bf16(tmem + p * 64, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, d_lo + 128 * k),
+                          IDESC, accum | (uint32_t)k);
+        }
+        ptx::mma_commit(&empty[st]);
+      }
+      accum = 1;
+      __syncwarp();
+      if (++st == g.stages) { st = 0; ph ^= 1; }
+    }
+    if (leader) ptx::mma_commit(done);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const bool has_work = q_end > q_beg;
+    if (has_work) {
+      ptx::mbar_wait(done, 0);
+      ptx::tc_fence_after();
+    }
+    float* dst = g.part + (size_t)split * g.Jd * g.Kf;
+    for (int p = 0; p < npairs; ++p) {
+      int tap = row < 64 ? 2 * p : 2 * p + 1;
+      bool ok = tap < rr;
+      int k = half * g.K0 + tap * g.C + cb * 64 + (row & 63);
+#pragma unroll 1
+      for (int c = 0; c < 64; c += 16) {
+        float v[16];
+        if (has_work) {
+          ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + p * 64 + c, v);
+          ptx::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0.f;
+        }
+        if (ok) {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) dst[(size_t)(jt * 64 + c + e) * g.Kf + k] = v[e];
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+struct W2Plan {
+  bool ok;
+  W2Args g;
+  size_t smem;
+};
+
+static W2Plan w2_plan(const Plan& P) {
+  W2Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  W2Args& g = pl.g;
+  if (P.s != 1 || P.r < 2 || P.C % 64 || P.Jd % 64) return pl;
+  int Wp = P.W + 2 * P.p;
+  if (P.OW != Wp - P.r + 1 || Wp > 256 || P.OW < 12) return pl;
+  int T_img = (P.OH * Wp + 127) / 128;
+  int RD = 0;
+  for (int t = 0; t < T_img; ++t) {
+    int q0 = 128 * t, lo = q0 / Wp, hi = (q0 + 127) / Wp;
+    if (hi - lo + 1 > RD) RD = hi - lo + 1;
+  }
+  int RX = RD + P.r - 1;
+  if (RX > 256) return pl;
+  uint32_t d_tx = (uint32_t)Wp * RD * 128, x_tx = (uint32_t)Wp * RX * 128;
+  uint32_t d_bytes = (d_tx + 1023) / 1024 * 1024, x_bytes = (x_tx + 1023) / 1024 * 1024;
+  int stages = (int)((210 * 1024) / (d_bytes + x_bytes));
+  if (stages > 4) stages = 4;
+  if (stages < 2) return pl;
+  if ((P.r * P.r + 1) / 2 * 64 > 512) return pl;
+  g.N = P.N; g.OHg = P.OH; g.OWg = P.OW; g.Jd = P.Jd; g.Kf = P.Kf; g.K0 = P.K0; g.C = P.C;
+  g.pe = P.p; g.r = P.r; g.Wp = Wp; g.RD = RD; g.RX = RX;
+  g.T_img = T_img; g.cblks = P.C / 64; g.ablocks = g.cblks * (P.sq == 2 ? 2 : 1); g.jtiles = P.Jd / 64;
+  int per = g.jtiles * g.ablocks;
+  int S = tc_num_sms() / per;
+  if (S < 1) S = 1;
+  int nblk = P.N * T_img;
+  if (S > nblk) S = nblk;
+  g.splits = S;
+  g.d_tx = d_tx; g.x_tx = x_tx; g.d_bytes = d_bytes; g.x_bytes = x_bytes; g.stages = stages;
+  pl.smem = 1024 + (size_t)stages * (d_bytes + x_bytes) + 1024;
+  pl.ok = true;
+  return pl;
+}
+
+int wgrad2_split(const Plan& P) {
+  W2Plan pl = w2_plan(P);
+  return pl.ok ? pl.g.splits : 0;
+}
+
+int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
+               cudaStream_t st) {
+  W2Plan pl = w2_plan(P);
+  if (!pl.ok || pl.g.splits != splits) return QD_ERR_UNSUPPORTED;
+  W2Args& g = pl.g;
+  g.part = part;
+  CUtensorMap X0, X1, Dm;
+  int rc;
+  cuuint64_t dX[4] = {(cuuint64_t)P.C, (cuuint64_t)P.W, (cuuint64_t)P.H, (cuuint64_t)P.N};
+  cuuint32_t bX[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RX, 1};
+  if ((rc = c2_map(&X0, x0, 4, dX, bX))) return rc;
+  if ((rc = c2_map(&X1, x1 ? x1 : x0, 4, dX, bX))) return rc;
+  cuuint64_t dD[4] = {(cuuint64_t)P.Jd, (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
+  cuuint32_t bD[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RD, 1};
+  if ((rc = c2_map(&Dm, D, 4, dD, bD))) return rc;
+  static int attr = 0;
+  if ((int)pl.smem > attr) {
+    cudaFuncSetAttribute(wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    attr = (int)pl.smem;
+  }
+  wgrad2_kernel<<<g.jtiles * g.ablocks * g.splits, 256, pl.smem, st>>>(X0, X1, Dm, g);
+  count_launch();
+  return check_launch("wgrad2");
+}
+
+}  // namespace qd

@@ -107,6 +107,15 @@ TC_CASES = [
     ("t2_linear", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
     ("t2_linear", "conv", 2, 128, 64, 5, 6, 3, 1, 1),
     ("first_order", "conv", 2, 64, 128, 8, 8, 3, 1, 1),
+    # CTA-pair / halo kernel (conv2): odd batch, streamed B, dual-K, k2/k5
+    ("proposed", "conv", 3, 64, 64, 16, 16, 3, 1, 1),
+    ("proposed", "conv", 2, 128, 128, 14, 20, 3, 1, 1),
+    ("t4", "conv", 4, 64, 64, 16, 16, 3, 1, 1),
+    ("t2", "conv", 2, 64, 64, 16, 16, 3, 1, 1),
+    ("t2_linear", "conv", 2, 64, 64, 16, 16, 3, 1, 1),
+    ("first_order", "conv", 2, 64, 128, 16, 16, 3, 1, 1),
+    ("proposed", "conv", 2, 64, 64, 13, 17, 2, 1, 0),
+    ("proposed", "conv", 2, 64, 64, 12, 12, 5, 1, 2),
     ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
     ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
     ("t2_linear", "fc", 64, 128, 64, 1, 1, 1, 1, 0),
@@ -136,6 +145,21 @@ def test_tcgen05_matches_cuda_core_path(case):
     assert Q.rel_err(r1[4], r0[4]) <= 1e-2
     for role in r1[3]:
         assert Q.rel_err(r1[3][role], r0[3][role]) <= 1e-2, role
+
+
+@pytest.mark.parametrize("case", [c for c in TC_CASES if c[1] == "conv" and c[5] >= 12], ids=str)
+def test_pair_halo_kernel_matches_v1(case):
+    """conv2 (CTA pairs, halo reuse) vs the v1 tcgen05 kernels on identical inputs."""
+    from paper_2204_01701_b200 import _lib
+    fam, kind, n, c, f, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, kind, n, c, f, h, w, k, s, p, seed=13, random_bias=True)
+    xq, gq = _q(x, torch.bfloat16), _q(g, torch.bfloat16)
+    r2 = run_device(fam, kind, xq, P, gq, torch.bfloat16, k, s, p)
+    r1 = run_device(fam, kind, xq, P, gq, torch.bfloat16, k, s, p, flags=_lib.FLAG_TC_V1)
+    for i in (0, 4):
+        assert Q.rel_err(r2[i], r1[i]) <= 1e-2, i
+    for role in r1[3]:
+        assert Q.rel_err(r2[3][role], r1[3][role]) <= 1e-2, role
 
 
 def test_c1_fc_fp32():
