@@ -46,9 +46,16 @@ void launch_bias_finish(const Plan& P, const float* bsum_part, int bs_split,
 // sum the wgrad partials [S][Jd][Kf] and scatter into reference layouts
 void launch_wgrad_finish(const Plan& P, const float* part, int S, float* const dW[3],
                          cudaStream_t st);
+// split-K partial counts of the wgrad rows: rows of tap pair p (tap / 2) have
+// s[p / pp] partials (ng == 0: every row has the uniform count)
+struct WSplits {
+  int pp, ng;
+  int s[16];
+};
+WSplits wgrad2_splits(const Plan& P);
 // tcgen05 path: wgrad partial fold + bias partial fold in one launch (Kf % 4 == 0)
-void launch_bwd_finish(const Plan& P, const float* wpart, int S, float* const dW[3], const float* bpart, int SB,
-                       float* const db[3], cudaStream_t st);
+void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& ws, float* const dW[3],
+                       const float* bpart, int SB, float* const db[3], cudaStream_t st);
 void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st);
 
 // ---- tcgen05 path ----------------------------------------------------------

@@ -439,26 +439,44 @@ int simt_backward(const Plan& P, const void* x, const void* wpack, const void* a
 
 namespace qd {
 // One launch folds both fixed-order reductions of the backward pass:
-// blocks [0, nwb) sum the wgrad split-K partials (4 elements per thread) and
+// blocks [0, nwb) sum the wgrad split-K partials -- 32 float4 columns x 8
+// partial groups per block, combined in a fixed order (deterministic) -- and
 // scatter them into the reference layouts; the rest sum the bias partials.
-__global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __restrict__ wpart, int S,
+__global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __restrict__ wpart, int S, WSplits wsp,
                                                          float* w0, float* w1, float* w2,
                                                          const float* __restrict__ bpart, int SB, float* d0,
                                                          float* d1, float* d2, int nwb) {
+  __shared__ float4 red4[8][33];
+  __shared__ float red[8][33];
+  const int col = threadIdx.x % 32, grp = threadIdx.x / 32;
   if ((int)blockIdx.x < nwb) {
     if (!w0) return;
     const long long total = (long long)P.Jd * P.Kf;
-    long long i4 = ((long long)blockIdx.x * 256 + threadIdx.x) * 4;
-    if (i4 >= total) return;
-    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-    const float4* src = reinterpret_cast<const float4*>(wpart + i4);
-    const long long stride4 = total / 4;
-#pragma unroll 4
-    for (int s = 0; s < S; ++s) {
-      float4 v = __ldg(src + s * stride4);
-      acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+    const long long i4 = ((long long)blockIdx.x * 32 + col) * 4;
+    int Sk = S;
+    if (i4 < total && wsp.ng > 0) {
+      int k = (int)(i4 % P.Kf), kk = k % P.K0;
+      int tap = kk / P.C;
+      Sk = wsp.s[(tap / 2) / wsp.pp];
     }
-    float av[4] = {acc.x, acc.y, acc.z, acc.w};
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i4 < total) {
+      const float4* src = reinterpret_cast<const float4*>(wpart + i4);
+      const long long stride4 = total / 4;
+      for (int s = grp; s < Sk; s += 8) {
+        float4 v = __ldg(src + s * stride4);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+    }
+    red4[grp][col] = acc;
+    __syncthreads();
+    if (grp != 0 || i4 >= total) return;
+    float4 t = red4[0][col];
+    for (int gq = 1; gq < 8; ++gq) {
+      float4 v = red4[gq][col];
+      t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+    }
+    float av[4] = {t.x, t.y, t.z, t.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       long long i = i4 + e;
@@ -474,8 +492,6 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
     }
   } else {
     if (P.nbias == 0 || !d0) return;
-    __shared__ float red[8][33];
-    int col = threadIdx.x % 32, grp = threadIdx.x / 32;
     int j = ((int)blockIdx.x - nwb) * 32 + col;
     float acc = 0.f;
     if (j < P.Jd)
@@ -492,14 +508,14 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
   }
 }
 
-void launch_bwd_finish(const Plan& P, const float* wpart, int S, float* const dW[3], const float* bpart, int SB,
-                       float* const db[3], cudaStream_t st) {
+void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& ws, float* const dW[3],
+                       const float* bpart, int SB, float* const db[3], cudaStream_t st) {
   long long total = (long long)P.Jd * P.Kf;  // Kf is a multiple of 64 on the tcgen05 path
-  int nwb = dW[0] ? (int)((total / 4 + 255) / 256) : 0;
+  int nwb = dW[0] ? (int)((total / 4 + 31) / 32) : 0;
   int nbb = (P.nbias && db[0]) ? (P.Jd + 31) / 32 : 0;
   if (nwb + nbb == 0) return;
-  bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1], db[2],
-                                                nwb);
+  bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
+                                                db[2], nwb);
   count_launch();
 }
 }  // namespace qd

@@ -799,7 +799,7 @@ int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
     if (!(P.flags & QD_FLAG_TC_V1) && wgrad2_split(P) == L.wg_split)
       rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st);
     if (rc == QD_OK) {
-      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, dW, bpart, L.bs_split, db, st);
+      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wgrad2_splits(P), dW, bpart, L.bs_split, db, st);
     } else if (rc != QD_ERR_UNSUPPORTED) {
       return rc;
     } else {
@@ -825,7 +825,9 @@ int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
     else if (nblk == 2) rc = launch_wgrad<2>(X0, X1, Dm, g, st);
     else rc = launch_wgrad<1>(X0, X1, Dm, g, st);
     if (rc) return rc;
-    launch_bwd_finish(P, g.part, g.splits, dW, bpart, L.bs_split, db, st);
+    WSplits uni;
+    memset(&uni, 0, sizeof(uni));
+    launch_bwd_finish(P, g.part, g.splits, uni, dW, bpart, L.bs_split, db, st);
     }
   } else if (db[0] && (mat || P.nbias)) {
     launch_bias_finish(P, bpart, L.bs_split, db, st);

@@ -139,12 +139,21 @@ __device__ __forceinline__ void c2_store_pass(const C2Args& g, const uint8_t* st
   }
 }
 
+template <int EPI, int NB>
+struct C2Threads {
+  static constexpr int NPASS = (EPI == E2_PROPOSED || EPI == E2_T4) ? 3 : (EPI == E2_PLAIN ? NB : 1);
+  // proposed / t4: two epilogue warpgroups (y | a, b) run concurrently
+  static constexpr int NEPI = NPASS == 3 ? 8 : 4;
+  static constexpr int THREADS = 128 + NEPI * 32;
+};
+
 template <int EPI, int NB, int R>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::THREADS, 1)
     conv2_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
                  const __grid_constant__ CUtensorMap mB, const C2Args g) {
   // output "passes": proposed/t4 write y, a, b; plain writes NB 64-channel blocks
-  constexpr int NPASS = (EPI == E2_PROPOSED || EPI == E2_T4) ? 3 : (EPI == E2_PLAIN ? NB : 1);
+  constexpr int NPASS = C2Threads<EPI, NB>::NPASS;
+  constexpr int NEPI = C2Threads<EPI, NB>::NEPI;
   constexpr int ACC = NB * 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -177,7 +186,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 8);
+      ptx::mbar_init(&tempty[i], 2 * NEPI);
     }
     ptx::mbar_init(bres, 1);
     for (int i = 0; i < g.b_slots; ++i) {
@@ -350,18 +359,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     // ===== epilogue (both CTAs, own TMEM rows); one 4 KB staging tile per warp,
     // one output pass at a time =====
     const int q = warp & 3;
+    const int eg = (warp - 4) >> 2;  // epilogue warpgroup
     {
       // every bias of the layer into smem once; read back as float4 broadcasts
       const int et = threadIdx.x - 128;
-      for (int i = et; i < g.nbias * g.Cout; i += 128) {
+      for (int i = et; i < g.nbias * g.Cout; i += NEPI * 32) {
         int role = i / g.Cout, c = i - role * g.Cout;
         const float* src = role == 0 ? g.bias0 : (role == 1 ? g.bias1 : g.bias2);
         sBias[i] = __ldg(src + c);
       }
-      ptx::named_bar_sync(1, 128);
+      ptx::named_bar_sync(1, NEPI * 32);
     }
-    uint8_t* stg = sStg + q * g.stg_tiles * 4096;
-    const bool multi = g.stg_tiles > 1;
+    // passes of this warp: with two warpgroups, group 0 writes y and group 1 a, b
+    const int o_beg = NEPI == 8 ? (eg == 0 ? 0 : 1) : 0;
+    const int o_end = NEPI == 8 ? (eg == 0 ? 1 : 3) : NPASS;
+    uint8_t* stg = NEPI == 8 ? sStg + (eg == 0 ? q * 4096 : 16384 + q * 8192) : sStg + q * g.stg_tiles * 4096;
+    const bool multi = NEPI == 8 ? (o_end - o_beg > 1) : g.stg_tiles > 1;
+    const bool tracer = q == 0 && eg == 0 && lane == 0;
     const uint32_t tempty0 = c2::peer0(&tempty[0]);
     int it = 0;
     for (int w = cluster; w < g.total; w += nclusters, ++it) {
@@ -375,9 +389,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       bool valid = n < g.N && hq < g.OHg && wq < g.OWg;
       int pix = valid ? (n * g.OHg + hq) * g.OWg + wq : -1;
       const int c_base = j * g.out_c_tile;
-      if (q == 0 && lane == 0) C2_TRACE(2, it, 0);
+      if (tracer) C2_TRACE(2, it, 0);
       ptx::mbar_wait(&tfull[acs], tph);
-      if (q == 0 && lane == 0) C2_TRACE(2, it, 1);
+      if (tracer) C2_TRACE(2, it, 1);
       ptx::tc_fence_after();
       if (g.dbg & 1) {
         __syncwarp();
@@ -386,7 +400,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       }
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acs * ACC;
 #pragma unroll 1
-      for (int o = 0; o < NPASS; ++o) {
+      for (int o = o_beg; o < o_end; ++o) {
 #pragma unroll 1
         for (int jj = 0; jj < 4; ++jj) {
           float out[16];
@@ -478,30 +492,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
               if (NB == 2) out[e] += v1[e];
             }
           }
-          c2::stage16(stg + (multi ? o * 4096 : 0), lane, jj, out);
+          c2::stage16(stg + (multi ? (o - o_beg) * 4096 : 0), lane, jj, out);
         }
-        if (q == 0 && lane == 0) C2_TRACE(2, it, 4 + 2 * o);
-        if (o == NPASS - 1) {
+        if (tracer) C2_TRACE(2, it, 4 + 2 * o);
+        if (o == o_end - 1) {
           // every TMEM read of this tile is done -> hand the accumulator back
           ptx::tc_fence_before();
           __syncwarp();
           if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
-          if (q == 0 && lane == 0) C2_TRACE(2, it, 2);
+          if (tracer) C2_TRACE(2, it, 2);
         }
         if (!multi) {
           __syncwarp();
           c2_store_pass<EPI>(g, stg, o, c_base, pix, lane);
           __syncwarp();
-          if (q == 0 && lane == 0) C2_TRACE(2, it, 5 + 2 * o);
+          if (tracer) C2_TRACE(2, it, 5 + 2 * o);
         }
       }
       if (multi) {
         __syncwarp();
 #pragma unroll 1
-        for (int o = 0; o < NPASS; ++o) c2_store_pass<EPI>(g, stg + o * 4096, o, c_base, pix, lane);
+        for (int o = o_beg; o < o_end; ++o) c2_store_pass<EPI>(g, stg + (o - o_beg) * 4096, o, c_base, pix, lane);
         __syncwarp();
       }
-      if (q == 0 && lane == 0) C2_TRACE(2, it, 3);
+      if (tracer) C2_TRACE(2, it, 3);
     }
   }
   ptx::tc_fence_before();
@@ -583,7 +597,7 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   int stg_tiles = NOUT;
   {
     const char* e = getenv("QD_C2_STG");
-    if (e) stg_tiles = atoi(e) > 1 ? NOUT : 1;
+    if (e && NOUT != 3) stg_tiles = atoi(e) > 1 ? NOUT : 1;
   }
   const size_t bias_bytes = (size_t)nbias * Cout * 4;
   const size_t fixed0 = 1024 + 4 * (size_t)stg_tiles * 4096 + bias_bytes + 1024;  // slack, staging, biases, barriers
@@ -628,7 +642,7 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   }
   int clusters = tc_num_sms() / 2;
   if (pl.g.total < clusters) clusters = pl.g.total;
-  conv2_kernel<EPI, NB, R><<<2 * clusters, 256, pl.smem, st>>>(A0, A1, B, pl.g);
+  conv2_kernel<EPI, NB, R><<<2 * clusters, C2Threads<EPI, NB>::THREADS, pl.smem, st>>>(A0, A1, B, pl.g);
   count_launch();
   return check_launch("conv2");
 }
@@ -700,9 +714,14 @@ struct W2Args {
   int N, OHg, OWg, Jd, Kf, K0, C;
   int pe, r, Wp, RD, RX;
   int T_img, cblks, ablocks, jtiles, splits;
-  uint32_t d_tx, x_tx, d_bytes, x_bytes;
+  int NT, ntb;          // N tile (j) width and its 64-wide boxes
+  int npairs, pp, tgroups;  // tap pairs, pairs per CTA (TMEM: pp * NT <= 512), tap groups
+  int gsplit[16];           // split-K count per tap group (weighted by its pairs)
+  int gstart[17];           // prefix sums of gsplit
+  uint32_t d_tx, x_tx, d_bytes, x_bytes;  // d_* per 64-j box
   int stages;
   float* part;
+  unsigned long long* trace;  // QD_TRACE (dev only)
 };
 
 __global__ void __launch_bounds__(256, 1)
@@ -710,7 +729,7 @@ __global__ void __launch_bounds__(256, 1)
                   const __grid_constant__ CUtensorMap mD, const W2Args g) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-  const uint32_t stage_bytes = g.d_bytes + g.x_bytes;
+  const uint32_t stage_bytes = g.ntb * g.d_bytes + g.x_bytes;
   uint64_t* full = (uint64_t*)(sm + g.stages * stage_bytes);
   uint64_t* empty = full + g.stages;
   uint64_t* done = empty + g.stages;
@@ -720,13 +739,18 @@ __global__ void __launch_bounds__(256, 1)
   const int jt = b % g.jtiles;
   b /= g.jtiles;
   const int ab = b % g.ablocks;
-  const int split = b / g.ablocks;
+  b /= g.ablocks;
+  int tg = 0;
+  while (tg + 1 < g.tgroups && b >= g.gstart[tg + 1]) ++tg;
+  const int split = b - g.gstart[tg];
+  const int gs = g.gsplit[tg];
   const int half = ab / g.cblks, cb = ab % g.cblks;
   const int nblk = g.N * g.T_img;
-  const int q_beg = (int)((long long)split * nblk / g.splits);
-  const int q_end = (int)((long long)(split + 1) * nblk / g.splits);
+  const int q_beg = (int)((long long)split * nblk / gs);
+  const int q_end = (int)((long long)(split + 1) * nblk / gs);
   const int rr = g.r * g.r;
-  const int npairs = (rr + 1) / 2;
+  const int p_beg = tg * g.pp;
+  const int p_end = min(g.npairs, p_beg + g.pp);
 
   if (threadIdx.x == 0) {
     ptx::prefetch_tmap(&mX0);
@@ -755,21 +779,27 @@ __global__ void __launch_bounds__(256, 1)
     for (int qb = q_beg; qb < q_end; ++qb) {
       int n = qb / g.T_img, t = qb % g.T_img;
       int hq_lo = (128 * t) / g.Wp;
+      if (leader) C2_TRACE(0, qb - q_beg, 0);
       ptx::mbar_wait(&empty[st], ph ^ 1);
       if (leader) {
+        C2_TRACE(0, qb - q_beg, 1);
         uint8_t* s = sm + st * stage_bytes;
-        ptx::mbar_arrive_expect_tx(&full[st], g.d_tx + g.x_tx);
-        ptx::tma_load_4d(&mD, &full[st], s, jt * 64, 0, hq_lo, n);
-        ptx::tma_load_4d(half ? &mX1 : &mX0, &full[st], s + g.d_bytes, cb * 64, -g.pe, hq_lo - g.pe, n);
+        ptx::mbar_arrive_expect_tx(&full[st], g.ntb * g.d_tx + g.x_tx);
+        for (int i = 0; i < g.ntb; ++i)
+          ptx::tma_load_4d(&mD, &full[st], s + i * g.d_bytes, (jt * g.ntb + i) * 64, 0, hq_lo, n);
+        ptx::tma_load_4d(half ? &mX1 : &mX0, &full[st], s + g.ntb * g.d_bytes, cb * 64, -g.pe, hq_lo - g.pe, n);
       }
       __syncwarp();
       if (++st == g.stages) { st = 0; ph ^= 1; }
     }
   } else if (warp == 1) {
-    constexpr uint32_t IDESC = ptx::idesc_bf16(128, 64, true, true);
+    // B = D (MN-major, N = NT j over ntb atoms g.d_bytes apart); A = x^T, M = two
+    // taps as two 64-channel atoms of the same halo, LBO = their row shift
+    const uint32_t IDESC = ptx::idesc_bf16(128, g.NT, true, true);
     constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
     const bool leader = ptx::elect_one();
     const uint32_t s_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sm), 0);
+    const uint32_t d_lbo = (g.d_bytes >> 4) << 16;
     int st = 0;
     uint32_t ph = 0;
     uint32_t accum = 0;
@@ -777,22 +807,25 @@ __global__ void __launch_bounds__(256, 1)
       int t = qb % g.T_img;
       int q0 = 128 * t;
       int row_off = q0 - (q0 / g.Wp) * g.Wp;
+      if (leader) C2_TRACE(1, qb - q_beg, 0);
       ptx::mbar_wait(&full[st], ph);
+      if (leader) C2_TRACE(1, qb - q_beg, 1);
       ptx::tc_fence_after();
-      const uint32_t d_lo = s_lo0 + st * (stage_bytes >> 4) + row_off * 8;
-      const uint32_t x_lo = s_lo0 + st * (stage_bytes >> 4) + (g.d_bytes >> 4) + row_off * 8;
+      const uint32_t d_lo = s_lo0 + st * (stage_bytes >> 4) + row_off * 8 + d_lbo;
+      const uint32_t x_lo = s_lo0 + st * (stage_bytes >> 4) + ((g.ntb * g.d_bytes) >> 4) + row_off * 8;
       if (leader) {
-        for (int p = 0; p < npairs; ++p) {
+        for (int p = p_beg; p < p_end; ++p) {
           int t0 = 2 * p, t1 = (2 * p + 1 < rr) ? 2 * p + 1 : 2 * p;
           int o0 = (t0 / g.r) * g.Wp + t0 % g.r, o1 = (t1 / g.r) * g.Wp + t1 % g.r;
-          // A: MN-major, atom 1 = atom 0 shifted by (o1 - o0) rows -> LBO field
           const uint32_t a_lo = x_lo + o0 * 8 + ((uint32_t)((o1 - o0) * 8) << 16);
+          const uint32_t dt = tmem + (p - p_beg) * g.NT;
 #pragma unroll
           for (int k = 0; k < 8; ++k)
-            ptx::mma_bf16(tmem + p * 64, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, d_lo + 128 * k),
-                          IDESC, accum | (uint32_t)k);
+            ptx::mma_bf16(dt, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, d_lo + 128 * k), IDESC,
+                          accum | (uint32_t)k);
         }
         ptx::mma_commit(&empty[st]);
+        C2_TRACE(1, qb - q_beg, 2);
       }
       accum = 1;
       __syncwarp();
@@ -809,15 +842,15 @@ __global__ void __launch_bounds__(256, 1)
       ptx::tc_fence_after();
     }
     float* dst = g.part + (size_t)split * g.Jd * g.Kf;
-    for (int p = 0; p < npairs; ++p) {
+    for (int p = p_beg; p < p_end; ++p) {
       int tap = row < 64 ? 2 * p : 2 * p + 1;
       bool ok = tap < rr;
       int k = half * g.K0 + tap * g.C + cb * 64 + (row & 63);
 #pragma unroll 1
-      for (int c = 0; c < 64; c += 16) {
+      for (int c = 0; c < g.NT; c += 16) {
         float v[16];
         if (has_work) {
-          ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + p * 64 + c, v);
+          ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + (p - p_beg) * g.NT + c, v);
           ptx::tmem_wait_ld();
         } else {
 #pragma unroll
@@ -825,7 +858,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         if (ok) {
 #pragma unroll
-          for (int e = 0; e < 16; ++e) dst[(size_t)(jt * 64 + c + e) * g.Kf + k] = v[e];
+          for (int e = 0; e < 16; ++e) dst[(size_t)(jt * g.NT + c + e) * g.Kf + k] = v[e];
         }
       }
     }
@@ -857,25 +890,60 @@ static W2Plan w2_plan(const Plan& P) {
     int q0 = 128 * t, lo = q0 / Wp, hi = (q0 + 127) / Wp;
     if (hi - lo + 1 > RD) RD = hi - lo + 1;
   }
-  int RX = RD + P.r - 1;
+  int RX = 0;  // x halo rows: q0 .. q0 + 127 + (r-1)(Wp+1)
+  for (int t = 0; t < T_img; ++t) {
+    int q0 = 128 * t, lo = q0 / Wp, hi = (q0 + 127 + (P.r - 1) * (Wp + 1)) / Wp;
+    if (hi - lo + 1 > RX) RX = hi - lo + 1;
+  }
   if (RX > 256) return pl;
+  // N tile: widest multiple of 64 <= 256 that divides Jd (192 for proposed F = 64)
+  int ntb = 1;
+  for (int c = 4; c >= 1; --c)
+    if ((P.Jd / 64) % c == 0) { ntb = c; break; }
+  const int NT = ntb * 64;
+  const int npairs = (P.r * P.r + 1) / 2;
+  int pp = 512 / NT;
+  if (pp > npairs) pp = npairs;
+  const int tgroups = (npairs + pp - 1) / pp;
   uint32_t d_tx = (uint32_t)Wp * RD * 128, x_tx = (uint32_t)Wp * RX * 128;
   uint32_t d_bytes = (d_tx + 1023) / 1024 * 1024, x_bytes = (x_tx + 1023) / 1024 * 1024;
-  int stages = (int)((210 * 1024) / (d_bytes + x_bytes));
+  uint32_t stage = ntb * d_bytes + x_bytes;
+  int stages = (int)((212 * 1024) / stage);
   if (stages > 4) stages = 4;
   if (stages < 2) return pl;
-  if ((P.r * P.r + 1) / 2 * 64 > 512) return pl;
   g.N = P.N; g.OHg = P.OH; g.OWg = P.OW; g.Jd = P.Jd; g.Kf = P.Kf; g.K0 = P.K0; g.C = P.C;
   g.pe = P.p; g.r = P.r; g.Wp = Wp; g.RD = RD; g.RX = RX;
-  g.T_img = T_img; g.cblks = P.C / 64; g.ablocks = g.cblks * (P.sq == 2 ? 2 : 1); g.jtiles = P.Jd / 64;
-  int per = g.jtiles * g.ablocks;
-  int S = tc_num_sms() / per;
-  if (S < 1) S = 1;
+  g.T_img = T_img; g.cblks = P.C / 64; g.ablocks = g.cblks * (P.sq == 2 ? 2 : 1); g.jtiles = P.Jd / NT;
+  g.NT = NT; g.ntb = ntb; g.npairs = npairs; g.pp = pp; g.tgroups = tgroups;
+  if (tgroups > 16) return pl;
+  // CTA budget per (j tile, channel block), shared among tap groups by their pair count
+  int budget = tc_num_sms() / (g.jtiles * g.ablocks);
+  if (budget < tgroups) budget = tgroups;
   int nblk = P.N * T_img;
-  if (S > nblk) S = nblk;
-  g.splits = S;
+  // per-q-block cost of a group ~ max(MMA issue, TMA fill): traced at ~NT/2 cycles per
+  // M128 MMA (+~400 loop) and ~64 B/cycle of TMA per SM
+  const double tma_cyc = (double)(ntb * d_bytes + x_bytes) / 64.0;
+  double wsum = 0, wg[16];
+  for (int t = 0; t < tgroups; ++t) {
+    int pg = min(pp, npairs - t * pp);
+    double mma_cyc = pg * 8 * (NT / 2.0) + 400.0;
+    wg[t] = mma_cyc > tma_cyc ? mma_cyc : tma_cyc;
+    wsum += wg[t];
+  }
+  int smax = 1, tot = 0;
+  for (int t = 0; t < tgroups; ++t) {
+    int sg = (int)(budget * wg[t] / wsum);
+    if (sg < 1) sg = 1;
+    if (sg > nblk) sg = nblk;
+    g.gsplit[t] = sg;
+    g.gstart[t] = tot;
+    tot += sg;
+    if (sg > smax) smax = sg;
+  }
+  g.gstart[tgroups] = tot;
+  g.splits = smax;  // partial slots; rows of group t use slots [0, gsplit[t])
   g.d_tx = d_tx; g.x_tx = x_tx; g.d_bytes = d_bytes; g.x_bytes = x_bytes; g.stages = stages;
-  pl.smem = 1024 + (size_t)stages * (d_bytes + x_bytes) + 1024;
+  pl.smem = 1024 + (size_t)stages * stage + 1024;
   pl.ok = true;
   return pl;
 }
@@ -885,12 +953,24 @@ int wgrad2_split(const Plan& P) {
   return pl.ok ? pl.g.splits : 0;
 }
 
+WSplits wgrad2_splits(const Plan& P) {
+  W2Plan pl = w2_plan(P);
+  WSplits w;
+  memset(&w, 0, sizeof(w));
+  if (!pl.ok) return w;
+  w.pp = pl.g.pp;
+  w.ng = pl.g.tgroups;
+  for (int t = 0; t < w.ng; ++t) w.s[t] = pl.g.gsplit[t];
+  return w;
+}
+
 int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st) {
   W2Plan pl = w2_plan(P);
   if (!pl.ok || pl.g.splits != splits) return QD_ERR_UNSUPPORTED;
   W2Args& g = pl.g;
   g.part = part;
+  g.trace = getenv("QD_TRACE") ? trace_buffer() : nullptr;
   CUtensorMap X0, X1, Dm;
   int rc;
   cuuint64_t dX[4] = {(cuuint64_t)P.C, (cuuint64_t)P.W, (cuuint64_t)P.H, (cuuint64_t)P.N};
@@ -905,7 +985,7 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cudaFuncSetAttribute(wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr = (int)pl.smem;
   }
-  wgrad2_kernel<<<g.jtiles * g.ablocks * g.splits, 256, pl.smem, st>>>(X0, X1, Dm, g);
+  wgrad2_kernel<<<g.jtiles * g.ablocks * g.gstart[g.tgroups], 256, pl.smem, st>>>(X0, X1, Dm, g);
   count_launch();
   return check_launch("wgrad2");
 }
