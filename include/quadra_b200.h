@@ -120,6 +120,16 @@ const char* qd_last_error(void); /* detail of the last failure (thread-local) */
  * it as gpu_launches). */
 unsigned long long qd_launch_count(void);
 
+/* Per-kernel timing for benchmarks: with profiling on, the library records a
+ * CUDA event on the launching stream after each of its kernels (also inside
+ * CUDA-graph capture). qd_profile_mark records a start mark; qd_profile_read(i)
+ * returns the name of the i-th mark and the ms since mark i-1 (i >= 1; the
+ * caller synchronises first). */
+int qd_profile(int enable);
+int qd_profile_mark(void* stream);
+int qd_profile_count(void);
+int qd_profile_read(int i, const char** name, float* ms);
+
 /* Library version string. */
 const char* qd_version(void);
 

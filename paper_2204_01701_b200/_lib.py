@@ -25,7 +25,8 @@ FLAG_NO_DX, FLAG_FORCE_SIMT, FLAG_NO_DW, FLAG_TC_V1 = 1, 2, 4, 8
 
 EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_pack_weights", "qd_forward", "qd_backward", "qd_path",
-           "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version")
+           "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version",
+           "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read")
 
 
 class QdDesc(ctypes.Structure):
@@ -82,6 +83,14 @@ def load():
         lib.qd_launch_count.restype = ctypes.c_ulonglong
         lib.qd_version.argtypes = []
         lib.qd_version.restype = ctypes.c_char_p
+        lib.qd_profile.argtypes = [ctypes.c_int]
+        lib.qd_profile.restype = ctypes.c_int
+        lib.qd_profile_mark.argtypes = [vp]
+        lib.qd_profile_mark.restype = ctypes.c_int
+        lib.qd_profile_count.argtypes = []
+        lib.qd_profile_count.restype = ctypes.c_int
+        lib.qd_profile_read.argtypes = [ctypes.c_int, P(ctypes.c_char_p), P(ctypes.c_float)]
+        lib.qd_profile_read.restype = ctypes.c_int
         _lib = lib
         return lib
 
@@ -112,3 +121,15 @@ def ptr3(*ptrs):
 
 def launch_count():
     return int(load().qd_launch_count())
+
+
+def profile_read():
+    """[(kernel name, ms)] since the last qd_profile(1) (caller synchronises)."""
+    lib = load()
+    out = []
+    for i in range(1, lib.qd_profile_count()):
+        nm = ctypes.c_char_p()
+        ms = ctypes.c_float()
+        raise_for(lib.qd_profile_read(i, ctypes.byref(nm), ctypes.byref(ms)), "qd_profile_read")
+        out.append((nm.value.decode(), ms.value))
+    return out

@@ -6,6 +6,7 @@
 #include <stdio.h>
 #include <string.h>
 #include <atomic>
+#include <vector>
 #include "qd_kernels.h"
 
 namespace qd {
@@ -13,7 +14,34 @@ namespace qd {
 static std::atomic<unsigned long long> g_launches{0};
 static thread_local char g_err[512] = "";
 
-void count_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+// ---- lightweight per-kernel profiling (bench.py roofline): an event after each
+// launch of ours, recorded on the launching stream (capturable into graphs) ----
+static bool g_prof = false;
+static std::vector<cudaEvent_t> g_prof_ev;
+static std::vector<const char*> g_prof_name;
+static size_t g_prof_used = 0;
+
+static void prof_mark(cudaStream_t st, const char* name) {
+  if (g_prof_used == g_prof_ev.size()) {
+    cudaEvent_t e;
+    if (cudaEventCreate(&e) != cudaSuccess) return;
+    g_prof_ev.push_back(e);
+    g_prof_name.push_back(name);
+  }
+  g_prof_name[g_prof_used] = name;
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(st, &cs);
+  if (cs == cudaStreamCaptureStatusActive)  // becomes an event-record node that fires on replay
+    cudaEventRecordWithFlags(g_prof_ev[g_prof_used], st, cudaEventRecordExternal);
+  else
+    cudaEventRecord(g_prof_ev[g_prof_used], st);
+  ++g_prof_used;
+}
+
+void count_launch(cudaStream_t st, const char* name) {
+  g_launches.fetch_add(1ull, std::memory_order_relaxed);
+  if (g_prof) prof_mark(st, name);
+}
 
 int set_error(int status, const char* fmt, ...) {
   va_list ap;
@@ -39,7 +67,9 @@ Workspace plan_workspace(const Plan& P, int path) {
     size_t a = (size_t)P.Mout * P.nb * P.F, b = (size_t)P.Min * P.Cd;
     L.sz_P = (a > b ? a : b) * 4;
   }
-  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4) L.sz_D = (size_t)P.Mout * P.Jd * es;
+  // stride-2 layers on the tcgen05 path run their backward on the stride-1 grid
+  const Plan Pg = (path == 1 && P.s == 2) ? stride1_plan(P) : P;
+  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4 || Pg.s != P.s) L.sz_D = (size_t)Pg.Mout * P.Jd * es;
   if (path == 0) {
     long long tiles = (long long)((P.Jd + 63) / 64) * ((P.Kf + 63) / 64);
     long long S = (2 * 148 + tiles - 1) / tiles;
@@ -49,10 +79,10 @@ Workspace plan_workspace(const Plan& P, int path) {
     if (S < 1) S = 1;
     L.wg_split = (int)S;
   } else {
-    L.wg_split = tc_wgrad_split(P);
+    L.wg_split = tc_wgrad_split(Pg);
   }
   L.sz_WG = (size_t)L.wg_split * P.Jd * P.Kf * 4;
-  long long bs = (P.Mout + 255) / 256;
+  long long bs = (Pg.Mout + 255) / 256;
   if (bs > 2 * 148) bs = 2 * 148;
   if (bs < 1) bs = 1;
   L.bs_split = (int)bs;
@@ -204,6 +234,29 @@ const char* qd_error_string(int status) {
 const char* qd_last_error(void) { return g_err; }
 
 unsigned long long qd_launch_count(void) { return g_launches.load(); }
+
+int qd_profile(int enable) {
+  g_prof = enable != 0;
+  if (g_prof) g_prof_used = 0;
+  return QD_OK;
+}
+
+int qd_profile_mark(void* stream) {
+  if (g_prof) prof_mark((cudaStream_t)stream, "begin");
+  return QD_OK;
+}
+
+int qd_profile_count(void) { return (int)g_prof_used; }
+
+int qd_profile_read(int i, const char** name, float* ms) {
+  if (i <= 0 || (size_t)i >= g_prof_used) return QD_ERR_ARG;
+  if (name) *name = g_prof_name[i];
+  float t = 0.f;
+  cudaError_t e = cudaEventElapsedTime(&t, g_prof_ev[i - 1], g_prof_ev[i]);
+  if (e != cudaSuccess) return set_error(QD_ERR_CUDA, "qd_profile_read: %s", cudaGetErrorString(e));
+  if (ms) *ms = t;
+  return QD_OK;
+}
 
 const char* qd_version(void) { return "quadra_b200 0.1.0 (sm_100a)"; }
 

@@ -7,7 +7,8 @@
 namespace qd {
 
 // ---- bookkeeping -----------------------------------------------------------
-void count_launch(int n = 1);
+// counts a launch of ours on `st`; with profiling on, also records a timing event
+void count_launch(cudaStream_t st, const char* name);
 int set_error(int status, const char* fmt, ...);
 int check_launch(const char* what);
 
@@ -69,7 +70,19 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st);
+              const void* xres, cudaStream_t st, int ss = 1);
+bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
+                int tiles_nn, int Cout, int nbias);
+// stride-2 layers run as their stride-1 equivalent: forward subsamples the
+// output, backward uses the zero-upsampled gradient operand
+inline Plan stride1_plan(const Plan& P) {
+  Plan Q = P;
+  Q.s = 1;
+  Q.OH = P.H + 2 * P.p - P.r + 1;
+  Q.OW = P.W + 2 * P.p - P.r + 1;
+  Q.Mout = (long long)P.N * Q.OH * Q.OW;
+  return Q;
+}
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3],
                void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st);
 // dW[0] == nullptr skips the weight/bias gradient GEMM (QD_FLAG_NO_DW)

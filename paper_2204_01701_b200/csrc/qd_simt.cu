@@ -68,7 +68,7 @@ void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream
     pack_all_kernel<bf16><<<blocks, 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack);
   else
     pack_all_kernel<float><<<blocks, 256, 0, st>>>(P, w[0], w[1], w[2], (float*)wpack);
-  count_launch();
+  count_launch(st, "pack");
 }
 
 // ---------------------------------------------------------------------------
@@ -137,7 +137,7 @@ static void simt_gemm(LA la, LB lb, int M, int N, long long K, int split, float*
   kper = (kper + SG_BK - 1) / SG_BK * SG_BK;
   dim3 grid((M + SG_BM - 1) / SG_BM, (N + SG_BN - 1) / SG_BN, split);
   simt_gemm_kernel<<<grid, 256, 0, st>>>(la, lb, M, N, K, kper, out);
-  count_launch();
+  count_launch(st, "simt_gemm");
 }
 
 // fprop A: implicit im2col of x (optionally squared), m = output pixel
@@ -274,7 +274,7 @@ void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const voi
   else
     bwd_prologue_kernel<float><<<split, threads, 0, st>>>(P, (const float*)dy, (const float*)a,
                                                           (const float*)b, (float*)D, part, rows_per);
-  count_launch();
+  count_launch(st, "prologue_simt");
 }
 
 // bias gradient per role: proposed ba <- sum(dy*b) (block 0), bb <- sum(dy*a)
@@ -303,7 +303,7 @@ __global__ void __launch_bounds__(256) bias_finish_kernel(Plan P, const float* p
 void launch_bias_finish(const Plan& P, const float* part, int S, float* const db[3], cudaStream_t st) {
   if (P.nbias == 0) return;
   bias_finish_kernel<<<(P.Jd + 31) / 32, 256, 0, st>>>(P, part, S, db[0], db[1], db[2]);
-  count_launch();
+  count_launch(st, "bias_finish");
 }
 
 // wgrad partials [S][Jd][Kf] -> reference layouts
@@ -328,7 +328,7 @@ __global__ void wgrad_finish_kernel(Plan P, const float* part, int S, float* w0,
 void launch_wgrad_finish(const Plan& P, const float* part, int S, float* const dW[3], cudaStream_t st) {
   long long total = (long long)P.Jd * P.Kf;
   wgrad_finish_kernel<<<grid_for(total), 256, 0, st>>>(P, part, S, dW[0], dW[1], dW[2]);
-  count_launch();
+  count_launch(st, "wgrad_finish");
 }
 
 template <typename T>
@@ -344,7 +344,7 @@ void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st) {
   long long n = P.Min * P.C;
   if (P.dtype == QD_BF16) square_kernel<bf16><<<grid_for(n), 256, 0, st>>>((const bf16*)x, (bf16*)xs, n);
   else square_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)x, (float*)xs, n);
-  count_launch();
+  count_launch(st, "square");
 }
 
 // dgrad epilogue: dx = Q (first_order/t4/proposed), 2 x Q (t2),
@@ -379,7 +379,7 @@ static int simt_forward_t(const Plan& P, const T* x, const T* wf, const float* c
   simt_gemm(la, lb, (int)P.Mout, P.nb * P.F, P.Kf, 1, G, st);
   long long total = P.Mout * P.F;
   fwd_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, G, bias[0], bias[1], bias[2], y, a, b);
-  count_launch();
+  count_launch(st, "fwd_epilogue_simt");
   return check_launch("simt forward");
 }
 
@@ -417,7 +417,7 @@ static int simt_backward_t(const Plan& P, const T* x, const T* wpack, const T* a
     simt_gemm(da, dbm, (int)P.Min, P.Cd, P.Kd, 1, Q, st);
     long long total = P.Min * P.C;
     dgrad_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, Q, x, dx);
-    count_launch();
+    count_launch(st, "dgrad_epilogue_simt");
   }
   return check_launch("simt backward");
 }
@@ -463,10 +463,18 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
     if (i4 < total) {
       const float4* src = reinterpret_cast<const float4*>(wpart + i4);
       const long long stride4 = total / 4;
-      for (int s = grp; s < Sk; s += 8) {
+      float4 acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
+      int s = grp;
+      for (; s + 8 < Sk; s += 16) {
+        float4 v = __ldg(src + s * stride4), u = __ldg(src + (s + 8) * stride4);
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        acc2.x += u.x; acc2.y += u.y; acc2.z += u.z; acc2.w += u.w;
+      }
+      if (s < Sk) {
         float4 v = __ldg(src + s * stride4);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
+      acc.x += acc2.x; acc.y += acc2.y; acc.z += acc2.z; acc.w += acc2.w;
     }
     red4[grp][col] = acc;
     __syncthreads();
@@ -491,16 +499,27 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
       else dst[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx] = av[e];
     }
   } else {
+    // bias columns: 8 columns x 32 partial groups per block, 4 independent chains per thread
     if (P.nbias == 0 || !d0) return;
-    int j = ((int)blockIdx.x - nwb) * 32 + col;
-    float acc = 0.f;
-    if (j < P.Jd)
-      for (int s = grp; s < SB; s += 8) acc += bpart[(size_t)s * P.Jd + j];
-    red[grp][col] = acc;
+    __shared__ float redb[32][9];
+    const int bc = threadIdx.x % 8, bg = threadIdx.x / 8;
+    int j = ((int)blockIdx.x - nwb) * 8 + bc;
+    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+    if (j < P.Jd) {
+      int s = bg;
+      for (; s + 96 < SB; s += 128) {
+        a0 += bpart[(size_t)s * P.Jd + j];
+        a1 += bpart[(size_t)(s + 32) * P.Jd + j];
+        a2 += bpart[(size_t)(s + 64) * P.Jd + j];
+        a3 += bpart[(size_t)(s + 96) * P.Jd + j];
+      }
+      for (; s < SB; s += 32) a0 += bpart[(size_t)s * P.Jd + j];
+    }
+    redb[bg][bc] = (a0 + a1) + (a2 + a3);
     __syncthreads();
-    if (grp == 0 && j < P.Jd) {
+    if (bg == 0 && j < P.Jd) {
       float t = 0.f;
-      for (int gq = 0; gq < 8; ++gq) t += red[gq][col];
+      for (int gq = 0; gq < 32; ++gq) t += redb[gq][bc];
       int role = j / P.F, f = j % P.F;
       float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
       if (dst) dst[f] = t;
@@ -512,10 +531,10 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
                        const float* bpart, int SB, float* const db[3], cudaStream_t st) {
   long long total = (long long)P.Jd * P.Kf;  // Kf is a multiple of 64 on the tcgen05 path
   int nwb = dW[0] ? (int)((total / 4 + 31) / 32) : 0;
-  int nbb = (P.nbias && db[0]) ? (P.Jd + 31) / 32 : 0;
+  int nbb = (P.nbias && db[0]) ? (P.Jd + 7) / 8 : 0;
   if (nwb + nbb == 0) return;
   bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
                                                 db[2], nwb);
-  count_launch();
+  count_launch(st, "bwd_finish");
 }
 }  // namespace qd

@@ -470,22 +470,80 @@ __global__ void __launch_bounds__(256, 1)
 // D = [dy*b | dy*a | dy] (proposed) / [dy*b | dy*a] (t4) in bf16 plus
 // fixed-order column partial sums (bias gradients) of the fp32 products.
 // ---------------------------------------------------------------------------
+// up = 1 (stride-2 layers): D rows live on the stride-1 grid (OH1 x OW1); rows
+// at odd positions are written as zeros (the zero-upsampled gradient operand).
 __global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf16* __restrict__ dy,
                                                                const bf16* __restrict__ a,
                                                                const bf16* __restrict__ b, bf16* __restrict__ D,
-                                                               float* __restrict__ part, long long rows_per) {
+                                                               float* __restrict__ part, long long rows_per,
+                                                               int up, int OH1, int OW1) {
   const int F = P.F, chunks = F / 8;
   const int lanes = 256 / chunks;  // rows processed concurrently
   const int ch = threadIdx.x % chunks, rl = threadIdx.x / chunks;
   const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
   const bool prop = P.family == QD_FAM_PROPOSED;
+  const long long rows = up ? (long long)P.N * OH1 * OW1 : P.Mout;
   long long r0 = (long long)blockIdx.x * rows_per, r1 = r0 + rows_per;
-  if (r1 > P.Mout) r1 = P.Mout;
+  if (r1 > rows) r1 = rows;
   float s0[8], s1[8], s2[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) s0[e] = s1[e] = s2[e] = 0.f;
-  if (rl < lanes) {
-    for (long long m = r0 + rl; m < r1; m += lanes) {
+  if (rl < lanes && !up && mat) {
+    // fast path (stride 1, D materialised): 4 rows per iteration, all 12 loads in flight
+    constexpr int U = 4;
+    for (long long m0 = r0 + rl; m0 < r1; m0 += (long long)U * lanes) {
+      uint4 gu[U], au[U], bu[U];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        long long m = m0 + (long long)u * lanes;
+        ok[u] = m < r1;
+        size_t off = (size_t)(ok[u] ? m : r0) * F + ch * 8;
+        gu[u] = __ldg(reinterpret_cast<const uint4*>(dy + off));
+        au[u] = __ldg(reinterpret_cast<const uint4*>(a + off));
+        bu[u] = __ldg(reinterpret_cast<const uint4*>(b + off));
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+        long long m = m0 + (long long)u * lanes;
+        const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu[u]);
+        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&au[u]);
+        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bu[u]);
+        uint4 d0, d1;
+        uint32_t* d0p = reinterpret_cast<uint32_t*>(&d0);
+        uint32_t* d1p = reinterpret_cast<uint32_t*>(&d1);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          float2 g = __bfloat1622float2(g2[e]), av = __bfloat1622float2(a2[e]), bv = __bfloat1622float2(b2[e]);
+          float x0 = g.x * bv.x, x1 = g.y * bv.y, y0 = g.x * av.x, y1 = g.y * av.y;
+          d0p[e] = pack_bf16x2(x0, x1);
+          d1p[e] = pack_bf16x2(y0, y1);
+          s0[2 * e] += x0; s0[2 * e + 1] += x1;
+          s1[2 * e] += y0; s1[2 * e + 1] += y1;
+          s2[2 * e] += g.x; s2[2 * e + 1] += g.y;
+        }
+        bf16* drow = D + (size_t)m * P.Jd + ch * 8;
+        *reinterpret_cast<uint4*>(drow) = d0;
+        *reinterpret_cast<uint4*>(drow + F) = d1;
+        if (prop) *reinterpret_cast<uint4*>(drow + 2 * F) = gu[u];
+      }
+    }
+  } else if (rl < lanes) {
+    for (long long md = r0 + rl; md < r1; md += lanes) {
+      long long m = md;
+      if (up) {
+        long long n = md / ((long long)OH1 * OW1), rem = md % ((long long)OH1 * OW1);
+        int h1 = (int)(rem / OW1), w1 = (int)(rem % OW1);
+        bool real = !(h1 & 1) && !(w1 & 1) && (h1 >> 1) < P.OH && (w1 >> 1) < P.OW;
+        if (!real) {
+          bf16* drow = D + (size_t)md * P.Jd + ch * 8;
+          uint4 z = make_uint4(0u, 0u, 0u, 0u);
+          for (int blk = 0; blk < P.Jd / F; ++blk) *reinterpret_cast<uint4*>(drow + blk * F) = z;
+          continue;
+        }
+        m = (n * P.OH + (h1 >> 1)) * P.OW + (w1 >> 1);
+      }
       size_t off = (size_t)m * F + ch * 8;
       uint4 gu = __ldg(reinterpret_cast<const uint4*>(dy + off));
       const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu);
@@ -507,11 +565,12 @@ __global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf1
           s1[2 * e] += y0; s1[2 * e + 1] += y1;
           s2[2 * e] += g.x; s2[2 * e + 1] += g.y;
         }
-        bf16* drow = D + (size_t)m * P.Jd + ch * 8;
+        bf16* drow = D + (size_t)md * P.Jd + ch * 8;
         *reinterpret_cast<uint4*>(drow) = d0;
         *reinterpret_cast<uint4*>(drow + F) = d1;
         if (prop) *reinterpret_cast<uint4*>(drow + 2 * F) = gu;
       } else {
+        if (up) *reinterpret_cast<uint4*>(D + (size_t)md * P.Jd + ch * 8) = gu;
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           float2 g = __bfloat1622float2(g2[e]);
@@ -571,13 +630,60 @@ static bool init_driver() {
 PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() { return g_encode; }
 int tc_num_sms() { return g_num_sms > 0 ? g_num_sms : 148; }
 
+static int plain_blocks(int ch);
+
+// fprop / dgrad kernel configurations (shared by dispatch and eligibility)
+struct GemmCfg {
+  int epi, nbk, tiles_nn, b_rs_tile, b_rs_blk, out_c_tile, nout, nbias;
+};
+static GemmCfg fprop_cfg(const Plan& P) {
+  GemmCfg c;
+  if (P.family == QD_FAM_PROPOSED) { c.epi = EPI_PROPOSED; c.nbk = 3; }
+  else if (P.family == QD_FAM_T4) { c.epi = EPI_T4; c.nbk = 2; }
+  else { c.epi = EPI_PLAIN; c.nbk = plain_blocks(P.F); }
+  if (c.epi == EPI_PLAIN) {
+    c.tiles_nn = P.F / (64 * c.nbk); c.b_rs_tile = 64 * c.nbk; c.out_c_tile = 64 * c.nbk; c.nout = c.nbk;
+    c.nbias = P.family == QD_FAM_FIRST_ORDER ? 1 : 0;
+  } else {
+    c.tiles_nn = P.F / 64; c.b_rs_tile = c.nbk * 64; c.out_c_tile = 64; c.nout = 3;
+    c.nbias = P.family == QD_FAM_PROPOSED ? 3 : 0;
+  }
+  c.b_rs_blk = 64;
+  return c;
+}
+static GemmCfg dgrad_cfg(const Plan& P) {
+  GemmCfg c;
+  c.epi = P.sq == 0 ? EPI_PLAIN : EPI_SQ;
+  c.nbk = P.sq == 0 ? plain_blocks(P.C) : (P.sq == 1 ? 1 : 2);
+  c.tiles_nn = P.sq == 0 ? P.C / (64 * c.nbk) : P.C / 64;
+  c.b_rs_tile = P.sq == 0 ? 64 * c.nbk : 64;
+  c.b_rs_blk = P.sq == 2 ? P.C : 64;
+  c.out_c_tile = P.sq == 0 ? 64 * c.nbk : 64;
+  c.nout = P.sq == 0 ? c.nbk : 1;
+  c.nbias = 0;
+  return c;
+}
+
+// stride-2 layers: only via the CTA-pair / halo kernels on the stride-1 grid
+static bool s2_fits(const Plan& P) {
+  if (P.s != 2 || P.r < 2) return false;
+  Plan P1 = stride1_plan(P);
+  GemmCfg f = fprop_cfg(P), d = dgrad_cfg(P);
+  if (!conv2_fits(P.N, P.C, P.W, P.H, P1.OW, P1.OH, P.p, P.r, P.sq == 2, f.nbk, f.nout, f.tiles_nn, P.F, f.nbias))
+    return false;
+  if (!conv2_fits(P.N, P.Jd, P1.OW, P1.OH, P.W, P.H, P.r - 1 - P.p, P.r, 0, d.nbk, d.nout, d.tiles_nn, P.C, 0))
+    return false;
+  return wgrad2_split(P1) > 0;
+}
+
 bool tc_supported(const Plan& P, unsigned flags) {
   if (flags & QD_FLAG_FORCE_SIMT) return false;
   if (P.dtype != QD_BF16) return false;
   if (P.C % 64 || P.F % 64) return false;
-  if (P.s != 1) return false;
   if (P.OH < 1 || P.OW < 1) return false;
-  return init_driver();
+  if (!init_driver()) return false;
+  if (P.s == 1) return true;
+  return !(flags & QD_FLAG_TC_V1) && s2_fits(P);
 }
 
 static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint32_t* box) {
@@ -656,7 +762,7 @@ static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   }
   int grid = args.total_tiles < g_num_sms ? args.total_tiles : g_num_sms;
   conv_gemm_kernel<EPI, NB><<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
-  count_launch();
+  count_launch(st, "conv_gemm");
   return check_launch("conv_gemm");
 }
 
@@ -671,7 +777,7 @@ static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUte
   }
   int grid = args.mtiles * args.ntiles * args.splits;
   wgrad_kernel<NBLK><<<grid, 256, Cfg::SMEM, st>>>(X0, X1, Dm, args);
-  count_launch();
+  count_launch(st, "wgrad_v1");
   return check_launch("wgrad");
 }
 
@@ -751,39 +857,41 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
     if (P.sq == 2) a1 = x;
   }
   const float* nb3[3] = {bias[0], bias[1], bias[2]};
-  int epi, nbk, tiles_nn, b_rs_tile, out_c_tile;
-  if (P.family == QD_FAM_PROPOSED) { epi = EPI_PROPOSED; nbk = 3; }
-  else if (P.family == QD_FAM_T4) { epi = EPI_T4; nbk = 2; }
-  else { epi = EPI_PLAIN; nbk = plain_blocks(P.F); }
-  if (epi == EPI_PLAIN) {
-    tiles_nn = P.F / (64 * nbk); b_rs_tile = 64 * nbk; out_c_tile = 64 * nbk;
-    if (P.family != QD_FAM_FIRST_ORDER) nb3[0] = nullptr;
-  } else {
-    tiles_nn = P.F / 64; b_rs_tile = nbk * 64; out_c_tile = 64;
+  GemmCfg c = fprop_cfg(P);
+  if (c.nbias == 0) nb3[0] = nb3[1] = nb3[2] = nullptr;
+  if (P.s == 2) {
+    // stride-1 grid, epilogue keeps the even positions
+    Plan P1 = stride1_plan(P);
+    return run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P1.OW, P1.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
+                     P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st, 2);
   }
   if (!(P.flags & QD_FLAG_TC_V1)) {
-    int rc2 = run_conv2(epi, nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
-                        P.nb * P.F, P.Kf, b_rs_tile, 64, tiles_nn, out_c_tile, y, a, b, P.F, nb3, nullptr, st);
+    int rc2 = run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
+                        P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st);
     if (rc2 != QD_ERR_UNSUPPORTED) return rc2;
   }
-  return run_conv(epi, nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
-                  P.nb * P.F, P.Kf, b_rs_tile, 64, tiles_nn, out_c_tile, y, a, b, P.F, nb3, nullptr, st);
+  return run_conv(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
+                  P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st);
 }
 
-int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
+int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
                 void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L,
                 cudaStream_t st) {
+  // stride-2 layers: the GEMMs run on the stride-1 grid over the zero-upsampled D
+  const bool up = P0.s == 2;
+  const Plan P = up ? stride1_plan(P0) : P0;
   const bf16* wd = (const bf16*)wpack + pack_fprop_elems(P);
   const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
   const bf16* D = (const bf16*)dy;
   float* bpart = (float*)(ws + L.off_BS);
-  if (mat || P.nbias) {
-    long long rows_per = (P.Mout + L.bs_split - 1) / L.bs_split;
-    bf16* Dw = mat ? (bf16*)(ws + L.off_D) : nullptr;
-    bwd_prologue_vec_kernel<<<L.bs_split, 256, 0, st>>>(P, (const bf16*)dy, (const bf16*)a, (const bf16*)b, Dw,
-                                                        bpart, rows_per);
-    count_launch();
-    if (mat) D = Dw;
+  if (mat || P.nbias || up) {
+    long long rows = up ? P.Mout : P0.Mout;
+    long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
+    bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;
+    bwd_prologue_vec_kernel<<<L.bs_split, 256, 0, st>>>(P0, (const bf16*)dy, (const bf16*)a, (const bf16*)b, Dw,
+                                                        bpart, rows_per, up ? 1 : 0, P.OH, P.OW);
+    count_launch(st, "prologue");
+    if (mat || up) D = Dw;
   }
   int rc;
   // ---- wgrad ----
@@ -832,24 +940,20 @@ int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
   } else if (db[0] && (mat || P.nbias)) {
     launch_bias_finish(P, bpart, L.bs_split, db, st);
   }
+  if (up && dx && (P.flags & QD_FLAG_TC_V1)) return set_error(QD_ERR_UNSUPPORTED, "stride 2 needs conv2");
   // ---- dgrad (stride 1: a conv of D with the flipped packed weights) ----
   if (dx) {
     const float* nob[3] = {nullptr, nullptr, nullptr};
     int pad_eff = P.r - 1 - P.p;
-    int epi = P.sq == 0 ? EPI_PLAIN : EPI_SQ;
-    int nbk = P.sq == 0 ? plain_blocks(P.C) : (P.sq == 1 ? 1 : 2);
-    int tiles_nn = P.sq == 0 ? P.C / (64 * nbk) : P.C / 64;
-    int b_rs_tile = P.sq == 0 ? 64 * nbk : 64;
-    int b_rs_blk = P.sq == 2 ? P.C : 64;
-    int out_c_tile = P.sq == 0 ? 64 * nbk : 64;
+    GemmCfg c = dgrad_cfg(P);
     const void* xr = P.sq ? x : nullptr;
     rc = QD_ERR_UNSUPPORTED;
     if (!(P.flags & QD_FLAG_TC_V1))
-      rc = run_conv2(epi, nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
-                     b_rs_tile, b_rs_blk, tiles_nn, out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
-    if (rc == QD_ERR_UNSUPPORTED)
-      rc = run_conv(epi, nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
-                    b_rs_tile, b_rs_blk, tiles_nn, out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
+      rc = run_conv2(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
+                     c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
+    if (rc == QD_ERR_UNSUPPORTED && !up)
+      rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
+                    c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
     if (rc) return rc;
   }
   return check_launch("tc backward");

@@ -36,6 +36,7 @@ enum { E2_PROPOSED = 0, E2_T4 = 1, E2_PLAIN = 2, E2_SQ = 3 };
 struct C2Args {
   int N, Cin, Win, Hin;
   int OHg, OWg;
+  int ss, OHo, OWo;  // output subsampling (stride-2 conv = stride-1 grid, even positions)
   int pe, r, Wp, HR;
   int T_img, tiles_nn, total;
   int cblks, ablocks, KBtot;
@@ -387,7 +388,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
       int qq = 128 * t + q * 32 + lane;
       int hq = qq / g.Wp, wq = qq - hq * g.Wp;
       bool valid = n < g.N && hq < g.OHg && wq < g.OWg;
-      int pix = valid ? (n * g.OHg + hq) * g.OWg + wq : -1;
+      if (g.ss > 1) valid = valid && (hq % g.ss) == 0 && (wq % g.ss) == 0;
+      int pix = valid ? (n * g.OHo + hq / g.ss) * g.OWo + wq / g.ss : -1;
       const int c_base = j * g.out_c_tile;
       if (tracer) C2_TRACE(2, it, 0);
       ptx::mbar_wait(&tfull[acs], tph);
@@ -643,7 +645,7 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   int clusters = tc_num_sms() / 2;
   if (pl.g.total < clusters) clusters = pl.g.total;
   conv2_kernel<EPI, NB, R><<<2 * clusters, C2Threads<EPI, NB>::THREADS, pl.smem, st>>>(A0, A1, B, pl.g);
-  count_launch();
+  count_launch(st, "conv2");
   return check_launch("conv2");
 }
 template <int EPI, int NB>
@@ -658,7 +660,7 @@ static int c2_launch(const CUtensorMap& A0, const CUtensorMap& A1, const CUtenso
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st) {
+              const void* xres, cudaStream_t st, int ss) {
   int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
   int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
   C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
@@ -669,6 +671,9 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   g.b_contig = (b_rs_blk == 64) ? 1 : 0;
   if (!g.b_contig && nbk != 2) return QD_ERR_UNSUPPORTED;
   g.out_c_tile = out_c_tile;
+  g.ss = ss;
+  g.OHo = (OHg - 1) / ss + 1;
+  g.OWo = (OWg - 1) / ss + 1;
   {
     const char* e = getenv("QD_DEBUG");
     g.dbg = e ? atoi(e) : 0;
@@ -948,6 +953,11 @@ static W2Plan w2_plan(const Plan& P) {
   return pl;
 }
 
+bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
+                int tiles_nn, int Cout, int nbias) {
+  return c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, nout, tiles_nn, Cout, nbias).ok;
+}
+
 int wgrad2_split(const Plan& P) {
   W2Plan pl = w2_plan(P);
   return pl.ok ? pl.g.splits : 0;
@@ -986,7 +996,7 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
     attr = (int)pl.smem;
   }
   wgrad2_kernel<<<g.jtiles * g.ablocks * g.gstart[g.tgroups], 256, pl.smem, st>>>(X0, X1, Dm, g);
-  count_launch();
+  count_launch(st, "wgrad2");
   return check_launch("wgrad2");
 }
 

@@ -116,6 +116,12 @@ TC_CASES = [
     ("first_order", "conv", 2, 64, 128, 16, 16, 3, 1, 1),
     ("proposed", "conv", 2, 64, 64, 13, 17, 2, 1, 0),
     ("proposed", "conv", 2, 64, 64, 12, 12, 5, 1, 2),
+    # stride 2 (ResNet downsampling): stride-1 grid + subsampled epilogue /
+    # zero-upsampled gradient operand
+    ("proposed", "conv", 2, 64, 128, 28, 28, 3, 2, 1),
+    ("proposed", "conv", 3, 64, 64, 29, 27, 3, 2, 1),
+    ("t4", "conv", 2, 64, 64, 16, 16, 3, 2, 1),
+    ("t2_linear", "conv", 2, 64, 64, 16, 18, 3, 2, 1),
     ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
     ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
     ("t2_linear", "fc", 64, 128, 64, 1, 1, 1, 1, 0),
