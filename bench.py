@@ -423,17 +423,240 @@ def run_ours(args, wl, wl_name):
     return 0
 
 
+# ---------------------------------------------------------------------------
+# network training step (BASELINE configs 3 and 4): img/s
+# ---------------------------------------------------------------------------
+NETS = {
+    # name: (builder, per-GPU batch, image HW, classes)
+    "qvgg16": ("QuadraVGG16", 256, 32, 10),
+    "qresnet18": ("QuadraResNet18", 128, 224, 1000),
+}
+
+
+def net_quad_layers(name):
+    """(spec, input CHW) of every quadratic conv in the net, for FLOP counting and
+    the CPU baseline (built on the meta device: shapes only)."""
+    import torch
+    from paper_2204_01701_b200 import qnets
+    import dataclasses
+    from paper_2204_01701_b200.nn import QuadConv2d
+    builder, batch, hw, classes = NETS[name]
+    shapes = []
+    hooks = []
+    with torch.device("meta"):
+        model = getattr(qnets, builder)(num_classes=classes)
+    inner = set()
+    for m in model.modules():
+        if isinstance(m, qnets.PaddedQuadConv2d):
+            inner.add(id(m.conv))
+            # algorithmic work counts the real input channels, not the zero padding
+            hooks.append(m.register_forward_pre_hook(
+                lambda mod, inp: shapes.append((dataclasses.replace(mod.conv.spec, in_dim=mod.cin),
+                                                tuple(inp[0].shape[1:])))))
+    for m in model.modules():
+        if isinstance(m, QuadConv2d) and id(m) not in inner:
+            hooks.append(m.register_forward_pre_hook(
+                lambda mod, inp: shapes.append((mod.spec, tuple(inp[0].shape[1:])))))
+    # trace shapes with a meta-device forward that bypasses the kernels
+    import paper_2204_01701_b200.nn as qnn
+    orig = qnn.QuadFunction.apply
+
+    def fake(spec, dtype, x, *ts):
+        oh = (x.shape[2] + 2 * spec.pad - spec.kernel) // spec.stride + 1
+        ow = (x.shape[3] + 2 * spec.pad - spec.kernel) // spec.stride + 1
+        return torch.empty(x.shape[0], spec.out_dim, oh, ow, device=x.device)
+    qnn.QuadFunction.apply = fake
+    try:
+        with torch.device("meta"):
+            model(torch.empty(1, 3, hw, hw))
+    finally:
+        qnn.QuadFunction.apply = orig
+        for h in hooks:
+            h.remove()
+    return shapes
+
+
+def net_flops(name, batch):
+    from paper_2204_01701_b200.spec import gemm_flops
+    return sum(gemm_flops(sp, batch, c_hw[1], c_hw[2]) for sp, c_hw in net_quad_layers(name))
+
+
+def net_cpu_baseline(name):
+    """Reference algorithm (oracle port) fwd+bwd of every quadratic layer at batch 1,
+    summed: seconds per image (linear in N)."""
+    from oracle import quadra_oracle as Q
+    tot = 0.0
+    for sp, (c, h, w) in net_quad_layers(name):
+        fam = sp.family
+        x, P, g = Q.synthetic_layer(fam, "conv", 1, c, sp.out_dim, h, w, sp.kernel, sp.stride, sp.pad, seed=0)
+        geo = Q.Geometry("conv", sp.kernel, sp.stride, sp.pad)
+        t0 = time.perf_counter()
+        y, a, b = Q.forward(fam, geo, P, x)
+        Q.symbolic_backward(fam, geo, P, x, a, b, g)
+        tot += time.perf_counter() - t0
+    return tot
+
+
+def run_net(args, name):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_01701_b200 import _lib, qnets
+    from paper_2204_01701_b200.dp import BucketedAllReduce, sgd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=dev)
+    builder, batch, hw, classes = NETS[name]
+    batch = args.batch or batch
+    torch.manual_seed(1234 + rank)
+    model = getattr(qnets, builder)(num_classes=classes).to(dev).to(memory_format=torch.channels_last)
+    opt = sgd(model.parameters(), lr=0.01)
+    red = BucketedAllReduce(model.parameters(), bucket_mb=25.0)
+    gen = torch.Generator(device=dev).manual_seed(rank)
+    x = torch.randn(batch, 3, hw, hw, device=dev, generator=gen).to(torch.bfloat16).contiguous(
+        memory_format=torch.channels_last)
+    y = torch.randint(0, classes, (batch,), device=dev, generator=gen)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step(xb=x, yb=y):
+        red.reset()
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = torch.nn.functional.cross_entropy(model(xb), yb)
+        loss.backward()
+        red.finish()
+        opt.step()
+        return loss
+
+    def timed(fn, k):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(k)]
+        for i in range(k):
+            flush.fill_(i & 0xFF)
+            evs[i][0].record(stream)
+            fn()
+            evs[i][1].record(stream)
+        torch.cuda.synchronize()
+        return [a.elapsed_time(b) for a, b in evs]
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    l0 = _lib.launch_count()
+    step()
+    torch.cuda.synchronize()
+    per_step = _lib.launch_count() - l0
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        ms = timed(step, args.steps)
+    tot = sum(ms)
+    if world > 1:
+        tt = torch.tensor([tot], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        tot = float(tt.item())
+    ms_step = tot / args.steps
+    value = world * batch / (ms_step * 1e-3)
+    qflops = net_flops(name, batch)
+    pk = load_peaks()
+    ach = qflops / (ms_step * 1e-3) / 1e12
+
+    # e2e: batch from pinned host memory each step, loss read back
+    x_h = x.detach().cpu().pin_memory()
+    y_h = y.detach().cpu().pin_memory()
+    loss_h = torch.empty((), dtype=torch.float32).pin_memory()
+
+    def e2e_step():
+        xb = x_h.to(dev, non_blocking=True).contiguous(memory_format=torch.channels_last)
+        yb = y_h.to(dev, non_blocking=True)
+        loss = step(xb, yb)
+        loss_h.copy_(loss.detach().float(), non_blocking=True)
+    e2e_step()
+    torch.cuda.synchronize()
+    e_ms = timed(e2e_step, args.steps)
+    e_step = sum(e_ms) / len(e_ms)
+    if world > 1:
+        tt = torch.tensor([e_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        e_step = float(tt.item())
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    cpu = None
+    if world == 1 and not args.no_cpu:
+        sec = net_cpu_baseline(name)
+        cpu = {"value": 1.0 / sec, "unit": "img/s", "cores": os.cpu_count(), "kind": "port",
+               "sample": f"reference algorithm (fp64 im2col+GEMM+col2im) fwd+bwd of the {len(net_quad_layers(name))} "
+                         f"quadratic layers of {name} at batch 1, summed ({sec:.2f} s/img; linear in batch, "
+                         "BASELINE.md §4); first-order layers not counted"}
+    out = {"metric": f"{name}_train_img_per_s", "value": value, "unit": "img/s", "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "bf16",
+           "data": "synthetic (seeded N(0,1) images, uniform labels)",
+           "config": {"workload": f"{name}: full training step (fwd, CE loss, bwd, bucketed all-reduce, "
+                                  f"SGD m=0.9 wd=5e-4)", "global_batch": batch * world, "per_gpu_batch": batch,
+                      "image": [3, hw, hw], "classes": classes, "parallelism": f"dp{world}",
+                      "l2": "flushed between timed steps (256 MiB write, untimed)", "cuda_graph": False,
+                      "params": qnets.count_params(model), "quad_gemm_flops_per_gpu_step": qflops},
+           "roofline": {"bound": "tensor", "kernel": "all quadratic-layer GEMM work of the step",
+                        "achieved": ach, "peak": pk["bf16"], "unit": "TFLOP/s", "frac": ach / pk["bf16"],
+                        "traffic": None,
+                        "note": "whole-step figure: quadratic GEMM FLOPs / step time (first-order layers, BN, "
+                                "optimizer and all-reduce included in the time)"},
+           "cpu_baseline": cpu,
+           "e2e": {"value": world * batch / (e_step * 1e-3), "unit": "img/s", "ms_per_step": e_step,
+                   "h2d_bytes_per_step": x_h.numel() * x_h.element_size() + y_h.numel() * y_h.element_size(),
+                   "d2h_bytes_per_step": 4},
+           "gpu_launches": per_step * args.steps, "launches_per_step": per_step, "clocks": clk.summary()}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_net_reference(args, name):
+    if int(os.environ.get("RANK", "0")) != 0:
+        return 0
+    builder, batch, hw, classes = NETS[name]
+    times = [net_cpu_baseline(name) for _ in range(max(1, args.steps))]
+    sec = sum(times) / len(times)
+    value = 1.0 / sec
+    out = {"metric": f"{name}_train_img_per_s", "value": value, "unit": "img/s", "impl": "reference",
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3 * batch,
+           "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": {"workload": f"{name}: quadratic layers fwd+bwd, batch 1 sample scaled", "per_gpu_batch": batch},
+           "cpu_baseline": {"value": value, "unit": "img/s", "cores": os.cpu_count(), "kind": "port",
+                            "sample": "quadratic layers at batch 1 (reference algorithm)"},
+           "e2e": {"value": value, "unit": "img/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
-    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS))
+    ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + sorted(NETS))
+    ap.add_argument("--batch", type=int, default=0, help="per-GPU batch for the net workloads")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    if args.workload in NETS:
+        if args.impl == "reference":
+            return run_net_reference(args, args.workload)
+        return run_net(args, args.workload)
     wl = WORKLOADS[args.workload]
     if args.impl == "reference":
         return run_reference(args, wl, args.workload)

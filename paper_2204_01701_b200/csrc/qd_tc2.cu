@@ -901,21 +901,23 @@ static W2Plan w2_plan(const Plan& P) {
     if (hi - lo + 1 > RX) RX = hi - lo + 1;
   }
   if (RX > 256) return pl;
-  // N tile: widest multiple of 64 <= 256 that divides Jd (192 for proposed F = 64)
-  int ntb = 1;
-  for (int c = 4; c >= 1; --c)
-    if ((P.Jd / 64) % c == 0) { ntb = c; break; }
+  uint32_t d_tx = (uint32_t)Wp * RD * 128, x_tx = (uint32_t)Wp * RX * 128;
+  uint32_t d_bytes = (d_tx + 1023) / 1024 * 1024, x_bytes = (x_tx + 1023) / 1024 * 1024;
+  // N tile: the widest multiple of 64 (<= 256, dividing Jd) whose stage still
+  // double-buffers in smem (192 for proposed F = 64 at 32x32; narrower for wide images)
+  int ntb = 0, stages = 0;
+  for (int c = 4; c >= 1; --c) {
+    if ((P.Jd / 64) % c) continue;
+    uint32_t stg = c * d_bytes + x_bytes;
+    int sn = (int)((212 * 1024) / stg);
+    if (sn >= 2) { ntb = c; stages = sn > 4 ? 4 : sn; break; }
+  }
+  if (ntb == 0) return pl;
   const int NT = ntb * 64;
   const int npairs = (P.r * P.r + 1) / 2;
   int pp = 512 / NT;
   if (pp > npairs) pp = npairs;
   const int tgroups = (npairs + pp - 1) / pp;
-  uint32_t d_tx = (uint32_t)Wp * RD * 128, x_tx = (uint32_t)Wp * RX * 128;
-  uint32_t d_bytes = (d_tx + 1023) / 1024 * 1024, x_bytes = (x_tx + 1023) / 1024 * 1024;
-  uint32_t stage = ntb * d_bytes + x_bytes;
-  int stages = (int)((212 * 1024) / stage);
-  if (stages > 4) stages = 4;
-  if (stages < 2) return pl;
   g.N = P.N; g.OHg = P.OH; g.OWg = P.OW; g.Jd = P.Jd; g.Kf = P.Kf; g.K0 = P.K0; g.C = P.C;
   g.pe = P.p; g.r = P.r; g.Wp = Wp; g.RD = RD; g.RX = RX;
   g.T_img = T_img; g.cblks = P.C / 64; g.ablocks = g.cblks * (P.sq == 2 ? 2 : 1); g.jtiles = P.Jd / NT;
@@ -948,7 +950,7 @@ static W2Plan w2_plan(const Plan& P) {
   g.gstart[tgroups] = tot;
   g.splits = smax;  // partial slots; rows of group t use slots [0, gsplit[t])
   g.d_tx = d_tx; g.x_tx = x_tx; g.d_bytes = d_bytes; g.x_bytes = x_bytes; g.stages = stages;
-  pl.smem = 1024 + (size_t)stages * stage + 1024;
+  pl.smem = 1024 + (size_t)stages * (ntb * d_bytes + x_bytes) + 1024;
   pl.ok = true;
   return pl;
 }

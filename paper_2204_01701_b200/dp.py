@@ -1,0 +1,99 @@
+"""Data-parallel gradient exchange: bucketed all-reduce overlapped with backward.
+
+The quadratic layer is per-sample independent; the only cross-sample
+coupling of batch-sharded training is the sum over samples inside dW / db
+(SURVEY.md §8(e)). Each rank runs its own batch and the gradients are
+averaged over ranks once per step -- one exchange, no other collective.
+
+Mechanics (one process per GPU, torch.distributed over NCCL on NVLink /
+NVSwitch; gloo on CPU for the tests):
+
+* parameters are grouped into flat fp32 buckets (~25 MB) in reverse
+  registration order, i.e. roughly the order backward produces them;
+* each parameter's ``.grad`` is a view into its bucket, so autograd
+  accumulates straight into the bucket (no copy);
+* a post-accumulate-grad hook counts ready parameters; when a bucket is
+  complete its all-reduce (ReduceOp.AVG) is launched asynchronously, so the
+  NCCL transfer of the deep layers overlaps the backward of the shallow ones;
+* ``finish()`` waits for the outstanding buckets before the optimizer step.
+
+The update itself is the reference's ``sgd_step`` (trainer.py:50-61:
+v <- m v + g + wd p; p <- p - lr v), which is exactly
+``torch.optim.SGD(momentum=0.9, weight_decay=5e-4, dampening=0)``.
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.distributed as dist
+
+
+class BucketedAllReduce:
+    def __init__(self, params, bucket_mb=25.0, group=None, reduce_dtype=torch.float32):
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        params = [p for p in params if p.requires_grad]
+        order = list(reversed(params))
+        cap = int(bucket_mb * (1 << 20) / 4)
+        self.buckets = []  # (flat tensor, [params])
+        cur, cur_n = [], 0
+        for p in order:
+            if cur and cur_n + p.numel() > cap:
+                self._make_bucket(cur, cur_n, reduce_dtype)
+                cur, cur_n = [], 0
+            cur.append(p)
+            cur_n += p.numel()
+        if cur:
+            self._make_bucket(cur, cur_n, reduce_dtype)
+        self.pending = [0] * len(self.buckets)
+        self.handles = [None] * len(self.buckets)
+        self.hooks = []
+        for bi, (_, ps) in enumerate(self.buckets):
+            for p in ps:
+                self.hooks.append(p.register_post_accumulate_grad_hook(self._hook(bi)))
+        self.reset()
+
+    def _make_bucket(self, ps, n, dtype):
+        flat = torch.zeros(n, dtype=dtype, device=ps[0].device)
+        off = 0
+        for p in ps:
+            p.grad = flat[off:off + p.numel()].view_as(p)
+            off += p.numel()
+        self.buckets.append((flat, ps))
+
+    def _hook(self, bi):
+        def fire(_p):
+            self.pending[bi] -= 1
+            if self.pending[bi] == 0 and self.world > 1:
+                op = dist.ReduceOp.AVG if dist.get_backend(self.group) == "nccl" else dist.ReduceOp.SUM
+                self.handles[bi] = dist.all_reduce(self.buckets[bi][0], op=op, group=self.group,
+                                                   async_op=True)
+        return fire
+
+    def reset(self):
+        """zero the buckets (the grads) and re-arm the per-bucket counters"""
+        for bi, (flat, ps) in enumerate(self.buckets):
+            flat.zero_()
+            self.pending[bi] = len(ps)
+            self.handles[bi] = None
+
+    def finish(self):
+        """wait for every bucket's all-reduce; gradients are then the rank mean"""
+        for bi, h in enumerate(self.handles):
+            if self.world > 1:
+                if h is None:  # a bucket whose params got no gradient this step
+                    op = dist.ReduceOp.AVG if dist.get_backend(self.group) == "nccl" else dist.ReduceOp.SUM
+                    h = dist.all_reduce(self.buckets[bi][0], op=op, group=self.group, async_op=True)
+                h.wait()
+                if dist.get_backend(self.group) != "nccl":
+                    self.buckets[bi][0].div_(self.world)
+
+    def remove(self):
+        for h in self.hooks:
+            h.remove()
+
+
+def sgd(params, lr=0.1, momentum=0.9, weight_decay=5e-4):
+    """The reference sgd_step (trainer.py:50-61) as torch's fused/foreach SGD."""
+    return torch.optim.SGD(params, lr=lr, momentum=momentum, weight_decay=weight_decay, dampening=0.0,
+                           foreach=True)

@@ -1,0 +1,135 @@
+"""QuadraResNet-18 and QuadraVGG-16 (BASELINE.json configs 3 and 4).
+
+The reference cannot express these nets (its ModelConfig is a plain chain
+with no pooling or residual ops, /root/reference/pkg/src/quadra/autobuild.py:75-118,
+model.py:151-155), so they are built here in torch around
+the quadratic conv module; every 3x3 conv is a ``QuadConv2d`` (proposed
+neuron by default) and everything else is first-order torch/cuDNN:
+
+* QuadraVGG-16 (CIFAR, 3x32x32, 10 classes): VGG-16 "D" layout, all 13 convs
+  quadratic, each followed by BatchNorm + ReLU, five 2x2 max-pools, a
+  512 -> 10 linear head. 44.16 M parameters (matches the
+  paper's 4.41E+7).
+* QuadraResNet-18 (ImageNet, 3x224x224, 1000 classes): first-order 7x7/2
+  stem + BN + ReLU + 3x3/2 max-pool, BasicBlocks [2, 2, 2, 2] at widths
+  64/128/256/512 whose 3x3 convs are quadratic (3 of them stride 2), 1x1/2
+  first-order downsample + BN, global average pool, 512 -> 1000 linear.
+
+Activations are bf16 channels_last; parameters are fp32 masters. Run the
+forward under ``torch.autocast("cuda", torch.bfloat16)`` so the first-order
+layers compute in bf16 too (batch norm keeps fp32 statistics).
+"""
+
+from __future__ import annotations
+
+import torch
+import torch.nn.functional as Fnn
+from torch import nn
+
+from .nn import QuadConv2d
+
+
+class PaddedQuadConv2d(nn.Module):
+    """QuadConv2d whose input channels are zero-padded to a multiple of 64 so
+    the layer runs on the tcgen05 kernels (e.g. the 3-channel stem of VGG).
+    The padding is part of the autograd graph, so gradients of the real
+    channels are exact and the padded ones are dropped."""
+
+    def __init__(self, in_channels, out_channels, kernel_size=3, stride=1, padding=1,
+                 family="proposed", device=None):
+        super().__init__()
+        self.cin = in_channels
+        self.cpad = ((in_channels + 63) // 64) * 64
+        self.conv = QuadConv2d(self.cpad, out_channels, kernel_size, stride, padding, family,
+                               device=device)
+        # re-initialise with the real fan-in and keep the padded weight columns at zero
+        with torch.no_grad():
+            for role in ("Wa", "Wb", "Wc"):
+                if hasattr(self.conv, role):
+                    w = getattr(self.conv, role)
+                    w[:, in_channels:].zero_()
+                    w[:, :in_channels].mul_((self.cpad / in_channels) ** 0.5)
+
+    def forward(self, x):
+        if self.cpad != self.cin:
+            x = Fnn.pad(x, (0, 0, 0, 0, 0, self.cpad - self.cin))
+            x = x.contiguous(memory_format=torch.channels_last)
+        return self.conv(x)
+
+
+def quad_conv(cin, cout, k=3, s=1, p=1, family="proposed"):
+    if cin % 64:
+        return PaddedQuadConv2d(cin, cout, k, s, p, family)
+    return QuadConv2d(cin, cout, k, s, p, family)
+
+
+VGG16_CFG = [64, 64, "M", 128, 128, "M", 256, 256, 256, "M", 512, 512, 512, "M", 512, 512, 512, "M"]
+
+
+class QuadraVGG16(nn.Module):
+    def __init__(self, num_classes=10, family="proposed"):
+        super().__init__()
+        layers = []
+        cin = 3
+        for v in VGG16_CFG:
+            if v == "M":
+                layers.append(nn.MaxPool2d(2, 2))
+            else:
+                layers += [quad_conv(cin, v, 3, 1, 1, family), nn.BatchNorm2d(v), nn.ReLU(inplace=True)]
+                cin = v
+        self.features = nn.Sequential(*layers)
+        self.classifier = nn.Linear(512, num_classes)
+
+    def forward(self, x):
+        x = self.features(x)
+        return self.classifier(torch.flatten(x, 1))
+
+
+class QuadBasicBlock(nn.Module):
+    expansion = 1
+
+    def __init__(self, inplanes, planes, stride=1, family="proposed"):
+        super().__init__()
+        self.conv1 = quad_conv(inplanes, planes, 3, stride, 1, family)
+        self.bn1 = nn.BatchNorm2d(planes)
+        self.conv2 = quad_conv(planes, planes, 3, 1, 1, family)
+        self.bn2 = nn.BatchNorm2d(planes)
+        self.relu = nn.ReLU(inplace=True)
+        self.down = None
+        if stride != 1 or inplanes != planes:
+            self.down = nn.Sequential(nn.Conv2d(inplanes, planes, 1, stride, bias=False),
+                                      nn.BatchNorm2d(planes))
+
+    def forward(self, x):
+        idt = x if self.down is None else self.down(x)
+        out = self.relu(self.bn1(self.conv1(x)))
+        out = self.bn2(self.conv2(out))
+        return self.relu(out + idt)
+
+
+class QuadraResNet18(nn.Module):
+    def __init__(self, num_classes=1000, family="proposed"):
+        super().__init__()
+        self.stem = nn.Sequential(nn.Conv2d(3, 64, 7, 2, 3, bias=False), nn.BatchNorm2d(64),
+                                  nn.ReLU(inplace=True), nn.MaxPool2d(3, 2, 1))
+        blocks = []
+        inplanes = 64
+        for planes, stride in ((64, 1), (128, 2), (256, 2), (512, 2)):
+            for i in range(2):
+                blocks.append(QuadBasicBlock(inplanes, planes, stride if i == 0 else 1, family))
+                inplanes = planes
+        self.layers = nn.Sequential(*blocks)
+        self.pool = nn.AdaptiveAvgPool2d(1)
+        self.fc = nn.Linear(512, num_classes)
+
+    def forward(self, x):
+        x = self.layers(self.stem(x))
+        return self.fc(torch.flatten(self.pool(x), 1))
+
+
+def quad_layers(model):
+    return [m for m in model.modules() if isinstance(m, QuadConv2d)]
+
+
+def count_params(model):
+    return sum(p.numel() for p in model.parameters())

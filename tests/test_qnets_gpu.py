@@ -1,0 +1,60 @@
+"""QuadraVGG-16 / QuadraResNet-18 training steps on the B200 kernels."""
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _train(model, x, y, steps):
+    from paper_2204_01701_b200.dp import BucketedAllReduce, sgd
+    opt = sgd(model.parameters(), lr=0.02)
+    red = BucketedAllReduce(model.parameters())
+    losses = []
+    for _ in range(steps):
+        red.reset()
+        with torch.autocast("cuda", dtype=torch.bfloat16):
+            loss = torch.nn.functional.cross_entropy(model(x), y)
+        loss.backward()
+        red.finish()
+        opt.step()
+        losses.append(float(loss))
+    return losses
+
+
+def test_qvgg16_params_and_training():
+    from paper_2204_01701_b200 import qnets
+    torch.manual_seed(0)
+    m = qnets.QuadraVGG16(10).cuda().to(memory_format=torch.channels_last)
+    real = sum(p.numel() for p in m.parameters()) - 3 * 64 * 61 * 9  # minus the zero stem padding
+    assert abs(real - 44.16e6) / 44.16e6 < 0.01  # PAPER.md:781 (4.41E+7)
+    x = torch.randn(8, 3, 32, 32, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    y = torch.randint(0, 10, (8,), device="cuda")
+    losses = _train(m, x, y, 25)
+    assert all(l == l for l in losses)
+    assert losses[-1] < losses[0] * 0.5, losses
+
+
+def test_qresnet18_training():
+    from paper_2204_01701_b200 import qnets
+    torch.manual_seed(0)
+    m = qnets.QuadraResNet18(100).cuda().to(memory_format=torch.channels_last)
+    x = torch.randn(4, 3, 112, 112, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    y = torch.randint(0, 100, (4,), device="cuda")
+    losses = _train(m, x, y, 20)
+    assert all(l == l for l in losses)
+    assert losses[-1] < losses[0], losses
+
+
+def test_quad_layers_use_tcgen05():
+    from paper_2204_01701_b200 import neurons, qnets
+    from paper_2204_01701_b200.nn import QuadConv2d
+    m = qnets.QuadraResNet18(10).cuda().to(memory_format=torch.channels_last)
+    seen = []
+    hooks = [q.register_forward_pre_hook(lambda mod, inp: seen.append(
+        neurons.device_path(mod.spec, tuple(inp[0].shape)))) for q in m.modules() if isinstance(q, QuadConv2d)]
+    x = torch.randn(2, 3, 224, 224, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
+        m(x)
+    for h in hooks:
+        h.remove()
+    assert len(seen) == 16 and all(p == 1 for p in seen), seen
