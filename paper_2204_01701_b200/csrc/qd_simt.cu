@@ -27,8 +27,7 @@ static inline int grid_for(long long n, int bs = 256, int cap = 148 * 16) {
 }
 
 template <typename T>
-__global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
-  // blocks [0, nfb) pack the fprop layout, the rest the dgrad layout
+__global__ void pack_one_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
   long long nf = (long long)P.nb * P.F * P.Kf;
   int nfb = (int)((nf + 255) / 256);
   if ((int)blockIdx.x < nfb) {
@@ -61,9 +60,61 @@ __global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const 
   }
 }
 
+template <typename T>
+__global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const float* w2, T* out) {
+  // blocks [0, nfb) pack the fprop layout, the rest the dgrad layout; 4 consecutive
+  // k (same row, so the row decode is shared) per thread
+  const long long nf = (long long)P.nb * P.F * P.Kf;
+  const int nfb = (int)((nf / 4 + 255) / 256);
+  if ((int)blockIdx.x < nfb) {
+    long long i0 = ((long long)blockIdx.x * 256 + threadIdx.x) * 4;
+    if (i0 >= nf) return;
+    int R = (int)(i0 / P.Kf), k0 = (int)(i0 % P.Kf);
+    int grp = P.nb * P.FT;
+    int tile = R / grp, rem = R % grp;
+    int br = rem / P.FT, f = tile * P.FT + rem % P.FT;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int k = k0 + e, role = br, kk = k;
+      if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+      int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
+      const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+      float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                       : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+      out[i0 + e] = cvt<T>(v);
+    }
+  } else {
+    long long i0 = ((long long)(blockIdx.x - nfb) * 256 + threadIdx.x) * 4;
+    if (i0 >= (long long)P.Cd * P.Kd) return;
+    int cp = (int)(i0 / P.Kd), k0 = (int)(i0 % P.Kd);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      int k = k0 + e;
+      int ee = k / P.Jd, j = k % P.Jd;
+      int ey = ee / P.r, ex = ee % P.r, dy = P.r - 1 - ey, dx = P.r - 1 - ex;
+      int role, f, c;
+      if (P.sq == 2) { role = cp / P.C; c = cp % P.C; f = j; }
+      else { role = j / P.F; f = j % P.F; c = cp; }
+      const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+      float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                       : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+      out[nf + i0 + e] = cvt<T>(v);
+    }
+  }
+}
+
 void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
   long long nf = (long long)pack_fprop_elems(P), nd = (long long)pack_dgrad_elems(P);
-  int blocks = (int)((nf + 255) / 256 + (nd + 255) / 256);
+  if (P.Kf % 4 || P.Kd % 4) {  // rows not a multiple of 4: one element per thread
+    int blocks1 = (int)((nf + 255) / 256 + (nd + 255) / 256);
+    if (P.dtype == QD_BF16)
+      pack_one_kernel<bf16><<<blocks1, 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack);
+    else
+      pack_one_kernel<float><<<blocks1, 256, 0, st>>>(P, w[0], w[1], w[2], (float*)wpack);
+    count_launch(st, "pack");
+    return;
+  }
+  int blocks = (int)((nf / 4 + 255) / 256 + (nd / 4 + 255) / 256);
   if (P.dtype == QD_BF16)
     pack_all_kernel<bf16><<<blocks, 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack);
   else
@@ -456,25 +507,32 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
     int Sk = S;
     if (i4 < total && wsp.ng > 0) {
       int k = (int)(i4 % P.Kf), kk = k % P.K0;
-      int tap = kk / P.C;
-      Sk = wsp.s[(tap / 2) / wsp.pp];
+      int tg = (kk / P.C / 2) / wsp.pp;
+#pragma unroll
+      for (int t = 0; t < 16; ++t)  // static indexing: no local-memory copy of wsp
+        if (t == tg) Sk = wsp.s[t];
     }
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (i4 < total) {
       const float4* src = reinterpret_cast<const float4*>(wpart + i4);
       const long long stride4 = total / 4;
-      float4 acc2 = make_float4(0.f, 0.f, 0.f, 0.f);
+      // four independent chains (loads in flight), combined in a fixed order
+      float4 c1 = make_float4(0.f, 0.f, 0.f, 0.f), c2 = c1, c3 = c1;
       int s = grp;
-      for (; s + 8 < Sk; s += 16) {
-        float4 v = __ldg(src + s * stride4), u = __ldg(src + (s + 8) * stride4);
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        acc2.x += u.x; acc2.y += u.y; acc2.z += u.z; acc2.w += u.w;
+      for (; s + 24 < Sk; s += 32) {
+        float4 v0 = __ldg(src + s * stride4), v1 = __ldg(src + (s + 8) * stride4);
+        float4 v2 = __ldg(src + (s + 16) * stride4), v3 = __ldg(src + (s + 24) * stride4);
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        c1.x += v1.x; c1.y += v1.y; c1.z += v1.z; c1.w += v1.w;
+        c2.x += v2.x; c2.y += v2.y; c2.z += v2.z; c2.w += v2.w;
+        c3.x += v3.x; c3.y += v3.y; c3.z += v3.z; c3.w += v3.w;
       }
-      if (s < Sk) {
+      for (; s < Sk; s += 8) {
         float4 v = __ldg(src + s * stride4);
         acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
       }
-      acc.x += acc2.x; acc.y += acc2.y; acc.z += acc2.z; acc.w += acc2.w;
+      acc.x += c1.x + (c2.x + c3.x); acc.y += c1.y + (c2.y + c3.y);
+      acc.z += c1.z + (c2.z + c3.z); acc.w += c1.w + (c2.w + c3.w);
     }
     red4[grp][col] = acc;
     __syncthreads();

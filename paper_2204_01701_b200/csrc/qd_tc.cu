@@ -874,6 +874,29 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
                   P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st);
 }
 
+// side stream for work that can overlap the main chain (one per device/thread pair
+// would be more general; the library drives one device per process)
+static cudaStream_t g_side = nullptr;
+static cudaEvent_t g_fork = nullptr, g_join = nullptr;
+static cudaStream_t fork_side(cudaStream_t st) {
+  if (!g_side) {
+    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaGetLastError();
+      g_side = nullptr;
+      return nullptr;
+    }
+  }
+  cudaEventRecord(g_fork, st);
+  cudaStreamWaitEvent(g_side, g_fork, 0);
+  return g_side;
+}
+static void join_side(cudaStream_t st, cudaStream_t side) {
+  cudaEventRecord(g_join, side);
+  cudaStreamWaitEvent(st, g_join, 0);
+}
+
 int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
                 void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L,
                 cudaStream_t st) {
@@ -884,6 +907,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
   const bf16* D = (const bf16*)dy;
   float* bpart = (float*)(ws + L.off_BS);
+  cudaStream_t side = nullptr;
   if (mat || P.nbias || up) {
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
@@ -907,7 +931,11 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if (!(P.flags & QD_FLAG_TC_V1) && wgrad2_split(P) == L.wg_split)
       rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st);
     if (rc == QD_OK) {
-      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wgrad2_splits(P), dW, bpart, L.bs_split, db, st);
+      // the memory-bound fold overlaps the (smem-bound) dgrad: it runs on the side
+      // stream, forked after wgrad and joined before this call returns
+      side = fork_side(st);
+      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wgrad2_splits(P), dW, bpart, L.bs_split, db,
+                        side ? side : st);
     } else if (rc != QD_ERR_UNSUPPORTED) {
       return rc;
     } else {
@@ -956,6 +984,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
                     c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
     if (rc) return rc;
   }
+  if (side) join_side(st, side);
   return check_launch("tc backward");
 }
 

@@ -46,6 +46,7 @@ struct C2Args {
   uint32_t halo_bytes, halo_tx, b_stage_bytes;
   int b_slots, a_slots, stg_tiles;
   int nbias;  // bias vectors staged in smem (3 proposed, 1 first_order, else 0), Cout floats each
+  int direct;  // epilogue stores straight from registers (no smem staging)
   int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
   unsigned long long* trace;  // QD_TRACE (dev only): per-role clock64 timeline of cluster 0
   const float* bias0;
@@ -377,6 +378,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
     uint8_t* stg = NEPI == 8 ? sStg + (eg == 0 ? q * 4096 : 16384 + q * 8192) : sStg + q * g.stg_tiles * 4096;
     const bool multi = NEPI == 8 ? (o_end - o_beg > 1) : g.stg_tiles > 1;
     const bool tracer = q == 0 && eg == 0 && lane == 0;
+    const bool tracer1 = q == 0 && eg == 1 && lane == 0;
     const uint32_t tempty0 = c2::peer0(&tempty[0]);
     int it = 0;
     for (int w = cluster; w < g.total; w += nclusters, ++it) {
@@ -394,6 +396,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
       if (tracer) C2_TRACE(2, it, 0);
       ptx::mbar_wait(&tfull[acs], tph);
       if (tracer) C2_TRACE(2, it, 1);
+      if (tracer1) C2_TRACE(2, it, 10);
       ptx::tc_fence_after();
       if (g.dbg & 1) {
         __syncwarp();
@@ -401,6 +404,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         continue;
       }
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acs * ACC;
+      if ((EPI == E2_PROPOSED || EPI == E2_T4) && NEPI == 8 && eg == 1 && !g.direct) {
+        // a and b in one sweep: one TMEM round trip per 16 channels for both,
+        // only the two biases they need
+#pragma unroll 1
+        for (int jj = 0; jj < 4; ++jj) {
+          const int c0 = c_base + jj * 16;
+          float va[16], vb[16];
+          ptx::tmem_ld16(tb + jj * 16, va);
+          ptx::tmem_ld16(tb + 64 + jj * 16, vb);
+          if (EPI == E2_PROPOSED) {
+            const float4* pa = reinterpret_cast<const float4*>(sBias + c0);
+            const float4* pb = reinterpret_cast<const float4*>(sBias + g.Cout + c0);
+            float ba[16], bbv[16];
+#pragma unroll
+            for (int v4 = 0; v4 < 4; ++v4) {
+              float4 x0 = pa[v4], x1 = pb[v4];
+              ba[4 * v4] = x0.x; ba[4 * v4 + 1] = x0.y; ba[4 * v4 + 2] = x0.z; ba[4 * v4 + 3] = x0.w;
+              bbv[4 * v4] = x1.x; bbv[4 * v4 + 1] = x1.y; bbv[4 * v4 + 2] = x1.z; bbv[4 * v4 + 3] = x1.w;
+            }
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              va[e] += ba[e];
+              vb[e] += bbv[e];
+            }
+          } else {
+            ptx::tmem_wait_ld();
+          }
+          c2::stage16(stg, lane, jj, va);
+          c2::stage16(stg + 4096, lane, jj, vb);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
+        if (tracer1) C2_TRACE(2, it, 11);
+        __syncwarp();
+        c2_store_pass<EPI>(g, stg, 1, c_base, pix, lane);
+        c2_store_pass<EPI>(g, stg + 4096, 2, c_base, pix, lane);
+        __syncwarp();
+        if (tracer1) C2_TRACE(2, it, 12);
+        continue;
+      }
 #pragma unroll 1
       for (int o = o_beg; o < o_end; ++o) {
 #pragma unroll 1
@@ -494,7 +539,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
               if (NB == 2) out[e] += v1[e];
             }
           }
-          c2::stage16(stg + (multi ? (o - o_beg) * 4096 : 0), lane, jj, out);
+          if (g.direct) {
+            // 32 B of this row's output straight from registers (two 16-B stores)
+            if (pix >= 0) {
+              bf16* dst = (EPI == E2_PROPOSED || EPI == E2_T4) ? (o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2))
+                                                               : g.out0;
+              const int ch = ((EPI == E2_PLAIN) ? c_base + o * 64 : c_base) + jj * 16;
+              uint4 lo, hi;
+              lo.x = c2::pack2(out[0], out[1]);   lo.y = c2::pack2(out[2], out[3]);
+              lo.z = c2::pack2(out[4], out[5]);   lo.w = c2::pack2(out[6], out[7]);
+              hi.x = c2::pack2(out[8], out[9]);   hi.y = c2::pack2(out[10], out[11]);
+              hi.z = c2::pack2(out[12], out[13]); hi.w = c2::pack2(out[14], out[15]);
+              uint4* p = reinterpret_cast<uint4*>(dst + (size_t)pix * g.Cout + ch);
+              p[0] = lo;
+              p[1] = hi;
+            }
+          } else {
+            c2::stage16(stg + (multi ? (o - o_beg) * 4096 : 0), lane, jj, out);
+          }
         }
         if (tracer) C2_TRACE(2, it, 4 + 2 * o);
         if (o == o_end - 1) {
@@ -503,21 +565,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
           __syncwarp();
           if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
           if (tracer) C2_TRACE(2, it, 2);
+          if (tracer1) C2_TRACE(2, it, 11);
         }
-        if (!multi) {
+        if (!multi && !g.direct) {
           __syncwarp();
           c2_store_pass<EPI>(g, stg, o, c_base, pix, lane);
           __syncwarp();
           if (tracer) C2_TRACE(2, it, 5 + 2 * o);
         }
       }
-      if (multi) {
+      if (multi && !g.direct) {
         __syncwarp();
 #pragma unroll 1
         for (int o = o_beg; o < o_end; ++o) c2_store_pass<EPI>(g, stg + (o - o_beg) * 4096, o, c_base, pix, lane);
         __syncwarp();
       }
       if (tracer) C2_TRACE(2, it, 3);
+      if (tracer1) C2_TRACE(2, it, 12);
     }
   }
   ptx::tc_fence_before();
@@ -534,17 +598,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
 static unsigned long long* g_trace = nullptr;
 static unsigned long long* trace_buffer() {
   if (!g_trace) {
-    cudaMalloc(&g_trace, 3 * 64 * 16 * sizeof(unsigned long long));
+    cudaMalloc(&g_trace, 4096 * sizeof(unsigned long long));
   }
-  cudaMemset(g_trace, 0, 3 * 64 * 16 * sizeof(unsigned long long));
+  cudaMemset(g_trace, 0, 4096 * sizeof(unsigned long long));
   return g_trace;
 }
 }  // namespace qd
-// dev-only: copy the last QD_TRACE timeline (3 roles x 64 tiles x 16 events, clock64)
+// dev-only: copy the last QD_TRACE buffer (3 roles x 64 tiles x 16 events of clock64,
+// then per-CTA begin/end globaltimer pairs from slot 3072)
 extern "C" int qd_debug_trace_copy(unsigned long long* host) {
   if (!qd::g_trace) return -1;
   cudaDeviceSynchronize();
-  return (int)cudaMemcpy(host, qd::g_trace, 3 * 64 * 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return (int)cudaMemcpy(host, qd::g_trace, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 namespace qd {
 extern PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn();
@@ -672,6 +737,10 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   if (!g.b_contig && nbk != 2) return QD_ERR_UNSUPPORTED;
   g.out_c_tile = out_c_tile;
   g.ss = ss;
+  {
+    const char* e = getenv("QD_C2_DIRECT");
+    g.direct = e ? atoi(e) : 0;
+  }
   g.OHo = (OHg - 1) / ss + 1;
   g.OWo = (OWg - 1) / ss + 1;
   {
@@ -729,9 +798,16 @@ struct W2Args {
   unsigned long long* trace;  // QD_TRACE (dev only)
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
 __global__ void __launch_bounds__(256, 1)
     wgrad2_kernel(const __grid_constant__ CUtensorMap mX0, const __grid_constant__ CUtensorMap mX1,
                   const __grid_constant__ CUtensorMap mD, const W2Args g) {
+  if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) g.trace[3072 + 2 * blockIdx.x] = gtimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   const uint32_t stage_bytes = g.ntb * g.d_bytes + g.x_bytes;
@@ -870,6 +946,7 @@ __global__ void __launch_bounds__(256, 1)
   }
   ptx::tc_fence_before();
   __syncthreads();
+  if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) g.trace[3072 + 2 * blockIdx.x + 1] = gtimer();
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem, 512);

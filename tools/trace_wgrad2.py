@@ -18,12 +18,19 @@ for _ in range(3):
     y, cache = neurons.forward(spec, params, xt)
     neurons.symbolic_backward(spec, params, cache, gt, want_dx=False)
 torch.cuda.synchronize()
-buf = np.zeros(3 * 64 * 16, dtype=np.uint64)
+buf = np.zeros(4096, dtype=np.uint64)
 lib.qd_debug_trace_copy(buf.ctypes.data)
-T = buf.reshape(3, 64, 16).astype(np.int64)
+T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
+C = buf[3072:].reshape(-1, 2).astype(np.int64)
 t0 = T[T > 0].min()
 for i in range(24):
     p = T[0, i]; m = T[1, i]
     if not (p > 0).any():
         break
     print(f"qb {i:2d}: prod wait {p[0]-t0:7d}->{p[1]-t0:7d} | mma wait {m[0]-t0:7d}->{m[1]-t0:7d} issued {m[2]-t0:7d}")
+
+C = C[C[:, 0] > 0]
+t0 = C[:, 0].min()
+dur = (C[:, 1] - C[:, 0]) / 1e3
+print(f"CTAs {len(C)}: start spread {(C[:,0].max()-t0)/1e3:.2f} us, dur min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, kernel span {(C[:,1].max()-t0)/1e3:.1f} us")
+print("per-CTA durations (us):", " ".join(f"{d:.0f}" for d in dur))
