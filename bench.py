@@ -232,6 +232,8 @@ def run_ours(args, wl, wl_name):
 
     from oracle import quadra_oracle as Q  # seeded input generator only (not timed)
     x64, P64, g64 = Q.synthetic_layer(fam, kind, n, c, f, h, w, r, s, p, seed=rank)
+    if rank:  # replicas share rank 0's weights; inputs are per-rank shards
+        P64 = Q.synthetic_layer(fam, kind, 1, c, f, h, w, r, s, p, seed=0)[1]
     x = torch.as_tensor(x64, device=dev).to(dt)
     gy = torch.as_tensor(g64, device=dev).to(dt)
     if kind == "conv":
@@ -241,14 +243,22 @@ def run_ours(args, wl, wl_name):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def step(want_dx=True, want_dw=True):
+    def compute(want_dx=True, want_dw=True):
         y, cache = neurons.forward(spec, params, x, dtype=dt)
         grads, dx = neurons.symbolic_backward(spec, params, cache, gy, want_dx=want_dx,
                                               want_dw=want_dw)
-        if world > 1 and want_dw:
+        return y, grads, dx
+
+    def exchange(grads):
+        # the one data-parallel exchange: rank mean of dW / db.
+        # Kept outside the captured graph: NCCL runs eagerly after each replay.
+        if world > 1:
             flat = torch.cat([t_.reshape(-1) for t_ in grads.values()])
-            dist.all_reduce(flat)
-            flat.div_(world)
+            dist.all_reduce(flat, op=dist.ReduceOp.AVG)
+
+    def step():
+        y, grads, dx = compute()
+        exchange(grads)
         return y, grads, dx
 
     def timed(fn, k):
@@ -272,17 +282,20 @@ def run_ours(args, wl, wl_name):
     per_step_launches = _lib.launch_count() - l0
     run = step
     if not args.no_graph:
-        # the whole step (pack + fwd + bwd [+ gradient all-reduce]) as one CUDA graph:
+        # the whole compute step (pack + fwd + bwd) as one CUDA graph:
         # no host launch gaps between the ~8 kernels
         side = torch.cuda.Stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.stream(side):
-            step()
+            compute()
         torch.cuda.current_stream().wait_stream(side)
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
-            step()
-        run = graph.replay
+            _, g_static, _ = compute()
+
+        def run():
+            graph.replay()
+            exchange(g_static)
         for _ in range(args.warmup):
             run()
     torch.cuda.synchronize()
@@ -313,13 +326,13 @@ def run_ours(args, wl, wl_name):
     side = torch.cuda.Stream()
     side.wait_stream(torch.cuda.current_stream())
     with torch.cuda.stream(side):
-        step()
+        compute()
     torch.cuda.current_stream().wait_stream(side)
     torch.cuda.synchronize()
     lib.qd_profile(1)  # marks from here on: [begin, kernel_1, ..., kernel_k] of the captured step
     with torch.cuda.graph(pgraph):
         lib.qd_profile_mark(torch.cuda.current_stream().cuda_stream)
-        step()
+        compute()
     lib.qd_profile(0)
     acc = {}
     reps = max(5, args.steps)
@@ -381,6 +394,7 @@ def run_ours(args, wl, wl_name):
         pd = {k_: v.to(dev, non_blocking=True) for k_, v in w_h.items()}
         yy, cc = neurons.forward(spec, pd, xd, dtype=dt)
         grads, dxx = neurons.symbolic_backward(spec, pd, cc, gd)
+        exchange(grads)
         dx_h.copy_(dxx.contiguous() if kind == "fc" else dxx.permute(0, 1, 2, 3).contiguous(),
                    non_blocking=True)
         for k_, v in grads.items():
@@ -511,7 +525,7 @@ def run_net(args, name):
     import torch.distributed as dist
 
     from paper_2204_01701_b200 import _lib, qnets
-    from paper_2204_01701_b200.dp import BucketedAllReduce, sgd
+    from paper_2204_01701_b200.dp import BucketedAllReduce, broadcast_module, sgd
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -523,8 +537,9 @@ def run_net(args, name):
         dist.init_process_group("nccl", device_id=dev)
     builder, batch, hw, classes = NETS[name]
     batch = args.batch or batch
-    torch.manual_seed(1234 + rank)
+    torch.manual_seed(1234)
     model = getattr(qnets, builder)(num_classes=classes).to(dev).to(memory_format=torch.channels_last)
+    broadcast_module(model)  # every replica starts from rank 0's weights and BN buffers
     opt = sgd(model.parameters(), lr=0.01)
     red = BucketedAllReduce(model.parameters(), bucket_mb=25.0)
     gen = torch.Generator(device=dev).manual_seed(rank)

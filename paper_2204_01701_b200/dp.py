@@ -93,6 +93,15 @@ class BucketedAllReduce:
             h.remove()
 
 
+def broadcast_module(module, src=0, group=None):
+    """Copy rank ``src``'s parameters and buffers to every rank (replica start state)."""
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+        return
+    with torch.no_grad():
+        for t in list(module.parameters()) + list(module.buffers()):
+            dist.broadcast(t.data, src=src, group=group)
+
+
 def sgd(params, lr=0.1, momentum=0.9, weight_decay=5e-4):
     """The reference sgd_step (trainer.py:50-61) as torch's fused/foreach SGD."""
     return torch.optim.SGD(params, lr=lr, momentum=momentum, weight_decay=weight_decay, dampening=0.0,

@@ -37,8 +37,13 @@ def _worker(rank, world, port, out):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
-    from paper_2204_01701_b200.dp import BucketedAllReduce
+    from paper_2204_01701_b200.dp import BucketedAllReduce, broadcast_module
     m = _model()
+    if rank == 1:  # a diverged replica is reset to rank 0's weights
+        with torch.no_grad():
+            for p in m.parameters():
+                p.add_(1.0)
+    broadcast_module(m)
     red = BucketedAllReduce(m.parameters(), bucket_mb=0.001)  # ~260 floats: several buckets
     assert len(red.buckets) >= 3
     for step in range(2):
