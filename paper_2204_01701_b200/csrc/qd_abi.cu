@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // C-ABI entry points of libquadra_b200.so (declared in include/quadra_b200.h).
 // Validation mirrors the reference's error conventions; dispatch picks the
 // tcgen05 kernels when the shape tiles onto them and the generic CUDA-core
@@ -83,7 +84,11 @@ Workspace plan_workspace(const Plan& P, int path) {
   }
   L.sz_WG = (size_t)L.wg_split * P.Jd * P.Kf * 4;
   long long bs = (Pg.Mout + 255) / 256;
-  if (bs > 2 * 148) bs = 2 * 148;
+  {
+    const char* e = getenv("QD_BS_MULT");
+    int mult = e ? atoi(e) : 2;
+    if (bs > mult * 148) bs = mult * 148;
+  }
   if (bs < 1) bs = 1;
   L.bs_split = (int)bs;
   L.sz_BS = (size_t)L.bs_split * P.Jd * 4;

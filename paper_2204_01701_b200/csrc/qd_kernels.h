@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Host launchers shared between the translation units of libquadra_b200.so.
 #pragma once
 #include <cuda_runtime.h>
@@ -64,13 +65,18 @@ bool tc_supported(const Plan& P, unsigned flags);
 int tc_wgrad_split(const Plan& P);
 // v2 wgrad with halo reuse (qd_tc2.cu); wgrad2_split() == 0 when not eligible
 int wgrad2_split(const Plan& P);
+// Dtail / jsplit: D channel blocks >= jsplit are read from Dtail (the dy tensor) instead of D
 int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
-               cudaStream_t st);
+               cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0);
+// v3 wgrad (r = 3) on CTA pairs with multicast stage loads; 0 when not eligible
+int wgrad3_split(const Plan& P);
+int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
+               cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0);
 // v2 stride-1 conv on CTA pairs (qd_tc2.cu); QD_ERR_UNSUPPORTED if the shape does not fit
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st, int ss = 1);
+              const void* xres, cudaStream_t st, int ss = 1, const void* a_tail = nullptr, int csplit = 0);
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                 int tiles_nn, int Cout, int nbias);
 // stride-2 layers run as their stride-1 equivalent: forward subsamples the

@@ -476,7 +476,7 @@ __global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf1
                                                                const bf16* __restrict__ a,
                                                                const bf16* __restrict__ b, bf16* __restrict__ D,
                                                                float* __restrict__ part, long long rows_per,
-                                                               int up, int OH1, int OW1) {
+                                                               int up, int OH1, int OW1, int dstride) {
   const int F = P.F, chunks = F / 8;
   const int lanes = 256 / chunks;  // rows processed concurrently
   const int ch = threadIdx.x % chunks, rl = threadIdx.x / chunks;
@@ -523,10 +523,10 @@ __global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf1
           s1[2 * e] += y0; s1[2 * e + 1] += y1;
           s2[2 * e] += g.x; s2[2 * e + 1] += g.y;
         }
-        bf16* drow = D + (size_t)m * P.Jd + ch * 8;
+        bf16* drow = D + (size_t)m * dstride + ch * 8;
         *reinterpret_cast<uint4*>(drow) = d0;
         *reinterpret_cast<uint4*>(drow + F) = d1;
-        if (prop) *reinterpret_cast<uint4*>(drow + 2 * F) = gu[u];
+        if (prop && dstride == P.Jd) *reinterpret_cast<uint4*>(drow + 2 * F) = gu[u];
       }
     }
   } else if (rl < lanes) {
@@ -790,6 +790,8 @@ static int wgrad_ntile_blocks(int Jd) {
 
 int tc_wgrad_split(const Plan& P) {
   if (!(P.flags & QD_FLAG_TC_V1)) {
+    int s3 = wgrad3_split(P);
+    if (s3 > 0) return s3;
     int s2 = wgrad2_split(P);
     if (s2 > 0) return s2;
   }
@@ -908,12 +910,23 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   const bf16* D = (const bf16*)dy;
   float* bpart = (float*)(ws + L.off_BS);
   cudaStream_t side = nullptr;
+  // proposed, stride 1, both GEMMs on the v2 kernels: D holds only [g b, g a]
+  // and the consumers read its third block (g itself) straight from dy
+  const bool w3 = !(P.flags & QD_FLAG_TC_V1) && wgrad3_split(P) == L.wg_split;
+  const bool w2 = !w3 && !(P.flags & QD_FLAG_TC_V1) && wgrad2_split(P) == L.wg_split;
+  bool d2 = P.family == QD_FAM_PROPOSED && !up && dW[0] && (w2 || w3) && !getenv("QD_NO_D2");
+  if (d2 && dx) {
+    GemmCfg c = dgrad_cfg(P);
+    d2 = conv2_fits(P.N, P.Jd, P.OW, P.OH, P.W, P.H, P.r - 1 - P.p, P.r, 0, c.nbk, c.nout, c.tiles_nn, P.C, 0);
+  }
+  const int dsplit = d2 ? 2 * P.F / 64 : 0;
   if (mat || P.nbias || up) {
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
     bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;
     bwd_prologue_vec_kernel<<<L.bs_split, 256, 0, st>>>(P0, (const bf16*)dy, (const bf16*)a, (const bf16*)b, Dw,
-                                                        bpart, rows_per, up ? 1 : 0, P.OH, P.OW);
+                                                        bpart, rows_per, up ? 1 : 0, P.OH, P.OW,
+                                                        d2 ? 2 * P.F : P.Jd);
     count_launch(st, "prologue");
     if (mat || up) D = Dw;
   }
@@ -928,13 +941,22 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       x0 = xs;
     }
     rc = QD_ERR_UNSUPPORTED;
-    if (!(P.flags & QD_FLAG_TC_V1) && wgrad2_split(P) == L.wg_split)
-      rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st);
+    WSplits wsp;
+    memset(&wsp, 0, sizeof(wsp));
+    if (w3) {
+      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st, dy, dsplit);
+      wsp.pp = (P.r * P.r + 1) / 2;  // every tap in every split slot
+      wsp.ng = 1;
+      wsp.s[0] = L.wg_split;
+    } else if (w2) {
+      rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st, dy, dsplit);
+      wsp = wgrad2_splits(P);
+    }
     if (rc == QD_OK) {
       // the memory-bound fold overlaps the (smem-bound) dgrad: it runs on the side
       // stream, forked after wgrad and joined before this call returns
       side = fork_side(st);
-      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wgrad2_splits(P), dW, bpart, L.bs_split, db,
+      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wsp, dW, bpart, L.bs_split, db,
                         side ? side : st);
     } else if (rc != QD_ERR_UNSUPPORTED) {
       return rc;
@@ -978,7 +1000,9 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     rc = QD_ERR_UNSUPPORTED;
     if (!(P.flags & QD_FLAG_TC_V1))
       rc = run_conv2(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
-                     c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
+                     c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st, 1,
+                     dy, dsplit);
+    if (d2 && rc == QD_ERR_UNSUPPORTED) return set_error(QD_ERR_UNSUPPORTED, "dgrad conv2 plan changed");
     if (rc == QD_ERR_UNSUPPORTED && !up)
       rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
                     c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);

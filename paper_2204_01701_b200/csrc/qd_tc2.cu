@@ -47,6 +47,7 @@ struct C2Args {
   int b_slots, a_slots, stg_tiles;
   int nbias;  // bias vectors staged in smem (3 proposed, 1 first_order, else 0), Cout floats each
   int direct;  // epilogue stores straight from registers (no smem staging)
+  int csplit;  // A channel blocks >= csplit come from the second map (dgrad: D = [g b, g a] then dy)
   int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
   unsigned long long* trace;  // QD_TRACE (dev only): per-role clock64 timeline of cluster 0
   const float* bias0;
@@ -58,6 +59,11 @@ struct C2Args {
   const bf16* xres;
 };
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 namespace c2 {
 // dev-only timeline: slot = (role * 64 + tile) * 16 + event, CTA 0 only
 #define C2_TRACE(role, tile, ev)                                                                  \
@@ -125,6 +131,31 @@ __device__ __forceinline__ void stage16(uint8_t* tile, int row, int j, const flo
   *reinterpret_cast<uint4*>(rp + (((2 * j + 1) ^ (row & 7)) << 4)) = hi;
 }
 }  // namespace c2
+
+// 16 packed bf16 (channels 16j..16j+15 of a 32-channel half row) into a 32 x 64 B
+// staging tile; chunk c of row r stored at c ^ ((r >> 1) & 3) (conflict free for
+// row-per-lane writes and for the 4-lanes-per-row reads below)
+__device__ __forceinline__ void c2_stage_h(uint8_t* tile, int row, int j, const uint4& lo, const uint4& hi) {
+  uint8_t* rp = tile + row * 64;
+  const int f = (row >> 1) & 3;
+  *reinterpret_cast<uint4*>(rp + (((2 * j) ^ f) << 4)) = lo;
+  *reinterpret_cast<uint4*>(rp + (((2 * j + 1) ^ f) << 4)) = hi;
+}
+// coalesced store of one 32 x 64 B staging tile: 8 rows (8 x 64 B) per instruction
+__device__ __forceinline__ void c2_store_h(const C2Args& g, const uint8_t* st, bf16* dst, int ch, int pix,
+                                           int lane) {
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int Rw = 8 * i + (lane >> 2), c = lane & 3;
+    int rp = __shfl_sync(0xffffffffu, pix, Rw);
+    uint4 val = *reinterpret_cast<const uint4*>(st + Rw * 64 + ((c ^ ((Rw >> 1) & 3)) << 4));
+    if (rp >= 0) *reinterpret_cast<uint4*>(dst + (size_t)rp * g.Cout + ch + c * 8) = val;
+  }
+}
+__device__ __forceinline__ void c2_pack16(const float* v, uint4& lo, uint4& hi) {
+  lo = make_uint4(c2::pack2(v[0], v[1]), c2::pack2(v[2], v[3]), c2::pack2(v[4], v[5]), c2::pack2(v[6], v[7]));
+  hi = make_uint4(c2::pack2(v[8], v[9]), c2::pack2(v[10], v[11]), c2::pack2(v[12], v[13]), c2::pack2(v[14], v[15]));
+}
 
 // coalesced store of one 32 x 128 B warp staging tile: 4 rows (512 B) per instruction
 template <int EPI>
@@ -236,8 +267,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         if (leader) {
           C2_TRACE(0, it, 2 * ab + 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&afull[as], 2u * g.halo_tx);
-          c2::tma4_cg2(half ? &mA1 : &mA0, c2::peer0(&afull[as]), sHalo + as * g.halo_bytes, cb * 64, -g.pe,
-                       hq_lo - g.pe, n);
+          const bool tail = g.csplit && cb >= g.csplit;
+          c2::tma4_cg2((half || tail) ? &mA1 : &mA0, c2::peer0(&afull[as]), sHalo + as * g.halo_bytes,
+                       (tail ? cb - g.csplit : cb) * 64, -g.pe, hq_lo - g.pe, n);
         }
         if (++as == g.a_slots) { as = 0; aph ^= 1; }
         if (!g.resident) {
@@ -375,7 +407,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
     // passes of this warp: with two warpgroups, group 0 writes y and group 1 a, b
     const int o_beg = NEPI == 8 ? (eg == 0 ? 0 : 1) : 0;
     const int o_end = NEPI == 8 ? (eg == 0 ? 1 : 3) : NPASS;
-    uint8_t* stg = NEPI == 8 ? sStg + (eg == 0 ? q * 4096 : 16384 + q * 8192) : sStg + q * g.stg_tiles * 4096;
+    // proposed / t4: warp (eg, q) owns a 2 KB half-row staging tile; else stg_tiles 4 KB tiles
+    uint8_t* stg = NEPI == 8 ? sStg + (warp - 4) * 2048 : sStg + q * g.stg_tiles * 4096;
     const bool multi = NEPI == 8 ? (o_end - o_beg > 1) : g.stg_tiles > 1;
     const bool tracer = q == 0 && eg == 0 && lane == 0;
     const bool tracer1 = q == 0 && eg == 1 && lane == 0;
@@ -404,7 +437,65 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         continue;
       }
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acs * ACC;
-      if ((EPI == E2_PROPOSED || EPI == E2_T4) && NEPI == 8 && eg == 1 && !g.direct) {
+      if ((EPI == E2_PROPOSED || EPI == E2_T4) && NEPI == 8 && !g.direct) {
+        // warpgroup eg takes channels [32 eg, 32 eg + 32) of all three outputs:
+        // 2 x (a, b, c) TMEM loads, y / a / b packed to bf16 in registers, the
+        // accumulator handed back, then three 2 KB staged store passes
+        uint4 pk[3][2][2];  // [y|a|b][jj][lo|hi]
+#pragma unroll
+        for (int jj = 0; jj < 2; ++jj) {
+          const int col = eg * 32 + jj * 16;
+          const int c0 = c_base + col;
+          float va[16], vb[16], vc[16];
+          ptx::tmem_ld16(tb + col, va);
+          ptx::tmem_ld16(tb + 64 + col, vb);
+          if (EPI == E2_PROPOSED) {
+            ptx::tmem_ld16(tb + 128 + col, vc);
+            const float4* pa = reinterpret_cast<const float4*>(sBias + c0);
+            const float4* pb = reinterpret_cast<const float4*>(sBias + g.Cout + c0);
+            const float4* pc = reinterpret_cast<const float4*>(sBias + 2 * g.Cout + c0);
+            float ba[16], bbv[16], bc[16];
+#pragma unroll
+            for (int v4 = 0; v4 < 4; ++v4) {
+              float4 x0 = pa[v4], x1 = pb[v4], x2 = pc[v4];
+              ba[4 * v4] = x0.x; ba[4 * v4 + 1] = x0.y; ba[4 * v4 + 2] = x0.z; ba[4 * v4 + 3] = x0.w;
+              bbv[4 * v4] = x1.x; bbv[4 * v4 + 1] = x1.y; bbv[4 * v4 + 2] = x1.z; bbv[4 * v4 + 3] = x1.w;
+              bc[4 * v4] = x2.x; bc[4 * v4 + 1] = x2.y; bc[4 * v4 + 2] = x2.z; bc[4 * v4 + 3] = x2.w;
+            }
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+              va[e] += ba[e];
+              vb[e] += bbv[e];
+              vc[e] = fmaf(va[e], vb[e], vc[e] + bc[e]);
+            }
+          } else {
+            ptx::tmem_wait_ld();
+#pragma unroll
+            for (int e = 0; e < 16; ++e) vc[e] = va[e] * vb[e];
+          }
+          c2_pack16(vc, pk[0][jj][0], pk[0][jj][1]);
+          c2_pack16(va, pk[1][jj][0], pk[1][jj][1]);
+          c2_pack16(vb, pk[2][jj][0], pk[2][jj][1]);
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
+        if (tracer) C2_TRACE(2, it, 2);
+        if (tracer1) C2_TRACE(2, it, 11);
+#pragma unroll
+        for (int o = 0; o < 3; ++o) {
+          c2_stage_h(stg, lane, 0, pk[o][0][0], pk[o][0][1]);
+          c2_stage_h(stg, lane, 1, pk[o][1][0], pk[o][1][1]);
+          __syncwarp();
+          c2_store_h(g, stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), c_base + eg * 32, pix, lane);
+          __syncwarp();
+        }
+        if (tracer) C2_TRACE(2, it, 3);
+        if (tracer1) C2_TRACE(2, it, 12);
+        continue;
+      }
+      if (false) {
         // a and b in one sweep: one TMEM round trip per 16 channels for both,
         // only the two biases they need
 #pragma unroll 1
@@ -604,6 +695,21 @@ static unsigned long long* trace_buffer() {
   return g_trace;
 }
 }  // namespace qd
+// dev-only: spin `cycles` SM clocks on every SM and record clock64 / globaltimer
+// at both ends of block 0 into out[4] (clock-rate probe under the caller's load)
+__global__ void qd_spin_kernel(long long cycles, unsigned long long* out) {
+  unsigned long long c0 = clock64(), t0 = qd::gtimer();
+  while ((long long)(clock64() - c0) < cycles) {
+  }
+  unsigned long long c1 = clock64(), t1 = qd::gtimer();
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    out[0] = c0; out[1] = c1; out[2] = t0; out[3] = t1;
+  }
+}
+extern "C" int qd_debug_spin(long long cycles, unsigned long long* dev_out, void* stream) {
+  qd_spin_kernel<<<148, 32, 0, (cudaStream_t)stream>>>(cycles, dev_out);
+  return (int)cudaGetLastError();
+}
 // dev-only: copy the last QD_TRACE buffer (3 roles x 64 tiles x 16 events of clock64,
 // then per-CTA begin/end globaltimer pairs from slot 3072)
 extern "C" int qd_debug_trace_copy(unsigned long long* host) {
@@ -612,6 +718,29 @@ extern "C" int qd_debug_trace_copy(unsigned long long* host) {
   return (int)cudaMemcpy(host, qd::g_trace, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 namespace qd {
+// co-resident clusters of size 2 for a kernel at this smem / block size (cached per kernel)
+template <typename K>
+static int max_pair_clusters(K kernel, int threads, size_t smem) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = dim3(2 * 148, 1, 1);
+  cfg.blockDim = dim3(threads, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, (void*)kernel, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    n = 0;
+  }
+  if (getenv("QD_VERBOSE")) fprintf(stderr, "[qd] max active 2-CTA clusters: %d (smem %zu)\n", n, smem);
+  return n;
+}
 extern PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn();
 extern int tc_num_sms();
 
@@ -661,7 +790,8 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   uint32_t bstage = NB * 32 * 128;
   // staging: one 4 KB tile per warp per output pass (single epilogue pass over TMEM,
   // stores after the hand-back) when smem allows, else one tile reused per pass
-  int stg_tiles = NOUT;
+  // (proposed / t4: 8 warps x 2 KB half-row tiles = 4 x 4 KB)
+  int stg_tiles = NOUT == 3 ? 1 : NOUT;
   {
     const char* e = getenv("QD_C2_STG");
     if (e && NOUT != 3) stg_tiles = atoi(e) > 1 ? NOUT : 1;
@@ -707,7 +837,16 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
     cudaFuncSetAttribute(conv2_kernel<EPI, NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr_smem = (int)pl.smem;
   }
+  // persistent grid: only as many pairs as can be co-resident (GPCs with an odd
+  // number of free SMs cannot host a pair; a second wave would double the time)
+  static int maxc = 0;
+  static size_t maxc_smem = 0;
+  if (maxc == 0 || maxc_smem != pl.smem) {
+    maxc = max_pair_clusters(conv2_kernel<EPI, NB, R>, C2Threads<EPI, NB>::THREADS, pl.smem);
+    maxc_smem = pl.smem;
+  }
   int clusters = tc_num_sms() / 2;
+  if (maxc > 0 && maxc < clusters) clusters = maxc;
   if (pl.g.total < clusters) clusters = pl.g.total;
   conv2_kernel<EPI, NB, R><<<2 * clusters, C2Threads<EPI, NB>::THREADS, pl.smem, st>>>(A0, A1, B, pl.g);
   count_launch(st, "conv2");
@@ -725,7 +864,7 @@ static int c2_launch(const CUtensorMap& A0, const CUtensorMap& A1, const CUtenso
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st, int ss) {
+              const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit) {
   int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
   int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
   C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
@@ -753,10 +892,18 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   g.xres = (const bf16*)xres;
   CUtensorMap A0, A1, B;
   int rc;
-  cuuint64_t dA[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)N};
   cuuint32_t bA[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.HR, 1};
-  if ((rc = c2_map(&A0, a0, 4, dA, bA))) return rc;
-  if ((rc = c2_map(&A1, a1 ? a1 : a0, 4, dA, bA))) return rc;
+  g.csplit = (a_tail && csplit > 0 && csplit < Cin / 64) ? csplit : 0;
+  if (g.csplit) {
+    cuuint64_t d0[4] = {(cuuint64_t)(64 * g.csplit), (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)N};
+    cuuint64_t d1[4] = {(cuuint64_t)(Cin - 64 * g.csplit), (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)N};
+    if ((rc = c2_map(&A0, a0, 4, d0, bA))) return rc;
+    if ((rc = c2_map(&A1, a_tail, 4, d1, bA))) return rc;
+  } else {
+    cuuint64_t dA[4] = {(cuuint64_t)Cin, (cuuint64_t)Win, (cuuint64_t)Hin, (cuuint64_t)N};
+    if ((rc = c2_map(&A0, a0, 4, dA, bA))) return rc;
+    if ((rc = c2_map(&A1, a1 ? a1 : a0, 4, dA, bA))) return rc;
+  }
   cuuint64_t dB[2] = {(cuuint64_t)wK, (cuuint64_t)wrows};
   cuuint32_t bB[2] = {64, (cuuint32_t)(nbk * 32)};
   if ((rc = c2_map(&B, wmat, 2, dB, bB))) return rc;
@@ -794,19 +941,16 @@ struct W2Args {
   int gstart[17];           // prefix sums of gsplit
   uint32_t d_tx, x_tx, d_bytes, x_bytes;  // d_* per 64-j box
   int stages;
+  int jsplit;  // D channel blocks >= jsplit are loaded from the second D map (dy)
   float* part;
   unsigned long long* trace;  // QD_TRACE (dev only)
 };
 
-__device__ __forceinline__ unsigned long long gtimer() {
-  unsigned long long t;
-  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-  return t;
-}
 
 __global__ void __launch_bounds__(256, 1)
     wgrad2_kernel(const __grid_constant__ CUtensorMap mX0, const __grid_constant__ CUtensorMap mX1,
-                  const __grid_constant__ CUtensorMap mD, const W2Args g) {
+                  const __grid_constant__ CUtensorMap mD, const __grid_constant__ CUtensorMap mD1,
+                  const W2Args g) {
   if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) g.trace[3072 + 2 * blockIdx.x] = gtimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -837,6 +981,7 @@ __global__ void __launch_bounds__(256, 1)
     ptx::prefetch_tmap(&mX0);
     ptx::prefetch_tmap(&mX1);
     ptx::prefetch_tmap(&mD);
+    if (g.jsplit) ptx::prefetch_tmap(&mD1);
     for (int i = 0; i < g.stages; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 1);
@@ -866,8 +1011,13 @@ __global__ void __launch_bounds__(256, 1)
         C2_TRACE(0, qb - q_beg, 1);
         uint8_t* s = sm + st * stage_bytes;
         ptx::mbar_arrive_expect_tx(&full[st], g.ntb * g.d_tx + g.x_tx);
-        for (int i = 0; i < g.ntb; ++i)
-          ptx::tma_load_4d(&mD, &full[st], s + i * g.d_bytes, (jt * g.ntb + i) * 64, 0, hq_lo, n);
+        for (int i = 0; i < g.ntb; ++i) {
+          const int jb = jt * g.ntb + i;
+          if (g.jsplit && jb >= g.jsplit)
+            ptx::tma_load_4d(&mD1, &full[st], s + i * g.d_bytes, (jb - g.jsplit) * 64, 0, hq_lo, n);
+          else
+            ptx::tma_load_4d(&mD, &full[st], s + i * g.d_bytes, jb * 64, 0, hq_lo, n);
+        }
         ptx::tma_load_4d(half ? &mX1 : &mX0, &full[st], s + g.ntb * g.d_bytes, cb * 64, -g.pe, hq_lo - g.pe, n);
       }
       __syncwarp();
@@ -1032,6 +1182,336 @@ static W2Plan w2_plan(const Plan& P) {
   return pl;
 }
 
+// ===========================================================================
+// K4 v3 (r = 3): wgrad on CTA pairs sharing every stage load.
+//   Both CTAs of a cluster walk the same q blocks; each issues half of the
+//   stage's TMA boxes (D boxes, x halo) multicast to both, so D and x are read
+//   from L2 once per pair instead of once per tap group. CTA r accumulates tap
+//   pairs {2r, 2r+1} over the whole N tile plus the ninth tap over its share
+//   of the N boxes (CTA0: the first ntb/2 boxes, CTA1: the rest), so the
+//   pair's TMEM holds every tap: 2 NT + ceil(ntb/2) 64 <= 512 columns.
+//   Stage release needs both CTAs' MMAs: each commit is multicast to both
+//   CTAs' empty barriers (count 2). Partials: one slot per cluster.
+// ===========================================================================
+struct W3Args {
+  int N, OHg, OWg, Jd, Kf, K0, C;
+  int pe, Wp, RD, RX;
+  int T_img, cblks, ablocks, jtiles, nsplit;
+  int NT, ntb;
+  uint32_t d_tx, x_tx, d_bytes, x_bytes;
+  int stages;
+  int jsplit;
+  float* part;
+  unsigned long long* trace;  // QD_TRACE (dev only)
+};
+
+__device__ __forceinline__ void w3_tma4_mc(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2,
+                                           int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2], %7;" ::"r"(ptx::smem_u32(dst)),
+      "l"(m), "r"(ptx::smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void w3_commit_mc(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+          ptx::smem_u32(bar)),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    wgrad3_kernel(const __grid_constant__ CUtensorMap mX0, const __grid_constant__ CUtensorMap mX1,
+                  const __grid_constant__ CUtensorMap mD, const __grid_constant__ CUtensorMap mD1,
+                  const W3Args g) {
+  if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) {
+    g.trace[3072 + 2 * blockIdx.x] = gtimer();
+    g.trace[2048 + 2 * blockIdx.x] = clock64();
+  }
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  const uint32_t stage_bytes = g.ntb * g.d_bytes + g.x_bytes;
+  uint64_t* full = (uint64_t*)(sm + g.stages * stage_bytes);
+  uint64_t* empty = full + g.stages;
+  uint64_t* done = empty + g.stages;
+  uint32_t* tslot = (uint32_t*)(done + 1);
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = c2::cluster_rank();
+  int b = blockIdx.x >> 1;
+  const int jt = b % g.jtiles;
+  b /= g.jtiles;
+  const int ab = b % g.ablocks;
+  const int split = b / g.ablocks;
+  const int half = ab / g.cblks, cb = ab % g.cblks;
+  const int nblk = g.N * g.T_img;
+  const int q_beg = (int)((long long)split * nblk / g.nsplit);
+  const int q_end = (int)((long long)(split + 1) * nblk / g.nsplit);
+  // ninth tap: CTA r takes N boxes [nlo, nhi)
+  const int nlo = rank == 0 ? 0 : g.ntb / 2;
+  const int nhi = rank == 0 ? g.ntb / 2 : g.ntb;
+
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(&mX0);
+    ptx::prefetch_tmap(&mX1);
+    ptx::prefetch_tmap(&mD);
+    if (g.jsplit) ptx::prefetch_tmap(&mD1);
+    for (int i = 0; i < g.stages; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 2);
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) {
+    ptx::tmem_alloc(tslot, 512);
+    ptx::tmem_relinquish();
+  }
+  ptx::tc_fence_before();
+  c2::cluster_sync();  // barriers of both CTAs initialised before any multicast lands
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tslot;
+
+  if (warp == 0) {
+    const bool leader = ptx::elect_one();
+    int st = 0;
+    uint32_t ph = 0;
+    // box i < ntb: D box i; i == ntb: the x halo. CTA0 issues [0, nsh), CTA1 the rest.
+    const int nsh = (g.ntb + 1) / 2;
+    for (int qb = q_beg; qb < q_end; ++qb) {
+      int n = qb / g.T_img, t = qb % g.T_img;
+      int hq_lo = (128 * t) / g.Wp;
+      if (leader) C2_TRACE(0, qb - q_beg, 0);
+      ptx::mbar_wait(&empty[st], ph ^ 1);
+      if (leader) {
+        C2_TRACE(0, qb - q_beg, 1);
+        uint8_t* s = sm + st * stage_bytes;
+        ptx::mbar_arrive_expect_tx(&full[st], g.ntb * g.d_tx + g.x_tx);
+        const int i0 = rank == 0 ? 0 : nsh, i1 = rank == 0 ? nsh : g.ntb + 1;
+        for (int i = i0; i < i1; ++i) {
+          if (i == g.ntb) {
+            w3_tma4_mc(half ? &mX1 : &mX0, &full[st], s + g.ntb * g.d_bytes, cb * 64, -g.pe, hq_lo - g.pe, n);
+          } else {
+            const int jb = jt * g.ntb + i;
+            if (g.jsplit && jb >= g.jsplit)
+              w3_tma4_mc(&mD1, &full[st], s + i * g.d_bytes, (jb - g.jsplit) * 64, 0, hq_lo, n);
+            else
+              w3_tma4_mc(&mD, &full[st], s + i * g.d_bytes, jb * 64, 0, hq_lo, n);
+          }
+        }
+      }
+      __syncwarp();
+      if (++st == g.stages) { st = 0; ph ^= 1; }
+    }
+  } else if (warp == 1) {
+    const uint32_t IDESC = ptx::idesc_bf16(128, g.NT, true, true);
+    const uint32_t IDESC9 = ptx::idesc_bf16(128, (nhi - nlo) * 64, true, true);
+    constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
+    const bool leader = ptx::elect_one();
+    const uint32_t s_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sm), 0);
+    const uint32_t d_lbo = (g.d_bytes >> 4) << 16;
+    // tap offsets in the halo (rows): pairs {2r, 2r+1}, {2r+2... } of this CTA; tap 8 = (2, 2)
+    const int ta = 4 * (int)rank;  // taps ta .. ta+3
+    int off[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) off[i] = ((ta + i) / 3) * g.Wp + (ta + i) % 3;
+    const int off8 = 2 * g.Wp + 2;
+    int st = 0;
+    uint32_t ph = 0;
+    uint32_t accum = 0;
+    for (int qb = q_beg; qb < q_end; ++qb) {
+      int t = qb % g.T_img;
+      int q0 = 128 * t;
+      int row_off = q0 - (q0 / g.Wp) * g.Wp;
+      if (leader) C2_TRACE(1, qb - q_beg, 0);
+      ptx::mbar_wait(&full[st], ph);
+      if (leader) C2_TRACE(1, qb - q_beg, 1);
+      ptx::tc_fence_after();
+      const uint32_t base = s_lo0 + st * (stage_bytes >> 4);
+      const uint32_t d_lo = base + row_off * 8 + d_lbo;
+      const uint32_t x_lo = base + ((g.ntb * g.d_bytes) >> 4) + row_off * 8;
+      if (leader) {
+#pragma unroll
+        for (int pr = 0; pr < 2; ++pr) {
+          const int o0 = off[2 * pr], o1 = off[2 * pr + 1];
+          const uint32_t a_lo = x_lo + o0 * 8 + ((uint32_t)((o1 - o0) * 8) << 16);
+          const uint32_t dt = tmem + pr * g.NT;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::mma_bf16(dt, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, d_lo + 128 * k), IDESC,
+                          accum | (uint32_t)k);
+        }
+        if (nhi > nlo) {
+          const uint32_t a_lo = x_lo + off8 * 8;  // both 64-row atoms: tap 8 (second discarded)
+          const uint32_t b_lo = d_lo + nlo * (g.d_bytes >> 4);
+          const uint32_t dt = tmem + 2 * g.NT;
+#pragma unroll
+          for (int k = 0; k < 8; ++k)
+            ptx::mma_bf16(dt, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, b_lo + 128 * k), IDESC9,
+                          accum | (uint32_t)k);
+        }
+        w3_commit_mc(&empty[st]);
+        C2_TRACE(1, qb - q_beg, 2);
+      }
+      accum = 1;
+      __syncwarp();
+      if (++st == g.stages) { st = 0; ph ^= 1; }
+    }
+    if (leader) ptx::mma_commit(done);
+    __syncwarp();
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const bool has_work = q_end > q_beg;
+    if (has_work) {
+      ptx::mbar_wait(done, 0);
+      ptx::tc_fence_after();
+    }
+    float* dst = g.part + (size_t)split * g.Jd * g.Kf;
+    // accumulators: 0, 1 = tap pairs of this CTA over NT; 2 = tap 8 over boxes [nlo, nhi)
+    for (int acc = 0; acc < 3; ++acc) {
+      int tap, c_lo, c_hi;
+      if (acc < 2) {
+        tap = 4 * (int)rank + 2 * acc + (row < 64 ? 0 : 1);
+        c_lo = 0;
+        c_hi = g.NT;
+      } else {
+        tap = 8;
+        c_lo = nlo * 64;
+        c_hi = nhi * 64;
+        if (q >= 2) continue;  // rows 64..127 hold the duplicate atom (warp-uniform skip)
+      }
+      const bool ok = c_hi > c_lo;
+      const int k = half * g.K0 + tap * g.C + cb * 64 + (row & 63);
+      const int ncols = (acc < 2) ? g.NT : (nhi - nlo) * 64;
+#pragma unroll 1
+      for (int c = 0; c < ncols; c += 16) {
+        float v[16];
+        if (has_work) {
+          ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * g.NT + c, v);
+          ptx::tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int e = 0; e < 16; ++e) v[e] = 0.f;
+        }
+        if (ok) {
+          const int j0 = jt * g.NT + c_lo + c;
+#pragma unroll
+          for (int e = 0; e < 16; ++e) dst[(size_t)(j0 + e) * g.Kf + k] = v[e];
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  c2::cluster_sync();  // no CTA exits while its partner may still multicast into it
+  if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) {
+    g.trace[3072 + 2 * blockIdx.x + 1] = gtimer();
+    g.trace[2048 + 2 * blockIdx.x + 1] = clock64();
+  }
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+struct W3Plan {
+  bool ok;
+  W3Args g;
+  size_t smem;
+};
+
+static W3Plan w3_plan(const Plan& P) {
+  W3Plan pl;
+  memset(&pl, 0, sizeof(pl));
+  W3Args& g = pl.g;
+  if (getenv("QD_NO_W3")) return pl;
+  if (P.s != 1 || P.r != 3 || P.C % 64 || P.Jd % 64) return pl;
+  int Wp = P.W + 2 * P.p;
+  if (P.OW != Wp - P.r + 1 || Wp > 256 || P.OW < 12) return pl;
+  int T_img = (P.OH * Wp + 127) / 128;
+  int RD = 0, RX = 0;
+  for (int t = 0; t < T_img; ++t) {
+    int q0 = 128 * t, lo = q0 / Wp;
+    int hd = (q0 + 127) / Wp, hx = (q0 + 127 + (P.r - 1) * (Wp + 1)) / Wp;
+    if (hd - lo + 1 > RD) RD = hd - lo + 1;
+    if (hx - lo + 1 > RX) RX = hx - lo + 1;
+  }
+  if (RX > 256) return pl;
+  uint32_t d_tx = (uint32_t)Wp * RD * 128, x_tx = (uint32_t)Wp * RX * 128;
+  uint32_t d_bytes = (d_tx + 1023) / 1024 * 1024, x_bytes = (x_tx + 1023) / 1024 * 1024;
+  int ntb = 0, stages = 0;
+  for (int c = 3; c >= 1; --c) {  // 2 NT + ceil(c/2) 64 <= 512
+    if ((P.Jd / 64) % c) continue;
+    uint32_t stg = c * d_bytes + x_bytes;
+    int sn = (int)((212 * 1024) / stg);
+    if (sn >= 2) { ntb = c; stages = sn > 4 ? 4 : sn; break; }
+  }
+  // narrow N tiles (wide images) re-read x per j tile and run N = 64 MMAs: wgrad2 is better there
+  if (ntb < 2) return pl;
+  g.N = P.N; g.OHg = P.OH; g.OWg = P.OW; g.Jd = P.Jd; g.Kf = P.Kf; g.K0 = P.K0; g.C = P.C;
+  g.pe = P.p; g.Wp = Wp; g.RD = RD; g.RX = RX;
+  g.T_img = T_img; g.cblks = P.C / 64; g.ablocks = g.cblks * (P.sq == 2 ? 2 : 1);
+  g.NT = ntb * 64; g.ntb = ntb; g.jtiles = P.Jd / g.NT;
+  const int nblk = P.N * T_img;
+  pl.smem = 1024 + (size_t)stages * (ntb * d_bytes + x_bytes) + 1024;
+  static int maxc = 0;
+  static size_t maxc_smem = 0;
+  if (maxc == 0 || maxc_smem != pl.smem) {
+    cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    maxc = max_pair_clusters(wgrad3_kernel, 256, pl.smem);
+    maxc_smem = pl.smem;
+  }
+  int pairs = tc_num_sms() / 2;
+  if (maxc > 0 && maxc < pairs) pairs = maxc;
+  int ns = pairs / (g.jtiles * g.ablocks);
+  if (ns < 1) ns = 1;
+  if (ns > nblk) ns = nblk;
+  g.nsplit = ns;
+  g.d_tx = d_tx; g.x_tx = x_tx; g.d_bytes = d_bytes; g.x_bytes = x_bytes; g.stages = stages;
+  pl.smem = 1024 + (size_t)stages * (ntb * d_bytes + x_bytes) + 1024;
+  pl.ok = true;
+  return pl;
+}
+
+int wgrad3_split(const Plan& P) {
+  W3Plan pl = w3_plan(P);
+  return pl.ok ? pl.g.nsplit : 0;
+}
+
+int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
+               cudaStream_t st, const void* Dtail, int jsplit) {
+  W3Plan pl = w3_plan(P);
+  if (!pl.ok || pl.g.nsplit != splits) return QD_ERR_UNSUPPORTED;
+  W3Args& g = pl.g;
+  g.part = part;
+  g.trace = getenv("QD_TRACE") ? trace_buffer() : nullptr;
+  CUtensorMap X0, X1, Dm, Dm1;
+  int rc;
+  cuuint64_t dX[4] = {(cuuint64_t)P.C, (cuuint64_t)P.W, (cuuint64_t)P.H, (cuuint64_t)P.N};
+  cuuint32_t bX[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RX, 1};
+  if ((rc = c2_map(&X0, x0, 4, dX, bX))) return rc;
+  if ((rc = c2_map(&X1, x1 ? x1 : x0, 4, dX, bX))) return rc;
+  g.jsplit = (Dtail && jsplit > 0 && jsplit < P.Jd / 64) ? jsplit : 0;
+  cuuint64_t dD[4] = {(cuuint64_t)(g.jsplit ? 64 * g.jsplit : P.Jd), (cuuint64_t)P.OW, (cuuint64_t)P.OH,
+                      (cuuint64_t)P.N};
+  cuuint32_t bD[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RD, 1};
+  if ((rc = c2_map(&Dm, D, 4, dD, bD))) return rc;
+  Dm1 = Dm;
+  if (g.jsplit) {
+    cuuint64_t d1[4] = {(cuuint64_t)(P.Jd - 64 * g.jsplit), (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
+    if ((rc = c2_map(&Dm1, Dtail, 4, d1, bD))) return rc;
+  }
+  static int attr = 0;
+  if ((int)pl.smem > attr) {
+    cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    attr = (int)pl.smem;
+  }
+  wgrad3_kernel<<<2 * g.jtiles * g.ablocks * g.nsplit, 256, pl.smem, st>>>(X0, X1, Dm, Dm1, g);
+  if (getenv("QD_W3_TWICE")) wgrad3_kernel<<<2 * g.jtiles * g.ablocks * g.nsplit, 256, pl.smem, st>>>(X0, X1, Dm, Dm1, g);
+  count_launch(st, "wgrad3");
+  return check_launch("wgrad3");
+}
+
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                 int tiles_nn, int Cout, int nbias) {
   return c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, nout, tiles_nn, Cout, nbias).ok;
@@ -1054,27 +1534,34 @@ WSplits wgrad2_splits(const Plan& P) {
 }
 
 int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
-               cudaStream_t st) {
+               cudaStream_t st, const void* Dtail, int jsplit) {
   W2Plan pl = w2_plan(P);
   if (!pl.ok || pl.g.splits != splits) return QD_ERR_UNSUPPORTED;
   W2Args& g = pl.g;
   g.part = part;
   g.trace = getenv("QD_TRACE") ? trace_buffer() : nullptr;
-  CUtensorMap X0, X1, Dm;
+  CUtensorMap X0, X1, Dm, Dm1;
   int rc;
   cuuint64_t dX[4] = {(cuuint64_t)P.C, (cuuint64_t)P.W, (cuuint64_t)P.H, (cuuint64_t)P.N};
   cuuint32_t bX[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RX, 1};
   if ((rc = c2_map(&X0, x0, 4, dX, bX))) return rc;
   if ((rc = c2_map(&X1, x1 ? x1 : x0, 4, dX, bX))) return rc;
-  cuuint64_t dD[4] = {(cuuint64_t)P.Jd, (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
+  g.jsplit = (Dtail && jsplit > 0 && jsplit < P.Jd / 64) ? jsplit : 0;
+  cuuint64_t dD[4] = {(cuuint64_t)(g.jsplit ? 64 * g.jsplit : P.Jd), (cuuint64_t)P.OW, (cuuint64_t)P.OH,
+                      (cuuint64_t)P.N};
   cuuint32_t bD[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RD, 1};
   if ((rc = c2_map(&Dm, D, 4, dD, bD))) return rc;
+  Dm1 = Dm;
+  if (g.jsplit) {
+    cuuint64_t d1[4] = {(cuuint64_t)(P.Jd - 64 * g.jsplit), (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
+    if ((rc = c2_map(&Dm1, Dtail, 4, d1, bD))) return rc;
+  }
   static int attr = 0;
   if ((int)pl.smem > attr) {
     cudaFuncSetAttribute(wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr = (int)pl.smem;
   }
-  wgrad2_kernel<<<g.jtiles * g.ablocks * g.gstart[g.tgroups], 256, pl.smem, st>>>(X0, X1, Dm, g);
+  wgrad2_kernel<<<g.jtiles * g.ablocks * g.gstart[g.tgroups], 256, pl.smem, st>>>(X0, X1, Dm, Dm1, g);
   count_launch(st, "wgrad2");
   return check_launch("wgrad2");
 }

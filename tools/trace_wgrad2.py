@@ -23,7 +23,7 @@ lib.qd_debug_trace_copy(buf.ctypes.data)
 T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
 C = buf[3072:].reshape(-1, 2).astype(np.int64)
 t0 = T[T > 0].min()
-for i in range(24):
+for i in range(20):
     p = T[0, i]; m = T[1, i]
     if not (p > 0).any():
         break
