@@ -43,6 +43,39 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   }
 }
 
+// one lane polls, the warp then synchronises: a warp-wide try_wait loop puts 32x
+// the polling traffic on the barrier unit (and slowed other warps' waits, traced)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  if ((threadIdx.x & 31) == 0) mbar_wait(bar, parity);
+  __syncwarp();
+}
+
+// ---- division by a runtime-constant divisor (multiply-high + shift) --------------
+// For 0 <= x < 2^31 and d >= 1: q = umulhi(x, mul) >> shr with mul = ceil(2^p / d),
+// p = 31 + ceil(log2 d) (d == 1: identity). Set up on the host.
+struct FastDiv {
+  int d;
+  unsigned mul, shr;
+};
+inline FastDiv make_fastdiv(int d) {
+  FastDiv f;
+  f.d = d;
+  if (d <= 1) {
+    f.mul = 0;
+    f.shr = 0;
+    return f;
+  }
+  unsigned l = 0;
+  while ((1u << l) < (unsigned)d) ++l;
+  unsigned p = 31 + l;
+  f.mul = (unsigned)(((1ull << p) + (unsigned)d - 1) / (unsigned)d);
+  f.shr = p - 32;
+  return f;
+}
+__device__ __forceinline__ int fdiv(int x, const FastDiv& f) {
+  return f.d == 1 ? x : (int)(__umulhi((unsigned)x, f.mul) >> f.shr);
+}
+
 // ---- TMA ---------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");

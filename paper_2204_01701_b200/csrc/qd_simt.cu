@@ -103,8 +103,68 @@ __global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const 
   }
 }
 
+// conv, no squared operand: one block per packed row, the row's source block staged in
+// smem so both the reads of w and the writes of the packed row are contiguous.
+//   fprop row (role br, filter f):  k = tap*C + c   <- w_br[f][c][tap]
+//   dgrad row c:                    k = e*Jd + j    <- w_{j/F}[j%F][c][r*r-1-e]
+template <typename T>
+__global__ void __launch_bounds__(256) pack_conv_kernel(Plan P, const float* w0, const float* w1, const float* w2,
+                                                        T* out) {
+  extern __shared__ float sbuf[];
+  const int rr = P.r * P.r;
+  const int nrow = P.nb * P.F;
+  if ((int)blockIdx.x < nrow) {
+    const int br = blockIdx.x / P.F, f = blockIdx.x - br * P.F;
+    const float* w = (br == 0 ? w0 : (br == 1 ? w1 : w2)) + (size_t)f * P.C * rr;
+    for (int i = threadIdx.x; i < P.C * rr; i += blockDim.x) sbuf[i] = w[i];
+    __syncthreads();
+    const int R = (f / P.FT) * (P.nb * P.FT) + br * P.FT + f % P.FT;
+    T* o = out + (size_t)R * P.Kf;
+    for (int k = threadIdx.x; k < P.Kf; k += blockDim.x) {
+      const int tap = k / P.C, c = k - tap * P.C;
+      o[k] = cvt<T>(sbuf[c * rr + tap]);
+    }
+  } else {
+    const int c = blockIdx.x - nrow;
+    for (int i = threadIdx.x; i < P.Jd * rr; i += blockDim.x) {
+      const int j = i / rr, t = i - j * rr;
+      const int br = j / P.F, f = j - br * P.F;
+      const float* w = br == 0 ? w0 : (br == 1 ? w1 : w2);
+      sbuf[i] = w[((size_t)f * P.C + c) * rr + t];
+    }
+    __syncthreads();
+    T* o = out + (size_t)nrow * P.Kf + (size_t)c * P.Kd;
+    for (int k = threadIdx.x; k < P.Kd; k += blockDim.x) {
+      const int e = k / P.Jd, j = k - e * P.Jd;
+      o[k] = cvt<T>(sbuf[j * rr + (rr - 1 - e)]);
+    }
+  }
+}
+
+template <typename T>
+static void launch_pack_conv(const Plan& P, const float* const w[3], T* out, size_t smem, cudaStream_t st) {
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(pack_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr = smem;
+  }
+  pack_conv_kernel<T><<<P.nb * P.F + P.C, 256, smem, st>>>(P, w[0], w[1], w[2], out);
+}
+
 void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
   long long nf = (long long)pack_fprop_elems(P), nd = (long long)pack_dgrad_elems(P);
+  if (P.kind == QD_KIND_CONV && P.sq == 0 && P.Jd == P.nb * P.F && P.Cd == P.C) {
+    const int rr = P.r * P.r;
+    size_t smem = (size_t)(P.C > P.Jd ? P.C : P.Jd) * rr * 4;
+    if (smem <= 200 * 1024) {
+      if (P.dtype == QD_BF16)
+        launch_pack_conv<bf16>(P, w, (bf16*)wpack, smem, st);
+      else
+        launch_pack_conv<float>(P, w, (float*)wpack, smem, st);
+      count_launch(st, "pack");
+      return;
+    }
+  }
   if (P.Kf % 4 || P.Kd % 4) {  // rows not a multiple of 4: one element per thread
     int blocks1 = (int)((nf + 255) / 256 + (nd + 255) / 256);
     if (P.dtype == QD_BF16)

@@ -47,6 +47,8 @@ struct C2Args {
   int b_slots, a_slots, stg_tiles;
   int nbias;  // bias vectors staged in smem (3 proposed, 1 first_order, else 0), Cout floats each
   int direct;  // epilogue stores straight from registers (no smem staging)
+  int pf;      // L2 prefetch distance of the A halo boxes, in this cluster's tiles (0 = off)
+  ptx::FastDiv fd_nn, fd_T, fd_Wp;  // tiles_nn, T_img, Wp
   int csplit;  // A channel blocks >= csplit come from the second map (dgrad: D = [g b, g a] then dy)
   int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
   unsigned long long* trace;  // QD_TRACE (dev only): per-role clock64 timeline of cluster 0
@@ -71,6 +73,12 @@ namespace c2 {
     if (g.trace && blockIdx.x == 0 && (tile) < 64)                                                \
       g.trace[((role) * 64 + (tile)) * 16 + (ev)] = (unsigned long long)clock64();                \
   } while (0)
+// same slots, written by CTA `blk` (dev only)
+#define C2_TRACE_B(blk, role, tile, ev)                                                           \
+  do {                                                                                            \
+    if (g.trace && blockIdx.x == (blk) && (tile) < 64)                                            \
+      g.trace[((role) * 64 + (tile)) * 16 + (ev)] = (unsigned long long)clock64();                \
+  } while (0)
 __device__ __forceinline__ uint32_t cluster_rank() {
   uint32_t r;
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
@@ -87,6 +95,12 @@ __device__ __forceinline__ void tma4_cg2(const CUtensorMap* m, uint32_t bar, voi
       " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(dst)),
       "l"(m), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
       : "memory");
+}
+// L2 prefetch of a future box (fire and forget; the later load then hits L2)
+__device__ __forceinline__ void tma4_prefetch(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
+  asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(m), "r"(c0), "r"(c1),
+               "r"(c2), "r"(c3)
+               : "memory");
 }
 __device__ __forceinline__ void tma2_cg2(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1) {
   asm volatile(
@@ -203,6 +217,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
   uint64_t* bempty = bfull + g.b_slots;
   uint32_t* tslot = (uint32_t*)(bempty + g.b_slots);
 
+  if (g.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    g.trace[4096 + 2 * blockIdx.x] = gtimer();
+    g.trace[6144 + 2 * blockIdx.x] = clock64();
+  }
   const uint32_t rank = c2::cluster_rank();
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
@@ -256,20 +274,31 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
     uint32_t aph = 0, bph = 0;
     int it = 0;
     for (int w = cluster; w < g.total; w += nclusters, ++it) {
-      int j = w % g.tiles_nn, rest = w / g.tiles_nn;
-      int t = rest % g.T_img, p = rest / g.T_img;
+      const int rest = ptx::fdiv(w, g.fd_nn), j = w - rest * g.tiles_nn;
+      const int p = ptx::fdiv(rest, g.fd_T), t = rest - p * g.T_img;
       int n = 2 * p + (int)rank;
-      int hq_lo = (128 * t) / g.Wp;
+      int hq_lo = ptx::fdiv(128 * t, g.fd_Wp);
       for (int ab = 0; ab < g.ablocks; ++ab) {
         int half = ab / g.cblks, cb = ab % g.cblks;
         if (leader) C2_TRACE(0, it, 2 * ab);
+        if (leader) C2_TRACE_B(1, 0, it, 8 + 2 * ab);
         ptx::mbar_wait(&aempty[as], aph ^ 1);
         if (leader) {
           C2_TRACE(0, it, 2 * ab + 1);
+          C2_TRACE_B(1, 0, it, 9 + 2 * ab);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&afull[as], 2u * g.halo_tx);
           const bool tail = g.csplit && cb >= g.csplit;
           c2::tma4_cg2((half || tail) ? &mA1 : &mA0, c2::peer0(&afull[as]), sHalo + as * g.halo_bytes,
                        (tail ? cb - g.csplit : cb) * 64, -g.pe, hq_lo - g.pe, n);
+          if (ab == 0) C2_TRACE(0, it, 7);
+          const int wf = w + g.pf * nclusters;
+          if (g.pf && wf < g.total) {
+            const int rf = wf / g.tiles_nn;
+            const int tf = rf % g.T_img, nf = 2 * (rf / g.T_img) + (int)rank;
+            if (nf < g.N)
+              c2::tma4_prefetch((half || tail) ? &mA1 : &mA0, (tail ? cb - g.csplit : cb) * 64, -g.pe,
+                                (128 * tf) / g.Wp - g.pe, nf);
+          }
         }
         if (++as == g.a_slots) { as = 0; aph ^= 1; }
         if (!g.resident) {
@@ -305,16 +334,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
       uint32_t aph = 0, bph = 0;
       int it = 0;
       for (int w = cluster; w < g.total; w += nclusters, ++it) {
-        int rest = w / g.tiles_nn;
-        int t = rest % g.T_img;
-        int q0 = 128 * t;
-        int row_off = q0 - (q0 / g.Wp) * g.Wp;
+        const int rest = ptx::fdiv(w, g.fd_nn);
+        const int t = rest - ptx::fdiv(rest, g.fd_T) * g.T_img;
+        const int q0 = 128 * t;
+        const int row_off = q0 - ptx::fdiv(q0, g.fd_Wp) * g.Wp;
         int acs = it & 1;
         uint32_t tph = (it >> 1) & 1;
         if (leader) C2_TRACE(1, it, 0);
         ptx::mbar_wait(&tempty[acs], tph ^ 1);
         if (leader) C2_TRACE(1, it, 1);
         ptx::tc_fence_after();
+        if (leader) C2_TRACE(1, it, 11);
         const uint32_t d = tmem + acs * ACC;
         uint32_t accum = 0;
         for (int ab = 0; ab < g.ablocks; ++ab) {
@@ -415,16 +445,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
     const uint32_t tempty0 = c2::peer0(&tempty[0]);
     int it = 0;
     for (int w = cluster; w < g.total; w += nclusters, ++it) {
-      int j = w % g.tiles_nn, rest = w / g.tiles_nn;
-      int t = rest % g.T_img, p = rest / g.T_img;
+      const int rest = ptx::fdiv(w, g.fd_nn), j = w - rest * g.tiles_nn;
+      const int p = ptx::fdiv(rest, g.fd_T), t = rest - p * g.T_img;
       int n = 2 * p + (int)rank;
       int acs = it & 1;
       uint32_t tph = (it >> 1) & 1;
       int qq = 128 * t + q * 32 + lane;
-      int hq = qq / g.Wp, wq = qq - hq * g.Wp;
+      int hq = ptx::fdiv(qq, g.fd_Wp), wq = qq - hq * g.Wp;
       bool valid = n < g.N && hq < g.OHg && wq < g.OWg;
-      if (g.ss > 1) valid = valid && (hq % g.ss) == 0 && (wq % g.ss) == 0;
-      int pix = valid ? (n * g.OHo + hq / g.ss) * g.OWo + wq / g.ss : -1;
+      int pix;
+      if (g.ss > 1) {
+        valid = valid && (hq % g.ss) == 0 && (wq % g.ss) == 0;
+        pix = valid ? (n * g.OHo + hq / g.ss) * g.OWo + wq / g.ss : -1;
+      } else {
+        pix = valid ? (n * g.OHo + hq) * g.OWo + wq : -1;
+      }
       const int c_base = j * g.out_c_tile;
       if (tracer) C2_TRACE(2, it, 0);
       ptx::mbar_wait(&tfull[acs], tph);
@@ -488,7 +523,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
           c2_stage_h(stg, lane, 0, pk[o][0][0], pk[o][0][1]);
           c2_stage_h(stg, lane, 1, pk[o][1][0], pk[o][1][1]);
           __syncwarp();
-          c2_store_h(g, stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), c_base + eg * 32, pix, lane);
+          if (!(g.dbg & 4))  // dev knob: skip the global stores
+            c2_store_h(g, stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), c_base + eg * 32, pix, lane);
           __syncwarp();
         }
         if (tracer) C2_TRACE(2, it, 3);
@@ -677,6 +713,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
   }
   ptx::tc_fence_before();
   c2::cluster_sync();
+  if (g.trace && threadIdx.x == 0 && blockIdx.x < 1024) {
+    g.trace[4096 + 2 * blockIdx.x + 1] = gtimer();
+    g.trace[6144 + 2 * blockIdx.x + 1] = clock64();
+  }
   if (warp == 2) {
     ptx::tc_fence_after();
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(512) : "memory");
@@ -689,9 +729,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
 static unsigned long long* g_trace = nullptr;
 static unsigned long long* trace_buffer() {
   if (!g_trace) {
-    cudaMalloc(&g_trace, 4096 * sizeof(unsigned long long));
+    cudaMalloc(&g_trace, 8192 * sizeof(unsigned long long));
   }
-  cudaMemset(g_trace, 0, 4096 * sizeof(unsigned long long));
+  cudaMemset(g_trace, 0, 8192 * sizeof(unsigned long long));
   return g_trace;
 }
 }  // namespace qd
@@ -710,12 +750,13 @@ extern "C" int qd_debug_spin(long long cycles, unsigned long long* dev_out, void
   qd_spin_kernel<<<148, 32, 0, (cudaStream_t)stream>>>(cycles, dev_out);
   return (int)cudaGetLastError();
 }
-// dev-only: copy the last QD_TRACE buffer (3 roles x 64 tiles x 16 events of clock64,
-// then per-CTA begin/end globaltimer pairs from slot 3072)
+// dev-only: copy the last QD_TRACE buffer (8192 u64: 3 roles x 64 tiles x 16 events of
+// clock64; wgrad: per-CTA globaltimer pairs from slot 3072, clock64 pairs from 2048;
+// conv2: per-CTA globaltimer pairs from 4096, clock64 pairs from 6144)
 extern "C" int qd_debug_trace_copy(unsigned long long* host) {
   if (!qd::g_trace) return -1;
   cudaDeviceSynchronize();
-  return (int)cudaMemcpy(host, qd::g_trace, 4096 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  return (int)cudaMemcpy(host, qd::g_trace, 8192 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 namespace qd {
 // co-resident clusters of size 2 for a kernel at this smem / block size (cached per kernel)
@@ -808,6 +849,8 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
       slots = KBtot;
       aslots = (int)(rest / halo);
       if (aslots > 4) aslots = 4;
+      const char* e = getenv("QD_ASLOTS");  // dev knob
+      if (e && atoi(e) >= 1 && atoi(e) < aslots) aslots = atoi(e);
     }
   }
   if (!resident) {
@@ -821,6 +864,7 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   g.N = N; g.Cin = Cin; g.Win = Win; g.Hin = Hin; g.OHg = OHg; g.OWg = OWg;
   g.pe = pe; g.r = r; g.Wp = Wp; g.HR = HR;
   g.T_img = T_img; g.tiles_nn = tiles_nn; g.total = ((N + 1) / 2) * T_img * tiles_nn;
+  g.fd_nn = ptx::make_fastdiv(tiles_nn); g.fd_T = ptx::make_fastdiv(T_img); g.fd_Wp = ptx::make_fastdiv(Wp);
   g.cblks = cblks; g.ablocks = ablocks; g.KBtot = KBtot; g.resident = resident;
   g.halo_bytes = halo; g.halo_tx = halo_tx; g.b_stage_bytes = bstage; g.b_slots = slots; g.a_slots = aslots; g.stg_tiles = stg_tiles; g.nbias = nbias;
   g.Cout = Cout;
@@ -879,6 +923,9 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   {
     const char* e = getenv("QD_C2_DIRECT");
     g.direct = e ? atoi(e) : 0;
+    const char* f = getenv("QD_PF");
+    g.pf = f ? atoi(f) : 0;  // measured: no gain on C2 (the pipe is MMA-bound)
+
   }
   g.OHo = (OHg - 1) / ss + 1;
   g.OWo = (OWg - 1) / ss + 1;

@@ -20,7 +20,7 @@ for _ in range(3):
     if which == "dgrad":
         neurons.symbolic_backward(spec, params, cache, gt, want_dw=False)
 torch.cuda.synchronize()
-buf = np.zeros(4096, dtype=np.uint64)
+buf = np.zeros(8192, dtype=np.uint64)
 lib.qd_debug_trace_copy(buf.ctypes.data)
 T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
 t0 = T[T > 0].min()
@@ -32,3 +32,11 @@ for tile in range(10):
         nz = [(i, int(v - t0)) for i, v in enumerate(ev) if v > 0]
         row.append(f"{names[role]}: " + " ".join(f"{i}@{v}" for i, v in nz))
     print(f"tile {tile}: " + " | ".join(row))
+G = buf[4096:6144].reshape(-1, 2).astype(np.int64)
+K = buf[6144:8192].reshape(-1, 2).astype(np.int64)
+nb = int((G[:, 0] > 0).sum())
+G, K = G[:nb], K[:nb]
+dur = (G[:, 1] - G[:, 0]) / 1e3
+ghz = (K[:, 1] - K[:, 0]) / (G[:, 1] - G[:, 0])
+print(f"CTAs {nb}: start spread {(G[:,0].max()-G[:,0].min())/1e3:.2f} us, span {(G[:,1].max()-G[:,0].min())/1e3:.1f} us, "
+      f"dur min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us, clock med {np.median(ghz):.3f} GHz")

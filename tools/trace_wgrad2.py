@@ -18,10 +18,10 @@ for _ in range(3):
     y, cache = neurons.forward(spec, params, xt)
     neurons.symbolic_backward(spec, params, cache, gt, want_dx=False)
 torch.cuda.synchronize()
-buf = np.zeros(4096, dtype=np.uint64)
+buf = np.zeros(8192, dtype=np.uint64)
 lib.qd_debug_trace_copy(buf.ctypes.data)
 T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
-C = buf[3072:].reshape(-1, 2).astype(np.int64)
+C = buf[3072:4096].reshape(-1, 2).astype(np.int64)
 t0 = T[T > 0].min()
 for i in range(20):
     p = T[0, i]; m = T[1, i]

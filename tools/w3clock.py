@@ -22,9 +22,9 @@ def step():
 for _ in range(50):
     step()
 torch.cuda.synchronize()
-buf = np.zeros(4096, dtype=np.uint64)
+buf = np.zeros(8192, dtype=np.uint64)
 lib.qd_debug_trace_copy(buf.ctypes.data)
-G = buf[3072:].reshape(-1, 2).astype(np.int64)
+G = buf[3072:4096].reshape(-1, 2).astype(np.int64)
 C = buf[2048:3072].reshape(-1, 2).astype(np.int64)
 nb = int((G[:, 0] > 0).sum())
 G, C = G[:nb], C[:nb]
