@@ -3,6 +3,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stddef.h>
+#include <string.h>
+#include <utility>
 #include "qd_common.cuh"
 
 namespace qd {
@@ -60,6 +62,38 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
                        const float* bpart, int SB, float* const db[3], cudaStream_t st);
 void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st);
 
+// Launch with programmatic stream serialization (PDL): the kernel may start while
+// the previous kernel of the stream drains; it must call ptx::pdl_wait() before
+// touching that kernel's outputs. QD_NO_PDL=1 falls back to ordinary launches.
+inline bool pdl_enabled() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("QD_NO_PDL");
+    on = (e && atoi(e)) ? 0 : 1;
+  }
+  return on == 1;
+}
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  if (!pdl_enabled()) {
+    kernel<<<grid, block, smem, st>>>(std::forward<Args>(args)...);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 // ---- tcgen05 path ----------------------------------------------------------
 bool tc_supported(const Plan& P, unsigned flags);
 int tc_wgrad_split(const Plan& P);
@@ -76,7 +110,8 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st, int ss = 1, const void* a_tail = nullptr, int csplit = 0);
+              const void* xres, cudaStream_t st, int ss = 1, const void* a_tail = nullptr, int csplit = 0,
+              int pdl_wait = 1);
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                 int tiles_nn, int Cout, int nbias);
 // stride-2 layers run as their stride-1 equivalent: forward subsamples the

@@ -76,6 +76,13 @@ __device__ __forceinline__ int fdiv(int x, const FastDiv& f) {
   return f.d == 1 ? x : (int)(__umulhi((unsigned)x, f.mul) >> f.shr);
 }
 
+// ---- programmatic dependent launch ----------------------------------------------
+// wait: block until the previous kernel in the stream has completed and its memory
+// is visible (no-op when this grid was not launched programmatically);
+// launch: let the next (programmatically launched) kernel's CTAs be scheduled.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- TMA ---------------------------------------------------------------------
 __device__ __forceinline__ void prefetch_tmap(const CUtensorMap* m) {
   asm volatile("prefetch.tensormap [%0];" ::"l"(m) : "memory");

@@ -10,6 +10,7 @@
 // instead of materialising the patch matrix (tensor.py:283-331).
 #include <stdio.h>
 #include "qd_kernels.h"
+#include "qd_ptx.cuh"
 
 namespace qd {
 
@@ -111,6 +112,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) pack_conv_kernel(Plan P, const float* w0, const float* w1, const float* w2,
                                                         T* out) {
   extern __shared__ float sbuf[];
+  ptx::pdl_launch();  // the forward kernel may start its setup while we pack
   const int rr = P.r * P.r;
   const int nrow = P.nb * P.F;
   if ((int)blockIdx.x < nrow) {

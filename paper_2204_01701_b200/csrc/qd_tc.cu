@@ -477,6 +477,8 @@ __global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf1
                                                                const bf16* __restrict__ b, bf16* __restrict__ D,
                                                                float* __restrict__ part, long long rows_per,
                                                                int up, int OH1, int OW1, int dstride) {
+  ptx::pdl_wait();  // a, b come from the forward kernel
+  ptx::pdl_launch();
   const int F = P.F, chunks = F / 8;
   const int lanes = 256 / chunks;  // rows processed concurrently
   const int ch = threadIdx.x % chunks, rl = threadIdx.x / chunks;
@@ -920,13 +922,13 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     d2 = conv2_fits(P.N, P.Jd, P.OW, P.OH, P.W, P.H, P.r - 1 - P.p, P.r, 0, c.nbk, c.nout, c.tiles_nn, P.C, 0);
   }
   const int dsplit = d2 ? 2 * P.F / 64 : 0;
+  bool wg_pdl = false;  // a PDL-launched v2/v3 wgrad immediately precedes the dgrad on `st`
   if (mat || P.nbias || up) {
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
     bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;
-    bwd_prologue_vec_kernel<<<L.bs_split, 256, 0, st>>>(P0, (const bf16*)dy, (const bf16*)a, (const bf16*)b, Dw,
-                                                        bpart, rows_per, up ? 1 : 0, P.OH, P.OW,
-                                                        d2 ? 2 * P.F : P.Jd);
+    launch_pdl(bwd_prologue_vec_kernel, dim3(L.bs_split), dim3(256), 0, st, P0, (const bf16*)dy, (const bf16*)a,
+               (const bf16*)b, Dw, bpart, rows_per, up ? 1 : 0, P.OH, P.OW, d2 ? 2 * P.F : P.Jd);
     count_launch(st, "prologue");
     if (mat || up) D = Dw;
   }
@@ -943,6 +945,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     rc = QD_ERR_UNSUPPORTED;
     WSplits wsp;
     memset(&wsp, 0, sizeof(wsp));
+    wg_pdl = false;
     if (w3) {
       rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st, dy, dsplit);
       wsp.pp = (P.r * P.r + 1) / 2;  // every tap in every split slot
@@ -952,6 +955,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st, dy, dsplit);
       wsp = wgrad2_splits(P);
     }
+    if (rc == QD_OK) wg_pdl = (w2 || w3) && pdl_enabled();
     if (rc == QD_OK) {
       // the memory-bound fold overlaps the (smem-bound) dgrad: it runs on the side
       // stream, forked after wgrad and joined before this call returns
@@ -999,9 +1003,11 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     const void* xr = P.sq ? x : nullptr;
     rc = QD_ERR_UNSUPPORTED;
     if (!(P.flags & QD_FLAG_TC_V1))
+      // D is complete once the (PDL-launched) v2/v3 wgrad is running, and nothing
+      // the dgrad reads is written by it: the dgrad need not wait for the wgrad
       rc = run_conv2(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
                      c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st, 1,
-                     dy, dsplit);
+                     dy, dsplit, wg_pdl ? 0 : 1);
     if (d2 && rc == QD_ERR_UNSUPPORTED) return set_error(QD_ERR_UNSUPPORTED, "dgrad conv2 plan changed");
     if (rc == QD_ERR_UNSUPPORTED && !up)
       rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,

@@ -48,6 +48,7 @@ struct C2Args {
   int nbias;  // bias vectors staged in smem (3 proposed, 1 first_order, else 0), Cout floats each
   int direct;  // epilogue stores straight from registers (no smem staging)
   int pf;      // L2 prefetch distance of the A halo boxes, in this cluster's tiles (0 = off)
+  int pdl_wait;  // 1: wait for the previous kernel's outputs (PDL) before the first global read
   ptx::FastDiv fd_nn, fd_T, fd_Wp;  // tiles_nn, T_img, Wp
   int csplit;  // A channel blocks >= csplit come from the second map (dgrad: D = [g b, g a] then dy)
   int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
@@ -146,23 +147,26 @@ __device__ __forceinline__ void stage16(uint8_t* tile, int row, int j, const flo
 }
 }  // namespace c2
 
-// 16 packed bf16 (channels 16j..16j+15 of a 32-channel half row) into a 32 x 64 B
-// staging tile; chunk c of row r stored at c ^ ((r >> 1) & 3) (conflict free for
-// row-per-lane writes and for the 4-lanes-per-row reads below)
-__device__ __forceinline__ void c2_stage_h(uint8_t* tile, int row, int j, const uint4& lo, const uint4& hi) {
-  uint8_t* rp = tile + row * 64;
-  const int f = (row >> 1) & 3;
+// 16 packed bf16 (channels 16j..16j+15) into a 32-row staging tile of RB-byte rows
+// (RB = 2 x channels per warp); chunk c of row r at c ^ ((r / (128/RB)) & (RB/16-1)),
+// conflict free for the row-per-lane writes and the lanes-per-row reads below
+template <int RB>
+__device__ __forceinline__ void c2_stage_rb(uint8_t* tile, int row, int j, const uint4& lo, const uint4& hi) {
+  constexpr int CH = RB / 16, RPL = 128 / RB;
+  uint8_t* rp = tile + row * RB;
+  const int f = (row / RPL) & (CH - 1);
   *reinterpret_cast<uint4*>(rp + (((2 * j) ^ f) << 4)) = lo;
   *reinterpret_cast<uint4*>(rp + (((2 * j + 1) ^ f) << 4)) = hi;
 }
-// coalesced store of one 32 x 64 B staging tile: 8 rows (8 x 64 B) per instruction
-__device__ __forceinline__ void c2_store_h(const C2Args& g, const uint8_t* st, bf16* dst, int ch, int pix,
-                                           int lane) {
+template <int RB>
+__device__ __forceinline__ void c2_store_rb(const C2Args& g, const uint8_t* st, bf16* dst, int ch, int pix,
+                                            int lane) {
+  constexpr int CH = RB / 16, RPL = 128 / RB, RPI = 32 / CH;  // chunks per row, rows per instr
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int Rw = 8 * i + (lane >> 2), c = lane & 3;
-    int rp = __shfl_sync(0xffffffffu, pix, Rw);
-    uint4 val = *reinterpret_cast<const uint4*>(st + Rw * 64 + ((c ^ ((Rw >> 1) & 3)) << 4));
+  for (int i = 0; i < 32 / RPI; ++i) {
+    const int Rw = RPI * i + lane / CH, c = lane % CH;
+    const int rp = __shfl_sync(0xffffffffu, pix, Rw);
+    uint4 val = *reinterpret_cast<const uint4*>(st + Rw * RB + ((c ^ ((Rw / RPL) & (CH - 1))) << 4));
     if (rp >= 0) *reinterpret_cast<uint4*>(dst + (size_t)rp * g.Cout + ch + c * 8) = val;
   }
 }
@@ -186,11 +190,14 @@ __device__ __forceinline__ void c2_store_pass(const C2Args& g, const uint8_t* st
   }
 }
 
+#ifndef C2_EPW
+#define C2_EPW 2
+#endif
 template <int EPI, int NB>
 struct C2Threads {
   static constexpr int NPASS = (EPI == E2_PROPOSED || EPI == E2_T4) ? 3 : (EPI == E2_PLAIN ? NB : 1);
-  // proposed / t4: two epilogue warpgroups (y | a, b) run concurrently
-  static constexpr int NEPI = NPASS == 3 ? 8 : 4;
+  // proposed / t4: C2_EPW epilogue warpgroups, each owning 64 / C2_EPW channels of y, a, b
+  static constexpr int NEPI = NPASS == 3 ? 4 * C2_EPW : 4;
   static constexpr int THREADS = 128 + NEPI * 32;
 };
 
@@ -255,6 +262,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
   ptx::tc_fence_before();
   c2::cluster_sync();
   ptx::tc_fence_after();
+  if (g.pdl_wait) ptx::pdl_wait();  // before any read of the previous kernel's outputs
+  ptx::pdl_launch();                 // the next kernel's CTAs may take SMs as ours retire
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
@@ -435,11 +444,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
       ptx::named_bar_sync(1, NEPI * 32);
     }
     // passes of this warp: with two warpgroups, group 0 writes y and group 1 a, b
-    const int o_beg = NEPI == 8 ? (eg == 0 ? 0 : 1) : 0;
-    const int o_end = NEPI == 8 ? (eg == 0 ? 1 : 3) : NPASS;
-    // proposed / t4: warp (eg, q) owns a 2 KB half-row staging tile; else stg_tiles 4 KB tiles
-    uint8_t* stg = NEPI == 8 ? sStg + (warp - 4) * 2048 : sStg + q * g.stg_tiles * 4096;
-    const bool multi = NEPI == 8 ? (o_end - o_beg > 1) : g.stg_tiles > 1;
+    constexpr bool SPLIT = NEPI > 4;  // proposed / t4: channel-split warpgroups
+    constexpr int CW = SPLIT ? 64 / (NEPI / 4) : 64;  // channels per warp
+    const int o_beg = 0;
+    const int o_end = NPASS;
+    // split: warp (eg, q) owns a CW x 32-row staging tile (16 KB in all); else stg_tiles 4 KB tiles
+    uint8_t* stg = SPLIT ? sStg + (warp - 4) * (CW * 64) : sStg + q * g.stg_tiles * 4096;
+    const bool multi = g.stg_tiles > 1;
     const bool tracer = q == 0 && eg == 0 && lane == 0;
     const bool tracer1 = q == 0 && eg == 1 && lane == 0;
     const uint32_t tempty0 = c2::peer0(&tempty[0]);
@@ -472,14 +483,15 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         continue;
       }
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acs * ACC;
-      if ((EPI == E2_PROPOSED || EPI == E2_T4) && NEPI == 8 && !g.direct) {
-        // warpgroup eg takes channels [32 eg, 32 eg + 32) of all three outputs:
-        // 2 x (a, b, c) TMEM loads, y / a / b packed to bf16 in registers, the
-        // accumulator handed back, then three 2 KB staged store passes
-        uint4 pk[3][2][2];  // [y|a|b][jj][lo|hi]
+      if (SPLIT && !g.direct) {
+        // warpgroup eg takes channels [CW eg, CW eg + CW) of all three outputs:
+        // (a, b, c) TMEM loads per 16 channels, y / a / b packed to bf16 in
+        // registers, the accumulator handed back, then three staged store passes
+        constexpr int JJ = CW / 16;
+        uint4 pk[3][JJ][2];  // [y|a|b][jj][lo|hi]
 #pragma unroll
-        for (int jj = 0; jj < 2; ++jj) {
-          const int col = eg * 32 + jj * 16;
+        for (int jj = 0; jj < JJ; ++jj) {
+          const int col = eg * CW + jj * 16;
           const int c0 = c_base + col;
           float va[16], vb[16], vc[16];
           ptx::tmem_ld16(tb + col, va);
@@ -520,56 +532,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         if (tracer1) C2_TRACE(2, it, 11);
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
-          c2_stage_h(stg, lane, 0, pk[o][0][0], pk[o][0][1]);
-          c2_stage_h(stg, lane, 1, pk[o][1][0], pk[o][1][1]);
+#pragma unroll
+          for (int jj = 0; jj < JJ; ++jj) c2_stage_rb<2 * CW>(stg, lane, jj, pk[o][jj][0], pk[o][jj][1]);
           __syncwarp();
           if (!(g.dbg & 4))  // dev knob: skip the global stores
-            c2_store_h(g, stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), c_base + eg * 32, pix, lane);
+            c2_store_rb<2 * CW>(g, stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), c_base + eg * CW, pix, lane);
           __syncwarp();
         }
         if (tracer) C2_TRACE(2, it, 3);
-        if (tracer1) C2_TRACE(2, it, 12);
-        continue;
-      }
-      if (false) {
-        // a and b in one sweep: one TMEM round trip per 16 channels for both,
-        // only the two biases they need
-#pragma unroll 1
-        for (int jj = 0; jj < 4; ++jj) {
-          const int c0 = c_base + jj * 16;
-          float va[16], vb[16];
-          ptx::tmem_ld16(tb + jj * 16, va);
-          ptx::tmem_ld16(tb + 64 + jj * 16, vb);
-          if (EPI == E2_PROPOSED) {
-            const float4* pa = reinterpret_cast<const float4*>(sBias + c0);
-            const float4* pb = reinterpret_cast<const float4*>(sBias + g.Cout + c0);
-            float ba[16], bbv[16];
-#pragma unroll
-            for (int v4 = 0; v4 < 4; ++v4) {
-              float4 x0 = pa[v4], x1 = pb[v4];
-              ba[4 * v4] = x0.x; ba[4 * v4 + 1] = x0.y; ba[4 * v4 + 2] = x0.z; ba[4 * v4 + 3] = x0.w;
-              bbv[4 * v4] = x1.x; bbv[4 * v4 + 1] = x1.y; bbv[4 * v4 + 2] = x1.z; bbv[4 * v4 + 3] = x1.w;
-            }
-            ptx::tmem_wait_ld();
-#pragma unroll
-            for (int e = 0; e < 16; ++e) {
-              va[e] += ba[e];
-              vb[e] += bbv[e];
-            }
-          } else {
-            ptx::tmem_wait_ld();
-          }
-          c2::stage16(stg, lane, jj, va);
-          c2::stage16(stg + 4096, lane, jj, vb);
-        }
-        ptx::tc_fence_before();
-        __syncwarp();
-        if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
-        if (tracer1) C2_TRACE(2, it, 11);
-        __syncwarp();
-        c2_store_pass<EPI>(g, stg, 1, c_base, pix, lane);
-        c2_store_pass<EPI>(g, stg + 4096, 2, c_base, pix, lane);
-        __syncwarp();
         if (tracer1) C2_TRACE(2, it, 12);
         continue;
       }
@@ -892,7 +862,8 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   int clusters = tc_num_sms() / 2;
   if (maxc > 0 && maxc < clusters) clusters = maxc;
   if (pl.g.total < clusters) clusters = pl.g.total;
-  conv2_kernel<EPI, NB, R><<<2 * clusters, C2Threads<EPI, NB>::THREADS, pl.smem, st>>>(A0, A1, B, pl.g);
+  launch_pdl(conv2_kernel<EPI, NB, R>, dim3(2 * clusters), dim3(C2Threads<EPI, NB>::THREADS), pl.smem, st, A0, A1, B,
+             pl.g);
   count_launch(st, "conv2");
   return check_launch("conv2");
 }
@@ -908,7 +879,7 @@ static int c2_launch(const CUtensorMap& A0, const CUtensorMap& A1, const CUtenso
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit) {
+              const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit, int pdl_wait) {
   int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
   int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
   C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
@@ -937,6 +908,7 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   g.bias0 = bias[0]; g.bias1 = bias[1]; g.bias2 = bias[2];
   g.out0 = (bf16*)o0; g.out1 = (bf16*)o1; g.out2 = (bf16*)o2;
   g.xres = (const bf16*)xres;
+  g.pdl_wait = pdl_wait;
   CUtensorMap A0, A1, B;
   int rc;
   cuuint32_t bA[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.HR, 1};
@@ -1043,6 +1015,8 @@ __global__ void __launch_bounds__(256, 1)
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  ptx::pdl_wait();
+  ptx::pdl_launch();
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
@@ -1317,6 +1291,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   ptx::tc_fence_before();
   c2::cluster_sync();  // barriers of both CTAs initialised before any multicast lands
   ptx::tc_fence_after();
+  ptx::pdl_wait();
+  ptx::pdl_launch();
   const uint32_t tmem = *tslot;
 
   if (warp == 0) {
@@ -1553,8 +1529,7 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr = (int)pl.smem;
   }
-  wgrad3_kernel<<<2 * g.jtiles * g.ablocks * g.nsplit, 256, pl.smem, st>>>(X0, X1, Dm, Dm1, g);
-  if (getenv("QD_W3_TWICE")) wgrad3_kernel<<<2 * g.jtiles * g.ablocks * g.nsplit, 256, pl.smem, st>>>(X0, X1, Dm, Dm1, g);
+  launch_pdl(wgrad3_kernel, dim3(2 * g.jtiles * g.ablocks * g.nsplit), dim3(256), pl.smem, st, X0, X1, Dm, Dm1, g);
   count_launch(st, "wgrad3");
   return check_launch("wgrad3");
 }
@@ -1608,7 +1583,8 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cudaFuncSetAttribute(wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr = (int)pl.smem;
   }
-  wgrad2_kernel<<<g.jtiles * g.ablocks * g.gstart[g.tgroups], 256, pl.smem, st>>>(X0, X1, Dm, Dm1, g);
+  launch_pdl(wgrad2_kernel, dim3(g.jtiles * g.ablocks * g.gstart[g.tgroups]), dim3(256), pl.smem, st, X0, X1, Dm,
+             Dm1, g);
   count_launch(st, "wgrad2");
   return check_launch("wgrad2");
 }
