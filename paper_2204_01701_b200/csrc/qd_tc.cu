@@ -946,20 +946,27 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     WSplits wsp;
     memset(&wsp, 0, sizeof(wsp));
     wg_pdl = false;
+    // dev: QD_BR2=1 runs wgrad + fold on the side stream concurrently with the dgrad
+    const bool br2 = (w2 || w3) && dx && !P.sq && getenv("QD_BR2") && atoi(getenv("QD_BR2"));
+    cudaStream_t wst = st;
+    if (br2) {
+      side = fork_side(st);
+      if (side) wst = side;
+    }
     if (w3) {
-      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st, dy, dsplit);
+      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, wst, dy, dsplit);
       wsp.pp = (P.r * P.r + 1) / 2;  // every tap in every split slot
       wsp.ng = 1;
       wsp.s[0] = L.wg_split;
     } else if (w2) {
-      rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, st, dy, dsplit);
+      rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, wst, dy, dsplit);
       wsp = wgrad2_splits(P);
     }
-    if (rc == QD_OK) wg_pdl = (w2 || w3) && pdl_enabled();
+    if (rc == QD_OK) wg_pdl = (w2 || w3) && pdl_enabled() && wst == st;
     if (rc == QD_OK) {
       // the memory-bound fold overlaps the (smem-bound) dgrad: it runs on the side
       // stream, forked after wgrad and joined before this call returns
-      side = fork_side(st);
+      if (wst == st) side = fork_side(st);
       launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wsp, dW, bpart, L.bs_split, db,
                         side ? side : st);
     } else if (rc != QD_ERR_UNSUPPORTED) {

@@ -483,7 +483,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         continue;
       }
       const uint32_t tb = tmem + ((uint32_t)(q * 32) << 16) + acs * ACC;
-      if (SPLIT && !g.direct) {
+      if (SPLIT) {
         // warpgroup eg takes channels [CW eg, CW eg + CW) of all three outputs:
         // (a, b, c) TMEM loads per 16 channels, y / a / b packed to bf16 in
         // registers, the accumulator handed back, then three staged store passes
@@ -530,6 +530,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
         if (tracer) C2_TRACE(2, it, 2);
         if (tracer1) C2_TRACE(2, it, 11);
+        if (g.direct) {
+          // straight from registers: this lane's pixel row, CW channels per output
+          if (pix >= 0 && !(g.dbg & 4)) {
+#pragma unroll
+            for (int o = 0; o < 3; ++o) {
+              bf16* dst = (o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2)) + (size_t)pix * g.Cout + c_base + eg * CW;
+#pragma unroll
+              for (int jj = 0; jj < JJ; ++jj) {
+                reinterpret_cast<uint4*>(dst + jj * 16)[0] = pk[o][jj][0];
+                reinterpret_cast<uint4*>(dst + jj * 16)[1] = pk[o][jj][1];
+              }
+            }
+          }
+          if (tracer) C2_TRACE(2, it, 3);
+          if (tracer1) C2_TRACE(2, it, 12);
+          continue;
+        }
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
 #pragma unroll
