@@ -47,6 +47,9 @@ WORKLOADS = {
     "c5_t2lin_64x56": ("t2_linear", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
     "c5_t4_512x7": ("t4", "conv", 64, 512, 512, 7, 7, 3, 1, 1, "bf16"),
     "c5_t2lin_512x7": ("t2_linear", "conv", 64, 512, 512, 7, 7, 3, 1, 1, "bf16"),
+    # families beyond the BASELINE sweep
+    "c5_t3_64x56": ("t3", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
+    "c5_t2and4_64x56": ("t2and4", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
 }
 METRIC = "quadratic_conv_fwd_bwd_tflops"
 L2_NOTE = ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read so the "

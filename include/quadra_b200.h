@@ -37,7 +37,9 @@ enum {
   QD_FAM_T2 = 1,          /* Wa (x*x)                                 */
   QD_FAM_T4 = 2,          /* (Wa x) * (Wb x)                          */
   QD_FAM_PROPOSED = 3,    /* (Wa x + ba) * (Wb x + bb) + (Wc x + bc)  */
-  QD_FAM_T2_LINEAR = 4    /* Wa (x*x) + Wc x                          */
+  QD_FAM_T2_LINEAR = 4,   /* Wa (x*x) + Wc x                          */
+  QD_FAM_T3 = 5,          /* (Wa x)^2                                 */
+  QD_FAM_T2AND4 = 6       /* (Wa x) * (Wb x) + Wc (x*x)               */
 };
 enum { QD_KIND_FC = 0, QD_KIND_CONV = 1 };
 enum { QD_F32 = 0, QD_BF16 = 1 };

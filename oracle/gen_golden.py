@@ -166,6 +166,38 @@ def gen_layer_golden(neurons, tensor, Spec):
         np.savez_compressed(os.path.join(OUT, name), **rec)
         files.append({"file": name, "family": "t2_linear", "kind": kind, "n": n, "c": c,
                       "f": f, "h": h, "w": w, "k": k, "s": s, "p": p})
+    # round-1 additions: t3 and t2and4 (neurons.py:257-267, :355-379, :406-432) on their
+    # own seed so the earlier files stay byte-identical
+    rng2 = np.random.default_rng(4321)
+    for idx, (fam, kind, n, c, f, h, w, k, s, p) in enumerate([
+            ("t3", "fc", 5, 7, 6, 1, 1, 1, 1, 0),
+            ("t3", "conv", 3, 3, 4, 5, 5, 3, 1, 1),
+            ("t3", "conv", 3, 3, 4, 5, 5, 3, 2, 1),
+            ("t3", "conv", 2, 3, 2, 5, 5, 2, 1, 0),
+            ("t2and4", "fc", 5, 7, 6, 1, 1, 1, 1, 0),
+            ("t2and4", "conv", 3, 3, 4, 5, 5, 3, 1, 1),
+            ("t2and4", "conv", 3, 3, 4, 5, 5, 3, 2, 1),
+            ("t2and4", "conv", 2, 3, 2, 5, 5, 2, 1, 0)]):
+        spec = Spec(kind=kind, family=fam, in_dim=c, out_dim=f, kernel=k, stride=s, pad=p)
+        params = {role: rng2.normal(size=shape)
+                  for role, shape in neurons.param_shapes(spec).items()}
+        x = rng2.normal(size=(n, c) if kind == "fc" else (n, c, h, w))
+        tp = {role: T.Tensor._wrap(v, is_param=True) for role, v in params.items()}
+        y, cache = neurons.forward(spec, tp, T.Tensor._wrap(x))
+        g = rng2.normal(size=y.shape)
+        grads, dx = neurons.symbolic_backward(spec, tp, cache, T.Tensor._wrap(g))
+        rec = {"x": x, "g": g, "y": y.data, "dx": dx}
+        for role, v in params.items():
+            rec["P_" + role] = v
+        for role, v in grads.items():
+            rec["G_" + role] = v
+        if cache.a is not None:
+            rec["a"] = cache.a.data
+            rec["b"] = cache.b.data
+        name = f"layer_x{idx:02d}_{fam}_{kind}_k{k}s{s}p{p}.npz"
+        np.savez_compressed(os.path.join(OUT, name), **rec)
+        files.append({"file": name, "family": fam, "kind": kind, "n": n, "c": c, "f": f,
+                      "h": h, "w": w, "k": k, "s": s, "p": p})
     return files
 
 

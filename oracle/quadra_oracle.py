@@ -109,10 +109,17 @@ def forward(family, geo, P, x):
         y = _bias(geo, _lin(geo, x, P["W"]), P["b"])
     elif family == "t2":
         y = _lin(geo, x * x, P["Wa"])
+    elif family == "t3":                                  # :257-259
+        av = _lin(geo, x, P["Wa"])
+        y = av * av
     elif family == "t4":
         a = _lin(geo, x, P["Wa"])
         b = _lin(geo, x, P["Wb"])
         y = a * b
+    elif family == "t2and4":                              # :264-267
+        a = _lin(geo, x, P["Wa"])
+        b = _lin(geo, x, P["Wb"])
+        y = a * b + _lin(geo, x * x, P["Wc"])
     elif family == "t2_linear":
         # reference t2 (neurons.py:255-256) + bias-free first_order (:242-244)
         y = _lin(geo, x * x, P["Wa"]) + _lin(geo, x, P["Wc"])
@@ -146,6 +153,24 @@ def symbolic_backward(family, geo, P, x, a, b, g):
             ds = g @ P["Wa"].T
             t = ds * xa
             dx = t + t
+        elif family == "t3":                             # :355-360
+            av = xa @ P["Wa"]
+            t = g * av
+            da = t + t
+            grads["Wa"] = xa.T @ da
+            dx = da @ P["Wa"].T
+        elif family == "t2and4":                         # :368-379
+            s = xa * xa
+            grads["Wc"] = s.T @ g
+            ds = g @ P["Wc"].T
+            t = ds * xa
+            dx = t + t
+            da = g * b
+            db = g * a
+            grads["Wb"] = xa.T @ db
+            dx = dx + db @ P["Wb"].T
+            grads["Wa"] = xa.T @ da
+            dx = dx + da @ P["Wa"].T
         elif family == "t4":                             # :361-367
             da = g * b
             db = g * a
@@ -189,6 +214,25 @@ def symbolic_backward(family, geo, P, x, a, b, g):
         grads["Wa"], ds = _grads(geo, g, col_s, P["Wa"], x_shape)
         t = ds * xa
         dx = t + t
+    elif family == "t3":                                 # :406-411
+        col = im2col(xa, r, s_, p_)[0]
+        av = _lin(geo, xa, P["Wa"])
+        t = g * av
+        da = t + t
+        grads["Wa"], dx = _grads(geo, da, col, P["Wa"], x_shape)
+    elif family == "t2and4":                             # :420-432
+        s = xa * xa
+        col_s = im2col(s, r, s_, p_)[0]
+        grads["Wc"], ds = _grads(geo, g, col_s, P["Wc"], x_shape)
+        t = ds * xa
+        dx = t + t
+        col = im2col(xa, r, s_, p_)[0]
+        da = g * b
+        db = g * a
+        grads["Wb"], dxb = _grads(geo, db, col, P["Wb"], x_shape)
+        dx = dx + dxb
+        grads["Wa"], dxa = _grads(geo, da, col, P["Wa"], x_shape)
+        dx = dx + dxa
     elif family == "t4":                                 # :412-419
         col = im2col(xa, r, s_, p_)[0]
         da = g * b
@@ -272,8 +316,9 @@ def synthetic_layer(family, kind, n, c, f, h=1, w=1, r=1, stride=1, pad=0,
         fan = c * r * r
         oh = conv_out_size(h, r, stride, pad)
         ow = conv_out_size(w, r, stride, pad)
-    roles = {"first_order": ("W",), "t2": ("Wa",), "t4": ("Wa", "Wb"),
-             "t2_linear": ("Wa", "Wc"), "proposed": ("Wa", "Wb", "Wc")}[family]
+    roles = {"first_order": ("W",), "t2": ("Wa",), "t3": ("Wa",), "t4": ("Wa", "Wb"),
+             "t2_linear": ("Wa", "Wc"), "t2and4": ("Wa", "Wb", "Wc"),
+             "proposed": ("Wa", "Wb", "Wc")}[family]
     P = {}
     bound = np.sqrt(6.0 / fan)
     for role in roles:

@@ -70,7 +70,8 @@ Workspace plan_workspace(const Plan& P, int path) {
   }
   // stride-2 layers on the tcgen05 path run their backward on the stride-1 grid
   const Plan Pg = (path == 1 && P.s == 2) ? stride1_plan(P) : P;
-  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4 || Pg.s != P.s) L.sz_D = (size_t)Pg.Mout * P.Jd * es;
+  if (caches_ab(P.family) || P.family == QD_FAM_T3 || Pg.s != P.s) L.sz_D = (size_t)Pg.Mout * P.Jd * es;
+  if (path == 1 && P.family == QD_FAM_T2AND4) L.sz_ZB = (size_t)3 * P.F * 4;
   if (path == 0) {
     long long tiles = (long long)((P.Jd + 63) / 64) * ((P.Kf + 63) / 64);
     long long S = (2 * 148 + tiles - 1) / tiles;
@@ -99,13 +100,14 @@ Workspace plan_workspace(const Plan& P, int path) {
   L.off_WG = off; off = align_up(off + L.sz_WG);
   L.off_BS = off; off = align_up(off + L.sz_BS);
   L.off_XS = off; off = align_up(off + L.sz_XS);
+  L.off_ZB = off; off = align_up(off + L.sz_ZB);
   L.total = off;
   return L;
 }
 
 static int validate(const qd_desc* d) {
   if (!d) return set_error(QD_ERR_ARG, "null descriptor");
-  if (d->family < 0 || d->family > QD_FAM_T2_LINEAR)
+  if (d->family < 0 || d->family > QD_FAM_T2AND4)
     return set_error(QD_ERR_CONFIG, "unknown family %d", d->family);
   if (d->kind != QD_KIND_FC && d->kind != QD_KIND_CONV)
     return set_error(QD_ERR_CONFIG, "unknown layer kind %d", d->kind);
@@ -187,7 +189,7 @@ int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* 
   if (!x || !wpack || !y) return set_error(QD_ERR_ARG, "null tensor pointer");
   for (int i = 0; i < P.nbias; ++i)
     if (!bias || !bias[i]) return set_error(QD_ERR_ARG, "bias role %d is NULL", i);
-  bool cache = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  bool cache = caches_ab(P.family);
   if (cache && (!a_cache || !b_cache))
     return set_error(QD_ERR_ARG, "family caches a and b: a_cache/b_cache must be given");
   const float* nob[3] = {nullptr, nullptr, nullptr};
@@ -207,7 +209,7 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* 
   if (st) return st;
   Plan P = make_plan(*d);
   if (!x || !wpack || !dy) return set_error(QD_ERR_ARG, "null tensor pointer");
-  bool cache = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  bool cache = caches_ab(P.family);
   if (cache && (!a_cache || !b_cache))
     return set_error(QD_ERR_INTEGRITY, "cache for this family must hold a and b");
   if (!(d->flags & QD_FLAG_NO_DX) && !dx) return set_error(QD_ERR_ARG, "dx is NULL");

@@ -52,6 +52,10 @@ inline Plan make_plan(const qd_desc& d) {
     case QD_FAM_T4:       P.nb = 2; P.sq = 0; P.Jd = 2 * P.F; P.nroles = 2; P.nbias = 0; break;
     case QD_FAM_T2:       P.nb = 1; P.sq = 1; P.Jd = P.F;     P.nroles = 1; P.nbias = 0; break;
     case QD_FAM_T2_LINEAR:P.nb = 1; P.sq = 2; P.Jd = P.F;     P.nroles = 2; P.nbias = 0; break;
+    case QD_FAM_T3:       P.nb = 1; P.sq = 0; P.Jd = P.F;     P.nroles = 1; P.nbias = 0; break;
+    // t2and4: K = [x*x | x] like t2_linear, three branches like proposed (a, b read
+    // the x half, c the x*x half; the other halves are structural zeros)
+    case QD_FAM_T2AND4:   P.nb = 3; P.sq = 2; P.Jd = 3 * P.F; P.nroles = 3; P.nbias = 0; break;
     default:              P.nb = 1; P.sq = 0; P.Jd = P.F;     P.nroles = 1; P.nbias = 1; break;
   }
   P.K0 = P.r * P.r * P.C;
@@ -60,6 +64,71 @@ inline Plan make_plan(const qd_desc& d) {
   P.Cd = (P.sq == 2) ? 2 * P.C : P.C;
   P.Kd = P.r * P.r * P.Jd;
   return P;
+}
+
+// families whose forward caches a and b (neurons.py:110-111)
+__host__ __device__ inline bool caches_ab(int family) {
+  return family == QD_FAM_PROPOSED || family == QD_FAM_T4 || family == QD_FAM_T2AND4;
+}
+// D = [g b | g a | g] (three blocks) for proposed and t2and4
+__host__ __device__ inline bool d_has_g(int family) {
+  return family == QD_FAM_PROPOSED || family == QD_FAM_T2AND4;
+}
+
+// packed fprop weight (branch br, GEMM column k): source role and tap-major index kk;
+// false for t2and4's structural zeros. K = [x*x | x] when sq == 2.
+__host__ __device__ inline bool fprop_src(const Plan& P, int br, int k, int& role, int& kk) {
+  if (P.sq == 2) {
+    const int half = k / P.K0;
+    kk = k - half * P.K0;
+    if (P.family == QD_FAM_T2AND4) {
+      role = br;
+      return (br == 2) == (half == 0);
+    }
+    role = half;  // t2_linear: Wa on x*x, Wc on x
+    return true;
+  }
+  role = br;
+  kk = k;
+  return true;
+}
+// packed dgrad weight (row cp, D channel j): source role, input channel c, filter f.
+// sq == 2: rows [0, C) produce the x*x-branch gradient, rows [C, 2C) the linear one.
+__host__ __device__ inline bool dgrad_src(const Plan& P, int cp, int j, int& role, int& c, int& f) {
+  if (P.family == QD_FAM_T2AND4) {
+    const int part = cp / P.C, jb = j / P.F;
+    c = cp - part * P.C;
+    f = j - jb * P.F;
+    role = jb;  // D blocks: g b -> Wa, g a -> Wb, g -> Wc
+    return (part == 0) == (jb == 2);
+  }
+  if (P.sq == 2) {
+    role = cp / P.C;
+    c = cp % P.C;
+    f = j;
+    return true;
+  }
+  role = j / P.F;
+  f = j % P.F;
+  c = cp;
+  return true;
+}
+// wgrad partial (D channel j, GEMM K index k) -> gradient role, filter f, tap-major kk
+__host__ __device__ inline bool wgrad_dst(const Plan& P, int j, int k, int& role, int& f, int& kk) {
+  f = j % P.F;
+  if (P.sq == 2) {
+    const int half = k / P.K0;
+    kk = k - half * P.K0;
+    if (P.family == QD_FAM_T2AND4) {
+      role = j / P.F;
+      return (role == 2) == (half == 0);
+    }
+    role = half;
+    return true;
+  }
+  role = j / P.F;
+  kk = k;
+  return true;
 }
 
 // Row of branch `br`, channel `f` inside the packed fprop weights: branches are

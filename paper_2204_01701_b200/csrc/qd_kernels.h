@@ -23,6 +23,7 @@ struct Workspace {
   size_t off_WG, sz_WG;    // wgrad split-K partials (fp32)
   size_t off_BS, sz_BS;    // bias-sum partials (fp32)
   size_t off_XS, sz_XS;    // squared input (dtype), t2/t2_linear tcgen05 path
+  size_t off_ZB, sz_ZB;    // zero bias vectors (t2and4 reuses the proposed epilogue)
   int wg_split;            // number of wgrad partials
   int bs_split;            // number of bias-sum partials
 };
@@ -45,6 +46,8 @@ int simt_backward(const Plan& P, const void* x, const void* wpack, const void* a
 // partials of D (or of dy) for the bias gradients.
 void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const void* b,
                          void* D, float* bsum_part, int bs_split, cudaStream_t st);
+// t3: D = 2 dy a from the recomputed a (fp32 SIMT GEMM output or dtype, may alias D)
+void launch_t3_prologue(const Plan& P, const void* dy, const void* a, bool a_fp32, void* D, cudaStream_t st);
 void launch_bias_finish(const Plan& P, const float* bsum_part, int bs_split,
                         float* const db[3], cudaStream_t st);
 // sum the wgrad partials [S][Jd][Kf] and scatter into reference layouts
@@ -61,6 +64,7 @@ WSplits wgrad2_splits(const Plan& P);
 void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& ws, float* const dW[3],
                        const float* bpart, int SB, float* const db[3], cudaStream_t st);
 void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st);
+void launch_square_out(const Plan& P, void* y, cudaStream_t st);  // y <- y*y in place (t3)
 
 // Launch with programmatic stream serialization (PDL): the kernel may start while
 // the previous kernel of the stream drains; it must call ptx::pdl_wait() before

@@ -38,12 +38,13 @@ __global__ void pack_one_kernel(Plan P, const float* w0, const float* w1, const 
     int grp = P.nb * P.FT;
     int tile = R / grp, rem = R % grp;
     int br = rem / P.FT, f = tile * P.FT + rem % P.FT;
-    int role = br, kk = k;
-    if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+    int role, kk;
+    const bool nz = fprop_src(P, br, k, role, kk);
     int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
     const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
-    float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
-                                     : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+    float v = !nz ? 0.f
+                  : (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                           : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
     out[i] = cvt<T>(v);
   } else {
     long long i = (long long)(blockIdx.x - nfb) * 256 + threadIdx.x;
@@ -52,11 +53,11 @@ __global__ void pack_one_kernel(Plan P, const float* w0, const float* w1, const 
     int e = k / P.Jd, j = k % P.Jd;
     int ey = e / P.r, ex = e % P.r, dy = P.r - 1 - ey, dx = P.r - 1 - ex;
     int role, f, c;
-    if (P.sq == 2) { role = cp / P.C; c = cp % P.C; f = j; }
-    else { role = j / P.F; f = j % P.F; c = cp; }
+    const bool nz = dgrad_src(P, cp, j, role, c, f);
     const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
-    float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
-                                     : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+    float v = !nz ? 0.f
+                  : (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                           : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
     out[nf + i] = cvt<T>(v);
   }
 }
@@ -76,12 +77,13 @@ __global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const 
     int br = rem / P.FT, f = tile * P.FT + rem % P.FT;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      int k = k0 + e, role = br, kk = k;
-      if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
+      int k = k0 + e, role, kk;
+      const bool nz = fprop_src(P, br, k, role, kk);
       int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
       const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
-      float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
-                                       : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+      float v = !nz ? 0.f
+                    : (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                             : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
       out[i0 + e] = cvt<T>(v);
     }
   } else {
@@ -94,11 +96,11 @@ __global__ void pack_all_kernel(Plan P, const float* w0, const float* w1, const 
       int ee = k / P.Jd, j = k % P.Jd;
       int ey = ee / P.r, ex = ee % P.r, dy = P.r - 1 - ey, dx = P.r - 1 - ex;
       int role, f, c;
-      if (P.sq == 2) { role = cp / P.C; c = cp % P.C; f = j; }
-      else { role = j / P.F; f = j % P.F; c = cp; }
+      const bool nz = dgrad_src(P, cp, j, role, c, f);
       const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
-      float v = (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
-                                       : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
+      float v = !nz ? 0.f
+                    : (P.kind == QD_KIND_FC) ? w[(size_t)c * P.F + f]
+                                             : w[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx];
       out[nf + i0 + e] = cvt<T>(v);
     }
   }
@@ -334,6 +336,12 @@ __global__ void fwd_epilogue_kernel(Plan P, const float* G, const float* b0, con
       float av = g[f], bv = g[P.F + f];
       out = av * bv;
       a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
+    } else if (P.family == QD_FAM_T2AND4) {
+      float av = g[f], bv = g[P.F + f];
+      out = av * bv + g[2 * P.F + f];
+      a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
+    } else if (P.family == QD_FAM_T3) {
+      out = g[f] * g[f];
     } else if (P.family == QD_FAM_FIRST_ORDER) {
       out = g[f] + b0[f];
     } else {
@@ -351,7 +359,7 @@ __global__ void bwd_prologue_kernel(Plan P, const T* dy, const T* a, const T* b,
   int s = blockIdx.x;
   long long r0 = (long long)s * rows_per, r1 = r0 + rows_per;
   if (r1 > P.Mout) r1 = P.Mout;
-  bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  bool mat = caches_ab(P.family);
   int F = P.F;
   for (int f = threadIdx.x; f < F; f += blockDim.x) {
     float s0 = 0.f, s1 = 0.f, s2 = 0.f;
@@ -364,17 +372,41 @@ __global__ void bwd_prologue_kernel(Plan P, const T* dy, const T* a, const T* b,
         T* drow = D + (size_t)m * P.Jd;
         drow[f] = cvt<T>(d0);
         drow[F + f] = cvt<T>(d1);
-        if (P.family == QD_FAM_PROPOSED) drow[2 * F + f] = cvt<T>(g);
+        if (d_has_g(P.family)) drow[2 * F + f] = cvt<T>(g);
         s0 += d0; s1 += d1; s2 += g;
       } else {
         s0 += g;
       }
     }
     float* o = part + (size_t)s * P.Jd;
-    if (P.family == QD_FAM_PROPOSED) { o[f] = s0; o[F + f] = s1; o[2 * F + f] = s2; }
+    if (d_has_g(P.family)) { o[f] = s0; o[F + f] = s1; o[2 * F + f] = s2; }
     else if (P.family == QD_FAM_T4) { o[f] = s0; o[F + f] = s1; }
     else o[f] = s0;
   }
+}
+
+// t3 (neurons.py:406-411): a = Wa x is recomputed (never cached); D = 2 g a.
+// `a` is the fp32 recompute (SIMT) or the stored bf16 recompute (tcgen05, in place).
+template <typename T, typename A>
+__global__ void t3_prologue_kernel(long long n, const T* dy, const A* a, T* D) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    float t = ld(dy + i) * ld(a + i);
+    D[i] = cvt<T>(t + t);
+  }
+}
+void launch_t3_prologue(const Plan& P, const void* dy, const void* a, bool a_fp32, void* D, cudaStream_t st) {
+  const long long n = P.Mout * P.F;
+  if (P.dtype == QD_BF16) {
+    if (a_fp32)
+      t3_prologue_kernel<bf16, float><<<grid_for(n), 256, 0, st>>>(n, (const bf16*)dy, (const float*)a, (bf16*)D);
+    else
+      t3_prologue_kernel<bf16, bf16><<<grid_for(n), 256, 0, st>>>(n, (const bf16*)dy, (const bf16*)a, (bf16*)D);
+  } else {
+    t3_prologue_kernel<float, float><<<grid_for(n), 256, 0, st>>>(n, (const float*)dy, (const float*)a,
+                                                                  (float*)D);
+  }
+  count_launch(st, "prologue_t3");
 }
 
 void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const void* b, void* D,
@@ -427,9 +459,8 @@ __global__ void wgrad_finish_kernel(Plan P, const float* part, int S, float* w0,
     int j = (int)(i / P.Kf), k = (int)(i % P.Kf);
     float acc = 0.f;
     for (int s = 0; s < S; ++s) acc += part[(size_t)s * total + i];
-    int role, f = j % P.F, kk = k;
-    if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
-    else role = j / P.F;
+    int role, f, kk;
+    if (!wgrad_dst(P, j, k, role, f, kk)) continue;  // t2and4 structural zero
     int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
     float* dst = role == 0 ? w0 : (role == 1 ? w1 : w2);
     if (!dst) continue;
@@ -451,6 +482,13 @@ __global__ void square_kernel(const T* x, T* xs, long long n) {
     float v = ld(x + i);
     xs[i] = cvt<T>(v * v);
   }
+}
+
+void launch_square_out(const Plan& P, void* y, cudaStream_t st) {
+  long long n = P.Mout * P.F;
+  if (P.dtype == QD_BF16) square_kernel<bf16><<<grid_for(n), 256, 0, st>>>((const bf16*)y, (bf16*)y, n);
+  else square_kernel<float><<<grid_for(n), 256, 0, st>>>((const float*)y, (float*)y, n);
+  count_launch(st, "square_out");
 }
 
 void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st) {
@@ -512,8 +550,18 @@ static int simt_backward_t(const Plan& P, const T* x, const T* wpack, const T* a
   const T* wd = wpack + pack_fprop_elems(P);
   float* bpart = (float*)(ws + L.off_BS);
   const T* D = dy;
-  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4) D = (const T*)(ws + L.off_D);
-  launch_bwd_prologue(P, dy, a, b, (void*)D, bpart, L.bs_split, st);
+  if (caches_ab(P.family)) D = (const T*)(ws + L.off_D);
+  if (P.family == QD_FAM_T3) {
+    // recompute a = Wa x (fp32, the forward GEMM) and form D = 2 g a
+    float* G = (float*)(ws + L.off_P);
+    FpropA<T> la{x, P.H, P.W, P.C, P.OH, P.OW, P.r, P.s, P.p, P.K0, P.sq};
+    FpropB<T> lb{wpack, P.F, P.nb, P.FT, P.Kf};
+    simt_gemm(la, lb, (int)P.Mout, P.F, P.Kf, 1, G, st);
+    D = (const T*)(ws + L.off_D);
+    launch_t3_prologue(P, dy, G, true, (void*)D, st);
+  } else {
+    launch_bwd_prologue(P, dy, a, b, (void*)D, bpart, L.bs_split, st);
+  }
   if (db[0]) launch_bias_finish(P, bpart, L.bs_split, db, st);
   if (dW[0]) {
     // wgrad: [Jd][Kf] = D^T * im2col(x | x*x), split over pixels
@@ -609,9 +657,8 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
     for (int e = 0; e < 4; ++e) {
       long long i = i4 + e;
       int j = (int)(i / P.Kf), k = (int)(i % P.Kf);
-      int role, f = j % P.F, kk = k;
-      if (P.sq == 2) { role = k / P.K0; kk = k % P.K0; }
-      else role = j / P.F;
+      int role, f, kk;
+      if (!wgrad_dst(P, j, k, role, f, kk)) continue;  // t2and4 structural zero
       int tap = kk / P.C, c = kk % P.C, dy = tap / P.r, dx = tap % P.r;
       float* dst = role == 0 ? w0 : (role == 1 ? w1 : w2);
       if (!dst) continue;

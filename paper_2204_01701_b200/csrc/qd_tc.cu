@@ -482,8 +482,8 @@ __global__ void __launch_bounds__(256) bwd_prologue_vec_kernel(Plan P, const bf1
   const int F = P.F, chunks = F / 8;
   const int lanes = 256 / chunks;  // rows processed concurrently
   const int ch = threadIdx.x % chunks, rl = threadIdx.x / chunks;
-  const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
-  const bool prop = P.family == QD_FAM_PROPOSED;
+  const bool mat = caches_ab(P.family);
+  const bool prop = d_has_g(P.family);
   const long long rows = up ? (long long)P.N * OH1 * OW1 : P.Mout;
   long long r0 = (long long)blockIdx.x * rows_per, r1 = r0 + rows_per;
   if (r1 > rows) r1 = rows;
@@ -640,7 +640,7 @@ struct GemmCfg {
 };
 static GemmCfg fprop_cfg(const Plan& P) {
   GemmCfg c;
-  if (P.family == QD_FAM_PROPOSED) { c.epi = EPI_PROPOSED; c.nbk = 3; }
+  if (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T2AND4) { c.epi = EPI_PROPOSED; c.nbk = 3; }
   else if (P.family == QD_FAM_T4) { c.epi = EPI_T4; c.nbk = 2; }
   else { c.epi = EPI_PLAIN; c.nbk = plain_blocks(P.F); }
   if (c.epi == EPI_PLAIN) {
@@ -648,7 +648,7 @@ static GemmCfg fprop_cfg(const Plan& P) {
     c.nbias = P.family == QD_FAM_FIRST_ORDER ? 1 : 0;
   } else {
     c.tiles_nn = P.F / 64; c.b_rs_tile = c.nbk * 64; c.out_c_tile = 64; c.nout = 3;
-    c.nbias = P.family == QD_FAM_PROPOSED ? 3 : 0;
+    c.nbias = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T2AND4) ? 3 : 0;  // t2and4: zero biases
   }
   c.b_rs_blk = 64;
   return c;
@@ -685,6 +685,7 @@ bool tc_supported(const Plan& P, unsigned flags) {
   if (P.OH < 1 || P.OW < 1) return false;
   if (!init_driver()) return false;
   if (P.s == 1) return true;
+  if (P.family == QD_FAM_T3) return false;  // t3 stride 2: CUDA-core path
   return !(flags & QD_FLAG_TC_V1) && s2_fits(P);
 }
 
@@ -850,6 +851,25 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
 
 static int plain_blocks(int ch) { return ch % 256 == 0 ? 4 : (ch % 128 == 0 ? 2 : 1); }
 
+// plain fprop GEMM (no bias, one output) -- the t3 forward and its backward recompute
+static int tc_fprop_plain(const Plan& P, const void* a0, const void* a1, const void* wpack, void* out,
+                          cudaStream_t st) {
+  GemmCfg c = fprop_cfg(P);
+  const float* nob[3] = {nullptr, nullptr, nullptr};
+  if (P.s == 2) {
+    Plan P1 = stride1_plan(P);
+    return run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P1.OW, P1.OH, P.p, P.r, 0, wpack, P.nb * P.F, P.Kf,
+                     c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, out, nullptr, nullptr, P.F, nob, nullptr, st, 2);
+  }
+  if (!(P.flags & QD_FLAG_TC_V1)) {
+    int rc2 = run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 0, wpack, P.nb * P.F,
+                        P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, out, nullptr, nullptr, P.F, nob, nullptr, st);
+    if (rc2 != QD_ERR_UNSUPPORTED) return rc2;
+  }
+  return run_conv(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 0, wpack, P.nb * P.F, P.Kf,
+                  c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, out, nullptr, nullptr, P.F, nob, nullptr, st);
+}
+
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
                void* b, char* ws, const Workspace& L, cudaStream_t st) {
   const void* a0 = x;
@@ -863,6 +883,19 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
   const float* nb3[3] = {bias[0], bias[1], bias[2]};
   GemmCfg c = fprop_cfg(P);
   if (c.nbias == 0) nb3[0] = nb3[1] = nb3[2] = nullptr;
+  if (P.family == QD_FAM_T2AND4) {
+    // y = a b + c through the proposed epilogue with zero biases
+    float* z = (float*)(ws + L.off_ZB);
+    cudaMemsetAsync(z, 0, (size_t)3 * P.F * 4, st);
+    nb3[0] = z; nb3[1] = z + P.F; nb3[2] = z + 2 * P.F;
+  }
+  if (P.family == QD_FAM_T3) {
+    // y = (Wa x)^2: the plain GEMM, then the square in place
+    int rc = tc_fprop_plain(P, a0, a1, wpack, y, st);
+    if (rc) return rc;
+    launch_square_out(P, y, st);
+    return check_launch("t3 forward");
+  }
   if (P.s == 2) {
     // stride-1 grid, epilogue keeps the even positions
     Plan P1 = stride1_plan(P);
@@ -908,7 +941,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   const bool up = P0.s == 2;
   const Plan P = up ? stride1_plan(P0) : P0;
   const bf16* wd = (const bf16*)wpack + pack_fprop_elems(P);
-  const bool mat = (P.family == QD_FAM_PROPOSED || P.family == QD_FAM_T4);
+  const bool mat = caches_ab(P.family);
   const bf16* D = (const bf16*)dy;
   float* bpart = (float*)(ws + L.off_BS);
   cudaStream_t side = nullptr;
@@ -923,7 +956,16 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   }
   const int dsplit = d2 ? 2 * P.F / 64 : 0;
   bool wg_pdl = false;  // a PDL-launched v2/v3 wgrad immediately precedes the dgrad on `st`
-  if (mat || P.nbias || up) {
+  if (P.family == QD_FAM_T3) {
+    // a = Wa x is recomputed into the D buffer, then D = 2 dy a in place
+    // (on the stride-1 grid for stride 2 the prologue below upsamples it)
+    bf16* Dw = (bf16*)(ws + L.off_D);
+    if (up) return set_error(QD_ERR_UNSUPPORTED, "t3 stride 2 on the tcgen05 path");
+    int rc0 = tc_fprop_plain(P0, x, nullptr, wpack, Dw, st);
+    if (rc0) return rc0;
+    launch_t3_prologue(P, dy, Dw, false, Dw, st);
+    D = Dw;
+  } else if (mat || P.nbias || up) {
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
     bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;

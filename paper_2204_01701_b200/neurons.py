@@ -34,12 +34,13 @@ from .spec import (DEVICE_FAMILIES, FAMILIES, KINDS, QUADRATIC_FAMILIES, T1_FAMI
 
 # weight roles in GEMM-branch order and bias roles, per family (the C ABI's
 # w[0..2] / bias[0..2] slots)
-WEIGHT_ROLES = {"proposed": ("Wa", "Wb", "Wc"), "t4": ("Wa", "Wb"), "t2": ("Wa",),
-                "first_order": ("W",), "t2_linear": ("Wa", "Wc")}
+WEIGHT_ROLES = {"proposed": ("Wa", "Wb", "Wc"), "t4": ("Wa", "Wb"), "t2": ("Wa",), "t3": ("Wa",),
+                "first_order": ("W",), "t2_linear": ("Wa", "Wc"), "t2and4": ("Wa", "Wb", "Wc")}
 BIAS_ROLES = {"proposed": ("ba", "bb", "bc"), "first_order": ("b",)}
 # gradient dict order of the reference symbolic_backward (neurons.py:380-391, :433-444)
 GRAD_ORDER = {"proposed": ("bc", "Wc", "bb", "Wb", "ba", "Wa"), "t4": ("Wb", "Wa"),
-              "t2": ("Wa",), "first_order": ("b", "W"), "t2_linear": ("Wa", "Wc")}
+              "t2": ("Wa",), "t3": ("Wa",), "first_order": ("b", "W"), "t2_linear": ("Wa", "Wc"),
+              "t2and4": ("Wc", "Wb", "Wa")}
 
 _DAMPED_SECOND_FACTOR = ("t4", "t2and4", "proposed")
 
@@ -179,7 +180,7 @@ def forward(spec, params, x, *, dtype=None, flags=0):
         mk = lambda: torch.empty(yshape, dtype=cdt, device=x.device)  # noqa: E731
     y = mk()
     a = b = None
-    if spec.family in ("proposed", "t4"):
+    if spec.family in ("proposed", "t4", "t2and4"):
         a, b = mk(), mk()
     ws = _workspace(desc, x.device)
     st = lib.qd_forward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),

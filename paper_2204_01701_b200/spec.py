@@ -34,7 +34,7 @@ KINDS = ("fc", "conv", "dwconv")
 
 # what the B200 kernels implement (the BASELINE.json hot path + first_order,
 # which the degeneration tests compare against)
-DEVICE_FAMILIES = ("first_order", "t2", "t4", "proposed", "t2_linear")
+DEVICE_FAMILIES = ("first_order", "t2", "t3", "t4", "t2and4", "proposed", "t2_linear")
 DEVICE_KINDS = ("fc", "conv")
 
 # second factor of a product branch starts small (neurons.py:47, :142-143)
@@ -218,14 +218,16 @@ def gemm_branches(family):
     proposed: [Wa;Wb;Wc] -> 3; t4: [Wa;Wb] -> 2; t2/first_order: 1;
     t2_linear: 1 branch whose K is doubled ([x*x | x] against [Wa | Wc]).
     """
-    return {"proposed": 3, "t4": 2, "t2": 1, "first_order": 1, "t2_linear": 1}[family]
+    return {"proposed": 3, "t4": 2, "t2": 1, "t3": 1, "first_order": 1, "t2_linear": 1, "t2and4": 3}[family]
 
 
 def gemm_flops(spec, n, h=1, w=1):
     """Algorithmic fwd+bwd FLOPs (2*MAC of fprop + dgrad + wgrad GEMMs).
 
     Matches SURVEY.md §8(d): 3+3+3 GEMMs for proposed, 2+2+2 for t4 and
-    t2_linear, 1+1+1 for t2/first_order; elementwise work excluded.
+    t2_linear, 1+1+1 for t2/first_order; t2and4 3+3+3 (a, b on x, c on x*x);
+    t3 1 + (1 recompute + 1 + 1) = 4 (the reference recomputes Wa x in the
+    backward, neurons.py:406-411); elementwise work excluded.
     """
     if spec.kind == "fc":
         oh = ow = 1
@@ -234,6 +236,8 @@ def gemm_flops(spec, n, h=1, w=1):
         oh = conv_out_size(h, spec.kernel, spec.stride, spec.pad)
         ow = conv_out_size(w, spec.kernel, spec.stride, spec.pad)
         k = spec.in_dim * spec.kernel ** 2
-    nb = {"proposed": 3, "t4": 2, "t2": 1, "first_order": 1, "t2_linear": 2}[spec.family]
     one = 2 * n * oh * ow * k * spec.out_dim
+    if spec.family == "t3":
+        return 4 * one
+    nb = {"proposed": 3, "t4": 2, "t2": 1, "first_order": 1, "t2_linear": 2, "t2and4": 3}[spec.family]
     return 3 * nb * one

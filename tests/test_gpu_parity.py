@@ -125,6 +125,14 @@ TC_CASES = [
     ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
     ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
     ("t2_linear", "fc", 64, 128, 64, 1, 1, 1, 1, 0),
+    # t3 (a recomputed in the backward) and t2and4 (dual K with structural zeros)
+    ("t3", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("t3", "conv", 2, 64, 128, 16, 16, 3, 1, 1),
+    ("t3", "fc", 96, 128, 64, 1, 1, 1, 1, 0),
+    ("t2and4", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("t2and4", "conv", 2, 64, 64, 16, 16, 3, 1, 1),
+    ("t2and4", "conv", 2, 64, 64, 16, 18, 3, 2, 1),
+    ("t2and4", "fc", 64, 64, 128, 1, 1, 1, 1, 0),
 ]
 
 

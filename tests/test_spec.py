@@ -63,8 +63,12 @@ def test_error_messages_match_reference_regexes():
 def test_device_spec_gate():
     S.validate_device_spec(S.QuadraticLayerSpec(kind="conv", family="proposed", in_dim=64,
                                                 out_dim=64, kernel=3, pad=1))
+    S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t3", in_dim=4, out_dim=4))
+    S.validate_device_spec(S.QuadraticLayerSpec(kind="conv", family="t2and4", in_dim=4, out_dim=4,
+                                                kernel=3, pad=1))
     with pytest.raises(E.ConfigError):
-        S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t3", in_dim=4, out_dim=4))
+        S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t1_pure", in_dim=4,
+                                                    out_dim=1))
     with pytest.raises(E.ConfigError):
         S.validate_device_spec(S.QuadraticLayerSpec(kind="dwconv", family="t4", in_dim=4,
                                                     out_dim=4, kernel=3))
