@@ -50,6 +50,7 @@ WORKLOADS = {
     # families beyond the BASELINE sweep
     "c5_t3_64x56": ("t3", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
     "c5_t2and4_64x56": ("t2and4", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
+    "dw_proposed_256x28": ("proposed", "dwconv", 64, 256, 256, 28, 28, 3, 1, 1, "bf16"),
 }
 METRIC = "quadratic_conv_fwd_bwd_tflops"
 L2_NOTE = ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read so the "
@@ -266,7 +267,7 @@ def run_ours(args, wl, wl_name):
         P64 = Q.synthetic_layer(fam, kind, 1, c, f, h, w, r, s, p, seed=0)[1]
     x = torch.as_tensor(x64, device=dev).to(dt)
     gy = torch.as_tensor(g64, device=dev).to(dt)
-    if kind == "conv":
+    if kind != "fc":
         x = x.contiguous(memory_format=torch.channels_last)
         gy = gy.contiguous(memory_format=torch.channels_last)
     params = {k_: torch.as_tensor(v, dtype=torch.float32, device=dev) for k_, v in P64.items()}

@@ -41,7 +41,7 @@ enum {
   QD_FAM_T3 = 5,          /* (Wa x)^2                                 */
   QD_FAM_T2AND4 = 6       /* (Wa x) * (Wb x) + Wc (x*x)               */
 };
-enum { QD_KIND_FC = 0, QD_KIND_CONV = 1 };
+enum { QD_KIND_FC = 0, QD_KIND_CONV = 1, QD_KIND_DWCONV = 2 /* depth-wise, C == F */ };
 enum { QD_F32 = 0, QD_BF16 = 1 };
 
 /* status codes; the Python layer re-raises the reference exception classes
@@ -112,7 +112,7 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack,
                 void* workspace, void* stream);
 
 /* Which implementation qd_forward / qd_backward will use for d:
- * 0 = generic CUDA-core (SIMT) kernels, 1 = tcgen05/TMA kernels. */
+ * 0 = generic CUDA-core (SIMT) kernels, 1 = tcgen05/TMA kernels, 2 = depth-wise direct kernels. */
 int qd_path(const qd_desc* d);
 
 const char* qd_error_string(int status);

@@ -177,7 +177,15 @@ def gen_layer_golden(neurons, tensor, Spec):
             ("t2and4", "fc", 5, 7, 6, 1, 1, 1, 1, 0),
             ("t2and4", "conv", 3, 3, 4, 5, 5, 3, 1, 1),
             ("t2and4", "conv", 3, 3, 4, 5, 5, 3, 2, 1),
-            ("t2and4", "conv", 2, 3, 2, 5, 5, 2, 1, 0)]):
+            ("t2and4", "conv", 2, 3, 2, 5, 5, 2, 1, 0),
+            # depth-wise kind (tensor.py:367-418) for every family that allows it
+            ("proposed", "dwconv", 3, 4, 4, 6, 6, 3, 1, 1),
+            ("proposed", "dwconv", 2, 3, 3, 7, 7, 3, 2, 1),
+            ("t4", "dwconv", 2, 4, 4, 6, 5, 3, 1, 1),
+            ("t2", "dwconv", 2, 4, 4, 6, 6, 3, 1, 1),
+            ("t3", "dwconv", 2, 4, 4, 6, 6, 2, 1, 0),
+            ("t2and4", "dwconv", 2, 4, 4, 6, 6, 3, 2, 1),
+            ("first_order", "dwconv", 2, 4, 4, 6, 6, 3, 1, 1)]):
         spec = Spec(kind=kind, family=fam, in_dim=c, out_dim=f, kernel=k, stride=s, pad=p)
         params = {role: rng2.normal(size=shape)
                   for role, shape in neurons.param_shapes(spec).items()}

@@ -82,6 +82,47 @@ def conv_backward(g, col, w, x_shape, stride, pad):
     return dw, col2im(dcol, x_shape, r, stride, pad, oh, ow)
 
 
+def dw_im2col(x, r, stride, pad):
+    """Per-channel patch matrix (N, C, r*r, oh*ow); tensor.py:367-380."""
+    n, c, h, w = x.shape
+    oh = conv_out_size(h, r, stride, pad)
+    ow = conv_out_size(w, r, stride, pad)
+    img = np.pad(x, ((0, 0), (0, 0), (pad, pad), (pad, pad)))
+    col = np.empty((n, c, r * r, oh * ow))
+    for dy in range(r):
+        ymax = dy + stride * oh
+        for dx in range(r):
+            xmax = dx + stride * ow
+            col[:, :, dy * r + dx, :] = img[:, :, dy:ymax:stride, dx:xmax:stride].reshape(n, c, -1)
+    return col, oh, ow
+
+
+def dwconv_forward(x, w, stride, pad):
+    """tensor.py:383-388: per-channel cross-correlation, w (C, r, r)."""
+    n, c = x.shape[:2]
+    col, oh, ow = dw_im2col(x, w.shape[-1], stride, pad)
+    y = np.einsum("nckl,ck->ncl", col, w.reshape(c, -1)).reshape(n, c, oh, ow)
+    return np.ascontiguousarray(y)
+
+
+def dwconv_backward(g, col, w, x_shape, stride, pad):
+    """tensor.py:391-405: (dW, dX)."""
+    n, c, oh, ow = g.shape
+    r = w.shape[-1]
+    gmat = g.reshape(n, c, -1)
+    dw = np.einsum("ncl,nckl->ck", gmat, col).reshape(w.shape)
+    dcol = np.einsum("ncl,ck->nckl", gmat, w.reshape(c, -1))
+    img = np.zeros((n, c, x_shape[2] + 2 * pad, x_shape[3] + 2 * pad))
+    for dy in range(r):
+        ymax = dy + stride * oh
+        for dx in range(r):
+            xmax = dx + stride * ow
+            img[:, :, dy:ymax:stride, dx:xmax:stride] += dcol[:, :, dy * r + dx, :].reshape(n, c, oh, ow)
+    if pad:
+        return dw, img[:, :, pad:pad + x_shape[2], pad:pad + x_shape[3]]
+    return dw, img
+
+
 class Geometry:
     """kind + (kernel, stride, pad); mirrors the spec fields the math needs."""
 
@@ -93,6 +134,8 @@ def _lin(geo, x, w):
     """neurons.py:223-228 (fc: x @ W with W (in, out); conv: im2col GEMM)."""
     if geo.kind == "fc":
         return x @ w
+    if geo.kind == "dwconv":
+        return dwconv_forward(x, w, geo.stride, geo.pad)
     return conv_forward(x, w, geo.stride, geo.pad)
 
 
@@ -133,8 +176,17 @@ def forward(family, geo, P, x):
 
 
 def _grads(geo, g, col, w, x_shape):
-    """neurons.py:283-286 (conv) / fc GEMMs."""
+    """neurons.py:283-286 (conv / dwconv)."""
+    if geo.kind == "dwconv":
+        return dwconv_backward(g, col, w, x_shape, geo.stride, geo.pad)
     return conv_backward(g, col, w, x_shape, geo.stride, geo.pad)
+
+
+def _col(geo, x):
+    """neurons.py:289-292 (_make_col)."""
+    if geo.kind == "dwconv":
+        return dw_im2col(x, geo.kernel, geo.stride, geo.pad)[0]
+    return im2col(x, geo.kernel, geo.stride, geo.pad)[0]
 
 
 def symbolic_backward(family, geo, P, x, a, b, g):
@@ -206,27 +258,27 @@ def symbolic_backward(family, geo, P, x, a, b, g):
     r, s_, p_ = geo.kernel, geo.stride, geo.pad
     if family == "first_order":                          # :396-399
         grads["b"] = g.sum(axis=(0, 2, 3))
-        col = im2col(xa, r, s_, p_)[0]
+        col = _col(geo, xa)
         grads["W"], dx = _grads(geo, g, col, P["W"], x_shape)
     elif family == "t2":                                 # :400-405
         s = xa * xa
-        col_s = im2col(s, r, s_, p_)[0]
+        col_s = _col(geo, s)
         grads["Wa"], ds = _grads(geo, g, col_s, P["Wa"], x_shape)
         t = ds * xa
         dx = t + t
     elif family == "t3":                                 # :406-411
-        col = im2col(xa, r, s_, p_)[0]
+        col = _col(geo, xa)
         av = _lin(geo, xa, P["Wa"])
         t = g * av
         da = t + t
         grads["Wa"], dx = _grads(geo, da, col, P["Wa"], x_shape)
     elif family == "t2and4":                             # :420-432
         s = xa * xa
-        col_s = im2col(s, r, s_, p_)[0]
+        col_s = _col(geo, s)
         grads["Wc"], ds = _grads(geo, g, col_s, P["Wc"], x_shape)
         t = ds * xa
         dx = t + t
-        col = im2col(xa, r, s_, p_)[0]
+        col = _col(geo, xa)
         da = g * b
         db = g * a
         grads["Wb"], dxb = _grads(geo, db, col, P["Wb"], x_shape)
@@ -234,7 +286,7 @@ def symbolic_backward(family, geo, P, x, a, b, g):
         grads["Wa"], dxa = _grads(geo, da, col, P["Wa"], x_shape)
         dx = dx + dxa
     elif family == "t4":                                 # :412-419
-        col = im2col(xa, r, s_, p_)[0]
+        col = _col(geo, xa)
         da = g * b
         db = g * a
         grads["Wb"], dxb = _grads(geo, db, col, P["Wb"], x_shape)
@@ -243,16 +295,16 @@ def symbolic_backward(family, geo, P, x, a, b, g):
         dx = dx + dxa
     elif family == "t2_linear":
         s = xa * xa
-        col_s = im2col(s, r, s_, p_)[0]
+        col_s = _col(geo, s)
         grads["Wa"], ds = _grads(geo, g, col_s, P["Wa"], x_shape)
         t = ds * xa
         dx = t + t
-        col = im2col(xa, r, s_, p_)[0]
+        col = _col(geo, xa)
         grads["Wc"], dxl = _grads(geo, g, col, P["Wc"], x_shape)
         dx = dx + dxl
     elif family == "proposed":                           # :433-444
         grads["bc"] = g.sum(axis=(0, 2, 3))
-        col = im2col(xa, r, s_, p_)[0]
+        col = _col(geo, xa)
         grads["Wc"], dx = _grads(geo, g, col, P["Wc"], x_shape)
         da = g * b
         db = g * a
@@ -310,6 +362,12 @@ def synthetic_layer(family, kind, n, c, f, h=1, w=1, r=1, stride=1, pad=0,
         wshape = (c, f)
         fan = c
         oh = ow = None
+    elif kind == "dwconv":
+        x = rx.standard_normal((n, c, h, w))
+        wshape = (c, r, r)
+        fan = r * r
+        oh = conv_out_size(h, r, stride, pad)
+        ow = conv_out_size(w, r, stride, pad)
     else:
         x = rx.standard_normal((n, c, h, w))
         wshape = (f, c, r, r)

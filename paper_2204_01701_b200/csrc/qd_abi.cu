@@ -60,10 +60,31 @@ int check_launch(const char* what) {
 
 static size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 
+static int device_path(const Plan& P, unsigned flags) {
+  if (P.kind == QD_KIND_DWCONV) return 2;
+  return tc_supported(P, flags) ? 1 : 0;
+}
+
 Workspace plan_workspace(const Plan& P, int path) {
   Workspace L;
   memset(&L, 0, sizeof(L));
   size_t es = P.dtype == QD_BF16 ? 2 : 4;
+  if (path == 2) {  // depth-wise: D, bias partials, wgrad partials
+    if (caches_ab(P.family) || P.family == QD_FAM_T3) L.sz_D = (size_t)P.Mout * P.Jd * es;
+    L.wg_split = dw_wgrad_split(P);
+    int nroles = P.nroles;
+    L.sz_WG = (size_t)L.wg_split * nroles * P.r * P.r * P.C * 4;
+    long long bs = (P.Mout + 255) / 256;
+    if (bs > 2 * 148) bs = 2 * 148;
+    L.bs_split = (int)(bs < 1 ? 1 : bs);
+    L.sz_BS = (size_t)L.bs_split * P.Jd * 4;
+    size_t off = 0;
+    L.off_D = off; off = align_up(off + L.sz_D);
+    L.off_WG = off; off = align_up(off + L.sz_WG);
+    L.off_BS = off; off = align_up(off + L.sz_BS);
+    L.total = off;
+    return L;
+  }
   if (path == 0) {
     size_t a = (size_t)P.Mout * P.nb * P.F, b = (size_t)P.Min * P.Cd;
     L.sz_P = (a > b ? a : b) * 4;
@@ -109,12 +130,14 @@ static int validate(const qd_desc* d) {
   if (!d) return set_error(QD_ERR_ARG, "null descriptor");
   if (d->family < 0 || d->family > QD_FAM_T2AND4)
     return set_error(QD_ERR_CONFIG, "unknown family %d", d->family);
-  if (d->kind != QD_KIND_FC && d->kind != QD_KIND_CONV)
+  if (d->kind != QD_KIND_FC && d->kind != QD_KIND_CONV && d->kind != QD_KIND_DWCONV)
     return set_error(QD_ERR_CONFIG, "unknown layer kind %d", d->kind);
   if (d->dtype != QD_F32 && d->dtype != QD_BF16)
     return set_error(QD_ERR_CONFIG, "unknown dtype %d", d->dtype);
   if (d->C < 1 || d->F < 1)
     return set_error(QD_ERR_CONFIG, "layer dims must be positive: %d->%d", d->C, d->F);
+  if (d->kind == QD_KIND_DWCONV && d->C != d->F)  // neurons.py:73-75
+    return set_error(QD_ERR_CONFIG, "dwconv requires in == out channels, got %d->%d", d->C, d->F);
   if (d->N < 1 || d->H < 1 || d->W < 1)
     return set_error(QD_ERR_DIM, "tensor dimensions must be positive, got (%d, %d, %d, %d)", d->N,
                      d->C, d->H, d->W);
@@ -154,6 +177,7 @@ int qd_out_shape(const qd_desc* d, int* OH, int* OW) {
 size_t qd_pack_bytes(const qd_desc* d) {
   if (validate(d)) return 0;
   Plan P = make_plan(*d);
+  if (P.kind == QD_KIND_DWCONV) return dw_pack_bytes(P);
   size_t es = P.dtype == QD_BF16 ? 2 : 4;
   return (pack_fprop_elems(P) + pack_dgrad_elems(P)) * es;
 }
@@ -161,13 +185,13 @@ size_t qd_pack_bytes(const qd_desc* d) {
 int qd_path(const qd_desc* d) {
   if (validate(d)) return -1;
   Plan P = make_plan(*d);
-  return tc_supported(P, d->flags) ? 1 : 0;
+  return device_path(P, d->flags);
 }
 
 size_t qd_workspace_bytes(const qd_desc* d) {
   if (validate(d)) return 0;
   Plan P = make_plan(*d);
-  return plan_workspace(P, tc_supported(P, d->flags) ? 1 : 0).total;
+  return plan_workspace(P, device_path(P, d->flags)).total;
 }
 
 int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void* stream) {
@@ -177,7 +201,10 @@ int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void
   for (int i = 0; i < P.nroles; ++i)
     if (!w || !w[i]) return set_error(QD_ERR_ARG, "weight role %d is NULL", i);
   if (!wpack) return set_error(QD_ERR_ARG, "wpack is NULL");
-  launch_pack(P, w, wpack, (cudaStream_t)stream);
+  if (P.kind == QD_KIND_DWCONV)
+    dw_pack(P, w, wpack, (cudaStream_t)stream);
+  else
+    launch_pack(P, w, wpack, (cudaStream_t)stream);
   return check_launch("pack weights");
 }
 
@@ -194,10 +221,11 @@ int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* 
     return set_error(QD_ERR_ARG, "family caches a and b: a_cache/b_cache must be given");
   const float* nob[3] = {nullptr, nullptr, nullptr};
   const float* const* bs = bias ? bias : nob;
-  int path = tc_supported(P, d->flags) ? 1 : 0;
+  int path = device_path(P, d->flags);
   Workspace L = plan_workspace(P, path);
   if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
   cudaStream_t s = (cudaStream_t)stream;
+  if (path == 2) return dw_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
   if (path == 1) return tc_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
   return simt_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
 }
@@ -216,11 +244,12 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* 
   float* nof[3] = {nullptr, nullptr, nullptr};
   float* const* w = (dW && !(d->flags & QD_FLAG_NO_DW)) ? dW : nof;
   float* const* b = (db && !(d->flags & QD_FLAG_NO_DW)) ? db : nof;
-  int path = tc_supported(P, d->flags) ? 1 : 0;
+  int path = device_path(P, d->flags);
   Workspace L = plan_workspace(P, path);
   if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
   void* dxp = (d->flags & QD_FLAG_NO_DX) ? nullptr : dx;
   cudaStream_t s = (cudaStream_t)stream;
+  if (path == 2) return dw_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
   if (path == 1) return tc_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
   return simt_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
 }

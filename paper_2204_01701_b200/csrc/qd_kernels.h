@@ -98,6 +98,15 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// ---- depth-wise path (qd_dw.cu): qd_path() == 2 ------------------------------
+size_t dw_pack_bytes(const Plan& P);
+void dw_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st);
+int dw_wgrad_split(const Plan& P);
+int dw_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
+               void* b, char* ws, const Workspace& L, cudaStream_t st);
+int dw_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
+                void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L, cudaStream_t st);
+
 // ---- tcgen05 path ----------------------------------------------------------
 bool tc_supported(const Plan& P, unsigned flags);
 int tc_wgrad_split(const Plan& P);

@@ -108,8 +108,8 @@ def make_desc(spec, x_shape, dtype, flags=0):
     d.dtype = _lib.BF16 if dtype == torch.bfloat16 else _lib.F32
     d.N = int(x_shape[0])
     d.C = int(x_shape[1])
-    d.H = int(x_shape[2]) if spec.kind == "conv" else 1
-    d.W = int(x_shape[3]) if spec.kind == "conv" else 1
+    d.H = int(x_shape[2]) if spec.kind != "fc" else 1
+    d.W = int(x_shape[3]) if spec.kind != "fc" else 1
     d.F = spec.out_dim
     d.r, d.stride, d.pad = spec.kernel, spec.stride, spec.pad
     d.flags = flags
@@ -117,7 +117,7 @@ def make_desc(spec, x_shape, dtype, flags=0):
 
 
 def _layout(t, kind):
-    return t.contiguous(memory_format=torch.channels_last) if kind == "conv" else t.contiguous()
+    return t.contiguous(memory_format=torch.channels_last) if kind != "fc" else t.contiguous()
 
 
 def _weights(spec, params):
@@ -171,7 +171,7 @@ def forward(spec, params, x, *, dtype=None, flags=0):
     oh, ow = ctypes.c_int(), ctypes.c_int()
     lib.qd_out_shape(ctypes.byref(desc), ctypes.byref(oh), ctypes.byref(ow))
     wpack, key, biases, _ = _pack(spec, desc, params)
-    if spec.kind == "conv":
+    if spec.kind != "fc":
         yshape = (x.shape[0], spec.out_dim, oh.value, ow.value)
         mk = lambda: torch.empty(yshape, dtype=cdt, device=x.device,  # noqa: E731
                                  memory_format=torch.channels_last)

@@ -35,7 +35,7 @@ KINDS = ("fc", "conv", "dwconv")
 # what the B200 kernels implement (the BASELINE.json hot path + first_order,
 # which the degeneration tests compare against)
 DEVICE_FAMILIES = ("first_order", "t2", "t3", "t4", "t2and4", "proposed", "t2_linear")
-DEVICE_KINDS = ("fc", "conv")
+DEVICE_KINDS = ("fc", "conv", "dwconv")
 
 # second factor of a product branch starts small (neurons.py:47, :142-143)
 _DAMPED_SECOND_FACTOR = ("t4", "t2and4", "proposed")
@@ -109,7 +109,7 @@ def validate_device_spec(spec):
             f"{', '.join(DEVICE_FAMILIES)})")
     if spec.kind not in DEVICE_KINDS:
         raise ConfigError(
-            f"kind {spec.kind!r} has no B200 kernel (supported: fc, conv)")
+            f"kind {spec.kind!r} has no B200 kernel (supported: fc, conv, dwconv)")
 
 
 def param_shapes(spec):
@@ -237,6 +237,8 @@ def gemm_flops(spec, n, h=1, w=1):
         ow = conv_out_size(w, spec.kernel, spec.stride, spec.pad)
         k = spec.in_dim * spec.kernel ** 2
     one = 2 * n * oh * ow * k * spec.out_dim
+    if spec.kind == "dwconv":  # one r*r filter per channel
+        one = 2 * n * oh * ow * spec.kernel ** 2 * spec.out_dim
     if spec.family == "t3":
         return 4 * one
     nb = {"proposed": 3, "t4": 2, "t2": 1, "first_order": 1, "t2_linear": 2, "t2and4": 3}[spec.family]

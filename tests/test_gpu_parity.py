@@ -269,3 +269,26 @@ def test_kernels_launch_counter():
     x, P, g = Q.synthetic_layer("proposed", "conv", 2, 64, 64, 8, 8, 3, 1, 1)
     run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
     assert _lib.launch_count() > before
+
+
+# depth-wise kind: direct kernels (qd_path == 2), every family that allows it
+DW_CASES = [
+    ("proposed", 4, 32, 14, 14, 3, 1, 1),
+    ("proposed", 3, 24, 15, 13, 3, 2, 1),
+    ("t4", 2, 16, 9, 9, 3, 1, 1),
+    ("t2", 2, 16, 9, 9, 5, 1, 2),
+    ("t3", 2, 16, 9, 9, 3, 1, 1),
+    ("t2_linear", 2, 16, 9, 9, 3, 1, 1),
+    ("t2and4", 2, 16, 10, 10, 3, 2, 1),
+    ("first_order", 2, 16, 9, 9, 3, 1, 1),
+]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("case", DW_CASES, ids=[f"{c[0]}-{c[2]}x{c[3]}-k{c[5]}s{c[6]}" for c in DW_CASES])
+def test_dwconv_parity(case, dtype):
+    fam, n, c, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, "dwconv", n, c, c, h, w, k, s, p, seed=11, random_bias=True)
+    path = check_against_oracle(fam, "dwconv", x, P, g, dtype, k, s, p)
+    assert path == 2

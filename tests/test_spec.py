@@ -69,9 +69,11 @@ def test_device_spec_gate():
     with pytest.raises(E.ConfigError):
         S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t1_pure", in_dim=4,
                                                     out_dim=1))
-    with pytest.raises(E.ConfigError):
+    S.validate_device_spec(S.QuadraticLayerSpec(kind="dwconv", family="t4", in_dim=4,
+                                                out_dim=4, kernel=3))
+    with pytest.raises(E.ConfigError, match="in == out"):
         S.validate_device_spec(S.QuadraticLayerSpec(kind="dwconv", family="t4", in_dim=4,
-                                                    out_dim=4, kernel=3))
+                                                    out_dim=8, kernel=3))
 
 
 def test_t2_linear_counters():
