@@ -48,6 +48,8 @@ void launch_bwd_prologue(const Plan& P, const void* dy, const void* a, const voi
                          void* D, float* bsum_part, int bs_split, cudaStream_t st);
 // t3: D = 2 dy a from the recomputed a (fp32 SIMT GEMM output or dtype, may alias D)
 void launch_t3_prologue(const Plan& P, const void* dy, const void* a, bool a_fp32, void* D, cudaStream_t st);
+void launch_bwd_prologue_vec(const Plan& P, const void* dy, const void* a, const void* b, void* D, float* part,
+                             int split, cudaStream_t st);  // bf16, F % 8 == 0
 void launch_bias_finish(const Plan& P, const float* bsum_part, int bs_split,
                         float* const db[3], cudaStream_t st);
 // sum the wgrad partials [S][Jd][Kf] and scatter into reference layouts

@@ -870,6 +870,15 @@ static int tc_fprop_plain(const Plan& P, const void* a0, const void* a1, const v
                   c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, out, nullptr, nullptr, P.F, nob, nullptr, st);
 }
 
+// the vectorised prologue for other callers (depth-wise path), bf16 only
+void launch_bwd_prologue_vec(const Plan& P, const void* dy, const void* a, const void* b, void* D, float* part,
+                             int split, cudaStream_t st) {
+  long long rows_per = (P.Mout + split - 1) / split;
+  bwd_prologue_vec_kernel<<<split, 256, 0, st>>>(P, (const bf16*)dy, (const bf16*)a, (const bf16*)b, (bf16*)D,
+                                                 part, rows_per, 0, P.OH, P.OW, P.Jd);
+  count_launch(st, "prologue");
+}
+
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
                void* b, char* ws, const Workspace& L, cudaStream_t st) {
   const void* a0 = x;
