@@ -120,7 +120,20 @@ __global__ void __launch_bounds__(256) pack_conv_kernel(Plan P, const float* w0,
   if ((int)blockIdx.x < nrow) {
     const int br = blockIdx.x / P.F, f = blockIdx.x - br * P.F;
     const float* w = (br == 0 ? w0 : (br == 1 ? w1 : w2)) + (size_t)f * P.C * rr;
-    for (int i = threadIdx.x; i < P.C * rr; i += blockDim.x) sbuf[i] = w[i];
+    const int nsrc = P.C * rr;
+    for (int i0 = threadIdx.x; i0 < nsrc; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * blockDim.x;
+        v[u] = i < nsrc ? __ldg(w + i) : 0.f;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < nsrc) sbuf[i] = v[u];
+      }
+    }
     __syncthreads();
     const int R = (f / P.FT) * (P.nb * P.FT) + br * P.FT + f % P.FT;
     T* o = out + (size_t)R * P.Kf;
@@ -130,11 +143,25 @@ __global__ void __launch_bounds__(256) pack_conv_kernel(Plan P, const float* w0,
     }
   } else {
     const int c = blockIdx.x - nrow;
-    for (int i = threadIdx.x; i < P.Jd * rr; i += blockDim.x) {
-      const int j = i / rr, t = i - j * rr;
-      const int br = j / P.F, f = j - br * P.F;
-      const float* w = br == 0 ? w0 : (br == 1 ? w1 : w2);
-      sbuf[i] = w[((size_t)f * P.C + c) * rr + t];
+    const int nsrc = P.Jd * rr;
+    for (int i0 = threadIdx.x; i0 < nsrc; i0 += 8 * blockDim.x) {  // 8 loads in flight per thread
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * blockDim.x;
+        v[u] = 0.f;
+        if (i < nsrc) {
+          const int j = i / rr, t = i - j * rr;
+          const int br = j / P.F, f = j - br * P.F;
+          const float* w = br == 0 ? w0 : (br == 1 ? w1 : w2);
+          v[u] = __ldg(w + ((size_t)f * P.C + c) * rr + t);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int i = i0 + u * blockDim.x;
+        if (i < nsrc) sbuf[i] = v[u];
+      }
     }
     __syncthreads();
     T* o = out + (size_t)nrow * P.Kf + (size_t)c * P.Kd;

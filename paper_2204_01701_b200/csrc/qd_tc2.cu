@@ -1399,8 +1399,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     if (leader) ptx::mma_commit(done);
     __syncwarp();
-  } else if (warp >= 4) {
-    const int q = warp & 3;
+  }
+  {
+    // ===== epilogue on all 8 warps: warp w reads TMEM lanes 32 (w % 4) and
+    // stores half h = w / 4 of every accumulator's columns =====
+    const int q = warp & 3, hh = warp >> 2;
     const int row = q * 32 + lane;
     const bool has_work = q_end > q_beg;
     if (has_work) {
@@ -1424,8 +1427,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       const bool ok = c_hi > c_lo;
       const int k = half * g.K0 + tap * g.C + cb * 64 + (row & 63);
       const int ncols = (acc < 2) ? g.NT : (nhi - nlo) * 64;
+      const int cw = ncols / 2;
 #pragma unroll 1
-      for (int c = 0; c < ncols; c += 16) {
+      for (int c = hh * cw; c < (hh + 1) * cw; c += 16) {
         float v[16];
         if (has_work) {
           ptx::tmem_ld16(tmem + ((uint32_t)(q * 32) << 16) + acc * g.NT + c, v);
