@@ -39,7 +39,10 @@ enum {
   QD_FAM_PROPOSED = 3,    /* (Wa x + ba) * (Wb x + bb) + (Wc x + bc)  */
   QD_FAM_T2_LINEAR = 4,   /* Wa (x*x) + Wc x                          */
   QD_FAM_T3 = 5,          /* (Wa x)^2                                 */
-  QD_FAM_T2AND4 = 6       /* (Wa x) * (Wb x) + Wc (x*x)               */
+  QD_FAM_T2AND4 = 6,      /* (Wa x) * (Wb x) + Wc (x*x)               */
+  QD_FAM_T1_PURE = 7,     /* x^T Wq x              (fc, one output)   */
+  QD_FAM_T1_FULL = 8,     /* x^T Wq x + x Wb       (fc, one output)   */
+  QD_FAM_T1AND2 = 9       /* x^T Wq x + (x*x) Wb   (fc, one output)   */
 };
 enum { QD_KIND_FC = 0, QD_KIND_CONV = 1, QD_KIND_DWCONV = 2 /* depth-wise, C == F */ };
 enum { QD_F32 = 0, QD_BF16 = 1 };

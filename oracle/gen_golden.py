@@ -185,7 +185,11 @@ def gen_layer_golden(neurons, tensor, Spec):
             ("t2", "dwconv", 2, 4, 4, 6, 6, 3, 1, 1),
             ("t3", "dwconv", 2, 4, 4, 6, 6, 2, 1, 0),
             ("t2and4", "dwconv", 2, 4, 4, 6, 6, 3, 2, 1),
-            ("first_order", "dwconv", 2, 4, 4, 6, 6, 3, 1, 1)]):
+            ("first_order", "dwconv", 2, 4, 4, 6, 6, 3, 1, 1),
+            # T1 families: fc, one output unit (neurons.py:58-65)
+            ("t1_pure", "fc", 5, 7, 1, 1, 1, 1, 1, 0),
+            ("t1_full", "fc", 5, 7, 1, 1, 1, 1, 1, 0),
+            ("t1and2", "fc", 5, 7, 1, 1, 1, 1, 1, 0)]):
         spec = Spec(kind=kind, family=fam, in_dim=c, out_dim=f, kernel=k, stride=s, pad=p)
         params = {role: rng2.normal(size=shape)
                   for role, shape in neurons.param_shapes(spec).items()}

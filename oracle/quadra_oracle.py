@@ -150,6 +150,16 @@ def forward(family, geo, P, x):
     a = b = None
     if family == "first_order":
         y = _bias(geo, _lin(geo, x, P["W"]), P["b"])
+    elif family == "t1_pure":                             # :245-247
+        v = x @ P["Wq"]
+        y = (v * x).sum(axis=1, keepdims=True)
+    elif family == "t1_full":                             # :248-250
+        v = x @ P["Wq"]
+        y = (v * x).sum(axis=1, keepdims=True) + x @ P["Wb"]
+    elif family == "t1and2":                              # :251-254
+        s = x * x
+        v = x @ P["Wq"]
+        y = (v * x).sum(axis=1, keepdims=True) + s @ P["Wb"]
     elif family == "t2":
         y = _lin(geo, x * x, P["Wa"])
     elif family == "t3":                                  # :257-259
@@ -205,6 +215,35 @@ def symbolic_backward(family, geo, P, x, a, b, g):
             ds = g @ P["Wa"].T
             t = ds * xa
             dx = t + t
+        elif family == "t1_pure":                        # :320-326
+            v = xa @ P["Wq"]
+            dh = np.broadcast_to(g, xa.shape).copy()
+            dv = dh * xa
+            dx = dh * v
+            grads["Wq"] = xa.T @ dv
+            dx = dx + dv @ P["Wq"].T
+        elif family == "t1_full":                        # :327-335
+            v = xa @ P["Wq"]
+            grads["Wb"] = xa.T @ g
+            dx = g @ P["Wb"].T
+            dh = np.broadcast_to(g, xa.shape).copy()
+            dv = dh * xa
+            dx = dx + dh * v
+            grads["Wq"] = xa.T @ dv
+            dx = dx + dv @ P["Wq"].T
+        elif family == "t1and2":                         # :336-348
+            s = xa * xa
+            v = xa @ P["Wq"]
+            grads["Wb"] = s.T @ g
+            ds = g @ P["Wb"].T
+            dh = np.broadcast_to(g, xa.shape).copy()
+            dv = dh * xa
+            dx = dh * v
+            grads["Wq"] = xa.T @ dv
+            dx = dx + dv @ P["Wq"].T
+            t = ds * xa
+            dx = dx + t
+            dx = dx + t
         elif family == "t3":                             # :355-360
             av = xa @ P["Wa"]
             t = g * av
@@ -376,7 +415,17 @@ def synthetic_layer(family, kind, n, c, f, h=1, w=1, r=1, stride=1, pad=0,
         ow = conv_out_size(w, r, stride, pad)
     roles = {"first_order": ("W",), "t2": ("Wa",), "t3": ("Wa",), "t4": ("Wa", "Wb"),
              "t2_linear": ("Wa", "Wc"), "t2and4": ("Wa", "Wb", "Wc"),
-             "proposed": ("Wa", "Wb", "Wc")}[family]
+             "proposed": ("Wa", "Wb", "Wc"), "t1_pure": ("Wq",), "t1_full": ("Wq", "Wb"),
+             "t1and2": ("Wq", "Wb")}[family]
+    if family.startswith("t1"):  # one output unit, full-rank quadratic weight (neurons.py:90-95)
+        x = rx.standard_normal((n, c))
+        P = {}
+        bound = np.sqrt(6.0 / c)
+        P["Wq"] = rw.uniform(-bound, bound, size=(c, c)) / np.sqrt(c)
+        if family != "t1_pure":
+            P["Wb"] = rw.uniform(-bound, bound, size=(c, 1))
+        g = rg.standard_normal((n, 1))
+        return x, P, g
     P = {}
     bound = np.sqrt(6.0 / fan)
     for role in roles:

@@ -15,7 +15,8 @@ from .errors import ConfigError, DeviceError, DimensionError, IntegrityError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libquadra_b200.so")
 
-FAMILY_CODE = {"first_order": 0, "t2": 1, "t4": 2, "proposed": 3, "t2_linear": 4, "t3": 5, "t2and4": 6}
+FAMILY_CODE = {"first_order": 0, "t2": 1, "t4": 2, "proposed": 3, "t2_linear": 4, "t3": 5, "t2and4": 6,
+               "t1_pure": 7, "t1_full": 8, "t1and2": 9}
 KIND_CODE = {"fc": 0, "conv": 1, "dwconv": 2}
 F32, BF16 = 0, 1
 

@@ -62,6 +62,7 @@ static size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 
 static int device_path(const Plan& P, unsigned flags) {
   if (P.kind == QD_KIND_DWCONV) return 2;
+  if (is_t1(P.family)) return 0;
   return tc_supported(P, flags) ? 1 : 0;
 }
 
@@ -69,6 +70,7 @@ Workspace plan_workspace(const Plan& P, int path) {
   Workspace L;
   memset(&L, 0, sizeof(L));
   size_t es = P.dtype == QD_BF16 ? 2 : 4;
+  if (is_t1(P.family)) return t1_workspace(P);
   if (path == 2) {  // depth-wise: D, bias partials, wgrad partials
     if (caches_ab(P.family) || P.family == QD_FAM_T3) L.sz_D = (size_t)P.Mout * P.Jd * es;
     L.wg_split = dw_wgrad_split(P);
@@ -128,7 +130,7 @@ Workspace plan_workspace(const Plan& P, int path) {
 
 static int validate(const qd_desc* d) {
   if (!d) return set_error(QD_ERR_ARG, "null descriptor");
-  if (d->family < 0 || d->family > QD_FAM_T2AND4)
+  if (d->family < 0 || d->family > QD_FAM_T1AND2)
     return set_error(QD_ERR_CONFIG, "unknown family %d", d->family);
   if (d->kind != QD_KIND_FC && d->kind != QD_KIND_CONV && d->kind != QD_KIND_DWCONV)
     return set_error(QD_ERR_CONFIG, "unknown layer kind %d", d->kind);
@@ -136,6 +138,15 @@ static int validate(const qd_desc* d) {
     return set_error(QD_ERR_CONFIG, "unknown dtype %d", d->dtype);
   if (d->C < 1 || d->F < 1)
     return set_error(QD_ERR_CONFIG, "layer dims must be positive: %d->%d", d->C, d->F);
+  if (is_t1(d->family)) {  // neurons.py:58-65
+    static const char* names[3] = {"t1_pure", "t1_full", "t1and2"};
+    const char* nm = names[d->family - QD_FAM_T1_PURE];
+    if (d->kind != QD_KIND_FC)
+      return set_error(QD_ERR_CONFIG,
+                       "%s carries a full-rank quadratic weight and is restricted to fc layers (got kind=%s)", nm,
+                       d->kind == QD_KIND_CONV ? "conv" : "dwconv");
+    if (d->F != 1) return set_error(QD_ERR_CONFIG, "%s defines a single output unit; got out=%d", nm, d->F);
+  }
   if (d->kind == QD_KIND_DWCONV && d->C != d->F)  // neurons.py:73-75
     return set_error(QD_ERR_CONFIG, "dwconv requires in == out channels, got %d->%d", d->C, d->F);
   if (d->N < 1 || d->H < 1 || d->W < 1)
@@ -178,6 +189,7 @@ size_t qd_pack_bytes(const qd_desc* d) {
   if (validate(d)) return 0;
   Plan P = make_plan(*d);
   if (P.kind == QD_KIND_DWCONV) return dw_pack_bytes(P);
+  if (is_t1(P.family)) return t1_pack_bytes(P);
   size_t es = P.dtype == QD_BF16 ? 2 : 4;
   return (pack_fprop_elems(P) + pack_dgrad_elems(P)) * es;
 }
@@ -203,6 +215,8 @@ int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void
   if (!wpack) return set_error(QD_ERR_ARG, "wpack is NULL");
   if (P.kind == QD_KIND_DWCONV)
     dw_pack(P, w, wpack, (cudaStream_t)stream);
+  else if (is_t1(P.family))
+    t1_pack(P, w, wpack, (cudaStream_t)stream);
   else
     launch_pack(P, w, wpack, (cudaStream_t)stream);
   return check_launch("pack weights");
@@ -225,6 +239,7 @@ int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* 
   Workspace L = plan_workspace(P, path);
   if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
   cudaStream_t s = (cudaStream_t)stream;
+  if (is_t1(P.family)) return t1_forward(P, x, wpack, y, (char*)workspace, L, s);
   if (path == 2) return dw_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
   if (path == 1) return tc_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
   return simt_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
@@ -249,6 +264,7 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* 
   if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
   void* dxp = (d->flags & QD_FLAG_NO_DX) ? nullptr : dx;
   cudaStream_t s = (cudaStream_t)stream;
+  if (is_t1(P.family)) return t1_backward(P, x, wpack, dy, dxp, w, (char*)workspace, L, s);
   if (path == 2) return dw_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
   if (path == 1) return tc_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
   return simt_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);

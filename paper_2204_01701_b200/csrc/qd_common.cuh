@@ -56,6 +56,9 @@ inline Plan make_plan(const qd_desc& d) {
     // t2and4: K = [x*x | x] like t2_linear, three branches like proposed (a, b read
     // the x half, c the x*x half; the other halves are structural zeros)
     case QD_FAM_T2AND4:   P.nb = 3; P.sq = 2; P.Jd = 3 * P.F; P.nroles = 3; P.nbias = 0; break;
+    case QD_FAM_T1_PURE:  P.nb = 1; P.sq = 0; P.Jd = P.F;     P.nroles = 1; P.nbias = 0; break;
+    case QD_FAM_T1_FULL:
+    case QD_FAM_T1AND2:   P.nb = 1; P.sq = 0; P.Jd = P.F;     P.nroles = 2; P.nbias = 0; break;
     default:              P.nb = 1; P.sq = 0; P.Jd = P.F;     P.nroles = 1; P.nbias = 1; break;
   }
   P.K0 = P.r * P.r * P.C;

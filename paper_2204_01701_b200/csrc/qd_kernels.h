@@ -100,6 +100,16 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// ---- T1 families (qd_t1.cu): fc, one output, CUDA-core path ----------------
+bool is_t1(int family);
+size_t t1_pack_bytes(const Plan& P);
+void t1_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st);
+Workspace t1_workspace(const Plan& P);
+int t1_forward(const Plan& P, const void* x, const void* wpack, void* y, char* ws, const Workspace& L,
+               cudaStream_t st);
+int t1_backward(const Plan& P, const void* x, const void* wpack, const void* dy, void* dx, float* const dW[3],
+                char* ws, const Workspace& L, cudaStream_t st);
+
 // ---- depth-wise path (qd_dw.cu): qd_path() == 2 ------------------------------
 size_t dw_pack_bytes(const Plan& P);
 void dw_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st);

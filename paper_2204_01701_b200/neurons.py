@@ -35,12 +35,14 @@ from .spec import (DEVICE_FAMILIES, FAMILIES, KINDS, QUADRATIC_FAMILIES, T1_FAMI
 # weight roles in GEMM-branch order and bias roles, per family (the C ABI's
 # w[0..2] / bias[0..2] slots)
 WEIGHT_ROLES = {"proposed": ("Wa", "Wb", "Wc"), "t4": ("Wa", "Wb"), "t2": ("Wa",), "t3": ("Wa",),
-                "first_order": ("W",), "t2_linear": ("Wa", "Wc"), "t2and4": ("Wa", "Wb", "Wc")}
+                "first_order": ("W",), "t2_linear": ("Wa", "Wc"), "t2and4": ("Wa", "Wb", "Wc"),
+                "t1_pure": ("Wq",), "t1_full": ("Wq", "Wb"), "t1and2": ("Wq", "Wb")}
 BIAS_ROLES = {"proposed": ("ba", "bb", "bc"), "first_order": ("b",)}
 # gradient dict order of the reference symbolic_backward (neurons.py:380-391, :433-444)
 GRAD_ORDER = {"proposed": ("bc", "Wc", "bb", "Wb", "ba", "Wa"), "t4": ("Wb", "Wa"),
               "t2": ("Wa",), "t3": ("Wa",), "first_order": ("b", "W"), "t2_linear": ("Wa", "Wc"),
-              "t2and4": ("Wc", "Wb", "Wa")}
+              "t2and4": ("Wc", "Wb", "Wa"), "t1_pure": ("Wq",), "t1_full": ("Wb", "Wq"),
+              "t1and2": ("Wb", "Wq")}
 
 _DAMPED_SECOND_FACTOR = ("t4", "t2and4", "proposed")
 

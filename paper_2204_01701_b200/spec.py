@@ -34,7 +34,8 @@ KINDS = ("fc", "conv", "dwconv")
 
 # what the B200 kernels implement (the BASELINE.json hot path + first_order,
 # which the degeneration tests compare against)
-DEVICE_FAMILIES = ("first_order", "t2", "t3", "t4", "t2and4", "proposed", "t2_linear")
+DEVICE_FAMILIES = ("first_order", "t1_pure", "t1_full", "t1and2", "t2", "t3", "t4", "t2and4", "proposed",
+                   "t2_linear")
 DEVICE_KINDS = ("fc", "conv", "dwconv")
 
 # second factor of a product branch starts small (neurons.py:47, :142-143)
@@ -237,6 +238,8 @@ def gemm_flops(spec, n, h=1, w=1):
         ow = conv_out_size(w, spec.kernel, spec.stride, spec.pad)
         k = spec.in_dim * spec.kernel ** 2
     one = 2 * n * oh * ow * k * spec.out_dim
+    if spec.family in T1_FAMILIES:  # x Wq (n x n), x^T dv, dv Wq^T, + the recompute of x Wq
+        return 4 * 2 * n * spec.in_dim * spec.in_dim
     if spec.kind == "dwconv":  # one r*r filter per channel
         one = 2 * n * oh * ow * spec.kernel ** 2 * spec.out_dim
     if spec.family == "t3":

@@ -292,3 +292,14 @@ def test_dwconv_parity(case, dtype):
     x, P, g = Q.synthetic_layer(fam, "dwconv", n, c, c, h, w, k, s, p, seed=11, random_bias=True)
     path = check_against_oracle(fam, "dwconv", x, P, g, dtype, k, s, p)
     assert path == 2
+
+
+# T1 families (fc, one output unit, full-rank quadratic weight): CUDA-core path
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
+@pytest.mark.parametrize("fam", ["t1_pure", "t1_full", "t1and2"])
+@pytest.mark.parametrize("n,c", [(64, 96), (300, 256)])
+def test_t1_parity(fam, n, c, dtype):
+    x, P, g = Q.synthetic_layer(fam, "fc", n, c, 1, seed=5)
+    path = check_against_oracle(fam, "fc", x, P, g, dtype)
+    assert path == 0

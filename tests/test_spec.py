@@ -66,9 +66,13 @@ def test_device_spec_gate():
     S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t3", in_dim=4, out_dim=4))
     S.validate_device_spec(S.QuadraticLayerSpec(kind="conv", family="t2and4", in_dim=4, out_dim=4,
                                                 kernel=3, pad=1))
-    with pytest.raises(E.ConfigError):
+    S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t1_pure", in_dim=4, out_dim=1))
+    with pytest.raises(E.ConfigError, match="single output"):
         S.validate_device_spec(S.QuadraticLayerSpec(kind="fc", family="t1_pure", in_dim=4,
-                                                    out_dim=1))
+                                                    out_dim=2))
+    with pytest.raises(E.ConfigError, match="fc layers"):
+        S.validate_device_spec(S.QuadraticLayerSpec(kind="conv", family="t1_full", in_dim=4,
+                                                    out_dim=1, kernel=3))
     S.validate_device_spec(S.QuadraticLayerSpec(kind="dwconv", family="t4", in_dim=4,
                                                 out_dim=4, kernel=3))
     with pytest.raises(E.ConfigError, match="in == out"):
