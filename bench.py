@@ -558,6 +558,7 @@ def run_net(args, name):
 
     from paper_2204_01701_b200 import _lib, qnets
     from paper_2204_01701_b200.dp import BucketedAllReduce, broadcast_module, sgd
+    from paper_2204_01701_b200.optim import QuadSGD
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -572,7 +573,9 @@ def run_net(args, name):
     torch.manual_seed(1234)
     model = getattr(qnets, builder)(num_classes=classes).to(dev).to(memory_format=torch.channels_last)
     broadcast_module(model)  # every replica starts from rank 0's weights and BN buffers
-    opt = sgd(model.parameters(), lr=0.01)
+    # fused SGD + weight pack for the quadratic layers;
+    # --torch-sgd for torch.optim.SGD everywhere (the forward then packs itself)
+    opt = sgd(model.parameters(), lr=0.01) if args.torch_sgd else QuadSGD(model, lr=0.01)
     red = BucketedAllReduce(model.parameters(), bucket_mb=25.0)
     gen = torch.Generator(device=dev).manual_seed(rank)
     x = torch.randn(batch, 3, hw, hw, device=dev, generator=gen).to(torch.bfloat16).contiguous(
@@ -707,6 +710,7 @@ def main():
     ap.add_argument("--workload", default="c2", choices=sorted(WORKLOADS) + sorted(NETS))
     ap.add_argument("--batch", type=int, default=0, help="per-GPU batch for the net workloads")
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
+    ap.add_argument("--torch-sgd", action="store_true", help="nets: torch.optim.SGD instead of the fused SGD+pack")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graph)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup

@@ -97,6 +97,17 @@ size_t qd_workspace_bytes(const qd_desc* d);
 int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack,
                     void* stream);
 
+/* Fused SGD + weight pack: the reference sgd_step
+ * (trainer.py:50-61) on the fp32 weight roles, in place,
+ *   v <- momentum v + (g + weight_decay w)   (v = g + weight_decay w when first != 0)
+ *   w <- w - lr v
+ * and, in the same pass, the updated weights written into wpack in the layout
+ * qd_pack_weights produces (structural zeros of the layout are left as they
+ * are: pass a wpack that was packed once before). fc / conv kinds, families
+ * other than the T1 ones. Biases are not touched. */
+int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const float* const grad[3],
+                float lr, float momentum, float weight_decay, int first, void* wpack, void* stream);
+
 /* Forward: neurons.forward (neurons.py:235-276).
  * bias[i]: fp32 (F) per role (proposed ba, bb, bc; first_order b; else NULL).
  * y: output NHWC; a_cache/b_cache: the LayerCache a, b (proposed/t4, NHWC,

@@ -27,7 +27,8 @@ FLAG_NO_DX, FLAG_FORCE_SIMT, FLAG_NO_DW, FLAG_TC_V1 = 1, 2, 4, 8
 EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_pack_weights", "qd_forward", "qd_backward", "qd_path",
            "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version",
-           "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read")
+           "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read",
+           "qd_sgd_pack")
 
 
 class QdDesc(ctypes.Structure):
@@ -70,6 +71,9 @@ def load():
         lib.qd_workspace_bytes.restype = ctypes.c_size_t
         lib.qd_pack_weights.argtypes = [P(QdDesc), fp3, vp, vp]
         lib.qd_pack_weights.restype = ctypes.c_int
+        lib.qd_sgd_pack.argtypes = [P(QdDesc), fp3, fp3, fp3, ctypes.c_float, ctypes.c_float, ctypes.c_float,
+                                    ctypes.c_int, vp, vp]
+        lib.qd_sgd_pack.restype = ctypes.c_int
         lib.qd_forward.argtypes = [P(QdDesc), vp, vp, fp3, vp, vp, vp, vp, vp]
         lib.qd_forward.restype = ctypes.c_int
         lib.qd_backward.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, fp3, fp3, vp, vp]

@@ -222,6 +222,20 @@ int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void
   return check_launch("pack weights");
 }
 
+int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const float* const grad[3],
+                float lr, float momentum, float weight_decay, int first, void* wpack, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  if (P.kind == QD_KIND_DWCONV || is_t1(P.family))
+    return set_error(QD_ERR_UNSUPPORTED, "qd_sgd_pack: fc / conv kinds of the non-T1 families only");
+  if (!w || !mom || !grad || !wpack) return set_error(QD_ERR_ARG, "qd_sgd_pack: NULL argument");
+  for (int i = 0; i < P.nroles; ++i)
+    if (!w[i] || !mom[i] || !grad[i]) return set_error(QD_ERR_ARG, "qd_sgd_pack: role %d has a NULL pointer", i);
+  launch_sgd_pack(P, w, mom, grad, lr, momentum, weight_decay, first, wpack, (cudaStream_t)stream);
+  return check_launch("sgd pack");
+}
+
 int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* const bias[3],
                void* y, void* a_cache, void* b_cache, void* workspace, void* stream) {
   int st = validate(d);

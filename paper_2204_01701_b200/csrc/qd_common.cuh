@@ -134,6 +134,28 @@ __host__ __device__ inline bool wgrad_dst(const Plan& P, int j, int k, int& role
   return true;
 }
 
+// inverse of fprop_src / dgrad_src: where weight element (role, f, c, tap) lives in
+// the packed fprop matrix (row R, column kf) and the packed dgrad matrix (row cp, column kd)
+__host__ __device__ inline void pack_positions(const Plan& P, int role, int f, int c, int tap, int& R, int& kf,
+                                               int& cp, int& kd) {
+  const int rr = P.r * P.r, e = rr - 1 - tap;
+  int br = role, half = 0, j = role * P.F + f;
+  cp = c;
+  if (P.family == QD_FAM_T2AND4) {
+    half = role == 2 ? 0 : 1;
+    cp = (role == 2 ? 0 : 1) * P.C + c;
+  } else if (P.sq == 2) {  // t2_linear: one branch, role = K half
+    br = 0;
+    half = role;
+    j = f;
+    cp = role * P.C + c;
+  }
+  const int tile = f / P.FT;
+  R = tile * P.nb * P.FT + br * P.FT + (f - tile * P.FT);
+  kf = half * P.K0 + tap * P.C + c;
+  kd = e * P.Jd + j;
+}
+
 // Row of branch `br`, channel `f` inside the packed fprop weights: branches are
 // interleaved per FT-wide channel tile so one TMA box of nb*FT rows carries
 // [Wa_tile; Wb_tile; Wc_tile] for the same output channels.

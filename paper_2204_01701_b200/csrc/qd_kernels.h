@@ -100,6 +100,9 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
+                     float momentum, float wd, int first, void* wpack, cudaStream_t st);
+
 // ---- T1 families (qd_t1.cu): fc, one output, CUDA-core path ----------------
 bool is_t1(int family);
 size_t t1_pack_bytes(const Plan& P);

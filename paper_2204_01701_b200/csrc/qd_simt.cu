@@ -214,6 +214,59 @@ void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream
   count_launch(st, "pack");
 }
 
+// fused SGD (trainer.py:50-61) + pack: one thread per weight element of every role
+template <typename T>
+__global__ void sgd_pack_kernel(Plan P, float* w0, float* w1, float* w2, float* m0, float* m1, float* m2,
+                                const float* g0, const float* g1, const float* g2, float lr, float mom, float wd,
+                                int first, T* out) {
+  const int rr = P.r * P.r;
+  const long long per = (long long)P.F * P.C * rr;  // elements of one role
+  const long long nf = (long long)P.nb * P.F * P.Kf;
+  const long long tot = per * P.nroles;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < tot;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int role = (int)(i / per);
+    const long long o = i - role * per;
+    float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+    float* m = role == 0 ? m0 : (role == 1 ? m1 : m2);
+    const float* g = role == 0 ? g0 : (role == 1 ? g1 : g2);
+    const float d = g[o] + wd * w[o];
+    const float v = first ? d : mom * m[o] + d;
+    m[o] = v;
+    const float nw = w[o] - lr * v;
+    w[o] = nw;
+    int f, c, tap;
+    if (P.kind == QD_KIND_FC) {  // reference fc layout (in, out)
+      c = (int)(o / P.F);
+      f = (int)(o - (long long)c * P.F);
+      tap = 0;
+    } else {  // (F, C, r, r)
+      f = (int)(o / ((long long)P.C * rr));
+      const int rem = (int)(o - (long long)f * P.C * rr);
+      c = rem / rr;
+      tap = rem - c * rr;
+    }
+    int R, kf, cp, kd;
+    pack_positions(P, role, f, c, tap, R, kf, cp, kd);
+    const T pv = cvt<T>(nw);
+    out[(size_t)R * P.Kf + kf] = pv;
+    out[nf + (size_t)cp * P.Kd + kd] = pv;
+  }
+}
+
+void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
+                     float momentum, float wd, int first, void* wpack, cudaStream_t st) {
+  const long long tot = (long long)P.F * P.C * P.r * P.r * P.nroles;
+  const int grid = grid_for(tot);
+  if (P.dtype == QD_BF16)
+    sgd_pack_kernel<bf16><<<grid, 256, 0, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2], grad[0], grad[1],
+                                                grad[2], lr, momentum, wd, first, (bf16*)wpack);
+  else
+    sgd_pack_kernel<float><<<grid, 256, 0, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2], grad[0], grad[1],
+                                                 grad[2], lr, momentum, wd, first, (float*)wpack);
+  count_launch(st, "sgd_pack");
+}
+
 // ---------------------------------------------------------------------------
 // generic tiled SIMT GEMM:  out[s][m][n] = sum_{k in split s} A(m,k) * B(n,k)
 // ---------------------------------------------------------------------------

@@ -139,10 +139,38 @@ def _pack_key(ws):
     return tuple((id(t), t._version, t.data_ptr()) for t in ws)
 
 
+def _pack_tag(desc):
+    """layout identity of a packed weight buffer (it does not depend on N, H, W)"""
+    return (desc.family, desc.kind, desc.dtype, desc.C, desc.F, desc.r)
+
+
+def _registered_pack(desc, ws):
+    """A packed buffer the fused optimizer (optim.QuadSGD) registered for exactly
+    these weight versions, else None. Only that optimizer registers packs, so
+    the default path packs on every call as before."""
+    hit = getattr(ws[0], "_qd_pack", None)
+    if hit is None:
+        return None
+    tag, key, wpack = hit
+    if tag == _pack_tag(desc) and key == _pack_key(ws):
+        return wpack
+    return None
+
+
+def register_pack(desc, params_by_role, wpack):
+    """Record `wpack` as the packed layout of the current weight versions."""
+    ws = list(params_by_role)
+    setattr(ws[0], "_qd_pack", (_pack_tag(desc), _pack_key(ws), wpack))
+
+
 def _pack(spec, desc, params):
     lib = _lib.load()
     roles = WEIGHT_ROLES[spec.family]
     P = _weights(spec, params)
+    hit = _registered_pack(desc, [P[r] for r in roles])
+    if hit is not None:
+        biases = [P[r].detach().to(torch.float32).contiguous() for r in BIAS_ROLES.get(spec.family, ())]
+        return hit, _pack_key([P[r] for r in roles]), biases, None
     ws = [P[r].detach().to(torch.float32).contiguous() for r in roles]
     nbytes = lib.qd_pack_bytes(ctypes.byref(desc))
     if nbytes == 0:

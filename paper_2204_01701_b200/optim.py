@@ -1,0 +1,90 @@
+"""Fused SGD + weight pack.
+
+``QuadSGD`` applies the reference ``sgd_step`` (trainer.py:50-61:
+v <- m v + g + wd p, first step v = g + wd p; p <- p - lr v -- the same update
+as ``torch.optim.SGD(momentum=m, weight_decay=wd, dampening=0)``) to every
+parameter. For the weight roles of the quadratic modules it runs one kernel
+per layer (``qd_sgd_pack``) that updates the fp32 masters and momentum in
+place AND writes the packed bf16 layouts the forward / backward kernels
+consume; the pack is registered on the weights' current versions, so the
+next forward skips its own packing launch. Gradients are read where autograd
+(or the data-parallel buckets of ``dp.BucketedAllReduce``) left them. All
+other parameters (biases, first-order layers, BN) go through
+``torch.optim.SGD`` with the same hyper-parameters.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import torch
+
+from . import _lib, neurons
+from .nn import _QuadBase
+
+
+class QuadSGD(torch.optim.Optimizer):
+    def __init__(self, model, lr=0.1, momentum=0.9, weight_decay=5e-4):
+        self.quad = [m for m in model.modules() if isinstance(m, _QuadBase) and m.spec.kind != "dwconv"
+                     and not m.spec.family.startswith("t1")]
+        fused = set()
+        for m in self.quad:
+            for r in neurons.WEIGHT_ROLES[m.spec.family]:
+                fused.add(id(getattr(m, r)))
+        # the kernel indexes weights in the reference layouts ((F, C, r, r) / (in, out)),
+        # so a module moved to channels_last gets its quadratic weights back in the
+        # standard layout (autograd then also produces gradients in that layout)
+        for m in self.quad:
+            for r in neurons.WEIGHT_ROLES[m.spec.family]:
+                w = getattr(m, r)
+                if not w.is_contiguous():
+                    w.data = w.data.contiguous()
+        params = [p for p in model.parameters() if p.requires_grad]
+        defaults = dict(lr=lr, momentum=momentum, weight_decay=weight_decay)
+        super().__init__(params, defaults)
+        rest = [p for p in params if id(p) not in fused]
+        self._rest = torch.optim.SGD(rest, lr=lr, momentum=momentum, weight_decay=weight_decay,
+                                     dampening=0.0, foreach=True) if rest else None
+        self._packs = {}
+
+    @torch.no_grad()
+    def step(self, closure=None):
+        loss = closure() if closure is not None else None
+        g = self.param_groups[0]
+        lr, mom, wd = g["lr"], g["momentum"], g["weight_decay"]
+        lib = _lib.load()
+        stream = torch.cuda.current_stream().cuda_stream
+        for m in self.quad:
+            roles = neurons.WEIGHT_ROLES[m.spec.family]
+            ws = [getattr(m, r) for r in roles]
+            if any(w.grad is None for w in ws):
+                continue
+            states = [self.state[w] for w in ws]
+            first = "momentum_buffer" not in states[0]
+            for w, stt in zip(ws, states):
+                if "momentum_buffer" not in stt:
+                    stt["momentum_buffer"] = torch.zeros_like(w, memory_format=torch.contiguous_format)
+            # the packed layout does not depend on the batch / image size
+            shape = (1, m.spec.in_dim) if m.spec.kind == "fc" else (1, m.spec.in_dim, m.spec.kernel,
+                                                                   m.spec.kernel)
+            desc = neurons.make_desc(m.spec, shape, m.compute_dtype)
+            key = id(m)
+            wpack = self._packs.get(key)
+            if wpack is None:
+                # once: a full pack (it also writes the layout's structural zeros)
+                wpack = neurons._pack(m.spec, desc, m.params())[0]
+                self._packs[key] = wpack
+            if not all(w.is_contiguous() for w in ws):
+                raise RuntimeError("QuadSGD: quadratic weights must stay in the standard contiguous layout")
+            grads = [w.grad.contiguous() for w in ws]
+            st = lib.qd_sgd_pack(ctypes.byref(desc), _lib.ptr3(*[w.data_ptr() for w in ws]),
+                                 _lib.ptr3(*[s_["momentum_buffer"].data_ptr() for s_ in states]),
+                                 _lib.ptr3(*[gr.data_ptr() for gr in grads]), float(lr), float(mom),
+                                 float(wd), int(first), wpack.data_ptr(), stream)
+            _lib.raise_for(st, "qd_sgd_pack")
+            for w in ws:  # the kernel changed the weights in place: bump their version counters
+                torch.autograd.graph.increment_version(w)
+            neurons.register_pack(desc, ws, wpack)
+        if self._rest is not None:
+            self._rest.step()
+        return loss

@@ -303,3 +303,43 @@ def test_t1_parity(fam, n, c, dtype):
     x, P, g = Q.synthetic_layer(fam, "fc", n, c, 1, seed=5)
     path = check_against_oracle(fam, "fc", x, P, g, dtype)
     assert path == 0
+
+
+# fused SGD + pack
+@pytest.mark.gpu
+@pytest.mark.parametrize("family,kind,c,f,k", [("proposed", "conv", 64, 64, 3), ("t4", "conv", 64, 128, 3),
+                                               ("t2_linear", "conv", 64, 64, 3), ("t2and4", "conv", 64, 64, 3),
+                                               ("proposed", "fc", 96, 64, 1), ("first_order", "conv", 8, 16, 3)])
+def test_quad_sgd_matches_torch_sgd_and_repack(family, kind, c, f, k):
+    from paper_2204_01701_b200 import neurons
+    from paper_2204_01701_b200.nn import QuadConv2d, QuadLinear
+    from paper_2204_01701_b200.optim import QuadSGD
+    torch.manual_seed(0)
+    mk = (lambda: QuadConv2d(c, f, k, 1, k // 2, family=family, device="cuda")) if kind == "conv" else \
+        (lambda: QuadLinear(c, f, family=family, device="cuda"))
+    m1, m2 = mk(), mk()
+    m2.load_state_dict(m1.state_dict())
+    if kind == "conv":  # the nets move whole models to channels_last
+        m1 = m1.to(memory_format=torch.channels_last)
+    o1 = QuadSGD(m1, lr=0.05, momentum=0.9, weight_decay=5e-4)
+    o2 = torch.optim.SGD(m2.parameters(), lr=0.05, momentum=0.9, weight_decay=5e-4, dampening=0.0)
+    x = torch.randn((4, c, 10, 10) if kind == "conv" else (32, c), device="cuda")
+    for it in range(3):
+        for mod, opt in ((m1, o1), (m2, o2)):
+            opt.zero_grad(set_to_none=True)
+            y = mod(x.to(torch.bfloat16).contiguous(memory_format=torch.channels_last) if kind == "conv"
+                    else x.to(torch.bfloat16))
+            y.float().square().mean().backward()
+            opt.step()
+        for (n1, p1), (n2, p2) in zip(m1.named_parameters(), m2.named_parameters()):
+            assert torch.allclose(p1, p2, rtol=1e-5, atol=1e-6), (it, n1)
+    # the registered pack equals a fresh pack of the updated weights, bit for bit
+    spec = m1.spec
+    shape = (1, c) if kind == "fc" else (1, c, k, k)
+    desc = neurons.make_desc(spec, shape, torch.bfloat16)
+    roles = neurons.WEIGHT_ROLES[spec.family]
+    reg = neurons._registered_pack(desc, [getattr(m1, r) for r in roles])
+    assert reg is not None
+    fresh = neurons._pack(spec, desc, {r: getattr(m1, r).detach().clone() for r in neurons.param_shapes(spec)})[0]
+    torch.cuda.synchronize()
+    assert torch.equal(reg, fresh)
