@@ -508,24 +508,34 @@ def net_quad_layers(name):
             hooks.append(m.register_forward_pre_hook(
                 lambda mod, inp: shapes.append((dataclasses.replace(mod.conv.spec, in_dim=mod.cin),
                                                 tuple(inp[0].shape[1:])))))
+    from paper_2204_01701_b200.bn import QuadConvBN
     for m in model.modules():
-        if isinstance(m, QuadConv2d) and id(m) not in inner:
+        if isinstance(m, QuadConvBN):  # fused conv -> BN (-> ReLU) node: its layer never runs forward()
+            hooks.append(m.register_forward_pre_hook(
+                lambda mod, inp: shapes.append((mod.layer.spec, tuple(inp[0].shape[1:])))))
+        elif isinstance(m, QuadConv2d) and id(m) not in inner:
             hooks.append(m.register_forward_pre_hook(
                 lambda mod, inp: shapes.append((mod.spec, tuple(inp[0].shape[1:])))))
     # trace shapes with a meta-device forward that bypasses the kernels
+    import paper_2204_01701_b200.bn as qbn
     import paper_2204_01701_b200.nn as qnn
-    orig = qnn.QuadFunction.apply
+    orig, orig_bn = qnn.QuadFunction.apply, qbn._QuadBNFunction.apply
 
     def fake(spec, dtype, x, *ts):
         oh = (x.shape[2] + 2 * spec.pad - spec.kernel) // spec.stride + 1
         ow = (x.shape[3] + 2 * spec.pad - spec.kernel) // spec.stride + 1
         return torch.empty(x.shape[0], spec.out_dim, oh, ow, device=x.device)
+
+    def fake_bn(spec, dtype, relu, bn, x, *ts):
+        return fake(spec, dtype, x)
     qnn.QuadFunction.apply = fake
+    qbn._QuadBNFunction.apply = fake_bn
     try:
         with torch.device("meta"):
             model(torch.empty(1, 3, hw, hw))
     finally:
         qnn.QuadFunction.apply = orig
+        qbn._QuadBNFunction.apply = orig_bn
         for h in hooks:
             h.remove()
     return shapes

@@ -68,6 +68,8 @@ enum {
                                  (frozen layers; per-kernel timing)        */
 #define QD_FLAG_TC_V1 8u      /* tcgen05 path without the CTA-pair / halo \
                                  conv kernel (tests compare the two)       */
+#define QD_FLAG_D_GIVEN 16u   /* backward: `dy` already is the operand D   \
+                                 (qd_bn_backward_D); bias grads not formed */
 
 typedef struct {
   int family, kind, dtype;
@@ -96,6 +98,24 @@ size_t qd_workspace_bytes(const qd_desc* d);
  * Replaces the implicit W.reshape(f,-1) of tensor.py:317, :329. */
 int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack,
                     void* stream);
+
+/* Batch norm (+ ReLU) around the quadratic conv,
+ * reference semantics tensor.py:423-470 / :552-570 (biased batch variance, also
+ * in the running update). NHWC tensors of M = N*OH*OW rows and C channels.
+ * Forward: z = relu?(gamma (y - mean) inv_std + beta); training computes the
+ * batch statistics (save_mean / save_invstd out) and folds them into
+ * run_mean / run_var; eval uses save_mean / save_invstd as given. */
+size_t qd_bn_workspace_bytes(long long M, int C, int Jd);
+int qd_bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta,
+                  float* run_mean, float* run_var, float momentum, float eps, int relu, int training,
+                  void* z, float* save_mean, float* save_invstd, void* ws, void* stream);
+/* BN(+ReLU) backward fused with the quadratic layer's backward prologue: from
+ * dz (gradient of z) and the layer's y, a, b it forms dgamma, dbeta, the layer's
+ * bias gradients db[] and the operand D the layer backward consumes; then call
+ * qd_backward with QD_FLAG_D_GIVEN and D as `dy`. Stride-1 layers; not t3. */
+int qd_bn_backward_D(const qd_desc* d, const void* dz, const void* y, const void* a, const void* b,
+                     const float* gamma, const float* beta, const float* save_mean, const float* save_invstd,
+                     int relu, void* D, float* dgamma, float* dbeta, float* const db[3], void* ws, void* stream);
 
 /* Fused SGD + weight pack: the reference sgd_step
  * (trainer.py:50-61) on the fp32 weight roles, in place,

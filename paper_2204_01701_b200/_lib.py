@@ -23,12 +23,13 @@ F32, BF16 = 0, 1
 QD_OK, QD_ERR_CONFIG, QD_ERR_DIM, QD_ERR_INTEGRITY = 0, 1, 2, 3
 QD_ERR_CUDA, QD_ERR_UNSUPPORTED, QD_ERR_ARG = 4, 5, 6
 FLAG_NO_DX, FLAG_FORCE_SIMT, FLAG_NO_DW, FLAG_TC_V1 = 1, 2, 4, 8
+FLAG_D_GIVEN = 16  # backward: dy is the operand D (qd_bn_backward_D)
 
 EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_pack_weights", "qd_forward", "qd_backward", "qd_path",
            "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version",
            "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read",
-           "qd_sgd_pack")
+           "qd_sgd_pack", "qd_bn_workspace_bytes", "qd_bn_forward", "qd_bn_backward_D")
 
 
 class QdDesc(ctypes.Structure):
@@ -74,6 +75,15 @@ def load():
         lib.qd_sgd_pack.argtypes = [P(QdDesc), fp3, fp3, fp3, ctypes.c_float, ctypes.c_float, ctypes.c_float,
                                     ctypes.c_int, vp, vp]
         lib.qd_sgd_pack.restype = ctypes.c_int
+        lib.qd_bn_workspace_bytes.argtypes = [ctypes.c_longlong, ctypes.c_int, ctypes.c_int]
+        lib.qd_bn_workspace_bytes.restype = ctypes.c_size_t
+        lib.qd_bn_forward.argtypes = [ctypes.c_longlong, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp,
+                                      ctypes.c_float, ctypes.c_float, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp,
+                                      vp]
+        lib.qd_bn_forward.restype = ctypes.c_int
+        lib.qd_bn_backward_D.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, fp3,
+                                         vp, vp]
+        lib.qd_bn_backward_D.restype = ctypes.c_int
         lib.qd_forward.argtypes = [P(QdDesc), vp, vp, fp3, vp, vp, vp, vp, vp]
         lib.qd_forward.restype = ctypes.c_int
         lib.qd_backward.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, fp3, fp3, vp, vp]

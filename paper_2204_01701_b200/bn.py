@@ -1,0 +1,216 @@
+"""Batch norm (+ ReLU) fused around the quadratic conv.
+
+Reference semantics (tensor.py:423-470 forward, :552-570 backward): batch
+statistics over (N, H, W) with the *biased* variance, used both to normalise
+and to update the running variance (momentum 0.1, eps 1e-5); eval mode uses
+the running statistics.
+
+``QuadConvBN`` = quadratic layer -> BN -> optional ReLU as ONE autograd node:
+
+* forward: the layer kernels produce y (and the a, b cache), one reduction
+  pass forms the batch statistics, one pass writes relu(BN(y));
+* backward: one reduction pass over (dz, y) gives dgamma / dbeta, ONE
+  elementwise pass applies the BN (+ReLU) backward and directly emits the
+  layer's backward operand D = [dy b | dy a | dy] and its bias gradients,
+  then the layer's wgrad / dgrad kernels run from D (``QD_FLAG_D_GIVEN``).
+  The BN-backward output dy is never materialised.
+
+Layers the fused backward does not cover (stride 2, t3, T1 families, dwconv)
+use the same reference BN semantics through torch ops (autograd).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+import torch
+from torch import nn
+
+from . import _lib, neurons
+from .nn import QuadFunction, _QuadBase
+from .spec import QuadraticLayerSpec, param_shapes
+
+
+def _rows(t):
+    """[M, C] row view of an NHWC (channels_last) or 2-D tensor (no copy)."""
+    if t.dim() == 4:
+        n, c, h, w = t.shape
+        return t.permute(0, 2, 3, 1).reshape(n * h * w, c)
+    return t
+
+
+def _dtype_code(t):
+    return _lib.BF16 if t.dtype == torch.bfloat16 else _lib.F32
+
+
+def bn_forward(y, gamma, beta, running_mean, running_var, momentum, eps, relu, training):
+    """z = relu?(gamma (y - mean) inv_std + beta); returns (z, save_mean, save_invstd)."""
+    lib = _lib.load()
+    yr = _rows(y)
+    M, C = yr.shape
+    if not yr.is_contiguous():
+        raise ValueError("bn_forward expects channels_last / row-major input")
+    z = torch.empty_like(y)
+    if training:
+        sm = torch.empty(C, dtype=torch.float32, device=y.device)
+        si = torch.empty(C, dtype=torch.float32, device=y.device)
+    else:
+        sm = running_mean.float().contiguous()
+        si = torch.rsqrt(running_var.float() + eps).contiguous()
+    ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, C), dtype=torch.uint8, device=y.device)
+    st = lib.qd_bn_forward(M, C, _dtype_code(y), y.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
+                           running_mean.data_ptr() if training else None,
+                           running_var.data_ptr() if training else None, float(momentum), float(eps), int(relu),
+                           int(training), z.data_ptr(), sm.data_ptr(), si.data_ptr(), ws.data_ptr(),
+                           torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_bn_forward")
+    return z, sm, si
+
+
+def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu):
+    """(D, dgamma, dbeta, {bias role: grad}) for the layer's backward from D."""
+    lib = _lib.load()
+    desc = neurons.make_desc(spec, cache.x.shape, cache.x.dtype)
+    pl = lib  # noqa: F841
+    fam = spec.family
+    nblk = 3 if fam in ("proposed", "t2and4") else (2 if fam == "t4" else 1)
+    C = spec.out_dim
+    yr = _rows(y)
+    M = yr.shape[0]
+    D = torch.empty((M, nblk * C), dtype=y.dtype, device=y.device)
+    dgamma = torch.empty(C, dtype=torch.float32, device=y.device)
+    dbeta = torch.empty(C, dtype=torch.float32, device=y.device)
+    broles = neurons.BIAS_ROLES.get(fam, ())
+    db = {r: torch.empty(C, dtype=torch.float32, device=y.device) for r in broles}
+    ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, nblk * C), dtype=torch.uint8, device=y.device)
+    dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
+    st = lib.qd_bn_backward_D(ctypes.byref(desc), dzr.data_ptr(), y.data_ptr(),
+                              cache.a.data_ptr() if cache.a is not None else None,
+                              cache.b.data_ptr() if cache.b is not None else None, gamma.data_ptr(),
+                              beta.data_ptr(), save_mean.data_ptr(), save_invstd.data_ptr(), int(relu),
+                              D.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
+                              _lib.ptr3(*[db[r].data_ptr() for r in broles]), ws.data_ptr(),
+                              torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_bn_backward_D")
+    return D, dgamma, dbeta, db
+
+
+class _QuadBNFunction(torch.autograd.Function):
+    @staticmethod
+    def forward(ctx, spec, dtype, relu, bn, x, gamma, beta, *tensors):
+        roles = tuple(param_shapes(spec).keys())
+        params = dict(zip(roles, tensors))
+        y, cache = neurons.forward(spec, params, x, dtype=dtype)
+        z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
+        ctx.spec, ctx.roles, ctx.params, ctx.cache, ctx.relu = spec, roles, params, cache, relu
+        ctx.x_dtype = x.dtype
+        ctx.save_for_backward(y, gamma, beta, sm, si)
+        return z
+
+    @staticmethod
+    def backward(ctx, dz):
+        y, gamma, beta, sm, si = ctx.saved_tensors
+        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, dz, y, gamma, beta, sm, si, ctx.relu)
+        want_dx = ctx.needs_input_grad[4]
+        grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx)
+        grads.update(db)
+        if dx is not None and dx.dtype != ctx.x_dtype:
+            dx = dx.to(ctx.x_dtype)
+        ctx.cache = None
+        return (None, None, None, None, dx, dgamma, dbeta) + tuple(grads[r] for r in ctx.roles)
+
+
+class _BNFunction(torch.autograd.Function):
+    """BN (+ReLU) alone on the same kernels (layers the fused backward does not
+    cover): the backward's D is the BN input gradient itself (one block)."""
+
+    @staticmethod
+    def forward(ctx, y, gamma, beta, bn, relu):
+        z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
+        ctx.relu = relu
+        ctx.save_for_backward(y, gamma, beta, sm, si)
+        return z
+
+    @staticmethod
+    def backward(ctx, dz):
+        y, gamma, beta, sm, si = ctx.saved_tensors
+        lib = _lib.load()
+        yr = _rows(y)
+        M, C = yr.shape
+        desc = _lib.QdDesc()
+        desc.family, desc.kind = _lib.FAMILY_CODE["first_order"], _lib.KIND_CODE["fc"]
+        desc.dtype = _dtype_code(y)
+        desc.N, desc.C, desc.H, desc.W, desc.F = M, C, 1, 1, C
+        desc.r, desc.stride, desc.pad, desc.flags = 1, 1, 0, 0
+        dy = torch.empty_like(y)
+        dgamma = torch.empty(C, dtype=torch.float32, device=y.device)
+        dbeta = torch.empty(C, dtype=torch.float32, device=y.device)
+        ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, C), dtype=torch.uint8, device=y.device)
+        dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
+        st = lib.qd_bn_backward_D(ctypes.byref(desc), dzr.data_ptr(), y.data_ptr(), None, None, gamma.data_ptr(),
+                                  beta.data_ptr(), sm.data_ptr(), si.data_ptr(), int(ctx.relu), dy.data_ptr(),
+                                  dgamma.data_ptr(), dbeta.data_ptr(), _lib.ptr3(), ws.data_ptr(),
+                                  torch.cuda.current_stream().cuda_stream)
+        _lib.raise_for(st, "qd_bn_backward_D (bn only)")
+        return dy, dgamma, dbeta, None, None
+
+
+def _ref_batchnorm(y, gamma, beta, running_mean, running_var, momentum, eps, training):
+    """tensor.py:423-470 with torch ops (autograd) -- the unfused fallback."""
+    yf = y.float()
+    axes = (0,) if y.dim() == 2 else (0, 2, 3)
+    shape = (1, -1) if y.dim() == 2 else (1, -1, 1, 1)
+    if training:
+        mean = yf.mean(dim=axes)
+        var = yf.var(dim=axes, unbiased=False)
+        with torch.no_grad():
+            running_mean.mul_(1.0 - momentum).add_(momentum * mean.detach())
+            running_var.mul_(1.0 - momentum).add_(momentum * var.detach())
+    else:
+        mean, var = running_mean, running_var
+    inv = torch.rsqrt(var + eps)
+    return (gamma.view(shape) * (yf - mean.view(shape)) * inv.view(shape) + beta.view(shape)).to(y.dtype)
+
+
+class _BNState(nn.Module):
+    def __init__(self, c, momentum=0.1, eps=1e-5, device=None):
+        super().__init__()
+        self.momentum, self.eps = momentum, eps
+        self.register_buffer("running_mean", torch.zeros(c, device=device))
+        self.register_buffer("running_var", torch.ones(c, device=device))
+
+
+class QuadConvBN(nn.Module):
+    """Quadratic conv (or fc) -> batch norm (reference semantics) -> optional ReLU."""
+
+    def __init__(self, layer: _QuadBase, relu=True, momentum=0.1, eps=1e-5):
+        super().__init__()
+        self.layer = layer
+        self.relu = relu
+        c = layer.spec.out_dim
+        dev = next(layer.parameters()).device
+        self.weight = nn.Parameter(torch.ones(c, device=dev))
+        self.bias = nn.Parameter(torch.zeros(c, device=dev))
+        self.bn = _BNState(c, momentum, eps, dev)
+
+    def fused(self):
+        sp = self.layer.spec
+        if os.environ.get("QD_NO_BNFUSE"):
+            return False
+        return (sp.stride == 1 and sp.kind in ("conv", "fc") and sp.family not in ("t3", "t1_pure", "t1_full",
+                                                                                   "t1and2"))
+
+    def forward(self, x):
+        spec = self.layer.spec
+        roles = tuple(param_shapes(spec).keys())
+        tensors = [getattr(self.layer, r) for r in roles]
+        if self.training and self.fused():
+            return _QuadBNFunction.apply(spec, self.layer.compute_dtype, self.relu, self.bn, x, self.weight,
+                                         self.bias, *tensors)
+        y = QuadFunction.apply(spec, self.layer.compute_dtype, x, *tensors)
+        if self.training and (y.dim() == 2 or y.is_contiguous(memory_format=torch.channels_last)):
+            return _BNFunction.apply(y, self.weight, self.bias, self.bn, self.relu)
+        z = _ref_batchnorm(y, self.weight, self.bias, self.bn.running_mean, self.bn.running_var, self.bn.momentum,
+                           self.bn.eps, self.training)
+        return torch.relu(z) if self.relu else z

@@ -222,6 +222,35 @@ int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void
   return check_launch("pack weights");
 }
 
+size_t qd_bn_workspace_bytes(long long M, int C, int Jd) { return bn_workspace_bytes(M, C, Jd); }
+
+int qd_bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta,
+                  float* run_mean, float* run_var, float momentum, float eps, int relu, int training, void* z,
+                  float* save_mean, float* save_invstd, void* ws, void* stream) {
+  if (M < 1 || C < 1) return set_error(QD_ERR_DIM, "batchnorm over %lld rows x %d channels", M, C);
+  if (dtype != QD_F32 && dtype != QD_BF16) return set_error(QD_ERR_CONFIG, "unknown dtype %d", dtype);
+  if (!(eps > 0.f)) return set_error(QD_ERR_CONFIG, "batchnorm eps must be positive");
+  if (!y || !gamma || !beta || !z || !save_mean || !save_invstd || (training && !ws))
+    return set_error(QD_ERR_ARG, "qd_bn_forward: NULL argument");
+  return bn_forward(M, C, dtype, y, gamma, beta, run_mean, run_var, momentum, eps, relu, training, z, save_mean,
+                    save_invstd, (char*)ws, (cudaStream_t)stream);
+}
+
+int qd_bn_backward_D(const qd_desc* d, const void* dz, const void* y, const void* a, const void* b,
+                     const float* gamma, const float* beta, const float* save_mean, const float* save_invstd,
+                     int relu, void* D, float* dgamma, float* dbeta, float* const db[3], void* ws, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  if (P.family == QD_FAM_T3 || is_t1(P.family))
+    return set_error(QD_ERR_UNSUPPORTED, "qd_bn_backward_D: t3 / T1 families recompute their operand");
+  if (caches_ab(P.family) && (!a || !b)) return set_error(QD_ERR_INTEGRITY, "cache for this family must hold a and b");
+  if (!dz || !y || !gamma || !beta || !save_mean || !save_invstd || !D || !dgamma || !dbeta || !ws)
+    return set_error(QD_ERR_ARG, "qd_bn_backward_D: NULL argument");
+  return bn_backward_D(P, dz, y, a, b, gamma, beta, save_mean, save_invstd, relu, D, dgamma, dbeta, db, (char*)ws,
+                       (cudaStream_t)stream);
+}
+
 int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const float* const grad[3],
                 float lr, float momentum, float weight_decay, int first, void* wpack, void* stream) {
   int st = validate(d);
@@ -266,13 +295,16 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* 
   if (st) return st;
   Plan P = make_plan(*d);
   if (!x || !wpack || !dy) return set_error(QD_ERR_ARG, "null tensor pointer");
-  bool cache = caches_ab(P.family);
+  const bool dgiven = (d->flags & QD_FLAG_D_GIVEN) != 0;
+  bool cache = caches_ab(P.family) && !dgiven;
   if (cache && (!a_cache || !b_cache))
     return set_error(QD_ERR_INTEGRITY, "cache for this family must hold a and b");
+  if (dgiven && (P.s != 1 || P.family == QD_FAM_T3 || is_t1(P.family) || P.kind == QD_KIND_DWCONV))
+    return set_error(QD_ERR_UNSUPPORTED, "QD_FLAG_D_GIVEN: stride-1 fc / conv layers, not t3 / T1");
   if (!(d->flags & QD_FLAG_NO_DX) && !dx) return set_error(QD_ERR_ARG, "dx is NULL");
   float* nof[3] = {nullptr, nullptr, nullptr};
   float* const* w = (dW && !(d->flags & QD_FLAG_NO_DW)) ? dW : nof;
-  float* const* b = (db && !(d->flags & QD_FLAG_NO_DW)) ? db : nof;
+  float* const* b = (db && !(d->flags & QD_FLAG_NO_DW) && !dgiven) ? db : nof;
   int path = device_path(P, d->flags);
   Workspace L = plan_workspace(P, path);
   if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");

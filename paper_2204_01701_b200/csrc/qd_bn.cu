@@ -1,0 +1,496 @@
+// Batch norm (+ ReLU) fused around the quadratic conv.
+// Reference semantics: tensor.py:423-470 (forward: biased batch variance for the
+// normalisation AND for the running-variance update, eps 1e-5, momentum 0.1)
+// and tensor.py:552-570 (backward: dx = inv/m (m dxhat - sum dxhat - xhat
+// sum dxhat xhat), dgamma = sum g xhat, dbeta = sum g).
+//
+// Forward: per-channel shifted sums (sum y-K, sum (y-K)^2, K = row 0, for a
+// stable variance) as fixed-order partials -> mean / inv_std / running stats ->
+// one normalise(+ReLU) pass.
+// Backward: one reduction pass over (dz, y) for sum g and sum g xhat (g = dz
+// masked by the recomputed ReLU), then ONE elementwise pass that applies the BN
+// backward and directly emits the quadratic layer's backward operand
+// D = [dy b | dy a | dy] (or [dy b | dy a], or dy) plus the layer's bias
+// partial sums -- the BN-backward output dy is never written to memory.
+// NHWC [M][C] tensors; fp32 arithmetic for both dtypes.
+#include <stdio.h>
+#include "qd_kernels.h"
+
+namespace qd {
+
+// row blocks: ~16K elements each (enough blocks for small-M / large-C layers too)
+static int bn_splits(long long M, int C) {
+  long long S = (M * C + 16383) / 16384;
+  if (S > 592) S = 592;
+  if (S > M) S = M;
+  return (int)(S < 1 ? 1 : S);
+}
+// 8-channel vector kernels when C % 8 == 0 and C / 8 <= 256
+static bool bn_vec(int C) { return C % 8 == 0 && C / 8 <= 256; }
+
+template <typename T> struct BV;
+template <> struct BV<bf16> {
+  __device__ static void ld8(const bf16* p, float v[8]) {
+    uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      float2 f = __bfloat1622float2(h[e]);
+      v[2 * e] = f.x;
+      v[2 * e + 1] = f.y;
+    }
+  }
+  __device__ static void st8(bf16* p, const float v[8]) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <> struct BV<float> {
+  __device__ static void ld8(const float* p, float v[8]) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ static void st8(float* p, const float v[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+// vector reduction: thread = (8-channel chunk q, row lane); rows [r0, r1) of block s;
+// lane partials folded in a fixed order through shared memory
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) bn_reduce_vec_kernel(long long M, int C, const T* __restrict__ y,
+                                                            const T* __restrict__ dz, const float* mean,
+                                                            const float* invstd, const float* gamma,
+                                                            const float* beta, int relu, float* part) {
+  __shared__ float red[2][256 * 8];
+  const int CQ = C / 8, lanes = 256 / CQ;
+  const int q = threadIdx.x % CQ, lane = threadIdx.x / CQ, c0 = q * 8;
+  const int S = gridDim.x, s = blockIdx.x;
+  const long long rows = (M + S - 1) / S;
+  const long long r0 = (long long)s * rows;
+  long long r1 = r0 + rows;
+  if (r1 > M) r1 = M;
+  float a0[8], a1[8], K[8], mu[8], is[8], ga[8], be[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) a0[e] = a1[e] = 0.f;
+  if (lane < lanes) {
+    if (MODE == 0) {
+      BV<T>::ld8(y + c0, K);
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        mu[e] = mean[c0 + e]; is[e] = invstd[c0 + e]; ga[e] = gamma[c0 + e]; be[e] = beta[c0 + e];
+      }
+    }
+#pragma unroll 4
+    for (long long r = r0 + lane; r < r1; r += lanes) {
+      float v[8];
+      BV<T>::ld8(y + (size_t)r * C + c0, v);
+      if (MODE == 0) {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float d = v[e] - K[e];
+          a0[e] += d;
+          a1[e] = fmaf(d, d, a1[e]);
+        }
+      } else {
+        float g[8];
+        BV<T>::ld8(dz + (size_t)r * C + c0, g);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          const float xh = (v[e] - mu[e]) * is[e];
+          const float gg = (relu && !(fmaf(ga[e], xh, be[e]) > 0.f)) ? 0.f : g[e];
+          a0[e] += gg;
+          a1[e] = fmaf(gg, xh, a1[e]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[0][threadIdx.x * 8 + e] = a0[e];
+    red[1][threadIdx.x * 8 + e] = a1[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int qq = c / 8, e = c % 8;
+    float t0 = 0.f, t1 = 0.f;
+    for (int l = 0; l < lanes; ++l) {
+      t0 += red[0][(l * CQ + qq) * 8 + e];
+      t1 += red[1][(l * CQ + qq) * 8 + e];
+    }
+    part[((size_t)s * 2 + 0) * C + c] = t0;
+    part[((size_t)s * 2 + 1) * C + c] = t1;
+  }
+}
+
+template <typename T>
+__global__ void bn_apply_vec_kernel(long long rows, int C, const T* y, const float* mean, const float* invstd,
+                                    const float* gamma, const float* beta, int relu, T* z) {
+  const int CQ = C / 8;
+  const long long n = rows * CQ;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c0 = (int)(i % CQ) * 8;
+    float v[8];
+    BV<T>::ld8(y + i * 8, v);
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      float t = fmaf(gamma[c0 + e], (v[e] - mean[c0 + e]) * invstd[c0 + e], beta[c0 + e]);
+      v[e] = (relu && t < 0.f) ? 0.f : t;
+    }
+    BV<T>::st8(z + i * 8, v);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) bn_emit_D_vec_kernel(Plan P, const T* __restrict__ dz,
+                                                            const T* __restrict__ y, const T* __restrict__ a,
+                                                            const T* __restrict__ b, const float* mean,
+                                                            const float* invstd, const float* gamma,
+                                                            const float* beta, const float* dgamma,
+                                                            const float* dbeta, int relu, T* D, float* bpart) {
+  __shared__ float red[3][256 * 8];
+  const long long M = P.Mout;
+  const int C = P.F, CQ = C / 8, lanes = 256 / CQ;
+  const int q = threadIdx.x % CQ, lane = threadIdx.x / CQ, c0 = q * 8;
+  const int S = gridDim.x, s = blockIdx.x;
+  const long long rows = (M + S - 1) / S;
+  const long long r0 = (long long)s * rows;
+  long long r1 = r0 + rows;
+  if (r1 > M) r1 = M;
+  const bool mat = caches_ab(P.family), hasg = d_has_g(P.family);
+  float s0[8], s1[8], s2[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) s0[e] = s1[e] = s2[e] = 0.f;
+  if (lane < lanes) {
+    float mu[8], is[8], ga[8], be[8], dg[8], db[8], k[8];
+    const float fm = (float)M, inv_m = 1.f / fm;
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      mu[e] = mean[c0 + e]; is[e] = invstd[c0 + e]; ga[e] = gamma[c0 + e]; be[e] = beta[c0 + e];
+      dg[e] = dgamma[c0 + e]; db[e] = dbeta[c0 + e]; k[e] = ga[e] * is[e] * inv_m;
+    }
+#pragma unroll 4
+    for (long long r = r0 + lane; r < r1; r += lanes) {
+      const size_t i = (size_t)r * C + c0;
+      float v[8], g[8], dyv[8];
+      BV<T>::ld8(y + i, v);
+      BV<T>::ld8(dz + i, g);
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float xh = (v[e] - mu[e]) * is[e];
+        const float gg = (relu && !(fmaf(ga[e], xh, be[e]) > 0.f)) ? 0.f : g[e];
+        dyv[e] = k[e] * (fm * gg - db[e] - xh * dg[e]);
+      }
+      T* drow = D + (size_t)r * P.Jd + c0;
+      if (mat) {
+        float av[8], bv[8], d0[8], d1[8];
+        BV<T>::ld8(a + i, av);
+        BV<T>::ld8(b + i, bv);
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+          d0[e] = dyv[e] * bv[e];
+          d1[e] = dyv[e] * av[e];
+          s0[e] += d0[e];
+          s1[e] += d1[e];
+          s2[e] += dyv[e];
+        }
+        BV<T>::st8(drow, d0);
+        BV<T>::st8(drow + C, d1);
+        if (hasg) BV<T>::st8(drow + 2 * C, dyv);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 8; ++e) s0[e] += dyv[e];
+        BV<T>::st8(drow, dyv);
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    red[0][threadIdx.x * 8 + e] = s0[e];
+    red[1][threadIdx.x * 8 + e] = s1[e];
+    red[2][threadIdx.x * 8 + e] = s2[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int qq = c / 8, e = c % 8;
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+    for (int l = 0; l < lanes; ++l) {
+      t0 += red[0][(l * CQ + qq) * 8 + e];
+      t1 += red[1][(l * CQ + qq) * 8 + e];
+      t2 += red[2][(l * CQ + qq) * 8 + e];
+    }
+    float* o = bpart + (size_t)s * P.Jd;
+    if (mat) {
+      o[c] = t0;
+      o[C + c] = t1;
+      if (hasg) o[2 * C + c] = t2;
+    } else {
+      o[c] = t0;
+    }
+  }
+}
+
+size_t bn_workspace_bytes(long long M, int C, int Jd) {
+  const int S = bn_splits(M, C);
+  return (size_t)S * 2 * C * 4 + (size_t)S * Jd * 4 + 256;
+}
+
+// per-block partials over rows [r0, r1): thread = (channel c = tid % C? no: strided)
+// Scalar channel loop per thread keeps it general (any C); rows are split over
+// the block's thread groups and folded in a fixed order through shared memory.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256) bn_reduce_kernel(long long M, int C, const T* __restrict__ y,
+                                                        const T* __restrict__ dz, const float* mean,
+                                                        const float* invstd, const float* gamma,
+                                                        const float* beta, int relu, float* part) {
+  // MODE 0: sum(y - K), sum((y - K)^2) with K = y[0][c]
+  // MODE 1: sum(g), sum(g xhat), g = dz * [relu ? z > 0 : 1]
+  __shared__ float red[2][256];
+  const int S = gridDim.x, s = blockIdx.x;
+  const long long rows = (M + S - 1) / S;
+  const long long r0 = (long long)s * rows;
+  long long r1 = r0 + rows;
+  if (r1 > M) r1 = M;
+  const int G = blockDim.x < C ? 1 : blockDim.x / C;  // row groups
+  const int cpt = blockDim.x < C ? 1 : 0;
+  for (int c0 = 0; c0 < C; c0 += (cpt ? blockDim.x : C)) {
+    int c = c0 + (cpt ? (int)threadIdx.x : (int)threadIdx.x % C);
+    const int grp = cpt ? 0 : (int)threadIdx.x / C;
+    float a0 = 0.f, a1 = 0.f;
+    const bool act = c < C && grp < G;
+    if (act) {
+      if (MODE == 0) {
+        const float K = ld(y + c);
+        for (long long r = r0 + grp; r < r1; r += G) {
+          const float v = ld(y + (size_t)r * C + c) - K;
+          a0 += v;
+          a1 = fmaf(v, v, a1);
+        }
+      } else {
+        const float mu = mean[c], is = invstd[c], ga = gamma[c], be = beta[c];
+        for (long long r = r0 + grp; r < r1; r += G) {
+          const size_t i = (size_t)r * C + c;
+          const float xh = (ld(y + i) - mu) * is;
+          float g = ld(dz + i);
+          if (relu && !(fmaf(ga, xh, be) > 0.f)) g = 0.f;
+          a0 += g;
+          a1 = fmaf(g, xh, a1);
+        }
+      }
+    }
+    red[0][threadIdx.x] = a0;
+    red[1][threadIdx.x] = a1;
+    __syncthreads();
+    if (act && grp == 0) {
+      float t0 = 0.f, t1 = 0.f;
+      for (int gq = 0; gq < G; ++gq) {
+        t0 += red[0][gq * C + (c - c0)];
+        t1 += red[1][gq * C + (c - c0)];
+      }
+      part[((size_t)s * 2 + 0) * C + c] = t0;
+      part[((size_t)s * 2 + 1) * C + c] = t1;
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+__global__ void bn_stats_finalize(long long M, int C, int S, const T* y, const float* part, float eps,
+                                  float momentum, int training, float* run_mean, float* run_var, float* save_mean,
+                                  float* save_invstd) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s1 = 0.f, s2 = 0.f;
+  for (int s = 0; s < S; ++s) {
+    s1 += part[((size_t)s * 2 + 0) * C + c];
+    s2 += part[((size_t)s * 2 + 1) * C + c];
+  }
+  const float inv_m = 1.f / (float)M;
+  const float dm = s1 * inv_m;
+  float var = s2 * inv_m - dm * dm;  // biased (tensor.py:444)
+  if (var < 0.f) var = 0.f;
+  const float mean = ld(y + c) + dm;
+  save_mean[c] = mean;
+  save_invstd[c] = rsqrtf(var + eps);
+  if (training && run_mean) {  // tensor.py:445-450 (biased var in the running update too)
+    run_mean[c] = run_mean[c] * (1.f - momentum) + momentum * mean;
+    run_var[c] = run_var[c] * (1.f - momentum) + momentum * var;
+  }
+}
+
+template <typename T>
+__global__ void bn_apply_kernel(long long n, int C, const T* y, const float* mean, const float* invstd,
+                                const float* gamma, const float* beta, int relu, T* z) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int c = (int)(i % C);
+    float v = fmaf(gamma[c], (ld(y + i) - mean[c]) * invstd[c], beta[c]);
+    if (relu && v < 0.f) v = 0.f;
+    z[i] = cvt<T>(v);
+  }
+}
+
+__global__ void bn_grad_finalize(int C, int S, const float* part, float* dgamma, float* dbeta) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= C) return;
+  float s1 = 0.f, s2 = 0.f;
+  for (int s = 0; s < S; ++s) {
+    s1 += part[((size_t)s * 2 + 0) * C + c];
+    s2 += part[((size_t)s * 2 + 1) * C + c];
+  }
+  dbeta[c] = s1;
+  dgamma[c] = s2;
+}
+
+// dy = gamma inv / m (m g - dbeta - xhat dgamma) (tensor.py:558-566 with s1 = gamma dbeta,
+// s2 = gamma dgamma), then D and the layer's bias partials; block s covers rows [r0, r1)
+template <typename T>
+__global__ void __launch_bounds__(256) bn_emit_D_kernel(Plan P, const T* __restrict__ dz, const T* __restrict__ y,
+                                                        const T* __restrict__ a, const T* __restrict__ b,
+                                                        const float* mean, const float* invstd, const float* gamma,
+                                                        const float* beta, const float* dgamma, const float* dbeta,
+                                                        int relu, T* D, float* bpart) {
+  __shared__ float red[3][256];
+  const long long M = P.Mout;
+  const int C = P.F, S = gridDim.x, s = blockIdx.x;
+  const long long rows = (M + S - 1) / S;
+  const long long r0 = (long long)s * rows;
+  long long r1 = r0 + rows;
+  if (r1 > M) r1 = M;
+  const bool mat = caches_ab(P.family), hasg = d_has_g(P.family);
+  const int G = blockDim.x < C ? 1 : blockDim.x / C;
+  const int cpt = blockDim.x < C ? 1 : 0;
+  const float inv_m = 1.f / (float)M;
+  for (int c0 = 0; c0 < C; c0 += (cpt ? blockDim.x : C)) {
+    int c = c0 + (cpt ? (int)threadIdx.x : (int)threadIdx.x % C);
+    const int grp = cpt ? 0 : (int)threadIdx.x / C;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f;
+    const bool act = c < C && grp < G;
+    if (act) {
+      const float mu = mean[c], is = invstd[c], ga = gamma[c], be = beta[c], dg = dgamma[c], db = dbeta[c];
+      const float k = ga * is * inv_m;
+      for (long long r = r0 + grp; r < r1; r += G) {
+        const size_t i = (size_t)r * C + c;
+        const float xh = (ld(y + i) - mu) * is;
+        float g = ld(dz + i);
+        if (relu && !(fmaf(ga, xh, be) > 0.f)) g = 0.f;
+        const float dyv = k * ((float)M * g - db - xh * dg);
+        T* drow = D + (size_t)r * P.Jd;
+        if (mat) {
+          const float d0 = dyv * ld(b + i), d1 = dyv * ld(a + i);
+          drow[c] = cvt<T>(d0);
+          drow[C + c] = cvt<T>(d1);
+          if (hasg) drow[2 * C + c] = cvt<T>(dyv);
+          s0 += d0;
+          s1 += d1;
+          s2 += dyv;
+        } else {
+          drow[c] = cvt<T>(dyv);
+          s0 += dyv;
+        }
+      }
+    }
+    red[0][threadIdx.x] = s0;
+    red[1][threadIdx.x] = s1;
+    red[2][threadIdx.x] = s2;
+    __syncthreads();
+    if (act && grp == 0) {
+      float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+      for (int gq = 0; gq < G; ++gq) {
+        t0 += red[0][gq * C + (c - c0)];
+        t1 += red[1][gq * C + (c - c0)];
+        t2 += red[2][gq * C + (c - c0)];
+      }
+      float* o = bpart + (size_t)s * P.Jd;
+      if (mat) {
+        o[c] = t0;
+        o[C + c] = t1;
+        if (hasg) o[2 * C + c] = t2;
+      } else {
+        o[c] = t0;
+      }
+    }
+    __syncthreads();
+  }
+}
+
+template <typename T>
+static int bn_forward_t(long long M, int C, const T* y, const float* gamma, const float* beta, float* rm, float* rv,
+                        float momentum, float eps, int relu, int training, T* z, float* sm, float* si, char* ws,
+                        cudaStream_t st) {
+  const int S = bn_splits(M, C);
+  float* part = (float*)ws;
+  if (training) {
+    if (bn_vec(C))
+      bn_reduce_vec_kernel<T, 0><<<S, 256, 0, st>>>(M, C, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, part);
+    else
+      bn_reduce_kernel<T, 0><<<S, 256, 0, st>>>(M, C, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, part);
+    count_launch(st, "bn_stats");
+    bn_stats_finalize<T><<<(C + 127) / 128, 128, 0, st>>>(M, C, S, y, part, eps, momentum, 1, rm, rv, sm, si);
+    count_launch(st, "bn_stats_finalize");
+  }
+  const long long n = M * C;
+  long long g = ((bn_vec(C) ? n / 8 : n) + 255) / 256;
+  if (g > 148 * 16) g = 148 * 16;
+  if (bn_vec(C))
+    bn_apply_vec_kernel<T><<<(int)g, 256, 0, st>>>(M, C, y, sm, si, gamma, beta, relu, z);
+  else
+    bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z);
+  count_launch(st, "bn_apply");
+  return check_launch("bn forward");
+}
+
+template <typename T>
+static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, const T* b, const float* gamma,
+                           const float* beta, const float* sm, const float* si, int relu, T* D, float* dgamma,
+                           float* dbeta, float* const db[3], char* ws, cudaStream_t st) {
+  const long long M = P.Mout;
+  const int C = P.F, S = bn_splits(M, C);
+  float* part = (float*)ws;
+  float* bpart = part + (size_t)S * 2 * C;
+  if (bn_vec(C))
+    bn_reduce_vec_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
+  else
+    bn_reduce_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
+  count_launch(st, "bn_bwd_reduce");
+  bn_grad_finalize<<<(C + 127) / 128, 128, 0, st>>>(C, S, part, dgamma, dbeta);
+  count_launch(st, "bn_bwd_finalize");
+  if (bn_vec(C))
+    bn_emit_D_vec_kernel<T><<<S, 256, 0, st>>>(P, dz, y, a, b, sm, si, gamma, beta, dgamma, dbeta, relu, D, bpart);
+  else
+    bn_emit_D_kernel<T><<<S, 256, 0, st>>>(P, dz, y, a, b, sm, si, gamma, beta, dgamma, dbeta, relu, D, bpart);
+  count_launch(st, "bn_emit_D");
+  if (db && db[0] && P.nbias) launch_bias_finish(P, bpart, S, db, st);
+  return check_launch("bn backward");
+}
+
+int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta, float* rm,
+               float* rv, float momentum, float eps, int relu, int training, void* z, float* sm, float* si, char* ws,
+               cudaStream_t st) {
+  if (dtype == QD_BF16)
+    return bn_forward_t<bf16>(M, C, (const bf16*)y, gamma, beta, rm, rv, momentum, eps, relu, training, (bf16*)z, sm,
+                              si, ws, st);
+  return bn_forward_t<float>(M, C, (const float*)y, gamma, beta, rm, rv, momentum, eps, relu, training, (float*)z,
+                             sm, si, ws, st);
+}
+
+int bn_backward_D(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,
+                  const float* beta, const float* sm, const float* si, int relu, void* D, float* dgamma,
+                  float* dbeta, float* const db[3], char* ws, cudaStream_t st) {
+  if (P.dtype == QD_BF16)
+    return bn_backward_D_t<bf16>(P, (const bf16*)dz, (const bf16*)y, (const bf16*)a, (const bf16*)b, gamma, beta, sm,
+                                 si, relu, (bf16*)D, dgamma, dbeta, db, ws, st);
+  return bn_backward_D_t<float>(P, (const float*)dz, (const float*)y, (const float*)a, (const float*)b, gamma, beta,
+                                sm, si, relu, (float*)D, dgamma, dbeta, db, ws, st);
+}
+
+}  // namespace qd

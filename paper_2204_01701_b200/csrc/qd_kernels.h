@@ -103,6 +103,15 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
                      float momentum, float wd, int first, void* wpack, cudaStream_t st);
 
+// ---- BN (+ReLU) around the quadratic conv (qd_bn.cu) ------------------------
+size_t bn_workspace_bytes(long long M, int C, int Jd);
+int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta, float* rm,
+               float* rv, float momentum, float eps, int relu, int training, void* z, float* sm, float* si, char* ws,
+               cudaStream_t st);
+int bn_backward_D(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,
+                  const float* beta, const float* sm, const float* si, int relu, void* D, float* dgamma,
+                  float* dbeta, float* const db[3], char* ws, cudaStream_t st);
+
 // ---- T1 families (qd_t1.cu): fc, one output, CUDA-core path ----------------
 bool is_t1(int family);
 size_t t1_pack_bytes(const Plan& P);

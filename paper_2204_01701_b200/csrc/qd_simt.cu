@@ -570,8 +570,10 @@ static int simt_backward_t(const Plan& P, const T* x, const T* wpack, const T* a
   const T* wd = wpack + pack_fprop_elems(P);
   float* bpart = (float*)(ws + L.off_BS);
   const T* D = dy;
-  if (caches_ab(P.family)) D = (const T*)(ws + L.off_D);
-  if (P.family == QD_FAM_T3) {
+  if (caches_ab(P.family) && !(P.flags & QD_FLAG_D_GIVEN)) D = (const T*)(ws + L.off_D);
+  if (P.flags & QD_FLAG_D_GIVEN) {
+    // `dy` is the operand D already (qd_bn_backward_D formed it and the bias grads)
+  } else if (P.family == QD_FAM_T3) {
     // recompute a = Wa x (fp32, the forward GEMM) and form D = 2 g a
     float* G = (float*)(ws + L.off_P);
     FpropA<T> la{x, P.H, P.W, P.C, P.OH, P.OW, P.r, P.s, P.p, P.K0, P.sq};

@@ -958,14 +958,17 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   // and the consumers read its third block (g itself) straight from dy
   const bool w3 = !(P.flags & QD_FLAG_TC_V1) && wgrad3_split(P) == L.wg_split;
   const bool w2 = !w3 && !(P.flags & QD_FLAG_TC_V1) && wgrad2_split(P) == L.wg_split;
-  bool d2 = P.family == QD_FAM_PROPOSED && !up && dW[0] && (w2 || w3) && !getenv("QD_NO_D2");
+  const bool dgiven = (P.flags & QD_FLAG_D_GIVEN) != 0;  // `dy` is D already (qd_bn_backward_D)
+  bool d2 = P.family == QD_FAM_PROPOSED && !up && dW[0] && (w2 || w3) && !dgiven && !getenv("QD_NO_D2");
   if (d2 && dx) {
     GemmCfg c = dgrad_cfg(P);
     d2 = conv2_fits(P.N, P.Jd, P.OW, P.OH, P.W, P.H, P.r - 1 - P.p, P.r, 0, c.nbk, c.nout, c.tiles_nn, P.C, 0);
   }
   const int dsplit = d2 ? 2 * P.F / 64 : 0;
   bool wg_pdl = false;  // a PDL-launched v2/v3 wgrad immediately precedes the dgrad on `st`
-  if (P.family == QD_FAM_T3) {
+  if (dgiven) {
+    D = (const bf16*)dy;
+  } else if (P.family == QD_FAM_T3) {
     // a = Wa x is recomputed into the D buffer, then D = 2 dy a in place
     // (on the stride-1 grid for stride 2 the prologue below upsamples it)
     bf16* Dw = (bf16*)(ws + L.off_D);

@@ -272,6 +272,38 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True):
     return grads, dx
 
 
+def backward_from_D(spec, params, cache, D, *, want_dx=True, want_dw=True):
+    """Layer backward from a precomputed operand D ([M, Jd] rows, e.g. from the
+    fused BN backward ``bn.bn_backward_D``); weight gradients and dx only (the
+    bias gradients come with D). Stride-1 fc / conv layers."""
+    lib = _lib.load()
+    x = cache.x
+    cdt = x.dtype
+    flags = (cache.desc.flags if cache.desc is not None else 0) | _lib.FLAG_D_GIVEN
+    if not want_dx:
+        flags |= _lib.FLAG_NO_DX
+    if not want_dw:
+        flags |= _lib.FLAG_NO_DW
+    desc = make_desc(spec, x.shape, cdt, flags)
+    P = _weights(spec, params)
+    roles = WEIGHT_ROLES[spec.family]
+    if cache.wpack is not None and cache.pack_key == _pack_key([P[r] for r in roles]):
+        wpack = cache.wpack
+    else:
+        wpack = _pack(spec, desc, params)[0]
+    dev = x.device
+    shapes = param_shapes(spec)
+    grads = {role: torch.empty(shapes[role], dtype=torch.float32, device=dev) for role in roles}
+    dx = torch.empty_like(x) if want_dx else None
+    ws = _workspace(desc, dev)
+    st = lib.qd_backward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(), None, None, D.data_ptr(),
+                         dx.data_ptr() if dx is not None else None,
+                         _lib.ptr3(*[grads[r].data_ptr() for r in roles]), _lib.ptr3(), ws.data_ptr(),
+                         torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_backward (D given)")
+    return grads, dx
+
+
 def device_path(spec, x_shape, dtype=torch.bfloat16, flags=0):
     """0 = generic CUDA-core kernels, 1 = tcgen05/TMA kernels."""
     desc = make_desc(spec, x_shape, dtype, flags)

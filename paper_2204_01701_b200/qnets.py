@@ -26,6 +26,7 @@ import torch
 import torch.nn.functional as Fnn
 from torch import nn
 
+from .bn import QuadConvBN
 from .nn import QuadConv2d
 
 
@@ -74,8 +75,11 @@ class QuadraVGG16(nn.Module):
         for v in VGG16_CFG:
             if v == "M":
                 layers.append(nn.MaxPool2d(2, 2))
-            else:
+            elif cin % 64:  # zero-padded stem: quad conv, then torch BN + ReLU
                 layers += [quad_conv(cin, v, 3, 1, 1, family), nn.BatchNorm2d(v), nn.ReLU(inplace=True)]
+                cin = v
+            else:  # quad conv -> BN -> ReLU as one fused node (bn.QuadConvBN)
+                layers.append(QuadConvBN(QuadConv2d(cin, v, 3, 1, 1, family), relu=True))
                 cin = v
         self.features = nn.Sequential(*layers)
         self.classifier = nn.Linear(512, num_classes)
@@ -90,10 +94,9 @@ class QuadBasicBlock(nn.Module):
 
     def __init__(self, inplanes, planes, stride=1, family="proposed"):
         super().__init__()
-        self.conv1 = quad_conv(inplanes, planes, 3, stride, 1, family)
-        self.bn1 = nn.BatchNorm2d(planes)
-        self.conv2 = quad_conv(planes, planes, 3, 1, 1, family)
-        self.bn2 = nn.BatchNorm2d(planes)
+        # conv -> BN (-> ReLU) fused (bn.QuadConvBN; stride 2 runs its unfused form)
+        self.cbr1 = QuadConvBN(quad_conv(inplanes, planes, 3, stride, 1, family), relu=True)
+        self.cb2 = QuadConvBN(quad_conv(planes, planes, 3, 1, 1, family), relu=False)
         self.relu = nn.ReLU(inplace=True)
         self.down = None
         if stride != 1 or inplanes != planes:
@@ -102,8 +105,7 @@ class QuadBasicBlock(nn.Module):
 
     def forward(self, x):
         idt = x if self.down is None else self.down(x)
-        out = self.relu(self.bn1(self.conv1(x)))
-        out = self.bn2(self.conv2(out))
+        out = self.cb2(self.cbr1(x))
         return self.relu(out + idt)
 
 

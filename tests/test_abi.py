@@ -15,7 +15,7 @@ HEADER = os.path.join(ROOT, "include", "quadra_b200.h")
 
 def declared_symbols():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"\b(qd_[a-z_]+)\s*\(", text)))
+    return sorted(set(re.findall(r"\b(qd_[A-Za-z0-9_]+)\s*\(", text)))
 
 
 def test_header_matches_binding_list():

@@ -343,3 +343,94 @@ def test_quad_sgd_matches_torch_sgd_and_repack(family, kind, c, f, k):
     fresh = neurons._pack(spec, desc, {r: getattr(m1, r).detach().clone() for r in neurons.param_shapes(spec)})[0]
     torch.cuda.synchronize()
     assert torch.equal(reg, fresh)
+
+
+# BN (+ReLU) fused around the quadratic conv
+@pytest.mark.gpu
+@pytest.mark.parametrize("family,kind,relu", [("proposed", "conv", True), ("proposed", "conv", False),
+                                               ("t4", "conv", True), ("first_order", "conv", True),
+                                               ("t2_linear", "conv", True), ("t2and4", "conv", True),
+                                               ("proposed", "fc", True)])
+def test_quadconvbn_fused_matches_reference_bn(family, kind, relu):
+    from paper_2204_01701_b200.bn import QuadConvBN, _ref_batchnorm
+    from paper_2204_01701_b200.nn import QuadConv2d, QuadFunction, QuadLinear
+    from paper_2204_01701_b200.spec import param_shapes
+    torch.manual_seed(3)
+    c, f = 64, 64
+    layer = QuadConv2d(c, f, 3, 1, 1, family=family, device="cuda") if kind == "conv" else \
+        QuadLinear(c, f, family=family, device="cuda")
+    mod = QuadConvBN(layer, relu=relu)
+    with torch.no_grad():
+        mod.weight.uniform_(0.5, 1.5)
+        mod.bias.uniform_(-0.2, 0.2)
+        for r in param_shapes(layer.spec):
+            if r.startswith("b"):
+                getattr(layer, r).uniform_(-0.1, 0.1)
+    assert mod.fused()
+    shape = (8, c, 12, 12) if kind == "conv" else (96, c)
+    x0 = torch.randn(shape, device="cuda").to(torch.bfloat16)
+    if kind == "conv":
+        x0 = x0.contiguous(memory_format=torch.channels_last)
+    gz = torch.randn((8, f, 12, 12) if kind == "conv" else (96, f), device="cuda").to(torch.bfloat16)
+    rm0, rv0 = mod.bn.running_mean.clone(), mod.bn.running_var.clone()
+    # fused
+    x1 = x0.clone().requires_grad_(True)
+    z1 = mod(x1)
+    z1.backward(gz)
+    g1 = {n: p.grad.clone() for n, p in mod.named_parameters()}
+    rm1, rv1 = mod.bn.running_mean.clone(), mod.bn.running_var.clone()
+    for p in mod.parameters():
+        p.grad = None
+    # reference composition: same layer kernels, reference BN with torch autograd
+    x2 = x0.clone().requires_grad_(True)
+    roles = tuple(param_shapes(layer.spec).keys())
+    y = QuadFunction.apply(layer.spec, torch.bfloat16, x2, *[getattr(layer, r) for r in roles])
+    rm2, rv2 = rm0.clone(), rv0.clone()
+    z2 = _ref_batchnorm(y, mod.weight, mod.bias, rm2, rv2, 0.1, 1e-5, True)
+    if relu:
+        z2 = torch.relu(z2)
+    z2.backward(gz)
+    g2 = {n: p.grad.clone() for n, p in mod.named_parameters()}
+    rel = lambda a, b: Q.rel_err(a.detach().double().cpu().numpy(), b.detach().double().cpu().numpy())  # noqa
+    assert rel(z1, z2) <= 2e-2, rel(z1, z2)
+    assert rel(x1.grad, x2.grad) <= 3e-2, rel(x1.grad, x2.grad)
+    for n in g1:
+        if n in ("layer.bc", "layer.b"):
+            # a bias added right before BN has an exactly zero gradient (BN removes the
+            # mean): the unfused path only sums bf16 rounding noise; the fused one (fp32 dy)
+            # must cancel to round-off relative to the layer's other gradients
+            other = max(float(g.abs().max()) for k, g in g1.items() if k.startswith("layer.W"))
+            assert float(g1[n].abs().max()) <= 1e-3 * other, (n, float(g1[n].abs().max()), other)
+            continue
+        assert rel(g1[n], g2[n]) <= 3e-2, (n, rel(g1[n], g2[n]))
+    assert torch.allclose(rm1, rm2, rtol=1e-3, atol=1e-4) and torch.allclose(rv1, rv2, rtol=1e-3, atol=1e-4)
+
+
+@pytest.mark.gpu
+def test_quadconvbn_stride2_bn_only_path():
+    """stride 2: the layer backward runs unfused; BN(+ReLU) still on the BN kernels"""
+    from paper_2204_01701_b200.bn import QuadConvBN, _ref_batchnorm
+    from paper_2204_01701_b200.nn import QuadConv2d, QuadFunction
+    torch.manual_seed(4)
+    layer = QuadConv2d(64, 128, 3, 2, 1, device="cuda")
+    mod = QuadConvBN(layer, relu=True)
+    assert not mod.fused()
+    x0 = torch.randn(4, 64, 16, 16, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    gz = torch.randn(4, 128, 8, 8, device="cuda").bfloat16()
+    x1 = x0.clone().requires_grad_(True)
+    mod(x1).backward(gz)
+    g1 = {n: p.grad.clone() for n, p in mod.named_parameters()}
+    for p in mod.parameters():
+        p.grad = None
+    x2 = x0.clone().requires_grad_(True)
+    y = QuadFunction.apply(layer.spec, torch.bfloat16, x2, *[getattr(layer, r) for r in ("Wa", "Wb", "Wc", "ba", "bb",
+                                                                                           "bc")])
+    z = torch.relu(_ref_batchnorm(y, mod.weight, mod.bias, torch.zeros(128, device="cuda"),
+                                  torch.ones(128, device="cuda"), 0.1, 1e-5, True))
+    z.backward(gz)
+    rel = lambda a, b: Q.rel_err(a.detach().double().cpu().numpy(), b.detach().double().cpu().numpy())  # noqa
+    assert rel(x1.grad, x2.grad) <= 3e-2
+    for n, p in mod.named_parameters():
+        if n in ("layer.bc",):
+            continue
+        assert rel(g1[n], p.grad) <= 3e-2, n

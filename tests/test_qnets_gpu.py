@@ -49,8 +49,12 @@ def test_quad_layers_use_tcgen05():
     from paper_2204_01701_b200 import neurons, qnets
     from paper_2204_01701_b200.nn import QuadConv2d
     m = qnets.QuadraResNet18(10).cuda().to(memory_format=torch.channels_last)
+    from paper_2204_01701_b200.bn import QuadConvBN
     seen = []
     hooks = [q.register_forward_pre_hook(lambda mod, inp: seen.append(
+        neurons.device_path(mod.layer.spec, tuple(inp[0].shape)))) for q in m.modules()
+        if isinstance(q, QuadConvBN)]
+    hooks += [q.register_forward_pre_hook(lambda mod, inp: seen.append(
         neurons.device_path(mod.spec, tuple(inp[0].shape)))) for q in m.modules() if isinstance(q, QuadConv2d)]
     x = torch.randn(2, 3, 224, 224, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
     with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
