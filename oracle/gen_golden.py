@@ -224,6 +224,40 @@ def gen_known_answers(neurons, tensor, Spec):
     return {"scalar_params": P, "x": 2.0, "y": float(y.data[0, 0]), "dx": float(dx[0, 0])}
 
 
+CKPT_CONFIG = """model tiny
+layer conv family=proposed in=3 out=8 k=3 s=1 p=1 bn=1 act=relu
+layer conv family=t4 in=8 out=8 k=3 s=2 p=1 bn=1 act=relu
+layer dwconv family=proposed in=8 out=8 k=3 s=1 p=1 bn=0 act=relu
+layer fc family=t2 in=2048 out=16 k=1 s=1 p=0 bn=1 act=relu
+head fc in=16 classes=10
+train epochs=1 batch=4 lr=0.1 seed=7 dataset=cifar10
+"""
+
+
+def gen_checkpoint():
+    """A reference-written checkpoint (model.py:236-263) of a small chain model with
+    batch norm, stride 2, dwconv and an fc after an implicit flatten, plus the
+    reference's eval-mode logits on a fixed input -> tests/golden/ckpt_tiny*."""
+    from quadra import autobuild, model as M  # noqa: E402
+    from quadra import tensor as T  # noqa: E402
+    cfg = autobuild.parse_config(CKPT_CONFIG)
+    mdl = M.Model(cfg)
+    rng = np.random.default_rng(99)
+    for layer in mdl.layers:
+        if layer.bn is not None:
+            c = layer.bn.running_mean.shape[0]
+            layer.bn.running_mean[:] = rng.normal(size=c) * 0.1
+            layer.bn.running_var[:] = rng.uniform(0.5, 1.5, size=c)
+            layer.bn.gamma = T.Tensor._wrap(rng.uniform(0.5, 1.5, size=c), is_param=True)
+            layer.bn.beta = T.Tensor._wrap(rng.normal(size=c) * 0.1, is_param=True)
+    path = os.path.join(OUT, "ckpt_tiny")
+    M.save_checkpoint(mdl, path)
+    x = rng.normal(size=(4, 3, 32, 32))
+    logits = mdl.forward(T.Tensor._wrap(x), tape=None, train=False).data
+    np.savez_compressed(os.path.join(OUT, "ckpt_tiny_io.npz"), x=x, logits=logits,
+                        serialized=np.array(autobuild.serialize_config(cfg)))
+
+
 def main():
     os.makedirs(OUT, exist_ok=True)
     neurons, tensor, Spec, errors = _import_reference()
@@ -232,6 +266,7 @@ def main():
         json.dump(spec_g, fh, separators=(",", ":"))
     files = gen_layer_golden(neurons, tensor, Spec)
     known = gen_known_answers(neurons, tensor, Spec)
+    gen_checkpoint()
     with open(os.path.join(OUT, "index.json"), "w") as fh:
         json.dump({"generated_from": REF_SRC, "layers": files, "known_answers": known},
                   fh, indent=1)
