@@ -434,3 +434,31 @@ def test_quadconvbn_stride2_bn_only_path():
         if n in ("layer.bc",):
             continue
         assert rel(g1[n], p.grad) <= 3e-2, n
+
+
+@pytest.mark.gpu
+def test_memory_ledger_accounts_minimal_cache():
+    """AUTO vs HYBRID retained bytes on QuadraVGG-16."""
+    from paper_2204_01701_b200 import qnets
+    from paper_2204_01701_b200.ledger import memory_ledger
+    m = qnets.QuadraVGG16(10).cuda().to(memory_format=torch.channels_last)
+    x = torch.randn(16, 3, 32, 32, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    led = memory_ledger(m, x)
+    assert led.peak_auto > 0 and led.peak_hybrid > 0
+    assert set(led.per_layer_auto) == set(led.per_layer_hybrid) and len(led.per_layer_hybrid) == 13
+    # the symbolic node keeps exactly its minimal cache: a, b (neurons.cache_names; x is the
+    # previous layer's output) + the BN input y + the output z, nothing else (no patches,
+    # no intermediate sums); the op-by-op twin keeps at least as much
+    from paper_2204_01701_b200.bn import QuadConvBN
+    obytes = {}
+    hooks = [mod.register_forward_hook(lambda md, i_, o, n=name: obytes.__setitem__(n, o.numel() * o.element_size()))
+             for name, mod in m.named_modules() if isinstance(mod, QuadConvBN)]
+    with torch.no_grad(), torch.autocast("cuda", dtype=torch.bfloat16):
+        m(x)
+    for h in hooks:
+        h.remove()
+    assert len(obytes) == 12
+    for name, ob in obytes.items():
+        got = led.per_layer_hybrid[name]
+        assert 4 * ob <= got <= 4 * ob + 0.15 * ob + 8192, (name, got, ob)  # + stats / allocator rounding
+        assert led.per_layer_auto[name] >= 4 * ob, (name, led.per_layer_auto[name], ob)
