@@ -9,6 +9,7 @@
 // neurons.py:295-445 backward) with the conv lowered as an implicit GEMM
 // instead of materialising the patch matrix (tensor.py:283-331).
 #include <stdio.h>
+#include <stdlib.h>
 #include "qd_kernels.h"
 #include "qd_gemm.cuh"
 #include "qd_ptx.cuh"

@@ -170,6 +170,18 @@ __device__ __forceinline__ void c2_store_rb(const C2Args& g, const uint8_t* st, 
     if (rp >= 0) *reinterpret_cast<uint4*>(dst + (size_t)rp * g.Cout + ch + c * 8) = val;
   }
 }
+// store pass with the per-row element offsets (pixel * Cout + channel chunk, -1 =
+// skip) computed once per tile for the 32/RPI rows this lane stores
+template <int RB>
+__device__ __forceinline__ void c2_store_rb_pre(const uint8_t* st, bf16* dst, const long long* roff, int lane) {
+  constexpr int CH = RB / 16, RPL = 128 / RB, RPI = 32 / CH;
+#pragma unroll
+  for (int i = 0; i < 32 / RPI; ++i) {
+    const int Rw = RPI * i + lane / CH, c = lane % CH;
+    uint4 val = *reinterpret_cast<const uint4*>(st + Rw * RB + ((c ^ ((Rw / RPL) & (CH - 1))) << 4));
+    if (roff[i] >= 0) *reinterpret_cast<uint4*>(dst + roff[i]) = val;
+  }
+}
 __device__ __forceinline__ void c2_pack16(const float* v, uint4& lo, uint4& hi) {
   lo = make_uint4(c2::pack2(v[0], v[1]), c2::pack2(v[2], v[3]), c2::pack2(v[4], v[5]), c2::pack2(v[6], v[7]));
   hi = make_uint4(c2::pack2(v[8], v[9]), c2::pack2(v[10], v[11]), c2::pack2(v[12], v[13]), c2::pack2(v[14], v[15]));
@@ -547,13 +559,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
           if (tracer1) C2_TRACE(2, it, 12);
           continue;
         }
+        // rows this lane stores in every pass: shuffles and address math once per tile
+        constexpr int SCH = (2 * CW) / 16, SRPI = 32 / SCH, NRI = 32 / SRPI;
+        long long roff[NRI];
+#pragma unroll
+        for (int i = 0; i < NRI; ++i) {
+          const int rp = __shfl_sync(0xffffffffu, pix, SRPI * i + lane / SCH);
+          roff[i] = rp >= 0 ? (long long)rp * g.Cout + c_base + eg * CW + (lane % SCH) * 8 : -1;
+        }
 #pragma unroll
         for (int o = 0; o < 3; ++o) {
 #pragma unroll
           for (int jj = 0; jj < JJ; ++jj) c2_stage_rb<2 * CW>(stg, lane, jj, pk[o][jj][0], pk[o][jj][1]);
           __syncwarp();
           if (!(g.dbg & 4))  // dev knob: skip the global stores
-            c2_store_rb<2 * CW>(g, stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), c_base + eg * CW, pix, lane);
+            c2_store_rb_pre<2 * CW>(stg, o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2), roff, lane);
           __syncwarp();
         }
         if (tracer) C2_TRACE(2, it, 3);
@@ -1410,6 +1430,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       ptx::mbar_wait(done, 0);
       ptx::tc_fence_after();
     }
+    if (g.trace && threadIdx.x == 0 && blockIdx.x < 1024) g.trace[4096 + blockIdx.x] = gtimer();  // main loop done
     float* dst = g.part + (size_t)split * g.Jd * g.Kf;
     // accumulators: 0, 1 = tap pairs of this CTA over NT; 2 = tap 8 over boxes [nlo, nhi)
     for (int acc = 0; acc < 3; ++acc) {

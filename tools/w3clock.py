@@ -34,3 +34,10 @@ print(f"CTAs {nb}: start spread {(G[:,0].max()-G[:,0].min())/1e3:.2f} us, span {
       f" dur min/med/max {dur.min():.1f}/{np.median(dur):.1f}/{dur.max():.1f} us")
 ghz = cyc / (G[:, 1] - G[:, 0])
 print(f"SM clock in-kernel: min/med/max {ghz.min():.3f}/{np.median(ghz):.3f}/{ghz.max():.3f} GHz")
+
+Dn = buf[4096:4096 + nb].astype(np.int64)
+if (Dn > 0).all():
+    epi = (G[:, 1] - Dn) / 1e3
+    main = (Dn - G[:, 0]) / 1e3
+    print(f"main loop min/med/max {main.min():.1f}/{np.median(main):.1f}/{main.max():.1f} us, "
+          f"epilogue min/med/max {epi.min():.1f}/{np.median(epi):.1f}/{epi.max():.1f} us")
