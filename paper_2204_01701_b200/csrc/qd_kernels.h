@@ -140,6 +140,8 @@ int wgrad2_split(const Plan& P);
 int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0);
 // v3 wgrad (r = 3) on CTA pairs with multicast stage loads; 0 when not eligible
+void set_conv2_cap(int pairs);
+int wgrad3_pairs_per_split(const Plan& P);
 int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0);

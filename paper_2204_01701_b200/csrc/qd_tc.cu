@@ -987,6 +987,21 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if (mat || up) D = Dw;
   }
   int rc;
+  // SM partition: the v3 wgrad runs on ~54% of the SM pairs (side stream) while
+  // the dgrad runs on the rest, both persistent and concurrent -- their tails
+  // (partial-store drain, last-tile imbalance) overlap instead of adding up.
+  // 54% balances the two on the measured C2 step; QD_PART=K pins
+  // K pairs, QD_NO_PART=1 runs them back to back on all SMs.
+  int part = 0, dg_pairs = 0;
+  if (w3 && dx && dW[0] && !P.sq && !getenv("QD_NO_PART") && !getenv("QD_BR2")) {
+    const int per = wgrad3_pairs_per_split(P);
+    const int total = L.wg_split * per;  // pairs the wgrad alone would fill
+    part = getenv("QD_PART") ? atoi(getenv("QD_PART")) : (total * 54 / per + 50) / 100;
+    dg_pairs = total - part * per;
+    // one pair per split only: with several (wide C) the split granularity is too
+    // coarse to balance the two (measured: 256x14 loses 15%)
+    if (per != 1 || part < 1 || part >= L.wg_split || dg_pairs < total / 4) part = 0;
+  }
   // ---- wgrad ----
   if (dW[0]) {
     const void* x0 = x;
@@ -1003,15 +1018,17 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     // dev: QD_BR2=1 runs wgrad + fold on the side stream concurrently with the dgrad
     const bool br2 = (w2 || w3) && dx && !P.sq && getenv("QD_BR2") && atoi(getenv("QD_BR2"));
     cudaStream_t wst = st;
-    if (br2) {
+    if (br2 || part) {
       side = fork_side(st);
       if (side) wst = side;
+      else part = 0;
     }
     if (w3) {
-      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, wst, dy, dsplit);
+      const int ns = part ? part : L.wg_split;
+      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), ns, wst, dy, dsplit);
       wsp.pp = (P.r * P.r + 1) / 2;  // every tap in every split slot
       wsp.ng = 1;
-      wsp.s[0] = L.wg_split;
+      wsp.s[0] = ns;
     } else if (w2) {
       rc = run_wgrad2(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), L.wg_split, wst, dy, dsplit);
       wsp = wgrad2_splits(P);
@@ -1063,12 +1080,14 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     GemmCfg c = dgrad_cfg(P);
     const void* xr = P.sq ? x : nullptr;
     rc = QD_ERR_UNSUPPORTED;
+    if (part) set_conv2_cap(dg_pairs);
     if (!(P.flags & QD_FLAG_TC_V1))
       // D is complete once the (PDL-launched) v2/v3 wgrad is running, and nothing
       // the dgrad reads is written by it: the dgrad need not wait for the wgrad
       rc = run_conv2(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
                      c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st, 1,
                      dy, dsplit, wg_pdl ? 0 : 1);
+    if (part) set_conv2_cap(0);
     if (d2 && rc == QD_ERR_UNSUPPORTED) return set_error(QD_ERR_UNSUPPORTED, "dgrad conv2 plan changed");
     if (rc == QD_ERR_UNSUPPORTED && !up)
       rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,

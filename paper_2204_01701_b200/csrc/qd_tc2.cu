@@ -880,6 +880,10 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   return pl;
 }
 
+// cap on the persistent conv2 grid (pairs) for the next launches; 0 = all SMs
+static int g_conv2_cap = 0;
+void set_conv2_cap(int pairs) { g_conv2_cap = pairs; }
+
 template <int EPI, int NB, int R>
 static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
                        cudaStream_t st) {
@@ -899,6 +903,7 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   int clusters = tc_num_sms() / 2;
   if (maxc > 0 && maxc < clusters) clusters = maxc;
   if (pl.g.total < clusters) clusters = pl.g.total;
+  if (g_conv2_cap > 0 && g_conv2_cap < clusters) clusters = g_conv2_cap;
   launch_pdl(conv2_kernel<EPI, NB, R>, dim3(2 * clusters), dim3(C2Threads<EPI, NB>::THREADS), pl.smem, st, A0, A1, B,
              pl.g);
   count_launch(st, "conv2");
@@ -1543,11 +1548,19 @@ int wgrad3_split(const Plan& P) {
   return pl.ok ? pl.g.nsplit : 0;
 }
 
+// SM pairs one split of the v3 wgrad occupies (its grid is this x nsplit pairs)
+int wgrad3_pairs_per_split(const Plan& P) {
+  W3Plan pl = w3_plan(P);
+  return pl.ok ? pl.g.jtiles * pl.g.ablocks : 0;
+}
+
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail, int jsplit) {
   W3Plan pl = w3_plan(P);
-  if (!pl.ok || pl.g.nsplit != splits) return QD_ERR_UNSUPPORTED;
+  // splits < the plan's: a partitioned launch sharing the SMs with a concurrent kernel
+  if (!pl.ok || splits < 1 || splits > pl.g.nsplit) return QD_ERR_UNSUPPORTED;
   W3Args& g = pl.g;
+  g.nsplit = splits;
   g.part = part;
   g.trace = getenv("QD_TRACE") ? trace_buffer() : nullptr;
   CUtensorMap X0, X1, Dm, Dm1;
