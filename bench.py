@@ -51,6 +51,12 @@ WORKLOADS = {
     "c5_t3_64x56": ("t3", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
     "c5_t2and4_64x56": ("t2and4", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
     "dw_proposed_256x28": ("proposed", "dwconv", 64, 256, 256, 28, 28, 3, 1, 1, "bf16"),
+    # QuadraVGG-16 layer shapes at its bench batch (per-layer profiling)
+    "vgg_64x32": ("proposed", "conv", 256, 64, 64, 32, 32, 3, 1, 1, "bf16"),
+    "vgg_128x16": ("proposed", "conv", 256, 128, 128, 16, 16, 3, 1, 1, "bf16"),
+    "vgg_256x8": ("proposed", "conv", 256, 256, 256, 8, 8, 3, 1, 1, "bf16"),
+    "vgg_512x4": ("proposed", "conv", 256, 512, 512, 4, 4, 3, 1, 1, "bf16"),
+    "vgg_512x2": ("proposed", "conv", 256, 512, 512, 2, 2, 3, 1, 1, "bf16"),
 }
 METRIC = "quadratic_conv_fwd_bwd_tflops"
 L2_NOTE = ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read so the "

@@ -14,6 +14,8 @@ import threading
 from .errors import ConfigError, DeviceError, DimensionError, IntegrityError
 
 LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libquadra_b200.so")
+if os.environ.get("QD_DEV_LIB"):  # dev A/B timing: another in-tree build of this library
+    LIB_PATH = os.path.join(os.path.dirname(LIB_PATH), os.environ["QD_DEV_LIB"])
 
 FAMILY_CODE = {"first_order": 0, "t2": 1, "t4": 2, "proposed": 3, "t2_linear": 4, "t3": 5, "t2and4": 6,
                "t1_pure": 7, "t1_full": 8, "t1and2": 9}

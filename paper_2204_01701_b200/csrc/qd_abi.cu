@@ -39,6 +39,16 @@ static void prof_mark(cudaStream_t st, const char* name) {
   ++g_prof_used;
 }
 
+// dev (timing ablation only; results are wrong): QD_SKIP=pack,fprop,prologue,wgrad,finish,dgrad
+bool dev_skip(const char* name) {
+  static const char* s = getenv("QD_SKIP");
+  if (!s) return false;
+  const size_t n = strlen(name);
+  for (const char* p = strstr(s, name); p; p = strstr(p + 1, name))
+    if ((p == s || p[-1] == ',') && (p[n] == 0 || p[n] == ',')) return true;
+  return false;
+}
+
 void count_launch(cudaStream_t st, const char* name) {
   g_launches.fetch_add(1ull, std::memory_order_relaxed);
   if (g_prof) prof_mark(st, name);
@@ -108,6 +118,12 @@ Workspace plan_workspace(const Plan& P, int path) {
   }
   L.sz_WG = (size_t)L.wg_split * P.Jd * P.Kf * 4;
   long long bs = (Pg.Mout + 255) / 256;
+  if (path == 1 && P.F % 8 == 0 && P.F <= 2048) {
+    // the vectorised prologue covers 4 x (2048 / F) rows per block iteration:
+    // wide layers need more blocks for the same rows
+    const long long rows_it = 4LL * (2048 / P.F);
+    bs = (Pg.Mout + rows_it - 1) / rows_it;
+  }
   {
     const char* e = getenv("QD_BS_MULT");
     int mult = e ? atoi(e) : 2;
@@ -117,6 +133,7 @@ Workspace plan_workspace(const Plan& P, int path) {
   L.bs_split = (int)bs;
   L.sz_BS = (size_t)L.bs_split * P.Jd * 4;
   if (path == 1 && P.sq) L.sz_XS = (size_t)P.Min * P.C * es;
+  if (path == 1 && !(P.flags & QD_FLAG_FORCE_SIMT)) L.sz_SK = tc_splitk_bytes(P);
   size_t off = 0;
   L.off_P = off; off = align_up(off + L.sz_P);
   L.off_D = off; off = align_up(off + L.sz_D);
@@ -124,6 +141,7 @@ Workspace plan_workspace(const Plan& P, int path) {
   L.off_BS = off; off = align_up(off + L.sz_BS);
   L.off_XS = off; off = align_up(off + L.sz_XS);
   L.off_ZB = off; off = align_up(off + L.sz_ZB);
+  L.off_SK = off; off = align_up(off + L.sz_SK);
   L.total = off;
   return L;
 }

@@ -24,10 +24,12 @@ struct Workspace {
   size_t off_BS, sz_BS;    // bias-sum partials (fp32)
   size_t off_XS, sz_XS;    // squared input (dtype), t2/t2_linear tcgen05 path
   size_t off_ZB, sz_ZB;    // zero bias vectors (t2and4 reuses the proposed epilogue)
+  size_t off_SK, sz_SK;    // split-K fp32 partials of the v1 fprop / dgrad (small output grids)
   int wg_split;            // number of wgrad partials
   int bs_split;            // number of bias-sum partials
 };
 Workspace plan_workspace(const Plan& P, int path);
+size_t tc_splitk_bytes(const Plan& P);
 
 // ---- packing (both paths) --------------------------------------------------
 size_t pack_fprop_elems(const Plan& P);
@@ -141,6 +143,7 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
                cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0);
 // v3 wgrad (r = 3) on CTA pairs with multicast stage loads; 0 when not eligible
 void set_conv2_cap(int pairs);
+bool dev_skip(const char* name);
 int wgrad3_pairs_per_split(const Plan& P);
 int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,

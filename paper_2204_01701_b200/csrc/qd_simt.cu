@@ -185,6 +185,7 @@ static void launch_pack_conv(const Plan& P, const float* const w[3], T* out, siz
 }
 
 void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
+  if (dev_skip("pack")) return;
   long long nf = (long long)pack_fprop_elems(P), nd = (long long)pack_dgrad_elems(P);
   if (P.kind == QD_KIND_CONV && P.sq == 0 && P.Jd == P.nb * P.F && P.Cd == P.C) {
     const int rr = P.r * P.r;
@@ -255,9 +256,136 @@ __global__ void sgd_pack_kernel(Plan P, float* w0, float* w1, float* w2, float* 
   }
 }
 
+// tiled variant: block = (role, TF filters, TC channels) with all r*r taps. The
+// update streams the role's contiguous (F, C, r, r) / (C, F) rows; the new weights
+// go through shared memory so the packed fprop rows (c fastest) and dgrad rows
+// (filter fastest) are written as contiguous runs instead of scattered 2-B stores.
+template <typename T, int TF, int TC, int RR>  // RR = r*r at compile time (0: runtime)
+__global__ void __launch_bounds__(256) sgd_pack_tiled_kernel(Plan P, float* w0, float* w1, float* w2, float* m0,
+                                                             float* m1, float* m2, const float* g0,
+                                                             const float* g1, const float* g2, float lr, float mom,
+                                                             float wd, int first, T* out) {
+  extern __shared__ float tile[];  // [TF][rr][TC]
+  __shared__ int Rrow[TF];
+  const int rr = RR ? RR : P.r * P.r;
+  const int ftiles = (P.F + TF - 1) / TF, ctiles = (P.C + TC - 1) / TC;
+  int b = blockIdx.x;
+  const int ct = b % ctiles;
+  b /= ctiles;
+  const int ft = b % ftiles, role = b / ftiles;
+  const int f0 = ft * TF, c0 = ct * TC;
+  float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+  float* m = role == 0 ? m0 : (role == 1 ? m1 : m2);
+  const float* g = role == 0 ? g0 : (role == 1 ? g1 : g2);
+  const bool fc = P.kind == QD_KIND_FC;
+  // packed positions are affine in (c, tap) for a fixed (role, f) and in f for a
+  // fixed (role, c, tap): take the offsets from pack_positions once
+  int R0, kf0, cp0, kdl;
+  pack_positions(P, role, f0, c0, rr - 1, R0, kf0, cp0, kdl);  // tap rr-1: kd = j(f0)
+  kf0 -= (rr - 1) * P.C;                                          // kf of (f0, c0, tap 0)
+  if ((int)threadIdx.x < TF) {
+    int R, kf, cp, kd;
+    const int f = f0 + threadIdx.x < P.F ? f0 + threadIdx.x : f0;
+    pack_positions(P, role, f, c0, 0, R, kf, cp, kd);
+    Rrow[threadIdx.x] = R;
+  }
+  const int n = TF * TC * rr;
+  constexpr int U = 4;  // elements per thread per pass, all 12 loads in flight
+  for (int e0 = threadIdx.x; e0 < n; e0 += U * blockDim.x) {
+    size_t o[U];
+    int ti[U];
+    bool ok[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int e = e0 + u * blockDim.x;
+      int fi, cl, tap;
+      if (fc) {  // (C, F): filter fastest
+        cl = e / TF;
+        fi = e - cl * TF;
+        tap = 0;
+      } else {  // (F, C, r, r): one contiguous run of TC*rr per filter
+        fi = e / (TC * rr);
+        const int rem = e - fi * TC * rr;
+        cl = rem / rr;
+        tap = rem - cl * rr;
+      }
+      const int f = f0 + fi, c = c0 + cl;
+      ok[u] = e < n && f < P.F && c < P.C;
+      o[u] = ok[u] ? (fc ? (size_t)c * P.F + f : ((size_t)f * P.C + c) * rr + tap) : 0;
+      ti[u] = (fi * rr + tap) * TC + cl;
+    }
+    float gv[U], wv[U], mv[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      gv[u] = ok[u] ? g[o[u]] : 0.f;
+      wv[u] = ok[u] ? w[o[u]] : 0.f;
+      mv[u] = (ok[u] && !first) ? m[o[u]] : 0.f;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      if (!ok[u]) continue;
+      const float d = gv[u] + wd * wv[u];
+      const float v = first ? d : mom * mv[u] + d;
+      m[o[u]] = v;
+      const float nw = wv[u] - lr * v;
+      w[o[u]] = nw;
+      tile[ti[u]] = nw;
+    }
+  }
+  __syncthreads();
+  const int fmax = P.F - f0, cmax = P.C - c0;
+  // fprop rows: channel fastest
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int cl = e % TC, t2 = e / TC, tap = t2 % rr, fi = t2 / rr;
+    if (fi >= fmax || cl >= cmax) continue;
+    out[(size_t)Rrow[fi] * P.Kf + kf0 + tap * P.C + cl] = cvt<T>(tile[e]);
+  }
+  // dgrad rows: filter fastest
+  T* od = out + (long long)P.nb * P.F * P.Kf + (size_t)cp0 * P.Kd + kdl;
+  for (int e = threadIdx.x; e < n; e += blockDim.x) {
+    const int fi = e % TF, t2 = e / TF, tap = t2 % rr, cl = t2 / rr;
+    if (fi >= fmax || cl >= cmax) continue;
+    od[(size_t)cl * P.Kd + (rr - 1 - tap) * P.Jd + fi] = cvt<T>(tile[(fi * rr + tap) * TC + cl]);
+  }
+}
+
+template <typename T, int TF, int TC>
+static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3],
+                             float lr, float momentum, float wd, int first, T* out, cudaStream_t st) {
+  const size_t smem = (size_t)TF * TC * P.r * P.r * 4;
+  const int blocks = P.nroles * ((P.F + TF - 1) / TF) * ((P.C + TC - 1) / TC);
+  if (P.r == 3) {
+    sgd_pack_tiled_kernel<T, TF, TC, 9><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
+                                                                    grad[0], grad[1], grad[2], lr, momentum, wd,
+                                                                    first, out);
+    return;
+  }
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && smem > attr) {
+    cudaFuncSetAttribute(sgd_pack_tiled_kernel<T, TF, TC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr = smem;
+  }
+  sgd_pack_tiled_kernel<T, TF, TC, 0><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
+                                                                  grad[0], grad[1], grad[2], lr, momentum, wd,
+                                                                  first, out);
+}
+
 void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
                      float momentum, float wd, int first, void* wpack, cudaStream_t st) {
-  const long long tot = (long long)P.F * P.C * P.r * P.r * P.nroles;
+  const int rr = P.r * P.r;
+  if (!getenv("QD_SGD_ELEM") && rr <= 49) {
+    if (P.dtype == QD_BF16) {
+      if (rr <= 9) launch_sgd_tiled<bf16, 32, 32>(P, w, mom, grad, lr, momentum, wd, first, (bf16*)wpack, st);
+      else launch_sgd_tiled<bf16, 16, 16>(P, w, mom, grad, lr, momentum, wd, first, (bf16*)wpack, st);
+    } else {
+      if (rr <= 9) launch_sgd_tiled<float, 32, 32>(P, w, mom, grad, lr, momentum, wd, first, (float*)wpack, st);
+      else launch_sgd_tiled<float, 16, 16>(P, w, mom, grad, lr, momentum, wd, first, (float*)wpack, st);
+    }
+    count_launch(st, "sgd_pack");
+    return;
+  }
+  const long long tot = (long long)P.F * P.C * rr * P.nroles;
   const int grid = grid_for(tot);
   if (P.dtype == QD_BF16)
     sgd_pack_kernel<bf16><<<grid, 256, 0, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2], grad[0], grad[1],
@@ -626,6 +754,35 @@ namespace qd {
 // blocks [0, nwb) sum the wgrad split-K partials -- 32 float4 columns x 8
 // partial groups per block, combined in a fixed order (deterministic) -- and
 // scatter them into the reference layouts; the rest sum the bias partials.
+// bias columns: 8 columns x 32 partial groups per block, 4 independent chains per thread
+__device__ __forceinline__ void finish_bias_block(const Plan& P, int bblk, const float* __restrict__ bpart, int SB,
+                                                  float* d0, float* d1, float* d2) {
+  if (P.nbias == 0 || !d0) return;
+  __shared__ float redb[32][9];
+  const int bc = threadIdx.x % 8, bg = threadIdx.x / 8;
+  int j = bblk * 8 + bc;
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (j < P.Jd) {
+    int s = bg;
+    for (; s + 96 < SB; s += 128) {
+      a0 += bpart[(size_t)s * P.Jd + j];
+      a1 += bpart[(size_t)(s + 32) * P.Jd + j];
+      a2 += bpart[(size_t)(s + 64) * P.Jd + j];
+      a3 += bpart[(size_t)(s + 96) * P.Jd + j];
+    }
+    for (; s < SB; s += 32) a0 += bpart[(size_t)s * P.Jd + j];
+  }
+  redb[bg][bc] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (bg == 0 && j < P.Jd) {
+    float t = 0.f;
+    for (int gq = 0; gq < 32; ++gq) t += redb[gq][bc];
+    int role = j / P.F, f = j % P.F;
+    float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
+    if (dst) dst[f] = t;
+  }
+}
+
 __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __restrict__ wpart, int S, WSplits wsp,
                                                          float* w0, float* w1, float* w2,
                                                          const float* __restrict__ bpart, int SB, float* d0,
@@ -689,42 +846,133 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
       else dst[(((size_t)f * P.C + c) * P.r + dy) * P.r + dx] = av[e];
     }
   } else {
-    // bias columns: 8 columns x 32 partial groups per block, 4 independent chains per thread
-    if (P.nbias == 0 || !d0) return;
-    __shared__ float redb[32][9];
-    const int bc = threadIdx.x % 8, bg = threadIdx.x / 8;
-    int j = ((int)blockIdx.x - nwb) * 8 + bc;
-    float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-    if (j < P.Jd) {
-      int s = bg;
-      for (; s + 96 < SB; s += 128) {
-        a0 += bpart[(size_t)s * P.Jd + j];
-        a1 += bpart[(size_t)(s + 32) * P.Jd + j];
-        a2 += bpart[(size_t)(s + 64) * P.Jd + j];
-        a3 += bpart[(size_t)(s + 96) * P.Jd + j];
+    finish_bias_block(P, (int)blockIdx.x - nwb, bpart, SB, d0, d1, d2);
+  }
+}
+
+// conv weight fold: block = (NJ D channels j, K half, 64-channel chunk). G warp
+// groups sum interleaved split subsets (fixed order) of the block's NJ x rr x 64
+// partial values (G x NJ = 8: with few splits the lanes cover more rows, so every
+// block keeps ~1k independent loads in flight), and the totals are written
+// transposed into the reference (F, C, r, r) layout: partial reads and gradient
+// writes are both coalesced (the element-wise fold above writes with stride r*r).
+template <int RR>  // r*r at compile time (0: runtime)
+__global__ void __launch_bounds__(256) wfinish_conv_kernel(Plan P, const float* __restrict__ wpart, int S,
+                                                           WSplits wsp, float* w0, float* w1, float* w2,
+                                                           const float* __restrict__ bpart, int SB, float* d0,
+                                                           float* d1, float* d2, int nwb) {
+  extern __shared__ float4 red[];  // [G][NJ][rr][17]: 64 channels + 4 pad floats per tap row
+  if ((int)blockIdx.x >= nwb) {
+    finish_bias_block(P, (int)blockIdx.x - nwb, bpart, SB, d0, d1, d2);
+    return;
+  }
+  if (!w0) return;
+  const int G = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1)), NJ = 8 / G, L = 256 / G;
+  const int rr = RR ? RR : P.r * P.r, nv = rr * 16, nvb = NJ * nv;
+  const int cch = P.C / 64, nh = P.Kf / P.K0;
+  int b = blockIdx.x;
+  const int cb = b % cch;
+  b /= cch;
+  const int half = b % nh, j0 = (b / nh) * NJ;
+  const int lane = threadIdx.x % L, grp = threadIdx.x / L;
+  const long long stride4 = (long long)P.Jd * P.Kf / 4;
+  const float4* src = reinterpret_cast<const float4*>(wpart + half * P.K0 + cb * 64) + (long long)j0 * (P.Kf / 4);
+  const int c4s = P.C / 4, kf4 = P.Kf / 4;
+  for (int v0 = 0; v0 < nvb; v0 += 4 * L) {
+    float4 acc[4];
+    int off[4], soff[4], sk[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+      const int vb = v0 + lane + L * u, jj = vb / nv, v = vb - jj * nv, tap = v >> 4, c4 = v & 15;
+      off[u] = jj * kf4 + tap * c4s + c4;
+      soff[u] = (jj * rr + tap) * 17 + c4;
+      int sv = S;
+      if (wsp.ng > 0) {
+        const int tg = (tap / 2) / wsp.pp;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)  // static indexing: no local-memory copy of wsp
+          if (t == tg) sv = wsp.s[t];
       }
-      for (; s < SB; s += 32) a0 += bpart[(size_t)s * P.Jd + j];
+      sk[u] = (vb < nvb && j0 + jj < P.Jd) ? sv : 0;
     }
-    redb[bg][bc] = (a0 + a1) + (a2 + a3);
-    __syncthreads();
-    if (bg == 0 && j < P.Jd) {
-      float t = 0.f;
-      for (int gq = 0; gq < 32; ++gq) t += redb[gq][bc];
-      int role = j / P.F, f = j % P.F;
-      float* dst = role == 0 ? d0 : (role == 1 ? d1 : d2);
-      if (dst) dst[f] = t;
+#pragma unroll 2
+    for (int s = grp; s < S; s += G) {
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (s < sk[u]) {
+          const float4 x = __ldg(src + s * stride4 + off[u]);
+          acc[u].x += x.x; acc[u].y += x.y; acc[u].z += x.z; acc[u].w += x.w;
+        }
     }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (v0 + lane + L * u < nvb) red[grp * NJ * rr * 17 + soff[u]] = acc[u];
+  }
+  __shared__ float* rowdst[8];
+  if ((int)threadIdx.x < NJ) {
+    const int j = j0 + threadIdx.x;
+    float* o = nullptr;
+    int role, f, kk;
+    if (j < P.Jd && wgrad_dst(P, j, half * P.K0, role, f, kk)) {  // else t2and4 structural zero
+      float* dst = role == 0 ? w0 : (role == 1 ? w1 : w2);
+      if (dst) o = dst + ((size_t)f * P.C + cb * 64) * rr;
+    }
+    rowdst[threadIdx.x] = o;
+  }
+  __syncthreads();
+  const float* redf = reinterpret_cast<const float*>(red);
+  const int gstride = NJ * rr * 68;  // floats per split group
+  const int per = 64 * rr;           // outputs per row, a multiple of 4
+  for (int q = threadIdx.x; q < NJ * per / 4; q += blockDim.x) {
+    const int e4 = 4 * q, jj = e4 / per, e = e4 - jj * per;
+    float* o = rowdst[jj];
+    if (!o) continue;
+    const float* rj = redf + jj * rr * 68;
+    float v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = (e + k) / rr, tap = e + k - c * rr;
+      const float* qp = rj + tap * 68 + c;
+      float t = qp[0];
+      for (int g = 1; g < G; ++g) t += qp[g * gstride];
+      v[k] = t;
+    }
+    *reinterpret_cast<float4*>(o + e) = make_float4(v[0], v[1], v[2], v[3]);  // (f C + 64 cb) rr % 4 == 0
   }
 }
 
 void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& ws, float* const dW[3],
                        const float* bpart, int SB, float* const db[3], cudaStream_t st) {
+  if (dev_skip("finish")) return;
   long long total = (long long)P.Jd * P.Kf;  // Kf is a multiple of 64 on the tcgen05 path
   int nwb = dW[0] ? (int)((total / 4 + 31) / 32) : 0;
   int nbb = (P.nbias && db[0]) ? (P.Jd + 7) / 8 : 0;
   if (nwb + nbb == 0) return;
-  bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
-                                                db[2], nwb);
+  bool al16 = true;  // the transposing fold writes float4
+  for (int i = 0; i < 3; ++i) al16 = al16 && ((uintptr_t)dW[i] % 16 == 0);
+  if (P.kind == QD_KIND_CONV && P.C % 64 == 0 && P.r <= 7 && al16 && !getenv("QD_OLD_FINISH")) {
+    const int G = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1)), NJ = 8 / G;  // as in the kernel
+    const int nwc = dW[0] ? (P.Jd + NJ - 1) / NJ * (P.Kf / P.K0) * (P.C / 64) : 0;
+    const size_t smem = (size_t)8 * P.r * P.r * 17 * sizeof(float4);
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && smem > attr) {
+      cudaFuncSetAttribute(wfinish_conv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      attr = smem;
+    }
+    if (P.r == 3)
+      wfinish_conv_kernel<9><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0],
+                                                           db[1], db[2], nwc);
+    else if (P.r == 1)
+      wfinish_conv_kernel<1><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0],
+                                                           db[1], db[2], nwc);
+    else
+      wfinish_conv_kernel<0><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0],
+                                                           db[1], db[2], nwc);
+  } else {
+    bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
+                                                  db[2], nwb);
+  }
   count_launch(st, "bwd_finish");
 }
 }  // namespace qd

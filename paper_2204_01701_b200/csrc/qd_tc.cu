@@ -43,6 +43,11 @@ struct ConvArgs {
   const float* bias1;
   const float* bias2;
   const bf16* xres;         // x (NHWC) for EPI_SQ
+  // split-K (small output grids): work item = (tile, K slice); the epilogue then
+  // writes fp32 partials [ksplit][Mpix][part_ld] and splitk_finish applies EPI
+  int ksplit, kb_per, part_ld;
+  long long Mpix;
+  float* part;
 };
 
 template <int EPI, int NB>
@@ -123,6 +128,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int KB = args.kb_half * (args.dual ? 2 : 1);
+  const int NWORK = args.total_tiles * args.ksplit;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -130,12 +136,14 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t bytes = (uint32_t)(args.box_rows * 128 + Cfg::B_BYTES);
-      for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x) {
+      for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x) {
+        const int t = wi / args.ksplit, ks = wi - t * args.ksplit;
+        const int kb0 = ks * args.kb_per, kb1 = min(KB, kb0 + args.kb_per);
         int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
         int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
         int tn = mt / (args.tiles_w * args.tiles_h);
         int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
-        for (int kb = 0; kb < KB; ++kb) {
+        for (int kb = kb0; kb < kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], bytes);
           int half = kb / args.kb_half, kk = kb % args.kb_half;
@@ -162,13 +170,15 @@ __global__ void __launch_bounds__(256, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+    for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x, ++it) {
+      const int ks = wi % args.ksplit;
+      const int kb0 = ks * args.kb_per, kb1 = min(KB, kb0 + args.kb_per);
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
       ptx::mbar_wait(&tempty[as], aph ^ 1);
       ptx::tc_fence_after();
       uint32_t d_tmem = tmem_base + as * Cfg::ACC_COLS;
-      for (int kb = 0; kb < KB; ++kb) {
+      for (int kb = kb0; kb < kb1; ++kb) {
         ptx::mbar_wait(&full[stage], phase);
         ptx::tc_fence_after();
         const uint32_t a_lo = a_lo0 + stage * (Cfg::A_BYTES >> 4);
@@ -177,7 +187,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             ptx::mma_bf16(d_tmem, ptx::mk_desc(DHI, a_lo + 2 * k), ptx::mk_desc(DHI, b_lo + 2 * k), IDESC,
-                          (kb | k) != 0);
+                          (kb != kb0) || (k != 0));
           ptx::mma_commit(&empty[stage]);
         }
         __syncwarp();
@@ -192,13 +202,44 @@ __global__ void __launch_bounds__(256, 1)
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 128;
     int it = 0;
-    for (int t = blockIdx.x; t < args.total_tiles; t += gridDim.x, ++it) {
+    for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x, ++it) {
+      const int t = wi / args.ksplit, ks = wi - t * args.ksplit;
       int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
       int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
       int tn = mt / (args.tiles_w * args.tiles_h);
       int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
+      if (args.part) {
+        // split-K slice: raw fp32 accumulator rows into the partial buffer
+        ptx::mbar_wait(&tfull[as], aph);
+        ptx::tc_fence_after();
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::ACC_COLS;
+        const int ww = row % args.Wb, hh = (row / args.Wb) % args.Hb, nn = row / (args.Wb * args.Hb);
+        const int n = n0 + nn, h = h0 + hh, w = w0 + ww;
+        const bool ok = row < args.box_rows && n < args.Ng && h < args.OHg && w < args.OWg;
+        float* prow = args.part + ((size_t)ks * args.Mpix + ((size_t)n * args.OHg + h) * args.OWg + w) * args.part_ld +
+                      (size_t)ntile * NB * 64;
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          float v[NB][16];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) ptx::tmem_ld16(tb + i * 64 + j * 16, v[i]);
+          ptx::tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+#pragma unroll
+              for (int e = 0; e < 16; e += 4)
+                *reinterpret_cast<float4*>(prow + i * 64 + j * 16 + e) =
+                    make_float4(v[i][e], v[i][e + 1], v[i][e + 2], v[i][e + 3]);
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+        continue;
+      }
       // previous tile's TMA stores must have finished reading the staging tiles
       if (etid == 0) ptx::bulk_wait_read0();
       ptx::named_bar_sync(1, 128);
@@ -303,6 +344,93 @@ __global__ void __launch_bounds__(256, 1)
   if (warp == 2) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tmem_base, 512);
+  }
+}
+
+// split-K fold: one thread per (pixel, 8 output channels) sums the K slices in
+// order and applies the conv_gemm epilogue (same math as above)
+template <int EPI, int NB>
+__global__ void __launch_bounds__(256) splitk_finish_kernel(const float* __restrict__ part, int S, long long Mpix,
+                                                            int ld, int Cout, bf16* o0, bf16* o1, bf16* o2,
+                                                            const float* __restrict__ bias0,
+                                                            const float* __restrict__ bias1,
+                                                            const float* __restrict__ bias2,
+                                                            const bf16* __restrict__ xres) {
+  const int c8n = Cout / 8;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= Mpix * c8n) return;
+  const long long pix = idx / c8n;
+  const int c = (int)(idx - pix * c8n) * 8;
+  constexpr int NACC = (EPI == EPI_PLAIN) ? 1 : NB;
+  // partial column of accumulator i for output channel c
+  int col[NACC];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i)
+    col[i] = (EPI == EPI_PLAIN) ? c : (c / 64) * NB * 64 + i * 64 + c % 64;
+  float acc[NACC][8];
+#pragma unroll
+  for (int i = 0; i < NACC; ++i)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[i][e] = 0.f;
+  for (int s = 0; s < S; ++s) {
+    const float* prow = part + ((size_t)s * Mpix + pix) * ld;
+#pragma unroll
+    for (int i = 0; i < NACC; ++i) {
+      const float4 u0 = __ldg(reinterpret_cast<const float4*>(prow + col[i]));
+      const float4 u1 = __ldg(reinterpret_cast<const float4*>(prow + col[i] + 4));
+      acc[i][0] += u0.x; acc[i][1] += u0.y; acc[i][2] += u0.z; acc[i][3] += u0.w;
+      acc[i][4] += u1.x; acc[i][5] += u1.y; acc[i][6] += u1.z; acc[i][7] += u1.w;
+    }
+  }
+  const size_t off = (size_t)pix * Cout + c;
+  uint4 outv[3];
+  uint32_t* p0 = reinterpret_cast<uint32_t*>(&outv[0]);
+  uint32_t* p1 = reinterpret_cast<uint32_t*>(&outv[1]);
+  uint32_t* p2 = reinterpret_cast<uint32_t*>(&outv[2]);
+  if (EPI == EPI_PROPOSED || EPI == EPI_T4) {
+    float y[8], a[8], b[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) {
+      if (EPI == EPI_PROPOSED) {
+        a[e] = acc[0][e] + __ldg(bias0 + c + e);
+        b[e] = acc[1 % NACC][e] + __ldg(bias1 + c + e);
+        y[e] = fmaf(a[e], b[e], acc[2 % NACC][e] + __ldg(bias2 + c + e));
+      } else {
+        a[e] = acc[0][e];
+        b[e] = acc[1 % NACC][e];
+        y[e] = a[e] * b[e];
+      }
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      p0[e] = pack_bf16x2(y[2 * e], y[2 * e + 1]);
+      p1[e] = pack_bf16x2(a[2 * e], a[2 * e + 1]);
+      p2[e] = pack_bf16x2(b[2 * e], b[2 * e + 1]);
+    }
+    *reinterpret_cast<uint4*>(o0 + off) = outv[0];
+    *reinterpret_cast<uint4*>(o1 + off) = outv[1];
+    *reinterpret_cast<uint4*>(o2 + off) = outv[2];
+  } else if (EPI == EPI_PLAIN) {
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = acc[0][e] + (bias0 ? __ldg(bias0 + c + e) : 0.f);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p0[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+    *reinterpret_cast<uint4*>(o0 + off) = outv[0];
+  } else {  // EPI_SQ
+    const uint4 xu = __ldg(reinterpret_cast<const uint4*>(xres + off));
+    const __nv_bfloat162* x2 = reinterpret_cast<const __nv_bfloat162*>(&xu);
+    float v[8];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 xf = __bfloat1622float2(x2[e]);
+      float t0 = acc[0][2 * e] * xf.x, t1 = acc[0][2 * e + 1] * xf.y;
+      v[2 * e] = t0 + t0 + (NB == 2 ? acc[NACC - 1][2 * e] : 0.f);
+      v[2 * e + 1] = t1 + t1 + (NB == 2 ? acc[NACC - 1][2 * e + 1] : 0.f);
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) p0[e] = pack_bf16x2(v[2 * e], v[2 * e + 1]);
+    *reinterpret_cast<uint4*>(o0 + off) = outv[0];
   }
 }
 
@@ -763,10 +891,35 @@ static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
     cudaFuncSetAttribute(conv_gemm_kernel<EPI, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  int grid = args.total_tiles < g_num_sms ? args.total_tiles : g_num_sms;
+  const int nwork = args.total_tiles * args.ksplit;
+  int grid = nwork < g_num_sms ? nwork : g_num_sms;
   conv_gemm_kernel<EPI, NB><<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
   count_launch(st, "conv_gemm");
   return check_launch("conv_gemm");
+}
+
+template <int EPI, int NB>
+static int launch_conv_split(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B,
+                             const CUtensorMap& O0, const CUtensorMap& O1, const CUtensorMap& O2,
+                             const ConvArgs& args, void* o0, void* o1, void* o2, cudaStream_t st) {
+  int rc = launch_conv<EPI, NB>(A0, A1, B, O0, O1, O2, args, st);
+  if (rc || args.ksplit <= 1) return rc;
+  const long long n = args.Mpix * (args.Cout / 8);
+  splitk_finish_kernel<EPI, NB><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      args.part, args.ksplit, args.Mpix, args.part_ld, args.Cout, (bf16*)o0, (bf16*)(o1 ? o1 : o0),
+      (bf16*)(o2 ? o2 : o0), args.bias0, args.bias1, args.bias2, args.xres);
+  count_launch(st, "splitk_finish");
+  return check_launch("splitk_finish");
+}
+
+// K slices for a conv_gemm launch: only when the output grid leaves most SMs idle,
+// each slice >= 8 k-blocks (K 512); QD_NO_SPLITK=1 disables
+static int conv_ksplit(long long tiles, int KB) {
+  const int sms = tc_num_sms();
+  if (getenv("QD_NO_SPLITK") || tiles * 2 > sms) return 1;
+  long long S = sms / tiles;
+  if (S > KB / 8) S = KB / 8;
+  return S < 1 ? 1 : (int)S;
 }
 
 template <int NBLK>
@@ -817,7 +970,8 @@ int tc_wgrad_split(const Plan& P) {
 static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N,
                     int OWg, int OHg, int pad_eff, int r, int dual, const void* wmat, int wrows, int wK,
                     int b_rs_tile, int b_rs_blk, int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2,
-                    int Cout, const float* const bias[3], const void* xres, cudaStream_t st) {
+                    int Cout, const float* const bias[3], const void* xres, cudaStream_t st,
+                    float* skpart = nullptr, size_t skbytes = 0) {
   Box bx = choose_box(OWg, OHg, N, 128, false);
   CUtensorMap A0, A1, B, O0, O1, O2;
   int rc;
@@ -838,15 +992,52 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
   g.b_rs_tile = b_rs_tile; g.b_rs_blk = b_rs_blk; g.out_c_tile = out_c_tile; g.Cout = Cout;
   g.bias0 = bias[0]; g.bias1 = bias[1]; g.bias2 = bias[2];
   g.xres = (const bf16*)xres;
-  if (epi == EPI_PROPOSED) return launch_conv<EPI_PROPOSED, 3>(A0, A1, B, O0, O1, O2, g, st);
-  if (epi == EPI_T4) return launch_conv<EPI_T4, 2>(A0, A1, B, O0, O1, O2, g, st);
-  if (epi == EPI_PLAIN) {
-    if (nbk == 4) return launch_conv<EPI_PLAIN, 4>(A0, A1, B, O0, O1, O2, g, st);
-    if (nbk == 2) return launch_conv<EPI_PLAIN, 2>(A0, A1, B, O0, O1, O2, g, st);
-    return launch_conv<EPI_PLAIN, 1>(A0, A1, B, O0, O1, O2, g, st);
+  const int KB = g.kb_half * (dual ? 2 : 1);
+  g.ksplit = 1;
+  g.kb_per = KB;
+  g.Mpix = (long long)N * OHg * OWg;
+  g.part_ld = tiles_nn * nbk * 64;
+  const int S = conv_ksplit(g.total_tiles, KB);
+  if (S > 1 && skpart && (size_t)S * g.Mpix * g.part_ld * 4 <= skbytes) {
+    g.kb_per = (KB + S - 1) / S;
+    g.ksplit = (KB + g.kb_per - 1) / g.kb_per;
+    g.part = skpart;
   }
-  if (nbk == 2) return launch_conv<EPI_SQ, 2>(A0, A1, B, O0, O1, O2, g, st);
-  return launch_conv<EPI_SQ, 1>(A0, A1, B, O0, O1, O2, g, st);
+#define QD_LC(E, NBV) launch_conv_split<E, NBV>(A0, A1, B, O0, O1, O2, g, o0, o1, o2, st)
+  if (epi == EPI_PROPOSED) return QD_LC(EPI_PROPOSED, 3);
+  if (epi == EPI_T4) return QD_LC(EPI_T4, 2);
+  if (epi == EPI_PLAIN) {
+    if (nbk == 4) return QD_LC(EPI_PLAIN, 4);
+    if (nbk == 2) return QD_LC(EPI_PLAIN, 2);
+    return QD_LC(EPI_PLAIN, 1);
+  }
+  if (nbk == 2) return QD_LC(EPI_SQ, 2);
+  return QD_LC(EPI_SQ, 1);
+#undef QD_LC
+}
+
+// split-K partial bytes the stride-1 v1 fprop / dgrad of P may use (workspace)
+size_t tc_splitk_bytes(const Plan& P) {
+  if (P.s != 1 || P.dtype != QD_BF16) return 0;
+  size_t need = 0;
+  {
+    GemmCfg c = fprop_cfg(P);
+    Box bx = choose_box(P.OW, P.OH, P.N, 128, false);
+    const long long tiles = (long long)bx.tw * bx.th * bx.tn * c.tiles_nn;
+    const int KB = P.r * P.r * (P.C / 64) * (P.sq == 2 ? 2 : 1);
+    const int S = conv_ksplit(tiles, KB);
+    if (S > 1) need = (size_t)S * P.N * P.OH * P.OW * c.tiles_nn * c.nbk * 64 * 4;
+  }
+  {
+    GemmCfg c = dgrad_cfg(P);
+    Box bx = choose_box(P.W, P.H, P.N, 128, false);
+    const long long tiles = (long long)bx.tw * bx.th * bx.tn * c.tiles_nn;
+    const int KB = P.r * P.r * (P.Jd / 64);
+    const int S = conv_ksplit(tiles, KB);
+    const size_t b = S > 1 ? (size_t)S * P.N * P.H * P.W * c.tiles_nn * c.nbk * 64 * 4 : 0;
+    if (b > need) need = b;
+  }
+  return need;
 }
 
 static int plain_blocks(int ch) { return ch % 256 == 0 ? 4 : (ch % 128 == 0 ? 2 : 1); }
@@ -911,13 +1102,15 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
     return run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P1.OW, P1.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
                      P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st, 2);
   }
+  if (dev_skip("fprop")) return QD_OK;
   if (!(P.flags & QD_FLAG_TC_V1)) {
     int rc2 = run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
                         P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st);
     if (rc2 != QD_ERR_UNSUPPORTED) return rc2;
   }
   return run_conv(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
-                  P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st);
+                  P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st,
+                  (float*)(ws + L.off_SK), L.sz_SK);
 }
 
 // side stream for work that can overlap the main chain (one per device/thread pair
@@ -981,7 +1174,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
     bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;
-    launch_pdl(bwd_prologue_vec_kernel, dim3(L.bs_split), dim3(256), 0, st, P0, (const bf16*)dy, (const bf16*)a,
+    if (!dev_skip("prologue")) launch_pdl(bwd_prologue_vec_kernel, dim3(L.bs_split), dim3(256), 0, st, P0, (const bf16*)dy, (const bf16*)a,
                (const bf16*)b, Dw, bpart, rows_per, up ? 1 : 0, P.OH, P.OW, d2 ? 2 * P.F : P.Jd);
     count_launch(st, "prologue");
     if (mat || up) D = Dw;
@@ -1081,7 +1274,8 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     const void* xr = P.sq ? x : nullptr;
     rc = QD_ERR_UNSUPPORTED;
     if (part) set_conv2_cap(dg_pairs);
-    if (!(P.flags & QD_FLAG_TC_V1))
+    if (dev_skip("dgrad")) rc = QD_OK;
+    else if (!(P.flags & QD_FLAG_TC_V1))
       // D is complete once the (PDL-launched) v2/v3 wgrad is running, and nothing
       // the dgrad reads is written by it: the dgrad need not wait for the wgrad
       rc = run_conv2(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
@@ -1091,7 +1285,8 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if (d2 && rc == QD_ERR_UNSUPPORTED) return set_error(QD_ERR_UNSUPPORTED, "dgrad conv2 plan changed");
     if (rc == QD_ERR_UNSUPPORTED && !up)
       rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
-                    c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st);
+                    c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st,
+                    (float*)(ws + L.off_SK), L.sz_SK);
     if (rc) return rc;
   }
   if (side) join_side(st, side);

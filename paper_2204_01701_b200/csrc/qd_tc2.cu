@@ -1261,6 +1261,7 @@ struct W3Args {
   int pe, Wp, RD, RX;
   int T_img, cblks, ablocks, jtiles, nsplit;
   int NT, ntb;
+  int R, ksteps;  // a q block = R whole rows of the padded grid (R Wp positions), ksteps x 16 MMA K
   uint32_t d_tx, x_tx, d_bytes, x_bytes;
   int stages;
   int jsplit;
@@ -1330,6 +1331,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ptx::tmem_alloc(tslot, 512);
     ptx::tmem_relinquish();
   }
+  {
+    // the slot tails past each box (K padding to 16 positions; the x rows the
+    // last K step may touch) are never written by TMA: zero them once. They
+    // only ever meet zero D / finite x, so they add nothing.
+    const uint32_t d_box = (uint32_t)g.RD * g.Wp * 128, x_box = (uint32_t)g.RX * g.Wp * 128;
+    for (int s = 0; s < g.stages; ++s) {
+      uint8_t* base = sm + s * stage_bytes;
+      for (int i = 0; i <= g.ntb; ++i) {
+        uint8_t* slot = base + i * g.d_bytes;
+        const uint32_t lo = i < g.ntb ? d_box : x_box, hi = i < g.ntb ? g.d_bytes : g.x_bytes;
+        for (uint32_t o = lo + 16 * threadIdx.x; o < hi; o += 16 * blockDim.x)
+          *(uint4*)(slot + o) = make_uint4(0, 0, 0, 0);
+      }
+    }
+    ptx::fence_proxy_async_smem();
+  }
   ptx::tc_fence_before();
   c2::cluster_sync();  // barriers of both CTAs initialised before any multicast lands
   ptx::tc_fence_after();
@@ -1345,7 +1362,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     const int nsh = (g.ntb + 1) / 2;
     for (int qb = q_beg; qb < q_end; ++qb) {
       int n = qb / g.T_img, t = qb % g.T_img;
-      int hq_lo = (128 * t) / g.Wp;
+      int hq_lo = g.R * t;
       if (leader) C2_TRACE(0, qb - q_beg, 0);
       ptx::mbar_wait(&empty[st], ph ^ 1);
       if (leader) {
@@ -1384,36 +1401,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     int st = 0;
     uint32_t ph = 0;
     uint32_t accum = 0;
+    const int ks = g.ksteps;
     for (int qb = q_beg; qb < q_end; ++qb) {
-      int t = qb % g.T_img;
-      int q0 = 128 * t;
-      int row_off = q0 - (q0 / g.Wp) * g.Wp;
       if (leader) C2_TRACE(1, qb - q_beg, 0);
       ptx::mbar_wait(&full[st], ph);
       if (leader) C2_TRACE(1, qb - q_beg, 1);
       ptx::tc_fence_after();
       const uint32_t base = s_lo0 + st * (stage_bytes >> 4);
-      const uint32_t d_lo = base + row_off * 8 + d_lbo;
-      const uint32_t x_lo = base + ((g.ntb * g.d_bytes) >> 4) + row_off * 8;
+      const uint32_t d_lo = base + d_lbo;
+      const uint32_t x_lo = base + ((g.ntb * g.d_bytes) >> 4);
       if (leader) {
 #pragma unroll
         for (int pr = 0; pr < 2; ++pr) {
           const int o0 = off[2 * pr], o1 = off[2 * pr + 1];
           const uint32_t a_lo = x_lo + o0 * 8 + ((uint32_t)((o1 - o0) * 8) << 16);
           const uint32_t dt = tmem + pr * g.NT;
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
+#pragma unroll 4
+          for (int k = 0; k < ks; ++k)
             ptx::mma_bf16(dt, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, d_lo + 128 * k), IDESC,
-                          accum | (uint32_t)k);
+                          accum | (uint32_t)(k > 0));
         }
         if (nhi > nlo) {
           const uint32_t a_lo = x_lo + off8 * 8;  // both 64-row atoms: tap 8 (second discarded)
           const uint32_t b_lo = d_lo + nlo * (g.d_bytes >> 4);
           const uint32_t dt = tmem + 2 * g.NT;
-#pragma unroll
-          for (int k = 0; k < 8; ++k)
+#pragma unroll 4
+          for (int k = 0; k < ks; ++k)
             ptx::mma_bf16(dt, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, b_lo + 128 * k), IDESC9,
-                          accum | (uint32_t)k);
+                          accum | (uint32_t)(k > 0));
         }
         w3_commit_mc(&empty[st]);
         C2_TRACE(1, qb - q_beg, 2);
@@ -1498,28 +1513,39 @@ static W3Plan w3_plan(const Plan& P) {
   if (P.s != 1 || P.r != 3 || P.C % 64 || P.Jd % 64) return pl;
   int Wp = P.W + 2 * P.p;
   if (P.OW != Wp - P.r + 1 || Wp > 256 || P.OW < 12) return pl;
-  int T_img = (P.OH * Wp + 127) / 128;
-  int RD = 0, RX = 0;
-  for (int t = 0; t < T_img; ++t) {
-    int q0 = 128 * t, lo = q0 / Wp;
-    int hd = (q0 + 127) / Wp, hx = (q0 + 127 + (P.r - 1) * (Wp + 1)) / Wp;
-    if (hd - lo + 1 > RD) RD = hd - lo + 1;
-    if (hx - lo + 1 > RX) RX = hx - lo + 1;
-  }
-  if (RX > 256) return pl;
-  uint32_t d_tx = (uint32_t)Wp * RD * 128, x_tx = (uint32_t)Wp * RX * 128;
-  uint32_t d_bytes = (d_tx + 1023) / 1024 * 1024, x_bytes = (x_tx + 1023) / 1024 * 1024;
-  int ntb = 0, stages = 0;
-  for (int c = 3; c >= 1; --c) {  // 2 NT + ceil(c/2) 64 <= 512
+  // q blocks of R whole rows: the D box is exactly the block (no row overfetch)
+  // and K = R Wp padded to 16. Pick R by MMA efficiency (positions computed /
+  // positions issued, incl. the rows past OH of the last block), then by bytes
+  // staged per position, with at least 2 stages.
+  int ntb = 0, stages = 0, R = 0, ksteps = 0;
+  uint32_t d_tx = 0, x_tx = 0, d_bytes = 0, x_bytes = 0;
+  for (int c = 3; c >= 1 && !ntb; --c) {  // 2 NT + ceil(c/2) 64 <= 512
     if ((P.Jd / 64) % c) continue;
-    uint32_t stg = c * d_bytes + x_bytes;
-    int sn = (int)((212 * 1024) / stg);
-    if (sn >= 2) { ntb = c; stages = sn > 4 ? 4 : sn; break; }
+    double best = 0.0;
+    const int rpin = getenv("QD_W3_R") ? atoi(getenv("QD_W3_R")) : 0;  // dev: pin R
+    for (int rr = 1; rr <= P.OH && rr + P.r - 1 <= 256; ++rr) {
+      const int kst = (rr * Wp + 15) / 16;
+      const uint32_t db = (uint32_t)kst * 16 * 128;  // multiple of 2048
+      const uint32_t xb = ((uint32_t)(kst * 16 + (P.r - 1) * (Wp + 1)) * 128 + 1023) / 1024 * 1024;
+      const uint32_t stg = c * db + xb;
+      const int sn = (int)((212 * 1024) / stg);
+      if (sn < 2) break;
+      const int tb = (P.OH + rr - 1) / rr;
+      const double eff = (double)P.OH * Wp / ((double)tb * kst * 16);
+      const double score = rpin ? (rr == rpin ? 1.0 : 0.0) : eff - 1e-7 * stg / (rr * Wp);
+      if (score > best) {
+        best = score;
+        ntb = c; stages = sn > 4 ? 4 : sn; R = rr; ksteps = kst;
+        d_tx = (uint32_t)Wp * rr * 128; x_tx = (uint32_t)Wp * (rr + P.r - 1) * 128;
+        d_bytes = db; x_bytes = xb;
+      }
+    }
   }
+  const int RD = R, RX = R + P.r - 1, T_img = R ? (P.OH + R - 1) / R : 0;
   // narrow N tiles (wide images) re-read x per j tile and run N = 64 MMAs: wgrad2 is better there
   if (ntb < 2) return pl;
   g.N = P.N; g.OHg = P.OH; g.OWg = P.OW; g.Jd = P.Jd; g.Kf = P.Kf; g.K0 = P.K0; g.C = P.C;
-  g.pe = P.p; g.Wp = Wp; g.RD = RD; g.RX = RX;
+  g.pe = P.p; g.Wp = Wp; g.RD = RD; g.RX = RX; g.R = R; g.ksteps = ksteps;
   g.T_img = T_img; g.cblks = P.C / 64; g.ablocks = g.cblks * (P.sq == 2 ? 2 : 1);
   g.NT = ntb * 64; g.ntb = ntb; g.jtiles = P.Jd / g.NT;
   const int nblk = P.N * T_img;
@@ -1556,6 +1582,7 @@ int wgrad3_pairs_per_split(const Plan& P) {
 
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail, int jsplit) {
+  if (dev_skip("wgrad")) return QD_OK;
   W3Plan pl = w3_plan(P);
   // splits < the plan's: a partitioned launch sharing the SMs with a concurrent kernel
   if (!pl.ok || splits < 1 || splits > pl.g.nsplit) return QD_ERR_UNSUPPORTED;

@@ -176,6 +176,51 @@ def test_pair_halo_kernel_matches_v1(case):
         assert Q.rel_err(r2[3][role], r1[3][role]) <= 1e-2, role
 
 
+# small output grids on the v1 kernels: the K loop is split across CTAs into fp32
+# partials that splitk_finish folds and runs the epilogue on
+SPLITK_CASES = [
+    ("proposed", "conv", 2, 128, 128, 4, 4, 3, 1, 1),
+    ("proposed", "conv", 4, 256, 256, 2, 2, 3, 1, 1),
+    ("t4", "conv", 2, 128, 64, 4, 4, 3, 1, 1),
+    ("t2", "conv", 2, 128, 128, 4, 4, 3, 1, 1),
+    ("t2_linear", "conv", 2, 128, 64, 4, 4, 3, 1, 1),
+    ("first_order", "conv", 2, 256, 256, 3, 3, 3, 1, 1),
+    ("proposed", "fc", 64, 1024, 256, 1, 1, 1, 1, 0),
+]
+
+
+def _kernel_names(fn):
+    from paper_2204_01701_b200 import _lib
+    lib = _lib.load()
+    torch.cuda.synchronize()
+    lib.qd_profile(1)
+    try:
+        out = fn()
+        torch.cuda.synchronize()
+        names = [n for n, _ in _lib.profile_read()]
+    finally:
+        lib.qd_profile(0)
+    return out, names
+
+
+@pytest.mark.parametrize("case", SPLITK_CASES, ids=str)
+def test_splitk_v1_parity(case, monkeypatch):
+    fam, kind, n, c, f, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, kind, n, c, f, h, w, k, s, p, seed=17, random_bias=True)
+    xq, gq = _q(x, torch.bfloat16), _q(g, torch.bfloat16)
+    path, names = _kernel_names(lambda: check_against_oracle(fam, kind, x, P, g, torch.bfloat16, k, s, p))
+    assert path == 1
+    assert "splitk_finish" in names, names
+    r_split = run_device(fam, kind, xq, P, gq, torch.bfloat16, k, s, p)
+    monkeypatch.setenv("QD_NO_SPLITK", "1")
+    r_whole, names1 = _kernel_names(lambda: run_device(fam, kind, xq, P, gq, torch.bfloat16, k, s, p))
+    assert "splitk_finish" not in names1
+    for i in (0, 4):
+        assert Q.rel_err(r_split[i], r_whole[i]) <= 1e-2, i
+    for role in r_whole[3]:
+        assert Q.rel_err(r_split[3][role], r_whole[3][role]) <= 1e-2, role
+
+
 def test_c1_fc_fp32():
     """BASELINE config 1: fc 256x512->512, fp32, Kaiming-uniform, b=0."""
     x, P, g = Q.synthetic_layer("proposed", "fc", 256, 512, 512, seed=0)
@@ -309,7 +354,8 @@ def test_t1_parity(fam, n, c, dtype):
 @pytest.mark.gpu
 @pytest.mark.parametrize("family,kind,c,f,k", [("proposed", "conv", 64, 64, 3), ("t4", "conv", 64, 128, 3),
                                                ("t2_linear", "conv", 64, 64, 3), ("t2and4", "conv", 64, 64, 3),
-                                               ("proposed", "fc", 96, 64, 1), ("first_order", "conv", 8, 16, 3)])
+                                               ("proposed", "fc", 96, 64, 1), ("first_order", "conv", 8, 16, 3),
+                                               ("proposed", "conv", 40, 72, 5), ("t4", "fc", 100, 36, 1)])
 def test_quad_sgd_matches_torch_sgd_and_repack(family, kind, c, f, k):
     from paper_2204_01701_b200 import neurons
     from paper_2204_01701_b200.nn import QuadConv2d, QuadLinear

@@ -41,3 +41,14 @@ if (Dn > 0).all():
     main = (Dn - G[:, 0]) / 1e3
     print(f"main loop min/med/max {main.min():.1f}/{np.median(main):.1f}/{main.max():.1f} us, "
           f"epilogue min/med/max {epi.min():.1f}/{np.median(epi):.1f}/{epi.max():.1f} us")
+T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
+t0 = T[T > 0].min()
+print("CTA0 per q block (cycles from first event): prod[acq empty] mma[full acquired, issued]")
+prev = None
+for blk in range(64):
+    pe, m1, m2 = T[0, blk, 1], T[1, blk, 1], T[1, blk, 2]
+    if m2 == 0:
+        break
+    d = "" if prev is None else f" period {m1 - prev}"
+    print(f"  blk {blk:2d}: prod {pe - t0:6d}  mma full@{m1 - t0:6d} issued@{m2 - t0:6d} (issue {m2 - m1}){d}")
+    prev = m1
