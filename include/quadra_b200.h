@@ -128,6 +128,17 @@ int qd_bn_backward_D(const qd_desc* d, const void* dz, const void* y, const void
 int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const float* const grad[3],
                 float lr, float momentum, float weight_decay, int first, void* wpack, void* stream);
 
+/* Max pooling around the quadratic layers in the QuadraNet training step
+ * (QuadraVGG 2x2/2, QuadraResNet stem 3x3/2 pad 1), torch.nn.MaxPool2d
+ * semantics (floor mode, -inf padding, first maximum wins, NaN propagates).
+ * NHWC, C % 8 == 0. argmax: one byte per output element (window offset
+ * ky*k + kx), written by the forward and read by the backward, which gathers
+ * (no atomics: deterministic) and writes every element of dx. */
+int qd_maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* x, void* y,
+                       void* argmax, void* stream);
+int qd_maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* dy,
+                        const void* argmax, void* dx, void* stream);
+
 /* Forward: neurons.forward (neurons.py:235-276).
  * bias[i]: fp32 (F) per role (proposed ba, bb, bc; first_order b; else NULL).
  * y: output NHWC; a_cache/b_cache: the LayerCache a, b (proposed/t4, NHWC,

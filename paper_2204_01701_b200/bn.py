@@ -214,3 +214,32 @@ class QuadConvBN(nn.Module):
         z = _ref_batchnorm(y, self.weight, self.bias, self.bn.running_mean, self.bn.running_var, self.bn.momentum,
                            self.bn.eps, self.training)
         return torch.relu(z) if self.relu else z
+
+
+class BNAct2d(nn.BatchNorm2d):
+    """nn.BatchNorm2d (+ fused ReLU) on the library's BN kernels, for the
+    first-order parts of the QuadraNets (ResNet stem, downsample shortcuts).
+
+    Same parameters, buffers and state-dict keys as nn.BatchNorm2d; statistics
+    follow the reference (tensor.py:423-470): biased batch variance, also in the
+    running update. CUDA channels_last / 2-D inputs run ``_BNFunction``; other
+    devices (CPU inspection, meta-device FLOP counting) use the torch ops with
+    the same semantics."""
+
+    def __init__(self, num_features, relu=False, eps=1e-5, momentum=0.1, device=None, dtype=None):
+        super().__init__(num_features, eps=eps, momentum=momentum, device=device, dtype=dtype)
+        self.relu = bool(relu)
+
+    def forward(self, x):
+        if self.training:
+            self.num_batches_tracked.add_(1)
+        if x.device.type == "cuda" and (x.dim() == 2 or x.is_contiguous(memory_format=torch.channels_last)):
+            if self.training:
+                return _BNFunction.apply(x, self.weight, self.bias, self, self.relu)
+            # eval: running statistics through the same apply kernel
+            z, _, _ = bn_forward(x, self.weight, self.bias, self.running_mean, self.running_var, self.momentum,
+                                 self.eps, self.relu, False)
+            return z
+        z = _ref_batchnorm(x, self.weight, self.bias, self.running_mean, self.running_var, self.momentum, self.eps,
+                           self.training)
+        return torch.relu(z) if self.relu else z

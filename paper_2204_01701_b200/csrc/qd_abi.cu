@@ -269,6 +269,20 @@ int qd_bn_backward_D(const qd_desc* d, const void* dz, const void* y, const void
                        (cudaStream_t)stream);
 }
 
+int qd_maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* x, void* y,
+                       void* argmax, void* stream) {
+  if (dtype != QD_F32 && dtype != QD_BF16) return set_error(QD_ERR_CONFIG, "unknown dtype %d", dtype);
+  if (!x || !y || !argmax) return set_error(QD_ERR_ARG, "qd_maxpool_forward: NULL argument");
+  return maxpool_forward(N, C, H, W, k, s, p, dtype, x, y, argmax, (cudaStream_t)stream);
+}
+
+int qd_maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* dy,
+                        const void* argmax, void* dx, void* stream) {
+  if (dtype != QD_F32 && dtype != QD_BF16) return set_error(QD_ERR_CONFIG, "unknown dtype %d", dtype);
+  if (!dy || !dx || !argmax) return set_error(QD_ERR_ARG, "qd_maxpool_backward: NULL argument");
+  return maxpool_backward(N, C, H, W, k, s, p, dtype, dy, argmax, dx, (cudaStream_t)stream);
+}
+
 int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const float* const grad[3],
                 float lr, float momentum, float weight_decay, int first, void* wpack, void* stream) {
   int st = validate(d);

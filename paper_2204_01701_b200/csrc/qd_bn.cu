@@ -303,17 +303,43 @@ __global__ void __launch_bounds__(256) bn_reduce_kernel(long long M, int C, cons
   }
 }
 
-template <typename T>
-__global__ void bn_stats_finalize(long long M, int C, int S, const T* y, const float* part, float eps,
-                                  float momentum, int training, float* run_mean, float* run_var, float* save_mean,
-                                  float* save_invstd) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  float s1 = 0.f, s2 = 0.f;
-  for (int s = 0; s < S; ++s) {
-    s1 += part[((size_t)s * 2 + 0) * C + c];
-    s2 += part[((size_t)s * 2 + 1) * C + c];
+// fold the S x (2, C) partials: block = 32 channels x both sums (64 columns) x 16
+// split groups; group g sums splits g, g+16, ... in order, then one thread per
+// column adds the 16 group totals in order (deterministic, ~S/16 loads deep)
+__device__ __forceinline__ bool bn_fold2(int C, int S, const float* part, float& s1, float& s2) {
+  __shared__ float red[16][65];
+  const int col = threadIdx.x % 64, grp = threadIdx.x / 64;
+  const int k = col / 32, c = blockIdx.x * 32 + col % 32;
+  float a0 = 0.f, a1 = 0.f;
+  if (c < C) {
+    const float* p = part + (size_t)k * C + c;
+    const size_t step = (size_t)2 * C;
+    int sp = grp;
+    for (; sp + 16 < S; sp += 32) {
+      a0 += p[(size_t)sp * step];
+      a1 += p[(size_t)(sp + 16) * step];
+    }
+    if (sp < S) a0 += p[(size_t)sp * step];
   }
+  red[grp][col] = a0 + a1;
+  __syncthreads();
+  if (grp != 0 || col >= 32 || c >= C) return false;
+  s1 = 0.f;
+  s2 = 0.f;
+  for (int g = 0; g < 16; ++g) {
+    s1 += red[g][col];
+    s2 += red[g][col + 32];
+  }
+  return true;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(1024) bn_stats_finalize(long long M, int C, int S, const T* y, const float* part,
+                                                          float eps, float momentum, int training, float* run_mean,
+                                                          float* run_var, float* save_mean, float* save_invstd) {
+  float s1, s2;
+  if (!bn_fold2(C, S, part, s1, s2)) return;
+  const int c = blockIdx.x * 32 + threadIdx.x;
   const float inv_m = 1.f / (float)M;
   const float dm = s1 * inv_m;
   float var = s2 * inv_m - dm * dm;  // biased (tensor.py:444)
@@ -339,14 +365,11 @@ __global__ void bn_apply_kernel(long long n, int C, const T* y, const float* mea
   }
 }
 
-__global__ void bn_grad_finalize(int C, int S, const float* part, float* dgamma, float* dbeta) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= C) return;
-  float s1 = 0.f, s2 = 0.f;
-  for (int s = 0; s < S; ++s) {
-    s1 += part[((size_t)s * 2 + 0) * C + c];
-    s2 += part[((size_t)s * 2 + 1) * C + c];
-  }
+__global__ void __launch_bounds__(1024) bn_grad_finalize(int C, int S, const float* part, float* dgamma,
+                                                          float* dbeta) {
+  float s1, s2;
+  if (!bn_fold2(C, S, part, s1, s2)) return;
+  const int c = blockIdx.x * 32 + threadIdx.x;
   dbeta[c] = s1;
   dgamma[c] = s2;
 }
@@ -435,7 +458,7 @@ static int bn_forward_t(long long M, int C, const T* y, const float* gamma, cons
     else
       bn_reduce_kernel<T, 0><<<S, 256, 0, st>>>(M, C, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, part);
     count_launch(st, "bn_stats");
-    bn_stats_finalize<T><<<(C + 127) / 128, 128, 0, st>>>(M, C, S, y, part, eps, momentum, 1, rm, rv, sm, si);
+    bn_stats_finalize<T><<<(C + 31) / 32, 1024, 0, st>>>(M, C, S, y, part, eps, momentum, 1, rm, rv, sm, si);
     count_launch(st, "bn_stats_finalize");
   }
   const long long n = M * C;
@@ -462,7 +485,7 @@ static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, c
   else
     bn_reduce_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
   count_launch(st, "bn_bwd_reduce");
-  bn_grad_finalize<<<(C + 127) / 128, 128, 0, st>>>(C, S, part, dgamma, dbeta);
+  bn_grad_finalize<<<(C + 31) / 32, 1024, 0, st>>>(C, S, part, dgamma, dbeta);
   count_launch(st, "bn_bwd_finalize");
   if (bn_vec(C))
     bn_emit_D_vec_kernel<T><<<S, 256, 0, st>>>(P, dz, y, a, b, sm, si, gamma, beta, dgamma, dbeta, relu, D, bpart);

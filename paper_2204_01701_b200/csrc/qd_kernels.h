@@ -144,6 +144,10 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
 // v3 wgrad (r = 3) on CTA pairs with multicast stage loads; 0 when not eligible
 void set_conv2_cap(int pairs);
 bool dev_skip(const char* name);
+int maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* x, void* y, void* arg,
+                    cudaStream_t st);
+int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* dy, const void* arg,
+                     void* dx, cudaStream_t st);
 int wgrad3_pairs_per_split(const Plan& P);
 int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,

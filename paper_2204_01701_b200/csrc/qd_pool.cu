@@ -1,0 +1,187 @@
+// Max pooling (NHWC) for the QuadraNet training step around the quadratic
+// layers: the ResNet stem pool (3x3/2, pad 1) and the VGG 2x2/2 pools.
+//
+// Forward: one thread per (output pixel, 8 channels) takes the window max in
+// scan order (ky, kx) with torch.nn.MaxPool2d's rule (first maximum wins, NaN
+// propagates) and records the winning window offset in one byte per channel.
+// Backward is a gather, not a scatter: one thread per (input pixel, 8 channels)
+// sums, in a fixed window order, the output gradients whose recorded offset
+// points at it -- no atomics, deterministic, every store coalesced.
+#include <stdint.h>
+#include <string.h>
+
+#include "qd_kernels.h"
+
+namespace qd {
+
+template <typename T> struct PV;
+template <> struct PV<bf16> {
+  __device__ static void ld8(const bf16* p, float v[8]) {
+    const uint4 u = __ldg(reinterpret_cast<const uint4*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float2 f = __bfloat1622float2(h[e]);
+      v[2 * e] = f.x;
+      v[2 * e + 1] = f.y;
+    }
+  }
+  __device__ static void st8(bf16* p, const float v[8]) {
+    uint4 u;
+    uint32_t* w = reinterpret_cast<uint32_t*>(&u);
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+      w[e] = *reinterpret_cast<const uint32_t*>(&h);
+    }
+    *reinterpret_cast<uint4*>(p) = u;
+  }
+};
+template <> struct PV<float> {
+  __device__ static void ld8(const float* p, float v[8]) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+    v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ static void st8(float* p, const float v[8]) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v[4], v[5], v[6], v[7]);
+  }
+};
+
+struct PoolGeo {
+  int N, C, H, W, OH, OW, k, s, p;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __restrict__ x, T* __restrict__ y,
+                                                          uint8_t* __restrict__ arg) {
+  const int c8 = g.C / 8;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)g.N * g.OH * g.OW * c8) return;
+  const int cq = (int)(i % c8);
+  long long t = i / c8;
+  const int ow = (int)(t % g.OW);
+  t /= g.OW;
+  const int oh = (int)(t % g.OH);
+  const int n = (int)(t / g.OH);
+  const int h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
+  // torch's initial index: the window's first in-bounds position
+  const uint8_t first = (uint8_t)((h0 < 0 ? -h0 : 0) * g.k + (w0 < 0 ? -w0 : 0));
+  float best[8];
+  uint8_t bi[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    best[e] = -__int_as_float(0x7f800000);  // -inf: padding never wins
+    bi[e] = first;
+  }
+  for (int ky = 0; ky < g.k; ++ky) {
+    const int h = h0 + ky;
+    if (h < 0 || h >= g.H) continue;
+    for (int kx = 0; kx < g.k; ++kx) {
+      const int w = w0 + kx;
+      if (w < 0 || w >= g.W) continue;
+      float v[8];
+      PV<T>::ld8(x + (((size_t)n * g.H + h) * g.W + w) * g.C + cq * 8, v);
+      const uint8_t o = (uint8_t)(ky * g.k + kx);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (v[e] > best[e] || v[e] != v[e]) {  // torch's rule: first maximum, a NaN always takes over
+          best[e] = v[e];
+          bi[e] = o;
+        }
+    }
+  }
+  const size_t oidx = (size_t)i * 8;
+  PV<T>::st8(y + oidx, best);
+  uint2 packed;
+  packed.x = bi[0] | (bi[1] << 8) | (bi[2] << 16) | ((uint32_t)bi[3] << 24);
+  packed.y = bi[4] | (bi[5] << 8) | (bi[6] << 16) | ((uint32_t)bi[7] << 24);
+  *reinterpret_cast<uint2*>(arg + oidx) = packed;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_bwd_kernel(PoolGeo g, const T* __restrict__ dy,
+                                                          const uint8_t* __restrict__ arg, T* __restrict__ dx) {
+  const int c8 = g.C / 8;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)g.N * g.H * g.W * c8) return;
+  const int cq = (int)(i % c8);
+  long long t = i / c8;
+  const int w = (int)(t % g.W);
+  t /= g.W;
+  const int h = (int)(t % g.H);
+  const int n = (int)(t / g.H);
+  // windows (oh, ow) with oh*s - p <= h <= oh*s - p + k - 1
+  int oh_lo = (h + g.p - g.k + g.s) / g.s, oh_hi = (h + g.p) / g.s;  // h + p - k + 1 >= 0 ? ceil : 0
+  if (h + g.p - g.k + 1 < 0) oh_lo = 0;
+  int ow_lo = (w + g.p - g.k + g.s) / g.s, ow_hi = (w + g.p) / g.s;
+  if (w + g.p - g.k + 1 < 0) ow_lo = 0;
+  if (oh_hi >= g.OH) oh_hi = g.OH - 1;
+  if (ow_hi >= g.OW) ow_hi = g.OW - 1;
+  float acc[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) acc[e] = 0.f;
+  for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+    const int ky = h - (oh * g.s - g.p);
+    for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+      const int kx = w - (ow * g.s - g.p);
+      const uint8_t o = (uint8_t)(ky * g.k + kx);
+      const size_t oidx = ((((size_t)n * g.OH + oh) * g.OW + ow) * g.C) + cq * 8;
+      const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + oidx));
+      const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
+      bool any = false;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) any |= ab[e] == o;
+      if (!any) continue;
+      float v[8];
+      PV<T>::ld8(dy + oidx, v);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (ab[e] == o) acc[e] += v[e];
+    }
+  }
+  PV<T>::st8(dx + (size_t)i * 8, acc);
+}
+
+static int pool_geo(int N, int C, int H, int W, int k, int s, int p, PoolGeo& g) {
+  if (N < 1 || C < 8 || C % 8 || H < 1 || W < 1) return set_error(QD_ERR_DIM, "maxpool: N %d C %d H %d W %d", N, C, H, W);
+  if (k < 1 || k > 15 || s < 1 || p < 0 || 2 * p > k) return set_error(QD_ERR_CONFIG, "maxpool: k %d s %d p %d", k, s, p);
+  g.N = N; g.C = C; g.H = H; g.W = W; g.k = k; g.s = s; g.p = p;
+  g.OH = (H + 2 * p - k) / s + 1;
+  g.OW = (W + 2 * p - k) / s + 1;
+  if (g.OH < 1 || g.OW < 1) return set_error(QD_ERR_DIM, "maxpool: empty output");
+  return QD_OK;
+}
+
+int maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* x, void* y, void* arg,
+                    cudaStream_t st) {
+  PoolGeo g;
+  int rc = pool_geo(N, C, H, W, k, s, p, g);
+  if (rc) return rc;
+  const long long n = (long long)N * g.OH * g.OW * (C / 8);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (dtype == QD_BF16)
+    maxpool_fwd_kernel<bf16><<<blocks, 256, 0, st>>>(g, (const bf16*)x, (bf16*)y, (uint8_t*)arg);
+  else
+    maxpool_fwd_kernel<float><<<blocks, 256, 0, st>>>(g, (const float*)x, (float*)y, (uint8_t*)arg);
+  count_launch(st, "maxpool_fwd");
+  return check_launch("maxpool forward");
+}
+
+int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* dy, const void* arg,
+                     void* dx, cudaStream_t st) {
+  PoolGeo g;
+  int rc = pool_geo(N, C, H, W, k, s, p, g);
+  if (rc) return rc;
+  const long long n = (long long)N * H * W * (C / 8);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (dtype == QD_BF16)
+    maxpool_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(g, (const bf16*)dy, (const uint8_t*)arg, (bf16*)dx);
+  else
+    maxpool_bwd_kernel<float><<<blocks, 256, 0, st>>>(g, (const float*)dy, (const uint8_t*)arg, (float*)dx);
+  count_launch(st, "maxpool_bwd");
+  return check_launch("maxpool backward");
+}
+
+}  // namespace qd

@@ -26,8 +26,9 @@ import torch
 import torch.nn.functional as Fnn
 from torch import nn
 
-from .bn import QuadConvBN
+from .bn import BNAct2d, QuadConvBN
 from .nn import QuadConv2d
+from .pool import MaxPool2d
 
 
 class PaddedQuadConv2d(nn.Module):
@@ -74,9 +75,9 @@ class QuadraVGG16(nn.Module):
         cin = 3
         for v in VGG16_CFG:
             if v == "M":
-                layers.append(nn.MaxPool2d(2, 2))
-            elif cin % 64:  # zero-padded stem: quad conv, then torch BN + ReLU
-                layers += [quad_conv(cin, v, 3, 1, 1, family), nn.BatchNorm2d(v), nn.ReLU(inplace=True)]
+                layers.append(MaxPool2d(2, 2))
+            elif cin % 64:  # zero-padded stem: quad conv, then BN + ReLU (one node; Identity keeps indices)
+                layers += [quad_conv(cin, v, 3, 1, 1, family), BNAct2d(v, relu=True), nn.Identity()]
                 cin = v
             else:  # quad conv -> BN -> ReLU as one fused node (bn.QuadConvBN)
                 layers.append(QuadConvBN(QuadConv2d(cin, v, 3, 1, 1, family), relu=True))
@@ -100,8 +101,7 @@ class QuadBasicBlock(nn.Module):
         self.relu = nn.ReLU(inplace=True)
         self.down = None
         if stride != 1 or inplanes != planes:
-            self.down = nn.Sequential(nn.Conv2d(inplanes, planes, 1, stride, bias=False),
-                                      nn.BatchNorm2d(planes))
+            self.down = nn.Sequential(nn.Conv2d(inplanes, planes, 1, stride, bias=False), BNAct2d(planes))
 
     def forward(self, x):
         idt = x if self.down is None else self.down(x)
@@ -112,8 +112,9 @@ class QuadBasicBlock(nn.Module):
 class QuadraResNet18(nn.Module):
     def __init__(self, num_classes=1000, family="proposed"):
         super().__init__()
-        self.stem = nn.Sequential(nn.Conv2d(3, 64, 7, 2, 3, bias=False), nn.BatchNorm2d(64),
-                                  nn.ReLU(inplace=True), nn.MaxPool2d(3, 2, 1))
+        # first-order stem; BN + ReLU as one node on the library kernels (Identity keeps indices)
+        self.stem = nn.Sequential(nn.Conv2d(3, 64, 7, 2, 3, bias=False), BNAct2d(64, relu=True), nn.Identity(),
+                                  MaxPool2d(3, 2, 1))
         blocks = []
         inplanes = 64
         for planes, stride in ((64, 1), (128, 2), (256, 2), (512, 2)):

@@ -509,3 +509,56 @@ def test_memory_ledger_accounts_minimal_cache():
         # + batch statistics and allocator rounding (under one extra tensor in any run order)
         assert 4 * ob <= got < 5 * ob, (name, got, ob)
         assert led.per_layer_auto[name] >= 4 * ob, (name, led.per_layer_auto[name], ob)
+
+
+# first-order pieces of the QuadraNet step on the library kernels
+@pytest.mark.gpu
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("geo", [(3, 2, 1, 2, 64, 23, 17), (2, 2, 0, 3, 16, 8, 8), (3, 1, 1, 1, 8, 5, 6),
+                                 (2, 2, 0, 2, 512, 3, 5)])
+def test_maxpool_matches_torch(geo, dtype):
+    from paper_2204_01701_b200.pool import MaxPool2d
+    k, s, p, n, c, h, w = geo
+    g = torch.Generator(device="cuda").manual_seed(5)
+    x = torch.randn(n, c, h, w, device="cuda", generator=g).to(dtype).contiguous(memory_format=torch.channels_last)
+    x[0, :, 0, 0] = x[0, :, 0, 1]  # ties: the first maximum in scan order wins
+    x1 = x.clone().requires_grad_(True)
+    x2 = x.clone().requires_grad_(True)
+    y1 = MaxPool2d(k, s, p)(x1)
+    y2 = torch.nn.functional.max_pool2d(x2, k, s, p)
+    assert torch.equal(y1, y2)
+    gy = torch.randn(y1.shape, device="cuda", generator=g).to(dtype)
+    y1.backward(gy)
+    y2.backward(gy)
+    tol = 1e-2 if dtype == torch.bfloat16 else 1e-6
+    assert Q.rel_err(x1.grad.double().cpu().numpy(), x2.grad.double().cpu().numpy()) <= tol
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("relu", [False, True])
+def test_bnact_matches_reference_bn(relu):
+    from paper_2204_01701_b200.bn import BNAct2d, _ref_batchnorm
+    g = torch.Generator(device="cuda").manual_seed(6)
+    x = (torch.randn(4, 64, 9, 11, device="cuda", generator=g) * 2 + 0.5).to(torch.bfloat16)
+    x = x.contiguous(memory_format=torch.channels_last)
+    m = BNAct2d(64, relu=relu).cuda()
+    with torch.no_grad():
+        m.weight.uniform_(0.5, 1.5, generator=g)
+        m.bias.uniform_(-0.5, 0.5, generator=g)
+    ref_rm, ref_rv = m.running_mean.clone(), m.running_var.clone()
+    x1 = x.clone().requires_grad_(True)
+    z = m(x1)
+    x2 = x.float().clone().requires_grad_(True)
+    w2, b2 = m.weight.detach().clone().requires_grad_(True), m.bias.detach().clone().requires_grad_(True)
+    z2 = _ref_batchnorm(x2, w2, b2, ref_rm, ref_rv, 0.1, 1e-5, True)
+    z2 = torch.relu(z2) if relu else z2
+    assert Q.rel_err(z.detach().double().cpu().numpy(), z2.detach().double().cpu().numpy()) <= 2e-2
+    assert torch.allclose(m.running_mean, ref_rm, rtol=1e-4, atol=1e-5)
+    assert torch.allclose(m.running_var, ref_rv, rtol=1e-4, atol=1e-5)  # biased variance (tensor.py:444)
+    gz = torch.randn(z.shape, device="cuda", generator=g)
+    z.backward(gz.to(z.dtype))
+    z2.backward(gz)
+    assert Q.rel_err(x1.grad.double().cpu().numpy(), x2.grad.double().cpu().numpy()) <= 2e-2
+    assert Q.rel_err(m.weight.grad.double().cpu().numpy(), w2.grad.double().cpu().numpy()) <= 2e-2
+    assert Q.rel_err(m.bias.grad.double().cpu().numpy(), b2.grad.double().cpu().numpy()) <= 2e-2
+    assert int(m.num_batches_tracked) == 1

@@ -62,3 +62,44 @@ def test_quad_layers_use_tcgen05():
     for h in hooks:
         h.remove()
     assert len(seen) == 16 and all(p == 1 for p in seen), seen
+
+
+def test_graphed_step_matches_eager():
+    """The CUDA-graph replay of the full step (fwd, bwd, bucketed all-reduce
+    hooks, fused SGD + pack) follows the eager step exactly."""
+    from paper_2204_01701_b200 import qnets
+    from paper_2204_01701_b200.dp import BucketedAllReduce
+    from paper_2204_01701_b200.graphstep import GraphedStep
+    from paper_2204_01701_b200.optim import QuadSGD
+
+    def build():
+        torch.manual_seed(3)
+        m = qnets.QuadraVGG16(10).cuda().to(memory_format=torch.channels_last)
+        opt = QuadSGD(m, lr=0.02)
+        red = BucketedAllReduce(m.parameters())
+
+        def step(xb, yb):
+            red.reset()
+            with torch.autocast("cuda", dtype=torch.bfloat16, cache_enabled=False):
+                loss = torch.nn.functional.cross_entropy(m(xb), yb)
+            loss.backward()
+            red.finish()
+            opt.step()
+            return loss
+        return m, step
+
+    g = torch.Generator(device="cuda").manual_seed(9)
+    xs = [torch.randn(8, 3, 32, 32, device="cuda", generator=g).bfloat16().contiguous(
+        memory_format=torch.channels_last) for _ in range(4)]
+    ys = [torch.randint(0, 10, (8,), device="cuda", generator=g) for _ in range(4)]
+    m1, s1 = build()
+    m2, s2 = build()
+    # the graphed model also takes 3 eager warm-up steps on (xs[0], ys[0]) before capture
+    for _ in range(3):
+        s1(xs[0], ys[0])
+    gs = GraphedStep(s2, xs[0], ys[0], warmup=3)
+    l1 = [float(s1(xs[0], ys[0]))] + [float(s1(xb, yb)) for xb, yb in zip(xs[1:], ys[1:])]
+    l2 = [float(gs())] + [float(gs(xb, yb)) for xb, yb in zip(xs[1:], ys[1:])]
+    assert l1 == l2, (l1, l2)
+    for p1, p2 in zip(m1.parameters(), m2.parameters()):
+        assert torch.equal(p1, p2)
