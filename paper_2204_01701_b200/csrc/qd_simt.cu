@@ -184,9 +184,36 @@ static void launch_pack_conv(const Plan& P, const float* const w[3], T* out, siz
   pack_conv_kernel<T><<<P.nb * P.F + P.C, 256, smem, st>>>(P, w[0], w[1], w[2], out);
 }
 
+template <typename T, int TF, int TC, int RR, bool UPD>
+__global__ void sgd_pack_tiled_kernel(Plan P, float* w0, float* w1, float* w2, float* m0, float* m1, float* m2,
+                                      const float* g0, const float* g1, const float* g2, float lr, float mom,
+                                      float wd, int first, T* out);
+
+template <typename T>
+static void launch_pack_tiled(const Plan& P, const float* const w[3], T* out, cudaStream_t st) {
+  float* wm[3] = {(float*)w[0], (float*)w[1], (float*)w[2]};
+  const size_t smem = (size_t)32 * (32 * 9 + 1) * 4;
+  const int blocks = P.nroles * ((P.F + 31) / 32) * ((P.C + 31) / 32);
+  sgd_pack_tiled_kernel<T, 32, 32, 9, false><<<blocks, 256, smem, st>>>(P, wm[0], wm[1], wm[2], nullptr, nullptr,
+                                                                          nullptr, nullptr, nullptr, nullptr, 0.f,
+                                                                          0.f, 0.f, 0, out);
+}
+
 void launch_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
   if (dev_skip("pack")) return;
   long long nf = (long long)pack_fprop_elems(P), nd = (long long)pack_dgrad_elems(P);
+  // every packed position is a weight (no structural zeros): the tiled kernel
+  // reads the roles once, coalesced, and writes both layouts in contiguous runs
+  // (large layers only: the row-per-block kernel below has more blocks for small ones)
+  if (P.kind == QD_KIND_CONV && P.r == 3 && P.sq == 0 && P.Jd == P.nb * P.F && P.Cd == P.C &&
+      (long long)P.nroles * ((P.F + 31) / 32) * ((P.C + 31) / 32) >= 2 * 148 && !getenv("QD_OLD_PACK")) {
+    if (P.dtype == QD_BF16)
+      launch_pack_tiled<bf16>(P, w, (bf16*)wpack, st);
+    else
+      launch_pack_tiled<float>(P, w, (float*)wpack, st);
+    count_launch(st, "pack");
+    return;
+  }
   if (P.kind == QD_KIND_CONV && P.sq == 0 && P.Jd == P.nb * P.F && P.Cd == P.C) {
     const int rr = P.r * P.r;
     size_t smem = (size_t)(P.C > P.Jd ? P.C : P.Jd) * rr * 4;
@@ -260,14 +287,20 @@ __global__ void sgd_pack_kernel(Plan P, float* w0, float* w1, float* w2, float* 
 // update streams the role's contiguous (F, C, r, r) / (C, F) rows; the new weights
 // go through shared memory so the packed fprop rows (c fastest) and dgrad rows
 // (filter fastest) are written as contiguous runs instead of scattered 2-B stores.
-template <typename T, int TF, int TC, int RR>  // RR = r*r at compile time (0: runtime)
+// UPD = false: pack only (the weights are read, nothing is updated).
+// Conv layouts only. Warp-row loops: phase 1 streams each filter's contiguous
+// (c0..c0+TC) x r*r run into the tile in source order (tile row = [cl][tap] + 1
+// pad float, an odd stride), phase 2 writes fprop rows (lane = channel), phase 3
+// dgrad rows (lane = filter) -- no per-element index division anywhere.
+template <typename T, int TF, int TC, int RR, bool UPD>  // RR = r*r at compile time (0: runtime)
 __global__ void __launch_bounds__(256) sgd_pack_tiled_kernel(Plan P, float* w0, float* w1, float* w2, float* m0,
                                                              float* m1, float* m2, const float* g0,
                                                              const float* g1, const float* g2, float lr, float mom,
                                                              float wd, int first, T* out) {
-  extern __shared__ float tile[];  // [TF][rr][TC]
+  extern __shared__ float tile[];  // [TF][TC * rr + 1]
   __shared__ int Rrow[TF];
   const int rr = RR ? RR : P.r * P.r;
+  const int RT = TC * rr, RS = RT + 1;
   const int ftiles = (P.F + TF - 1) / TF, ctiles = (P.C + TC - 1) / TC;
   int b = blockIdx.x;
   const int ct = b % ctiles;
@@ -277,7 +310,7 @@ __global__ void __launch_bounds__(256) sgd_pack_tiled_kernel(Plan P, float* w0, 
   float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
   float* m = role == 0 ? m0 : (role == 1 ? m1 : m2);
   const float* g = role == 0 ? g0 : (role == 1 ? g1 : g2);
-  const bool fc = P.kind == QD_KIND_FC;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32, nw = blockDim.x / 32;
   // packed positions are affine in (c, tap) for a fixed (role, f) and in f for a
   // fixed (role, c, tap): take the offsets from pack_positions once
   int R0, kf0, cp0, kdl;
@@ -289,84 +322,74 @@ __global__ void __launch_bounds__(256) sgd_pack_tiled_kernel(Plan P, float* w0, 
     pack_positions(P, role, f, c0, 0, R, kf, cp, kd);
     Rrow[threadIdx.x] = R;
   }
-  const int n = TF * TC * rr;
-  constexpr int U = 4;  // elements per thread per pass, all 12 loads in flight
-  for (int e0 = threadIdx.x; e0 < n; e0 += U * blockDim.x) {
-    size_t o[U];
-    int ti[U];
-    bool ok[U];
+  const int fmax = min(TF, P.F - f0), cmax = min(TC, P.C - c0);
+  const int qmax = cmax * rr;  // valid run length of one filter row
+  for (int fi = warp; fi < fmax; fi += nw) {
+    const size_t base = ((size_t)(f0 + fi) * P.C + c0) * rr;
+    float* trow = tile + fi * RS;
+#pragma unroll 3
+    for (int q0 = 0; q0 < RT; q0 += 96) {
+      float wv[3], gv[3], mv[3];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int e = e0 + u * blockDim.x;
-      int fi, cl, tap;
-      if (fc) {  // (C, F): filter fastest
-        cl = e / TF;
-        fi = e - cl * TF;
-        tap = 0;
-      } else {  // (F, C, r, r): one contiguous run of TC*rr per filter
-        fi = e / (TC * rr);
-        const int rem = e - fi * TC * rr;
-        cl = rem / rr;
-        tap = rem - cl * rr;
+      for (int u = 0; u < 3; ++u) {
+        const int q = q0 + lane + 32 * u;
+        const bool ok = q < qmax;
+        wv[u] = ok ? w[base + q] : 0.f;
+        gv[u] = (UPD && ok) ? g[base + q] : 0.f;
+        mv[u] = (UPD && ok && !first) ? m[base + q] : 0.f;
       }
-      const int f = f0 + fi, c = c0 + cl;
-      ok[u] = e < n && f < P.F && c < P.C;
-      o[u] = ok[u] ? (fc ? (size_t)c * P.F + f : ((size_t)f * P.C + c) * rr + tap) : 0;
-      ti[u] = (fi * rr + tap) * TC + cl;
-    }
-    float gv[U], wv[U], mv[U];
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      gv[u] = ok[u] ? g[o[u]] : 0.f;
-      wv[u] = ok[u] ? w[o[u]] : 0.f;
-      mv[u] = (ok[u] && !first) ? m[o[u]] : 0.f;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      if (!ok[u]) continue;
-      const float d = gv[u] + wd * wv[u];
-      const float v = first ? d : mom * mv[u] + d;
-      m[o[u]] = v;
-      const float nw = wv[u] - lr * v;
-      w[o[u]] = nw;
-      tile[ti[u]] = nw;
+      for (int u = 0; u < 3; ++u) {
+        const int q = q0 + lane + 32 * u;
+        if (q >= qmax) continue;
+        float nw_ = wv[u];
+        if (UPD) {
+          const float d = gv[u] + wd * wv[u];
+          const float v = first ? d : mom * mv[u] + d;
+          m[base + q] = v;
+          nw_ = wv[u] - lr * v;
+          w[base + q] = nw_;
+        }
+        trow[q] = nw_;
+      }
     }
   }
   __syncthreads();
-  const int fmax = P.F - f0, cmax = P.C - c0;
-  // fprop rows: channel fastest
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const int cl = e % TC, t2 = e / TC, tap = t2 % rr, fi = t2 / rr;
-    if (fi >= fmax || cl >= cmax) continue;
-    out[(size_t)Rrow[fi] * P.Kf + kf0 + tap * P.C + cl] = cvt<T>(tile[e]);
+  // fprop rows (role, f): columns kf0 + tap C + c, channel fastest
+  for (int row = warp; row < fmax * rr; row += nw) {
+    const int fi = row / rr, tap = row - fi * rr;
+    T* o = out + (size_t)Rrow[fi] * P.Kf + kf0 + tap * P.C;
+    const float* t = tile + fi * RS + tap;
+    for (int cl = lane; cl < cmax; cl += 32) o[cl] = cvt<T>(t[cl * rr]);
   }
-  // dgrad rows: filter fastest
+  // dgrad rows (c): columns (rr-1-tap) Jd + j(f0) + fi, filter fastest
   T* od = out + (long long)P.nb * P.F * P.Kf + (size_t)cp0 * P.Kd + kdl;
-  for (int e = threadIdx.x; e < n; e += blockDim.x) {
-    const int fi = e % TF, t2 = e / TF, tap = t2 % rr, cl = t2 / rr;
-    if (fi >= fmax || cl >= cmax) continue;
-    od[(size_t)cl * P.Kd + (rr - 1 - tap) * P.Jd + fi] = cvt<T>(tile[(fi * rr + tap) * TC + cl]);
+  for (int row = warp; row < cmax * rr; row += nw) {
+    const int cl = row / rr, tap = row - cl * rr;
+    T* o = od + (size_t)cl * P.Kd + (rr - 1 - tap) * P.Jd;
+    const float* t = tile + cl * rr + tap;
+    for (int fi = lane; fi < fmax; fi += 32) o[fi] = cvt<T>(t[fi * RS]);
   }
 }
 
 template <typename T, int TF, int TC>
 static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3],
                              float lr, float momentum, float wd, int first, T* out, cudaStream_t st) {
-  const size_t smem = (size_t)TF * TC * P.r * P.r * 4;
+  const size_t smem = (size_t)TF * (TC * P.r * P.r + 1) * 4;
   const int blocks = P.nroles * ((P.F + TF - 1) / TF) * ((P.C + TC - 1) / TC);
   if (P.r == 3) {
-    sgd_pack_tiled_kernel<T, TF, TC, 9><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
+    sgd_pack_tiled_kernel<T, TF, TC, 9, true><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
                                                                     grad[0], grad[1], grad[2], lr, momentum, wd,
                                                                     first, out);
     return;
   }
   static size_t attr = 0;
   if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(sgd_pack_tiled_kernel<T, TF, TC, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(sgd_pack_tiled_kernel<T, TF, TC, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
     attr = smem;
   }
-  sgd_pack_tiled_kernel<T, TF, TC, 0><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
+  sgd_pack_tiled_kernel<T, TF, TC, 0, true><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
                                                                   grad[0], grad[1], grad[2], lr, momentum, wd,
                                                                   first, out);
 }
@@ -374,12 +397,14 @@ static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[
 void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
                      float momentum, float wd, int first, void* wpack, cudaStream_t st) {
   const int rr = P.r * P.r;
-  if (!getenv("QD_SGD_ELEM") && rr <= 49) {
+  // 32 x 32 tiles unless that leaves most SMs idle (small layers: 16 x 16)
+  const bool big = (long long)P.nroles * ((P.F + 31) / 32) * ((P.C + 31) / 32) >= 2 * 148;
+  if (!getenv("QD_SGD_ELEM") && rr <= 49 && P.kind == QD_KIND_CONV) {
     if (P.dtype == QD_BF16) {
-      if (rr <= 9) launch_sgd_tiled<bf16, 32, 32>(P, w, mom, grad, lr, momentum, wd, first, (bf16*)wpack, st);
+      if (rr <= 9 && big) launch_sgd_tiled<bf16, 32, 32>(P, w, mom, grad, lr, momentum, wd, first, (bf16*)wpack, st);
       else launch_sgd_tiled<bf16, 16, 16>(P, w, mom, grad, lr, momentum, wd, first, (bf16*)wpack, st);
     } else {
-      if (rr <= 9) launch_sgd_tiled<float, 32, 32>(P, w, mom, grad, lr, momentum, wd, first, (float*)wpack, st);
+      if (rr <= 9 && big) launch_sgd_tiled<float, 32, 32>(P, w, mom, grad, lr, momentum, wd, first, (float*)wpack, st);
       else launch_sgd_tiled<float, 16, 16>(P, w, mom, grad, lr, momentum, wd, first, (float*)wpack, st);
     }
     count_launch(st, "sgd_pack");

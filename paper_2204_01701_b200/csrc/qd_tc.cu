@@ -937,11 +937,23 @@ static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUte
   return check_launch("wgrad");
 }
 
-static int wgrad_ntile_blocks(int Jd) {
-  int nb = Jd / 64;
-  for (int c = 4; c >= 1; --c)
-    if (nb % c == 0) return c;
-  return 1;
+// N tile (64-column blocks) of the v1 wgrad: the widest of 4 / 3 / 2 / 1 that
+// divides Jd, unless a narrower one fills the last wave of the (one CTA per SM)
+// grid clearly better (e.g. Jd 1536, Kf 4608: 216 tiles = 1.46 waves at N 256,
+// 288 tiles = 1.95 waves at N 192)
+static int wgrad_ntile_blocks(int Jd, int Kf) {
+  const int nb = Jd / 64, mtiles = (Kf / 64 + 1) / 2, sms = tc_num_sms();
+  int best = 1;
+  double best_eff = -1.0;
+  for (int c = 4; c >= 2; --c) {
+    if (nb % c) continue;
+    const long long tiles = (long long)mtiles * (nb / c);
+    const long long waves = (tiles + sms - 1) / sms;
+    const double fill = (double)tiles / (double)(waves * sms);
+    const double eff = fill * (c == 4 ? 1.0 : (c == 3 ? 0.97 : 0.9));  // narrower N: more operand bytes per MMA
+    if (eff > best_eff + 1e-9) { best_eff = eff; best = c; }
+  }
+  return best;
 }
 
 int tc_wgrad_split(const Plan& P) {
@@ -953,7 +965,7 @@ int tc_wgrad_split(const Plan& P) {
   }
   int nkb = P.Kf / 64;
   int mtiles = (nkb + 1) / 2;
-  int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P.Jd);
+  int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P.Jd, P.Kf);
   Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
   long long ptiles = (long long)pb.tw * pb.th * pb.tn;
   int sms = g_num_sms > 0 ? g_num_sms : 148;
@@ -1243,7 +1255,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
     WgArgs g;
     memset(&g, 0, sizeof(g));
-    int nblk = wgrad_ntile_blocks(P.Jd);
+    int nblk = wgrad_ntile_blocks(P.Jd, P.Kf);
     g.nkb = P.Kf / 64;
     g.mtiles = (g.nkb + 1) / 2;
     g.ntiles = (P.Jd / 64) / nblk;

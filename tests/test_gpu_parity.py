@@ -186,6 +186,7 @@ SPLITK_CASES = [
     ("t2_linear", "conv", 2, 128, 64, 4, 4, 3, 1, 1),
     ("first_order", "conv", 2, 256, 256, 3, 3, 3, 1, 1),
     ("proposed", "fc", 64, 1024, 256, 1, 1, 1, 1, 0),
+    ("proposed", "conv", 2, 512, 512, 3, 3, 3, 1, 1),  # + the tiled weight pack (large layer)
 ]
 
 
@@ -355,7 +356,8 @@ def test_t1_parity(fam, n, c, dtype):
 @pytest.mark.parametrize("family,kind,c,f,k", [("proposed", "conv", 64, 64, 3), ("t4", "conv", 64, 128, 3),
                                                ("t2_linear", "conv", 64, 64, 3), ("t2and4", "conv", 64, 64, 3),
                                                ("proposed", "fc", 96, 64, 1), ("first_order", "conv", 8, 16, 3),
-                                               ("proposed", "conv", 40, 72, 5), ("t4", "fc", 100, 36, 1)])
+                                               ("proposed", "conv", 40, 72, 5), ("t4", "fc", 100, 36, 1),
+                                               ("proposed", "conv", 330, 340, 3)])
 def test_quad_sgd_matches_torch_sgd_and_repack(family, kind, c, f, k):
     from paper_2204_01701_b200 import neurons
     from paper_2204_01701_b200.nn import QuadConv2d, QuadLinear
