@@ -499,7 +499,6 @@ def net_quad_layers(name):
     the CPU baseline (built on the meta device: shapes only)."""
     import torch
     from paper_2204_01701_b200 import qnets
-    import dataclasses
     from paper_2204_01701_b200.nn import QuadConv2d
     builder, batch, hw, classes = NETS[name]
     shapes = []
@@ -507,13 +506,12 @@ def net_quad_layers(name):
     with torch.device("meta"):
         model = getattr(qnets, builder)(num_classes=classes)
     inner = set()
+    from paper_2204_01701_b200.im2col import Im2colConv2d
     for m in model.modules():
-        if isinstance(m, qnets.PaddedQuadConv2d):
-            inner.add(id(m.conv))
-            # algorithmic work counts the real input channels, not the zero padding
+        if isinstance(m, Im2colConv2d) and m.conv_spec.family != "first_order":
+            # algorithmic work of the conv itself (real input channels, not the K padding)
             hooks.append(m.register_forward_pre_hook(
-                lambda mod, inp: shapes.append((dataclasses.replace(mod.conv.spec, in_dim=mod.cin),
-                                                tuple(inp[0].shape[1:])))))
+                lambda mod, inp: shapes.append((mod.conv_spec, tuple(inp[0].shape[1:])))))
     from paper_2204_01701_b200.bn import QuadConvBN
     for m in model.modules():
         if isinstance(m, QuadConvBN):  # fused conv -> BN (-> ReLU) node: its layer never runs forward()
@@ -586,6 +584,9 @@ def run_net(args, name):
         dist.init_process_group("nccl", device_id=dev)
     builder, batch, hw, classes = NETS[name]
     batch = args.batch or batch
+    # the first-order convs (ResNet stem, 1x1 shortcuts) run on cuDNN: let it time
+    # its algorithms for these fixed shapes once instead of taking its heuristic pick
+    torch.backends.cudnn.benchmark = os.environ.get("QD_CUDNN_BENCH", "1") == "1"
     torch.manual_seed(1234)
     model = getattr(qnets, builder)(num_classes=classes).to(dev).to(memory_format=torch.channels_last)
     broadcast_module(model)  # every replica starts from rank 0's weights and BN buffers

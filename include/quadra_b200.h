@@ -139,6 +139,13 @@ int qd_maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtyp
 int qd_maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* dy,
                         const void* argmax, void* dx, void* stream);
 
+/* im2col of an NHWC tensor for small-channel convs run as one fc GEMM (the
+ * QuadraResNet 7x7/2 stem, the QuadraVGG first layer -- 3 input channels):
+ * col[m][k], m = (n, oh, ow), k = (ky r + kx) C + c for k < r*r*C, zero up to
+ * Kp (a multiple of 8). Same geometry rules as conv_out_size (tensor.py:279). */
+int qd_im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, const void* x, void* col,
+              void* stream);
+
 /* Forward: neurons.forward (neurons.py:235-276).
  * bias[i]: fp32 (F) per role (proposed ba, bb, bc; first_order b; else NULL).
  * y: output NHWC; a_cache/b_cache: the LayerCache a, b (proposed/t4, NHWC,

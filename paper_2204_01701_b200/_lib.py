@@ -32,7 +32,7 @@ EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version",
            "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read",
            "qd_sgd_pack", "qd_bn_workspace_bytes", "qd_bn_forward", "qd_bn_backward_D",
-           "qd_maxpool_forward", "qd_maxpool_backward")
+           "qd_maxpool_forward", "qd_maxpool_backward", "qd_im2col")
 
 
 class QdDesc(ctypes.Structure):
@@ -92,6 +92,8 @@ def load():
         lib.qd_maxpool_forward.restype = ctypes.c_int
         lib.qd_maxpool_backward.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, vp, vp, vp, vp]
         lib.qd_maxpool_backward.restype = ctypes.c_int
+        lib.qd_im2col.argtypes = [ci, ci, ci, ci, ci, ci, ci, ci, ci, vp, vp, vp]
+        lib.qd_im2col.restype = ctypes.c_int
         lib.qd_forward.argtypes = [P(QdDesc), vp, vp, fp3, vp, vp, vp, vp, vp]
         lib.qd_forward.restype = ctypes.c_int
         lib.qd_backward.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, fp3, fp3, vp, vp]

@@ -283,6 +283,13 @@ int qd_maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dty
   return maxpool_backward(N, C, H, W, k, s, p, dtype, dy, argmax, dx, (cudaStream_t)stream);
 }
 
+int qd_im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, const void* x, void* col,
+              void* stream) {
+  if (dtype != QD_F32 && dtype != QD_BF16) return set_error(QD_ERR_CONFIG, "unknown dtype %d", dtype);
+  if (!x || !col) return set_error(QD_ERR_ARG, "qd_im2col: NULL argument");
+  return im2col(N, C, H, W, r, s, p, Kp, dtype, x, col, (cudaStream_t)stream);
+}
+
 int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const float* const grad[3],
                 float lr, float momentum, float weight_decay, int first, void* wpack, void* stream) {
   int st = validate(d);

@@ -148,6 +148,8 @@ int maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, 
                     cudaStream_t st);
 int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype, const void* dy, const void* arg,
                      void* dx, cudaStream_t st);
+int im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, const void* x, void* col,
+           cudaStream_t st);
 int wgrad3_pairs_per_split(const Plan& P);
 int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,

@@ -185,3 +185,68 @@ int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype,
 }
 
 }  // namespace qd
+
+namespace qd {
+
+// im2col for small-channel convs run as one fc GEMM (the ResNet stem 7x7/2 over
+// 3 channels, the VGG stem 3x3 over 3 channels): NHWC x -> col[M][Kp], column
+// k = (ky r + kx) C + c for k < r*r*C, zeros up to Kp (a multiple of 8). One
+// thread per (output pixel, 8 columns), one 16-byte store each.
+template <typename T>
+__global__ void __launch_bounds__(256) im2col_kernel(int N, int C, int H, int W, int OH, int OW, int r, int s, int p,
+                                                     int Kp, const T* __restrict__ x, T* __restrict__ col) {
+  // 32-bit index math (the host checks M * Kp / 8 < 2^31); the 8 columns walk
+  // (tap, c) incrementally -- one division per thread, not per element
+  const unsigned k8n = (unsigned)Kp / 8;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (unsigned)N * OH * OW * k8n) return;
+  const unsigned m = i / k8n, k0 = (i - m * k8n) * 8;
+  const unsigned ow = m % (unsigned)OW, t = m / (unsigned)OW;
+  const unsigned oh = t % (unsigned)OH, n = t / (unsigned)OH;
+  const int K = r * r * C;
+  int tap = (int)k0 / C, c = (int)k0 - tap * C;
+  int ky = tap / r, kx = tap - ky * r;
+  const int hb = (int)oh * s - p, wb = (int)ow * s - p;
+  const T* xn = x + (size_t)n * H * W * C;
+  T v[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {
+    float val = 0.f;
+    if ((int)k0 + e < K) {
+      const int h = hb + ky, w = wb + kx;
+      if (h >= 0 && h < H && w >= 0 && w < W) val = ld(xn + ((size_t)h * W + w) * C + c);
+    }
+    v[e] = cvt<T>(val);
+    if (++c == C) {
+      c = 0;
+      if (++kx == r) { kx = 0; ++ky; }
+    }
+  }
+  T* dst = col + (size_t)m * Kp + k0;
+  if (sizeof(T) == 2) {
+    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+  } else {
+    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(v)[0];
+    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(v)[1];
+  }
+}
+
+int im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, const void* x, void* col,
+           cudaStream_t st) {
+  if (N < 1 || C < 1 || H < 1 || W < 1 || r < 1 || s < 1 || p < 0)
+    return set_error(QD_ERR_DIM, "im2col: N %d C %d H %d W %d r %d s %d p %d", N, C, H, W, r, s, p);
+  if (Kp % 8 || Kp < r * r * C) return set_error(QD_ERR_CONFIG, "im2col: Kp %d (need a multiple of 8 >= %d)", Kp, r * r * C);
+  const int OH = (H + 2 * p - r) / s + 1, OW = (W + 2 * p - r) / s + 1;
+  if (OH < 1 || OW < 1) return set_error(QD_ERR_DIM, "im2col: empty output");
+  const long long n = (long long)N * OH * OW * (Kp / 8);
+  if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "im2col: %lld column groups (max 2^31)", n);
+  const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (dtype == QD_BF16)
+    im2col_kernel<bf16><<<blocks, 256, 0, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x, (bf16*)col);
+  else
+    im2col_kernel<float><<<blocks, 256, 0, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const float*)x, (float*)col);
+  count_launch(st, "im2col");
+  return check_launch("im2col");
+}
+
+}  // namespace qd

@@ -159,11 +159,12 @@ def memory_ledger(model: nn.Module, x: torch.Tensor) -> MemoryLedger:
         return [(n, c) for n, c in m.named_modules() if isinstance(c, (_QuadBase, QuadConvBN, AutoQuad, _AutoQuadBN))
                 and not isinstance(getattr(c, "_parent_quad", None), object)]
     model.train()
-    hyb_layers = [(n, c) for n, c in model.named_modules() if isinstance(c, QuadConvBN) or
+    from .im2col import Im2colConv2d  # 3-channel stems: the same module in both modes
+    hyb_layers = [(n, c) for n, c in model.named_modules() if isinstance(c, (QuadConvBN, Im2colConv2d)) or
                   (isinstance(c, _QuadBase) and not n.endswith(".layer"))]
     th, ph = _retained(model, x, hyb_layers)
     auto = to_auto(model)
-    auto_layers = [(n, c) for n, c in auto.named_modules() if isinstance(c, _AutoQuadBN) or
+    auto_layers = [(n, c) for n, c in auto.named_modules() if isinstance(c, (_AutoQuadBN, Im2colConv2d)) or
                    (isinstance(c, AutoQuad) and not n.endswith(".q"))]
     ta, pa = _retained(auto, x, auto_layers)
     return MemoryLedger(per_layer_auto=pa, per_layer_hybrid=ph, peak_auto=ta, peak_hybrid=th)

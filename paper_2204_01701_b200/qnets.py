@@ -4,7 +4,10 @@ The reference cannot express these nets (its ModelConfig is a plain chain
 with no pooling or residual ops, /root/reference/pkg/src/quadra/autobuild.py:75-118,
 model.py:151-155), so they are built here in torch around
 the quadratic conv module; every 3x3 conv is a ``QuadConv2d`` (proposed
-neuron by default) and everything else is first-order torch/cuDNN:
+neuron by default). Around them: BN (+ReLU) and max-pool on the library's
+kernels (``bn.BNAct2d``, ``pool.MaxPool2d``), the 3-channel stems as one fc
+GEMM over im2col'd patches (``im2col.Im2colConv2d``), the 1x1 shortcuts,
+residual adds, pooling head and loss in torch:
 
 * QuadraVGG-16 (CIFAR, 3x32x32, 10 classes): VGG-16 "D" layout, all 13 convs
   quadratic, each followed by BatchNorm + ReLU, five 2x2 max-pools, a
@@ -23,45 +26,17 @@ layers compute in bf16 too (batch norm keeps fp32 statistics).
 from __future__ import annotations
 
 import torch
-import torch.nn.functional as Fnn
 from torch import nn
 
 from .bn import BNAct2d, QuadConvBN
 from .nn import QuadConv2d
+from .im2col import Im2colConv2d
 from .pool import MaxPool2d
 
 
-class PaddedQuadConv2d(nn.Module):
-    """QuadConv2d whose input channels are zero-padded to a multiple of 64 so
-    the layer runs on the tcgen05 kernels (e.g. the 3-channel stem of VGG).
-    The padding is part of the autograd graph, so gradients of the real
-    channels are exact and the padded ones are dropped."""
-
-    def __init__(self, in_channels, out_channels, kernel_size=3, stride=1, padding=1,
-                 family="proposed", device=None):
-        super().__init__()
-        self.cin = in_channels
-        self.cpad = ((in_channels + 63) // 64) * 64
-        self.conv = QuadConv2d(self.cpad, out_channels, kernel_size, stride, padding, family,
-                               device=device)
-        # re-initialise with the real fan-in and keep the padded weight columns at zero
-        with torch.no_grad():
-            for role in ("Wa", "Wb", "Wc"):
-                if hasattr(self.conv, role):
-                    w = getattr(self.conv, role)
-                    w[:, in_channels:].zero_()
-                    w[:, :in_channels].mul_((self.cpad / in_channels) ** 0.5)
-
-    def forward(self, x):
-        if self.cpad != self.cin:
-            x = Fnn.pad(x, (0, 0, 0, 0, 0, self.cpad - self.cin))
-            x = x.contiguous(memory_format=torch.channels_last)
-        return self.conv(x)
-
-
 def quad_conv(cin, cout, k=3, s=1, p=1, family="proposed"):
-    if cin % 64:
-        return PaddedQuadConv2d(cin, cout, k, s, p, family)
+    if cin % 64:  # few input channels (a stem): one fc GEMM over the im2col'd input
+        return Im2colConv2d(cin, cout, k, s, p, family)
     return QuadConv2d(cin, cout, k, s, p, family)
 
 
@@ -76,7 +51,7 @@ class QuadraVGG16(nn.Module):
         for v in VGG16_CFG:
             if v == "M":
                 layers.append(MaxPool2d(2, 2))
-            elif cin % 64:  # zero-padded stem: quad conv, then BN + ReLU (one node; Identity keeps indices)
+            elif cin % 64:  # 3-channel stem (im2col + fc GEMM), then BN + ReLU (one node; Identity keeps indices)
                 layers += [quad_conv(cin, v, 3, 1, 1, family), BNAct2d(v, relu=True), nn.Identity()]
                 cin = v
             else:  # quad conv -> BN -> ReLU as one fused node (bn.QuadConvBN)
@@ -113,8 +88,8 @@ class QuadraResNet18(nn.Module):
     def __init__(self, num_classes=1000, family="proposed"):
         super().__init__()
         # first-order stem; BN + ReLU as one node on the library kernels (Identity keeps indices)
-        self.stem = nn.Sequential(nn.Conv2d(3, 64, 7, 2, 3, bias=False), BNAct2d(64, relu=True), nn.Identity(),
-                                  MaxPool2d(3, 2, 1))
+        self.stem = nn.Sequential(Im2colConv2d(3, 64, 7, 2, 3, family="first_order", bias=False),
+                                  BNAct2d(64, relu=True), nn.Identity(), MaxPool2d(3, 2, 1))
         blocks = []
         inplanes = 64
         for planes, stride in ((64, 1), (128, 2), (256, 2), (512, 2)):

@@ -564,3 +564,41 @@ def test_bnact_matches_reference_bn(relu):
     assert Q.rel_err(m.weight.grad.double().cpu().numpy(), w2.grad.double().cpu().numpy()) <= 2e-2
     assert Q.rel_err(m.bias.grad.double().cpu().numpy(), b2.grad.double().cpu().numpy()) <= 2e-2
     assert int(m.num_batches_tracked) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("family,k,s,p,c", [("first_order", 7, 2, 3, 3), ("proposed", 3, 1, 1, 3),
+                                          ("t4", 3, 1, 1, 5), ("proposed", 5, 2, 2, 2)])
+def test_im2col_conv_matches_torch_conv(family, k, s, p, c):
+    """3-channel stems as one fc GEMM over im2col'd patches vs the conv computed
+    by torch in fp32 from the same bf16 values."""
+    from paper_2204_01701_b200.im2col import Im2colConv2d
+    import torch.nn.functional as F
+    torch.manual_seed(2)
+    m = Im2colConv2d(c, 64, k, s, p, family=family, bias=(family != "first_order")).cuda()
+    with torch.no_grad():
+        for name, t in m.named_parameters():
+            if name.startswith("b"):
+                t.uniform_(-0.2, 0.2)
+    x = torch.randn(3, c, 19, 23, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    y = m(x)
+    assert y.is_contiguous(memory_format=torch.channels_last)
+    gy = torch.randn(y.shape, device="cuda")
+    y.backward(gy.to(y.dtype))
+    xf = x.float()
+    ref = {n: t.detach().bfloat16().float().requires_grad_(True) if t.dim() == 4 else t.detach().clone().requires_grad_(True)
+           for n, t in m.named_parameters()}
+    conv = lambda w: F.conv2d(xf, w, stride=s, padding=p)  # noqa: E731
+    if family == "first_order":
+        yr = conv(ref["W"])
+    elif family == "t4":
+        yr = conv(ref["Wa"]) * conv(ref["Wb"])
+    else:
+        a = conv(ref["Wa"]) + ref["ba"].view(1, -1, 1, 1)
+        b = conv(ref["Wb"]) + ref["bb"].view(1, -1, 1, 1)
+        yr = a * b + conv(ref["Wc"]) + ref["bc"].view(1, -1, 1, 1)
+    yr.backward(gy)
+    cv = lambda t: t.detach().double().cpu().numpy()  # noqa: E731
+    assert Q.rel_err(cv(y), cv(yr)) <= 2e-2
+    for n, t in m.named_parameters():
+        assert Q.rel_err(cv(t.grad), cv(ref[n].grad)) <= 2e-2, n

@@ -13,6 +13,7 @@ builder, batch, hw, classes = bench.NETS[name]
 batch = int(sys.argv[2]) if len(sys.argv) > 2 and int(sys.argv[2]) > 0 else batch
 top = int(sys.argv[3]) if len(sys.argv) > 3 else 30
 dev = torch.device("cuda")
+torch.backends.cudnn.benchmark = os.environ.get("QD_CUDNN_BENCH", "1") == "1"
 torch.manual_seed(0)
 model = getattr(qnets, builder)(num_classes=classes).to(dev).to(memory_format=torch.channels_last)
 opt = QuadSGD(model, lr=0.01)

@@ -42,7 +42,7 @@ if (Dn > 0).all():
     print(f"main loop min/med/max {main.min():.1f}/{np.median(main):.1f}/{main.max():.1f} us, "
           f"epilogue min/med/max {epi.min():.1f}/{np.median(epi):.1f}/{epi.max():.1f} us")
 T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
-t0 = T[T > 0].min()
+t0 = T[0, 0, 0] if T[0, 0, 0] > 0 else T[T > 0].min()
 print("CTA0 per q block (cycles from first event): prod[acq empty] mma[full acquired, issued]")
 prev = None
 for blk in range(64):
