@@ -192,42 +192,54 @@ namespace qd {
 // 3 channels, the VGG stem 3x3 over 3 channels): NHWC x -> col[M][Kp], column
 // k = (ky r + kx) C + c for k < r*r*C, zeros up to Kp (a multiple of 8). One
 // thread per (output pixel, 8 columns), one 16-byte store each.
+// block = (n, oh, 32 output pixels of that row): the r input rows the block
+// needs are staged in shared memory with the zero padding materialised
+// (coalesced NHWC loads), then every thread assembles 16-byte column chunks
+// from shared memory and stores them: the col rows are written contiguously.
+constexpr int IM2COL_TW = 32;
 template <typename T>
 __global__ void __launch_bounds__(256) im2col_kernel(int N, int C, int H, int W, int OH, int OW, int r, int s, int p,
                                                      int Kp, const T* __restrict__ x, T* __restrict__ col) {
-  // 32-bit index math (the host checks M * Kp / 8 < 2^31); the 8 columns walk
-  // (tap, c) incrementally -- one division per thread, not per element
-  const unsigned k8n = (unsigned)Kp / 8;
-  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (unsigned)N * OH * OW * k8n) return;
-  const unsigned m = i / k8n, k0 = (i - m * k8n) * 8;
-  const unsigned ow = m % (unsigned)OW, t = m / (unsigned)OW;
-  const unsigned oh = t % (unsigned)OH, n = t / (unsigned)OH;
-  const int K = r * r * C;
-  int tap = (int)k0 / C, c = (int)k0 - tap * C;
-  int ky = tap / r, kx = tap - ky * r;
-  const int hb = (int)oh * s - p, wb = (int)ow * s - p;
-  const T* xn = x + (size_t)n * H * W * C;
-  T v[8];
-#pragma unroll
-  for (int e = 0; e < 8; ++e) {
-    float val = 0.f;
-    if ((int)k0 + e < K) {
-      const int h = hb + ky, w = wb + kx;
-      if (h >= 0 && h < H && w >= 0 && w < W) val = ld(xn + ((size_t)h * W + w) * C + c);
-    }
-    v[e] = cvt<T>(val);
-    if (++c == C) {
-      c = 0;
-      if (++kx == r) { kx = 0; ++ky; }
-    }
+  extern __shared__ unsigned char im2col_smem[];
+  T* rows = reinterpret_cast<T*>(im2col_smem);  // [r][RW][C]
+  const int owt = (OW + IM2COL_TW - 1) / IM2COL_TW;
+  int b = blockIdx.x;
+  const int ot = b % owt;
+  b /= owt;
+  const int oh = b % OH, n = b / OH;
+  const int ow0 = ot * IM2COL_TW, tw = min(IM2COL_TW, OW - ow0);
+  const int RW = (IM2COL_TW - 1) * s + r, RC = RW * C;
+  const int h0 = oh * s - p, w0 = ow0 * s - p;
+  for (int e = threadIdx.x; e < r * RC; e += blockDim.x) {
+    const int j = e / RC, q = e - j * RC;
+    const int h = h0 + j, w = w0 + q / C;
+    rows[e] = (h >= 0 && h < H && w >= 0 && w < W) ? x[(((size_t)n * H + h) * W + w0) * C + q]
+                                                  : cvt<T>(0.f);
   }
-  T* dst = col + (size_t)m * Kp + k0;
-  if (sizeof(T) == 2) {
-    *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
-  } else {
-    reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(v)[0];
-    reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(v)[1];
+  // column k -> offset in the staged rows relative to the pixel's window (-1: K padding)
+  int* koff = reinterpret_cast<int*>(im2col_smem + (((size_t)r * RC * sizeof(T) + 15) & ~(size_t)15));
+  const int K = r * r * C, k8n = Kp / 8, rCw = r * C;
+  for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
+    const int ky = k / rCw;
+    koff[k] = k < K ? ky * RC + (k - ky * rCw) : -1;
+  }
+  __syncthreads();
+  T* dst0 = col + ((size_t)(n * OH + oh) * OW + ow0) * Kp;
+  for (int id = threadIdx.x; id < tw * k8n; id += blockDim.x) {
+    const int l = id / k8n, k0 = (id - l * k8n) * 8;
+    const T* win = rows + l * s * C;
+    const int4 oa = *reinterpret_cast<const int4*>(koff + k0), ob = *reinterpret_cast<const int4*>(koff + k0 + 4);
+    const int o[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
+    T v[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) v[e] = o[e] >= 0 ? win[o[e]] : cvt<T>(0.f);
+    T* dst = dst0 + (size_t)l * Kp + k0;
+    if (sizeof(T) == 2) {
+      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+    } else {
+      reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(v)[0];
+      reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(v)[1];
+    }
   }
 }
 
@@ -238,13 +250,17 @@ int im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, c
   if (Kp % 8 || Kp < r * r * C) return set_error(QD_ERR_CONFIG, "im2col: Kp %d (need a multiple of 8 >= %d)", Kp, r * r * C);
   const int OH = (H + 2 * p - r) / s + 1, OW = (W + 2 * p - r) / s + 1;
   if (OH < 1 || OW < 1) return set_error(QD_ERR_DIM, "im2col: empty output");
-  const long long n = (long long)N * OH * OW * (Kp / 8);
-  if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "im2col: %lld column groups (max 2^31)", n);
-  const unsigned blocks = (unsigned)((n + 255) / 256);
+  const long long blocks = (long long)N * OH * ((OW + IM2COL_TW - 1) / IM2COL_TW);
+  if (blocks >= (1LL << 31)) return set_error(QD_ERR_DIM, "im2col: %lld blocks", blocks);
+  const size_t es = dtype == QD_BF16 ? 2 : 4;
+  const size_t smem = (((size_t)r * ((IM2COL_TW - 1) * s + r) * C * es + 15) & ~(size_t)15) + (size_t)Kp * 4;
+  if (smem > 48 * 1024) return set_error(QD_ERR_UNSUPPORTED, "im2col: %zu B of staged rows (r %d, s %d, C %d)", smem, r, s, C);
   if (dtype == QD_BF16)
-    im2col_kernel<bf16><<<blocks, 256, 0, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x, (bf16*)col);
+    im2col_kernel<bf16><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x,
+                                                               (bf16*)col);
   else
-    im2col_kernel<float><<<blocks, 256, 0, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const float*)x, (float*)col);
+    im2col_kernel<float><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const float*)x,
+                                                                (float*)col);
   count_launch(st, "im2col");
   return check_launch("im2col");
 }

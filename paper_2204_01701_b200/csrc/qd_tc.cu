@@ -937,23 +937,38 @@ static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUte
   return check_launch("wgrad");
 }
 
-// N tile (64-column blocks) of the v1 wgrad: the widest of 4 / 3 / 2 / 1 that
-// divides Jd, unless a narrower one fills the last wave of the (one CTA per SM)
-// grid clearly better (e.g. Jd 1536, Kf 4608: 216 tiles = 1.46 waves at N 256,
-// 288 tiles = 1.95 waves at N 192)
-static int wgrad_ntile_blocks(int Jd, int Kf) {
-  const int nb = Jd / 64, mtiles = (Kf / 64 + 1) / 2, sms = tc_num_sms();
+// v1 wgrad shape: N tile (64-column blocks: 4 / 3 / 2 / 1 dividing Jd) and the
+// pixel split S. One CTA per SM, so the grid (tiles x S) should fill whole waves:
+// S = SMs / tiles when there are few tiles, and among the N tiles the one with the
+// best wave fill wins (narrower N pays a little in operand bytes per MMA), e.g.
+// Jd 1536, Kf 4608: 216 tiles (1.46 waves) at N 256 vs 288 (1.95) at N 192.
+static long long wgrad_split_for(long long tiles, long long ptiles, int sms) {
+  long long S = sms / tiles;
+  long long cap = ptiles / 4;
+  if (cap < 1) cap = 1;
+  if (S > cap) S = cap;
+  return S < 1 ? 1 : S;
+}
+
+static int wgrad_ntile_blocks(const Plan& P, long long ptiles) {
+  const int nb = P.Jd / 64, mtiles = (P.Kf / 64 + 1) / 2, sms = tc_num_sms();
   int best = 1;
   double best_eff = -1.0;
-  for (int c = 4; c >= 2; --c) {
+  for (int c = 4; c >= 1; --c) {
     if (nb % c) continue;
     const long long tiles = (long long)mtiles * (nb / c);
-    const long long waves = (tiles + sms - 1) / sms;
-    const double fill = (double)tiles / (double)(waves * sms);
-    const double eff = fill * (c == 4 ? 1.0 : (c == 3 ? 0.97 : 0.9));  // narrower N: more operand bytes per MMA
+    const long long ctas = tiles * wgrad_split_for(tiles, ptiles, sms);
+    const long long waves = (ctas + sms - 1) / sms;
+    const double fill = (double)ctas / (double)(waves * sms);
+    const double eff = fill * (c == 4 ? 1.0 : (c == 3 ? 0.97 : (c == 2 ? 0.9 : 0.75)));
     if (eff > best_eff + 1e-9) { best_eff = eff; best = c; }
   }
   return best;
+}
+
+static long long wgrad_ptiles(const Plan& P) {
+  Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
+  return (long long)pb.tw * pb.th * pb.tn;
 }
 
 int tc_wgrad_split(const Plan& P) {
@@ -963,19 +978,10 @@ int tc_wgrad_split(const Plan& P) {
     int s2 = wgrad2_split(P);
     if (s2 > 0) return s2;
   }
-  int nkb = P.Kf / 64;
-  int mtiles = (nkb + 1) / 2;
-  int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P.Jd, P.Kf);
-  Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
-  long long ptiles = (long long)pb.tw * pb.th * pb.tn;
-  int sms = g_num_sms > 0 ? g_num_sms : 148;
-  // one wave: every CTA holds ~200 KB of smem, so > #SMs CTAs would run a tail wave
-  long long S = sms / (mtiles * ntiles);
-  long long cap = ptiles / 4;
-  if (cap < 1) cap = 1;
-  if (S > cap) S = cap;
-  if (S < 1) S = 1;
-  return (int)S;
+  const long long ptiles = wgrad_ptiles(P);
+  const int mtiles = (P.Kf / 64 + 1) / 2;
+  const int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P, ptiles);
+  return (int)wgrad_split_for((long long)mtiles * ntiles, ptiles, tc_num_sms());
 }
 
 // generic conv-GEMM launch (fprop or dgrad)
@@ -1182,7 +1188,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if (rc0) return rc0;
     launch_t3_prologue(P, dy, Dw, false, Dw, st);
     D = Dw;
-  } else if (mat || P.nbias || up) {
+  } else if (mat || up || (P.nbias && db[0])) {  // (bias sums only when asked for)
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
     bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;
@@ -1255,7 +1261,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
     WgArgs g;
     memset(&g, 0, sizeof(g));
-    int nblk = wgrad_ntile_blocks(P.Jd, P.Kf);
+    int nblk = wgrad_ntile_blocks(P, wgrad_ptiles(P));
     g.nkb = P.Kf / 64;
     g.mtiles = (g.nkb + 1) / 2;
     g.ntiles = (P.Jd / 64) / nblk;

@@ -222,7 +222,7 @@ def forward(spec, params, x, *, dtype=None, flags=0):
     return y, LayerCache(spec.family, spec.kind, x, a, b, tuple(y.shape), desc, wpack, key)
 
 
-def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True):
+def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, want_db=True):
     """Closed-form gradients on the GPU; returns ({role: grad}, dx).
 
     neurons.py:295-445 -- same checks (IntegrityError for a cache of another
@@ -257,8 +257,9 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True):
         wpack = _pack(spec, desc, params)[0]
     dev = x.device
     shapes = param_shapes(spec)
+    broles = BIAS_ROLES.get(spec.family, ()) if want_db else ()  # want_db=False: no bias grads (constant bias)
     grads = {role: torch.empty(shapes[role], dtype=torch.float32, device=dev)
-             for role in GRAD_ORDER[spec.family]}
+             for role in GRAD_ORDER[spec.family] if want_db or role not in BIAS_ROLES.get(spec.family, ())}
     dx = torch.empty_like(x) if want_dx else None  # preserves channels_last
     ws = _workspace(desc, dev)
     st = lib.qd_backward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
@@ -266,7 +267,7 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True):
                          cache.b.data_ptr() if cache.b is not None else None,
                          g.data_ptr(), dx.data_ptr() if dx is not None else None,
                          _lib.ptr3(*[grads[r].data_ptr() for r in roles]),
-                         _lib.ptr3(*[grads[r].data_ptr() for r in BIAS_ROLES.get(spec.family, ())]),
+                         _lib.ptr3(*[grads[r].data_ptr() for r in broles]),
                          ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
     _lib.raise_for(st, "qd_backward")
     return grads, dx

@@ -35,12 +35,16 @@ class QuadFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, gy):
         want_dx = ctx.needs_input_grad[2]
+        # bias gradients only when some bias is trained (a constant zero bias, e.g.
+        # a bias-free first-order stem, skips the bias reduction pass)
+        bro = neurons.BIAS_ROLES.get(ctx.spec.family, ())
+        want_db = any(ctx.needs_input_grad[3 + i] for i, r in enumerate(ctx.roles) if r in bro)
         grads, dx = neurons.symbolic_backward(ctx.spec, ctx.params, ctx.cache, gy,
-                                              want_dx=want_dx)
+                                              want_dx=want_dx, want_db=want_db)
         if dx is not None and dx.dtype != ctx.x_dtype:
             dx = dx.to(ctx.x_dtype)
         ctx.cache = None
-        return (None, None, dx) + tuple(grads[r] for r in ctx.roles)
+        return (None, None, dx) + tuple(grads.get(r) for r in ctx.roles)
 
 
 def quadratic(spec, params, x, dtype=None):
