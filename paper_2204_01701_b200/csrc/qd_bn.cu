@@ -26,7 +26,7 @@ static int bn_splits(long long M, int C) {
   return (int)(S < 1 ? 1 : S);
 }
 // 8-channel vector kernels when C % 8 == 0 and C / 8 <= 256
-static bool bn_vec(int C) { return C % 8 == 0 && C / 8 <= 256; }
+static bool bn_vec(int C) { return C % 8 == 0 && C / 8 <= 256 && 256 % (C / 8) == 0; }
 
 template <typename T> struct BV;
 template <> struct BV<bf16> {
@@ -131,22 +131,32 @@ __global__ void __launch_bounds__(256) bn_reduce_vec_kernel(long long M, int C, 
   }
 }
 
+// thread = (8-channel chunk q, row lane) with 256 % (C / 8) == 0: the chunk's
+// BN constants stay in registers and rows stride by the grid's lane count
 template <typename T>
-__global__ void bn_apply_vec_kernel(long long rows, int C, const T* y, const float* mean, const float* invstd,
-                                    const float* gamma, const float* beta, int relu, T* z) {
-  const int CQ = C / 8;
-  const long long n = rows * CQ;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int c0 = (int)(i % CQ) * 8;
+__global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C, const T* __restrict__ y,
+                                                           const float* mean, const float* invstd,
+                                                           const float* gamma, const float* beta, int relu,
+                                                           T* __restrict__ z) {
+  const int CQ = C / 8, lanes = 256 / CQ;
+  const int q = threadIdx.x % CQ, c0 = q * 8;
+  float sc[8], sh[8];
+#pragma unroll
+  for (int e = 0; e < 8; ++e) {  // z = sc * y + sh
+    sc[e] = gamma[c0 + e] * invstd[c0 + e];
+    sh[e] = beta[c0 + e] - sc[e] * mean[c0 + e];
+  }
+  const long long step = (long long)gridDim.x * lanes;
+#pragma unroll 4
+  for (long long r = (long long)blockIdx.x * lanes + threadIdx.x / CQ; r < rows; r += step) {
     float v[8];
-    BV<T>::ld8(y + i * 8, v);
+    BV<T>::ld8(y + (size_t)r * C + c0, v);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      float t = fmaf(gamma[c0 + e], (v[e] - mean[c0 + e]) * invstd[c0 + e], beta[c0 + e]);
+      const float t = fmaf(sc[e], v[e], sh[e]);
       v[e] = (relu && t < 0.f) ? 0.f : t;
     }
-    BV<T>::st8(z + i * 8, v);
+    BV<T>::st8(z + (size_t)r * C + c0, v);
   }
 }
 

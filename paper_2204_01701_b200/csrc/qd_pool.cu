@@ -56,15 +56,16 @@ struct PoolGeo {
 template <typename T>
 __global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __restrict__ x, T* __restrict__ y,
                                                           uint8_t* __restrict__ arg) {
-  const int c8 = g.C / 8;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long long)g.N * g.OH * g.OW * c8) return;
-  const int cq = (int)(i % c8);
-  long long t = i / c8;
-  const int ow = (int)(t % g.OW);
-  t /= g.OW;
-  const int oh = (int)(t % g.OH);
-  const int n = (int)(t / g.OH);
+  // 32-bit index math (the host checks the element count)
+  const unsigned c8 = g.C / 8;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (unsigned)g.N * g.OH * g.OW * c8) return;
+  const unsigned cq = i % c8;
+  unsigned t = i / c8;
+  const int ow = (int)(t % (unsigned)g.OW);
+  t /= (unsigned)g.OW;
+  const int oh = (int)(t % (unsigned)g.OH);
+  const int n = (int)(t / (unsigned)g.OH);
   const int h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
   // torch's initial index: the window's first in-bounds position
   const uint8_t first = (uint8_t)((h0 < 0 ? -h0 : 0) * g.k + (w0 < 0 ? -w0 : 0));
@@ -103,15 +104,15 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __
 template <typename T>
 __global__ void __launch_bounds__(256) maxpool_bwd_kernel(PoolGeo g, const T* __restrict__ dy,
                                                           const uint8_t* __restrict__ arg, T* __restrict__ dx) {
-  const int c8 = g.C / 8;
-  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= (long long)g.N * g.H * g.W * c8) return;
-  const int cq = (int)(i % c8);
-  long long t = i / c8;
-  const int w = (int)(t % g.W);
-  t /= g.W;
-  const int h = (int)(t % g.H);
-  const int n = (int)(t / g.H);
+  const unsigned c8 = g.C / 8;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (unsigned)g.N * g.H * g.W * c8) return;
+  const unsigned cq = i % c8;
+  unsigned t = i / c8;
+  const int w = (int)(t % (unsigned)g.W);
+  t /= (unsigned)g.W;
+  const int h = (int)(t % (unsigned)g.H);
+  const int n = (int)(t / (unsigned)g.H);
   // windows (oh, ow) with oh*s - p <= h <= oh*s - p + k - 1
   int oh_lo = (h + g.p - g.k + g.s) / g.s, oh_hi = (h + g.p) / g.s;  // h + p - k + 1 >= 0 ? ceil : 0
   if (h + g.p - g.k + 1 < 0) oh_lo = 0;
@@ -160,6 +161,7 @@ int maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, 
   int rc = pool_geo(N, C, H, W, k, s, p, g);
   if (rc) return rc;
   const long long n = (long long)N * g.OH * g.OW * (C / 8);
+  if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
   if (dtype == QD_BF16)
     maxpool_fwd_kernel<bf16><<<blocks, 256, 0, st>>>(g, (const bf16*)x, (bf16*)y, (uint8_t*)arg);
@@ -175,6 +177,7 @@ int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype,
   int rc = pool_geo(N, C, H, W, k, s, p, g);
   if (rc) return rc;
   const long long n = (long long)N * H * W * (C / 8);
+  if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
   if (dtype == QD_BF16)
     maxpool_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(g, (const bf16*)dy, (const uint8_t*)arg, (bf16*)dx);
