@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // Batch norm (+ ReLU) fused around the quadratic conv.
 // Reference semantics: tensor.py:423-470 (forward: biased batch variance for the
 // normalisation AND for the running-variance update, eps 1e-5, momentum 0.1)
@@ -20,8 +21,9 @@ namespace qd {
 
 // row blocks: ~16K elements each (enough blocks for small-M / large-C layers too)
 static int bn_splits(long long M, int C) {
+  static const long long cap = getenv("QD_BN_SPLITS_MAX") ? atoll(getenv("QD_BN_SPLITS_MAX")) : 592;  // dev knob
   long long S = (M * C + 16383) / 16384;
-  if (S > 592) S = 592;
+  if (S > cap) S = cap;
   if (S > M) S = M;
   return (int)(S < 1 ? 1 : S);
 }
