@@ -70,6 +70,54 @@ def flush_l2(buf, i):
     buf.view(-1, 4096).amax(dim=1, keepdim=False).sum()
 
 
+def pipelined_e2e(k, h2d, compute, d2h):
+    """ms per step of k end-to-end steps through host memory: h2d(b) fills device
+    input set b on a copy-in stream, compute(b) runs on the current stream and
+    returns its result tensors, d2h(outs) copies them to pinned host memory on a
+    copy-out stream. Inputs are double-buffered, so step i+1's H2D overlaps step
+    i's compute and step i-1's D2H (PCIe is full duplex) -- a prefetching input
+    pipeline; every step still moves its own inputs and results. Timed with CUDA
+    events on the compute stream around all k steps (pipeline fill included)."""
+    import torch
+    comp = torch.cuda.current_stream()
+    s_in, s_out = torch.cuda.Stream(), torch.cuda.Stream()
+    in_done = [torch.cuda.Event(), torch.cuda.Event()]
+    freed = [torch.cuda.Event(), torch.cuda.Event()]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(comp)
+    s_in.wait_stream(comp)
+    s_out.wait_stream(comp)
+
+    def issue_in(i):
+        b = i % 2
+        with torch.cuda.stream(s_in):
+            if i >= 2:
+                s_in.wait_event(freed[b])  # compute i-2 is done with set b
+            h2d(b)
+            in_done[b].record(s_in)
+
+    issue_in(0)
+    for i in range(k):
+        b = i % 2
+        if i + 1 < k:
+            issue_in(i + 1)
+        comp.wait_event(in_done[b])
+        outs = compute(b)
+        freed[b].record(comp)
+        done = torch.cuda.Event()
+        done.record(comp)
+        with torch.cuda.stream(s_out):
+            s_out.wait_event(done)
+            for t_ in outs:
+                t_.record_stream(s_out)
+            d2h(outs)
+    comp.wait_stream(s_out)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / k
+
+
 def load_peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -434,25 +482,32 @@ def run_ours(args, wl, wl_name):
     x_h = x.detach().cpu().pin_memory()
     g_h = gy.detach().cpu().pin_memory()
     w_h = {k_: v.detach().cpu().pin_memory() for k_, v in params.items()}
-    dx_h = torch.empty(x.shape, dtype=dt).pin_memory()
+    dx_h = (torch.empty(x.shape, dtype=dt) if kind == "fc" else
+            torch.empty(x.shape, dtype=dt, memory_format=torch.channels_last)).pin_memory()
     gr_h = {k_: torch.empty(v.shape, dtype=torch.float32).pin_memory() for k_, v in params.items()}
 
-    def e2e_step():
-        xd = x_h.to(dev, non_blocking=True)
-        gd = g_h.to(dev, non_blocking=True)
-        pd = {k_: v.to(dev, non_blocking=True) for k_, v in w_h.items()}
-        yy, cc = neurons.forward(spec, pd, xd, dtype=dt)
-        grads, dxx = neurons.symbolic_backward(spec, pd, cc, gd)
+    bufs = [{"x": torch.empty_like(x), "g": torch.empty_like(gy),
+             "w": {k_: torch.empty_like(v) for k_, v in params.items()}} for _ in range(2)]
+
+    def h2d_in(b):
+        bufs[b]["x"].copy_(x_h, non_blocking=True)
+        bufs[b]["g"].copy_(g_h, non_blocking=True)
+        for k_, v in w_h.items():
+            bufs[b]["w"][k_].copy_(v, non_blocking=True)
+
+    def compute_e2e(b):
+        yy, cc = neurons.forward(spec, bufs[b]["w"], bufs[b]["x"], dtype=dt)
+        grads, dxx = neurons.symbolic_backward(spec, bufs[b]["w"], cc, bufs[b]["g"])
         exchange(grads)
-        dx_h.copy_(dxx.contiguous() if kind == "fc" else dxx.permute(0, 1, 2, 3).contiguous(),
-                   non_blocking=True)
-        for k_, v in grads.items():
+        return [dxx] + [grads[k_] for k_ in gr_h]
+
+    def d2h_out(outs):
+        dx_h.copy_(outs[0], non_blocking=True)
+        for k_, v in zip(gr_h, outs[1:]):
             gr_h[k_].copy_(v, non_blocking=True)
-    for _ in range(2):
-        e2e_step()
-    torch.cuda.synchronize()
-    e2e_ms = timed(e2e_step, args.steps)
-    e2e_step_ms = sum(e2e_ms) / len(e2e_ms)
+
+    pipelined_e2e(3, h2d_in, compute_e2e, d2h_out)  # warm-up
+    e2e_step_ms = pipelined_e2e(args.steps, h2d_in, compute_e2e, d2h_out)
     if world > 1:
         tt = torch.tensor([e2e_step_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -485,7 +540,12 @@ def run_ours(args, wl, wl_name):
            "roofline": roof, "cpu_baseline": cpu,
            "e2e": {"value": world * flops / (e2e_step_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                    "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": h2d,
-                   "d2h_bytes_per_step": d2h},
+                   "d2h_bytes_per_step": d2h,
+                   "note": "public API (neurons.forward / symbolic_backward); every step copies its x, dy and fp32 "
+                           "weights from pinned host memory and dx and the fp32 gradients back; double-buffered "
+                           "inputs on a copy stream overlap step i+1's H2D with step i's compute and D2H; no L2 "
+                           "flush inside the loop (inputs arrive over PCIe every step, the step's own traffic "
+                           "exceeds L2)"},
            "gpu_launches": launches, "launches_per_step": launches / args.steps,
            "clocks": clocks,
            "path": "tcgen05" if neurons.device_path(spec, x.shape, dt) == 1 else "cuda-core"}
@@ -688,18 +748,20 @@ def run_net(args, name):
     y_h = y.detach().cpu().pin_memory()
     loss_h = torch.empty((), dtype=torch.float32).pin_memory()
 
-    def e2e_step():
-        if graph is not None:  # H2D straight into the graph's static input buffers
-            loss = graph(x_h, y_h)
-        else:
-            xb = x_h.to(dev, non_blocking=True).contiguous(memory_format=torch.channels_last)
-            yb = y_h.to(dev, non_blocking=True)
-            loss = step(xb, yb)
-        loss_h.copy_(loss.detach().float(), non_blocking=True)
-    e2e_step()
-    torch.cuda.synchronize()
-    e_ms = timed(e2e_step, args.steps)
-    e_step = sum(e_ms) / len(e_ms)
+    stage = [(torch.empty_like(x), torch.empty_like(y)) for _ in range(2)]
+
+    def h2d_in(b):
+        stage[b][0].copy_(x_h, non_blocking=True)
+        stage[b][1].copy_(y_h, non_blocking=True)
+
+    def compute_e2e(b):
+        return [step(stage[b][0], stage[b][1]).detach()]
+
+    def d2h_out(outs):
+        loss_h.copy_(outs[0].float(), non_blocking=True)
+
+    pipelined_e2e(3, h2d_in, compute_e2e, d2h_out)  # warm-up
+    e_step = pipelined_e2e(args.steps, h2d_in, compute_e2e, d2h_out)
     if world > 1:
         tt = torch.tensor([e_step], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -734,7 +796,10 @@ def run_net(args, name):
            "cpu_baseline": cpu,
            "e2e": {"value": world * batch / (e_step * 1e-3), "unit": "img/s", "ms_per_step": e_step,
                    "h2d_bytes_per_step": x_h.numel() * x_h.element_size() + y_h.numel() * y_h.element_size(),
-                   "d2h_bytes_per_step": 4},
+                   "d2h_bytes_per_step": 4,
+                   "note": "every step copies its image batch and labels from pinned host memory (double-buffered "
+                           "on a copy stream, overlapping the previous step's compute) into the graph's input "
+                           "buffers and reads the loss back"},
            "gpu_launches": per_step * args.steps, "launches_per_step": per_step, "clocks": clocks}
     print(json.dumps(out), flush=True)
     if world > 1:
