@@ -967,6 +967,61 @@ __global__ void __launch_bounds__(256) wfinish_conv_kernel(Plan P, const float* 
   }
 }
 
+// phase 1 of the conv fold when S > 1: the S partial slices summed in place into
+// slice 0. Block = L float4 columns x G split groups (G = min(S, 8) rounded down
+// to a power of two, L = 256 / G: every thread loads); group g sums splits
+// g, g+G, ... with 4 loads in flight and the groups are added in order --
+// contiguous reads and writes; the transposing fold then reads one slice
+__global__ void __launch_bounds__(256) wsum_kernel(Plan P, float* __restrict__ part, int S, WSplits wsp) {
+  __shared__ float4 red[256];
+  const int G = S >= 8 ? 8 : (S >= 4 ? 4 : 2), L = 256 / G;
+  const int col = threadIdx.x % L, grp = threadIdx.x / L;
+  const long long n4 = (long long)P.Jd * P.Kf / 4;
+  float4* p4 = reinterpret_cast<float4*>(part);
+  // grid-stride over column tiles: a few resident blocks per SM do all the work
+  // (one short block per tile spent its time in block launch, not in loads)
+  for (long long i0 = (long long)blockIdx.x * L; i0 < n4; i0 += (long long)gridDim.x * L) {
+    const long long i = i0 + col;
+    float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (i < n4) {
+      int Sk = S;
+      if (wsp.ng > 0) {
+        const int k = (int)((i * 4) % P.Kf), kk = k % P.K0, tg = (kk / P.C / 2) / wsp.pp;
+#pragma unroll
+        for (int t = 0; t < 16; ++t)  // static indexing: no local-memory copy of wsp
+          if (t == tg) Sk = wsp.s[t];
+      }
+      float4 c1 = acc, c2 = acc, c3 = acc;
+      int s = grp;
+      for (; s + 3 * G < Sk; s += 4 * G) {
+        const float4 v0 = p4[s * n4 + i], v1 = p4[(s + G) * n4 + i];
+        const float4 v2 = p4[(s + 2 * G) * n4 + i], v3 = p4[(s + 3 * G) * n4 + i];
+        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
+        c1.x += v1.x; c1.y += v1.y; c1.z += v1.z; c1.w += v1.w;
+        c2.x += v2.x; c2.y += v2.y; c2.z += v2.z; c2.w += v2.w;
+        c3.x += v3.x; c3.y += v3.y; c3.z += v3.z; c3.w += v3.w;
+      }
+      for (; s < Sk; s += G) {
+        const float4 v = p4[s * n4 + i];
+        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+      }
+      acc.x += c1.x + (c2.x + c3.x); acc.y += c1.y + (c2.y + c3.y);
+      acc.z += c1.z + (c2.z + c3.z); acc.w += c1.w + (c2.w + c3.w);
+    }
+    red[threadIdx.x] = acc;
+    __syncthreads();  // every group has read slice 0 before it is overwritten
+    if (grp == 0 && i < n4) {
+      float4 t = red[col];
+      for (int g = 1; g < G; ++g) {
+        const float4 v = red[g * L + col];
+        t.x += v.x; t.y += v.y; t.z += v.z; t.w += v.w;
+      }
+      p4[i] = t;
+    }
+    __syncthreads();  // red is reused by the next tile
+  }
+}
+
 void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& ws, float* const dW[3],
                        const float* bpart, int SB, float* const db[3], cudaStream_t st) {
   if (dev_skip("finish")) return;
@@ -977,6 +1032,17 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
   bool al16 = true;  // the transposing fold writes float4
   for (int i = 0; i < 3; ++i) al16 = al16 && ((uintptr_t)dW[i] % 16 == 0);
   if (P.kind == QD_KIND_CONV && P.C % 64 == 0 && P.r <= 7 && al16 && !getenv("QD_OLD_FINISH")) {
+    WSplits ws1 = ws;
+    if (S > 1 && dW[0] && !getenv("QD_FOLD_1PASS")) {
+      // sum the slices first (contiguous, all SMs busy), then transpose one slice
+      const long long n4 = (long long)P.Jd * P.Kf / 4;
+      const int L = 256 / (S >= 8 ? 8 : (S >= 4 ? 4 : 2));  // as in the kernel
+      const long long tiles = (n4 + L - 1) / L;
+      wsum_kernel<<<(unsigned)(tiles < 148 * 8 ? tiles : 148 * 8), 256, 0, st>>>(P, const_cast<float*>(wpart), S, ws);
+      count_launch(st, "wsum");
+      S = 1;
+      ws1.ng = 0;
+    }
     const int G = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1)), NJ = 8 / G;  // as in the kernel
     const int nwc = dW[0] ? (P.Jd + NJ - 1) / NJ * (P.Kf / P.K0) * (P.C / 64) : 0;
     const size_t smem = (size_t)8 * P.r * P.r * 17 * sizeof(float4);
@@ -986,13 +1052,13 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
       attr = smem;
     }
     if (P.r == 3)
-      wfinish_conv_kernel<9><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0],
+      wfinish_conv_kernel<9><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws1, dW[0], dW[1], dW[2], bpart, SB, db[0],
                                                            db[1], db[2], nwc);
     else if (P.r == 1)
-      wfinish_conv_kernel<1><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0],
+      wfinish_conv_kernel<1><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws1, dW[0], dW[1], dW[2], bpart, SB, db[0],
                                                            db[1], db[2], nwc);
     else
-      wfinish_conv_kernel<0><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0],
+      wfinish_conv_kernel<0><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws1, dW[0], dW[1], dW[2], bpart, SB, db[0],
                                                            db[1], db[2], nwc);
   } else {
     bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
