@@ -462,6 +462,7 @@ template <typename T>
 static int bn_forward_t(long long M, int C, const T* y, const float* gamma, const float* beta, float* rm, float* rv,
                         float momentum, float eps, int relu, int training, T* z, float* sm, float* si, char* ws,
                         cudaStream_t st) {
+  if (dev_skip("bn")) return QD_OK;
   const int S = bn_splits(M, C);
   float* part = (float*)ws;
   if (training) {
@@ -488,6 +489,7 @@ template <typename T>
 static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, const T* b, const float* gamma,
                            const float* beta, const float* sm, const float* si, int relu, T* D, float* dgamma,
                            float* dbeta, float* const db[3], char* ws, cudaStream_t st) {
+  if (dev_skip("bn")) return QD_OK;
   const long long M = P.Mout;
   const int C = P.F, S = bn_splits(M, C);
   float* part = (float*)ws;

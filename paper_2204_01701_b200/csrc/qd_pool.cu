@@ -160,6 +160,7 @@ int maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, 
   PoolGeo g;
   int rc = pool_geo(N, C, H, W, k, s, p, g);
   if (rc) return rc;
+  if (dev_skip("pool")) return QD_OK;
   const long long n = (long long)N * g.OH * g.OW * (C / 8);
   if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
@@ -176,6 +177,7 @@ int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype,
   PoolGeo g;
   int rc = pool_geo(N, C, H, W, k, s, p, g);
   if (rc) return rc;
+  if (dev_skip("pool")) return QD_OK;
   const long long n = (long long)N * H * W * (C / 8);
   if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
@@ -253,6 +255,7 @@ int im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, c
   if (Kp % 8 || Kp < r * r * C) return set_error(QD_ERR_CONFIG, "im2col: Kp %d (need a multiple of 8 >= %d)", Kp, r * r * C);
   const int OH = (H + 2 * p - r) / s + 1, OW = (W + 2 * p - r) / s + 1;
   if (OH < 1 || OW < 1) return set_error(QD_ERR_DIM, "im2col: empty output");
+  if (dev_skip("im2col")) return QD_OK;
   const long long blocks = (long long)N * OH * ((OW + IM2COL_TW - 1) / IM2COL_TW);
   if (blocks >= (1LL << 31)) return set_error(QD_ERR_DIM, "im2col: %lld blocks", blocks);
   const size_t es = dtype == QD_BF16 ? 2 : 4;

@@ -396,6 +396,7 @@ static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[
 
 void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
                      float momentum, float wd, int first, void* wpack, cudaStream_t st) {
+  if (dev_skip("sgd")) return;
   const int rr = P.r * P.r;
   // 32 x 32 tiles unless that leaves most SMs idle (small layers: 16 x 16)
   const bool big = (long long)P.nroles * ((P.F + 31) / 32) * ((P.C + 31) / 32) >= 2 * 148;
