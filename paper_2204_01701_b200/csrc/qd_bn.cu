@@ -16,6 +16,7 @@
 // NHWC [M][C] tensors; fp32 arithmetic for both dtypes.
 #include <stdio.h>
 #include "qd_kernels.h"
+#include "qd_ptx.cuh"
 
 namespace qd {
 
@@ -71,6 +72,8 @@ __global__ void __launch_bounds__(256) bn_reduce_vec_kernel(long long M, int C, 
                                                             const T* __restrict__ dz, const float* mean,
                                                             const float* invstd, const float* gamma,
                                                             const float* beta, int relu, float* part) {
+  ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
+  ptx::pdl_launch();
   __shared__ float red[2][256 * 8];
   const int CQ = C / 8, lanes = 256 / CQ;
   const int q = threadIdx.x % CQ, lane = threadIdx.x / CQ, c0 = q * 8;
@@ -140,6 +143,8 @@ __global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C
                                                            const float* mean, const float* invstd,
                                                            const float* gamma, const float* beta, int relu,
                                                            T* __restrict__ z) {
+  ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
+  ptx::pdl_launch();
   const int CQ = C / 8, lanes = 256 / CQ;
   const int q = threadIdx.x % CQ, c0 = q * 8;
   float sc[8], sh[8];
@@ -169,6 +174,8 @@ __global__ void __launch_bounds__(256) bn_emit_D_vec_kernel(Plan P, const T* __r
                                                             const float* invstd, const float* gamma,
                                                             const float* beta, const float* dgamma,
                                                             const float* dbeta, int relu, T* D, float* bpart) {
+  ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
+  ptx::pdl_launch();
   __shared__ float red[3][256 * 8];
   const long long M = P.Mout;
   const int C = P.F, CQ = C / 8, lanes = 256 / CQ;
@@ -349,6 +356,8 @@ template <typename T>
 __global__ void __launch_bounds__(1024) bn_stats_finalize(long long M, int C, int S, const T* y, const float* part,
                                                           float eps, float momentum, int training, float* run_mean,
                                                           float* run_var, float* save_mean, float* save_invstd) {
+  ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
+  ptx::pdl_launch();
   float s1, s2;
   if (!bn_fold2(C, S, part, s1, s2)) return;
   const int c = blockIdx.x * 32 + threadIdx.x;
@@ -379,6 +388,8 @@ __global__ void bn_apply_kernel(long long n, int C, const T* y, const float* mea
 
 __global__ void __launch_bounds__(1024) bn_grad_finalize(int C, int S, const float* part, float* dgamma,
                                                           float* dbeta) {
+  ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
+  ptx::pdl_launch();
   float s1, s2;
   if (!bn_fold2(C, S, part, s1, s2)) return;
   const int c = blockIdx.x * 32 + threadIdx.x;
@@ -467,18 +478,21 @@ static int bn_forward_t(long long M, int C, const T* y, const float* gamma, cons
   float* part = (float*)ws;
   if (training) {
     if (bn_vec(C))
-      bn_reduce_vec_kernel<T, 0><<<S, 256, 0, st>>>(M, C, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, part);
+      launch_pdl(bn_reduce_vec_kernel<T, 0>, dim3(S), dim3(256), 0, st, M, C, y, (const T*)nullptr, (const float*)nullptr,
+                 (const float*)nullptr, (const float*)nullptr, (const float*)nullptr, 0, part);
     else
       bn_reduce_kernel<T, 0><<<S, 256, 0, st>>>(M, C, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, part);
     count_launch(st, "bn_stats");
-    bn_stats_finalize<T><<<(C + 31) / 32, 1024, 0, st>>>(M, C, S, y, part, eps, momentum, 1, rm, rv, sm, si);
+    launch_pdl(bn_stats_finalize<T>, dim3((C + 31) / 32), dim3(1024), 0, st, M, C, S, y, (const float*)part, eps,
+               momentum, 1, rm, rv, sm, si);
     count_launch(st, "bn_stats_finalize");
   }
   const long long n = M * C;
   long long g = ((bn_vec(C) ? n / 8 : n) + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
   if (bn_vec(C))
-    bn_apply_vec_kernel<T><<<(int)g, 256, 0, st>>>(M, C, y, sm, si, gamma, beta, relu, z);
+    launch_pdl(bn_apply_vec_kernel<T>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, (const float*)sm, (const float*)si,
+               gamma, beta, relu, z);
   else
     bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z);
   count_launch(st, "bn_apply");
@@ -495,14 +509,15 @@ static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, c
   float* part = (float*)ws;
   float* bpart = part + (size_t)S * 2 * C;
   if (bn_vec(C))
-    bn_reduce_vec_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
+    launch_pdl(bn_reduce_vec_kernel<T, 1>, dim3(S), dim3(256), 0, st, M, C, y, dz, sm, si, gamma, beta, relu, part);
   else
     bn_reduce_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
   count_launch(st, "bn_bwd_reduce");
-  bn_grad_finalize<<<(C + 31) / 32, 1024, 0, st>>>(C, S, part, dgamma, dbeta);
+  launch_pdl(bn_grad_finalize, dim3((C + 31) / 32), dim3(1024), 0, st, C, S, (const float*)part, dgamma, dbeta);
   count_launch(st, "bn_bwd_finalize");
   if (bn_vec(C))
-    bn_emit_D_vec_kernel<T><<<S, 256, 0, st>>>(P, dz, y, a, b, sm, si, gamma, beta, dgamma, dbeta, relu, D, bpart);
+    launch_pdl(bn_emit_D_vec_kernel<T>, dim3(S), dim3(256), 0, st, P, dz, y, a, b, sm, si, gamma, beta,
+               (const float*)dgamma, (const float*)dbeta, relu, D, bpart);
   else
     bn_emit_D_kernel<T><<<S, 256, 0, st>>>(P, dz, y, a, b, sm, si, gamma, beta, dgamma, dbeta, relu, D, bpart);
   count_launch(st, "bn_emit_D");
