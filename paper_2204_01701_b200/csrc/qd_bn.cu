@@ -94,8 +94,36 @@ __global__ void __launch_bounds__(256) bn_reduce_vec_kernel(long long M, int C, 
         mu[e] = mean[c0 + e]; is[e] = invstd[c0 + e]; ga[e] = gamma[c0 + e]; be[e] = beta[c0 + e];
       }
     }
-#pragma unroll 4
-    for (long long r = r0 + lane; r < r1; r += lanes) {
+    long long r = r0 + lane;
+    constexpr int U = MODE == 0 ? 4 : 2;  // rows whose loads are issued before any use
+    for (; r + (U - 1) * lanes < r1; r += U * lanes) {
+      float v[U][8], gv[U][8];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        BV<T>::ld8(y + (size_t)(r + u * lanes) * C + c0, v[u]);
+        if (MODE != 0) BV<T>::ld8(dz + (size_t)(r + u * lanes) * C + c0, gv[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (MODE == 0) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float d = v[u][e] - K[e];
+            a0[e] += d;
+            a1[e] = fmaf(d, d, a1[e]);
+          }
+        } else {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            const float xh = (v[u][e] - mu[e]) * is[e];
+            const float gg = (relu && !(fmaf(ga[e], xh, be[e]) > 0.f)) ? 0.f : gv[u][e];
+            a0[e] += gg;
+            a1[e] = fmaf(gg, xh, a1[e]);
+          }
+        }
+      }
+    }
+    for (; r < r1; r += lanes) {
       float v[8];
       BV<T>::ld8(y + (size_t)r * C + c0, v);
       if (MODE == 0) {
@@ -154,8 +182,24 @@ __global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C
     sh[e] = beta[c0 + e] - sc[e] * mean[c0 + e];
   }
   const long long step = (long long)gridDim.x * lanes;
-#pragma unroll 4
-  for (long long r = (long long)blockIdx.x * lanes + threadIdx.x / CQ; r < rows; r += step) {
+  long long r = (long long)blockIdx.x * lanes + threadIdx.x / CQ;
+  // main loop: 4 rows whose loads are all issued before any use (a guarded
+  // single-row loop keeps one load in flight per thread: ~2.4 TB/s)
+  for (; r + 3 * step < rows; r += 4 * step) {
+    float v[4][8];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) BV<T>::ld8(y + (size_t)(r + u * step) * C + c0, v[u]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const float t = fmaf(sc[e], v[u][e], sh[e]);
+        v[u][e] = (relu && t < 0.f) ? 0.f : t;
+      }
+      BV<T>::st8(z + (size_t)(r + u * step) * C + c0, v[u]);
+    }
+  }
+  for (; r < rows; r += step) {
     float v[8];
     BV<T>::ld8(y + (size_t)r * C + c0, v);
 #pragma unroll
@@ -489,7 +533,8 @@ static int bn_forward_t(long long M, int C, const T* y, const float* gamma, cons
   }
   const long long n = M * C;
   long long g = ((bn_vec(C) ? n / 8 : n) + 255) / 256;
-  if (g > 148 * 16) g = 148 * 16;
+  if (bn_vec(C)) g = (g + 3) / 4;  // each thread takes >= 4 rows (the unguarded batch)
+  if (g > 148 * 8) g = 148 * 8;
   if (bn_vec(C))
     launch_pdl(bn_apply_vec_kernel<T>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, (const float*)sm, (const float*)si,
                gamma, beta, relu, z);
