@@ -8,6 +8,7 @@
 // sums, in a fixed window order, the output gradients whose recorded offset
 // points at it -- no atomics, deterministic, every store coalesced.
 #include <stdint.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "qd_kernels.h"
@@ -53,7 +54,9 @@ struct PoolGeo {
   int N, C, H, W, OH, OW, k, s, p;
 };
 
-template <typename T>
+// KW = window size at compile time (2, 3) so every window load of a thread is
+// issued before any use (a runtime-bound loop waits on each load in turn); 0 = runtime
+template <typename T, int KW>
 __global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __restrict__ x, T* __restrict__ y,
                                                           uint8_t* __restrict__ arg) {
   // 32-bit index math (the host checks the element count)
@@ -66,9 +69,10 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __
   t /= (unsigned)g.OW;
   const int oh = (int)(t % (unsigned)g.OH);
   const int n = (int)(t / (unsigned)g.OH);
+  const int k = KW ? KW : g.k;
   const int h0 = oh * g.s - g.p, w0 = ow * g.s - g.p;
   // torch's initial index: the window's first in-bounds position
-  const uint8_t first = (uint8_t)((h0 < 0 ? -h0 : 0) * g.k + (w0 < 0 ? -w0 : 0));
+  const uint8_t first = (uint8_t)((h0 < 0 ? -h0 : 0) * k + (w0 < 0 ? -w0 : 0));
   float best[8];
   uint8_t bi[8];
 #pragma unroll
@@ -76,21 +80,44 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __
     best[e] = -__int_as_float(0x7f800000);  // -inf: padding never wins
     bi[e] = first;
   }
-  for (int ky = 0; ky < g.k; ++ky) {
-    const int h = h0 + ky;
-    if (h < 0 || h >= g.H) continue;
-    for (int kx = 0; kx < g.k; ++kx) {
-      const int w = w0 + kx;
-      if (w < 0 || w >= g.W) continue;
-      float v[8];
-      PV<T>::ld8(x + (((size_t)n * g.H + h) * g.W + w) * g.C + cq * 8, v);
-      const uint8_t o = (uint8_t)(ky * g.k + kx);
+  const T* xn = x + ((size_t)n * g.H * g.W) * g.C + cq * 8;
+  if (KW) {
+    constexpr int KK = KW ? KW * KW : 1;
+    float v[KK][8];
+    bool ok[KK];
+#pragma unroll
+    for (int o = 0; o < KW * KW; ++o) {
+      const int h = h0 + o / KW, w = w0 + o % KW;
+      ok[o] = h >= 0 && h < g.H && w >= 0 && w < g.W;
+      if (ok[o]) PV<T>::ld8(xn + ((size_t)h * g.W + w) * g.C, v[o]);
+    }
+#pragma unroll
+    for (int o = 0; o < KW * KW; ++o) {
+      if (!ok[o]) continue;
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        if (v[e] > best[e] || v[e] != v[e]) {  // torch's rule: first maximum, a NaN always takes over
-          best[e] = v[e];
-          bi[e] = o;
+        if (v[o][e] > best[e] || v[o][e] != v[o][e]) {  // torch's rule: first maximum, a NaN always takes over
+          best[e] = v[o][e];
+          bi[e] = (uint8_t)o;
         }
+    }
+  } else {
+    for (int ky = 0; ky < k; ++ky) {
+      const int h = h0 + ky;
+      if (h < 0 || h >= g.H) continue;
+      for (int kx = 0; kx < k; ++kx) {
+        const int w = w0 + kx;
+        if (w < 0 || w >= g.W) continue;
+        float v[8];
+        PV<T>::ld8(xn + ((size_t)h * g.W + w) * g.C, v);
+        const uint8_t o = (uint8_t)(ky * k + kx);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (v[e] > best[e] || v[e] != v[e]) {
+            best[e] = v[e];
+            bi[e] = o;
+          }
+      }
     }
   }
   const size_t oidx = (size_t)i * 8;
@@ -101,7 +128,10 @@ __global__ void __launch_bounds__(256) maxpool_fwd_kernel(PoolGeo g, const T* __
   *reinterpret_cast<uint2*>(arg + oidx) = packed;
 }
 
-template <typename T>
+// backward gather; NW = max windows per axis covering one input position
+// (ceil(k / s): 2 for 3x3/2 and 2x2/2) at compile time so all index and
+// gradient loads of a thread are in flight together; 0 = runtime loop
+template <typename T, int NW>
 __global__ void __launch_bounds__(256) maxpool_bwd_kernel(PoolGeo g, const T* __restrict__ dy,
                                                           const uint8_t* __restrict__ arg, T* __restrict__ dx) {
   const unsigned c8 = g.C / 8;
@@ -123,23 +153,47 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(PoolGeo g, const T* __
   float acc[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) acc[e] = 0.f;
-  for (int oh = oh_lo; oh <= oh_hi; ++oh) {
-    const int ky = h - (oh * g.s - g.p);
-    for (int ow = ow_lo; ow <= ow_hi; ++ow) {
-      const int kx = w - (ow * g.s - g.p);
-      const uint8_t o = (uint8_t)(ky * g.k + kx);
-      const size_t oidx = ((((size_t)n * g.OH + oh) * g.OW + ow) * g.C) + cq * 8;
-      const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + oidx));
-      const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
-      bool any = false;
+  const size_t nbase = (size_t)n * g.OH * g.OW;
+  if (NW) {
+    constexpr int NN = NW ? NW * NW : 1;
+    uint2 av[NN];
+    float v[NN][8];
+    bool ok[NN];
+    uint8_t o[NN];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) any |= ab[e] == o;
-      if (!any) continue;
-      float v[8];
-      PV<T>::ld8(dy + oidx, v);
+    for (int u = 0; u < NW * NW; ++u) {
+      const int oh = oh_lo + u / NW, ow = ow_lo + u % NW;
+      ok[u] = oh <= oh_hi && ow <= ow_hi;
+      o[u] = (uint8_t)((h - (oh * g.s - g.p)) * g.k + (w - (ow * g.s - g.p)));
+      const size_t oidx = ((nbase + (size_t)oh * g.OW + ow) * g.C) + cq * 8;
+      if (ok[u]) {
+        av[u] = __ldg(reinterpret_cast<const uint2*>(arg + oidx));
+        PV<T>::ld8(dy + oidx, v[u]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < NW * NW; ++u) {
+      if (!ok[u]) continue;
+      const uint8_t* ab = reinterpret_cast<const uint8_t*>(&av[u]);
 #pragma unroll
       for (int e = 0; e < 8; ++e)
-        if (ab[e] == o) acc[e] += v[e];
+        if (ab[e] == o[u]) acc[e] += v[u][e];
+    }
+  } else {
+    for (int oh = oh_lo; oh <= oh_hi; ++oh) {
+      const int ky = h - (oh * g.s - g.p);
+      for (int ow = ow_lo; ow <= ow_hi; ++ow) {
+        const int kx = w - (ow * g.s - g.p);
+        const uint8_t o = (uint8_t)(ky * g.k + kx);
+        const size_t oidx = ((nbase + (size_t)oh * g.OW + ow) * g.C) + cq * 8;
+        const uint2 a = __ldg(reinterpret_cast<const uint2*>(arg + oidx));
+        const uint8_t* ab = reinterpret_cast<const uint8_t*>(&a);
+        float v[8];
+        PV<T>::ld8(dy + oidx, v);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          if (ab[e] == o) acc[e] += v[e];
+      }
     }
   }
   PV<T>::st8(dx + (size_t)i * 8, acc);
@@ -164,10 +218,18 @@ int maxpool_forward(int N, int C, int H, int W, int k, int s, int p, int dtype, 
   const long long n = (long long)N * g.OH * g.OW * (C / 8);
   if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  if (dtype == QD_BF16)
-    maxpool_fwd_kernel<bf16><<<blocks, 256, 0, st>>>(g, (const bf16*)x, (bf16*)y, (uint8_t*)arg);
-  else
-    maxpool_fwd_kernel<float><<<blocks, 256, 0, st>>>(g, (const float*)x, (float*)y, (uint8_t*)arg);
+#define QD_MPF(T, KW) maxpool_fwd_kernel<T, KW><<<blocks, 256, 0, st>>>(g, (const T*)x, (T*)y, (uint8_t*)arg)
+  // the runtime-loop forward measured at least as fast as the unrolled one (64 regs)
+  // on the ResNet stem pool; QD_MPF_UNROLL=1 selects the unrolled variant
+  static const bool unr = getenv("QD_MPF_UNROLL") != nullptr;
+  if (unr && k == 3) {
+    if (dtype == QD_BF16) QD_MPF(bf16, 3); else QD_MPF(float, 3);
+  } else if (unr && k == 2) {
+    if (dtype == QD_BF16) QD_MPF(bf16, 2); else QD_MPF(float, 2);
+  } else {
+    if (dtype == QD_BF16) QD_MPF(bf16, 0); else QD_MPF(float, 0);
+  }
+#undef QD_MPF
   count_launch(st, "maxpool_fwd");
   return check_launch("maxpool forward");
 }
@@ -181,10 +243,15 @@ int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype,
   const long long n = (long long)N * H * W * (C / 8);
   if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
-  if (dtype == QD_BF16)
-    maxpool_bwd_kernel<bf16><<<blocks, 256, 0, st>>>(g, (const bf16*)dy, (const uint8_t*)arg, (bf16*)dx);
-  else
-    maxpool_bwd_kernel<float><<<blocks, 256, 0, st>>>(g, (const float*)dy, (const uint8_t*)arg, (float*)dx);
+  // windows per axis covering an input position: ceil(k / s); 2 is the common case
+  const int nw = (k + s - 1) / s;
+#define QD_MPB(T, NW) maxpool_bwd_kernel<T, NW><<<blocks, 256, 0, st>>>(g, (const T*)dy, (const uint8_t*)arg, (T*)dx)
+  if (dtype == QD_BF16) {
+    if (nw == 2) QD_MPB(bf16, 2); else if (nw == 1) QD_MPB(bf16, 1); else QD_MPB(bf16, 0);
+  } else {
+    if (nw == 2) QD_MPB(float, 2); else if (nw == 1) QD_MPB(float, 1); else QD_MPB(float, 0);
+  }
+#undef QD_MPB
   count_launch(st, "maxpool_bwd");
   return check_launch("maxpool backward");
 }
