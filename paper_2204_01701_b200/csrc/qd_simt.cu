@@ -184,6 +184,8 @@ static void launch_pack_conv(const Plan& P, const float* const w[3], T* out, siz
   pack_conv_kernel<T><<<P.nb * P.F + P.C, 256, smem, st>>>(P, w[0], w[1], w[2], out);
 }
 
+// threads per tile block: 16 warps share a 32 x 32 tile's filter rows (more loads in flight)
+#define QD_SGD_THREADS 512
 template <typename T, int TF, int TC, int RR, bool UPD>
 __global__ void sgd_pack_tiled_kernel(Plan P, float* w0, float* w1, float* w2, float* m0, float* m1, float* m2,
                                       const float* g0, const float* g1, const float* g2, float lr, float mom,
@@ -194,7 +196,7 @@ static void launch_pack_tiled(const Plan& P, const float* const w[3], T* out, cu
   float* wm[3] = {(float*)w[0], (float*)w[1], (float*)w[2]};
   const size_t smem = (size_t)32 * (32 * 9 + 1) * 4;
   const int blocks = P.nroles * ((P.F + 31) / 32) * ((P.C + 31) / 32);
-  sgd_pack_tiled_kernel<T, 32, 32, 9, false><<<blocks, 256, smem, st>>>(P, wm[0], wm[1], wm[2], nullptr, nullptr,
+  sgd_pack_tiled_kernel<T, 32, 32, 9, false><<<blocks, QD_SGD_THREADS, smem, st>>>(P, wm[0], wm[1], wm[2], nullptr, nullptr,
                                                                           nullptr, nullptr, nullptr, nullptr, 0.f,
                                                                           0.f, 0.f, 0, out);
 }
@@ -293,7 +295,7 @@ __global__ void sgd_pack_kernel(Plan P, float* w0, float* w1, float* w2, float* 
 // pad float, an odd stride), phase 2 writes fprop rows (lane = channel), phase 3
 // dgrad rows (lane = filter) -- no per-element index division anywhere.
 template <typename T, int TF, int TC, int RR, bool UPD>  // RR = r*r at compile time (0: runtime)
-__global__ void __launch_bounds__(256) sgd_pack_tiled_kernel(Plan P, float* w0, float* w1, float* w2, float* m0,
+__global__ void __launch_bounds__(512) sgd_pack_tiled_kernel(Plan P, float* w0, float* w1, float* w2, float* m0,
                                                              float* m1, float* m2, const float* g0,
                                                              const float* g1, const float* g2, float lr, float mom,
                                                              float wd, int first, T* out) {
@@ -378,7 +380,7 @@ static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[
   const size_t smem = (size_t)TF * (TC * P.r * P.r + 1) * 4;
   const int blocks = P.nroles * ((P.F + TF - 1) / TF) * ((P.C + TC - 1) / TC);
   if (P.r == 3) {
-    sgd_pack_tiled_kernel<T, TF, TC, 9, true><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
+    sgd_pack_tiled_kernel<T, TF, TC, 9, true><<<blocks, QD_SGD_THREADS, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
                                                                     grad[0], grad[1], grad[2], lr, momentum, wd,
                                                                     first, out);
     return;
@@ -389,7 +391,7 @@ static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[
                          (int)smem);
     attr = smem;
   }
-  sgd_pack_tiled_kernel<T, TF, TC, 0, true><<<blocks, 256, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
+  sgd_pack_tiled_kernel<T, TF, TC, 0, true><<<blocks, QD_SGD_THREADS, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
                                                                   grad[0], grad[1], grad[2], lr, momentum, wd,
                                                                   first, out);
 }
