@@ -52,6 +52,14 @@ WORKLOADS = {
     "c5_t2and4_64x56": ("t2and4", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
     "dw_proposed_256x28": ("proposed", "dwconv", 64, 256, 256, 28, 28, 3, 1, 1, "bf16"),
     # QuadraVGG-16 layer shapes at its bench batch (per-layer profiling)
+    # QuadraResNet-18 quadratic layers (batch 128; stride-2 = first conv of stages 2-4)
+    "r18_64x56": ("proposed", "conv", 128, 64, 64, 56, 56, 3, 1, 1, "bf16"),
+    "r18_s2_64x56": ("proposed", "conv", 128, 64, 128, 56, 56, 3, 2, 1, "bf16"),
+    "r18_128x28": ("proposed", "conv", 128, 128, 128, 28, 28, 3, 1, 1, "bf16"),
+    "r18_s2_128x28": ("proposed", "conv", 128, 128, 256, 28, 28, 3, 2, 1, "bf16"),
+    "r18_256x14": ("proposed", "conv", 128, 256, 256, 14, 14, 3, 1, 1, "bf16"),
+    "r18_s2_256x14": ("proposed", "conv", 128, 256, 512, 14, 14, 3, 2, 1, "bf16"),
+    "r18_512x7": ("proposed", "conv", 128, 512, 512, 7, 7, 3, 1, 1, "bf16"),
     "vgg_64x32": ("proposed", "conv", 256, 64, 64, 32, 32, 3, 1, 1, "bf16"),
     "vgg_128x16": ("proposed", "conv", 256, 128, 128, 16, 16, 3, 1, 1, "bf16"),
     "vgg_256x8": ("proposed", "conv", 256, 256, 256, 8, 8, 3, 1, 1, "bf16"),

@@ -15,7 +15,8 @@ the running statistics.
   then the layer's wgrad / dgrad kernels run from D (``QD_FLAG_D_GIVEN``).
   The BN-backward output dy is never materialised.
 
-Layers the fused backward does not cover (stride 2, t3, T1 families, dwconv)
+Layers the fused backward does not cover (stride 2 off the direct path, t3,
+T1 families, dwconv)
 use the same reference BN semantics through torch ops (autograd).
 """
 
@@ -194,10 +195,20 @@ class QuadConvBN(nn.Module):
         self.bias = nn.Parameter(torch.zeros(c, device=dev))
         self.bn = _BNState(c, momentum, eps, dev)
 
-    def fused(self):
+    def fused(self, x=None):
         sp = self.layer.spec
         if os.environ.get("QD_NO_BNFUSE"):
             return False
+        if sp.stride == 2:
+            # stride 2 fuses when the layer runs on its own output grid (the
+            # library's tc_s2_direct: tcgen05 path, plain-K family, k >= 2), so
+            # the emitted D is the operand its backward consumes as is
+            if x is None or sp.kind != "conv" or sp.family not in ("proposed", "t4", "first_order"):
+                return False
+            oh = (x.shape[2] + 2 * sp.pad - sp.kernel) // 2 + 1
+            ow = (x.shape[3] + 2 * sp.pad - sp.kernel) // 2 + 1
+            return (sp.kernel >= 2 and oh <= 128 and ow <= 128 and self.layer.compute_dtype == torch.bfloat16
+                    and neurons.device_path(sp, tuple(x.shape), torch.bfloat16) == 1)
         return (sp.stride == 1 and sp.kind in ("conv", "fc") and sp.family not in ("t3", "t1_pure", "t1_full",
                                                                                    "t1and2"))
 
@@ -205,7 +216,7 @@ class QuadConvBN(nn.Module):
         spec = self.layer.spec
         roles = tuple(param_shapes(spec).keys())
         tensors = [getattr(self.layer, r) for r in roles]
-        if self.training and self.fused():
+        if self.training and self.fused(x):
             return _QuadBNFunction.apply(spec, self.layer.compute_dtype, self.relu, self.bn, x, self.weight,
                                          self.bias, *tensors)
         y = QuadFunction.apply(spec, self.layer.compute_dtype, x, *tensors)

@@ -102,7 +102,7 @@ Workspace plan_workspace(const Plan& P, int path) {
     L.sz_P = (a > b ? a : b) * 4;
   }
   // stride-2 layers on the tcgen05 path run their backward on the stride-1 grid
-  const Plan Pg = (path == 1 && P.s == 2) ? stride1_plan(P) : P;
+  const Plan Pg = (path == 1 && P.s == 2 && !tc_s2_direct(P)) ? stride1_plan(P) : P;
   if (caches_ab(P.family) || P.family == QD_FAM_T3 || Pg.s != P.s) L.sz_D = (size_t)Pg.Mout * P.Jd * es;
   if (path == 1 && P.family == QD_FAM_T2AND4) L.sz_ZB = (size_t)3 * P.F * 4;
   if (path == 0) {
@@ -338,8 +338,11 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* 
   bool cache = caches_ab(P.family) && !dgiven;
   if (cache && (!a_cache || !b_cache))
     return set_error(QD_ERR_INTEGRITY, "cache for this family must hold a and b");
-  if (dgiven && (P.s != 1 || P.family == QD_FAM_T3 || is_t1(P.family) || P.kind == QD_KIND_DWCONV))
-    return set_error(QD_ERR_UNSUPPORTED, "QD_FLAG_D_GIVEN: stride-1 fc / conv layers, not t3 / T1");
+  // stride 2 only on its own output grid (the D the caller emits is on that grid)
+  const bool s2ok = P.s == 2 && tc_supported(P, d->flags) && tc_s2_direct(P);
+  if (dgiven && ((P.s != 1 && !s2ok) || P.family == QD_FAM_T3 || is_t1(P.family) || P.kind == QD_KIND_DWCONV))
+    return set_error(QD_ERR_UNSUPPORTED,
+                     "QD_FLAG_D_GIVEN: stride-1 fc / conv layers or direct stride-2 convs, not t3 / T1");
   if (!(d->flags & QD_FLAG_NO_DX) && !dx) return set_error(QD_ERR_ARG, "dx is NULL");
   float* nof[3] = {nullptr, nullptr, nullptr};
   float* const* w = (dW && !(d->flags & QD_FLAG_NO_DW)) ? dW : nof;

@@ -162,7 +162,9 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
               int pdl_wait = 1);
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                 int tiles_nn, int Cout, int nbias);
-// stride-2 layers run as their stride-1 equivalent: forward subsamples the
+// stride 2 on its own output grid (strided x maps, parity-class dgrad)
+bool tc_s2_direct(const Plan& P);
+// otherwise stride-2 layers run as their stride-1 equivalent: forward subsamples the
 // output, backward uses the zero-upsampled gradient operand
 inline Plan stride1_plan(const Plan& P) {
   Plan Q = P;

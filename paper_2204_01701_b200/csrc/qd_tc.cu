@@ -48,7 +48,38 @@ struct ConvArgs {
   int ksplit, kb_per, part_ld;
   long long Mpix;
   float* part;
+  // stride 2 without the stride-1 grid: the fprop's A map walks x with traversal
+  // stride `sstride` (box origin sstride * output + tap - pad); the dgrad runs as
+  // four output-parity classes (cls = 1): class (ph, pw) is a stride-1 conv of D
+  // over the taps with ey = ph + pad_eff (mod 2) (resp. ex), D row offset
+  // (ph + ey - pad_eff) / 2, written to dx pixels (2h + ph, 2w + pw)
+  int sstride;
+  int cls, cls_tiles;       // class mode; tiles per class (all classes share the grid)
+  int cls_code[4];          // per class in work order: ph | pw << 1 | k-blocks << 2
+  int Hx, Wx;               // dx extent (class mode)
+  bf16* out;                // dx, direct row stores (class mode)
 };
+
+// work item -> (tile, K slice, parity class, k-block range)
+struct ConvWork { int t, ks, ph, pw, kb0, kb1; };
+__device__ __forceinline__ ConvWork conv_work(const ConvArgs& a, int wi, int KB) {
+  ConvWork w;
+  if (a.cls) {
+    const int ci = wi / a.cls_tiles;
+    int code = a.cls_code[0];
+#pragma unroll
+    for (int i = 1; i < 4; ++i)  // static indexing: no local copy of the array
+      if (i == ci) code = a.cls_code[i];
+    w.t = wi - ci * a.cls_tiles; w.ks = 0;
+    w.ph = code & 1; w.pw = (code >> 1) & 1;
+    w.kb0 = 0; w.kb1 = code >> 2;
+    return w;
+  }
+  w.t = wi / a.ksplit; w.ks = wi - w.t * a.ksplit;
+  w.ph = w.pw = 0;
+  w.kb0 = w.ks * a.kb_per; w.kb1 = min(KB, w.kb0 + a.kb_per);
+  return w;
+}
 
 template <int EPI, int NB>
 struct ConvCfg {
@@ -128,7 +159,7 @@ __global__ void __launch_bounds__(256, 1)
   const uint32_t tmem_base = *tmem_slot;
 
   const int KB = args.kb_half * (args.dual ? 2 : 1);
-  const int NWORK = args.total_tiles * args.ksplit;
+  const int NWORK = args.cls ? 4 * args.cls_tiles : args.total_tiles * args.ksplit;
 
   if (warp == 0) {
     if (lane == 0) {
@@ -136,25 +167,38 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t bytes = (uint32_t)(args.box_rows * 128 + Cfg::B_BYTES);
+      const int ss = args.sstride;
       for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x) {
-        const int t = wi / args.ksplit, ks = wi - t * args.ksplit;
-        const int kb0 = ks * args.kb_per, kb1 = min(KB, kb0 + args.kb_per);
+        const ConvWork cw = conv_work(args, wi, KB);
+        const int t = cw.t;
         int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
         int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
         int tn = mt / (args.tiles_w * args.tiles_h);
         int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
-        for (int kb = kb0; kb < kb1; ++kb) {
+        // class mode: first tap of the class's parity and its tap count along x
+        const int ey0 = (args.pad_eff - cw.ph) & 1, ex0 = (args.pad_eff - cw.pw) & 1;
+        const int ntx = (args.r - ex0 + 1) >> 1;
+        for (int kb = cw.kb0; kb < cw.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           ptx::mbar_arrive_expect_tx(&full[stage], bytes);
           int half = kb / args.kb_half, kk = kb % args.kb_half;
           int tap = kk / args.cblks, cb = kk % args.cblks;
-          int ey = tap / args.r, ex = tap % args.r;
+          int ax, ay, bk = kb;
+          if (args.cls) {
+            const int ty = tap / ntx, ey = ey0 + 2 * ty, ex = ex0 + 2 * (tap - ty * ntx);
+            ay = h0 + ((cw.ph + ey - args.pad_eff) >> 1);  // even numerator: exact
+            ax = w0 + ((cw.pw + ex - args.pad_eff) >> 1);
+            bk = (ey * args.r + ex) * args.cblks + cb;
+          } else {
+            int ey = tap / args.r, ex = tap % args.r;
+            ax = ss * w0 + ex - args.pad_eff;
+            ay = ss * h0 + ey - args.pad_eff;
+          }
           const CUtensorMap* ma = half ? &mapA1 : &mapA0;
-          ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, w0 + ex - args.pad_eff,
-                           h0 + ey - args.pad_eff, n0);
+          ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
 #pragma unroll
           for (int i = 0; i < NB; ++i)
-            ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, kb * 64,
+            ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, bk * 64,
                              ntile * args.b_rs_tile + i * args.b_rs_blk);
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
@@ -171,8 +215,8 @@ __global__ void __launch_bounds__(256, 1)
     uint32_t phase = 0;
     int it = 0;
     for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x, ++it) {
-      const int ks = wi % args.ksplit;
-      const int kb0 = ks * args.kb_per, kb1 = min(KB, kb0 + args.kb_per);
+      const ConvWork cw = conv_work(args, wi, KB);
+      const int kb0 = cw.kb0, kb1 = cw.kb1;
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
       ptx::mbar_wait(&tempty[as], aph ^ 1);
@@ -203,13 +247,51 @@ __global__ void __launch_bounds__(256, 1)
     const int etid = threadIdx.x - 128;
     int it = 0;
     for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x, ++it) {
-      const int t = wi / args.ksplit, ks = wi - t * args.ksplit;
+      const ConvWork cw = conv_work(args, wi, KB);
+      const int t = cw.t, ks = cw.ks;
       int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
       int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
       int tn = mt / (args.tiles_w * args.tiles_h);
       int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
+      if (EPI == EPI_PLAIN && args.cls) {
+        // parity class (ph, pw): each row is one dx pixel (2h + ph, 2w + pw), its
+        // NB x 64 channels stored straight from registers (full 128-B lines)
+        ptx::mbar_wait(&tfull[as], aph);
+        ptx::tc_fence_after();
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + as * Cfg::ACC_COLS;
+        const int ww = row % args.Wb, hh = (row / args.Wb) % args.Hb, nn = row / (args.Wb * args.Hb);
+        const int n = n0 + nn, h = h0 + hh, w = w0 + ww;
+        const int ih = 2 * h + cw.ph, iw = 2 * w + cw.pw;
+        const bool ok = row < args.box_rows && n < args.Ng && h < args.OHg && w < args.OWg && ih < args.Hx &&
+                        iw < args.Wx;
+        bf16* orow = args.out + (((size_t)n * args.Hx + ih) * args.Wx + iw) * args.Cout + ntile * args.out_c_tile;
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          float v[NB][16];
+#pragma unroll
+          for (int i = 0; i < NB; ++i) ptx::tmem_ld16(tb + i * 64 + j * 16, v[i]);
+          ptx::tmem_wait_ld();
+          if (ok) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i) {
+              uint4 lo, hi;
+              lo.x = pack_bf16x2(v[i][0], v[i][1]);   lo.y = pack_bf16x2(v[i][2], v[i][3]);
+              lo.z = pack_bf16x2(v[i][4], v[i][5]);   lo.w = pack_bf16x2(v[i][6], v[i][7]);
+              hi.x = pack_bf16x2(v[i][8], v[i][9]);   hi.y = pack_bf16x2(v[i][10], v[i][11]);
+              hi.z = pack_bf16x2(v[i][12], v[i][13]); hi.w = pack_bf16x2(v[i][14], v[i][15]);
+              uint4* op = reinterpret_cast<uint4*>(orow + i * 64 + j * 16);
+              op[0] = lo;
+              op[1] = hi;
+            }
+          }
+        }
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+        continue;
+      }
       if (args.part) {
         // split-K slice: raw fp32 accumulator rows into the partial buffer
         ptx::mbar_wait(&tfull[as], aph);
@@ -443,6 +525,7 @@ struct WgArgs {
   int pt_w, pt_h, ptiles;               // pixel tiles along w, h; total
   int r, pad, cblks, kb_half, nkb;      // 64-row k-block decode
   int Jd, Kf;
+  int sstride;                          // x traversal stride (stride-2 layers, strided x maps)
   float* part;                          // [splits][Jd][Kf]
 };
 
@@ -518,7 +601,7 @@ __global__ void __launch_bounds__(256, 1)
           int tap = kk / args.cblks, cb = kk % args.cblks;
           int ey = tap / args.r, ex = tap % args.r;
           ptx::tma_load_4d(half ? &mapX1 : &mapX0, &full[stage], sA + stage * Cfg::A_BYTES + a * 8192, cb * 64,
-                           w0 + ex - args.pad, h0 + ey - args.pad, n0);
+                           args.sstride * w0 + ex - args.pad, args.sstride * h0 + ey - args.pad, n0);
         }
 #pragma unroll
         for (int i = 0; i < NBLK; ++i)
@@ -806,6 +889,17 @@ static bool s2_fits(const Plan& P) {
   return wgrad2_split(P1) > 0;
 }
 
+// stride 2 on its own output grid (v1 kernels): fprop and wgrad read x through
+// traversal-stride-2 TMA maps, the dgrad runs as four output-parity classes of
+// D (no zero-upsampled operand, no 4x work). Every class needs a tap (r >= 2);
+// the squared-input families keep the stride-1-grid path (x*x operand, EPI_SQ
+// dgrad). QD_S2_UPSAMPLE=1 forces the stride-1-grid path (A/B checks).
+bool tc_s2_direct(const Plan& P) {
+  static const bool off = getenv("QD_S2_UPSAMPLE") && atoi(getenv("QD_S2_UPSAMPLE"));
+  return P.s == 2 && P.kind == QD_KIND_CONV && P.r >= 2 && P.sq == 0 && P.family != QD_FAM_T3 && !off &&
+         P.OW <= 128 && P.OH <= 128 && P.dtype == QD_BF16 && P.C % 64 == 0 && P.F % 64 == 0;
+}
+
 bool tc_supported(const Plan& P, unsigned flags) {
   if (flags & QD_FLAG_FORCE_SIMT) return false;
   if (P.dtype != QD_BF16) return false;
@@ -814,17 +908,20 @@ bool tc_supported(const Plan& P, unsigned flags) {
   if (!init_driver()) return false;
   if (P.s == 1) return true;
   if (P.family == QD_FAM_T3) return false;  // t3 stride 2: CUDA-core path
+  if (tc_s2_direct(P)) return true;
   return !(flags & QD_FLAG_TC_V1) && s2_fits(P);
 }
 
-static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint32_t* box) {
+static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* dims, const cuuint32_t* box,
+                    int trav = 1) {
   cuuint64_t strides[4];
   cuuint64_t acc = dims[0] * 2;
   for (int i = 1; i < rank; ++i) {
     strides[i - 1] = acc;
     acc *= dims[i];
   }
-  cuuint32_t es[5] = {1, 1, 1, 1, 1};
+  // trav > 1: traversal stride along W and H (the box spans trav x the pixels it loads)
+  cuuint32_t es[5] = {1, (cuuint32_t)trav, (cuuint32_t)trav, 1, 1};
   CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                         CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
@@ -832,11 +929,13 @@ static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t*
   return QD_OK;
 }
 
-// NHWC activation map with a (64, Wb, Hb, Nb) box
-static int map_act(CUtensorMap* m, const void* p, int Cch, int W, int H, int N, int Wb, int Hb, int Nb) {
+// NHWC activation map with a (64, Wb, Hb, Nb) box; trav = 2 loads every second
+// pixel along W and H (Wb x Hb pixels from a 2Wb x 2Hb window)
+static int map_act(CUtensorMap* m, const void* p, int Cch, int W, int H, int N, int Wb, int Hb, int Nb,
+                   int trav = 1) {
   cuuint64_t dims[4] = {(cuuint64_t)Cch, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
-  cuuint32_t box[4] = {64, (cuuint32_t)Wb, (cuuint32_t)Hb, (cuuint32_t)Nb};
-  return make_map(m, p, 4, dims, box);
+  cuuint32_t box[4] = {64, (cuuint32_t)(Wb * trav), (cuuint32_t)(Hb * trav), (cuuint32_t)Nb};
+  return make_map(m, p, 4, dims, box, trav);
 }
 static int map_rows(CUtensorMap* m, const void* p, int K, int rows) {
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
@@ -891,7 +990,7 @@ static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
     cudaFuncSetAttribute(conv_gemm_kernel<EPI, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
   }
-  const int nwork = args.total_tiles * args.ksplit;
+  const int nwork = args.cls ? 4 * args.cls_tiles : args.total_tiles * args.ksplit;
   int grid = nwork < g_num_sms ? nwork : g_num_sms;
   conv_gemm_kernel<EPI, NB><<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
   count_launch(st, "conv_gemm");
@@ -989,12 +1088,13 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
                     int OWg, int OHg, int pad_eff, int r, int dual, const void* wmat, int wrows, int wK,
                     int b_rs_tile, int b_rs_blk, int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2,
                     int Cout, const float* const bias[3], const void* xres, cudaStream_t st,
-                    float* skpart = nullptr, size_t skbytes = 0) {
+                    float* skpart = nullptr, size_t skbytes = 0, int trav = 1, int cls = 0, int Hx = 0,
+                    int Wx = 0) {
   Box bx = choose_box(OWg, OHg, N, 128, false);
   CUtensorMap A0, A1, B, O0, O1, O2;
   int rc;
-  if ((rc = map_act(&A0, a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
-  if ((rc = map_act(&A1, a1 ? a1 : a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
+  if ((rc = map_act(&A0, a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb, trav))) return rc;
+  if ((rc = map_act(&A1, a1 ? a1 : a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb, trav))) return rc;
   if ((rc = map_rows(&B, wmat, wK, wrows))) return rc;
   if ((rc = map_act(&O0, o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
   if ((rc = map_act(&O1, o1 ? o1 : o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
@@ -1020,6 +1120,27 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
     g.kb_per = (KB + S - 1) / S;
     g.ksplit = (KB + g.kb_per - 1) / g.kb_per;
     g.part = skpart;
+  }
+  g.sstride = trav;
+  if (cls) {
+    if (epi != EPI_PLAIN || dual) return set_error(QD_ERR_UNSUPPORTED, "parity-class dgrad: plain epilogue only");
+    // the four output-parity classes of a stride-2 dgrad, most k-blocks first
+    // (static round-robin over the persistent grid then balances like LPT)
+    int code[4], n = 0;
+    for (int ph = 0; ph < 2; ++ph)
+      for (int pw = 0; pw < 2; ++pw) {
+        const int nty = (r - ((pad_eff - ph) & 1) + 1) / 2, ntx = (r - ((pad_eff - pw) & 1) + 1) / 2;
+        if (nty < 1 || ntx < 1) return set_error(QD_ERR_UNSUPPORTED, "parity class without taps");
+        code[n++] = ph | pw << 1 | (nty * ntx * g.cblks) << 2;
+      }
+    for (int i = 0; i < 4; ++i)
+      for (int j = i + 1; j < 4; ++j)
+        if ((code[j] >> 2) > (code[i] >> 2)) { int t = code[i]; code[i] = code[j]; code[j] = t; }
+    for (int i = 0; i < 4; ++i) g.cls_code[i] = code[i];
+    g.cls = 1;
+    g.cls_tiles = g.total_tiles;
+    g.Hx = Hx; g.Wx = Wx;
+    g.out = (bf16*)o0;
   }
 #define QD_LC(E, NBV) launch_conv_split<E, NBV>(A0, A1, B, O0, O1, O2, g, o0, o1, o2, st)
   if (epi == EPI_PROPOSED) return QD_LC(EPI_PROPOSED, 3);
@@ -1114,6 +1235,11 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
     launch_square_out(P, y, st);
     return check_launch("t3 forward");
   }
+  if (tc_s2_direct(P)) {
+    if (dev_skip("fprop")) return QD_OK;
+    return run_conv(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 0, wpack, P.nb * P.F, P.Kf,
+                    c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st, nullptr, 0, 2);
+  }
   if (P.s == 2) {
     // stride-1 grid, epilogue keeps the even positions
     Plan P1 = stride1_plan(P);
@@ -1157,8 +1283,10 @@ static void join_side(cudaStream_t st, cudaStream_t side) {
 int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
                 void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L,
                 cudaStream_t st) {
-  // stride-2 layers: the GEMMs run on the stride-1 grid over the zero-upsampled D
-  const bool up = P0.s == 2;
+  // stride-2 layers: on their own grid when tc_s2_direct, else the GEMMs run on
+  // the stride-1 grid over the zero-upsampled D
+  const bool s2d = tc_s2_direct(P0);
+  const bool up = P0.s == 2 && !s2d;
   const Plan P = up ? stride1_plan(P0) : P0;
   const bf16* wd = (const bf16*)wpack + pack_fprop_elems(P);
   const bool mat = caches_ab(P.family);
@@ -1256,8 +1384,8 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     } else {
     Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
     CUtensorMap X0, X1, Dm;
-    if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
-    if ((rc = map_act(&X1, x1, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
+    if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
+    if ((rc = map_act(&X1, x1, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
     if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
     WgArgs g;
     memset(&g, 0, sizeof(g));
@@ -1270,6 +1398,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     g.pt_w = pb.tw; g.pt_h = pb.th; g.ptiles = pb.tw * pb.th * pb.tn;
     g.r = P.r; g.pad = P.p; g.cblks = P.C / 64; g.kb_half = P.K0 / 64;
     g.Jd = P.Jd; g.Kf = P.Kf;
+    g.sstride = P.s;
     g.part = (float*)(ws + L.off_WG);
     if (nblk == 4) rc = launch_wgrad<4>(X0, X1, Dm, g, st);
     else if (nblk == 3) rc = launch_wgrad<3>(X0, X1, Dm, g, st);
@@ -1293,6 +1422,10 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     rc = QD_ERR_UNSUPPORTED;
     if (part) set_conv2_cap(dg_pairs);
     if (dev_skip("dgrad")) rc = QD_OK;
+    else if (s2d)
+      rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, (P.W + 1) / 2, (P.H + 1) / 2, pad_eff, P.r, 0,
+                    wd, P.Cd, P.Kd, c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C,
+                    nob, xr, st, nullptr, 0, 1, 1, P.H, P.W);
     else if (!(P.flags & QD_FLAG_TC_V1))
       // D is complete once the (PDL-launched) v2/v3 wgrad is running, and nothing
       // the dgrad reads is written by it: the dgrad need not wait for the wgrad

@@ -116,11 +116,18 @@ TC_CASES = [
     ("first_order", "conv", 2, 64, 128, 16, 16, 3, 1, 1),
     ("proposed", "conv", 2, 64, 64, 13, 17, 2, 1, 0),
     ("proposed", "conv", 2, 64, 64, 12, 12, 5, 1, 2),
-    # stride 2 (ResNet downsampling): stride-1 grid + subsampled epilogue /
-    # zero-upsampled gradient operand
+    # stride 2 (ResNet downsampling) on its own output grid: traversal-stride-2
+    # x maps for the fprop / wgrad, four output-parity classes for the dgrad
+    # (odd H / W: classes of unequal size; k2 p0 / k5 p2: other tap parities);
+    # t2_linear keeps the stride-1 grid + subsampled epilogue / upsampled operand
     ("proposed", "conv", 2, 64, 128, 28, 28, 3, 2, 1),
     ("proposed", "conv", 3, 64, 64, 29, 27, 3, 2, 1),
+    ("proposed", "conv", 4, 128, 256, 14, 14, 3, 2, 1),
+    ("proposed", "conv", 2, 64, 64, 15, 13, 2, 2, 0),
+    ("proposed", "conv", 3, 64, 64, 11, 10, 5, 2, 2),
     ("t4", "conv", 2, 64, 64, 16, 16, 3, 2, 1),
+    ("t4", "conv", 5, 128, 64, 8, 8, 3, 2, 1),
+    ("first_order", "conv", 2, 64, 128, 16, 16, 3, 2, 1),
     ("t2_linear", "conv", 2, 64, 64, 16, 18, 3, 2, 1),
     ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
     ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
@@ -455,15 +462,16 @@ def test_quadconvbn_fused_matches_reference_bn(family, kind, relu):
 
 
 @pytest.mark.gpu
-def test_quadconvbn_stride2_bn_only_path():
-    """stride 2: the layer backward runs unfused; BN(+ReLU) still on the BN kernels"""
+def test_quadconvbn_stride2_fused_path():
+    """stride 2 on its own grid: BN(+ReLU) fused, D emitted on the stride-2
+    output grid and consumed by the strided wgrad / parity-class dgrad"""
     from paper_2204_01701_b200.bn import QuadConvBN, _ref_batchnorm
     from paper_2204_01701_b200.nn import QuadConv2d, QuadFunction
     torch.manual_seed(4)
     layer = QuadConv2d(64, 128, 3, 2, 1, device="cuda")
     mod = QuadConvBN(layer, relu=True)
-    assert not mod.fused()
     x0 = torch.randn(4, 64, 16, 16, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    assert mod.fused(x0) and not mod.fused()
     gz = torch.randn(4, 128, 8, 8, device="cuda").bfloat16()
     x1 = x0.clone().requires_grad_(True)
     mod(x1).backward(gz)
