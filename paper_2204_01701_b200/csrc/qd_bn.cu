@@ -31,6 +31,11 @@ static int bn_splits(long long M, int C) {
 // 8-channel vector kernels when C % 8 == 0 and C / 8 <= 256
 static bool bn_vec(int C) { return C % 8 == 0 && C / 8 <= 256 && 256 % (C / 8) == 0; }
 
+// 4-channel chunks (the backward kernels: their per-channel constants and
+// partial sums would otherwise hold 8 x 12 registers per thread and halve the
+// resident warps of these HBM-bound passes)
+static bool bn_c4(int C) { return C % 4 == 0 && C / 4 <= 256 && 256 % (C / 4) == 0; }
+
 template <typename T> struct BV;
 template <> struct BV<bf16> {
   __device__ static void ld8(const bf16* p, float v[8]) {
@@ -42,6 +47,19 @@ template <> struct BV<bf16> {
       v[2 * e] = f.x;
       v[2 * e + 1] = f.y;
     }
+  }
+  __device__ static void ld4(const bf16* p, float v[4]) {
+    uint2 u = __ldg(reinterpret_cast<const uint2*>(p));
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+    float2 f0 = __bfloat1622float2(h[0]), f1 = __bfloat1622float2(h[1]);
+    v[0] = f0.x; v[1] = f0.y; v[2] = f1.x; v[3] = f1.y;
+  }
+  __device__ static void st4(bf16* p, const float v[4]) {
+    uint2 u;
+    __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
+    u.x = *reinterpret_cast<uint32_t*>(&h0);
+    u.y = *reinterpret_cast<uint32_t*>(&h1);
+    *reinterpret_cast<uint2*>(p) = u;
   }
   __device__ static void st8(bf16* p, const float v[8]) {
     uint4 u;
@@ -58,6 +76,13 @@ template <> struct BV<float> {
   __device__ static void ld8(const float* p, float v[8]) {
     float4 a = __ldg(reinterpret_cast<const float4*>(p)), b = __ldg(reinterpret_cast<const float4*>(p) + 1);
     v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  }
+  __device__ static void ld4(const float* p, float v[4]) {
+    float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+  __device__ static void st4(float* p, const float v[4]) {
+    *reinterpret_cast<float4*>(p) = make_float4(v[0], v[1], v[2], v[3]);
   }
   __device__ static void st8(float* p, const float v[8]) {
     reinterpret_cast<float4*>(p)[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -212,15 +237,21 @@ __global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C
 }
 
 template <typename T>
-__global__ void __launch_bounds__(256) bn_emit_D_vec_kernel(Plan P, const T* __restrict__ dz,
-                                                            const T* __restrict__ y, const T* __restrict__ a,
-                                                            const T* __restrict__ b, const float* mean,
-                                                            const float* invstd, const float* gamma,
-                                                            const float* beta, const float* dgamma,
-                                                            const float* dbeta, int relu, T* D, float* bpart) {
+__global__ void __launch_bounds__(256, 3) bn_emit_D_vec_kernel(Plan P, const T* __restrict__ dz,
+                                                               const T* __restrict__ y, const T* __restrict__ a,
+                                                               const T* __restrict__ b, const float* mean,
+                                                               const float* invstd, const float* gamma,
+                                                               const float* beta, const float* dgamma,
+                                                               const float* dbeta, int relu, T* __restrict__ D,
+                                                               float* bpart) {
   ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
   ptx::pdl_launch();
-  __shared__ float red[3][256 * 8];
+  // per-channel constants in shared memory (registers go to the loads in flight:
+  // 3 blocks per SM); the same buffer takes the partial-sum fold afterwards.
+  //   dy = kA g' + kC y + kB, g' = g masked where kA y + kQ <= 0 (the forward
+  //   apply's z = kA y + kQ, same fmaf); kA = gamma inv, kC = -gamma inv^2 dgamma / M,
+  //   kB = -gamma inv dbeta / M - kC mean
+  __shared__ __align__(16) float sm[4 * 2048];
   const long long M = P.Mout;
   const int C = P.F, CQ = C / 8, lanes = 256 / CQ;
   const int q = threadIdx.x % CQ, lane = threadIdx.x / CQ, c0 = q * 8;
@@ -230,34 +261,54 @@ __global__ void __launch_bounds__(256) bn_emit_D_vec_kernel(Plan P, const T* __r
   long long r1 = r0 + rows;
   if (r1 > M) r1 = M;
   const bool mat = caches_ab(P.family), hasg = d_has_g(P.family);
+  float* kA = sm;
+  float* kB = sm + C;
+  float* kC = sm + 2 * C;
+  float* kQ = sm + 3 * C;
+  {
+    const float inv_m = 1.f / (float)M;
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      const float mu = mean[c], is = invstd[c];
+      const float ka = gamma[c] * is, kc = -ka * is * dgamma[c] * inv_m;
+      kA[c] = ka;
+      kQ[c] = beta[c] - ka * mu;
+      kC[c] = kc;
+      kB[c] = -ka * dbeta[c] * inv_m - kc * mu;
+    }
+  }
+  __syncthreads();
   float s0[8], s1[8], s2[8];
 #pragma unroll
   for (int e = 0; e < 8; ++e) s0[e] = s1[e] = s2[e] = 0.f;
   if (lane < lanes) {
-    float mu[8], is[8], ga[8], be[8], dg[8], db[8], k[8];
-    const float fm = (float)M, inv_m = 1.f / fm;
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      mu[e] = mean[c0 + e]; is[e] = invstd[c0 + e]; ga[e] = gamma[c0 + e]; be[e] = beta[c0 + e];
-      dg[e] = dgamma[c0 + e]; db[e] = dbeta[c0 + e]; k[e] = ga[e] * is[e] * inv_m;
-    }
-#pragma unroll 4
     for (long long r = r0 + lane; r < r1; r += lanes) {
       const size_t i = (size_t)r * C + c0;
-      float v[8], g[8], dyv[8];
+      float v[8], g[8], av[8], bv[8];
       BV<T>::ld8(y + i, v);
       BV<T>::ld8(dz + i, g);
+      if (mat) {
+        BV<T>::ld8(a + i, av);
+        BV<T>::ld8(b + i, bv);
+      }
+      float dyv[8];
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float xh = (v[e] - mu[e]) * is[e];
-        const float gg = (relu && !(fmaf(ga[e], xh, be[e]) > 0.f)) ? 0.f : g[e];
-        dyv[e] = k[e] * (fm * gg - db[e] - xh * dg[e]);
+      for (int h = 0; h < 2; ++h) {
+        const float4 A4 = *reinterpret_cast<const float4*>(kA + c0 + 4 * h);
+        const float4 B4 = *reinterpret_cast<const float4*>(kB + c0 + 4 * h);
+        const float4 C4 = *reinterpret_cast<const float4*>(kC + c0 + 4 * h);
+        const float4 Q4 = *reinterpret_cast<const float4*>(kQ + c0 + 4 * h);
+        const float ka[4] = {A4.x, A4.y, A4.z, A4.w}, kb[4] = {B4.x, B4.y, B4.z, B4.w};
+        const float kc[4] = {C4.x, C4.y, C4.z, C4.w}, kq[4] = {Q4.x, Q4.y, Q4.z, Q4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int f = 4 * h + e;
+          const float gg = (relu && !(fmaf(ka[e], v[f], kq[e]) > 0.f)) ? 0.f : g[f];
+          dyv[f] = fmaf(ka[e], gg, fmaf(kc[e], v[f], kb[e]));
+        }
       }
       T* drow = D + (size_t)r * P.Jd + c0;
       if (mat) {
-        float av[8], bv[8], d0[8], d1[8];
-        BV<T>::ld8(a + i, av);
-        BV<T>::ld8(b + i, bv);
+        float d0[8], d1[8];
 #pragma unroll
         for (int e = 0; e < 8; ++e) {
           d0[e] = dyv[e] * bv[e];
@@ -276,20 +327,150 @@ __global__ void __launch_bounds__(256) bn_emit_D_vec_kernel(Plan P, const T* __r
       }
     }
   }
+  __syncthreads();  // constants no longer read: the buffer takes the fold
+  float (*red)[256 * 8] = reinterpret_cast<float (*)[256 * 8]>(sm);
+  // 3 x 256 x 8 floats > 4 x 2048: fold in two rounds (s0, s1), then s2
 #pragma unroll
   for (int e = 0; e < 8; ++e) {
     red[0][threadIdx.x * 8 + e] = s0[e];
     red[1][threadIdx.x * 8 + e] = s1[e];
-    red[2][threadIdx.x * 8 + e] = s2[e];
   }
   __syncthreads();
+  float* o = bpart + (size_t)s * P.Jd;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
     const int qq = c / 8, e = c % 8;
-    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+    float t0 = 0.f, t1 = 0.f;
     for (int l = 0; l < lanes; ++l) {
       t0 += red[0][(l * CQ + qq) * 8 + e];
       t1 += red[1][(l * CQ + qq) * 8 + e];
-      t2 += red[2][(l * CQ + qq) * 8 + e];
+    }
+    o[c] = t0;
+    if (mat) o[C + c] = t1;
+  }
+  if (mat && hasg) {
+    __syncthreads();
+#pragma unroll
+    for (int e = 0; e < 8; ++e) red[0][threadIdx.x * 8 + e] = s2[e];
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += blockDim.x) {
+      const int qq = c / 8, e = c % 8;
+      float t2 = 0.f;
+      for (int l = 0; l < lanes; ++l) t2 += red[0][(l * CQ + qq) * 8 + e];
+      o[2 * C + c] = t2;
+    }
+  }
+}
+
+// Backward kernels on 4-channel chunks: thread = (chunk q, row lane), rows
+// [r0, r1) of block s, two rows' loads issued before any use. The BN backward is
+// folded into per-channel constants:
+//   dy = kA g' + kC y + kB,  g' = g masked where kP y + kQ <= 0 (the ReLU of the
+//   forward apply, z = kP y + kQ, evaluated with the same fmaf)
+// with kA = gamma inv, kC = -gamma inv^2 dgamma / M, kB = -gamma inv dbeta / M - kC mean.
+struct BnBwdK {
+  float kA[4], kB[4], kC[4], kP[4], kQ[4];
+  __device__ void load(int c0, long long M, const float* mean, const float* invstd, const float* gamma,
+                       const float* beta, const float* dgamma, const float* dbeta) {
+    const float inv_m = 1.f / (float)M;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float mu = mean[c0 + e], is = invstd[c0 + e], ga = gamma[c0 + e];
+      kP[e] = ga * is;
+      kQ[e] = beta[c0 + e] - kP[e] * mu;
+      kA[e] = kP[e];
+      kC[e] = dgamma ? -kP[e] * is * dgamma[c0 + e] * inv_m : 0.f;
+      kB[e] = dbeta ? -kP[e] * dbeta[c0 + e] * inv_m - kC[e] * mu : 0.f;
+    }
+  }
+};
+
+template <typename T>
+__global__ void __launch_bounds__(256, 4) bn_emit_D_c4_kernel(Plan P, const T* __restrict__ dz, const T* __restrict__ y,
+                                                           const T* __restrict__ a, const T* __restrict__ b,
+                                                           const float* mean, const float* invstd,
+                                                           const float* gamma, const float* beta,
+                                                           const float* dgamma, const float* dbeta, int relu,
+                                                           T* __restrict__ D, float* bpart) {
+  ptx::pdl_wait();  // dgamma / dbeta come from the finalize kernel (PDL launch)
+  ptx::pdl_launch();
+  __shared__ float red[3][256 * 4];
+  const long long M = P.Mout;
+  const int C = P.F, CQ = C / 4, lanes = 256 / CQ;
+  const int q = threadIdx.x % CQ, lane = threadIdx.x / CQ, c0 = q * 4;
+  const int S = gridDim.x, s = blockIdx.x;
+  const long long rows = (M + S - 1) / S;
+  const long long r0 = (long long)s * rows;
+  long long r1 = r0 + rows;
+  if (r1 > M) r1 = M;
+  const bool mat = caches_ab(P.family), hasg = d_has_g(P.family);
+  float s0[4], s1[4], s2[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) s0[e] = s1[e] = s2[e] = 0.f;
+  if (lane < lanes) {
+    BnBwdK k;
+    k.load(c0, M, mean, invstd, gamma, beta, dgamma, dbeta);
+    long long r = r0 + lane;
+    constexpr int U = 2;
+    for (; r < r1; r += U * lanes) {
+      float v[U][4], g[U][4], av[U][4], bv[U][4];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {  // all loads of the batch in flight (clamped rows)
+        const long long ru = r + u * lanes;
+        ok[u] = ru < r1;
+        const size_t i = (size_t)(ok[u] ? ru : r) * C + c0;
+        BV<T>::ld4(y + i, v[u]);
+        BV<T>::ld4(dz + i, g[u]);
+        if (mat) {
+          BV<T>::ld4(a + i, av[u]);
+          BV<T>::ld4(b + i, bv[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+        float dy[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float gg = (relu && !(fmaf(k.kP[e], v[u][e], k.kQ[e]) > 0.f)) ? 0.f : g[u][e];
+          dy[e] = fmaf(k.kA[e], gg, fmaf(k.kC[e], v[u][e], k.kB[e]));
+        }
+        T* drow = D + (size_t)(r + u * lanes) * P.Jd + c0;
+        if (mat) {
+          float d0[4], d1[4];
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            d0[e] = dy[e] * bv[u][e];
+            d1[e] = dy[e] * av[u][e];
+            s0[e] += d0[e];
+            s1[e] += d1[e];
+            s2[e] += dy[e];
+          }
+          BV<T>::st4(drow, d0);
+          BV<T>::st4(drow + C, d1);
+          if (hasg) BV<T>::st4(drow + 2 * C, dy);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 4; ++e) s0[e] += dy[e];
+          BV<T>::st4(drow, dy);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    red[0][threadIdx.x * 4 + e] = s0[e];
+    red[1][threadIdx.x * 4 + e] = s1[e];
+    red[2][threadIdx.x * 4 + e] = s2[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int qq = c / 4, e = c % 4;
+    float t0 = 0.f, t1 = 0.f, t2 = 0.f;
+    for (int l = 0; l < lanes; ++l) {
+      t0 += red[0][(l * CQ + qq) * 4 + e];
+      t1 += red[1][(l * CQ + qq) * 4 + e];
+      t2 += red[2][(l * CQ + qq) * 4 + e];
     }
     float* o = bpart + (size_t)s * P.Jd;
     if (mat) {
@@ -299,6 +480,77 @@ __global__ void __launch_bounds__(256) bn_emit_D_vec_kernel(Plan P, const T* __r
     } else {
       o[c] = t0;
     }
+  }
+}
+
+// backward reduction (sum g', sum g' xhat) on 4-channel chunks, four rows' loads
+// in flight; xhat = (y - mean) inv
+template <typename T>
+__global__ void __launch_bounds__(256, 4) bn_bwd_reduce_c4_kernel(long long M, int C, const T* __restrict__ y,
+                                                               const T* __restrict__ dz, const float* mean,
+                                                               const float* invstd, const float* gamma,
+                                                               const float* beta, int relu, float* part) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
+  __shared__ float red[2][256 * 4];
+  const int CQ = C / 4, lanes = 256 / CQ;
+  const int q = threadIdx.x % CQ, lane = threadIdx.x / CQ, c0 = q * 4;
+  const int S = gridDim.x, s = blockIdx.x;
+  const long long rows = (M + S - 1) / S;
+  const long long r0 = (long long)s * rows;
+  long long r1 = r0 + rows;
+  if (r1 > M) r1 = M;
+  float a0[4], a1[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) a0[e] = a1[e] = 0.f;
+  if (lane < lanes) {
+    float mu[4], is[4], kP[4], kQ[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      mu[e] = mean[c0 + e]; is[e] = invstd[c0 + e];
+      kP[e] = gamma[c0 + e] * is[e];
+      kQ[e] = beta[c0 + e] - kP[e] * mu[e];
+    }
+    constexpr int U = 4;
+    for (long long r = r0 + lane; r < r1; r += U * lanes) {
+      float v[U][4], g[U][4];
+      bool ok[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const long long ru = r + u * lanes;
+        ok[u] = ru < r1;
+        const size_t i = (size_t)(ok[u] ? ru : r) * C + c0;
+        BV<T>::ld4(y + i, v[u]);
+        BV<T>::ld4(dz + i, g[u]);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        if (!ok[u]) continue;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const float xh = (v[u][e] - mu[e]) * is[e];
+          const float gg = (relu && !(fmaf(kP[e], v[u][e], kQ[e]) > 0.f)) ? 0.f : g[u][e];
+          a0[e] += gg;
+          a1[e] = fmaf(gg, xh, a1[e]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    red[0][threadIdx.x * 4 + e] = a0[e];
+    red[1][threadIdx.x * 4 + e] = a1[e];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < C; c += blockDim.x) {
+    const int qq = c / 4, e = c % 4;
+    float t0 = 0.f, t1 = 0.f;
+    for (int l = 0; l < lanes; ++l) {
+      t0 += red[0][(l * CQ + qq) * 4 + e];
+      t1 += red[1][(l * CQ + qq) * 4 + e];
+    }
+    part[((size_t)s * 2 + 0) * C + c] = t0;
+    part[((size_t)s * 2 + 1) * C + c] = t1;
   }
 }
 
@@ -553,14 +805,19 @@ static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, c
   const int C = P.F, S = bn_splits(M, C);
   float* part = (float*)ws;
   float* bpart = part + (size_t)S * 2 * C;
-  if (bn_vec(C))
+  if (bn_c4(C) && !getenv("QD_BN_C8"))
+    launch_pdl(bn_bwd_reduce_c4_kernel<T>, dim3(S), dim3(256), 0, st, M, C, y, dz, sm, si, gamma, beta, relu, part);
+  else if (bn_vec(C))
     launch_pdl(bn_reduce_vec_kernel<T, 1>, dim3(S), dim3(256), 0, st, M, C, y, dz, sm, si, gamma, beta, relu, part);
   else
     bn_reduce_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
   count_launch(st, "bn_bwd_reduce");
   launch_pdl(bn_grad_finalize, dim3((C + 31) / 32), dim3(1024), 0, st, C, S, (const float*)part, dgamma, dbeta);
   count_launch(st, "bn_bwd_finalize");
-  if (bn_vec(C))
+  if (bn_c4(C) && getenv("QD_BN_C4"))  // dev: the 4-channel emit (slower, measured)
+    launch_pdl(bn_emit_D_c4_kernel<T>, dim3(S), dim3(256), 0, st, P, dz, y, a, b, sm, si, gamma, beta,
+               (const float*)dgamma, (const float*)dbeta, relu, D, bpart);
+  else if (bn_vec(C))
     launch_pdl(bn_emit_D_vec_kernel<T>, dim3(S), dim3(256), 0, st, P, dz, y, a, b, sm, si, gamma, beta,
                (const float*)dgamma, (const float*)dbeta, relu, D, bpart);
   else

@@ -268,7 +268,7 @@ namespace qd {
 // needs are staged in shared memory with the zero padding materialised
 // (coalesced NHWC loads), then every thread assembles 16-byte column chunks
 // from shared memory and stores them: the col rows are written contiguously.
-constexpr int IM2COL_TW = 32;
+constexpr int IM2COL_TW = 112;  // a whole ResNet stem output row per block (32: 4x the blocks, latency-bound)
 template <typename T>
 __global__ void __launch_bounds__(256) im2col_kernel(int N, int C, int H, int W, int OH, int OW, int r, int s, int p,
                                                      int Kp, const T* __restrict__ x, T* __restrict__ col) {
