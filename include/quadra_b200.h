@@ -141,8 +141,9 @@ int qd_maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dty
 
 /* im2col of an NHWC tensor for small-channel convs run as one fc GEMM (the
  * QuadraResNet 7x7/2 stem, the QuadraVGG first layer -- 3 input channels):
- * col[m][k], m = (n, oh, ow), k = (ky r + kx) C + c for k < r*r*C, zero up to
- * Kp (a multiple of 8). Same geometry rules as conv_out_size (tensor.py:279). */
+ * col[m][k], m = (n, oh, ow), run-padded columns k = ky runp + kx C + c with
+ * runp = r*C rounded up to 8 (zeros in the run tails and from r*runp up to Kp,
+ * a multiple of 8). Same geometry rules as conv_out_size (tensor.py:279). */
 int qd_im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, const void* x, void* col,
               void* stream);
 

@@ -261,57 +261,72 @@ int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype,
 namespace qd {
 
 // im2col for small-channel convs run as one fc GEMM (the ResNet stem 7x7/2 over
-// 3 channels, the VGG stem 3x3 over 3 channels): NHWC x -> col[M][Kp], column
-// k = (ky r + kx) C + c for k < r*r*C, zeros up to Kp (a multiple of 8). One
-// thread per (output pixel, 8 columns), one 16-byte store each.
-// block = (n, oh, 32 output pixels of that row): the r input rows the block
-// needs are staged in shared memory with the zero padding materialised
-// (coalesced NHWC loads), then every thread assembles 16-byte column chunks
-// from shared memory and stores them: the col rows are written contiguously.
+// 3 channels, the VGG stem 3x3 over 3 channels): NHWC x -> col[M][Kp] in the
+// run-padded layout k = ky runp + kx C + c (runp = r C rounded up to 8; zeros
+// in the run tails and up to Kp, a multiple of 8).
+// block = (n, oh, up to 112 output pixels of that row): the r input rows the
+// block needs are staged in shared memory (row stride rounded to 8 elements,
+// the zero padding materialised, coalesced NHWC loads). For a pixel, the kx, c
+// columns of filter row ky are ONE contiguous run of the staged row ky, so a
+// thread copies a whole run (pixel, ky) as 32-bit words (funnel-shifted when
+// the run starts at an odd element) into runp / 8 16-byte stores (measured:
+// 0.30 ms on the ResNet stem vs 0.34 with one 16-byte chunk per thread).
 constexpr int IM2COL_TW = 112;  // a whole ResNet stem output row per block (32: 4x the blocks, latency-bound)
 template <typename T>
 __global__ void __launch_bounds__(256) im2col_kernel(int N, int C, int H, int W, int OH, int OW, int r, int s, int p,
                                                      int Kp, const T* __restrict__ x, T* __restrict__ col) {
-  extern __shared__ unsigned char im2col_smem[];
-  T* rows = reinterpret_cast<T*>(im2col_smem);  // [r][RW][C]
+  extern __shared__ __align__(16) unsigned char im2col_smem[];
+  T* rows = reinterpret_cast<T*>(im2col_smem);  // [r][RCp]
   const int owt = (OW + IM2COL_TW - 1) / IM2COL_TW;
   int b = blockIdx.x;
   const int ot = b % owt;
   b /= owt;
   const int oh = b % OH, n = b / OH;
   const int ow0 = ot * IM2COL_TW, tw = min(IM2COL_TW, OW - ow0);
-  const int RW = (IM2COL_TW - 1) * s + r, RC = RW * C;
+  const int RW = (IM2COL_TW - 1) * s + r, RC = RW * C, RCp = (RC + 7) & ~7;
   const int h0 = oh * s - p, w0 = ow0 * s - p;
-  for (int e = threadIdx.x; e < r * RC; e += blockDim.x) {
-    const int j = e / RC, q = e - j * RC;
+  for (int e = threadIdx.x; e < r * RCp; e += blockDim.x) {
+    const int j = e / RCp, q = e - j * RCp;
     const int h = h0 + j, w = w0 + q / C;
-    rows[e] = (h >= 0 && h < H && w >= 0 && w < W) ? x[(((size_t)n * H + h) * W + w0) * C + q]
-                                                  : cvt<T>(0.f);
-  }
-  // column k -> offset in the staged rows relative to the pixel's window (-1: K padding)
-  int* koff = reinterpret_cast<int*>(im2col_smem + (((size_t)r * RC * sizeof(T) + 15) & ~(size_t)15));
-  const int K = r * r * C, k8n = Kp / 8, rCw = r * C;
-  for (int k = threadIdx.x; k < Kp; k += blockDim.x) {
-    const int ky = k / rCw;
-    koff[k] = k < K ? ky * RC + (k - ky * rCw) : -1;
+    rows[e] = (q < RC && h >= 0 && h < H && w >= 0 && w < W) ? x[(((size_t)n * H + h) * W + w0) * C + q]
+                                                             : cvt<T>(0.f);
   }
   __syncthreads();
+  const int rc = r * C, runp = (rc + 7) & ~7;
   T* dst0 = col + ((size_t)(n * OH + oh) * OW + ow0) * Kp;
-  for (int id = threadIdx.x; id < tw * k8n; id += blockDim.x) {
-    const int l = id / k8n, k0 = (id - l * k8n) * 8;
-    const T* win = rows + l * s * C;
-    const int4 oa = *reinterpret_cast<const int4*>(koff + k0), ob = *reinterpret_cast<const int4*>(koff + k0 + 4);
-    const int o[8] = {oa.x, oa.y, oa.z, oa.w, ob.x, ob.y, ob.z, ob.w};
-    T v[8];
-#pragma unroll
-    for (int e = 0; e < 8; ++e) v[e] = o[e] >= 0 ? win[o[e]] : cvt<T>(0.f);
-    T* dst = dst0 + (size_t)l * Kp + k0;
+  for (int id = threadIdx.x; id < tw * r; id += blockDim.x) {
+    const int l = id / r, ky = id - l * r;
+    const int off = ky * RCp + l * s * C;  // first element of the run
+    T* dst = dst0 + (size_t)l * Kp + ky * runp;
     if (sizeof(T) == 2) {
-      *reinterpret_cast<uint4*>(dst) = *reinterpret_cast<const uint4*>(v);
+      const uint32_t* ws = reinterpret_cast<const uint32_t*>(rows) + (off >> 1);
+      const uint32_t sh = (off & 1) * 16;
+      uint32_t prev = ws[0];
+      for (int c8 = 0; c8 < runp / 8; ++c8) {
+        uint32_t o[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t nxt = ws[c8 * 4 + e + 1];
+          uint32_t v = __funnelshift_r(prev, nxt, sh);
+          prev = nxt;
+          const int kk = c8 * 8 + 2 * e;  // run elements kk, kk + 1
+          if (kk >= rc) v = 0u;
+          else if (kk + 1 >= rc) v &= 0xFFFFu;
+          o[e] = v;
+        }
+        *reinterpret_cast<uint4*>(dst + c8 * 8) = make_uint4(o[0], o[1], o[2], o[3]);
+      }
     } else {
-      reinterpret_cast<uint4*>(dst)[0] = reinterpret_cast<const uint4*>(v)[0];
-      reinterpret_cast<uint4*>(dst)[1] = reinterpret_cast<const uint4*>(v)[1];
+      for (int k = 0; k < runp; ++k) dst[k] = k < rc ? rows[off + k] : cvt<T>(0.f);
     }
+    if (ky == r - 1)  // K padding after the last run
+      for (int k = r * runp; k < Kp; k += 8) {
+        if (sizeof(T) == 2) {
+          *reinterpret_cast<uint4*>(dst0 + (size_t)l * Kp + k) = make_uint4(0u, 0u, 0u, 0u);
+        } else {
+          for (int e = 0; e < 8; ++e) dst0[(size_t)l * Kp + k + e] = cvt<T>(0.f);
+        }
+      }
   }
 }
 
@@ -319,14 +334,17 @@ int im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, c
            cudaStream_t st) {
   if (N < 1 || C < 1 || H < 1 || W < 1 || r < 1 || s < 1 || p < 0)
     return set_error(QD_ERR_DIM, "im2col: N %d C %d H %d W %d r %d s %d p %d", N, C, H, W, r, s, p);
-  if (Kp % 8 || Kp < r * r * C) return set_error(QD_ERR_CONFIG, "im2col: Kp %d (need a multiple of 8 >= %d)", Kp, r * r * C);
+  const int runp = (r * C + 7) & ~7;
+  if (Kp % 8 || Kp < r * runp)
+    return set_error(QD_ERR_CONFIG, "im2col: Kp %d (need a multiple of 8 >= %d)", Kp, r * runp);
   const int OH = (H + 2 * p - r) / s + 1, OW = (W + 2 * p - r) / s + 1;
   if (OH < 1 || OW < 1) return set_error(QD_ERR_DIM, "im2col: empty output");
   if (dev_skip("im2col")) return QD_OK;
   const long long blocks = (long long)N * OH * ((OW + IM2COL_TW - 1) / IM2COL_TW);
   if (blocks >= (1LL << 31)) return set_error(QD_ERR_DIM, "im2col: %lld blocks", blocks);
   const size_t es = dtype == QD_BF16 ? 2 : 4;
-  const size_t smem = (((size_t)r * ((IM2COL_TW - 1) * s + r) * C * es + 15) & ~(size_t)15) + (size_t)Kp * 4;
+  // staged rows + slack for the word past the last run
+  const size_t smem = (size_t)r * ((((IM2COL_TW - 1) * s + r) * C + 7) & ~7) * es + (size_t)(runp + 8) * es;
   if (smem > 48 * 1024) return set_error(QD_ERR_UNSUPPORTED, "im2col: %zu B of staged rows (r %d, s %d, C %d)", smem, r, s, C);
   if (dtype == QD_BF16)
     im2col_kernel<bf16><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x,

@@ -3,9 +3,10 @@
 A conv with 3 input channels (the QuadraResNet 7x7/2 stem, the QuadraVGG first
 layer) cannot feed the 64-channel-block tcgen05 conv kernels, and zero-padding
 the channels to 64 multiplies its work by 21. ``Im2colConv2d`` instead writes
-the patches once (``qd_im2col``: col[m][k], k = (ky r + kx) C + c, zero-padded
-to a multiple of 64) and runs the layer as the same family's *fc* layer over
-them, K = r*r*C rounded up to 64 (147 -> 192, 27 -> 64). The weights keep the
+the patches once (``qd_im2col``: col[m][k], k = ky runp + kx C + c with the
+filter-row run r*C padded to 8, then zeros to a multiple of 64) and runs the
+layer as the same family's *fc* layer over them (ResNet 7x7: runs 21 -> 24,
+K 168 -> 192; VGG 3x3: 9 -> 16, 48 -> 64). The weights keep the
 reference conv layout (F, C, r, r) and role names; their fc view is a
 differentiable permute + pad, so gradients land in the conv-shaped parameters.
 The input gradient (col2im) is not implemented: the layer is for data inputs.
@@ -43,7 +44,9 @@ class Im2colConv2d(nn.Module):
         super().__init__()
         self.conv_spec = QuadraticLayerSpec(kind="conv", family=family, in_dim=in_channels, out_dim=out_channels,
                                             kernel=kernel_size, stride=stride, pad=padding)
-        self.k = kernel_size * kernel_size * in_channels
+        self.run = kernel_size * in_channels           # the (kx, c) columns of one filter row
+        self.runp = (self.run + 7) // 8 * 8             # padded to 16-byte runs (qd_im2col layout)
+        self.k = kernel_size * self.runp
         self.kp = (self.k + 63) // 64 * 64
         self.fc_spec = QuadraticLayerSpec(kind="fc", family=family, in_dim=self.kp, out_dim=out_channels)
         fk = dict(device=device, dtype=dtype or torch.float32)
@@ -60,8 +63,10 @@ class Im2colConv2d(nn.Module):
         out = []
         for role in param_shapes(self.fc_spec):
             t = getattr(self, role)
-            if t.dim() == 4:  # (F, C, r, r) -> (r, r, C, F) -> (k, F) -> zero rows to kp
-                t = t.permute(2, 3, 1, 0).reshape(self.k, t.shape[0])
+            if t.dim() == 4:  # (F, C, r, r) -> (r, r C, F) -> zero rows to (r, runp, F) -> (k, F) -> kp
+                r = t.shape[2]
+                t = t.permute(2, 3, 1, 0).reshape(r, self.run, t.shape[0])
+                t = F.pad(t, (0, 0, 0, self.runp - self.run)).reshape(self.k, t.shape[2])
                 t = F.pad(t, (0, 0, 0, self.kp - self.k))
             out.append(t)
         return out

@@ -575,11 +575,13 @@ def test_bnact_matches_reference_bn(relu):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("family,k,s,p,c", [("first_order", 7, 2, 3, 3), ("proposed", 3, 1, 1, 3),
-                                          ("t4", 3, 1, 1, 5), ("proposed", 5, 2, 2, 2)])
-def test_im2col_conv_matches_torch_conv(family, k, s, p, c):
+@pytest.mark.parametrize("family,k,s,p,c,w", [("first_order", 7, 2, 3, 3, 23), ("proposed", 3, 1, 1, 3, 23),
+                                            ("t4", 3, 1, 1, 5, 23), ("proposed", 5, 2, 2, 2, 23),
+                                            ("first_order", 7, 2, 3, 3, 240), ("proposed", 3, 1, 1, 3, 131)])
+def test_im2col_conv_matches_torch_conv(family, k, s, p, c, w):
     """3-channel stems as one fc GEMM over im2col'd patches vs the conv computed
-    by torch in fp32 from the same bf16 values."""
+    by torch in fp32 from the same bf16 values (odd run starts at stride 1 with
+    odd C; rows wider than one 112-pixel block)."""
     from paper_2204_01701_b200.im2col import Im2colConv2d
     import torch.nn.functional as F
     torch.manual_seed(2)
@@ -588,7 +590,7 @@ def test_im2col_conv_matches_torch_conv(family, k, s, p, c):
         for name, t in m.named_parameters():
             if name.startswith("b"):
                 t.uniform_(-0.2, 0.2)
-    x = torch.randn(3, c, 19, 23, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    x = torch.randn(3, c, 19, w, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
     y = m(x)
     assert y.is_contiguous(memory_format=torch.channels_last)
     gy = torch.randn(y.shape, device="cuda")
