@@ -975,9 +975,9 @@ __global__ void __launch_bounds__(256) wfinish_conv_kernel(Plan P, const float* 
 // to a power of two, L = 256 / G: every thread loads); group g sums splits
 // g, g+G, ... with 4 loads in flight and the groups are added in order --
 // contiguous reads and writes; the transposing fold then reads one slice
-__global__ void __launch_bounds__(256) wsum_kernel(Plan P, float* __restrict__ part, int S, WSplits wsp) {
+__global__ void __launch_bounds__(256) wsum_kernel(Plan P, float* __restrict__ part, int S, WSplits wsp, int G) {
   __shared__ float4 red[256];
-  const int G = S >= 8 ? 8 : (S >= 4 ? 4 : 2), L = 256 / G;
+  const int L = 256 / G;
   const int col = threadIdx.x % L, grp = threadIdx.x / L;
   const long long n4 = (long long)P.Jd * P.Kf / 4;
   float4* p4 = reinterpret_cast<float4*>(part);
@@ -1039,9 +1039,15 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
     if (S > 1 && dW[0] && !getenv("QD_FOLD_1PASS")) {
       // sum the slices first (contiguous, all SMs busy), then transpose one slice
       const long long n4 = (long long)P.Jd * P.Kf / 4;
-      const int L = 256 / (S >= 8 ? 8 : (S >= 4 ? 4 : 2));  // as in the kernel
+      // split groups per column only while the columns alone leave threads
+      // idle (~300K threads fill the GPU): a group of one slice-load per
+      // thread per tile is L2-latency bound (measured 21 us on 7 MB slices)
+      int G = 1;
+      while (G < 8 && 2 * G <= S && n4 * G < 150000) G *= 2;
+      const int L = 256 / G;
       const long long tiles = (n4 + L - 1) / L;
-      wsum_kernel<<<(unsigned)(tiles < 148 * 8 ? tiles : 148 * 8), 256, 0, st>>>(P, const_cast<float*>(wpart), S, ws);
+      wsum_kernel<<<(unsigned)(tiles < 148 * 8 ? tiles : 148 * 8), 256, 0, st>>>(P, const_cast<float*>(wpart), S, ws,
+                                                                                 G);
       count_launch(st, "wsum");
       S = 1;
       ws1.ng = 0;
