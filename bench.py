@@ -428,11 +428,13 @@ def run_ours(args, wl, wl_name):
     # (marks on one stream), which is what the roofline of a kernel means
     part_env = os.environ.get("QD_NO_PART")
     os.environ["QD_NO_PART"] = "1"
+    os.environ["QD_FOLD_MAIN"] = "1"  # the wgrad fold on the same stream (one chain of marks)
     lib.qd_profile(1)  # marks from here on: [begin, kernel_1, ..., kernel_k] of the captured step
     with torch.cuda.graph(pgraph):
         lib.qd_profile_mark(torch.cuda.current_stream().cuda_stream)
         compute()
     lib.qd_profile(0)
+    del os.environ["QD_FOLD_MAIN"]
     if part_env is None:
         del os.environ["QD_NO_PART"]
     else:

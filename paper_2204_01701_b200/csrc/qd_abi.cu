@@ -20,6 +20,7 @@ static thread_local char g_err[512] = "";
 static bool g_prof = false;
 static std::vector<cudaEvent_t> g_prof_ev;
 static std::vector<const char*> g_prof_name;
+static std::vector<cudaStream_t> g_prof_st;
 static size_t g_prof_used = 0;
 
 static void prof_mark(cudaStream_t st, const char* name) {
@@ -28,8 +29,10 @@ static void prof_mark(cudaStream_t st, const char* name) {
     if (cudaEventCreate(&e) != cudaSuccess) return;
     g_prof_ev.push_back(e);
     g_prof_name.push_back(name);
+    g_prof_st.push_back(st);
   }
   g_prof_name[g_prof_used] = name;
+  g_prof_st[g_prof_used] = st;
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(st, &cs);
   if (cs == cudaStreamCaptureStatusActive)  // becomes an event-record node that fires on replay
@@ -98,7 +101,11 @@ Workspace plan_workspace(const Plan& P, int path) {
     return L;
   }
   if (path == 0) {
-    size_t a = (size_t)P.Mout * P.nb * P.F, b = (size_t)P.Min * P.Cd;
+    // SIMT fprop / dgrad outputs, one fp32 slice per K split (small grids: C1's
+    // 256 x 1536 fprop would fill 96 CTAs, its 256 x 512 dgrad 32)
+    L.sk_f = simt_ksplit(P.Mout, (long long)P.nb * P.F, P.Kf);
+    L.sk_d = simt_ksplit(P.Min, P.Cd, P.Kd);
+    size_t a = (size_t)L.sk_f * P.Mout * P.nb * P.F, b = (size_t)L.sk_d * P.Min * P.Cd;
     L.sz_P = (a > b ? a : b) * 4;
   }
   // stride-2 layers on the tcgen05 path run their backward on the stride-1 grid
@@ -118,6 +125,7 @@ Workspace plan_workspace(const Plan& P, int path) {
   }
   L.sz_WG = (size_t)L.wg_split * P.Jd * P.Kf * 4;
   long long bs = (Pg.Mout + 255) / 256;
+  if (path == 0) bs = Pg.Mout < 2 * 148 ? Pg.Mout : (bs > 2 * 148 ? bs : 2 * 148);  // row blocks for every SM
   if (path == 1 && P.F % 8 == 0 && P.F <= 2048) {
     // the vectorised prologue covers 4 x (2048 / F) rows per block iteration:
     // wide layers need more blocks for the same rows
@@ -391,8 +399,13 @@ int qd_profile_count(void) { return (int)g_prof_used; }
 int qd_profile_read(int i, const char** name, float* ms) {
   if (i <= 0 || (size_t)i >= g_prof_used) return QD_ERR_ARG;
   if (name) *name = g_prof_name[i];
+  // interval from the latest earlier mark on the same stream (a kernel on a
+  // forked side stream: from the latest earlier mark, the fork point)
+  size_t j = (size_t)i - 1;
+  for (size_t k = (size_t)i - 1; k >= 1; --k)
+    if (g_prof_st[k] == g_prof_st[i]) { j = k; break; }
   float t = 0.f;
-  cudaError_t e = cudaEventElapsedTime(&t, g_prof_ev[i - 1], g_prof_ev[i]);
+  cudaError_t e = cudaEventElapsedTime(&t, g_prof_ev[j], g_prof_ev[i]);
   if (e != cudaSuccess) return set_error(QD_ERR_CUDA, "qd_profile_read: %s", cudaGetErrorString(e));
   if (ms) *ms = t;
   return QD_OK;

@@ -27,7 +27,15 @@ struct Workspace {
   size_t off_SK, sz_SK;    // split-K fp32 partials of the v1 fprop / dgrad (small output grids)
   int wg_split;            // number of wgrad partials
   int bs_split;            // number of bias-sum partials
+  int sk_f, sk_d;          // SIMT fprop / dgrad K slices (slices of P, summed by the epilogues)
 };
+// SIMT GEMM K slices: enough CTAs for two per SM, each slice >= 64 of K
+inline int simt_ksplit(long long M, long long N, long long K) {
+  const long long tiles = ((M + 63) / 64) * ((N + 63) / 64);
+  long long S = (2 * 148 + tiles - 1) / tiles;
+  if (S > K / 64) S = K / 64;
+  return S < 1 ? 1 : (int)S;
+}
 Workspace plan_workspace(const Plan& P, int path);
 size_t tc_splitk_bytes(const Plan& P);
 

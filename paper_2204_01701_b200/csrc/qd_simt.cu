@@ -495,35 +495,43 @@ struct WgradB {
 // elementwise / reduction pieces
 // ---------------------------------------------------------------------------
 template <typename T>
-__global__ void fwd_epilogue_kernel(Plan P, const float* G, const float* b0, const float* b1,
+__global__ void fwd_epilogue_kernel(Plan P, const float* G, int S, const float* b0, const float* b1,
                                     const float* b2, T* y, T* a, T* b) {
   long long total = P.Mout * P.F;
   int NG = P.nb * P.F;
+  const size_t slice = (size_t)P.Mout * NG;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     long long m = i / P.F;
     int f = (int)(i % P.F);
-    const float* g = G + m * NG;
+    // the K slices of the GEMM output, summed in slice order (deterministic)
+    float gv[3] = {0.f, 0.f, 0.f};
+    for (int s = 0; s < S; ++s) {
+      const float* gs = G + s * slice + m * NG;
+      for (int br = 0; br < P.nb; ++br) gv[br] += gs[br * P.F + f];
+    }
+#define g_(br) gv[br]
     float out;
     if (P.family == QD_FAM_PROPOSED) {
-      float av = g[f] + b0[f], bv = g[P.F + f] + b1[f];
-      out = av * bv + (g[2 * P.F + f] + b2[f]);
+      float av = g_(0) + b0[f], bv = g_(1) + b1[f];
+      out = av * bv + (g_(2) + b2[f]);
       a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
     } else if (P.family == QD_FAM_T4) {
-      float av = g[f], bv = g[P.F + f];
+      float av = g_(0), bv = g_(1);
       out = av * bv;
       a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
     } else if (P.family == QD_FAM_T2AND4) {
-      float av = g[f], bv = g[P.F + f];
-      out = av * bv + g[2 * P.F + f];
+      float av = g_(0), bv = g_(1);
+      out = av * bv + g_(2);
       a[i] = cvt<T>(av); b[i] = cvt<T>(bv);
     } else if (P.family == QD_FAM_T3) {
-      out = g[f] * g[f];
+      out = g_(0) * g_(0);
     } else if (P.family == QD_FAM_FIRST_ORDER) {
-      out = g[f] + b0[f];
+      out = g_(0) + b0[f];
     } else {
-      out = g[f];
+      out = g_(0);
     }
+#undef g_
     y[i] = cvt<T>(out);
   }
 }
@@ -678,18 +686,24 @@ void launch_square(const Plan& P, const void* x, void* xs, cudaStream_t st) {
 // dgrad epilogue: dx = Q (first_order/t4/proposed), 2 x Q (t2),
 // 2 x Q[:, :C] + Q[:, C:] (t2_linear)  -- neurons.py:400-405 "t = ds*x; dx = t + t"
 template <typename T>
-__global__ void dgrad_epilogue_kernel(Plan P, const float* Q, const T* x, T* dx) {
+__global__ void dgrad_epilogue_kernel(Plan P, const float* Q, int S, const T* x, T* dx) {
   long long total = P.Min * P.C;
+  const size_t slice = (size_t)P.Min * P.Cd;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
        i += (long long)gridDim.x * blockDim.x) {
     long long m = i / P.C;
     int c = (int)(i % P.C);
+    float q0 = 0.f, q1 = 0.f;  // K slices summed in slice order (deterministic)
+    for (int s = 0; s < S; ++s) {
+      q0 += Q[s * slice + m * P.Cd + c];
+      if (P.sq == 2) q1 += Q[s * slice + m * P.Cd + P.C + c];
+    }
     float v;
-    if (P.sq == 0) v = Q[i];
+    if (P.sq == 0) v = q0;
     else {
-      float t = Q[m * P.Cd + c] * ld(x + i);
+      float t = q0 * ld(x + i);
       v = t + t;
-      if (P.sq == 2) v += Q[m * P.Cd + P.C + c];
+      if (P.sq == 2) v += q1;
     }
     dx[i] = cvt<T>(v);
   }
@@ -704,9 +718,10 @@ static int simt_forward_t(const Plan& P, const T* x, const T* wf, const float* c
   float* G = (float*)(ws + L.off_P);
   FpropA<T> la{x, P.H, P.W, P.C, P.OH, P.OW, P.r, P.s, P.p, P.K0, P.sq};
   FpropB<T> lb{wf, P.F, P.nb, P.FT, P.Kf};
-  simt_gemm(la, lb, (int)P.Mout, P.nb * P.F, P.Kf, 1, G, st);
+  const int S = L.sk_f > 0 ? L.sk_f : 1;
+  simt_gemm(la, lb, (int)P.Mout, P.nb * P.F, P.Kf, S, G, st);
   long long total = P.Mout * P.F;
-  fwd_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, G, bias[0], bias[1], bias[2], y, a, b);
+  fwd_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, G, S, bias[0], bias[1], bias[2], y, a, b);
   count_launch(st, "fwd_epilogue_simt");
   return check_launch("simt forward");
 }
@@ -754,9 +769,10 @@ static int simt_backward_t(const Plan& P, const T* x, const T* wpack, const T* a
     float* Q = (float*)(ws + L.off_P);
     DgradA<T> da{D, P.H, P.W, P.OH, P.OW, P.r, P.s, P.p, P.Jd};
     RowMajorB<T> dbm{wd, P.Kd};
-    simt_gemm(da, dbm, (int)P.Min, P.Cd, P.Kd, 1, Q, st);
+    const int S = L.sk_d > 0 ? L.sk_d : 1;
+    simt_gemm(da, dbm, (int)P.Min, P.Cd, P.Kd, S, Q, st);
     long long total = P.Min * P.C;
-    dgrad_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, Q, x, dx);
+    dgrad_epilogue_kernel<T><<<grid_for(total), 256, 0, st>>>(P, Q, S, x, dx);
     count_launch(st, "dgrad_epilogue_simt");
   }
   return check_launch("simt backward");

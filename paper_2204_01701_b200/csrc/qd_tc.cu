@@ -1376,7 +1376,9 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if (rc == QD_OK) {
       // the memory-bound fold overlaps the (smem-bound) dgrad: it runs on the side
       // stream, forked after wgrad and joined before this call returns
-      if (wst == st) side = fork_side(st);
+      // (QD_FOLD_MAIN=1: on `st`, for per-kernel timing with one stream of marks)
+      const bool fold_main = getenv("QD_FOLD_MAIN") && atoi(getenv("QD_FOLD_MAIN"));
+      if (wst == st && !fold_main) side = fork_side(st);
       launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wsp, dW, bpart, L.bs_split, db,
                         side ? side : st);
     } else if (rc != QD_ERR_UNSUPPORTED) {
