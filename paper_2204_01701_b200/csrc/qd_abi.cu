@@ -113,9 +113,9 @@ Workspace plan_workspace(const Plan& P, int path) {
   if (caches_ab(P.family) || P.family == QD_FAM_T3 || Pg.s != P.s) L.sz_D = (size_t)Pg.Mout * P.Jd * es;
   if (path == 1 && P.family == QD_FAM_T2AND4) L.sz_ZB = (size_t)3 * P.F * 4;
   if (path == 0) {
-    long long tiles = (long long)((P.Jd + 63) / 64) * ((P.Kf + 63) / 64);
+    long long tiles = (long long)((P.Jd + 127) / 128) * ((P.Kf + 127) / 128);  // SIMT GEMM tiles
     long long S = (2 * 148 + tiles - 1) / tiles;
-    long long cap = P.Mout / 256;
+    long long cap = P.Mout / 64;
     if (cap < 1) cap = 1;
     if (S > cap) S = cap;
     if (S < 1) S = 1;

@@ -31,7 +31,7 @@ struct Workspace {
 };
 // SIMT GEMM K slices: enough CTAs for two per SM, each slice >= 64 of K
 inline int simt_ksplit(long long M, long long N, long long K) {
-  const long long tiles = ((M + 63) / 64) * ((N + 63) / 64);
+  const long long tiles = ((M + 127) / 128) * ((N + 127) / 128);  // SG_BM x SG_BN tiles
   long long S = (2 * 148 + tiles - 1) / tiles;
   if (S > K / 64) S = K / 64;
   return S < 1 ? 1 : (int)S;

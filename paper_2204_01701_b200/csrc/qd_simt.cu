@@ -435,6 +435,7 @@ static void simt_gemm(LA la, LB lb, int M, int N, long long K, int split, float*
 // fprop A: implicit im2col of x (optionally squared), m = output pixel
 template <typename T>
 struct FpropA {
+  static constexpr bool kfast = true;  // k = (tap, c): channels contiguous
   const T* x; int H, W, C, OH, OW, r, s, p, K0, sq;
   __device__ float operator()(int m, long long kl) const {
     int k = (int)kl;
@@ -451,6 +452,7 @@ struct FpropA {
 // fprop B: GEMM column n = br*F + f -> packed row
 template <typename T>
 struct FpropB {
+  static constexpr bool kfast = true;
   const T* wf; int F, nb, FT, Kf;
   __device__ float operator()(int n, long long k) const {
     int br = n / F, f = n % F;
@@ -460,6 +462,7 @@ struct FpropB {
 // dgrad A: transposed-conv gather of D, m = input pixel, k = (e, j)
 template <typename T>
 struct DgradA {
+  static constexpr bool kfast = true;  // k = (e, j): D channels contiguous
   const T* D; int H, W, OH, OW, r, s, p, Jd;
   __device__ float operator()(int m, long long kl) const {
     int k = (int)kl;
@@ -475,18 +478,21 @@ struct DgradA {
 };
 template <typename T>
 struct RowMajorB {  // B(n, k) = w[n*K + k]
+  static constexpr bool kfast = true;
   const T* w; long long K;
   __device__ float operator()(int n, long long k) const { return ld(w + (size_t)n * K + k); }
 };
 // wgrad A: A(j, pixel) = D[pixel][j]
 template <typename T>
 struct WgradA {
+  static constexpr bool kfast = false;  // consecutive j contiguous
   const T* D; int Jd;
   __device__ float operator()(int j, long long q) const { return ld(D + (size_t)q * Jd + j); }
 };
 // wgrad B: B(kw, pixel) = im2col(x or x*x)[pixel][kw]
 template <typename T>
 struct WgradB {
+  static constexpr bool kfast = false;  // consecutive kw (channels) contiguous
   FpropA<T> a;
   __device__ float operator()(int kw, long long q) const { return a((int)q, kw); }
 };

@@ -46,23 +46,28 @@ Workspace t1_workspace(const Plan& P) {
 
 template <typename T>
 struct T1RowA {  // A(m, k) = x[m][k] (optionally squared)
+  static constexpr bool kfast = true;
   const T* x; int n;
   __device__ float operator()(int m, long long k) const { return ld(x + (size_t)m * n + k); }
 };
 struct T1ColB {  // B(j, k) = W[k][j] (x @ W)
+  static constexpr bool kfast = false;
   const float* w; int n;
   __device__ float operator()(int j, long long k) const { return w[(size_t)k * n + j]; }
 };
 struct T1RowB {  // B(i, k) = W[i][k] (dv @ W^T)
+  static constexpr bool kfast = true;
   const float* w; int n;
   __device__ float operator()(int i, long long k) const { return w[(size_t)i * n + k]; }
 };
 template <typename T>
 struct T1XtA {  // A(i, m) = x[m][i]   (x^T dv)
+  static constexpr bool kfast = false;
   const T* x; int n;
   __device__ float operator()(int i, long long m) const { return ld(x + (size_t)m * n + i); }
 };
 struct T1DvB {  // B(j, m) = dv[m][j]
+  static constexpr bool kfast = false;
   const float* dv; int n;
   __device__ float operator()(int j, long long m) const { return dv[(size_t)m * n + j]; }
 };
