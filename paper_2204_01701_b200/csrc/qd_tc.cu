@@ -1362,9 +1362,19 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       if (side) wst = side;
       else part = 0;
     }
+    // partitioned (wgrad3 beside the dgrad): wgrad3 folds its own partials (grid
+    // barrier + fixed-order sums, written transposed; C2 step 116 -> 111 us) --
+    // no wsum / transpose launches behind it. Unpartitioned, the separate fold on
+    // the side stream overlaps the dgrad instead. QD_W3_NOFOLD=1 forces the latter.
+    bool fold3 = false;
     if (w3) {
       const int ns = part ? part : L.wg_split;
-      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), ns, wst, dy, dsplit);
+      bool al16 = true;
+      for (int i = 0; i < 3; ++i) al16 = al16 && ((uintptr_t)dW[i] % 16 == 0);
+      fold3 = part > 0 && al16 && P.kind == QD_KIND_CONV &&
+              !(getenv("QD_W3_NOFOLD") && atoi(getenv("QD_W3_NOFOLD")));
+      rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), ns, wst, dy, dsplit,
+                      fold3 ? dW : nullptr, bpart, L.bs_split, db);
       wsp.pp = (P.r * P.r + 1) / 2;  // every tap in every split slot
       wsp.ng = 1;
       wsp.s[0] = ns;
@@ -1378,9 +1388,11 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       // stream, forked after wgrad and joined before this call returns
       // (QD_FOLD_MAIN=1: on `st`, for per-kernel timing with one stream of marks)
       const bool fold_main = getenv("QD_FOLD_MAIN") && atoi(getenv("QD_FOLD_MAIN"));
-      if (wst == st && !fold_main) side = fork_side(st);
-      launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wsp, dW, bpart, L.bs_split, db,
-                        side ? side : st);
+      if (!fold3) {
+        if (wst == st && !fold_main) side = fork_side(st);
+        launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, wsp, dW, bpart, L.bs_split, db,
+                          side ? side : st);
+      }
     } else if (rc != QD_ERR_UNSUPPORTED) {
       return rc;
     } else {

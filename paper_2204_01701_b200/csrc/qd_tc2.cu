@@ -1267,7 +1267,26 @@ struct W3Args {
   int jsplit;
   float* part;
   unsigned long long* trace;  // QD_TRACE (dev only)
+  // in-kernel fold (fold_bar != null): after a grid barrier each CTA sums whole
+  // (j, half, channel block) units of the partial slots in a fixed order and
+  // writes them transposed into the reference (F, C, 3, 3) layouts
+  int fold_slot;  // >= 0: fold in-kernel, grid barrier on counter slot fold_slot
+  float* dw0;
+  float* dw1;
+  float* dw2;
+  const float* bpart;  // bias partial sums [SB][Jd] (prologue / BN emit), folded here too
+  int SB;
+  float* db0;
+  float* db1;
+  float* db2;
+  Plan P;
 };
+
+// grid-barrier counters of the in-kernel fold (zero at module load): launches
+// take slots round-robin, so only 64 wgrad3 launches in flight at once could
+// collide; the last CTA to leave a barrier resets its slot for the next use
+__device__ unsigned g_w3_arrive[64];
+__device__ unsigned g_w3_depart[64];
 
 __device__ __forceinline__ void w3_tma4_mc(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2,
                                            int c3) {
@@ -1489,6 +1508,118 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   }
   ptx::tc_fence_before();
   c2::cluster_sync();  // no CTA exits while its partner may still multicast into it
+  if (g.fold_slot >= 0) {
+    // ===== in-kernel fold. Every CTA of the (persistent, co-resident) grid has
+    // stored its slot region: grid barrier (release / acquire at GPU scope) =====
+    unsigned* arrive = &g_w3_arrive[g.fold_slot];
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      atomicAdd(arrive, 1u);
+      unsigned seen;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
+        if (seen < gridDim.x) __nanosleep(64);
+      } while (seen < gridDim.x);
+    }
+    __syncthreads();
+    const Plan& P = g.P;
+    // bias partial sums: 8 columns x 32 split groups per pass, fixed order
+    if (g.db0 && P.nbias) {
+      float* redb = reinterpret_cast<float*>(sm);
+      const int bc = threadIdx.x % 8, bg = threadIdx.x / 8;
+      for (int bb = blockIdx.x; bb * 8 < P.Jd; bb += gridDim.x) {
+        const int j = bb * 8 + bc;
+        float a0 = 0.f, a1 = 0.f;
+        if (j < P.Jd) {
+          int s2 = bg;
+          for (; s2 + 32 < g.SB; s2 += 64) {
+            a0 += __ldcg(g.bpart + (size_t)s2 * P.Jd + j);
+            a1 += __ldcg(g.bpart + (size_t)(s2 + 32) * P.Jd + j);
+          }
+          for (; s2 < g.SB; s2 += 32) a0 += __ldcg(g.bpart + (size_t)s2 * P.Jd + j);
+        }
+        redb[bg * 9 + bc] = a0 + a1;
+        __syncthreads();
+        if (bg == 0 && j < P.Jd) {
+          float t = 0.f;
+          for (int gq = 0; gq < 32; ++gq) t += redb[gq * 9 + bc];
+          const int role = j / P.F, f = j % P.F;
+          float* dst = role == 0 ? g.db0 : (role == 1 ? g.db1 : g.db2);
+          if (dst) dst[f] = t;
+        }
+        __syncthreads();
+      }
+    }
+    // unit = (j, half, 64-channel block): 9 taps x 64 channels = 144 float4
+    // columns of partial row j, summed over the slots in a fixed order (four
+    // interleaved chains, combined in order), transposed through shared memory
+    // (the stage buffers are idle: every load landed and every MMA retired) and
+    // written as one contiguous 576-float run of dW[role][f][cb*64 ..][9]
+    const int nh = P.Kf / P.K0, units = P.Jd * nh * g.cblks, S = g.nsplit;
+    const long long slot4 = (long long)P.Jd * P.Kf / 4;
+    const float4* part4 = reinterpret_cast<const float4*>(g.part);
+    float* red = reinterpret_cast<float*>(sm);
+    // units per batch: as many 576-float tiles as the stage buffers hold (<= 64)
+    const int UB = min(64, (int)((g.stages * stage_bytes) / 2304));
+    for (int u0 = blockIdx.x; u0 < units; u0 += UB * gridDim.x) {
+      int nu = 0;
+      for (int u = u0; u < units && nu < UB; u += gridDim.x) ++nu;
+      for (int i = threadIdx.x; i < nu * 144; i += blockDim.x) {
+        const int ul = i / 144, col = i - ul * 144, u = u0 + ul * gridDim.x;
+        const int cbk = u % g.cblks, rest = u / g.cblks, hf = rest % nh, j = rest / nh;
+        const int tap = col >> 4, c4 = col & 15;
+        const long long o4 = ((long long)j * P.Kf + hf * P.K0 + tap * P.C + cbk * 64) / 4 + c4;
+        // eight independent chains (8 loads in flight per thread: the fold is
+        // L2-latency bound), combined in a fixed order
+        float4 ac[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) ac[e] = make_float4(0.f, 0.f, 0.f, 0.f);
+        int sl = 0;
+        for (; sl + 7 < S; sl += 8) {
+          float4 v[8];
+#pragma unroll
+          for (int e = 0; e < 8; ++e) v[e] = __ldcg(part4 + (sl + e) * slot4 + o4);
+#pragma unroll
+          for (int e = 0; e < 8; ++e) {
+            ac[e].x += v[e].x; ac[e].y += v[e].y; ac[e].z += v[e].z; ac[e].w += v[e].w;
+          }
+        }
+        for (; sl < S; ++sl) {
+          const float4 v = __ldcg(part4 + sl * slot4 + o4);
+          ac[0].x += v.x; ac[0].y += v.y; ac[0].z += v.z; ac[0].w += v.w;
+        }
+#pragma unroll
+        for (int e = 4; e > 0; e >>= 1)
+#pragma unroll
+          for (int i2 = 0; i2 < e; ++i2) {
+            ac[i2].x += ac[i2 + e].x; ac[i2].y += ac[i2 + e].y; ac[i2].z += ac[i2 + e].z; ac[i2].w += ac[i2 + e].w;
+          }
+        const float t[4] = {ac[0].x, ac[0].y, ac[0].z, ac[0].w};
+        float* ru = red + ul * 576;
+#pragma unroll
+        for (int e = 0; e < 4; ++e) ru[(c4 * 4 + e) * 9 + tap] = t[e];  // (c, tap) order
+      }
+      __syncthreads();
+      for (int i = threadIdx.x; i < nu * 144; i += blockDim.x) {
+        const int ul = i / 144, q4 = i - ul * 144, u = u0 + ul * gridDim.x;
+        const int cbk = u % g.cblks, rest = u / g.cblks, hf = rest % nh, j = rest / nh;
+        int role, f, kk;
+        if (!wgrad_dst(P, j, hf * P.K0, role, f, kk)) continue;  // t2and4 structural zero
+        float* dst = role == 0 ? g.dw0 : (role == 1 ? g.dw1 : g.dw2);
+        if (!dst) continue;
+        const float4 v = *reinterpret_cast<const float4*>(red + ul * 576 + 4 * q4);
+        reinterpret_cast<float4*>(dst + ((size_t)f * P.C + cbk * 64) * 9)[q4] = v;
+      }
+      __syncthreads();
+    }
+    // the last CTA out resets the slot (every CTA has passed its wait by then)
+    if (threadIdx.x == 0 && atomicAdd(&g_w3_depart[g.fold_slot], 1u) == gridDim.x - 1) {
+      g_w3_arrive[g.fold_slot] = 0u;
+      g_w3_depart[g.fold_slot] = 0u;
+      __threadfence();
+    }
+  }
   if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) {
     g.trace[3072 + 2 * blockIdx.x + 1] = gtimer();
     g.trace[2048 + 2 * blockIdx.x + 1] = clock64();
@@ -1581,7 +1712,8 @@ int wgrad3_pairs_per_split(const Plan& P) {
 }
 
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
-               cudaStream_t st, const void* Dtail, int jsplit) {
+               cudaStream_t st, const void* Dtail, int jsplit, float* const* dW, const float* bpart, int SB,
+               float* const* db) {
   if (dev_skip("wgrad")) return QD_OK;
   W3Plan pl = w3_plan(P);
   // splits < the plan's: a partitioned launch sharing the SMs with a concurrent kernel
@@ -1589,6 +1721,17 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
   W3Args& g = pl.g;
   g.nsplit = splits;
   g.part = part;
+  g.fold_slot = -1;
+  g.P = P;
+  if (dW && dW[0]) {
+    // the grid barrier needs every CTA resident at once: the grid never exceeds
+    // the co-resident clusters (w3_plan)
+    static unsigned slot = 0;
+    g.fold_slot = (int)(slot++ % 64);
+    g.dw0 = dW[0]; g.dw1 = dW[1]; g.dw2 = dW[2];
+    g.bpart = bpart; g.SB = SB;
+    g.db0 = db ? db[0] : nullptr; g.db1 = db ? db[1] : nullptr; g.db2 = db ? db[2] : nullptr;
+  }
   g.trace = getenv("QD_TRACE") ? trace_buffer() : nullptr;
   CUtensorMap X0, X1, Dm, Dm1;
   int rc;
