@@ -272,9 +272,12 @@ namespace qd {
 // the run starts at an odd element) into runp / 8 16-byte stores (measured:
 // 0.30 ms on the ResNet stem vs 0.34 with one 16-byte chunk per thread).
 constexpr int IM2COL_TW = 112;  // a whole ResNet stem output row per block (32: 4x the blocks, latency-bound)
-template <typename T>
-__global__ void __launch_bounds__(256) im2col_kernel(int N, int C, int H, int W, int OH, int OW, int r, int s, int p,
-                                                     int Kp, const T* __restrict__ x, T* __restrict__ col) {
+template <typename T, int CT, int RT>  // CT / RT: C and r at compile time (0: runtime)
+__global__ void __launch_bounds__(256) im2col_kernel(int N, int C_, int H, int W, int OH, int OW, int r_, int s,
+                                                     int p, int Kp, const T* __restrict__ x, T* __restrict__ col) {
+  // the kernel is instruction-bound (ncu: issue slots 80% busy): index math by
+  // compile-time C and r (the stems: C = 3, r = 7 / 3) and per-row staging loops
+  const int C = CT ? CT : C_, r = RT ? RT : r_;
   extern __shared__ __align__(16) unsigned char im2col_smem[];
   T* rows = reinterpret_cast<T*>(im2col_smem);  // [r][RCp]
   const int owt = (OW + IM2COL_TW - 1) / IM2COL_TW;
@@ -285,11 +288,27 @@ __global__ void __launch_bounds__(256) im2col_kernel(int N, int C, int H, int W,
   const int ow0 = ot * IM2COL_TW, tw = min(IM2COL_TW, OW - ow0);
   const int RW = (IM2COL_TW - 1) * s + r, RC = RW * C, RCp = (RC + 7) & ~7;
   const int h0 = oh * s - p, w0 = ow0 * s - p;
-  for (int e = threadIdx.x; e < r * RCp; e += blockDim.x) {
-    const int j = e / RCp, q = e - j * RCp;
-    const int h = h0 + j, w = w0 + q / C;
-    rows[e] = (q < RC && h >= 0 && h < H && w >= 0 && w < W) ? x[(((size_t)n * H + h) * W + w0) * C + q]
-                                                             : cvt<T>(0.f);
+  // staging, one input row at a time: 4 elements per thread per pass, all 4
+  // loads issued before the shared stores; valid w is a contiguous q range
+  const int qlo = (w0 < 0 ? -w0 : 0) * C, qhi = min(RC, (W - w0) * C);
+  for (int j = 0; j < r; ++j) {
+    const int h = h0 + j;
+    const bool hok = h >= 0 && h < H;
+    const T* src = x + (((size_t)n * H + (hok ? h : 0)) * W) * C + (long long)w0 * C;
+    T* dst = rows + j * RCp;
+    for (int q0 = threadIdx.x; q0 < RCp; q0 += 4 * blockDim.x) {
+      T v[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * blockDim.x;
+        v[u] = (hok && q >= qlo && q < qhi) ? src[q] : cvt<T>(0.f);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int q = q0 + u * blockDim.x;
+        if (q < RCp) dst[q] = v[u];
+      }
+    }
   }
   __syncthreads();
   const int rc = r * C, runp = (rc + 7) & ~7;
@@ -346,12 +365,20 @@ int im2col(int N, int C, int H, int W, int r, int s, int p, int Kp, int dtype, c
   // staged rows + slack for the word past the last run
   const size_t smem = (size_t)r * ((((IM2COL_TW - 1) * s + r) * C + 7) & ~7) * es + (size_t)(runp + 8) * es;
   if (smem > 48 * 1024) return set_error(QD_ERR_UNSUPPORTED, "im2col: %zu B of staged rows (r %d, s %d, C %d)", smem, r, s, C);
-  if (dtype == QD_BF16)
-    im2col_kernel<bf16><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x,
-                                                               (bf16*)col);
-  else
-    im2col_kernel<float><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const float*)x,
-                                                                (float*)col);
+  if (dtype == QD_BF16) {
+    if (C == 3 && r == 7)
+      im2col_kernel<bf16, 3, 7><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x,
+                                                                     (bf16*)col);
+    else if (C == 3 && r == 3)
+      im2col_kernel<bf16, 3, 3><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x,
+                                                                     (bf16*)col);
+    else
+      im2col_kernel<bf16, 0, 0><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp, (const bf16*)x,
+                                                                     (bf16*)col);
+  } else {
+    im2col_kernel<float, 0, 0><<<(unsigned)blocks, 256, smem, st>>>(N, C, H, W, OH, OW, r, s, p, Kp,
+                                                                    (const float*)x, (float*)col);
+  }
   count_launch(st, "im2col");
   return check_launch("im2col");
 }
