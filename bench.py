@@ -453,31 +453,6 @@ def run_ours(args, wl, wl_name):
                 seen[nm] = seen.get(nm, 0) + 1
             acc.setdefault(k, []).append(t)
     kern = {k: sum(v) / len(v) for k, v in acc.items()}
-    # wgrad3 folds its split-K partials in-kernel (grid barrier + fixed-order
-    # sum); its GEMM part alone: the same capture with the fold as separate kernels
-    w3_gemm_ms = None
-    if "wgrad3" in kern:
-        os.environ.update({"QD_NO_PART": "1", "QD_FOLD_MAIN": "1", "QD_W3_NOFOLD": "1"})
-        g2 = torch.cuda.CUDAGraph()
-        lib.qd_profile(1)
-        with torch.cuda.graph(g2):
-            lib.qd_profile_mark(torch.cuda.current_stream().cuda_stream)
-            compute()
-        lib.qd_profile(0)
-        for k_ in ("QD_FOLD_MAIN", "QD_W3_NOFOLD"):
-            del os.environ[k_]
-        if part_env is None:
-            del os.environ["QD_NO_PART"]
-        else:
-            os.environ["QD_NO_PART"] = part_env
-        ts = []
-        for _ in range(reps):
-            flush_l2(flush, 7)
-            g2.replay()
-            torch.cuda.synchronize()
-            ts += [t for nm, t in _lib.profile_read() if nm == "wgrad3"]
-        w3_gemm_ms = sum(ts) / len(ts) if ts else None
-        del g2
     third = flops / 3.0  # fprop, dgrad and wgrad each carry one third of the GEMM work
     tensor_k = {k: v for k, v in kern.items()
                 if k.split("[")[0] in ("conv2", "conv_gemm", "wgrad2", "wgrad3", "wgrad_v1", "simt_gemm")}
@@ -509,13 +484,9 @@ def run_ours(args, wl, wl_name):
             "algorithmic": "per launch: 1/3 of 9 x 2*M*K*F (one GEMM set); traffic = ncu dram read+write "
                            "of the same kernel (profiles/ncu_summary.json)",
             "timing": "kernel durations from CUDA events on the launching stream, each kernel alone on all "
-                      "SMs (QD_NO_PART); the timed step overlaps wgrad3 and dgrad on disjoint SM partitions"}
-    if w3_gemm_ms:
-        roof["wgrad3_gemm_only"] = {"ms": w3_gemm_ms, "tflops": third / (w3_gemm_ms * 1e-3) / 1e12,
-                                    "frac": third / (w3_gemm_ms * 1e-3) / 1e12 / pk["bf16"],
-                                    "note": "wgrad3 with its split-K fold as separate kernels (QD_W3_NOFOLD=1); "
-                                            "the step uses the in-kernel fold (grid barrier + fixed-order sum of "
-                                            "the fp32 partial slots), which the 'achieved' time above includes"}
+                      "SMs (QD_NO_PART; the split-K fold then runs as wsum + bwd_finish); the timed step "
+                      "overlaps wgrad3 and dgrad on disjoint SM partitions, the partitioned wgrad3 folding "
+                      "its partials in-kernel"}
     if dts != "bf16":
         roof["note"] = "fp32 runs on the CUDA-core (FFMA) path; the bf16 tensor peak is the denominator"
 
