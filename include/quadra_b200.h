@@ -109,6 +109,12 @@ size_t qd_bn_workspace_bytes(long long M, int C, int Jd);
 int qd_bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta,
                   float* run_mean, float* run_var, float momentum, float eps, int relu, int training,
                   void* z, float* save_mean, float* save_invstd, void* ws, void* stream);
+/* Same with a residual added before the ReLU (a ResNet block tail):
+ * z = relu?(BN(y) + res), res of y's shape and dtype. Not in the reference
+ * (its nets have no residual); the ReLU mask for the backward is z > 0. */
+int qd_bn_forward_res(long long M, int C, int dtype, const void* y, const void* res, const float* gamma,
+                      const float* beta, float* run_mean, float* run_var, float momentum, float eps, int relu,
+                      int training, void* z, float* save_mean, float* save_invstd, void* ws, void* stream);
 /* BN(+ReLU) backward fused with the quadratic layer's backward prologue: from
  * dz (gradient of z) and the layer's y, a, b it forms dgamma, dbeta, the layer's
  * bias gradients db[] and the operand D the layer backward consumes; then call

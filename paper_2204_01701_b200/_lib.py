@@ -31,7 +31,7 @@ EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_pack_weights", "qd_forward", "qd_backward", "qd_path",
            "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version",
            "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read",
-           "qd_sgd_pack", "qd_bn_workspace_bytes", "qd_bn_forward", "qd_bn_backward_D",
+           "qd_sgd_pack", "qd_bn_workspace_bytes", "qd_bn_forward", "qd_bn_forward_res", "qd_bn_backward_D",
            "qd_maxpool_forward", "qd_maxpool_backward", "qd_im2col")
 
 
@@ -84,6 +84,10 @@ def load():
                                       ctypes.c_float, ctypes.c_float, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp,
                                       vp]
         lib.qd_bn_forward.restype = ctypes.c_int
+        lib.qd_bn_forward_res.argtypes = [ctypes.c_longlong, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, vp,
+                                          ctypes.c_float, ctypes.c_float, ctypes.c_int, ctypes.c_int, vp, vp, vp,
+                                          vp, vp]
+        lib.qd_bn_forward_res.restype = ctypes.c_int
         lib.qd_bn_backward_D.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, fp3,
                                          vp, vp]
         lib.qd_bn_backward_D.restype = ctypes.c_int

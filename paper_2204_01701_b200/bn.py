@@ -45,8 +45,8 @@ def _dtype_code(t):
     return _lib.BF16 if t.dtype == torch.bfloat16 else _lib.F32
 
 
-def bn_forward(y, gamma, beta, running_mean, running_var, momentum, eps, relu, training):
-    """z = relu?(gamma (y - mean) inv_std + beta); returns (z, save_mean, save_invstd)."""
+def bn_forward(y, gamma, beta, running_mean, running_var, momentum, eps, relu, training, res=None):
+    """z = relu?(gamma (y - mean) inv_std + beta [+ res]); returns (z, save_mean, save_invstd)."""
     lib = _lib.load()
     yr = _rows(y)
     M, C = yr.shape
@@ -60,11 +60,20 @@ def bn_forward(y, gamma, beta, running_mean, running_var, momentum, eps, relu, t
         sm = running_mean.float().contiguous()
         si = torch.rsqrt(running_var.float() + eps).contiguous()
     ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, C), dtype=torch.uint8, device=y.device)
-    st = lib.qd_bn_forward(M, C, _dtype_code(y), y.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
-                           running_mean.data_ptr() if training else None,
-                           running_var.data_ptr() if training else None, float(momentum), float(eps), int(relu),
-                           int(training), z.data_ptr(), sm.data_ptr(), si.data_ptr(), ws.data_ptr(),
-                           torch.cuda.current_stream().cuda_stream)
+    if res is None:
+        st = lib.qd_bn_forward(M, C, _dtype_code(y), y.data_ptr(), gamma.data_ptr(), beta.data_ptr(),
+                               running_mean.data_ptr() if training else None,
+                               running_var.data_ptr() if training else None, float(momentum), float(eps),
+                               int(relu), int(training), z.data_ptr(), sm.data_ptr(), si.data_ptr(), ws.data_ptr(),
+                               torch.cuda.current_stream().cuda_stream)
+    else:
+        if res.shape != y.shape or res.dtype != y.dtype or not _rows(res).is_contiguous():
+            raise ValueError("bn_forward: residual must match y (shape, dtype, channels_last)")
+        st = lib.qd_bn_forward_res(M, C, _dtype_code(y), y.data_ptr(), res.data_ptr(), gamma.data_ptr(),
+                                   beta.data_ptr(), running_mean.data_ptr() if training else None,
+                                   running_var.data_ptr() if training else None, float(momentum), float(eps),
+                                   int(relu), int(training), z.data_ptr(), sm.data_ptr(), si.data_ptr(),
+                                   ws.data_ptr(), torch.cuda.current_stream().cuda_stream)
     _lib.raise_for(st, "qd_bn_forward")
     return z, sm, si
 
@@ -120,6 +129,42 @@ class _QuadBNFunction(torch.autograd.Function):
             dx = dx.to(ctx.x_dtype)
         ctx.cache = None
         return (None, None, None, None, dx, dgamma, dbeta) + tuple(grads[r] for r in ctx.roles)
+
+
+class _QuadBNAddReLUFunction(torch.autograd.Function):
+    """quadratic layer -> BN -> + residual -> ReLU (a ResNet block tail) as ONE
+    node: the residual add and the ReLU ride on the BN apply pass
+    (qd_bn_forward_res). Backward: g = dz masked by z > 0 (one pass; it is also
+    the residual's gradient), then the BN backward without ReLU emits the
+    layer's D from g as in _QuadBNFunction."""
+
+    @staticmethod
+    def forward(ctx, spec, dtype, bn, x, res, gamma, beta, *tensors):
+        roles = tuple(param_shapes(spec).keys())
+        params = dict(zip(roles, tensors))
+        y, cache = neurons.forward(spec, params, x, dtype=dtype)
+        if res.dtype != y.dtype or (y.dim() == 4 and not res.is_contiguous(memory_format=torch.channels_last)):
+            res = res.to(y.dtype).contiguous(memory_format=torch.channels_last)
+        z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, True, True,
+                               res=res)
+        ctx.spec, ctx.roles, ctx.params, ctx.cache = spec, roles, params, cache
+        ctx.x_dtype, ctx.res_dtype = x.dtype, res.dtype
+        ctx.save_for_backward(y, z, gamma, beta, sm, si)
+        return z
+
+    @staticmethod
+    def backward(ctx, dz):
+        y, z, gamma, beta, sm, si = ctx.saved_tensors
+        g = torch.ops.aten.threshold_backward(dz.to(z.dtype), z, 0)
+        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, g, y, gamma, beta, sm, si, False)
+        want_dx = ctx.needs_input_grad[3]
+        grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx)
+        grads.update(db)
+        if dx is not None and dx.dtype != ctx.x_dtype:
+            dx = dx.to(ctx.x_dtype)
+        ctx.cache = None
+        dres = g if ctx.needs_input_grad[4] else None
+        return (None, None, None, dx, dres, dgamma, dbeta) + tuple(grads[r] for r in ctx.roles)
 
 
 class _BNFunction(torch.autograd.Function):
@@ -211,6 +256,23 @@ class QuadConvBN(nn.Module):
                     and neurons.device_path(sp, tuple(x.shape), torch.bfloat16) == 1)
         return (sp.stride == 1 and sp.kind in ("conv", "fc") and sp.family not in ("t3", "t1_pure", "t1_full",
                                                                                    "t1and2"))
+
+    def forward_add_relu(self, x, res):
+        """relu(BN(layer(x)) + res) -- the block tail of a residual net; one
+        fused node on the library kernels when the layer's BN is fused, else the
+        composition (the module's own relu flag is not applied here)."""
+        if (self.training and x.device.type == "cuda" and self.fused(x)
+                and res.shape[1] == self.layer.spec.out_dim):
+            spec = self.layer.spec
+            tensors = [getattr(self.layer, r) for r in param_shapes(spec).keys()]
+            return _QuadBNAddReLUFunction.apply(spec, self.layer.compute_dtype, self.bn, x, res, self.weight,
+                                                self.bias, *tensors)
+        relu, self.relu = self.relu, False
+        try:
+            out = self.forward(x)
+        finally:
+            self.relu = relu
+        return torch.relu(out + res)
 
     def forward(self, x):
         spec = self.layer.spec

@@ -262,6 +262,19 @@ int qd_bn_forward(long long M, int C, int dtype, const void* y, const float* gam
                     save_invstd, (char*)ws, (cudaStream_t)stream);
 }
 
+int qd_bn_forward_res(long long M, int C, int dtype, const void* y, const void* res, const float* gamma,
+                      const float* beta, float* run_mean, float* run_var, float momentum, float eps, int relu,
+                      int training, void* z, float* save_mean, float* save_invstd, void* ws, void* stream) {
+  if (!res) return set_error(QD_ERR_ARG, "qd_bn_forward_res: NULL residual");
+  if (M < 1 || C < 1) return set_error(QD_ERR_DIM, "batchnorm over %lld rows x %d channels", M, C);
+  if (dtype != QD_F32 && dtype != QD_BF16) return set_error(QD_ERR_CONFIG, "unknown dtype %d", dtype);
+  if (!(eps > 0.f)) return set_error(QD_ERR_CONFIG, "batchnorm eps must be positive");
+  if (!y || !gamma || !beta || !z || !save_mean || !save_invstd || (training && !ws))
+    return set_error(QD_ERR_ARG, "qd_bn_forward_res: NULL argument");
+  return bn_forward(M, C, dtype, y, gamma, beta, run_mean, run_var, momentum, eps, relu, training, z, save_mean,
+                    save_invstd, (char*)ws, (cudaStream_t)stream, res);
+}
+
 int qd_bn_backward_D(const qd_desc* d, const void* dz, const void* y, const void* a, const void* b,
                      const float* gamma, const float* beta, const float* save_mean, const float* save_invstd,
                      int relu, void* D, float* dgamma, float* dbeta, float* const db[3], void* ws, void* stream) {

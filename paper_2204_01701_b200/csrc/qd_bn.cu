@@ -195,7 +195,7 @@ template <typename T>
 __global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C, const T* __restrict__ y,
                                                            const float* mean, const float* invstd,
                                                            const float* gamma, const float* beta, int relu,
-                                                           T* __restrict__ z) {
+                                                           T* __restrict__ z, const T* __restrict__ res) {
   ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
   ptx::pdl_launch();
   const int CQ = C / 8, lanes = 256 / CQ;
@@ -211,25 +211,29 @@ __global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C
   // main loop: 4 rows whose loads are all issued before any use (a guarded
   // single-row loop keeps one load in flight per thread: ~2.4 TB/s)
   for (; r + 3 * step < rows; r += 4 * step) {
-    float v[4][8];
+    float v[4][8], rv[4][8];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) BV<T>::ld8(y + (size_t)(r + u * step) * C + c0, v[u]);
+    for (int u = 0; u < 4; ++u) {
+      BV<T>::ld8(y + (size_t)(r + u * step) * C + c0, v[u]);
+      if (res) BV<T>::ld8(res + (size_t)(r + u * step) * C + c0, rv[u]);
+    }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
-        const float t = fmaf(sc[e], v[u][e], sh[e]);
+        const float t = fmaf(sc[e], v[u][e], sh[e]) + (res ? rv[u][e] : 0.f);
         v[u][e] = (relu && t < 0.f) ? 0.f : t;
       }
       BV<T>::st8(z + (size_t)(r + u * step) * C + c0, v[u]);
     }
   }
   for (; r < rows; r += step) {
-    float v[8];
+    float v[8], rv[8];
     BV<T>::ld8(y + (size_t)r * C + c0, v);
+    if (res) BV<T>::ld8(res + (size_t)r * C + c0, rv);
 #pragma unroll
     for (int e = 0; e < 8; ++e) {
-      const float t = fmaf(sc[e], v[e], sh[e]);
+      const float t = fmaf(sc[e], v[e], sh[e]) + (res ? rv[e] : 0.f);
       v[e] = (relu && t < 0.f) ? 0.f : t;
     }
     BV<T>::st8(z + (size_t)r * C + c0, v);
@@ -672,11 +676,11 @@ __global__ void __launch_bounds__(1024) bn_stats_finalize(long long M, int C, in
 
 template <typename T>
 __global__ void bn_apply_kernel(long long n, int C, const T* y, const float* mean, const float* invstd,
-                                const float* gamma, const float* beta, int relu, T* z) {
+                                const float* gamma, const float* beta, int relu, T* z, const T* res) {
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
        i += (long long)gridDim.x * blockDim.x) {
     const int c = (int)(i % C);
-    float v = fmaf(gamma[c], (ld(y + i) - mean[c]) * invstd[c], beta[c]);
+    float v = fmaf(gamma[c], (ld(y + i) - mean[c]) * invstd[c], beta[c]) + (res ? ld(res + i) : 0.f);
     if (relu && v < 0.f) v = 0.f;
     z[i] = cvt<T>(v);
   }
@@ -768,7 +772,7 @@ __global__ void __launch_bounds__(256) bn_emit_D_kernel(Plan P, const T* __restr
 template <typename T>
 static int bn_forward_t(long long M, int C, const T* y, const float* gamma, const float* beta, float* rm, float* rv,
                         float momentum, float eps, int relu, int training, T* z, float* sm, float* si, char* ws,
-                        cudaStream_t st) {
+                        cudaStream_t st, const T* res) {
   if (dev_skip("bn")) return QD_OK;
   const int S = bn_splits(M, C);
   float* part = (float*)ws;
@@ -789,9 +793,9 @@ static int bn_forward_t(long long M, int C, const T* y, const float* gamma, cons
   if (g > 148 * 8) g = 148 * 8;
   if (bn_vec(C))
     launch_pdl(bn_apply_vec_kernel<T>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, (const float*)sm, (const float*)si,
-               gamma, beta, relu, z);
+               gamma, beta, relu, z, res);
   else
-    bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z);
+    bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z, res);
   count_launch(st, "bn_apply");
   return check_launch("bn forward");
 }
@@ -829,12 +833,12 @@ static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, c
 
 int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta, float* rm,
                float* rv, float momentum, float eps, int relu, int training, void* z, float* sm, float* si, char* ws,
-               cudaStream_t st) {
+               cudaStream_t st, const void* res) {
   if (dtype == QD_BF16)
     return bn_forward_t<bf16>(M, C, (const bf16*)y, gamma, beta, rm, rv, momentum, eps, relu, training, (bf16*)z, sm,
-                              si, ws, st);
+                              si, ws, st, (const bf16*)res);
   return bn_forward_t<float>(M, C, (const float*)y, gamma, beta, rm, rv, momentum, eps, relu, training, (float*)z,
-                             sm, si, ws, st);
+                             sm, si, ws, st, (const float*)res);
 }
 
 int bn_backward_D(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,

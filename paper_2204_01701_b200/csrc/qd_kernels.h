@@ -117,7 +117,7 @@ void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], cons
 size_t bn_workspace_bytes(long long M, int C, int Jd);
 int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta, float* rm,
                float* rv, float momentum, float eps, int relu, int training, void* z, float* sm, float* si, char* ws,
-               cudaStream_t st);
+               cudaStream_t st, const void* res = nullptr);
 int bn_backward_D(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,
                   const float* beta, const float* sm, const float* si, int relu, void* D, float* dgamma,
                   float* dbeta, float* const db[3], char* ws, cudaStream_t st);

@@ -80,8 +80,8 @@ class QuadBasicBlock(nn.Module):
 
     def forward(self, x):
         idt = x if self.down is None else self.down(x)
-        out = self.cb2(self.cbr1(x))
-        return self.relu(out + idt)
+        # cb2's BN apply also adds the identity and applies the block's ReLU
+        return self.cb2.forward_add_relu(self.cbr1(x), idt)
 
 
 class QuadraResNet18(nn.Module):

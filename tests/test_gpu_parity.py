@@ -276,6 +276,53 @@ def test_deterministic_replay():
         assert (r1[3][role] == r2[3][role]).all()
 
 
+def test_c2_partitioned_step_fold_deterministic(monkeypatch):
+    """C2 geometry: the wgrad3 / dgrad SM partition with wgrad3's in-kernel
+    split-K fold (grid barrier + fixed-order slot sums) replays bit for bit, and
+    agrees with the separate-kernel fold (QD_W3_NOFOLD=1; another summation
+    order) to fp32 round-off; also under a CUDA graph replay."""
+    from paper_2204_01701_b200 import neurons
+    x, P, g = Q.synthetic_layer("proposed", "conv", 128, 64, 64, 32, 32, 3, 1, 1, seed=9)
+    r1 = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    r2 = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    for role in r1[3]:
+        assert (r1[3][role] == r2[3][role]).all(), role
+    assert (r1[4] == r2[4]).all()
+    monkeypatch.setenv("QD_W3_NOFOLD", "1")
+    r3 = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    monkeypatch.delenv("QD_W3_NOFOLD")
+    for role in r1[3]:
+        assert Q.rel_err(r1[3][role], r3[3][role]) <= 1e-5, role
+    # graph capture + two replays (the barrier slots reset themselves)
+    dev = torch.device("cuda")
+    spec = _spec("proposed", "conv", 64, 64, 3, 1, 1)
+    xt = torch.as_tensor(x, device=dev).bfloat16().contiguous(memory_format=torch.channels_last)
+    gt = torch.as_tensor(g, device=dev).bfloat16().contiguous(memory_format=torch.channels_last)
+    params = {r: torch.as_tensor(v, dtype=torch.float32, device=dev) for r, v in P.items()}
+    out = {}
+
+    def step():
+        y, cache = neurons.forward(spec, params, xt)
+        grads, dx = neurons.symbolic_backward(spec, params, cache, gt)
+        out["g"] = grads
+    s = torch.cuda.Stream()
+    s.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(s):
+        step()
+    torch.cuda.current_stream().wait_stream(s)
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        step()
+    reps = []
+    for _ in range(2):
+        graph.replay()
+        torch.cuda.synchronize()
+        reps.append({r: v.double().cpu().numpy().copy() for r, v in out["g"].items()})
+    for role in reps[0]:
+        assert (reps[0][role] == reps[1][role]).all(), role
+        assert Q.rel_err(reps[0][role], r1[3][role]) <= 1e-5, role
+
+
 def test_error_conventions_on_device():
     from paper_2204_01701_b200 import neurons
     from paper_2204_01701_b200.errors import DimensionError, IntegrityError
@@ -459,6 +506,50 @@ def test_quadconvbn_fused_matches_reference_bn(family, kind, relu):
             continue
         assert rel(g1[n], g2[n]) <= 3e-2, (n, rel(g1[n], g2[n]))
     assert torch.allclose(rm1, rm2, rtol=1e-3, atol=1e-4) and torch.allclose(rv1, rv2, rtol=1e-3, atol=1e-4)
+
+
+@pytest.mark.gpu
+def test_quadconvbn_add_relu_matches_composition():
+    """ResNet block tail relu(BN(layer(x)) + res) as one fused node (residual add
+    and ReLU on the BN apply pass, mask z > 0 in the backward) vs the module's
+    unfused composition on identical inputs and parameters."""
+    import copy
+    from paper_2204_01701_b200.bn import QuadConvBN
+    from paper_2204_01701_b200.nn import QuadConv2d
+    torch.manual_seed(6)
+    mod = QuadConvBN(QuadConv2d(64, 64, 3, 1, 1, device="cuda"), relu=False)
+    ref = copy.deepcopy(mod)
+    x0 = torch.randn(4, 64, 12, 12, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    r0 = torch.randn(4, 64, 12, 12, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    gz = torch.randn(4, 64, 12, 12, device="cuda").bfloat16()
+    x1, r1 = x0.clone().requires_grad_(True), r0.clone().requires_grad_(True)
+    z1 = mod.forward_add_relu(x1, r1)
+    z1.backward(gz)
+    x2, r2 = x0.clone().requires_grad_(True), r0.clone().requires_grad_(True)
+    import os
+    os.environ["QD_NO_BNFUSE"] = "1"
+    try:
+        z2 = ref.forward_add_relu(x2, r2)
+    finally:
+        del os.environ["QD_NO_BNFUSE"]
+    z2.backward(gz)
+    rel = lambda a, b: Q.rel_err(a.detach().double().cpu().numpy(), b.detach().double().cpu().numpy())  # noqa
+    assert rel(z1, z2) <= 2e-2, rel(z1, z2)
+    # the ReLU masks agree except where bf16 rounding of BN(y) + res lands on the
+    # other side of 0 (a max-norm error there is one whole gz value): the residual
+    # gradient equals gz on the fused path's own mask exactly, and gradients are
+    # compared in the Frobenius norm
+    assert ((z1 > 0) != (z2 > 0)).float().mean().item() <= 5e-3
+    assert torch.equal(r1.grad, gz * (z1.detach() > 0))
+    fro = lambda a, b: ((a.double() - b.double()).norm() / b.double().norm()).item()  # noqa: E731
+    assert fro(r1.grad, r2.grad) <= 5e-2, fro(r1.grad, r2.grad)
+    assert fro(x1.grad, x2.grad) <= 5e-2, fro(x1.grad, x2.grad)
+    g2 = dict(ref.named_parameters())
+    for n, p in mod.named_parameters():
+        if n == "layer.bc":  # exactly zero through BN: round-off only
+            continue
+        assert fro(p.grad, g2[n].grad) <= 5e-2, (n, fro(p.grad, g2[n].grad))
+    assert torch.allclose(mod.bn.running_mean, ref.bn.running_mean, rtol=1e-3, atol=1e-4)
 
 
 @pytest.mark.gpu
