@@ -199,6 +199,67 @@ __global__ void __launch_bounds__(256) maxpool_bwd_kernel(PoolGeo g, const T* __
   PV<T>::st8(dx + (size_t)i * 8, acc);
 }
 
+// k3 s2 p1 (the ResNet stem), even H and W: one thread per 2x2 input block x 8
+// channels. The block's pixels are covered by windows (i, j), (i, j+1),
+// (i+1, j), (i+1, j+1) only (i = h/2, j = w/2), so each window's argmax bytes
+// and dy are loaded once for four pixels (the per-pixel gather loaded 9 window
+// reads per 4 pixels and redid the index math for each); the per-pixel sums
+// keep the window order of the general kernel (bit-identical results).
+template <typename T>
+__global__ void __launch_bounds__(256) maxpool_bwd_k3s2_kernel(PoolGeo g, const T* __restrict__ dy,
+                                                               const uint8_t* __restrict__ arg, T* __restrict__ dx) {
+  const unsigned c8 = g.C / 8, BW = g.W / 2, BH = g.H / 2;
+  const unsigned i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (unsigned)g.N * BH * BW * c8) return;
+  const unsigned cq = i % c8;
+  unsigned t = i / c8;
+  const int bj = (int)(t % BW);
+  t /= BW;
+  const int bi = (int)(t % BH);
+  const int n = (int)(t / BH);
+  float acc[4][8];
+#pragma unroll
+  for (int q = 0; q < 4; ++q)
+#pragma unroll
+    for (int e = 0; e < 8; ++e) acc[q][e] = 0.f;
+  uint2 av[4];
+  float v[4][8];
+  bool ok[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {  // windows (bi + u/2, bj + u%2), all loads in flight
+    const int oh = bi + u / 2, ow = bj + u % 2;
+    ok[u] = oh < g.OH && ow < g.OW;
+    const size_t oidx = (((size_t)n * g.OH + oh) * g.OW + ow) * g.C + cq * 8;
+    if (ok[u]) {
+      av[u] = __ldg(reinterpret_cast<const uint2*>(arg + oidx));
+      PV<T>::ld8(dy + oidx, v[u]);
+    }
+  }
+  // pixel (dh, dw) of the block sits at window offset ky * 3 + kx with
+  // ky = dh + 1 (window row bi) or dh - 1 (row bi + 1, only dh = 1); kx alike
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    if (!ok[u]) continue;
+    const uint8_t* ab = reinterpret_cast<const uint8_t*>(&av[u]);
+    const int wy = u / 2, wx = u % 2;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int dh = q / 2, dw = q % 2;
+      const int ky = wy == 0 ? dh + 1 : dh - 1, kx = wx == 0 ? dw + 1 : dw - 1;
+      if (ky < 0 || kx < 0) continue;
+      const uint8_t o = (uint8_t)(ky * 3 + kx);
+#pragma unroll
+      for (int e = 0; e < 8; ++e)
+        if (ab[e] == o) acc[q][e] += v[u][e];
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int h = 2 * bi + q / 2, w = 2 * bj + q % 2;
+    PV<T>::st8(dx + ((((size_t)n * g.H + h) * g.W + w) * g.C) + cq * 8, acc[q]);
+  }
+}
+
 static int pool_geo(int N, int C, int H, int W, int k, int s, int p, PoolGeo& g) {
   if (N < 1 || C < 8 || C % 8 || H < 1 || W < 1) return set_error(QD_ERR_DIM, "maxpool: N %d C %d H %d W %d", N, C, H, W);
   if (k < 1 || k > 15 || s < 1 || p < 0 || 2 * p > k) return set_error(QD_ERR_CONFIG, "maxpool: k %d s %d p %d", k, s, p);
@@ -243,6 +304,15 @@ int maxpool_backward(int N, int C, int H, int W, int k, int s, int p, int dtype,
   const long long n = (long long)N * H * W * (C / 8);
   if (n >= (1LL << 31)) return set_error(QD_ERR_DIM, "maxpool: %lld channel groups (max 2^31)", n);
   const unsigned blocks = (unsigned)((n + 255) / 256);
+  if (k == 3 && s == 2 && p == 1 && H % 2 == 0 && W % 2 == 0 && g.OH == H / 2 && g.OW == W / 2) {
+    const unsigned b4 = (unsigned)((n / 4 + 255) / 256);
+    if (dtype == QD_BF16)
+      maxpool_bwd_k3s2_kernel<bf16><<<b4, 256, 0, st>>>(g, (const bf16*)dy, (const uint8_t*)arg, (bf16*)dx);
+    else
+      maxpool_bwd_k3s2_kernel<float><<<b4, 256, 0, st>>>(g, (const float*)dy, (const uint8_t*)arg, (float*)dx);
+    count_launch(st, "maxpool_bwd");
+    return check_launch("maxpool backward");
+  }
   // windows per axis covering an input position: ceil(k / s); 2 is the common case
   const int nw = (k + s - 1) / s;
 #define QD_MPB(T, NW) maxpool_bwd_kernel<T, NW><<<blocks, 256, 0, st>>>(g, (const T*)dy, (const uint8_t*)arg, (T*)dx)

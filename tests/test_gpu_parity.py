@@ -616,7 +616,8 @@ def test_memory_ledger_accounts_minimal_cache():
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
 @pytest.mark.parametrize("geo", [(3, 2, 1, 2, 64, 23, 17), (2, 2, 0, 3, 16, 8, 8), (3, 1, 1, 1, 8, 5, 6),
-                                 (2, 2, 0, 2, 512, 3, 5)])
+                                 (2, 2, 0, 2, 512, 3, 5),
+                                 (3, 2, 1, 2, 64, 24, 18), (3, 2, 1, 3, 16, 2, 4)])  # k3s2p1 even: 2x2-block bwd
 def test_maxpool_matches_torch(geo, dtype):
     from paper_2204_01701_b200.pool import MaxPool2d
     k, s, p, n, c, h, w = geo
