@@ -598,8 +598,10 @@ def net_quad_layers(name):
     from paper_2204_01701_b200.bn import QuadConvBN
     for m in model.modules():
         if isinstance(m, QuadConvBN):  # fused conv -> BN (-> ReLU) node: its layer never runs forward()
+            # (the first-order 1x1 shortcuts are not quadratic layers)
             hooks.append(m.register_forward_pre_hook(
-                lambda mod, inp: shapes.append((mod.layer.spec, tuple(inp[0].shape[1:])))))
+                lambda mod, inp: shapes.append((mod.layer.spec, tuple(inp[0].shape[1:])))
+                if mod.layer.spec.family != "first_order" else None))
         elif isinstance(m, QuadConv2d) and id(m) not in inner:
             hooks.append(m.register_forward_pre_hook(
                 lambda mod, inp: shapes.append((mod.spec, tuple(inp[0].shape[1:])))))

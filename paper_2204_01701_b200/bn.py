@@ -246,13 +246,13 @@ class QuadConvBN(nn.Module):
             return False
         if sp.stride == 2:
             # stride 2 fuses when the layer runs on its own output grid (the
-            # library's tc_s2_direct: tcgen05 path, plain-K family, k >= 2), so
+            # library's tc_s2_direct: tcgen05 path, plain-K family), so
             # the emitted D is the operand its backward consumes as is
             if x is None or sp.kind != "conv" or sp.family not in ("proposed", "t4", "first_order"):
                 return False
             oh = (x.shape[2] + 2 * sp.pad - sp.kernel) // 2 + 1
             ow = (x.shape[3] + 2 * sp.pad - sp.kernel) // 2 + 1
-            return (sp.kernel >= 2 and oh <= 128 and ow <= 128 and self.layer.compute_dtype == torch.bfloat16
+            return (oh <= 128 and ow <= 128 and self.layer.compute_dtype == torch.bfloat16
                     and neurons.device_path(sp, tuple(x.shape), torch.bfloat16) == 1)
         return (sp.stride == 1 and sp.kind in ("conv", "fc") and sp.family not in ("t3", "t1_pure", "t1_full",
                                                                                    "t1and2"))
@@ -260,7 +260,8 @@ class QuadConvBN(nn.Module):
     def forward_add_relu(self, x, res):
         """relu(BN(layer(x)) + res) -- the block tail of a residual net; one
         fused node on the library kernels when the layer's BN is fused, else the
-        composition (the module's own relu flag is not applied here)."""
+        composition (the module's own relu flag is not applied here). Reached as
+        ``module(x, res)`` (so module hooks see it)."""
         if (self.training and x.device.type == "cuda" and self.fused(x)
                 and res.shape[1] == self.layer.spec.out_dim):
             spec = self.layer.spec
@@ -274,7 +275,9 @@ class QuadConvBN(nn.Module):
             self.relu = relu
         return torch.relu(out + res)
 
-    def forward(self, x):
+    def forward(self, x, res=None):
+        if res is not None:
+            return self.forward_add_relu(x, res)
         spec = self.layer.spec
         roles = tuple(param_shapes(spec).keys())
         tensors = [getattr(self.layer, r) for r in roles]

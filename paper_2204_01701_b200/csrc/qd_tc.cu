@@ -266,6 +266,7 @@ __global__ void __launch_bounds__(256, 1)
         const int ih = 2 * h + cw.ph, iw = 2 * w + cw.pw;
         const bool ok = row < args.box_rows && n < args.Ng && h < args.OHg && w < args.OWg && ih < args.Hx &&
                         iw < args.Wx;
+        const bool zero = cw.kb1 == cw.kb0;  // a class no tap reaches (r = 1): dx = 0 there
         bf16* orow = args.out + (((size_t)n * args.Hx + ih) * args.Wx + iw) * args.Cout + ntile * args.out_c_tile;
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) {
@@ -273,6 +274,12 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
           for (int i = 0; i < NB; ++i) ptx::tmem_ld16(tb + i * 64 + j * 16, v[i]);
           ptx::tmem_wait_ld();
+          if (zero) {
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+#pragma unroll
+              for (int e = 0; e < 16; ++e) v[i][e] = 0.f;
+          }
           if (ok) {
 #pragma unroll
             for (int i = 0; i < NB; ++i) {
@@ -891,12 +898,12 @@ static bool s2_fits(const Plan& P) {
 
 // stride 2 on its own output grid (v1 kernels): fprop and wgrad read x through
 // traversal-stride-2 TMA maps, the dgrad runs as four output-parity classes of
-// D (no zero-upsampled operand, no 4x work). Every class needs a tap (r >= 2);
-// the squared-input families keep the stride-1-grid path (x*x operand, EPI_SQ
+// D (no zero-upsampled operand, no 4x work); a class no tap reaches (r = 1)
+// stores zeros. The squared-input families keep the stride-1-grid path (x*x operand, EPI_SQ
 // dgrad). QD_S2_UPSAMPLE=1 forces the stride-1-grid path (A/B checks).
 bool tc_s2_direct(const Plan& P) {
   static const bool off = getenv("QD_S2_UPSAMPLE") && atoi(getenv("QD_S2_UPSAMPLE"));
-  return P.s == 2 && P.kind == QD_KIND_CONV && P.r >= 2 && P.sq == 0 && P.family != QD_FAM_T3 && !off &&
+  return P.s == 2 && P.kind == QD_KIND_CONV && P.r >= 1 && P.sq == 0 && P.family != QD_FAM_T3 && !off &&
          P.OW <= 128 && P.OH <= 128 && P.dtype == QD_BF16 && P.C % 64 == 0 && P.F % 64 == 0;
 }
 
@@ -1129,8 +1136,8 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
     int code[4], n = 0;
     for (int ph = 0; ph < 2; ++ph)
       for (int pw = 0; pw < 2; ++pw) {
+        // a class no tap reaches (r = 1) keeps 0 k-blocks: its tiles store zeros
         const int nty = (r - ((pad_eff - ph) & 1) + 1) / 2, ntx = (r - ((pad_eff - pw) & 1) + 1) / 2;
-        if (nty < 1 || ntx < 1) return set_error(QD_ERR_UNSUPPORTED, "parity class without taps");
         code[n++] = ph | pw << 1 | (nty * ntx * g.cblks) << 2;
       }
     for (int i = 0; i < 4; ++i)

@@ -76,12 +76,14 @@ class QuadBasicBlock(nn.Module):
         self.relu = nn.ReLU(inplace=True)
         self.down = None
         if stride != 1 or inplanes != planes:
-            self.down = nn.Sequential(nn.Conv2d(inplanes, planes, 1, stride, bias=False), BNAct2d(planes))
+            # 1x1 (stride 2) shortcut + BN as one node on the library kernels (first-order
+            # family; its bias cancels in the BN like the quadratic layers' biases)
+            self.down = QuadConvBN(quad_conv(inplanes, planes, 1, stride, 0, "first_order"), relu=False)
 
     def forward(self, x):
         idt = x if self.down is None else self.down(x)
         # cb2's BN apply also adds the identity and applies the block's ReLU
-        return self.cb2.forward_add_relu(self.cbr1(x), idt)
+        return self.cb2(self.cbr1(x), idt)
 
 
 class QuadraResNet18(nn.Module):

@@ -129,6 +129,9 @@ TC_CASES = [
     ("t4", "conv", 5, 128, 64, 8, 8, 3, 2, 1),
     ("first_order", "conv", 2, 64, 128, 16, 16, 3, 2, 1),
     ("t2_linear", "conv", 2, 64, 64, 16, 18, 3, 2, 1),
+    # 1x1 stride 2 (ResNet shortcuts): three of the four parity classes get no tap
+    ("first_order", "conv", 2, 64, 128, 16, 16, 1, 2, 0),
+    ("proposed", "conv", 3, 64, 64, 9, 11, 1, 2, 0),
     ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
     ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
     ("t2_linear", "fc", 64, 128, 64, 1, 1, 1, 1, 0),

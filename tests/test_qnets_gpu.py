@@ -51,7 +51,8 @@ def test_quad_layers_use_tcgen05():
     from paper_2204_01701_b200 import neurons, qnets
     from paper_2204_01701_b200.nn import QuadConv2d
     m = qnets.QuadraResNet18(10).cuda().to(memory_format=torch.channels_last)
-    assert len([q for q in m.modules() if isinstance(q, QuadConv2d)]) == 16
+    # 16 quadratic 3x3 convs + the three first-order 1x1 shortcuts
+    assert len([q for q in m.modules() if isinstance(q, QuadConv2d)]) == 19
     # every quadratic conv's forward goes through neurons.forward (fused BN node,
     # fused BN + residual + ReLU node, or the plain layer): record its device path
     seen = []
@@ -68,7 +69,7 @@ def test_quad_layers_use_tcgen05():
             m(x)
     finally:
         neurons.forward = orig
-    assert len(seen) == 16 and all(p == 1 for p in seen), seen
+    assert len(seen) == 19 and all(p == 1 for p in seen), seen
 
 
 def test_graphed_step_matches_eager():
