@@ -629,18 +629,25 @@ __device__ __forceinline__ bool bn_fold2(int C, int S, const float* part, float&
   __shared__ float red[16][65];
   const int col = threadIdx.x % 64, grp = threadIdx.x / 64;
   const int k = col / 32, c = blockIdx.x * 32 + col % 32;
-  float a0 = 0.f, a1 = 0.f;
+  // eight independent chains per thread (8 partial loads in flight: the fold
+  // is L2-latency bound -- two chains took ~7 us for S ~ 600), combined in order
+  float a[8];
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.f;
   if (c < C) {
     const float* p = part + (size_t)k * C + c;
     const size_t step = (size_t)2 * C;
     int sp = grp;
-    for (; sp + 16 < S; sp += 32) {
-      a0 += p[(size_t)sp * step];
-      a1 += p[(size_t)(sp + 16) * step];
+    for (; sp + 7 * 16 < S; sp += 8 * 16) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = p[(size_t)(sp + 16 * u) * step];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += v[u];
     }
-    if (sp < S) a0 += p[(size_t)sp * step];
+    for (; sp < S; sp += 16) a[0] += p[(size_t)sp * step];
   }
-  red[grp][col] = a0 + a1;
+  red[grp][col] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   __syncthreads();
   if (grp != 0 || col >= 32 || c >= C) return false;
   s1 = 0.f;
