@@ -811,18 +811,21 @@ __device__ __forceinline__ void finish_bias_block(const Plan& P, int bblk, const
   __shared__ float redb[32][9];
   const int bc = threadIdx.x % 8, bg = threadIdx.x / 8;
   int j = bblk * 8 + bc;
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  float a[8];  // eight chains: 8 partial loads in flight per thread (latency-bound fold)
+#pragma unroll
+  for (int u = 0; u < 8; ++u) a[u] = 0.f;
   if (j < P.Jd) {
     int s = bg;
-    for (; s + 96 < SB; s += 128) {
-      a0 += bpart[(size_t)s * P.Jd + j];
-      a1 += bpart[(size_t)(s + 32) * P.Jd + j];
-      a2 += bpart[(size_t)(s + 64) * P.Jd + j];
-      a3 += bpart[(size_t)(s + 96) * P.Jd + j];
+    for (; s + 7 * 32 < SB; s += 8 * 32) {
+      float v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = bpart[(size_t)(s + 32 * u) * P.Jd + j];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) a[u] += v[u];
     }
-    for (; s < SB; s += 32) a0 += bpart[(size_t)s * P.Jd + j];
+    for (; s < SB; s += 32) a[0] += bpart[(size_t)s * P.Jd + j];
   }
-  redb[bg][bc] = (a0 + a1) + (a2 + a3);
+  redb[bg][bc] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
   __syncthreads();
   if (bg == 0 && j < P.Jd) {
     float t = 0.f;
