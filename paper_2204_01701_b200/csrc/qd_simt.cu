@@ -1019,22 +1019,31 @@ __global__ void __launch_bounds__(256) wsum_kernel(Plan P, float* __restrict__ p
         for (int t = 0; t < 16; ++t)  // static indexing: no local-memory copy of wsp
           if (t == tg) Sk = wsp.s[t];
       }
-      float4 c1 = acc, c2 = acc, c3 = acc;
+      // eight chains: 8 slice loads in flight per thread (L2-latency bound)
+      float4 c[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) c[u] = acc;
       int s = grp;
-      for (; s + 3 * G < Sk; s += 4 * G) {
-        const float4 v0 = p4[s * n4 + i], v1 = p4[(s + G) * n4 + i];
-        const float4 v2 = p4[(s + 2 * G) * n4 + i], v3 = p4[(s + 3 * G) * n4 + i];
-        acc.x += v0.x; acc.y += v0.y; acc.z += v0.z; acc.w += v0.w;
-        c1.x += v1.x; c1.y += v1.y; c1.z += v1.z; c1.w += v1.w;
-        c2.x += v2.x; c2.y += v2.y; c2.z += v2.z; c2.w += v2.w;
-        c3.x += v3.x; c3.y += v3.y; c3.z += v3.z; c3.w += v3.w;
+      for (; s + 7 * G < Sk; s += 8 * G) {
+        float4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = p4[(s + u * G) * n4 + i];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          c[u].x += v[u].x; c[u].y += v[u].y; c[u].z += v[u].z; c[u].w += v[u].w;
+        }
       }
       for (; s < Sk; s += G) {
         const float4 v = p4[s * n4 + i];
-        acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        c[0].x += v.x; c[0].y += v.y; c[0].z += v.z; c[0].w += v.w;
       }
-      acc.x += c1.x + (c2.x + c3.x); acc.y += c1.y + (c2.y + c3.y);
-      acc.z += c1.z + (c2.z + c3.z); acc.w += c1.w + (c2.w + c3.w);
+#pragma unroll
+      for (int e = 4; e > 0; e >>= 1)
+#pragma unroll
+        for (int u = 0; u < e; ++u) {
+          c[u].x += c[u + e].x; c[u].y += c[u + e].y; c[u].z += c[u + e].z; c[u].w += c[u + e].w;
+        }
+      acc = c[0];
     }
     red[threadIdx.x] = acc;
     __syncthreads();  // every group has read slice 0 before it is overwritten
