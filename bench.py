@@ -280,15 +280,26 @@ def run_reference(args, wl, wl_name):
     value = flops / mean / 1e12
     sample = (f"{wl_name} at batch {batch} of {wl[2]} (fp64 numpy/BLAS reference algorithm: "
               f"im2col + GEMM + col2im), mean of {args.steps} steps")
+    # ms_per_step is the MEASURED time of one step of the bounded sample (batch
+    # `step_batch`); value is its rate, which is linear in the batch (im2col, GEMM M
+    # and col2im all scale with N)
     out = {"metric": METRIC, "value": value, "unit": "TFLOP/s", "impl": "reference",
            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-           "ms_per_step": mean * 1e3 * wl[2] / batch, "higher_is_better": True,
+           "ms_per_step": mean * 1e3, "step_batch": batch, "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": config_of(wl, wl_name, args.gpus),
            "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": cores, "kind": "port",
                             "sample": sample},
            "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
+    nets = {}
+    for net in args.nets:
+        secs = [net_cpu_baseline(net) for _ in range(max(1, min(args.steps, 3)))]
+        sec = sum(secs) / len(secs)
+        nets[net] = {"metric": f"{net}_train_img_per_s", "value": 1.0 / sec, "unit": "img/s",
+                     "ms_per_step": sec * 1e3, "step_batch": 1,
+                     "sample": "reference algorithm fwd+bwd of every quadratic layer at batch 1, summed"}
+    out["nets"] = nets
     print(json.dumps(out), flush=True)
     return 0
 
@@ -464,7 +475,11 @@ def run_ours(args, wl, wl_name):
         if k in tensor_k:
             e["tflops"] = third / (v * 1e-3) / 1e12
         elif k.startswith("prologue"):
-            e["gbs"] = 2 * 3 * m_out * f * es / (v * 1e-3) / 1e9  # reads dy, a, b; writes D (3 F channels)
+            # reads dy, a, b (3 F channels); writes D: [g b | g a] (2 F) for proposed at
+            # stride 1 (the GEMMs read g from dy), [g b | g a | g] (3 F) otherwise; t4 2 F
+            wcols = 2 * f if (fam == "t4" or (fam == "proposed" and s == 1)) else 3 * f
+            e["gbs"] = (3 * f + wcols) * m_out * es / (v * 1e-3) / 1e9
+            e["bytes"] = (3 * f + wcols) * m_out * es
         kernels[k] = e
     dom = max(tensor_k, key=lambda k_: tensor_k[k_]) if tensor_k else max(kern, key=lambda k_: kern[k_])
     traffic = None
@@ -487,7 +502,22 @@ def run_ours(args, wl, wl_name):
                       "SMs (QD_NO_PART; the split-K fold then runs as wsum + bwd_finish); the timed step "
                       "overlaps wgrad3 and dgrad on disjoint SM partitions, the partitioned wgrad3 folding "
                       "its partials in-kernel"}
-    if dts != "bf16":
+    if kind == "dwconv":
+        # depth-wise: r*r MACs per output element -- HBM-bound elementwise-like kernels;
+        # algorithmic bytes per launch in units of one (M x C) activation tensor
+        unit = m_out * c * es
+        per = {"dw_fwd": 4, "prologue": 6, "dw_wgrad": 4, "dw_dgrad": 4}  # x->y,a,b; dy,a,b->D; x,D; D->dx
+        for k_, e in kernels.items():
+            if k_ in per:
+                e["bytes"] = per[k_] * unit
+                e["gbs"] = e["bytes"] / (e["ms"] * 1e-3) / 1e9
+        dk = max((k_ for k_ in kernels if k_ in per), key=lambda k_: kernels[k_]["ms"])
+        roof = {"bound": "hbm", "kernel": dk, "achieved": kernels[dk]["gbs"], "peak": pk["hbm"], "unit": "GB/s",
+                "frac": kernels[dk]["gbs"] / pk["hbm"], "traffic": None, "kernels": kernels,
+                "peak_src": f"{pk['src']} HBM copy bandwidth",
+                "algorithmic": "per launch: the activation tensors the kernel must read and write once "
+                               "(dw_fwd x -> y, a, b; prologue dy, a, b -> D; dw_wgrad x, D; dw_dgrad D -> dx)"}
+    elif dts != "bf16":
         roof["note"] = "fp32 runs on the CUDA-core (FFMA) path; the bf16 tensor peak is the denominator"
 
     # ---- end to end through the public API with host buffers ----
@@ -528,6 +558,12 @@ def run_ours(args, wl, wl_name):
         v.numel() * 4 for v in w_h.values())
     d2h = dx_h.numel() * dx_h.element_size() + sum(v.numel() * 4 for v in gr_h.values())
 
+    # the data-parallel training config the scaling target names (BASELINE.json:
+    # QuadraResNet-18 img/s at 1/2/4/8 GPUs), measured in the same run at this N
+    nets = {}
+    for net in args.nets:
+        nets[net] = measure_net(args, net, world, rank, local, dev)
+
     if world > 1:
         dist.barrier()
     if rank != 0:
@@ -548,7 +584,7 @@ def run_ours(args, wl, wl_name):
            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
            "dtype": dts, "data": "synthetic (seeded N(0,1) x and dy, Kaiming-uniform W, b=0)",
-           "config": dict(config_of(wl, wl_name, world), cuda_graph=not args.no_graph),
+           "config": config_of(wl, wl_name, world), "cuda_graph": not args.no_graph,
            "roofline": roof, "cpu_baseline": cpu,
            "e2e": {"value": world * flops / (e2e_step_ms * 1e-3) / 1e12, "unit": "TFLOP/s",
                    "ms_per_step": e2e_step_ms, "h2d_bytes_per_step": h2d,
@@ -559,7 +595,7 @@ def run_ours(args, wl, wl_name):
                            "flush inside the loop (inputs arrive over PCIe every step, the step's own traffic "
                            "exceeds L2)"},
            "gpu_launches": launches, "launches_per_step": launches / args.steps,
-           "clocks": clocks,
+           "clocks": clocks, "nets": nets,
            "path": "tcgen05" if neurons.device_path(spec, x.shape, dt) == 1 else "cuda-core"}
     print(json.dumps(out), flush=True)
     if world > 1:
@@ -655,10 +691,6 @@ def run_net(args, name):
     import torch
     import torch.distributed as dist
 
-    from paper_2204_01701_b200 import _lib, qnets
-    from paper_2204_01701_b200.dp import BucketedAllReduce, broadcast_module, sgd
-    from paper_2204_01701_b200.optim import QuadSGD
-
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -667,6 +699,24 @@ def run_net(args, name):
     if world > 1:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
+    out = measure_net(args, name, world, rank, local, dev)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def measure_net(args, name, world, rank, local, dev):
+    """One QuadraNet training-step measurement on every rank (the process group,
+    if any, is already up); returns rank 0's JSON object (None on other ranks)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2204_01701_b200 import _lib, qnets
+    from paper_2204_01701_b200.dp import BucketedAllReduce, broadcast_module, sgd
+    from paper_2204_01701_b200.optim import QuadSGD
+
     builder, batch, hw, classes = NETS[name]
     batch = args.batch or batch
     # the first-order convs (ResNet stem, 1x1 shortcuts) run on cuDNN: let it time
@@ -782,10 +832,9 @@ def run_net(args, name):
         e_step = float(tt.item())
     if world > 1:
         dist.barrier()
+    red.remove()
     if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return 0
+        return None
     cpu = None
     if world == 1 and not args.no_cpu:
         sec = net_cpu_baseline(name)
@@ -815,10 +864,7 @@ def run_net(args, name):
                            "on a copy stream, overlapping the previous step's compute) into the graph's input "
                            "buffers and reads the loss back"},
            "gpu_launches": per_step * args.steps, "launches_per_step": per_step, "clocks": clocks}
-    print(json.dumps(out), flush=True)
-    if world > 1:
-        dist.destroy_process_group()
-    return 0
+    return out
 
 
 def run_net_reference(args, name):
@@ -850,7 +896,16 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the CPU baseline sample")
     ap.add_argument("--torch-sgd", action="store_true", help="nets: torch.optim.SGD instead of the fused SGD+pack")
     ap.add_argument("--no-graph", action="store_true", help="launch the step eagerly (no CUDA graph)")
+    ap.add_argument("--nets", default=None,
+                    help="layer workloads: comma list of net training steps measured in the same run and "
+                         "reported under 'nets' (default: qresnet18 for c2, none otherwise; '' = none)")
     args = ap.parse_args()
+    if args.nets is None:
+        args.nets = "qresnet18" if args.workload == "c2" else ""
+    args.nets = [n for n in args.nets.split(",") if n]
+    for n in args.nets:
+        if n not in NETS:
+            ap.error(f"--nets: unknown net {n!r}")
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     if args.workload in NETS:
         if args.impl == "reference":

@@ -110,6 +110,34 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// PDL launch with the cooperative attribute (coop = 1): the driver launches the
+// grid only when every CTA can be resident at once (software grid barriers)
+template <typename... KArgs, typename... Args>
+inline cudaError_t cudaLaunchCoop(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                                  bool coop, Args&&... args) {
+  cudaLaunchConfig_t cfg;
+  memset(&cfg, 0, sizeof(cfg));
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  int n = 0;
+  if (pdl_enabled()) {
+    at[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[n].val.programmaticStreamSerializationAllowed = 1;
+    ++n;
+  }
+  if (coop) {
+    at[n].id = cudaLaunchAttributeCooperative;
+    at[n].val.cooperative = 1;
+    ++n;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = n;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
+
 void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], const float* const grad[3], float lr,
                      float momentum, float wd, int first, void* wpack, cudaStream_t st);
 
@@ -162,7 +190,7 @@ int wgrad3_pairs_per_split(const Plan& P);
 int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0, float* const* dW = nullptr,
-               const float* bpart = nullptr, int SB = 0, float* const* db = nullptr);
+               const float* bpart = nullptr, int SB = 0, float* const* db = nullptr, bool* folded = nullptr);
 // v2 stride-1 conv on CTA pairs (qd_tc2.cu); QD_ERR_UNSUPPORTED if the shape does not fit
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,

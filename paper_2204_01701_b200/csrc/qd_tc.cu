@@ -1380,8 +1380,10 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       for (int i = 0; i < 3; ++i) al16 = al16 && ((uintptr_t)dW[i] % 16 == 0);
       fold3 = part > 0 && al16 && P.kind == QD_KIND_CONV &&
               !(getenv("QD_W3_NOFOLD") && atoi(getenv("QD_W3_NOFOLD")));
+      bool folded = false;
       rc = run_wgrad3(P, x0, P.sq == 2 ? x1 : nullptr, D, (float*)(ws + L.off_WG), ns, wst, dy, dsplit,
-                      fold3 ? dW : nullptr, bpart, L.bs_split, db);
+                      fold3 ? dW : nullptr, bpart, L.bs_split, db, &folded);
+      fold3 = folded;  // the driver may refuse the cooperative launch: then fold separately
       wsp.pp = (P.r * P.r + 1) / 2;  // every tap in every split slot
       wsp.ng = 1;
       wsp.s[0] = ns;

@@ -23,6 +23,7 @@
 // junk columns; TMEM accumulators are double-buffered so this overlaps the
 // next tile's main loop.
 #include <cudaTypedefs.h>
+#include <atomic>
 #include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
@@ -1282,11 +1283,40 @@ struct W3Args {
   Plan P;
 };
 
-// grid-barrier counters of the in-kernel fold (zero at module load): launches
-// take slots round-robin, so only 64 wgrad3 launches in flight at once could
-// collide; the last CTA to leave a barrier resets its slot for the next use
-__device__ unsigned g_w3_arrive[64];
-__device__ unsigned g_w3_depart[64];
+// grid barrier of the in-kernel fold: a sense-reversing barrier per slot. Each
+// CTA reads the slot's generation, arrives on the count; the last arrival
+// re-arms the count and publishes generation + 1, the others wait for the
+// generation to move. Nothing is reset "after" the barrier, so a replay (or
+// a launch of another shape on the same slot) never sees a stale count.
+// Launches take slots from a host-side atomic round-robin allocator; only 64
+// fold launches in flight at once could share a slot.
+__device__ unsigned g_w3_count[64];
+__device__ unsigned g_w3_gen[64];
+
+// grid barrier over a co-resident grid (thread 0 of each CTA calls it between
+// two __syncthreads). A wait past `timeout_ns` traps: a co-residency violation
+// becomes a loud launch failure instead of a hang.
+__device__ __forceinline__ void w3_grid_barrier(int slot, unsigned long long timeout_ns) {
+  unsigned* cnt = &g_w3_count[slot];
+  unsigned* gen = &g_w3_gen[slot];
+  unsigned my;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(my) : "l"(gen) : "memory");
+  __threadfence();  // this CTA's partial stores before its arrival
+  if (atomicAdd(cnt, 1u) == gridDim.x - 1) {
+    atomicExch(cnt, 0u);
+    __threadfence();
+    asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(gen), "r"(my + 1u) : "memory");
+  } else {
+    const unsigned long long t0 = gtimer();
+    unsigned g;
+    for (;;) {
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(gen) : "memory");
+      if (g != my) break;
+      __nanosleep(64);
+      if (gtimer() - t0 > timeout_ns) __trap();
+    }
+  }
+}
 
 __device__ __forceinline__ void w3_tma4_mc(const CUtensorMap* m, uint64_t* bar, void* dst, int c0, int c1, int c2,
                                            int c3) {
@@ -1511,17 +1541,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   if (g.fold_slot >= 0) {
     // ===== in-kernel fold. Every CTA of the (persistent, co-resident) grid has
     // stored its slot region: grid barrier (release / acquire at GPU scope) =====
-    unsigned* arrive = &g_w3_arrive[g.fold_slot];
     __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(arrive, 1u);
-      unsigned seen;
-      do {
-        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(seen) : "l"(arrive) : "memory");
-        if (seen < gridDim.x) __nanosleep(64);
-      } while (seen < gridDim.x);
-    }
+    if (threadIdx.x == 0) w3_grid_barrier(g.fold_slot, 20000000000ull);
     __syncthreads();
     const Plan& P = g.P;
     // bias partial sums: 8 columns x 32 split groups per pass, fixed order
@@ -1612,12 +1633,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
         reinterpret_cast<float4*>(dst + ((size_t)f * P.C + cbk * 64) * 9)[q4] = v;
       }
       __syncthreads();
-    }
-    // the last CTA out resets the slot (every CTA has passed its wait by then)
-    if (threadIdx.x == 0 && atomicAdd(&g_w3_depart[g.fold_slot], 1u) == gridDim.x - 1) {
-      g_w3_arrive[g.fold_slot] = 0u;
-      g_w3_depart[g.fold_slot] = 0u;
-      __threadfence();
     }
   }
   if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) {
@@ -1713,7 +1728,7 @@ int wgrad3_pairs_per_split(const Plan& P) {
 
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail, int jsplit, float* const* dW, const float* bpart, int SB,
-               float* const* db) {
+               float* const* db, bool* folded) {
   if (dev_skip("wgrad")) return QD_OK;
   W3Plan pl = w3_plan(P);
   // splits < the plan's: a partitioned launch sharing the SMs with a concurrent kernel
@@ -1723,11 +1738,13 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
   g.part = part;
   g.fold_slot = -1;
   g.P = P;
+  if (folded) *folded = false;
   if (dW && dW[0]) {
     // the grid barrier needs every CTA resident at once: the grid never exceeds
-    // the co-resident clusters (w3_plan)
-    static unsigned slot = 0;
-    g.fold_slot = (int)(slot++ % 64);
+    // the co-resident clusters (w3_plan), and the launch is cooperative (the
+    // driver then guarantees co-residency even beside other kernels)
+    static std::atomic<unsigned> slot{0};
+    g.fold_slot = (int)(slot.fetch_add(1u) % 64u);
     g.dw0 = dW[0]; g.dw1 = dW[1]; g.dw2 = dW[2];
     g.bpart = bpart; g.SB = SB;
     g.db0 = db ? db[0] : nullptr; g.db1 = db ? db[1] : nullptr; g.db2 = db ? db[2] : nullptr;
@@ -1754,7 +1771,21 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr = (int)pl.smem;
   }
-  launch_pdl(wgrad3_kernel, dim3(2 * g.jtiles * g.ablocks * g.nsplit), dim3(256), pl.smem, st, X0, X1, Dm, Dm1, g);
+  const dim3 grid(2 * g.jtiles * g.ablocks * g.nsplit);
+  if (g.fold_slot >= 0) {
+    // in-kernel fold: cooperative launch (co-residency guaranteed by the driver);
+    // if the driver refuses it, the caller folds with separate kernels instead
+    const char* ce = getenv("QD_W3_COOP");
+    const bool coop = !(ce && atoi(ce) == 0);
+    if (cudaLaunchCoop(wgrad3_kernel, grid, dim3(256), pl.smem, st, coop, X0, X1, Dm, Dm1, g) == cudaSuccess) {
+      if (folded) *folded = true;
+      count_launch(st, "wgrad3");
+      return check_launch("wgrad3");
+    }
+    cudaGetLastError();
+    g.fold_slot = -1;
+  }
+  launch_pdl(wgrad3_kernel, grid, dim3(256), pl.smem, st, X0, X1, Dm, Dm1, g);
   count_launch(st, "wgrad3");
   return check_launch("wgrad3");
 }

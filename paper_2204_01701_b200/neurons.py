@@ -235,7 +235,7 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, wa
             f"cache for {cache.family}/{cache.kind} used with {spec.family}/{spec.kind} layer")
     validate_device_spec(spec)
     lib = _lib.load()
-    g = _as_device(dy.data if hasattr(dy, "data") and not isinstance(dy, torch.Tensor) else dy)
+    g = _as_device(dy.data if hasattr(dy, "data") and not isinstance(dy, (torch.Tensor, np.ndarray)) else dy)
     if tuple(g.shape) != tuple(cache.y_shape):
         raise IntegrityError(
             f"output gradient shape {tuple(g.shape)} does not match forward {tuple(cache.y_shape)}")
@@ -338,10 +338,143 @@ def init_params(spec, rng, device=None):
     return out
 
 
-def _symbolic_rule(spec, params, cache, g):
-    return symbolic_backward(spec, params, cache, g)
+# ---------------------------------------------------------------------------
+# tape / plugin-registry boundary (reference neurons.py:448-477, tensor.py:598-609)
+# ---------------------------------------------------------------------------
+SYMBOLIC = "symbolic"  # reference tensor.py:31 (tape mode of a closed-form node)
+
+_dev_ids = __import__("itertools").count(1 << 40)  # ids of device-tensor wrappers
 
 
-# family -> closed-form backward rule (reference registry tensor.py:598,
-# populated at import like neurons.py:462-463)
-SYMBOLIC_BACKWARD = {fam: _symbolic_rule for fam in DEVICE_FAMILIES}
+class DeviceTensor:
+    """Tape-facing wrapper of a device tensor for tapes whose inputs are torch
+    tensors: the attributes the reference Tape reads (``id``, ``shape``,
+    ``nbytes``, ``is_param``; tensor.py:43-90, :151-185) over ``data``."""
+
+    __slots__ = ("data", "id", "is_param")
+
+    def __init__(self, data, is_param=False):
+        self.data = data
+        self.id = next(_dev_ids)
+        self.is_param = is_param
+
+    @property
+    def shape(self):
+        return tuple(self.data.shape)
+
+    @property
+    def nbytes(self):
+        return self.data.numel() * self.data.element_size()
+
+
+def _host_array(t):
+    """device tensor -> C-contiguous fp64 ndarray (the reference's array type)."""
+    return np.ascontiguousarray(t.detach().to(torch.float64).cpu().numpy())
+
+
+def _wrap_like(x, t):
+    """Result tensor of the caller's kind: a reference ``Tensor`` (fp64 host
+    copy, via the class's own ``_wrap``) when x is one, else a DeviceTensor."""
+    if t is None:
+        return None
+    if isinstance(x, torch.Tensor) or not hasattr(type(x), "_wrap"):
+        return DeviceTensor(t)
+    return type(x)._wrap(_host_array(t))
+
+
+def record_symbolic(tape, spec, params, x, tag="", *, dtype=None):
+    """Run a layer forward on the GPU and record it on ``tape`` as ONE symbolic
+    node retaining ``cache_names(family)`` (reference neurons.py:466-477).
+
+    ``tape`` is any object with the reference ``Tape.record(op, arrays,
+    input_names, tag=, mode=, meta=)`` method (tensor.py:151); ``x`` a reference
+    ``Tensor`` (fp64, host) or a torch tensor. The node's arrays are the
+    caller's tensor kind (the reference tape accounts their bytes); the device
+    cache rides along in ``meta["b200_cache"]`` so the registered backward
+    (``_quad_node_backward``) runs from the device-resident x, a, b.
+    """
+    xin = x.data if (not isinstance(x, torch.Tensor) and hasattr(x, "data")) else x
+    y, cache = forward(spec, params, xin, dtype=dtype)
+    yt = _wrap_like(x, y)
+    xt = x if not isinstance(x, torch.Tensor) else DeviceTensor(x)
+    arrays = {"out": yt, "x": xt}
+    if cache.a is not None:
+        arrays["a"] = _wrap_like(x, cache.a)
+        arrays["b"] = _wrap_like(x, cache.b)
+    tape.record("quad", arrays, ("x",), tag=tag, mode=SYMBOLIC,
+                meta={"family": spec.family, "spec": spec, "params": params,
+                      "retain": cache_names(spec.family), "b200_cache": cache})
+    return yt
+
+
+def _node_cache(node, spec):
+    """The device LayerCache of a tape node: the one record_symbolic stored, or
+    (a node the reference recorded itself) one rebuilt from the node's arrays."""
+    cache = node.meta.get("b200_cache")
+    if cache is not None:
+        return cache
+    x = node.arrays["x"]
+    xa = _as_device(x.data if hasattr(x, "data") and not isinstance(x, torch.Tensor) else x)
+    _check_x(spec, xa)
+    cdt = _compute_dtype(xa, None)
+    xa = _layout(xa.detach().to(cdt), spec.kind)
+
+    def dev(name):
+        t = node.arrays.get(name)
+        if t is None:
+            return None
+        t = _as_device(t.data if hasattr(t, "data") and not isinstance(t, torch.Tensor) else t)
+        return _layout(t.detach().to(cdt), spec.kind)
+    return LayerCache(spec.family, spec.kind, xa, dev("a"), dev("b"), tuple(node.arrays["out"].shape),
+                      make_desc(spec, xa.shape, cdt))
+
+
+def _quad_node_backward(node, g):
+    """Registry contract ``fn(node, g) -> [(tensor_id, grad), ...]`` of the
+    reference (tensor.py:598-609; adapter neurons.py:448-459): the closed-form
+    backward of one symbolic quadratic node, computed on the GPU.
+
+    Gradients come back in the kind of ``g``: fp64 ndarrays when the tape is
+    the reference's (its sweep adds them with numpy, tensor.py:634-637), torch
+    tensors otherwise.
+    """
+    spec = node.meta["spec"]
+    params = node.meta["params"]
+    cache = _node_cache(node, spec)
+    host = not isinstance(g, torch.Tensor)
+    gin = g.data if (host and hasattr(g, "data") and not isinstance(g, np.ndarray)) else g
+    grads, dx = symbolic_backward(spec, params, cache, gin)
+    conv = _host_array if host else (lambda t: t)
+    out = [(node.arrays["x"].id, conv(dx))]
+    for role, grad in grads.items():
+        p = params[role]
+        out.append((p.id if hasattr(p, "id") else id(p), conv(grad)))
+    return out
+
+
+# family -> closed-form backward rule with the registry contract fn(node, g)
+# (reference tensor.py:598, populated at import like neurons.py:462-463)
+SYMBOLIC_BACKWARD = {fam: _quad_node_backward for fam in DEVICE_FAMILIES}
+
+
+def install(tensor_module, families=None):
+    """Route a reference tape's quadratic nodes to the device: register
+    ``_quad_node_backward`` in the reference's ``tensor.SYMBOLIC_BACKWARD``
+    (tensor.py:598) for ``families`` (default: every family both support).
+    Returns the previous entries so a caller can restore them."""
+    reg = tensor_module.SYMBOLIC_BACKWARD
+    fams = families or [f for f in reg if f in DEVICE_FAMILIES]
+    prev = {f: reg.get(f) for f in fams}
+    for f in fams:
+        reg[f] = _quad_node_backward
+    return prev
+
+
+def uninstall(tensor_module, prev):
+    """Restore the registry entries ``install`` returned."""
+    reg = tensor_module.SYMBOLIC_BACKWARD
+    for f, fn in prev.items():
+        if fn is None:
+            reg.pop(f, None)
+        else:
+            reg[f] = fn

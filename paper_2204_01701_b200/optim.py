@@ -86,5 +86,30 @@ class QuadSGD(torch.optim.Optimizer):
                 torch.autograd.graph.increment_version(w)
             neurons.register_pack(desc, ws, wpack)
         if self._rest is not None:
+            self._sync_rest()
             self._rest.step()
         return loss
+
+    def _sync_rest(self):
+        """The non-fused parameters follow this optimizer's hyper-parameters (an LR
+        schedule such as the reference's per-epoch cosine_lr, trainer.py:210,
+        edits ``self.param_groups``)."""
+        g = self.param_groups[0]
+        for rg in self._rest.param_groups:
+            for k in ("lr", "momentum", "weight_decay"):
+                rg[k] = g[k]
+
+    def state_dict(self):
+        sd = super().state_dict()
+        if self._rest is not None:
+            sd["rest"] = self._rest.state_dict()
+        return sd
+
+    def load_state_dict(self, state_dict):
+        state_dict = dict(state_dict)
+        rest = state_dict.pop("rest", None)
+        super().load_state_dict(state_dict)
+        if rest is not None and self._rest is not None:
+            self._rest.load_state_dict(rest)
+        # the packed layouts were written from the old weights: repack on the next step
+        self._packs.clear()

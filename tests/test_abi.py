@@ -47,8 +47,12 @@ def test_validate_status_codes():
     assert v(kind=1, r=0) == _lib.QD_ERR_CONFIG
     assert v(kind=0, r=3) == _lib.QD_ERR_CONFIG  # fc must be k=1 s=1 p=0
     assert v(H=1, W=1, r=5, pad=1) == _lib.QD_ERR_DIM  # kernel larger than padded input
+    msg = lib.qd_last_error().decode()
+    assert "kernel 5 larger than padded input" in msg and "pad 1" in msg, msg
     assert v(N=0) == _lib.QD_ERR_DIM
-    assert b"larger than padded input" in lib.qd_last_error() or True
+    assert "dimensions must be positive" in lib.qd_last_error().decode()
+    assert v(kind=2, F=32) == _lib.QD_ERR_CONFIG  # dwconv needs in == out
+    assert "in == out" in lib.qd_last_error().decode()
 
 
 def test_out_shape_and_sizes():
