@@ -727,6 +727,8 @@ def measure_net(args, name, world, rank, local, dev):
     broadcast_module(model)  # every replica starts from rank 0's weights and BN buffers
     # fused SGD + weight pack for the quadratic layers;
     # --torch-sgd for torch.optim.SGD everywhere (the forward then packs itself)
+    for p_ in model.parameters():  # activations are channels_last; parameters keep the standard layout
+        p_.data = p_.data.contiguous()
     opt = sgd(model.parameters(), lr=0.01) if args.torch_sgd else QuadSGD(model, lr=0.01)
     red = BucketedAllReduce(model.parameters(), bucket_mb=25.0)
     gen = torch.Generator(device=dev).manual_seed(rank)

@@ -39,6 +39,12 @@ class QuadSGD(torch.optim.Optimizer):
                 w = getattr(m, r)
                 if not w.is_contiguous():
                     w.data = w.data.contiguous()
+        # every other parameter too: the gradients the library and the DP buckets
+        # produce are in the standard layout, and a channels_last parameter would
+        # make autograd accumulate them strided (gradient layout contract)
+        for p in model.parameters():
+            if not p.is_contiguous():
+                p.data = p.data.contiguous()
         params = [p for p in model.parameters() if p.requires_grad]
         defaults = dict(lr=lr, momentum=momentum, weight_decay=weight_decay)
         super().__init__(params, defaults)

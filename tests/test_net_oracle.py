@@ -73,7 +73,7 @@ def _state(model, dtype):
 
 def _zero_through_bn(n_):
     # a bias added right before BN has an exactly zero gradient (BN removes the mean)
-    return n_.endswith(".layer.bc") or n_.endswith("down.layer.b")
+    return n_.endswith(".layer.bc") or n_.endswith("down.layer.b") or n_ == "features.0.bc"
 
 
 @pytest.mark.gpu
@@ -81,10 +81,8 @@ def _zero_through_bn(n_):
 def test_net_train_step_fp32_vs_fp64_composition(net, batch, hw):
     """The whole training step in fp32 on the device (every layer, BN, pool and
     the loss) against the fp64 composition: gradients of EVERY parameter and
-    the fused SGD update. Tolerance from the measured conditioning of the fp64
-    step itself (oracle weights perturbed by 6e-8 relative noise move VGG
-    gradients by <= 2e-6 and ResNet's (batch 2: BN over 98 values in the last
-    stage) by <= 2.2e-3, Frobenius-relative)."""
+    the fused SGD update, Frobenius-relative 1e-4 (the north-star fp32 bound;
+    measured <= 6.4e-6 on both nets)."""
     from paper_2204_01701_b200.optim import QuadSGD
     model, classes = _build(net, torch.float32)
     x, labels = _inputs(batch, hw, classes, torch.float32)
@@ -101,7 +99,7 @@ def test_net_train_step_fp32_vs_fp64_composition(net, batch, hw):
     r_logits, r_loss, r_grads = NO.train_step_grads(net, ref_in, x, labels)
     assert _rel_fro(logits, r_logits) <= 1e-4, _rel_fro(logits, r_logits)
     assert abs(float(loss) - r_loss) <= 1e-4 * abs(r_loss)
-    tol = {"qvgg16": 1e-3, "qresnet18": 5e-2}[net]
+    tol = 1e-4  # measured: <= 6.4e-6 on both nets
     errs = {}
     for n_, gd in grads.items():
         if _zero_through_bn(n_):
@@ -121,9 +119,9 @@ def test_net_train_step_bf16_nodes_vs_fp64(net, batch, hw):
     """The timed (bf16) training step, node by node: every fused quadratic-conv +
     BN (+ residual) + ReLU node of the net is re-run in fp64 from the node's
     OWN device input (and residual) and output gradient, and its output and
-    every parameter gradient compared (Frobenius-relative 5e-2, the fused-BN
-    tests' bound: a ReLU mask element whose bf16 pre-activation lands on the
-    other side of 0 moves a whole gradient value). End to end, bf16 is not
+    every parameter gradient compared at the bf16 bound 2e-2 (Frobenius-relative;
+    measured <= 5.3e-3), the ReLU mask taken from the device output (a
+    pre-activation within rounding of 0 may land on either side). End to end, bf16 is not
     comparable element-wise on these nets: rounding only the fp64 oracle's
     weights to bf16 already moves its gradients by up to 44 % (VGG, batch 8) /
     38 % (ResNet, batch 2) -- so the logits / loss are checked at 5e-2."""
@@ -165,10 +163,14 @@ def test_net_train_step_bf16_nodes_vs_fp64(net, batch, hw):
         xx = r["x"].to("cpu", torch.float64)
         y = NO.quad_conv(xx, P, "", sp.family, sp.stride, sp.pad)
         z = NO.batchnorm(y, gam, bet)
+        # the ReLU mask is the device's own (z > 0): a pre-activation within bf16
+        # rounding of 0 lands on either side, and a flipped mask element moves a
+        # whole gradient value (that is the conditioning, not kernel error)
+        mask = (r["z"] > 0).to("cpu", torch.float64)
         if r["res"] is not None:
-            z = torch.relu(z + r["res"].to("cpu", torch.float64))
+            z = (z + r["res"].to("cpu", torch.float64)) * mask
         elif mod.relu:
-            z = torch.relu(z)
+            z = z * mask
         z.backward(r["dz"].to("cpu", torch.float64))
         errs = {"z": _rel_fro(r["z"], z.detach()), "gamma": _rel_fro(mod.weight.grad, gam.grad),
                 "beta": _rel_fro(mod.bias.grad, bet.grad)}
@@ -183,7 +185,7 @@ def test_net_train_step_bf16_nodes_vs_fp64(net, batch, hw):
         worst.append((w[1], name, w[0]))
     worst.sort(reverse=True)
     print(net, "bf16 node worst", worst[:5])
-    assert worst[0][0] <= 5e-2, worst[:5]
+    assert worst[0][0] <= 2e-2, worst[:5]
 
 
 def param_shapes_of(spec):
