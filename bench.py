@@ -67,6 +67,7 @@ WORKLOADS = {
     "vgg_512x2": ("proposed", "conv", 256, 512, 512, 2, 2, 3, 1, 1, "bf16"),
 }
 METRIC = "quadratic_conv_fwd_bwd_tflops"
+TF32_PEAK = 720.9  # cuBLAS TF32 8192^3 burst on this pool's B200 (tools/tf32_peak.py, profiles/r2_tf32_peak.json)
 L2_NOTE = ("flushed between timed steps (untimed): 256 MiB write, then a 256 MiB read so the "
            "step starts from a cold, clean L2 (no dirty-line write-back billed to the step)")
 
@@ -517,6 +518,15 @@ def run_ours(args, wl, wl_name):
                 "peak_src": f"{pk['src']} HBM copy bandwidth",
                 "algorithmic": "per launch: the activation tensors the kernel must read and write once "
                                "(dw_fwd x -> y, a, b; prologue dy, a, b -> D; dw_wgrad x, D; dw_dgrad D -> dx)"}
+    elif dts != "bf16" and neurons.device_path(spec, x.shape, dt) == 3:
+        # fp32 as split bf16 operands: 3 bf16 MMA products per fp32 product, so the ceiling
+        # of this path is a third of the bf16 tensor peak (same unit: fp32-equivalent FLOPs)
+        roof["peak"] = pk["bf16"] / 3.0
+        roof["frac"] = ach / roof["peak"]
+        roof["peak_src"] = (f"{pk['src']} bf16 dense burst {pk['bf16']} / 3 (three bf16 products per fp32 "
+                            f"product); TF32 for comparison: {TF32_PEAK} (cuBLAS, profiles/r2_tf32_peak.json)")
+        roof["note"] = ("fp32 on the tcgen05 kernels: operands split into bf16 hi + lo, products hi*hi + hi*lo "
+                        "+ lo*hi accumulated in fp32 (error ~1e-5, tolerance 1e-4)")
     elif dts != "bf16":
         roof["note"] = "fp32 runs on the CUDA-core (FFMA) path; the bf16 tensor peak is the denominator"
 
@@ -596,7 +606,8 @@ def run_ours(args, wl, wl_name):
                            "exceeds L2)"},
            "gpu_launches": launches, "launches_per_step": launches / args.steps,
            "clocks": clocks, "nets": nets,
-           "path": "tcgen05" if neurons.device_path(spec, x.shape, dt) == 1 else "cuda-core"}
+           "path": {0: "cuda-core", 1: "tcgen05", 2: "depth-wise", 3: "tcgen05 fp32 (split bf16 x3)"}[
+               neurons.device_path(spec, x.shape, dt)]}
     print(json.dumps(out), flush=True)
     if world > 1:
         dist.destroy_process_group()

@@ -76,6 +76,7 @@ static size_t align_up(size_t v, size_t a = 256) { return (v + a - 1) / a * a; }
 static int device_path(const Plan& P, unsigned flags) {
   if (P.kind == QD_KIND_DWCONV) return 2;
   if (is_t1(P.family)) return 0;
+  if (x3_supported(P, flags)) return 3;
   return tc_supported(P, flags) ? 1 : 0;
 }
 
@@ -84,6 +85,27 @@ Workspace plan_workspace(const Plan& P, int path) {
   memset(&L, 0, sizeof(L));
   size_t es = P.dtype == QD_BF16 ? 2 : 4;
   if (is_t1(P.family)) return t1_workspace(P);
+  if (path == 3) {  // fp32 split operands (hi / lo bf16), raw accumulators, 3 wgrad products
+    L.sz_XS = (size_t)2 * P.Min * P.C * 2;
+    L.sz_D = (size_t)2 * P.Mout * P.Jd * 2;
+    L.sz_P = x3_raw_bytes(P);
+    L.wg_split = x3_wgrad_split(P);
+    L.sz_WG = (size_t)3 * L.wg_split * P.Jd * P.Kf * 4;
+    // one row-lane iteration per thread where the rows allow (256 / (F / 8) rows per block)
+    const long long lanes = 256 / (P.F / 8 > 0 ? P.F / 8 : 1);
+    long long bs = (P.Mout + lanes - 1) / (lanes > 0 ? lanes : 1);
+    if (bs > 2 * 148) bs = 2 * 148;
+    L.bs_split = (int)(bs < 1 ? 1 : bs);
+    L.sz_BS = (size_t)L.bs_split * P.Jd * 4;
+    size_t off = 0;
+    L.off_P = off; off = align_up(off + L.sz_P);
+    L.off_D = off; off = align_up(off + L.sz_D);
+    L.off_WG = off; off = align_up(off + L.sz_WG);
+    L.off_BS = off; off = align_up(off + L.sz_BS);
+    L.off_XS = off; off = align_up(off + L.sz_XS);
+    L.total = off;
+    return L;
+  }
   if (path == 2) {  // depth-wise: D, bias partials, wgrad partials
     if (caches_ab(P.family) || P.family == QD_FAM_T3) L.sz_D = (size_t)P.Mout * P.Jd * es;
     L.wg_split = dw_wgrad_split(P);
@@ -216,6 +238,7 @@ size_t qd_pack_bytes(const qd_desc* d) {
   Plan P = make_plan(*d);
   if (P.kind == QD_KIND_DWCONV) return dw_pack_bytes(P);
   if (is_t1(P.family)) return t1_pack_bytes(P);
+  if (device_path(P, d->flags) == 3) return (pack_fprop_elems(P) + pack_dgrad_elems(P)) * 3 * 2;  // [hi|lo|hi] bf16
   size_t es = P.dtype == QD_BF16 ? 2 : 4;
   return (pack_fprop_elems(P) + pack_dgrad_elems(P)) * es;
 }
@@ -243,6 +266,8 @@ int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack, void
     dw_pack(P, w, wpack, (cudaStream_t)stream);
   else if (is_t1(P.family))
     t1_pack(P, w, wpack, (cudaStream_t)stream);
+  else if (device_path(P, d->flags) == 3)
+    launch_x3_pack(P, w, wpack, (cudaStream_t)stream);
   else
     launch_pack(P, w, wpack, (cudaStream_t)stream);
   return check_launch("pack weights");
@@ -318,6 +343,8 @@ int qd_sgd_pack(const qd_desc* d, float* const w[3], float* const mom[3], const 
   Plan P = make_plan(*d);
   if (P.kind == QD_KIND_DWCONV || is_t1(P.family))
     return set_error(QD_ERR_UNSUPPORTED, "qd_sgd_pack: fc / conv kinds of the non-T1 families only");
+  if (device_path(P, d->flags) == 3)
+    return set_error(QD_ERR_UNSUPPORTED, "qd_sgd_pack: fp32 layers on the split tensor-core path pack themselves");
   if (!w || !mom || !grad || !wpack) return set_error(QD_ERR_ARG, "qd_sgd_pack: NULL argument");
   for (int i = 0; i < P.nroles; ++i)
     if (!w[i] || !mom[i] || !grad[i]) return set_error(QD_ERR_ARG, "qd_sgd_pack: role %d has a NULL pointer", i);
@@ -345,6 +372,7 @@ int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* 
   if (is_t1(P.family)) return t1_forward(P, x, wpack, y, (char*)workspace, L, s);
   if (path == 2) return dw_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
   if (path == 1) return tc_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
+  if (path == 3) return x3_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
   return simt_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
 }
 
@@ -376,6 +404,7 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* 
   if (is_t1(P.family)) return t1_backward(P, x, wpack, dy, dxp, w, (char*)workspace, L, s);
   if (path == 2) return dw_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
   if (path == 1) return tc_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
+  if (path == 3) return x3_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
   return simt_backward(P, x, wpack, a_cache, b_cache, dy, dxp, w, b, (char*)workspace, L, s);
 }
 

@@ -169,6 +169,22 @@ int dw_forward(const Plan& P, const void* x, const void* wpack, const float* con
 int dw_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
                 void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L, cudaStream_t st);
 
+// ---- fp32 on the tensor cores (path 3, qd_x3.cu + qd_tc.cu) -----------------
+bool x3_supported(const Plan& P, unsigned flags);
+size_t x3_raw_bytes(const Plan& P);
+int x3_wgrad_split(const Plan& P);
+void launch_x3_split(const float* x, bf16* hi, bf16* lo, long long n, cudaStream_t st);
+void launch_x3_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st);
+void launch_x3_prologue(const Plan& P, const float* dy, const float* a, const float* b, bf16* Dh, bf16* Dl,
+                        float* part, int split, cudaStream_t st);
+void launch_x3_fprop_finish(const float* raw, int S, long long M, int ld, int F, int nb, int epi, float* y, float* a,
+                            float* b, const float* const bias[3], cudaStream_t st);
+void launch_x3_sum(const float* raw, int S, long long n, float* out, cudaStream_t st);
+int x3_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
+               void* b, char* ws, const Workspace& L, cudaStream_t st);
+int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
+                void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L, cudaStream_t st);
+
 // ---- tcgen05 path ----------------------------------------------------------
 bool tc_supported(const Plan& P, unsigned flags);
 int tc_wgrad_split(const Plan& P);

@@ -158,7 +158,9 @@ __global__ void __launch_bounds__(256, 1)
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
-  const int KB = args.kb_half * (args.dual ? 2 : 1);
+  // dual = extra K segments: 1 = [x*x | x] (t2_linear; segment 1 from A1), 2 = the
+  // fp32 split [hi | hi | lo] (qd_x3.cu; segment 2 from A1)
+  const int KB = args.kb_half * (1 + args.dual);
   const int NWORK = args.cls ? 4 * args.cls_tiles : args.total_tiles * args.ksplit;
 
   if (warp == 0) {
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(256, 1)
             ax = ss * w0 + ex - args.pad_eff;
             ay = ss * h0 + ey - args.pad_eff;
           }
-          const CUtensorMap* ma = half ? &mapA1 : &mapA0;
+          const CUtensorMap* ma = (half > 0 && half == args.dual) ? &mapA1 : &mapA0;
           ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
 #pragma unroll
           for (int i = 0; i < NB; ++i)
@@ -1096,7 +1098,7 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
                     int b_rs_tile, int b_rs_blk, int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2,
                     int Cout, const float* const bias[3], const void* xres, cudaStream_t st,
                     float* skpart = nullptr, size_t skbytes = 0, int trav = 1, int cls = 0, int Hx = 0,
-                    int Wx = 0) {
+                    int Wx = 0, int force_part = 0, int* ksplit_out = nullptr) {
   Box bx = choose_box(OWg, OHg, N, 128, false);
   CUtensorMap A0, A1, B, O0, O1, O2;
   int rc;
@@ -1117,7 +1119,7 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
   g.b_rs_tile = b_rs_tile; g.b_rs_blk = b_rs_blk; g.out_c_tile = out_c_tile; g.Cout = Cout;
   g.bias0 = bias[0]; g.bias1 = bias[1]; g.bias2 = bias[2];
   g.xres = (const bf16*)xres;
-  const int KB = g.kb_half * (dual ? 2 : 1);
+  const int KB = g.kb_half * (1 + dual);
   g.ksplit = 1;
   g.kb_per = KB;
   g.Mpix = (long long)N * OHg * OWg;
@@ -1127,6 +1129,25 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
     g.kb_per = (KB + S - 1) / S;
     g.ksplit = (KB + g.kb_per - 1) / g.kb_per;
     g.part = skpart;
+  }
+  // raw fp32 accumulators whatever the split (fp32 x3 path): force_part 1 -> skpart,
+  // 2 -> o0 itself when unsplit (a plain epilogue's raw rows ARE the fp32 output)
+  if (force_part && !g.part) {
+    g.part = force_part == 2 ? (float*)o0 : skpart;
+    if (!g.part || (force_part == 1 && (size_t)g.Mpix * g.part_ld * 4 > skbytes))
+      return set_error(QD_ERR_UNSUPPORTED, "x3: raw accumulator buffer too small");
+  }
+  if (ksplit_out) *ksplit_out = g.ksplit;
+  g.sstride = trav;
+  if (g.part && force_part) {
+    // the split-K finish of the bf16 epilogues must not run: the caller folds
+#define QD_LCP(E, NBV) launch_conv<E, NBV>(A0, A1, B, O0, O1, O2, g, st)
+    if (epi == EPI_PROPOSED) return QD_LCP(EPI_PROPOSED, 3);
+    if (epi == EPI_T4) return QD_LCP(EPI_T4, 2);
+    if (nbk == 4) return QD_LCP(EPI_PLAIN, 4);
+    if (nbk == 2) return QD_LCP(EPI_PLAIN, 2);
+    return QD_LCP(EPI_PLAIN, 1);
+#undef QD_LCP
   }
   g.sstride = trav;
   if (cls) {
@@ -1465,6 +1486,159 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   }
   if (side) join_side(st, side);
   return check_launch("tc backward");
+}
+
+// ===========================================================================
+// fp32 layers on the tensor cores (device path 3; kernels in qd_x3.cu): the
+// v1 conv GEMM over the K-tripled split operands, raw fp32 accumulators, fp32
+// epilogue passes; three v1 wgrad products into one fixed-order fold
+// ===========================================================================
+bool x3_supported(const Plan& P, unsigned flags) {
+  static const bool off = getenv("QD_NO_X3") && atoi(getenv("QD_NO_X3"));
+  if (off || (flags & QD_FLAG_FORCE_SIMT) || P.dtype != QD_F32) return false;
+  if (P.family != QD_FAM_PROPOSED && P.family != QD_FAM_T4 && P.family != QD_FAM_FIRST_ORDER) return false;
+  if (P.kind != QD_KIND_FC && P.kind != QD_KIND_CONV) return false;
+  if (P.s != 1 || P.C % 64 || P.F % 64 || P.OH < 1 || P.OW < 1) return false;
+  return init_driver();
+}
+
+static int x3_fprop_split(const Plan& P) {
+  GemmCfg c = fprop_cfg(P);
+  Box bx = choose_box(P.OW, P.OH, P.N, 128, false);
+  const long long tiles = (long long)bx.tw * bx.th * bx.tn * c.tiles_nn;
+  const int KB = 3 * P.r * P.r * (P.C / 64);
+  int S = conv_ksplit(tiles, KB);
+  if (S > 1) {
+    const int per = (KB + S - 1) / S;
+    S = (KB + per - 1) / per;
+  }
+  return S;
+}
+static int x3_dgrad_split(const Plan& P) {
+  GemmCfg c = dgrad_cfg(P);
+  Box bx = choose_box(P.W, P.H, P.N, 128, false);
+  const long long tiles = (long long)bx.tw * bx.th * bx.tn * c.tiles_nn;
+  const int KB = 3 * P.r * P.r * (P.Jd / 64);
+  int S = conv_ksplit(tiles, KB);
+  if (S > 1) {
+    const int per = (KB + S - 1) / S;
+    S = (KB + per - 1) / per;
+  }
+  return S;
+}
+size_t x3_raw_bytes(const Plan& P) {
+  GemmCfg c = fprop_cfg(P);
+  const size_t f = (size_t)x3_fprop_split(P) * P.Mout * c.tiles_nn * c.nbk * 64 * 4;
+  const int sd = x3_dgrad_split(P);
+  const size_t d = sd > 1 ? (size_t)sd * P.Min * P.C * 4 : 0;
+  return f > d ? f : d;
+}
+int x3_wgrad_split(const Plan& P) {
+  if (!(P.flags & QD_FLAG_TC_V1)) {
+    const int s3 = wgrad3_split(P);  // r = 3 on CTA pairs (one product per launch, no in-kernel fold)
+    if (s3 > 0) return s3;
+  }
+  const long long ptiles = wgrad_ptiles(P);
+  const int mtiles = (P.Kf / 64 + 1) / 2;
+  const int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P, ptiles);
+  return (int)wgrad_split_for((long long)mtiles * ntiles, ptiles, tc_num_sms());
+}
+
+// one v1 wgrad product (x0 taps, D) into `splits` fp32 partial slots at `part`
+static int run_wgrad_v1(const Plan& P, const void* x0, const void* D, float* part, int splits, cudaStream_t st) {
+  Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
+  CUtensorMap X0, Dm;
+  int rc;
+  if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
+  if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
+  WgArgs g;
+  memset(&g, 0, sizeof(g));
+  int nblk = wgrad_ntile_blocks(P, wgrad_ptiles(P));
+  g.nkb = P.Kf / 64;
+  g.mtiles = (g.nkb + 1) / 2;
+  g.ntiles = (P.Jd / 64) / nblk;
+  g.splits = splits;
+  g.pb_w = pb.Wb; g.pb_h = pb.Hb; g.pb_n = pb.Nb;
+  g.pt_w = pb.tw; g.pt_h = pb.th; g.ptiles = pb.tw * pb.th * pb.tn;
+  g.r = P.r; g.pad = P.p; g.cblks = P.C / 64; g.kb_half = P.K0 / 64;
+  g.Jd = P.Jd; g.Kf = P.Kf;
+  g.sstride = P.s;
+  g.part = part;
+  if (nblk == 4) return launch_wgrad<4>(X0, X0, Dm, g, st);
+  if (nblk == 3) return launch_wgrad<3>(X0, X0, Dm, g, st);
+  if (nblk == 2) return launch_wgrad<2>(X0, X0, Dm, g, st);
+  return launch_wgrad<1>(X0, X0, Dm, g, st);
+}
+
+int x3_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
+               void* b, char* ws, const Workspace& L, cudaStream_t st) {
+  bf16* xh = (bf16*)(ws + L.off_XS);
+  bf16* xl = xh + (size_t)P.Min * P.C;
+  launch_x3_split((const float*)x, xh, xl, P.Min * P.C, st);
+  GemmCfg c = fprop_cfg(P);
+  const float* nob[3] = {nullptr, nullptr, nullptr};
+  int S = 1;
+  int rc = run_conv(c.epi, c.nbk, xh, xl, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 2, wpack, P.nb * P.F, 3 * P.Kf,
+                    c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nob, nullptr, st,
+                    (float*)(ws + L.off_P), L.sz_P, 1, 0, 0, 0, 1, &S);
+  if (rc) return rc;
+  const float* bz[3] = {bias[0], bias[1], bias[2]};
+  if (c.nbias == 0) bz[0] = bz[1] = bz[2] = nullptr;
+  launch_x3_fprop_finish((const float*)(ws + L.off_P), S, P.Mout, c.tiles_nn * c.nbk * 64, P.F, P.nb,
+                         c.epi == EPI_PROPOSED ? 0 : (c.epi == EPI_T4 ? 1 : 2), (float*)y, (float*)a, (float*)b, bz,
+                         st);
+  return check_launch("x3 forward");
+}
+
+int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
+                void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L, cudaStream_t st) {
+  const bf16* wd = (const bf16*)wpack + 3 * pack_fprop_elems(P);
+  bf16* Dh = (bf16*)(ws + L.off_D);
+  bf16* Dl = Dh + (size_t)P.Mout * P.Jd;
+  float* bpart = (float*)(ws + L.off_BS);
+  const bool dgiven = (P.flags & QD_FLAG_D_GIVEN) != 0;
+  if (dgiven) {
+    // `dy` is the fp32 operand D (qd_bn_backward_D formed it and the bias grads)
+    launch_x3_split((const float*)dy, Dh, Dl, P.Mout * P.Jd, st);
+  } else {
+    const bool need_part = P.nbias && db[0];
+    launch_x3_prologue(P, (const float*)dy, (const float*)a, (const float*)b, Dh, Dl, need_part ? bpart : nullptr,
+                       L.bs_split, st);
+  }
+  int rc;
+  if (dW[0]) {
+    bf16* xh = (bf16*)(ws + L.off_XS);
+    bf16* xl = xh + (size_t)P.Min * P.C;
+    launch_x3_split((const float*)x, xh, xl, P.Min * P.C, st);
+    float* part = (float*)(ws + L.off_WG);
+    const size_t slot = (size_t)P.Jd * P.Kf;
+    const int S = L.wg_split;
+    const bf16* xa[3] = {xh, xh, xl};
+    const bf16* da[3] = {Dh, Dl, Dh};
+    const bool w3 = !(P.flags & QD_FLAG_TC_V1) && wgrad3_split(P) == S;
+    for (int i = 0; i < 3; ++i) {
+      float* pi = part + (size_t)i * S * slot;
+      rc = w3 ? run_wgrad3(P, xa[i], nullptr, da[i], pi, S, st) : run_wgrad_v1(P, xa[i], da[i], pi, S, st);
+      if (rc) return rc;
+    }
+    WSplits uni;
+    memset(&uni, 0, sizeof(uni));
+    float* const nodb[3] = {nullptr, nullptr, nullptr};
+    launch_bwd_finish(P, part, 3 * S, uni, dW, bpart, L.bs_split, (dgiven || !P.nbias) ? nodb : db, st);
+  } else if (!dgiven && db[0] && P.nbias) {
+    launch_bias_finish(P, bpart, L.bs_split, db, st);
+  }
+  if (dx) {
+    GemmCfg c = dgrad_cfg(P);
+    const float* nob[3] = {nullptr, nullptr, nullptr};
+    int S = 1;
+    rc = run_conv(c.epi, c.nbk, Dh, Dl, P.Jd, P.OW, P.OH, P.N, P.W, P.H, P.r - 1 - P.p, P.r, 2, wd, P.Cd, 3 * P.Kd,
+                  c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, nullptr, st,
+                  (float*)(ws + L.off_P), L.sz_P, 1, 0, 0, 0, 2, &S);
+    if (rc) return rc;
+    if (S > 1) launch_x3_sum((const float*)(ws + L.off_P), S, P.Min * P.C, (float*)dx, st);
+  }
+  return check_launch("x3 backward");
 }
 
 }  // namespace qd

@@ -306,7 +306,9 @@ def backward_from_D(spec, params, cache, D, *, want_dx=True, want_dw=True):
 
 
 def device_path(spec, x_shape, dtype=torch.bfloat16, flags=0):
-    """0 = generic CUDA-core kernels, 1 = tcgen05/TMA kernels."""
+    """0 = generic CUDA-core kernels, 1 = tcgen05/TMA kernels (bf16), 2 = depth-wise
+    kernels, 3 = fp32 on the tcgen05 kernels through split bf16 operands
+    (hi*hi + hi*lo + lo*hi, qd_x3.cu)."""
     desc = make_desc(spec, x_shape, dtype, flags)
     p = _lib.load().qd_path(ctypes.byref(desc))
     if p < 0:

@@ -23,10 +23,19 @@ from . import _lib, neurons
 from .nn import _QuadBase
 
 
+def _pack_shape(spec):
+    """an input shape for the layer's descriptor: the packed layout does not
+    depend on the batch / image size"""
+    return (1, spec.in_dim) if spec.kind == "fc" else (1, spec.in_dim, spec.kernel, spec.kernel)
+
+
 class QuadSGD(torch.optim.Optimizer):
     def __init__(self, model, lr=0.1, momentum=0.9, weight_decay=5e-4):
+        # fp32 layers on the split tensor-core path (device path 3) pack their own
+        # [hi | lo | hi] layout in the forward: they take the plain SGD below
         self.quad = [m for m in model.modules() if isinstance(m, _QuadBase) and m.spec.kind != "dwconv"
-                     and not m.spec.family.startswith("t1")]
+                     and not m.spec.family.startswith("t1") and neurons.device_path(
+                         m.spec, _pack_shape(m.spec), m.compute_dtype) != 3]
         fused = set()
         for m in self.quad:
             for r in neurons.WEIGHT_ROLES[m.spec.family]:
@@ -70,10 +79,7 @@ class QuadSGD(torch.optim.Optimizer):
             for w, stt in zip(ws, states):
                 if "momentum_buffer" not in stt:
                     stt["momentum_buffer"] = torch.zeros_like(w, memory_format=torch.contiguous_format)
-            # the packed layout does not depend on the batch / image size
-            shape = (1, m.spec.in_dim) if m.spec.kind == "fc" else (1, m.spec.in_dim, m.spec.kernel,
-                                                                   m.spec.kernel)
-            desc = neurons.make_desc(m.spec, shape, m.compute_dtype)
+            desc = neurons.make_desc(m.spec, _pack_shape(m.spec), m.compute_dtype)
             key = id(m)
             wpack = self._packs.get(key)
             if wpack is None:

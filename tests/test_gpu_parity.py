@@ -238,6 +238,46 @@ def test_c1_fc_fp32():
     check_against_oracle("proposed", "fc", x, P, g, torch.float32)
 
 
+# fp32 on the tensor cores (path 3): split bf16 operands, 3 products per GEMM, 1e-4
+X3_CASES = [
+    # family, kind, n, c, f, h, w, k, s, p
+    ("proposed", "conv", 2, 64, 64, 8, 8, 3, 1, 1),
+    ("proposed", "conv", 3, 64, 128, 10, 12, 3, 1, 1),
+    ("proposed", "conv", 2, 128, 64, 6, 6, 1, 1, 0),
+    ("proposed", "conv", 2, 64, 64, 9, 7, 2, 1, 0),
+    ("t4", "conv", 2, 64, 128, 11, 9, 3, 1, 1),
+    ("first_order", "conv", 2, 64, 128, 8, 8, 3, 1, 1),
+    ("proposed", "conv", 2, 256, 256, 4, 4, 3, 1, 1),  # split K (small grid)
+    ("proposed", "fc", 200, 128, 192, 1, 1, 1, 1, 0),
+    ("t4", "fc", 130, 64, 64, 1, 1, 1, 1, 0),
+    ("first_order", "fc", 64, 256, 128, 1, 1, 1, 1, 0),
+]
+
+
+@pytest.mark.parametrize("case", X3_CASES, ids=[f"{c[0]}-{c[1]}-{c[3]}x{c[4]}-{c[5]}x{c[6]}-k{c[7]}"
+                                               for c in X3_CASES])
+def test_fp32_tensor_core_path_parity(case):
+    fam, kind, n, c, f, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, kind, n, c, f, h, w, k, s, p, seed=21, random_bias=True)
+    path = check_against_oracle(fam, kind, x, P, g, torch.float32, k, s, p)
+    assert path == 3, "expected the fp32 split tensor-core path for this shape"
+
+
+@pytest.mark.parametrize("case", X3_CASES[:3] + X3_CASES[7:8], ids=str)
+def test_fp32_tensor_core_matches_ffma_path(case):
+    """fp32 through the split tensor-core kernels and the exact FFMA kernels."""
+    from paper_2204_01701_b200 import _lib
+    fam, kind, n, c, f, h, w, k, s, p = case
+    x, P, g = Q.synthetic_layer(fam, kind, n, c, f, h, w, k, s, p, seed=23, random_bias=True)
+    r3 = run_device(fam, kind, x, P, g, torch.float32, k, s, p)
+    r0 = run_device(fam, kind, x, P, g, torch.float32, k, s, p, flags=_lib.FLAG_FORCE_SIMT)
+    assert r3[5] == 3 and r0[5] == 0
+    for i in (0, 4):
+        assert Q.rel_err(r3[i], r0[i]) <= 1e-4, i
+    for role in r3[3]:
+        assert Q.rel_err(r3[3][role], r0[3][role]) <= 1e-4, role
+
+
 def test_variants_fp32_conv():
     for fam in ("proposed", "t4", "t2", "t2_linear", "first_order"):
         x, P, g = Q.synthetic_layer(fam, "conv", 2, 5, 6, 7, 6, 3, 2, 1, seed=3, random_bias=True)
