@@ -1238,6 +1238,8 @@ void launch_bwd_prologue_vec(const Plan& P, const void* dy, const void* a, const
   count_launch(st, "prologue");
 }
 
+__device__ float g_zero_bias[3 * 2048];  // zero-initialised at module load, never written
+
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
                void* b, char* ws, const Workspace& L, cudaStream_t st) {
   const void* a0 = x;
@@ -1252,9 +1254,16 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
   GemmCfg c = fprop_cfg(P);
   if (c.nbias == 0) nb3[0] = nb3[1] = nb3[2] = nullptr;
   if (P.family == QD_FAM_T2AND4) {
-    // y = a b + c through the proposed epilogue with zero biases
+    // y = a b + c through the proposed epilogue with zero biases: a static zero
+    // vector (no per-forward memset) when the layer is narrow enough
+    static float* zdev = nullptr;
+    if (!zdev && cudaGetSymbolAddress((void**)&zdev, g_zero_bias) != cudaSuccess) {
+      cudaGetLastError();
+      zdev = nullptr;
+    }
     float* z = (float*)(ws + L.off_ZB);
-    cudaMemsetAsync(z, 0, (size_t)3 * P.F * 4, st);
+    if (zdev && 3 * P.F <= (int)(sizeof(g_zero_bias) / sizeof(float))) z = zdev;
+    else cudaMemsetAsync(z, 0, (size_t)3 * P.F * 4, st);
     nb3[0] = z; nb3[1] = z + P.F; nb3[2] = z + 2 * P.F;
   }
   if (P.family == QD_FAM_T3) {
