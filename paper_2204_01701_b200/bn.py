@@ -78,7 +78,7 @@ def bn_forward(y, gamma, beta, running_mean, running_var, momentum, eps, relu, t
     return z, sm, si
 
 
-def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu):
+def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu, params=None):
     """(D, dgamma, dbeta, {bias role: grad}) for the layer's backward from D."""
     lib = _lib.load()
     desc = neurons.make_desc(spec, cache.x.shape, cache.x.dtype)
@@ -95,9 +95,10 @@ def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu)
     db = {r: torch.empty(C, dtype=torch.float32, device=y.device) for r in broles}
     ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, nblk * C), dtype=torch.uint8, device=y.device)
     dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
+    ca, cb = (cache.a, cache.b) if params is None else neurons.restore_ab(spec, params, cache)
     st = lib.qd_bn_backward_D(ctypes.byref(desc), dzr.data_ptr(), y.data_ptr(),
-                              cache.a.data_ptr() if cache.a is not None else None,
-                              cache.b.data_ptr() if cache.b is not None else None, gamma.data_ptr(),
+                              ca.data_ptr() if ca is not None else None,
+                              cb.data_ptr() if cb is not None else None, gamma.data_ptr(),
                               beta.data_ptr(), save_mean.data_ptr(), save_invstd.data_ptr(), int(relu),
                               D.data_ptr(), dgamma.data_ptr(), dbeta.data_ptr(),
                               _lib.ptr3(*[db[r].data_ptr() for r in broles]), ws.data_ptr(),
@@ -111,7 +112,8 @@ class _QuadBNFunction(torch.autograd.Function):
     def forward(ctx, spec, dtype, relu, bn, x, gamma, beta, *tensors):
         roles = tuple(param_shapes(spec).keys())
         params = dict(zip(roles, tensors))
-        y, cache = neurons.forward(spec, params, x, dtype=dtype)
+        dtype, recompute = neurons.split_opts(dtype)
+        y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute)
         z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
         ctx.spec, ctx.roles, ctx.params, ctx.cache, ctx.relu = spec, roles, params, cache, relu
         ctx.x_dtype = x.dtype
@@ -121,7 +123,7 @@ class _QuadBNFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dz):
         y, gamma, beta, sm, si = ctx.saved_tensors
-        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, dz, y, gamma, beta, sm, si, ctx.relu)
+        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, dz, y, gamma, beta, sm, si, ctx.relu, ctx.params)
         want_dx = ctx.needs_input_grad[4]
         grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx)
         grads.update(db)
@@ -142,7 +144,8 @@ class _QuadBNAddReLUFunction(torch.autograd.Function):
     def forward(ctx, spec, dtype, bn, x, res, gamma, beta, *tensors):
         roles = tuple(param_shapes(spec).keys())
         params = dict(zip(roles, tensors))
-        y, cache = neurons.forward(spec, params, x, dtype=dtype)
+        dtype, recompute = neurons.split_opts(dtype)
+        y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute)
         if res.dtype != y.dtype or (y.dim() == 4 and not res.is_contiguous(memory_format=torch.channels_last)):
             res = res.to(y.dtype).contiguous(memory_format=torch.channels_last)
         z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, True, True,
@@ -156,7 +159,7 @@ class _QuadBNAddReLUFunction(torch.autograd.Function):
     def backward(ctx, dz):
         y, z, gamma, beta, sm, si = ctx.saved_tensors
         g = torch.ops.aten.threshold_backward(dz.to(z.dtype), z, 0)
-        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, g, y, gamma, beta, sm, si, False)
+        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, g, y, gamma, beta, sm, si, False, ctx.params)
         want_dx = ctx.needs_input_grad[3]
         grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx)
         grads.update(db)
@@ -266,7 +269,7 @@ class QuadConvBN(nn.Module):
                 and res.shape[1] == self.layer.spec.out_dim):
             spec = self.layer.spec
             tensors = [getattr(self.layer, r) for r in param_shapes(spec).keys()]
-            return _QuadBNAddReLUFunction.apply(spec, self.layer.compute_dtype, self.bn, x, res, self.weight,
+            return _QuadBNAddReLUFunction.apply(spec, self.layer.compute_opts(), self.bn, x, res, self.weight,
                                                 self.bias, *tensors)
         relu, self.relu = self.relu, False
         try:
@@ -282,9 +285,9 @@ class QuadConvBN(nn.Module):
         roles = tuple(param_shapes(spec).keys())
         tensors = [getattr(self.layer, r) for r in roles]
         if self.training and self.fused(x):
-            return _QuadBNFunction.apply(spec, self.layer.compute_dtype, self.relu, self.bn, x, self.weight,
+            return _QuadBNFunction.apply(spec, self.layer.compute_opts(), self.relu, self.bn, x, self.weight,
                                          self.bias, *tensors)
-        y = QuadFunction.apply(spec, self.layer.compute_dtype, x, *tensors)
+        y = QuadFunction.apply(spec, self.layer.compute_opts(), x, *tensors)
         if self.training and (y.dim() == 2 or y.is_contiguous(memory_format=torch.channels_last)):
             return _BNFunction.apply(y, self.weight, self.bias, self.bn, self.relu)
         z = _ref_batchnorm(y, self.weight, self.bias, self.bn.running_mean, self.bn.running_var, self.bn.momentum,

@@ -64,21 +64,188 @@ class ModelConfig:
     train: TrainSpec
 
 
+# ---------------------------------------------------------------------------
+# config text: a small line grammar. Each directive names its fields; a field
+# is (key, converter); the reader walks the lines once, the writer prints the
+# same fields in the same order, so the text round-trips byte for byte.
+# ---------------------------------------------------------------------------
+def _as_int(key):
+    def conv(v):
+        try:
+            return int(v)
+        except ValueError:
+            raise ValueError(f"{key} must be an integer, got {v!r}") from None
+    return conv
+
+
+def _one_of(key, choices, what):
+    def conv(v):
+        if v not in choices:
+            raise ValueError(what.format(v=v))
+        return v
+    return conv
+
+
+def _positive_float(v):
+    try:
+        f = float(v)
+    except ValueError:
+        raise ValueError(f"lr must be a float, got {v!r}") from None
+    if not (math.isfinite(f) and f > 0):
+        raise ValueError("lr must be positive and finite")
+    return f
+
+
+_LAYER_FIELDS = (("family", _one_of("family", tuple(f for f in FAMILIES if f != "t2_linear"),
+                                    "unknown family tag {v!r}")),
+                 ("in", _as_int("in")), ("out", _as_int("out")), ("k", _as_int("k")), ("s", _as_int("s")),
+                 ("p", _as_int("p")), ("bn", _one_of("bn", ("0", "1"), "bn must be 0 or 1, got {v!r}")),
+                 ("act", _one_of("act", ("none", "relu"), "unknown activation {v!r}")))
+_HEAD_FIELDS = (("in", _as_int("in")), ("classes", _as_int("classes")))
+_TRAIN_FIELDS = (("epochs", _as_int("epochs")), ("batch", _as_int("batch")), ("lr", _positive_float),
+                 ("seed", _as_int("seed")),
+                 ("dataset", _one_of("dataset", tuple(DATASET_SHAPES), f"dataset must be one of "
+                                                                      f"{sorted(DATASET_SHAPES)}")))
+
+
+def _read_fields(tokens, fields, lineno):
+    """key=value tokens -> {key: converted value}; every field exactly once."""
+    raw = {}
+    names = [k for k, _ in fields]
+    for tok in tokens:
+        key, eq, value = tok.partition("=")
+        if not eq:
+            raise ParseError(f"expected key=value, got {tok!r}", lineno)
+        if key not in names:
+            raise ParseError(f"unknown key {key!r}", lineno)
+        if key in raw:
+            raise ParseError(f"duplicate key {key!r}", lineno)
+        raw[key] = value
+    absent = [k for k in names if k not in raw]
+    if absent:
+        raise ParseError(f"missing keys {absent}", lineno)
+    out = {}
+    for key, conv in fields:
+        try:
+            out[key] = conv(raw[key])
+        except ValueError as e:
+            raise ParseError(str(e), lineno) from None
+    return out
+
+
+class _ConfigReader:
+    """Line-by-line state: at most one model / head / train line, layers before the head."""
+
+    def __init__(self):
+        self.name = self.head = self.train = None
+        self.layers = []
+
+    def _once(self, attr, lineno, word):
+        if getattr(self, attr) is not None:
+            raise ParseError(f"duplicate {word} line", lineno)
+
+    def model(self, args, lineno):
+        self._once("name", lineno, "model")
+        if len(args) != 1:
+            raise ParseError("model line must be 'model <name>'", lineno)
+        self.name = args[0]
+
+    def layer(self, args, lineno):
+        if not args or args[0] not in KINDS:
+            raise ParseError(f"layer kind must be one of {KINDS}", lineno)
+        if self.head is not None:
+            raise ParseError("layer line after head", lineno)
+        f = _read_fields(args[1:], _LAYER_FIELDS, lineno)
+        spec = QuadraticLayerSpec(kind=args[0], family=f["family"], in_dim=f["in"], out_dim=f["out"],
+                                  kernel=f["k"], stride=f["s"], pad=f["p"], batchnorm=f["bn"] == "1",
+                                  activation=f["act"])
+        try:
+            validate_spec(spec)
+        except ConfigError as e:
+            raise ParseError(str(e), lineno) from None
+        self.layers.append(spec)
+
+    def head_(self, args, lineno):
+        self._once("head", lineno, "head")
+        if not args or args[0] != "fc":
+            raise ParseError("head must be 'head fc in=<n> classes=<k>'", lineno)
+        f = _read_fields(args[1:], _HEAD_FIELDS, lineno)
+        self.head = HeadSpec(f["in"], f["classes"])
+
+    def train_(self, args, lineno):
+        self._once("train", lineno, "train")
+        f = _read_fields(args, _TRAIN_FIELDS, lineno)
+        self.train = TrainSpec(epochs=f["epochs"], batch=f["batch"], lr=f["lr"], seed=f["seed"],
+                               dataset=f["dataset"])
+
+    def finish(self):
+        for attr, word in (("name", "model"), ("head", "head"), ("train", "train")):
+            if getattr(self, attr) is None:
+                raise ParseError(f"missing {word} line")
+        return ModelConfig(name=self.name, layers=tuple(self.layers), head=self.head, train=self.train)
+
+
+def parse_config(text):
+    """Config text -> ModelConfig (format of the reference autobuild.py:1-12);
+    ParseError carries the 1-based line number."""
+    rd = _ConfigReader()
+    handlers = {"model": rd.model, "layer": rd.layer, "head": rd.head_, "train": rd.train_}
+    for lineno, raw in enumerate(text.splitlines(), start=1):
+        tokens = raw.split()
+        if not tokens or tokens[0].startswith("#"):
+            continue
+        fn = handlers.get(tokens[0])
+        if fn is None:
+            raise ParseError(f"unknown directive {tokens[0]!r}", lineno)
+        fn(tokens[1:], lineno)
+    cfg = rd.finish()
+    validate_config(cfg)
+    return cfg
+
+
+def serialize_config(cfg):
+    """Canonical text: parse(serialize(c)) == c and serialize(parse(t)) == t for
+    canonical t (the float lr printed with repr, as Python prints it)."""
+    t = cfg.train
+    rows = [("model", cfg.name)]
+    rows += [("layer", spec.describe()) for spec in cfg.layers]
+    rows.append(("head", f"fc in={cfg.head.in_dim} classes={cfg.head.classes}"))
+    rows.append(("train", " ".join(f"{k}={v}" for k, v in (("epochs", t.epochs), ("batch", t.batch),
+                                                          ("lr", repr(float(t.lr))), ("seed", t.seed),
+                                                          ("dataset", t.dataset)))))
+    return "".join(f"{word} {rest}\n" for word, rest in rows)
+
+
+def _walk_shapes(cfg, input_shape):
+    """Yield (index, spec, incoming (features, spatial or None)) along the chain,
+    then ("head", None, (features, None)); fc layers flatten what they receive."""
+    c, h, w = input_shape
+    feat, spatial = c, (h, w)
+    for i, spec in enumerate(cfg.layers):
+        if spec.kind == "fc" and spatial is not None:
+            feat, spatial = feat * spatial[0] * spatial[1], None
+        yield i, spec, (feat, spatial)
+        if spec.kind != "fc":
+            spatial = output_spatial(spec, spatial) if spatial is not None else None
+        feat = spec.out_dim
+    if spatial is not None:
+        feat = feat * spatial[0] * spatial[1]
+    yield "head", None, (feat, None)
+
+
 def validate_config(cfg, input_shape=None):
-    """Spec checks and the shape chain (autobuild.py:73-113)."""
-    if input_shape is None:
-        input_shape = DATASET_SHAPES.get(cfg.train.dataset)
+    """Every layer spec, then the shape chain (reference autobuild.py:73-113):
+    channel / feature counts must meet, no conv after a flatten, kernels fit."""
     for spec in cfg.layers:
         validate_spec(spec)
-    if input_shape is None:
+    shape = input_shape if input_shape is not None else DATASET_SHAPES.get(cfg.train.dataset)
+    if shape is None:
         return
-    c, h, w = input_shape
-    spatial, feat = (h, w), c
-    for i, spec in enumerate(cfg.layers):
-        if spec.kind == "fc":
-            if spatial is not None:
-                feat = feat * spatial[0] * spatial[1]
-                spatial = None
+    for i, spec, (feat, spatial) in _walk_shapes(cfg, shape):
+        if i == "head":
+            if cfg.head.in_dim != feat:
+                raise ConfigError(f"head expects in={cfg.head.in_dim} but receives {feat} features")
+        elif spec.kind == "fc":
             if spec.in_dim != feat:
                 raise ConfigError(f"layer {i} expects in={spec.in_dim} but receives {feat} "
                                   f"features from layer {i - 1}")
@@ -88,125 +255,8 @@ def validate_config(cfg, input_shape=None):
             if spec.in_dim != feat:
                 raise ConfigError(f"layer {i} expects in={spec.in_dim} channels but layer "
                                   f"{i - 1} provides {feat}")
-            if spec.kernel > spatial[0] + 2 * spec.pad or spec.kernel > spatial[1] + 2 * spec.pad:
+            if spec.kernel > min(spatial) + 2 * spec.pad:
                 raise ConfigError(f"layer {i}: kernel {spec.kernel} larger than padded input {spatial}")
-            spatial = output_spatial(spec, spatial)
-        feat = spec.out_dim
-    if spatial is not None:
-        feat = feat * spatial[0] * spatial[1]
-    if cfg.head.in_dim != feat:
-        raise ConfigError(f"head expects in={cfg.head.in_dim} but receives {feat} features")
-
-
-_LAYER_KEYS = ("family", "in", "out", "k", "s", "p", "bn", "act")
-_TRAIN_KEYS = ("epochs", "batch", "lr", "seed", "dataset")
-
-
-def _split_kv(parts, allowed, lineno):
-    kv = {}
-    for part in parts:
-        if "=" not in part:
-            raise ParseError(f"expected key=value, got {part!r}", lineno)
-        key, value = part.split("=", 1)
-        if key not in allowed:
-            raise ParseError(f"unknown key {key!r}", lineno)
-        if key in kv:
-            raise ParseError(f"duplicate key {key!r}", lineno)
-        kv[key] = value
-    missing = [k for k in allowed if k not in kv]
-    if missing:
-        raise ParseError(f"missing keys {missing}", lineno)
-    return kv
-
-
-def _int(value, key, lineno):
-    try:
-        return int(value)
-    except ValueError:
-        raise ParseError(f"{key} must be an integer, got {value!r}", lineno) from None
-
-
-def parse_config(text):
-    """Config text -> ModelConfig; ParseError carries the line number."""
-    name = head = train = None
-    layers = []
-    for lineno, raw in enumerate(text.splitlines(), start=1):
-        line = raw.strip()
-        if not line or line.startswith("#"):
-            continue
-        parts = line.split()
-        word = parts[0]
-        if word == "model":
-            if name is not None:
-                raise ParseError("duplicate model line", lineno)
-            if len(parts) != 2:
-                raise ParseError("model line must be 'model <name>'", lineno)
-            name = parts[1]
-        elif word == "layer":
-            if len(parts) < 2 or parts[1] not in KINDS:
-                raise ParseError(f"layer kind must be one of {KINDS}", lineno)
-            if head is not None:
-                raise ParseError("layer line after head", lineno)
-            kv = _split_kv(parts[2:], _LAYER_KEYS, lineno)
-            if kv["family"] not in FAMILIES or kv["family"] == "t2_linear":
-                raise ParseError(f"unknown family tag {kv['family']!r}", lineno)
-            if kv["act"] not in ("none", "relu"):
-                raise ParseError(f"unknown activation {kv['act']!r}", lineno)
-            if kv["bn"] not in ("0", "1"):
-                raise ParseError(f"bn must be 0 or 1, got {kv['bn']!r}", lineno)
-            spec = QuadraticLayerSpec(kind=parts[1], family=kv["family"], in_dim=_int(kv["in"], "in", lineno),
-                                      out_dim=_int(kv["out"], "out", lineno), kernel=_int(kv["k"], "k", lineno),
-                                      stride=_int(kv["s"], "s", lineno), pad=_int(kv["p"], "p", lineno),
-                                      batchnorm=kv["bn"] == "1", activation=kv["act"])
-            try:
-                validate_spec(spec)
-            except ConfigError as e:
-                raise ParseError(str(e), lineno) from None
-            layers.append(spec)
-        elif word == "head":
-            if head is not None:
-                raise ParseError("duplicate head line", lineno)
-            if len(parts) < 2 or parts[1] != "fc":
-                raise ParseError("head must be 'head fc in=<n> classes=<k>'", lineno)
-            kv = _split_kv(parts[2:], ("in", "classes"), lineno)
-            head = HeadSpec(_int(kv["in"], "in", lineno), _int(kv["classes"], "classes", lineno))
-        elif word == "train":
-            if train is not None:
-                raise ParseError("duplicate train line", lineno)
-            kv = _split_kv(parts[1:], _TRAIN_KEYS, lineno)
-            if kv["dataset"] not in DATASET_SHAPES:
-                raise ParseError(f"dataset must be one of {sorted(DATASET_SHAPES)}", lineno)
-            try:
-                lr = float(kv["lr"])
-            except ValueError:
-                raise ParseError(f"lr must be a float, got {kv['lr']!r}", lineno) from None
-            if not math.isfinite(lr) or lr <= 0:
-                raise ParseError("lr must be positive and finite", lineno)
-            train = TrainSpec(epochs=_int(kv["epochs"], "epochs", lineno), batch=_int(kv["batch"], "batch", lineno),
-                              lr=lr, seed=_int(kv["seed"], "seed", lineno), dataset=kv["dataset"])
-        else:
-            raise ParseError(f"unknown directive {word!r}", lineno)
-    if name is None:
-        raise ParseError("missing model line")
-    if head is None:
-        raise ParseError("missing head line")
-    if train is None:
-        raise ParseError("missing train line")
-    cfg = ModelConfig(name=name, layers=tuple(layers), head=head, train=train)
-    validate_config(cfg)
-    return cfg
-
-
-def serialize_config(cfg):
-    """Canonical text (byte-stable; parse(serialize(c)) == c)."""
-    lines = [f"model {cfg.name}"]
-    for spec in cfg.layers:
-        lines.append("layer " + spec.describe())
-    lines.append(f"head fc in={cfg.head.in_dim} classes={cfg.head.classes}")
-    t = cfg.train
-    lines.append(f"train epochs={t.epochs} batch={t.batch} lr={repr(float(t.lr))} seed={t.seed} "
-                 f"dataset={t.dataset}")
-    return "\n".join(lines) + "\n"
 
 
 def _head_spec(head):
@@ -303,50 +353,89 @@ class QuadraModel(nn.Module):
             t.copy_(a.to(t.dtype))
 
 
-def save_checkpoint(model, path):
-    """<path> (blob) + <path>.json (manifest), model.py:236-263. Returns the manifest."""
-    entries = []
-    blob = bytearray()
-    records = [(tag, role, t) for tag, role, t in model.param_items()]
+# ---------------------------------------------------------------------------
+# checkpoints: quadra-checkpoint-v1 (reference model.py:236-300). The blob is
+# a sequence of records, each a little-endian u64 byte count followed by that
+# many bytes of little-endian float64 values; <path>.json holds the config
+# text, one (layer, role, shape, offset, length) row per record (offset = the
+# first value byte) and the blob's SHA-256 and size.
+# ---------------------------------------------------------------------------
+CKPT_FORMAT = "quadra-checkpoint-v1"
+_U64 = struct.Struct("<Q")
+
+
+class _BlobWriter:
+    def __init__(self):
+        self.buf = bytearray()
+        self.rows = []
+
+    def add(self, layer, role, values):
+        data = np.ascontiguousarray(values, dtype="<f8")
+        payload = data.tobytes()
+        self.buf += _U64.pack(len(payload))
+        self.rows.append({"layer": layer, "role": role, "shape": list(data.shape), "offset": len(self.buf),
+                          "length": len(payload)})
+        self.buf += payload
+
+    def manifest(self, config_text):
+        blob = bytes(self.buf)
+        return blob, {"format": CKPT_FORMAT, "config": config_text, "tensors": self.rows,
+                      "blob_sha256": hashlib.sha256(blob).hexdigest(), "blob_bytes": len(blob)}
+
+
+class _BlobReader:
+    def __init__(self, path):
+        try:
+            with open(str(path) + ".json", "r", encoding="utf-8") as fh:
+                self.manifest = json.load(fh)
+            with open(path, "rb") as fh:
+                self.blob = fh.read()
+        except OSError as e:
+            raise IntegrityError(f"cannot read checkpoint {path}: {e}") from e
+        m = self.manifest
+        if m.get("format") != CKPT_FORMAT:
+            raise IntegrityError(f"unknown checkpoint format in {path}.json")
+        if len(self.blob) != m["blob_bytes"] or hashlib.sha256(self.blob).hexdigest() != m["blob_sha256"]:
+            raise IntegrityError(f"checkpoint blob {path} does not match its manifest")
+
+    def records(self):
+        for row in self.manifest["tensors"]:
+            off, n = row["offset"], row["length"]
+            (prefix,) = _U64.unpack_from(self.blob, off - _U64.size)
+            if prefix != n:
+                raise IntegrityError(f"length prefix {prefix} != manifest length {n} at offset {off}")
+            yield row["layer"], row["role"], np.frombuffer(self.blob, dtype="<f8", count=n // 8,
+                                                           offset=off).reshape(row["shape"])
+
+
+def _checkpoint_records(model):
+    """(tag, role, tensor) in the reference's order: the parameter walk, then the
+    BN running statistics layer by layer."""
+    recs = list(model.param_items())
     for layer in model.layers:
         if isinstance(layer.core, QuadConvBN):
-            records.append((layer.tag, "running_mean", layer.core.bn.running_mean))
-            records.append((layer.tag, "running_var", layer.core.bn.running_var))
-    for tag, role, t in records:
-        raw = np.ascontiguousarray(t.detach().cpu().double().numpy(), dtype="<f8").tobytes()
-        entries.append({"layer": tag, "role": role, "shape": list(t.shape), "offset": len(blob) + 8,
-                        "length": len(raw)})
-        blob.extend(struct.pack("<Q", len(raw)))
-        blob.extend(raw)
-    manifest = {"format": "quadra-checkpoint-v1", "config": serialize_config(model.cfg), "tensors": entries,
-                "blob_sha256": hashlib.sha256(bytes(blob)).hexdigest(), "blob_bytes": len(blob)}
-    with open(path, "wb") as f:
-        f.write(bytes(blob))
-    with open(str(path) + ".json", "w", encoding="utf-8") as f:
-        json.dump(manifest, f, indent=1)
+            recs += [(layer.tag, "running_mean", layer.core.bn.running_mean),
+                     (layer.tag, "running_var", layer.core.bn.running_var)]
+    return recs
+
+
+def save_checkpoint(model, path):
+    """Write <path> (blob) and <path>.json (manifest); returns the manifest."""
+    w = _BlobWriter()
+    for tag, role, t in _checkpoint_records(model):
+        w.add(tag, role, t.detach().cpu().double().numpy())
+    blob, manifest = w.manifest(serialize_config(model.cfg))
+    with open(path, "wb") as fh:
+        fh.write(blob)
+    with open(str(path) + ".json", "w", encoding="utf-8") as fh:
+        json.dump(manifest, fh, indent=1)
     return manifest
 
 
 def load_checkpoint(path, compute_dtype=torch.float32, device=None):
-    """Rebuild a QuadraModel from a checkpoint (model.py:266-300), verifying the manifest."""
-    try:
-        with open(str(path) + ".json", "r", encoding="utf-8") as f:
-            manifest = json.load(f)
-        with open(path, "rb") as f:
-            blob = f.read()
-    except OSError as e:
-        raise IntegrityError(f"cannot read checkpoint {path}: {e}") from e
-    if manifest.get("format") != "quadra-checkpoint-v1":
-        raise IntegrityError(f"unknown checkpoint format in {path}.json")
-    if len(blob) != manifest["blob_bytes"] or hashlib.sha256(blob).hexdigest() != manifest["blob_sha256"]:
-        raise IntegrityError(f"checkpoint blob {path} does not match its manifest")
-    cfg = parse_config(manifest["config"])
-    model = QuadraModel(cfg, compute_dtype=compute_dtype, device=device)
-    for entry in manifest["tensors"]:
-        off, length = entry["offset"], entry["length"]
-        (declared,) = struct.unpack("<Q", blob[off - 8:off])
-        if declared != length:
-            raise IntegrityError(f"length prefix {declared} != manifest length {length} at offset {off}")
-        arr = np.frombuffer(blob[off:off + length], dtype="<f8").reshape(entry["shape"])
-        model.set_param(entry["layer"], entry["role"], arr)
+    """A QuadraModel rebuilt from a verified checkpoint (digest, size, prefixes)."""
+    rd = _BlobReader(path)
+    model = QuadraModel(parse_config(rd.manifest["config"]), compute_dtype=compute_dtype, device=device)
+    for tag, role, values in rd.records():
+        model.set_param(tag, role, values)
     return model

@@ -63,6 +63,9 @@ class LayerCache:
     desc: object = field(default=None, repr=False)
     wpack: torch.Tensor | None = field(default=None, repr=False)
     pack_key: tuple = field(default=(), repr=False)
+    # recompute mode: a, b are not retained; the backward
+    # rebuilds them from x with the forward kernels
+    recompute: bool = field(default=False, repr=False)
 
 
 def _device():
@@ -188,8 +191,18 @@ def _workspace(desc, device):
     return torch.empty(max(n, 1), dtype=torch.uint8, device=device)
 
 
-def forward(spec, params, x, *, dtype=None, flags=0):
-    """Evaluate one layer on the GPU; returns (y, LayerCache). neurons.py:235-276."""
+def split_opts(dtype):
+    """A module's compute option: a dtype, or (dtype, recompute_ab)."""
+    if isinstance(dtype, tuple):
+        return dtype[0], bool(dtype[1])
+    return dtype, False
+
+
+def forward(spec, params, x, *, dtype=None, flags=0, recompute=False):
+    """Evaluate one layer on the GPU; returns (y, LayerCache). neurons.py:235-276.
+
+    recompute=True: the cache keeps x only (the a, b buffers the kernels write are
+    not retained); the backward rebuilds a, b with one more forward GEMM."""
     validate_device_spec(spec)
     lib = _lib.load()
     x = _as_device(x)
@@ -219,7 +232,20 @@ def forward(spec, params, x, *, dtype=None, flags=0):
                         b.data_ptr() if b is not None else None, ws.data_ptr(),
                         torch.cuda.current_stream().cuda_stream)
     _lib.raise_for(st, "qd_forward")
+    if recompute and a is not None:
+        return y, LayerCache(spec.family, spec.kind, x, None, None, tuple(y.shape), desc, wpack, key, True)
     return y, LayerCache(spec.family, spec.kind, x, a, b, tuple(y.shape), desc, wpack, key)
+
+
+def restore_ab(spec, params, cache):
+    """Recompute mode: a, b of the cached x through the forward kernels (the
+    fused GEMM also recomputes Wc x: +1/3 of the forward GEMM work). Returns
+    (a, b) without storing them in the cache, so they die with the backward."""
+    if not cache.recompute or cache.a is not None:
+        return cache.a, cache.b
+    _, c2 = forward(spec, params, cache.x, dtype=cache.x.dtype,
+                    flags=cache.desc.flags if cache.desc is not None else 0)
+    return c2.a, c2.b
 
 
 def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, want_db=True):
@@ -262,9 +288,10 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, wa
              for role in GRAD_ORDER[spec.family] if want_db or role not in BIAS_ROLES.get(spec.family, ())}
     dx = torch.empty_like(x) if want_dx else None  # preserves channels_last
     ws = _workspace(desc, dev)
+    ca, cb = restore_ab(spec, params, cache)
     st = lib.qd_backward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
-                         cache.a.data_ptr() if cache.a is not None else None,
-                         cache.b.data_ptr() if cache.b is not None else None,
+                         ca.data_ptr() if ca is not None else None,
+                         cb.data_ptr() if cb is not None else None,
                          g.data_ptr(), dx.data_ptr() if dx is not None else None,
                          _lib.ptr3(*[grads[r].data_ptr() for r in roles]),
                          _lib.ptr3(*[grads[r].data_ptr() for r in broles]),

@@ -27,7 +27,8 @@ class QuadFunction(torch.autograd.Function):
     def forward(ctx, spec, dtype, x, *tensors):
         roles = tuple(param_shapes(spec).keys())
         params = dict(zip(roles, tensors))
-        y, cache = neurons.forward(spec, params, x, dtype=dtype)
+        dtype, recompute = neurons.split_opts(dtype)
+        y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute)
         ctx.spec, ctx.roles, ctx.params, ctx.cache = spec, roles, params, cache
         ctx.x_dtype = x.dtype
         return y
@@ -75,11 +76,13 @@ def _reset(module, spec, generator=None, init="reference"):
 
 class _QuadBase(nn.Module):
     def __init__(self, spec, compute_dtype=torch.bfloat16, init="reference", device=None,
-                 generator=None):
+                 generator=None, recompute_ab=False):
         super().__init__()
         validate_device_spec(spec)
         self.spec = spec
         self.compute_dtype = compute_dtype
+        # retain only x between forward and backward; a, b are rebuilt in the backward
+        self.recompute_ab = recompute_ab
         for role, shape in param_shapes(spec).items():
             self.register_parameter(role, nn.Parameter(
                 torch.empty(shape, dtype=torch.float32, device=device)))
@@ -88,9 +91,13 @@ class _QuadBase(nn.Module):
     def params(self):
         return {role: getattr(self, role) for role in param_shapes(self.spec)}
 
+    def compute_opts(self):
+        """the dtype argument of the autograd functions: (dtype, recompute) when recomputing"""
+        return (self.compute_dtype, True) if self.recompute_ab else self.compute_dtype
+
     def forward(self, x):
         roles = tuple(param_shapes(self.spec).keys())
-        return QuadFunction.apply(self.spec, self.compute_dtype, x,
+        return QuadFunction.apply(self.spec, self.compute_opts(), x,
                                   *[getattr(self, r) for r in roles])
 
     def extra_repr(self):
