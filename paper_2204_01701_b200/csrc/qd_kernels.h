@@ -206,8 +206,7 @@ int wgrad3_pairs_per_split(const Plan& P);
 int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0, float* const* dW = nullptr,
-               const float* bpart = nullptr, int SB = 0, float* const* db = nullptr, bool* folded = nullptr,
-               const void* tf_a = nullptr, const void* tf_b = nullptr);
+               const float* bpart = nullptr, int SB = 0, float* const* db = nullptr, bool* folded = nullptr);
 // v2 stride-1 conv on CTA pairs (qd_tc2.cu); QD_ERR_UNSUPPORTED if the shape does not fit
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,

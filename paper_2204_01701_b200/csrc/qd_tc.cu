@@ -1343,58 +1343,6 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   }
   const int dsplit = d2 ? 2 * P.F / 64 : 0;
   bool wg_pdl = false;  // a PDL-launched v2/v3 wgrad immediately precedes the dgrad on `st`
-  // proposed, F = 64, SM partition (C2, the 64-channel ResNet / VGG layers): the
-  // wgrad forms g b and g a itself in shared memory from the cached a, b and dy
-  // (wgrad3 tf mode), so on its SM share it starts right after the forward,
-  // concurrently with the backward prologue -- which then only feeds the dgrad
-  // (D = [g b | g a]) and the bias sums -- and with the dgrad behind it.
-  // Opt-in (QD_W3_TF=1): measured slower on C2 (765 vs 784 TFLOP/s at the best
-  // partition of each) -- the transform warps' loads are not hidden
-  // behind a 2-stage ring, and the prologue slows under the concurrent wgrad.
-  if (d2 && dx && w3 && P.F == 64 && P.kind == QD_KIND_CONV && !P.sq && !getenv("QD_NO_PART") &&
-      getenv("QD_W3_TF") && atoi(getenv("QD_W3_TF")) == 1 && wgrad3_pairs_per_split(P) == 1) {
-    const int total = L.wg_split;
-    int part = getenv("QD_PART") ? atoi(getenv("QD_PART")) : (total * 46 + 50) / 100;
-    const int dg_pairs = total - part;
-    bool al16 = true;
-    for (int i = 0; i < 3; ++i) al16 = al16 && ((uintptr_t)dW[i] % 16 == 0);
-    cudaStream_t sd = (part >= 1 && part < total && dg_pairs >= total / 4 && al16) ? fork_side(st) : nullptr;
-    if (sd) {
-      float* const nodb[3] = {nullptr, nullptr, nullptr};
-      bool folded = false;
-      // bias sums: formed by the wgrad's transform warps, folded with its slots
-      int rc = run_wgrad3(P, x, nullptr, dy, (float*)(ws + L.off_WG), part, sd, nullptr, 0, dW, bpart, 0, db,
-                          &folded, a, b);
-      if (rc) return rc;
-      if (!folded) {
-        WSplits wsp;
-        memset(&wsp, 0, sizeof(wsp));
-        wsp.pp = (P.r * P.r + 1) / 2;
-        wsp.ng = 1;
-        wsp.s[0] = part;
-        launch_bwd_finish(P, (float*)(ws + L.off_WG), part, wsp, dW, bpart, part, db, sd);
-      }
-      (void)nodb;
-      // the prologue now only writes the dgrad's operand D = [g b | g a]
-      bf16* Dw = (bf16*)(ws + L.off_D);
-      const long long rows_per = (P.Mout + L.bs_split - 1) / L.bs_split;
-      if (!dev_skip("prologue"))
-        launch_pdl(bwd_prologue_vec_kernel, dim3(L.bs_split), dim3(256), 0, st, P0, (const bf16*)dy, (const bf16*)a,
-                   (const bf16*)b, Dw, (float*)nullptr, rows_per, 0, P.OH, P.OW, 2 * P.F);
-      count_launch(st, "prologue");
-      GemmCfg c = dgrad_cfg(P);
-      const float* nob[3] = {nullptr, nullptr, nullptr};
-      set_conv2_cap(dg_pairs);
-      rc = dev_skip("dgrad") ? QD_OK
-                             : run_conv2(c.epi, c.nbk, Dw, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, P.r - 1 - P.p,
-                                         P.r, 0, wd, P.Cd, P.Kd, c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx,
-                                         nullptr, nullptr, P.C, nob, nullptr, st, 1, dy, dsplit, 1);
-      set_conv2_cap(0);
-      if (rc) return rc;
-      join_side(st, sd);
-      return check_launch("tc backward (wgrad products in smem)");
-    }
-  }
   if (dgiven) {
     D = (const bf16*)dy;
   } else if (P.family == QD_FAM_T3) {

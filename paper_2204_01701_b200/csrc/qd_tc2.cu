@@ -1020,8 +1020,7 @@ __global__ void __launch_bounds__(256, 1)
   uint64_t* full = (uint64_t*)(sm + g.stages * stage_bytes);
   uint64_t* empty = full + g.stages;
   uint64_t* done = empty + g.stages;
-  uint64_t* tdone = done + 1;  // tf: products formed (6 transform warps)
-  uint32_t* tslot = (uint32_t*)(tdone + g.stages);
+  uint32_t* tslot = (uint32_t*)(done + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   int b = blockIdx.x;
   const int jt = b % g.jtiles;
@@ -1267,14 +1266,6 @@ struct W3Args {
   uint32_t d_tx, x_tx, d_bytes, x_bytes;
   int stages;
   int jsplit;
-  // tf = 1: the three D boxes are loaded as b, a (the forward's cache) and g (dy)
-  // and warps 2-7 form g b, g a in place in shared memory before the MMAs --
-  // the wgrad then does not wait for the backward prologue (proposed, F = 64)
-  int tf;
-  const void* tf_a;
-  const void* tf_b;
-  const void* tf_g;
-  float* tf_bias;  // tf: per-pair bias sums [pairs][3F] (folded with the slots after the grid barrier)
   float* part;
   unsigned long long* trace;  // QD_TRACE (dev only)
   // in-kernel fold (fold_bar != null): after a grid barrier each CTA sums whole
@@ -1346,7 +1337,7 @@ __device__ __forceinline__ void w3_commit_mc(uint64_t* bar) {
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     wgrad3_kernel(const __grid_constant__ CUtensorMap mX0, const __grid_constant__ CUtensorMap mX1,
                   const __grid_constant__ CUtensorMap mD, const __grid_constant__ CUtensorMap mD1,
-                  const __grid_constant__ CUtensorMap mD2, const W3Args g) {
+                  const W3Args g) {
   if (g.trace && threadIdx.x == 0 && blockIdx.x < 512) {
     g.trace[3072 + 2 * blockIdx.x] = gtimer();
     g.trace[2048 + 2 * blockIdx.x] = clock64();
@@ -1357,8 +1348,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
   uint64_t* full = (uint64_t*)(sm + g.stages * stage_bytes);
   uint64_t* empty = full + g.stages;
   uint64_t* done = empty + g.stages;
-  uint64_t* tdone = done + 1;  // tf: products formed (6 transform warps)
-  uint32_t* tslot = (uint32_t*)(tdone + g.stages);
+  uint32_t* tslot = (uint32_t*)(done + 1);
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = c2::cluster_rank();
   int b = blockIdx.x >> 1;
@@ -1378,12 +1368,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     ptx::prefetch_tmap(&mX0);
     ptx::prefetch_tmap(&mX1);
     ptx::prefetch_tmap(&mD);
-    if (g.jsplit || g.tf) ptx::prefetch_tmap(&mD1);
-    if (g.tf) ptx::prefetch_tmap(&mD2);
+    if (g.jsplit) ptx::prefetch_tmap(&mD1);
     for (int i = 0; i < g.stages; ++i) {
       ptx::mbar_init(&full[i], 1);
       ptx::mbar_init(&empty[i], 2);
-      ptx::mbar_init(&tdone[i], 6);
     }
     ptx::mbar_init(done, 1);
     ptx::fence_barrier_init();
@@ -1429,11 +1417,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       if (leader) {
         C2_TRACE(0, qb - q_beg, 1);
         uint8_t* s = sm + st * stage_bytes;
-        // tf: only the x halo comes through TMA (CTA0 issues it for the pair); the
-        // D boxes are written by the transform warps
-        ptx::mbar_arrive_expect_tx(&full[st], (g.tf ? 0 : g.ntb * g.d_tx) + g.x_tx);
-        const int i0 = g.tf ? (rank == 0 ? g.ntb : g.ntb + 1) : (rank == 0 ? 0 : nsh);
-        const int i1 = g.tf ? g.ntb + 1 : (rank == 0 ? nsh : g.ntb + 1);
+        ptx::mbar_arrive_expect_tx(&full[st], g.ntb * g.d_tx + g.x_tx);
+        const int i0 = rank == 0 ? 0 : nsh, i1 = rank == 0 ? nsh : g.ntb + 1;
         for (int i = i0; i < i1; ++i) {
           if (i == g.ntb) {
             w3_tma4_mc(half ? &mX1 : &mX0, &full[st], s + g.ntb * g.d_bytes, cb * 64, -g.pe, hq_lo - g.pe, n);
@@ -1469,7 +1454,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     for (int qb = q_beg; qb < q_end; ++qb) {
       if (leader) C2_TRACE(1, qb - q_beg, 0);
       ptx::mbar_wait(&full[st], ph);
-      if (g.tf) ptx::mbar_wait(&tdone[st], ph);
       if (leader) C2_TRACE(1, qb - q_beg, 1);
       ptx::tc_fence_after();
       const uint32_t base = s_lo0 + st * (stage_bytes >> 4);
@@ -1504,105 +1488,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     }
     if (leader) ptx::mma_commit(done);
     __syncwarp();
-  } else if (g.tf) {
-    // ===== warps 2-7: D = [g b | g a | g] of this q block, formed in registers from
-    // global loads of b, a (the forward's cache) and g (dy) and stored swizzled
-    // into the stage (same fp32 product and round-to-nearest as the backward
-    // prologue: D is bit-identical to the materialised one). Smem sees only the
-    // stores, as with TMA. Bias sums of the three blocks ride along (CTA0 of the
-    // pair; thread tt always owns channel chunk tt % 8). =====
-    const int tt = threadIdx.x - 64;
-    const int c8 = tt & 7;
-    const int nchunk = g.RD * g.Wp * 8;
-    const bf16* gB = reinterpret_cast<const bf16*>(g.tf_b);
-    const bf16* gA = reinterpret_cast<const bf16*>(g.tf_a);
-    const bf16* gG = reinterpret_cast<const bf16*>(g.tf_g);
-    float bs[3][8];
-#pragma unroll
-    for (int q = 0; q < 3; ++q)
-#pragma unroll
-      for (int e = 0; e < 8; ++e) bs[q][e] = 0.f;
-    int st = 0;
-    uint32_t ph = 0;
-    constexpr int UNR = 6;  // chunks per thread per block (1088 / 192 = 5.7 for C2)
-    for (int qb = q_beg; qb < q_end; ++qb) {
-      const int n = qb / g.T_img, t = qb % g.T_img;
-      const int hq_lo = g.R * t;
-      ptx::mbar_wait(&empty[st], ph ^ 1);
-      uint8_t* sb = sm + st * stage_bytes;
-      for (int i0 = tt; i0 < nchunk; i0 += 192 * UNR) {
-        uint4 gu[UNR], au[UNR], bu[UNR];
-        bool ok[UNR];
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const int i = i0 + 192 * u;
-          const int pos = i >> 3, rr = pos / g.Wp, w = pos - rr * g.Wp, h = hq_lo + rr;
-          ok[u] = i < nchunk && w < g.OWg && h < g.OHg;
-          const size_t off = ok[u] ? ((((size_t)n * g.OHg + h) * g.OWg + w) * 64 + c8 * 8) : 0;
-          gu[u] = ok[u] ? __ldg(reinterpret_cast<const uint4*>(gG + off)) : make_uint4(0, 0, 0, 0);
-          au[u] = ok[u] ? __ldg(reinterpret_cast<const uint4*>(gA + off)) : make_uint4(0, 0, 0, 0);
-          bu[u] = ok[u] ? __ldg(reinterpret_cast<const uint4*>(gB + off)) : make_uint4(0, 0, 0, 0);
-        }
-#pragma unroll
-        for (int u = 0; u < UNR; ++u) {
-          const int i = i0 + 192 * u;
-          if (i >= nchunk) break;
-          const int pos = i >> 3;
-          const __nv_bfloat162* g2 = reinterpret_cast<const __nv_bfloat162*>(&gu[u]);
-          const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&au[u]);
-          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&bu[u]);
-          uint4 gb, ga;
-          uint32_t* gbp = reinterpret_cast<uint32_t*>(&gb);
-          uint32_t* gap = reinterpret_cast<uint32_t*>(&ga);
-#pragma unroll
-          for (int e = 0; e < 4; ++e) {
-            const float2 gv = __bfloat1622float2(g2[e]), av = __bfloat1622float2(a2[e]),
-                         bv = __bfloat1622float2(b2[e]);
-            const float x0 = gv.x * bv.x, x1 = gv.y * bv.y, y0 = gv.x * av.x, y1 = gv.y * av.y;
-            gbp[e] = c2::pack2(x0, x1);
-            gap[e] = c2::pack2(y0, y1);
-            bs[0][2 * e] += x0; bs[0][2 * e + 1] += x1;
-            bs[1][2 * e] += y0; bs[1][2 * e + 1] += y1;
-            bs[2][2 * e] += gv.x; bs[2][2 * e + 1] += gv.y;
-          }
-          const uint32_t so = (uint32_t)pos * 128 + ((uint32_t)(c8 ^ (pos & 7)) << 4);  // SWIZZLE_128B
-          *reinterpret_cast<uint4*>(sb + so) = gb;
-          *reinterpret_cast<uint4*>(sb + g.d_bytes + so) = ga;
-          *reinterpret_cast<uint4*>(sb + 2 * g.d_bytes + so) = gu[u];
-        }
-      }
-      ptx::fence_proxy_async_smem();  // generic-proxy stores before the tensor core reads them
-      __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tdone[st]);
-      if (++st == g.stages) { st = 0; ph ^= 1; }
-    }
-    if (g.tf_bias) {
-      // per-CTA bias sums, fixed order: lanes l, l+8, l+16, l+24 (same chunk) by
-      // shuffles, then the six warps in order; CTA0 of each pair writes its slot
-#pragma unroll
-      for (int q = 0; q < 3; ++q)
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          float v = bs[q][e];
-          v += __shfl_down_sync(0xffffffffu, v, 16);
-          v += __shfl_down_sync(0xffffffffu, v, 8);
-          bs[q][e] = v;
-        }
-      float* red = reinterpret_cast<float*>(tslot + 4);  // 6 warps x 8 chunks x 24 floats, past the barriers
-      if (lane < 8) {
-#pragma unroll
-        for (int q = 0; q < 3; ++q)
-#pragma unroll
-          for (int e = 0; e < 8; ++e) red[((warp - 2) * 8 + lane) * 24 + q * 8 + e] = bs[q][e];
-      }
-      ptx::named_bar_sync(2, 192);
-      if (rank == 0 && tt < 192) {
-        const int q = tt / 64, c = tt % 64, ch = c / 8, e = c % 8;
-        float v = 0.f;
-        for (int w = 0; w < 6; ++w) v += red[(w * 8 + ch) * 24 + q * 8 + e];
-        g.tf_bias[(size_t)(blockIdx.x >> 1) * 192 + tt] = v;  // [pair][g b | g a | g] x 64
-      }
-    }
   }
   {
     // ===== epilogue on all 8 warps: warp w reads TMEM lanes 32 (w % 4) and
@@ -1825,7 +1710,7 @@ static W3Plan w3_plan(const Plan& P) {
   if (ns > nblk) ns = nblk;
   g.nsplit = ns;
   g.d_tx = d_tx; g.x_tx = x_tx; g.d_bytes = d_bytes; g.x_bytes = x_bytes; g.stages = stages;
-  pl.smem = 1024 + (size_t)stages * (ntb * d_bytes + x_bytes) + 1024 + 6 * 1024;  // + tf bias scratch
+  pl.smem = 1024 + (size_t)stages * (ntb * d_bytes + x_bytes) + 1024;
   pl.ok = true;
   return pl;
 }
@@ -1843,15 +1728,12 @@ int wgrad3_pairs_per_split(const Plan& P) {
 
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail, int jsplit, float* const* dW, const float* bpart, int SB,
-               float* const* db, bool* folded, const void* tf_a, const void* tf_b) {
+               float* const* db, bool* folded) {
   if (dev_skip("wgrad")) return QD_OK;
   W3Plan pl = w3_plan(P);
   // splits < the plan's: a partitioned launch sharing the SMs with a concurrent kernel
   if (!pl.ok || splits < 1 || splits > pl.g.nsplit) return QD_ERR_UNSUPPORTED;
   W3Args& g = pl.g;
-  g.tf = (tf_a && tf_b) ? 1 : 0;
-  if (g.tf && (g.ntb != 3 || g.jtiles != 1 || P.F != 64 || P.family != QD_FAM_PROPOSED))
-    return set_error(QD_ERR_UNSUPPORTED, "wgrad3 in-smem products: proposed, F = 64 only");
   g.nsplit = splits;
   g.part = part;
   g.fold_slot = -1;
@@ -1880,20 +1762,7 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
   cuuint32_t bD[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.RD, 1};
   if ((rc = c2_map(&Dm, D, 4, dD, bD))) return rc;
   Dm1 = Dm;
-  CUtensorMap Dm2 = Dm;
-  if (g.tf) {
-    // the transform warps read b, a and g (= `D`, the dy tensor) with plain loads;
-    // bias sums per pair go to `bpart` ([pairs][3F]) and are folded from there
-    g.jsplit = 0;
-    g.tf_a = tf_a; g.tf_b = tf_b; g.tf_g = D;
-    const bool bias = db && db[0] && bpart;
-    g.tf_bias = bias ? const_cast<float*>(bpart) : nullptr;
-    if (g.fold_slot >= 0) {
-      g.bpart = bias ? bpart : nullptr;
-      g.SB = g.jtiles * g.ablocks * g.nsplit;
-      if (!bias) g.db0 = g.db1 = g.db2 = nullptr;
-    }
-  } else if (g.jsplit) {
+  if (g.jsplit) {
     cuuint64_t d1[4] = {(cuuint64_t)(P.Jd - 64 * g.jsplit), (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
     if ((rc = c2_map(&Dm1, Dtail, 4, d1, bD))) return rc;
   }
@@ -1906,7 +1775,7 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
     // if the driver refuses it, the caller folds with separate kernels instead
     const char* ce = getenv("QD_W3_COOP");
     const bool coop = !(ce && atoi(ce) == 0);
-    if (cudaLaunchCoop(wgrad3_kernel, grid, dim3(256), pl.smem, st, coop, X0, X1, Dm, Dm1, Dm2, g) == cudaSuccess) {
+    if (cudaLaunchCoop(wgrad3_kernel, grid, dim3(256), pl.smem, st, coop, X0, X1, Dm, Dm1, g) == cudaSuccess) {
       if (folded) *folded = true;
       count_launch(st, "wgrad3");
       return check_launch("wgrad3");
@@ -1914,7 +1783,7 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cudaGetLastError();
     g.fold_slot = -1;
   }
-  launch_pdl(wgrad3_kernel, grid, dim3(256), pl.smem, st, X0, X1, Dm, Dm1, Dm2, g);
+  launch_pdl(wgrad3_kernel, grid, dim3(256), pl.smem, st, X0, X1, Dm, Dm1, g);
   count_launch(st, "wgrad3");
   return check_launch("wgrad3");
 }
