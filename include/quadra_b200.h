@@ -171,7 +171,14 @@ int qd_backward(const qd_desc* d, const void* x, const void* wpack,
                 void* workspace, void* stream);
 
 /* Which implementation qd_forward / qd_backward will use for d:
- * 0 = generic CUDA-core (SIMT) kernels, 1 = tcgen05/TMA kernels, 2 = depth-wise direct kernels. */
+ * 0 = generic CUDA-core (SIMT) kernels (exact fp32 FFMA / bf16),
+ * 1 = tcgen05/TMA kernels (bf16), 2 = depth-wise direct kernels,
+ * 3 = fp32 on the tcgen05 kernels: each fp32 operand split into two bf16 terms
+ *     (hi = bf16(v), lo = bf16(v - hi)), products hi*hi + hi*lo + lo*hi
+ *     accumulated in fp32 -- one K-tripled GEMM; error ~1e-5 relative.
+ *     proposed / t4 / first_order, stride 1, C and F multiples of 64.
+ *     qd_pack_bytes / qd_pack_weights then use the [hi | lo | hi] layout and
+ *     qd_sgd_pack returns QD_ERR_UNSUPPORTED (the layer packs itself). */
 int qd_path(const qd_desc* d);
 
 const char* qd_error_string(int status);
