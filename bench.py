@@ -887,8 +887,11 @@ def run_net_reference(args, name):
     times = [net_cpu_baseline(name) for _ in range(max(1, args.steps))]
     sec = sum(times) / len(times)
     value = 1.0 / sec
+    # ms_per_step: the MEASURED time of one step of the bounded sample (every quadratic
+    # layer at batch 1, `step_batch`); value is its rate (linear in the batch)
     out = {"metric": f"{name}_train_img_per_s", "value": value, "unit": "img/s", "impl": "reference",
-           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3 * batch,
+           "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3,
+           "step_batch": 1,
            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
            "config": {"workload": f"{name}: quadratic layers fwd+bwd, batch 1 sample scaled", "per_gpu_batch": batch},
            "cpu_baseline": {"value": value, "unit": "img/s", "cores": os.cpu_count(), "kind": "port",

@@ -25,7 +25,7 @@ bench.main()
 PY
 done; done
 QD_NO_PART=1 QD_FOLD_MAIN=1 python tools/prof_step.py 3 > ${o}_prof_plain.log 2>&1 && \
-  ncu --set full --clock-control none --import-source on -k regex:"conv2|wgrad3|prologue|pack|wsum|wfinish" -s 7 -c 7 \
+  QD_NO_PART=1 QD_FOLD_MAIN=1 ncu --set full --clock-control none --import-source on -k regex:"conv2|wgrad3|prologue|pack|wsum|wfinish" -s 7 -c 7 \
       -o ${o}_c2_full python tools/prof_step.py 3 > ${o}_ncu_full.log 2>&1
 python bench.py --steps 2 --warmup 3 --nets "" --no-cpu > ${o}_plain_launch.log 2>&1 && \
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${o}_launches.csv \
