@@ -9,6 +9,20 @@
 
 namespace qd {
 
+// ---- per-(thread, device) host state ------------------------------------------
+// Kernel attributes are per device, and the side stream / fork-join events of the
+// concurrent backward are per host thread: caches are thread_local arrays indexed
+// by the current device, so threads and devices never share them.
+constexpr int kMaxDev = 16;
+inline int cur_device() {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess) {
+    cudaGetLastError();
+    d = 0;
+  }
+  return d < 0 ? 0 : (d >= kMaxDev ? kMaxDev - 1 : d);
+}
+
 // ---- bookkeeping -----------------------------------------------------------
 // counts a launch of ours on `st`; with profiling on, also records a timing event
 void count_launch(cudaStream_t st, const char* name);

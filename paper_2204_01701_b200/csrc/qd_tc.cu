@@ -829,8 +829,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 static int g_num_sms = 0;
 static int g_arch_ok = -1;
 
-static bool init_driver() {
-  if (g_arch_ok >= 0) return g_arch_ok == 1;
+static bool init_driver_once() {
   int dev = 0;
   cudaDeviceProp prop;
   g_arch_ok = 0;
@@ -848,6 +847,11 @@ static bool init_driver() {
   g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   g_arch_ok = 1;
   return true;
+}
+// first call from any thread initialises (a function-local static: thread-safe)
+static bool init_driver() {
+  static const bool ok = init_driver_once();
+  return ok;
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() { return g_encode; }
@@ -995,7 +999,8 @@ template <int EPI, int NB>
 static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const CUtensorMap& O0,
                        const CUtensorMap& O1, const CUtensorMap& O2, const ConvArgs& args, cudaStream_t st) {
   using Cfg = ConvCfg<EPI, NB>;
-  static bool attr = false;
+  thread_local bool attr_[kMaxDev] = {};
+  bool& attr = attr_[cur_device()];
   if (!attr) {
     cudaFuncSetAttribute(conv_gemm_kernel<EPI, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
@@ -1035,7 +1040,8 @@ template <int NBLK>
 static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUtensorMap& Dm, const WgArgs& args,
                         cudaStream_t st) {
   using Cfg = WgCfg<NBLK>;
-  static bool attr = false;
+  thread_local bool attr_[kMaxDev] = {};
+  bool& attr = attr_[cur_device()];
   if (!attr) {
     cudaFuncSetAttribute(wgrad_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     attr = true;
@@ -1256,7 +1262,8 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
   if (P.family == QD_FAM_T2AND4) {
     // y = a b + c through the proposed epilogue with zero biases: a static zero
     // vector (no per-forward memset) when the layer is narrow enough
-    static float* zdev = nullptr;
+    thread_local float* zdev_[kMaxDev] = {};
+    float*& zdev = zdev_[cur_device()];
     if (!zdev && cudaGetSymbolAddress((void**)&zdev, g_zero_bias) != cudaSuccess) {
       cudaGetLastError();
       zdev = nullptr;
@@ -1297,25 +1304,35 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
 
 // side stream for work that can overlap the main chain (one per device/thread pair
 // would be more general; the library drives one device per process)
-static cudaStream_t g_side = nullptr;
-static cudaEvent_t g_fork = nullptr, g_join = nullptr;
+// per (host thread, device): one side stream and its fork / join events, so
+// concurrent callers never record into each other's events
+struct SideState {
+  cudaStream_t side = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static SideState& side_state() {
+  thread_local SideState s[kMaxDev];
+  return s[cur_device()];
+}
 static cudaStream_t fork_side(cudaStream_t st) {
-  if (!g_side) {
-    if (cudaStreamCreateWithFlags(&g_side, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_fork, cudaEventDisableTiming) != cudaSuccess ||
-        cudaEventCreateWithFlags(&g_join, cudaEventDisableTiming) != cudaSuccess) {
+  SideState& s = side_state();
+  if (!s.side) {
+    if (cudaStreamCreateWithFlags(&s.side, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.fork, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventCreateWithFlags(&s.join, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
-      g_side = nullptr;
+      s.side = nullptr;
       return nullptr;
     }
   }
-  cudaEventRecord(g_fork, st);
-  cudaStreamWaitEvent(g_side, g_fork, 0);
-  return g_side;
+  cudaEventRecord(s.fork, st);
+  cudaStreamWaitEvent(s.side, s.fork, 0);
+  return s.side;
 }
 static void join_side(cudaStream_t st, cudaStream_t side) {
-  cudaEventRecord(g_join, side);
-  cudaStreamWaitEvent(st, g_join, 0);
+  SideState& s = side_state();
+  cudaEventRecord(s.join, side);
+  cudaStreamWaitEvent(st, s.join, 0);
 }
 
 int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a, const void* b, const void* dy,

@@ -882,21 +882,24 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
 }
 
 // cap on the persistent conv2 grid (pairs) for the next launches; 0 = all SMs
-static int g_conv2_cap = 0;
+static thread_local int g_conv2_cap = 0;  // per host thread (set around one launch)
 void set_conv2_cap(int pairs) { g_conv2_cap = pairs; }
 
 template <int EPI, int NB, int R>
 static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
                        cudaStream_t st) {
-  static int attr_smem = 0;
+  thread_local int attr_smem_[kMaxDev] = {};
+  int& attr_smem = attr_smem_[cur_device()];
   if ((int)pl.smem > attr_smem) {
     cudaFuncSetAttribute(conv2_kernel<EPI, NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr_smem = (int)pl.smem;
   }
   // persistent grid: only as many pairs as can be co-resident (GPCs with an odd
   // number of free SMs cannot host a pair; a second wave would double the time)
-  static int maxc = 0;
-  static size_t maxc_smem = 0;
+  thread_local int maxc_[kMaxDev] = {};
+  thread_local size_t maxc_smem_[kMaxDev] = {};
+  int& maxc = maxc_[cur_device()];
+  size_t& maxc_smem = maxc_smem_[cur_device()];
   if (maxc == 0 || maxc_smem != pl.smem) {
     maxc = max_pair_clusters(conv2_kernel<EPI, NB, R>, C2Threads<EPI, NB>::THREADS, pl.smem);
     maxc_smem = pl.smem;
@@ -1696,8 +1699,10 @@ static W3Plan w3_plan(const Plan& P) {
   g.NT = ntb * 64; g.ntb = ntb; g.jtiles = P.Jd / g.NT;
   const int nblk = P.N * T_img;
   pl.smem = 1024 + (size_t)stages * (ntb * d_bytes + x_bytes) + 1024;
-  static int maxc = 0;
-  static size_t maxc_smem = 0;
+  thread_local int maxc_[kMaxDev] = {};
+  thread_local size_t maxc_smem_[kMaxDev] = {};
+  int& maxc = maxc_[cur_device()];
+  size_t& maxc_smem = maxc_smem_[cur_device()];
   if (maxc == 0 || maxc_smem != pl.smem) {
     cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     maxc = max_pair_clusters(wgrad3_kernel, 256, pl.smem);
@@ -1832,7 +1837,8 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cuuint64_t d1[4] = {(cuuint64_t)(P.Jd - 64 * g.jsplit), (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
     if ((rc = c2_map(&Dm1, Dtail, 4, d1, bD))) return rc;
   }
-  static int attr = 0;
+  thread_local int attr_[kMaxDev] = {};
+  int& attr = attr_[cur_device()];
   if ((int)pl.smem > attr) {
     cudaFuncSetAttribute(wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
     attr = (int)pl.smem;

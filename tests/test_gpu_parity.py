@@ -747,3 +747,42 @@ def test_im2col_conv_matches_torch_conv(family, k, s, p, c, w):
     assert Q.rel_err(cv(y), cv(yr)) <= 2e-2
     for n, t in m.named_parameters():
         assert Q.rel_err(cv(t.grad), cv(ref[n].grad)) <= 2e-2, n
+
+
+def test_concurrent_host_threads_same_results():
+    """Two host threads, each on its own CUDA stream, run the C2-shaped layer step
+    (partitioned backward: side stream + fork/join events per thread and device)
+    concurrently; each result equals the same step run alone, bit for bit."""
+    import threading
+    from paper_2204_01701_b200 import neurons
+    dev = torch.device("cuda")
+    spec = _spec("proposed", "conv", 64, 64, 3, 1, 1)
+    cases = []
+    for seed in (31, 32):
+        x, P, g = Q.synthetic_layer("proposed", "conv", 32, 64, 64, 32, 32, 3, 1, 1, seed=seed)
+        cases.append((torch.as_tensor(x, device=dev).bfloat16().contiguous(memory_format=torch.channels_last),
+                      torch.as_tensor(g, device=dev).bfloat16().contiguous(memory_format=torch.channels_last),
+                      {r: torch.as_tensor(v, dtype=torch.float32, device=dev) for r, v in P.items()}))
+
+    def run(i, out, stream):
+        xt, gt, params = cases[i]
+        with torch.cuda.stream(stream):
+            for _ in range(5):
+                y, cache = neurons.forward(spec, params, xt)
+                grads, dx = neurons.symbolic_backward(spec, params, cache, gt)
+            stream.synchronize()
+        out[i] = (y.clone(), dx.clone(), {k: v.clone() for k, v in grads.items()})
+
+    alone = {}
+    for i in range(2):
+        run(i, alone, torch.cuda.Stream())
+    conc = {}
+    ths = [threading.Thread(target=run, args=(i, conc, torch.cuda.Stream())) for i in range(2)]
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    for i in range(2):
+        assert torch.equal(alone[i][0], conc[i][0]) and torch.equal(alone[i][1], conc[i][1])
+        for k in alone[i][2]:
+            assert torch.equal(alone[i][2][k], conc[i][2][k]), (i, k)
