@@ -226,7 +226,7 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
               const void* xres, cudaStream_t st, int ss = 1, const void* a_tail = nullptr, int csplit = 0,
-              int pdl_wait = 1);
+              int pdl_wait = 1, int f32out = 0);
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                 int tiles_nn, int Cout, int nbias);
 // stride 2 on its own output grid (strided x maps, parity-class dgrad)

@@ -943,6 +943,43 @@ __global__ void __launch_bounds__(256) bwd_finish_kernel(Plan P, const float* __
   }
 }
 
+// fc weight fold: 32 x 32 tiles of the [Jd][Kf] partials, slices summed in order,
+// transposed through shared memory into the fc layout (in, out) = dst[c F + f]:
+// reads coalesced along c, writes along f (the element-wise fold above writes
+// with stride F). Blocks [0, ntile) fold weights, the rest the bias partials.
+__global__ void __launch_bounds__(256) wfinish_fc_kernel(Plan P, const float* __restrict__ wpart, int S,
+                                                         float* w0, float* w1, float* w2,
+                                                         const float* __restrict__ bpart, int SB, float* d0,
+                                                         float* d1, float* d2, int ntile) {
+  __shared__ float t[32][33];
+  if ((int)blockIdx.x >= ntile) {
+    finish_bias_block(P, (int)blockIdx.x - ntile, bpart, SB, d0, d1, d2);
+    return;
+  }
+  if (!w0) return;
+  const int tk = (P.Kf + 31) / 32;
+  const int j0 = (blockIdx.x / tk) * 32, k0 = (blockIdx.x % tk) * 32;
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+  const size_t slice = (size_t)P.Jd * P.Kf;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int j = j0 + ty + 8 * i, k = k0 + tx;
+    float acc = 0.f;
+    if (j < P.Jd && k < P.Kf)
+      for (int sl = 0; sl < S; ++sl) acc += __ldg(wpart + sl * slice + (size_t)j * P.Kf + k);
+    t[ty + 8 * i][tx] = acc;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int k = k0 + ty + 8 * i, j = j0 + tx;  // k = input channel c, j = role F + f
+    if (j >= P.Jd || k >= P.Kf) continue;
+    const int role = j / P.F, f = j - role * P.F;
+    float* dst = role == 0 ? w0 : (role == 1 ? w1 : w2);
+    if (dst) dst[(size_t)k * P.F + f] = t[tx][ty + 8 * i];
+  }
+}
+
 // conv weight fold: block = (NJ D channels j, K half, 64-channel chunk). G warp
 // groups sum interleaved split subsets (fixed order) of the block's NJ x rr x 64
 // partial values (G x NJ = 8: with few splits the lanes cover more rows, so every
@@ -1144,6 +1181,10 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
     else
       wfinish_conv_kernel<0><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws1, dW[0], dW[1], dW[2], bpart, SB, db[0],
                                                            db[1], db[2], nwc);
+  } else if (P.kind == QD_KIND_FC && P.sq == 0 && ws.ng == 0 && !getenv("QD_OLD_FINISH")) {
+    const int ntile = dW[0] ? ((P.Jd + 31) / 32) * ((P.Kf + 31) / 32) : 0;
+    wfinish_fc_kernel<<<ntile + nbb, 256, 0, st>>>(P, wpart, S, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1], db[2],
+                                                   ntile);
   } else {
     bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
                                                   db[2], nwb);

@@ -1605,13 +1605,21 @@ int x3_forward(const Plan& P, const void* x, const void* wpack, const float* con
   launch_x3_split((const float*)x, xh, xl, P.Min * P.C, st);
   GemmCfg c = fprop_cfg(P);
   const float* nob[3] = {nullptr, nullptr, nullptr};
+  const float* bz[3] = {bias[0], bias[1], bias[2]};
+  if (c.nbias == 0) bz[0] = bz[1] = bz[2] = nullptr;
+  if (!(P.flags & QD_FLAG_TC_V1) && P.kind == QD_KIND_CONV) {
+    // CTA-pair halo kernel with the fp32 epilogue in registers: y, a, b written
+    // once, no raw accumulator pass
+    int rc2 = run_conv2(c.epi, c.nbk, xh, xl, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 2, wpack, P.nb * P.F,
+                        3 * P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, bz, nullptr, st, 1,
+                        nullptr, 0, 1, 1);
+    if (rc2 != QD_ERR_UNSUPPORTED) return rc2 ? rc2 : check_launch("x3 forward");
+  }
   int S = 1;
   int rc = run_conv(c.epi, c.nbk, xh, xl, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 2, wpack, P.nb * P.F, 3 * P.Kf,
                     c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nob, nullptr, st,
                     (float*)(ws + L.off_P), L.sz_P, 1, 0, 0, 0, 1, &S);
   if (rc) return rc;
-  const float* bz[3] = {bias[0], bias[1], bias[2]};
-  if (c.nbias == 0) bz[0] = bz[1] = bz[2] = nullptr;
   launch_x3_fprop_finish((const float*)(ws + L.off_P), S, P.Mout, c.tiles_nn * c.nbk * 64, P.F, P.nb,
                          c.epi == EPI_PROPOSED ? 0 : (c.epi == EPI_T4 ? 1 : 2), (float*)y, (float*)a, (float*)b, bz,
                          st);
@@ -1623,8 +1631,12 @@ int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
   const bf16* wd = (const bf16*)wpack + 3 * pack_fprop_elems(P);
   bf16* Dh = (bf16*)(ws + L.off_D);
   bf16* Dl = Dh + (size_t)P.Mout * P.Jd;
+  bf16* xh = (bf16*)(ws + L.off_XS);
+  bf16* xl = xh + (size_t)P.Min * P.C;
   float* bpart = (float*)(ws + L.off_BS);
   const bool dgiven = (P.flags & QD_FLAG_D_GIVEN) != 0;
+  // the HBM-bound passes first, back to back: x for the weight products, then D
+  if (dW[0]) launch_x3_split((const float*)x, xh, xl, P.Min * P.C, st);
   if (dgiven) {
     // `dy` is the fp32 operand D (qd_bn_backward_D formed it and the bias grads)
     launch_x3_split((const float*)dy, Dh, Dl, P.Mout * P.Jd, st);
@@ -1634,38 +1646,65 @@ int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
                        L.bs_split, st);
   }
   int rc;
+  const GemmCfg dc = dgrad_cfg(P);
+  const bool c2d = dx && !(P.flags & QD_FLAG_TC_V1) && P.kind == QD_KIND_CONV &&
+                   conv2_fits(P.N, P.Jd, P.OW, P.OH, P.W, P.H, P.r - 1 - P.p, P.r, 2, dc.nbk, dc.nout, dc.tiles_nn,
+                              P.C, 0);
+  const bool w3 = dW[0] && !(P.flags & QD_FLAG_TC_V1) && wgrad3_split(P) == L.wg_split &&
+                  wgrad3_pairs_per_split(P) == 1;
+  // SM partition as in the bf16 backward: the three wgrad3 products (and their fold)
+  // on ~half of the pairs on the side stream, the persistent dgrad capped to the rest
+  int S = L.wg_split, dg_pairs = 0;
+  if (w3 && c2d && !getenv("QD_NO_PART")) {
+    const int part = getenv("QD_X3_PART") ? atoi(getenv("QD_X3_PART")) : (L.wg_split * 35 + 50) / 100;  // measured best on C2-fp32 (26 of 74)
+    if (part >= 1 && part < L.wg_split) {
+      S = part;
+      dg_pairs = L.wg_split - part;
+    }
+  }
+  // the weight-gradient chain (three products, fold) runs on the side stream beside
+  // the dgrad: both only read D, x and the packed weights
+  cudaStream_t side = (dW[0] && dx) ? fork_side(st) : nullptr;
+  cudaStream_t wst = side ? side : st;
   if (dW[0]) {
-    bf16* xh = (bf16*)(ws + L.off_XS);
-    bf16* xl = xh + (size_t)P.Min * P.C;
-    launch_x3_split((const float*)x, xh, xl, P.Min * P.C, st);
     float* part = (float*)(ws + L.off_WG);
     const size_t slot = (size_t)P.Jd * P.Kf;
-    const int S = L.wg_split;
     const bf16* xa[3] = {xh, xh, xl};
     const bf16* da[3] = {Dh, Dl, Dh};
-    const bool w3 = !(P.flags & QD_FLAG_TC_V1) && wgrad3_split(P) == S;
     for (int i = 0; i < 3; ++i) {
-      float* pi = part + (size_t)i * S * slot;
-      rc = w3 ? run_wgrad3(P, xa[i], nullptr, da[i], pi, S, st) : run_wgrad_v1(P, xa[i], da[i], pi, S, st);
+      float* pi = part + (size_t)i * S * slot;  // 3 S contiguous slots
+      rc = w3 ? run_wgrad3(P, xa[i], nullptr, da[i], pi, S, wst) : run_wgrad_v1(P, xa[i], da[i], pi, S, wst);
       if (rc) return rc;
     }
     WSplits uni;
     memset(&uni, 0, sizeof(uni));
     float* const nodb[3] = {nullptr, nullptr, nullptr};
-    launch_bwd_finish(P, part, 3 * S, uni, dW, bpart, L.bs_split, (dgiven || !P.nbias) ? nodb : db, st);
+    launch_bwd_finish(P, part, 3 * S, uni, dW, bpart, L.bs_split, (dgiven || !P.nbias) ? nodb : db, wst);
   } else if (!dgiven && db[0] && P.nbias) {
     launch_bias_finish(P, bpart, L.bs_split, db, st);
   }
   if (dx) {
-    GemmCfg c = dgrad_cfg(P);
     const float* nob[3] = {nullptr, nullptr, nullptr};
-    int S = 1;
-    rc = run_conv(c.epi, c.nbk, Dh, Dl, P.Jd, P.OW, P.OH, P.N, P.W, P.H, P.r - 1 - P.p, P.r, 2, wd, P.Cd, 3 * P.Kd,
-                  c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, nullptr, st,
-                  (float*)(ws + L.off_P), L.sz_P, 1, 0, 0, 0, 2, &S);
-    if (rc) return rc;
-    if (S > 1) launch_x3_sum((const float*)(ws + L.off_P), S, P.Min * P.C, (float*)dx, st);
+    rc = QD_ERR_UNSUPPORTED;
+    if (c2d) {
+      if (dg_pairs) set_conv2_cap(dg_pairs);
+      rc = run_conv2(dc.epi, dc.nbk, Dh, Dl, P.Jd, P.OW, P.OH, P.N, P.W, P.H, P.r - 1 - P.p, P.r, 2, wd, P.Cd,
+                     3 * P.Kd, dc.b_rs_tile, dc.b_rs_blk, dc.tiles_nn, dc.out_c_tile, dx, nullptr, nullptr, P.C, nob,
+                     nullptr, st, 1, nullptr, 0, 1, 1);
+      set_conv2_cap(0);
+    }
+    if (rc == QD_ERR_UNSUPPORTED) {
+      int Sd = 1;
+      rc = run_conv(dc.epi, dc.nbk, Dh, Dl, P.Jd, P.OW, P.OH, P.N, P.W, P.H, P.r - 1 - P.p, P.r, 2, wd, P.Cd,
+                    3 * P.Kd, dc.b_rs_tile, dc.b_rs_blk, dc.tiles_nn, dc.out_c_tile, dx, nullptr, nullptr, P.C, nob,
+                    nullptr, st, (float*)(ws + L.off_P), L.sz_P, 1, 0, 0, 0, 2, &Sd);
+      if (rc) return rc;
+      if (Sd > 1) launch_x3_sum((const float*)(ws + L.off_P), Sd, P.Min * P.C, (float*)dx, st);
+    } else if (rc) {
+      return rc;
+    }
   }
+  if (side) join_side(st, side);
   return check_launch("x3 backward");
 }
 

@@ -52,6 +52,9 @@ struct C2Args {
   int pdl_wait;  // 1: wait for the previous kernel's outputs (PDL) before the first global read
   ptx::FastDiv fd_nn, fd_T, fd_Wp;  // tiles_nn, T_img, Wp
   int csplit;  // A channel blocks >= csplit come from the second map (dgrad: D = [g b, g a] then dy)
+  int dual;    // extra K segments of A: 1 = [x*x | x] (segment 1 from the second map), 2 = the fp32
+               // split [hi | hi | lo] (segment 2 from the second map)
+  int f32out;  // fp32 outputs stored straight from registers (the fp32 split path)
   int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
   unsigned long long* trace;  // QD_TRACE (dev only): per-role clock64 timeline of cluster 0
   const float* bias0;
@@ -310,7 +313,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
           C2_TRACE_B(1, 0, it, 9 + 2 * ab);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&afull[as], 2u * g.halo_tx);
           const bool tail = g.csplit && cb >= g.csplit;
-          c2::tma4_cg2((half || tail) ? &mA1 : &mA0, c2::peer0(&afull[as]), sHalo + as * g.halo_bytes,
+          const bool second = (half > 0 && half == g.dual) || tail;
+          c2::tma4_cg2(second ? &mA1 : &mA0, c2::peer0(&afull[as]), sHalo + as * g.halo_bytes,
                        (tail ? cb - g.csplit : cb) * 64, -g.pe, hq_lo - g.pe, n);
           if (ab == 0) C2_TRACE(0, it, 7);
           const int wf = w + g.pf * nclusters;
@@ -318,7 +322,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
             const int rf = wf / g.tiles_nn;
             const int tf = rf % g.T_img, nf = 2 * (rf / g.T_img) + (int)rank;
             if (nf < g.N)
-              c2::tma4_prefetch((half || tail) ? &mA1 : &mA0, (tail ? cb - g.csplit : cb) * 64, -g.pe,
+              c2::tma4_prefetch(second ? &mA1 : &mA0, (tail ? cb - g.csplit : cb) * 64, -g.pe,
                                 (128 * tf) / g.Wp - g.pe, nf);
           }
         }
@@ -534,6 +538,21 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
 #pragma unroll
             for (int e = 0; e < 16; ++e) vc[e] = va[e] * vb[e];
           }
+          if (g.f32out) {
+            // fp32 y, a, b rows of this lane's pixel, straight from registers
+            if (pix >= 0) {
+              float* dy_ = reinterpret_cast<float*>(g.out0) + (size_t)pix * g.Cout + c0;
+              float* da_ = reinterpret_cast<float*>(g.out1) + (size_t)pix * g.Cout + c0;
+              float* db_ = reinterpret_cast<float*>(g.out2) + (size_t)pix * g.Cout + c0;
+#pragma unroll
+              for (int v4 = 0; v4 < 4; ++v4) {
+                reinterpret_cast<float4*>(dy_)[v4] = make_float4(vc[4 * v4], vc[4 * v4 + 1], vc[4 * v4 + 2], vc[4 * v4 + 3]);
+                reinterpret_cast<float4*>(da_)[v4] = make_float4(va[4 * v4], va[4 * v4 + 1], va[4 * v4 + 2], va[4 * v4 + 3]);
+                reinterpret_cast<float4*>(db_)[v4] = make_float4(vb[4 * v4], vb[4 * v4 + 1], vb[4 * v4 + 2], vb[4 * v4 + 3]);
+              }
+            }
+            continue;
+          }
           c2_pack16(vc, pk[0][jj][0], pk[0][jj][1]);
           c2_pack16(va, pk[1][jj][0], pk[1][jj][1]);
           c2_pack16(vb, pk[2][jj][0], pk[2][jj][1]);
@@ -543,6 +562,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
         if (tracer) C2_TRACE(2, it, 2);
         if (tracer1) C2_TRACE(2, it, 11);
+        if (g.f32out) continue;  // stored above
         if (g.direct) {
           // straight from registers: this lane's pixel row, CW channels per output
           if (pix >= 0 && !(g.dbg & 4)) {
@@ -674,7 +694,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
               if (NB == 2) out[e] += v1[e];
             }
           }
-          if (g.direct) {
+          if (g.f32out) {
+            // fp32 rows straight from registers (64 B: four 16-B stores)
+            if (pix >= 0) {
+              const int ch = ((EPI == E2_PLAIN) ? c_base + o * 64 : c_base) + jj * 16;
+              float* dst = reinterpret_cast<float*>((EPI == E2_PROPOSED || EPI == E2_T4)
+                                                        ? (o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2))
+                                                        : g.out0) + (size_t)pix * g.Cout + ch;
+#pragma unroll
+              for (int v4 = 0; v4 < 4; ++v4)
+                reinterpret_cast<float4*>(dst)[v4] =
+                    make_float4(out[4 * v4], out[4 * v4 + 1], out[4 * v4 + 2], out[4 * v4 + 3]);
+            }
+          } else if (g.direct) {
             // 32 B of this row's output straight from registers (two 16-B stores)
             if (pix >= 0) {
               bf16* dst = (EPI == E2_PROPOSED || EPI == E2_T4) ? (o == 0 ? g.out0 : (o == 1 ? g.out1 : g.out2))
@@ -834,7 +866,7 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   uint32_t halo = (halo_tx + 1023) / 1024 * 1024;
   if (halo > 64 * 1024) return pl;
   int cblks = Cin / 64;
-  int ablocks = cblks * (dual ? 2 : 1);
+  int ablocks = cblks * (1 + dual);
   int KBtot = ablocks * r * r;
   uint32_t bstage = NB * 32 * 128;
   // staging: one 4 KB tile per warp per output pass (single epilogue pass over TMEM,
@@ -925,7 +957,8 @@ static int c2_launch(const CUtensorMap& A0, const CUtensorMap& A1, const CUtenso
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
-              const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit, int pdl_wait) {
+              const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit, int pdl_wait,
+              int f32out) {
   int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
   int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
   C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
@@ -937,9 +970,12 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   if (!g.b_contig && nbk != 2) return QD_ERR_UNSUPPORTED;
   g.out_c_tile = out_c_tile;
   g.ss = ss;
+  g.dual = dual;
+  g.f32out = f32out;
+  if (f32out && (ss != 1 || epi == E2_SQ)) return QD_ERR_UNSUPPORTED;
   {
     const char* e = getenv("QD_C2_DIRECT");
-    g.direct = e ? atoi(e) : 0;
+    g.direct = f32out ? 1 : (e ? atoi(e) : 0);
     const char* f = getenv("QD_PF");
     g.pf = f ? atoi(f) : 0;  // measured: no gain on C2 (the pipe is MMA-bound)
 

@@ -59,10 +59,11 @@ void launch_x3_split(const float* x, bf16* hi, bf16* lo, long long n, cudaStream
 }
 
 // packed weights, x3 layout: fprop rows [nb F][3 Kf] = [hi | lo | hi] of the bf16
-// fprop layout (fprop_src / fprop_row), then dgrad rows [Cd][3 Kd] likewise
-__global__ void x3_pack_kernel(Plan P, const float* w0, const float* w1, const float* w2, bf16* out) {
+// fprop layout (fprop_src / fprop_row), then dgrad rows [Cd][3 Kd] likewise.
+// Elements [i0, nf + nd) of that (fprop, dgrad) sequence.
+__global__ void x3_pack_kernel(Plan P, const float* w0, const float* w1, const float* w2, bf16* out, long long i0) {
   const long long nf = (long long)P.nb * P.F * P.Kf, nd = (long long)P.Cd * P.Kd;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nf + nd;
+  for (long long i = i0 + blockIdx.x * (long long)blockDim.x + threadIdx.x; i < nf + nd;
        i += (long long)gridDim.x * blockDim.x) {
     float v;
     bf16* base;
@@ -103,11 +104,47 @@ __global__ void x3_pack_kernel(Plan P, const float* w0, const float* w1, const f
   }
 }
 
+// fc fprop part of the x3 pack as 32 x 32 transposes: the fc weights are (in, out)
+// = w[c F + f] while a packed fprop row runs over c (fprop_row for the f index);
+// reads coalesced along f, writes along c. grid (F / 32, C / 32, roles).
+__global__ void __launch_bounds__(256) x3_pack_fc_kernel(Plan P, const float* w0, const float* w1, const float* w2,
+                                                         bf16* out) {
+  __shared__ float t[32][33];
+  const int role = blockIdx.z, f0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+  const int tx = threadIdx.x % 32, ty = threadIdx.x / 32;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int c = c0 + ty + 8 * i, f = f0 + tx;
+    t[ty + 8 * i][tx] = (c < P.C && f < P.F) ? __ldg(w + (size_t)c * P.F + f) : 0.f;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int f = f0 + ty + 8 * i, c = c0 + tx;
+    if (f >= P.F || c >= P.C) continue;
+    const int R = fprop_row(role, f, P.nb, P.FT);
+    bf16 hi, lo;
+    x3_split1(t[tx][ty + 8 * i], hi, lo);
+    bf16* row = out + (size_t)R * 3 * P.Kf;
+    row[c] = hi;
+    row[P.Kf + c] = lo;
+    row[2 * P.Kf + c] = hi;
+  }
+}
+
 void launch_x3_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
-  const long long n = (long long)P.nb * P.F * P.Kf + (long long)P.Cd * P.Kd;
+  const long long nf = (long long)P.nb * P.F * P.Kf;
+  long long i0 = 0;
+  if (P.kind == QD_KIND_FC && P.sq == 0) {
+    x3_pack_fc_kernel<<<dim3((P.F + 31) / 32, (P.C + 31) / 32, P.nroles), 256, 0, st>>>(P, w[0], w[1], w[2],
+                                                                                         (bf16*)wpack);
+    i0 = nf;  // the dgrad rows read the fc weights along f: coalesced in the generic kernel
+  }
+  const long long n = nf + (long long)P.Cd * P.Kd - i0;
   long long g = (n + 255) / 256;
   if (g > 148 * 16) g = 148 * 16;
-  x3_pack_kernel<<<(unsigned)g, 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack);
+  x3_pack_kernel<<<(unsigned)g, 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack, i0);
   count_launch(st, "x3_pack");
 }
 
@@ -134,51 +171,67 @@ __global__ void __launch_bounds__(256) x3_prologue_kernel(Plan P, const float* _
   for (int q = 0; q < 3; ++q)
 #pragma unroll
     for (int e = 0; e < 8; ++e) s[q][e] = 0.f;
-  if (rl < lanes) {
-    for (long long m = r0 + rl; m < r1; m += lanes) {
-      const size_t off = (size_t)m * F + ch * 8;
-      float g[8], av[8], bv[8];
-      {
-        const float4* p = reinterpret_cast<const float4*>(dy + off);
-        float4 u = __ldg(p), w = __ldg(p + 1);
-        g[0] = u.x; g[1] = u.y; g[2] = u.z; g[3] = u.w; g[4] = w.x; g[5] = w.y; g[6] = w.z; g[7] = w.w;
+  auto ld8 = [](const float* p, float v[8]) {
+    const float4 u = __ldg(reinterpret_cast<const float4*>(p)), w = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    v[0] = u.x; v[1] = u.y; v[2] = u.z; v[3] = u.w; v[4] = w.x; v[5] = w.y; v[6] = w.z; v[7] = w.w;
+  };
+  auto emit = [&](long long m, const float* g, const float* av, const float* bv) {
+    bf16* hrow = Dh + (size_t)m * P.Jd + ch * 8;
+    bf16* lrow = Dl + (size_t)m * P.Jd + ch * 8;
+    uint4 h, l;
+    if (mat) {
+      float gb[8], ga[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        gb[e] = g[e] * bv[e];
+        ga[e] = g[e] * av[e];
+        s[0][e] += gb[e];
+        s[1][e] += ga[e];
+        s[2][e] += g[e];
       }
-      bf16* hrow = Dh + (size_t)m * P.Jd + ch * 8;
-      bf16* lrow = Dl + (size_t)m * P.Jd + ch * 8;
-      uint4 h, l;
-      if (mat) {
-        const float4* pa = reinterpret_cast<const float4*>(a + off);
-        const float4* pb = reinterpret_cast<const float4*>(b + off);
-        float4 a0 = __ldg(pa), a1 = __ldg(pa + 1), b0 = __ldg(pb), b1 = __ldg(pb + 1);
-        av[0] = a0.x; av[1] = a0.y; av[2] = a0.z; av[3] = a0.w; av[4] = a1.x; av[5] = a1.y; av[6] = a1.z; av[7] = a1.w;
-        bv[0] = b0.x; bv[1] = b0.y; bv[2] = b0.z; bv[3] = b0.w; bv[4] = b1.x; bv[5] = b1.y; bv[6] = b1.z; bv[7] = b1.w;
-        float gb[8], ga[8];
-#pragma unroll
-        for (int e = 0; e < 8; ++e) {
-          gb[e] = g[e] * bv[e];
-          ga[e] = g[e] * av[e];
-          s[0][e] += gb[e];
-          s[1][e] += ga[e];
-          s[2][e] += g[e];
-        }
-        x3_split8(gb, h, l);
-        *reinterpret_cast<uint4*>(hrow) = h;
-        *reinterpret_cast<uint4*>(lrow) = l;
-        x3_split8(ga, h, l);
-        *reinterpret_cast<uint4*>(hrow + F) = h;
-        *reinterpret_cast<uint4*>(lrow + F) = l;
-        if (nblk == 3) {
-          x3_split8(g, h, l);
-          *reinterpret_cast<uint4*>(hrow + 2 * F) = h;
-          *reinterpret_cast<uint4*>(lrow + 2 * F) = l;
-        }
-      } else {
-#pragma unroll
-        for (int e = 0; e < 8; ++e) s[0][e] += g[e];
+      x3_split8(gb, h, l);
+      *reinterpret_cast<uint4*>(hrow) = h;
+      *reinterpret_cast<uint4*>(lrow) = l;
+      x3_split8(ga, h, l);
+      *reinterpret_cast<uint4*>(hrow + F) = h;
+      *reinterpret_cast<uint4*>(lrow + F) = l;
+      if (nblk == 3) {
         x3_split8(g, h, l);
-        *reinterpret_cast<uint4*>(hrow) = h;
-        *reinterpret_cast<uint4*>(lrow) = l;
+        *reinterpret_cast<uint4*>(hrow + 2 * F) = h;
+        *reinterpret_cast<uint4*>(lrow + 2 * F) = l;
       }
+    } else {
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s[0][e] += g[e];
+      x3_split8(g, h, l);
+      *reinterpret_cast<uint4*>(hrow) = h;
+      *reinterpret_cast<uint4*>(lrow) = l;
+    }
+  };
+  if (rl < lanes) {
+    // two rows per iteration: all twelve 16-B loads in flight before any use
+    long long m = r0 + rl;
+    for (; m + lanes < r1; m += 2 * lanes) {
+      float g0[8], a0[8], b0[8], g1[8], a1[8], b1[8];
+      const size_t o0 = (size_t)m * F + ch * 8, o1 = (size_t)(m + lanes) * F + ch * 8;
+      ld8(dy + o0, g0);
+      ld8(dy + o1, g1);
+      if (mat) {
+        ld8(a + o0, a0); ld8(b + o0, b0);
+        ld8(a + o1, a1); ld8(b + o1, b1);
+      }
+      emit(m, g0, a0, b0);
+      emit(m + lanes, g1, a1, b1);
+    }
+    if (m < r1) {
+      float g0[8], a0[8], b0[8];
+      const size_t o0 = (size_t)m * F + ch * 8;
+      ld8(dy + o0, g0);
+      if (mat) {
+        ld8(a + o0, a0);
+        ld8(b + o0, b0);
+      }
+      emit(m, g0, a0, b0);
     }
   }
   if (!part) return;

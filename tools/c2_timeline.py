@@ -12,8 +12,10 @@ wl = bench.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "c2"]
 fam, kind, n, c, f, h, w, r, s, p, dts = wl
 spec = bench.make_spec(wl)
 x64, P64, g64 = Q.synthetic_layer(fam, kind, n, c, f, h, w, r, s, p, seed=0)
-x = torch.as_tensor(x64, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
-gy = torch.as_tensor(g64, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+_dt = torch.bfloat16 if dts == "bf16" else torch.float32
+_fmt = torch.channels_last if kind != "fc" else torch.contiguous_format
+x = torch.as_tensor(x64, device="cuda").to(_dt).contiguous(memory_format=_fmt)
+gy = torch.as_tensor(g64, device="cuda").to(_dt).contiguous(memory_format=_fmt)
 params = {k: torch.as_tensor(v, dtype=torch.float32, device="cuda") for k, v in P64.items()}
 flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
 
