@@ -138,3 +138,31 @@ def test_reference_recorded_node_device_backward(family, kind):
     assert _rel(dx_dev, dx_ref) <= 1e-4
     for k in g_ref:
         assert _rel(g_dev[k], g_ref[k]) <= 1e-4, k
+
+
+def test_init_params_same_draws_as_reference():
+    """neurons.init_params consumes the same Generator draws, in the same role
+    order, as the reference init_params (neurons.py:132-147): identical values
+    (our fp32 masters = the reference's fp64 draws rounded) and the same
+    generator state afterwards, for every family and kind."""
+    import torch
+    from paper_2204_01701_b200 import neurons
+    from paper_2204_01701_b200.spec import QuadraticLayerSpec
+    T, N, A = _import_reference()
+    cases = []
+    for fam in N.FAMILIES:
+        if fam.startswith("t1"):
+            cases.append(("fc", fam, 7, 1, 1))
+            continue
+        cases += [("fc", fam, 6, 5, 1), ("conv", fam, 3, 4, 3), ("dwconv", fam, 4, 4, 3)]
+    for kind, fam, c, f, k in cases:
+        rspec = A.QuadraticLayerSpec(kind=kind, family=fam, in_dim=c, out_dim=f, kernel=k, stride=1,
+                                     pad=k // 2)
+        ospec = QuadraticLayerSpec(kind=kind, family=fam, in_dim=c, out_dim=f, kernel=k, stride=1, pad=k // 2)
+        r1, r2 = np.random.default_rng(99), np.random.default_rng(99)
+        ref = N.init_params(rspec, r1)
+        ours = neurons.init_params(ospec, r2, device="cpu")
+        assert list(ref) == list(ours), (kind, fam)
+        for role in ref:
+            assert torch.equal(ours[role], torch.as_tensor(ref[role].data, dtype=torch.float32)), (kind, fam, role)
+        assert r1.integers(1 << 62) == r2.integers(1 << 62), (kind, fam)
