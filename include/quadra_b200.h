@@ -115,6 +115,21 @@ int qd_bn_forward(long long M, int C, int dtype, const void* y, const float* gam
 int qd_bn_forward_res(long long M, int C, int dtype, const void* y, const void* res, const float* gamma,
                       const float* beta, float* run_mean, float* run_var, float momentum, float eps, int relu,
                       int training, void* z, float* save_mean, float* save_invstd, void* ws, void* stream);
+/* BN forward statistics in the layer's fprop epilogue:
+ * qd_bn_stats_rows(d) = rows of per-(tile, 32-pixel warp) statistics the fprop
+ * epilogue can write for d (0: this layer's forward path has none -- use
+ * qd_bn_forward). qd_forward_bnstats = qd_forward that also writes them into
+ * `stats` (float [rows*F mean | rows*F M2 | rows count], of the stored y
+ * values); qd_bn_forward_stats merges the rows (Chan's formula, fixed order)
+ * into the batch mean / biased variance (+ running update) and applies
+ * z = relu?(BN(y) (+ res)) -- no reduction pass over y. */
+int qd_bn_stats_rows(const qd_desc* d);
+int qd_forward_bnstats(const qd_desc* d, const void* x, const void* wpack, const float* const bias[3], void* y,
+                       void* a_cache, void* b_cache, void* workspace, float* stats, void* stream);
+int qd_bn_forward_stats(long long M, int C, int dtype, const void* y, const void* res, const float* stats, int rows,
+                        const float* gamma, const float* beta, float* run_mean, float* run_var, float momentum,
+                        float eps, int relu, int training, void* z, float* save_mean, float* save_invstd,
+                        void* stream);
 /* BN(+ReLU) backward fused with the quadratic layer's backward prologue: from
  * dz (gradient of z) and the layer's y, a, b it forms dgamma, dbeta, the layer's
  * bias gradients db[] and the operand D the layer backward consumes; then call

@@ -32,7 +32,8 @@ EXPORTS = ("qd_validate", "qd_out_shape", "qd_pack_bytes", "qd_workspace_bytes",
            "qd_error_string", "qd_last_error", "qd_launch_count", "qd_version",
            "qd_profile", "qd_profile_mark", "qd_profile_count", "qd_profile_read",
            "qd_sgd_pack", "qd_bn_workspace_bytes", "qd_bn_forward", "qd_bn_forward_res", "qd_bn_backward_D",
-           "qd_maxpool_forward", "qd_maxpool_backward", "qd_im2col")
+           "qd_maxpool_forward", "qd_maxpool_backward", "qd_im2col",
+           "qd_bn_stats_rows", "qd_forward_bnstats", "qd_bn_forward_stats")
 
 
 class QdDesc(ctypes.Structure):
@@ -87,6 +88,14 @@ def load():
         lib.qd_bn_forward_res.argtypes = [ctypes.c_longlong, ctypes.c_int, ctypes.c_int, vp, vp, vp, vp, vp, vp,
                                           ctypes.c_float, ctypes.c_float, ctypes.c_int, ctypes.c_int, vp, vp, vp,
                                           vp, vp]
+        lib.qd_bn_stats_rows.argtypes = [P(QdDesc)]
+        lib.qd_bn_stats_rows.restype = ctypes.c_int
+        lib.qd_forward_bnstats.argtypes = [P(QdDesc), vp, vp, fp3, vp, vp, vp, vp, vp, vp]
+        lib.qd_forward_bnstats.restype = ctypes.c_int
+        lib.qd_bn_forward_stats.argtypes = [ctypes.c_longlong, ctypes.c_int, ctypes.c_int, vp, vp, vp, ctypes.c_int,
+                                            vp, vp, vp, vp, ctypes.c_float, ctypes.c_float, ctypes.c_int,
+                                            ctypes.c_int, vp, vp, vp, vp]
+        lib.qd_bn_forward_stats.restype = ctypes.c_int
         lib.qd_bn_forward_res.restype = ctypes.c_int
         lib.qd_bn_backward_D.argtypes = [P(QdDesc), vp, vp, vp, vp, vp, vp, vp, vp, ctypes.c_int, vp, vp, vp, fp3,
                                          vp, vp]

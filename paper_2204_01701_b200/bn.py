@@ -78,6 +78,48 @@ def bn_forward(y, gamma, beta, running_mean, running_var, momentum, eps, relu, t
     return z, sm, si
 
 
+def _epilogue_stat_rows(spec, x, dtype):
+    """rows of BN statistics the layer's fprop epilogue can write (0: reduce y
+    separately). Opt-in (QD_BN_EPI=1): measured slower on the nets (ResNet-18
+    13.5k vs 15.6k img/s: the per-warp reductions lengthen the fprop epilogue by
+    ~16% and the row merge is latency-bound), DESIGN.md §9."""
+    if os.environ.get("QD_BN_EPI", "0") != "1" or x.device.type != "cuda":
+        return 0
+    dt = dtype if dtype is not None else (torch.float32 if x.dtype == torch.float64 else x.dtype)
+    return neurons.bn_stats_rows(spec, tuple(x.shape), dt)
+
+
+def bn_forward_from_stats(y, stats, rows, gamma, beta, running_mean, running_var, momentum, eps, relu, res=None):
+    """BN forward from the fprop epilogue's statistics rows: merge + apply, no
+    reduction pass over y. Returns (z, save_mean, save_invstd)."""
+    lib = _lib.load()
+    yr = _rows(y)
+    M, C = yr.shape
+    z = torch.empty_like(y)
+    sm = torch.empty(C, dtype=torch.float32, device=y.device)
+    si = torch.empty(C, dtype=torch.float32, device=y.device)
+    if res is not None and (res.shape != y.shape or res.dtype != y.dtype or not _rows(res).is_contiguous()):
+        raise ValueError("bn_forward_from_stats: residual must match y (shape, dtype, channels_last)")
+    st = lib.qd_bn_forward_stats(M, C, _dtype_code(y), y.data_ptr(), res.data_ptr() if res is not None else None,
+                                 stats.data_ptr(), int(rows), gamma.data_ptr(), beta.data_ptr(),
+                                 running_mean.data_ptr(), running_var.data_ptr(), float(momentum), float(eps),
+                                 int(relu), 1, z.data_ptr(), sm.data_ptr(), si.data_ptr(),
+                                 torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_bn_forward_stats")
+    return z, sm, si
+
+
+def _forward_with_stats(spec, params, x, dtype, recompute):
+    """layer forward; with the BN statistics rows when its epilogue has them"""
+    rows = _epilogue_stat_rows(spec, x, dtype)
+    if not rows:
+        y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute)
+        return y, cache, None, 0
+    stats = torch.empty(rows * (2 * spec.out_dim + 1), dtype=torch.float32, device=x.device)
+    y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute, bn_stats=stats)
+    return y, cache, stats, rows
+
+
 def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu, params=None):
     """(D, dgamma, dbeta, {bias role: grad}) for the layer's backward from D."""
     lib = _lib.load()
@@ -113,8 +155,12 @@ class _QuadBNFunction(torch.autograd.Function):
         roles = tuple(param_shapes(spec).keys())
         params = dict(zip(roles, tensors))
         dtype, recompute = neurons.split_opts(dtype)
-        y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute)
-        z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
+        y, cache, stats, rows = _forward_with_stats(spec, params, x, dtype, recompute)
+        if stats is not None:
+            z, sm, si = bn_forward_from_stats(y, stats, rows, gamma, beta, bn.running_mean, bn.running_var,
+                                              bn.momentum, bn.eps, relu)
+        else:
+            z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
         ctx.spec, ctx.roles, ctx.params, ctx.cache, ctx.relu = spec, roles, params, cache, relu
         ctx.x_dtype = x.dtype
         ctx.save_for_backward(y, gamma, beta, sm, si)
@@ -145,11 +191,15 @@ class _QuadBNAddReLUFunction(torch.autograd.Function):
         roles = tuple(param_shapes(spec).keys())
         params = dict(zip(roles, tensors))
         dtype, recompute = neurons.split_opts(dtype)
-        y, cache = neurons.forward(spec, params, x, dtype=dtype, recompute=recompute)
+        y, cache, stats, rows = _forward_with_stats(spec, params, x, dtype, recompute)
         if res.dtype != y.dtype or (y.dim() == 4 and not res.is_contiguous(memory_format=torch.channels_last)):
             res = res.to(y.dtype).contiguous(memory_format=torch.channels_last)
-        z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, True, True,
-                               res=res)
+        if stats is not None:
+            z, sm, si = bn_forward_from_stats(y, stats, rows, gamma, beta, bn.running_mean, bn.running_var,
+                                              bn.momentum, bn.eps, True, res=res)
+        else:
+            z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, True, True,
+                                   res=res)
         ctx.spec, ctx.roles, ctx.params, ctx.cache = spec, roles, params, cache
         ctx.x_dtype, ctx.res_dtype = x.dtype, res.dtype
         ctx.save_for_backward(y, z, gamma, beta, sm, si)

@@ -376,6 +376,46 @@ int qd_forward(const qd_desc* d, const void* x, const void* wpack, const float* 
   return simt_forward(P, x, wpack, bs, y, a_cache, b_cache, (char*)workspace, L, s);
 }
 
+int qd_bn_stats_rows(const qd_desc* d) {
+  if (validate(d)) return 0;
+  Plan P = make_plan(*d);
+  const int path = device_path(P, d->flags);
+  return (path == 1 || path == 3) ? tc_stat_rows(P, path) : 0;
+}
+
+int qd_forward_bnstats(const qd_desc* d, const void* x, const void* wpack, const float* const bias[3], void* y,
+                       void* a_cache, void* b_cache, void* workspace, float* stats, void* stream) {
+  int st = validate(d);
+  if (st) return st;
+  Plan P = make_plan(*d);
+  if (!x || !wpack || !y || !stats) return set_error(QD_ERR_ARG, "null tensor pointer");
+  for (int i = 0; i < P.nbias; ++i)
+    if (!bias || !bias[i]) return set_error(QD_ERR_ARG, "bias role %d is NULL", i);
+  if (caches_ab(P.family) && (!a_cache || !b_cache))
+    return set_error(QD_ERR_ARG, "family caches a and b: a_cache/b_cache must be given");
+  const int path = device_path(P, d->flags);
+  if (!((path == 1 || path == 3) && tc_stat_rows(P, path) > 0))
+    return set_error(QD_ERR_UNSUPPORTED, "qd_forward_bnstats: no epilogue statistics on this layer's path");
+  Workspace L = plan_workspace(P, path);
+  if (L.total && !workspace) return set_error(QD_ERR_ARG, "workspace is NULL");
+  cudaStream_t s = (cudaStream_t)stream;
+  if (path == 3) return x3_forward(P, x, wpack, bias, y, a_cache, b_cache, (char*)workspace, L, s, stats);
+  return tc_forward(P, x, wpack, bias, y, a_cache, b_cache, (char*)workspace, L, s, stats);
+}
+
+int qd_bn_forward_stats(long long M, int C, int dtype, const void* y, const void* res, const float* stats, int rows,
+                        const float* gamma, const float* beta, float* run_mean, float* run_var, float momentum,
+                        float eps, int relu, int training, void* z, float* save_mean, float* save_invstd,
+                        void* stream) {
+  if (M < 1 || C < 1 || rows < 1) return set_error(QD_ERR_DIM, "batchnorm over %lld rows x %d channels", M, C);
+  if (dtype != QD_F32 && dtype != QD_BF16) return set_error(QD_ERR_CONFIG, "unknown dtype %d", dtype);
+  if (!(eps > 0.f)) return set_error(QD_ERR_CONFIG, "batchnorm eps must be positive");
+  if (!y || !stats || !gamma || !beta || !z || !save_mean || !save_invstd)
+    return set_error(QD_ERR_ARG, "qd_bn_forward_stats: NULL argument");
+  return bn_forward_stats(M, C, dtype, y, res, stats, rows, gamma, beta, run_mean, run_var, momentum, eps, relu,
+                          training, z, save_mean, save_invstd, (cudaStream_t)stream);
+}
+
 int qd_backward(const qd_desc* d, const void* x, const void* wpack, const void* a_cache,
                 const void* b_cache, const void* dy, void* dx, float* const dW[3],
                 float* const db[3], void* workspace, void* stream) {

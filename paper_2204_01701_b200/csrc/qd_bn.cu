@@ -848,6 +848,83 @@ int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma,
                              sm, si, ws, st, (const float*)res);
 }
 
+// Chan's parallel-variance merge of two (count, mean, M2) groups
+__device__ __forceinline__ void chan_merge(float& n, float& mean, float& m2, float nb, float mb, float m2b) {
+  const float nt = n + nb;
+  if (nb == 0.f) return;
+  if (n == 0.f) {
+    n = nb; mean = mb; m2 = m2b;
+    return;
+  }
+  const float d = mb - mean, f = nb / nt;
+  mean += d * f;
+  m2 += m2b + d * d * n * f;
+  n = nt;
+}
+
+// statistics rows of the fprop epilogue -> batch mean / invstd (+ running update):
+// block = 32 channels x 32 row groups; group g merges rows g, g + 32, ... in order,
+// then the 32 group results merge in order (fixed order: deterministic)
+__global__ void __launch_bounds__(1024) bn_merge_finalize(int C, int R, const float* __restrict__ stats, float eps,
+                                                          float momentum, int training, float* run_mean,
+                                                          float* run_var, float* save_mean, float* save_invstd) {
+  ptx::pdl_wait();
+  ptx::pdl_launch();
+  __shared__ float sn[32][33], sm_[32][33], sq[32][33];
+  const int col = threadIdx.x % 32, grp = threadIdx.x / 32;
+  const int c = blockIdx.x * 32 + col;
+  const float* mean_r = stats;
+  const float* m2_r = stats + (size_t)R * C;
+  const float* cnt_r = stats + (size_t)2 * R * C;
+  float n = 0.f, mean = 0.f, m2 = 0.f;
+  if (c < C)
+    for (int r = grp; r < R; r += 32) chan_merge(n, mean, m2, __ldg(cnt_r + r), __ldg(mean_r + (size_t)r * C + c),
+                                                 __ldg(m2_r + (size_t)r * C + c));
+  sn[grp][col] = n; sm_[grp][col] = mean; sq[grp][col] = m2;
+  __syncthreads();
+  if (grp != 0 || c >= C) return;
+  n = 0.f; mean = 0.f; m2 = 0.f;
+  for (int g = 0; g < 32; ++g) chan_merge(n, mean, m2, sn[g][col], sm_[g][col], sq[g][col]);
+  const float var = n > 0.f ? m2 / n : 0.f;  // biased (tensor.py:444)
+  save_mean[c] = mean;
+  save_invstd[c] = rsqrtf(var + eps);
+  if (training && run_mean) {  // tensor.py:445-450 (biased var in the running update too)
+    run_mean[c] = run_mean[c] * (1.f - momentum) + momentum * mean;
+    run_var[c] = run_var[c] * (1.f - momentum) + momentum * var;
+  }
+}
+
+template <typename T>
+static int bn_forward_stats_t(long long M, int C, const T* y, const T* res, const float* stats, int R,
+                              const float* gamma, const float* beta, float* rm, float* rv, float momentum, float eps,
+                              int relu, int training, T* z, float* sm, float* si, cudaStream_t st) {
+  if (dev_skip("bn")) return QD_OK;
+  launch_pdl(bn_merge_finalize, dim3((C + 31) / 32), dim3(1024), 0, st, C, R, stats, eps, momentum, training, rm, rv,
+             sm, si);
+  count_launch(st, "bn_stats_merge");
+  const long long n = M * C;
+  long long g = ((bn_vec(C) ? n / 8 : n) + 255) / 256;
+  if (bn_vec(C)) g = (g + 3) / 4;
+  if (g > 148 * 8) g = 148 * 8;
+  if (bn_vec(C))
+    launch_pdl(bn_apply_vec_kernel<T>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, (const float*)sm, (const float*)si,
+               gamma, beta, relu, z, res);
+  else
+    bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z, res);
+  count_launch(st, "bn_apply");
+  return check_launch("bn forward (epilogue statistics)");
+}
+
+int bn_forward_stats(long long M, int C, int dtype, const void* y, const void* res, const float* stats, int rows,
+                     const float* gamma, const float* beta, float* rm, float* rv, float momentum, float eps, int relu,
+                     int training, void* z, float* sm, float* si, cudaStream_t st) {
+  if (dtype == QD_BF16)
+    return bn_forward_stats_t<bf16>(M, C, (const bf16*)y, (const bf16*)res, stats, rows, gamma, beta, rm, rv, momentum,
+                                    eps, relu, training, (bf16*)z, sm, si, st);
+  return bn_forward_stats_t<float>(M, C, (const float*)y, (const float*)res, stats, rows, gamma, beta, rm, rv,
+                                   momentum, eps, relu, training, (float*)z, sm, si, st);
+}
+
 int bn_backward_D(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,
                   const float* beta, const float* sm, const float* si, int relu, void* D, float* dgamma,
                   float* dbeta, float* const db[3], char* ws, cudaStream_t st) {

@@ -160,6 +160,11 @@ size_t bn_workspace_bytes(long long M, int C, int Jd);
 int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta, float* rm,
                float* rv, float momentum, float eps, int relu, int training, void* z, float* sm, float* si, char* ws,
                cudaStream_t st, const void* res = nullptr);
+// BN forward from the statistics rows of the fprop epilogue (mean / M2 / count per
+// row, merged with Chan's formula in a fixed order), then the apply pass
+int bn_forward_stats(long long M, int C, int dtype, const void* y, const void* res, const float* stats, int rows,
+                     const float* gamma, const float* beta, float* rm, float* rv, float momentum, float eps, int relu,
+                     int training, void* z, float* sm, float* si, cudaStream_t st);
 int bn_backward_D(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,
                   const float* beta, const float* sm, const float* si, int relu, void* D, float* dgamma,
                   float* dbeta, float* const db[3], char* ws, cudaStream_t st);
@@ -195,7 +200,8 @@ void launch_x3_fprop_finish(const float* raw, int S, long long M, int ld, int F,
                             float* b, const float* const bias[3], cudaStream_t st);
 void launch_x3_sum(const float* raw, int S, long long n, float* out, cudaStream_t st);
 int x3_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
-               void* b, char* ws, const Workspace& L, cudaStream_t st);
+               void* b, char* ws, const Workspace& L, cudaStream_t st, float* stats = nullptr);
+int tc_stat_rows(const Plan& P, int path);
 int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
                 void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L, cudaStream_t st);
 
@@ -226,7 +232,9 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
               const void* xres, cudaStream_t st, int ss = 1, const void* a_tail = nullptr, int csplit = 0,
-              int pdl_wait = 1, int f32out = 0);
+              int pdl_wait = 1, int f32out = 0, float* stats = nullptr);
+int conv2_stat_rows(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
+                    int tiles_nn, int Cout, int nbias);
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                 int tiles_nn, int Cout, int nbias);
 // stride 2 on its own output grid (strided x maps, parity-class dgrad)
@@ -242,7 +250,7 @@ inline Plan stride1_plan(const Plan& P) {
   return Q;
 }
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3],
-               void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st);
+               void* y, void* a, void* b, char* ws, const Workspace& L, cudaStream_t st, float* stats = nullptr);
 // dW[0] == nullptr skips the weight/bias gradient GEMM (QD_FLAG_NO_DW)
 int tc_backward(const Plan& P, const void* x, const void* wpack, const void* a, const void* b,
                 const void* dy, void* dx, float* const dW[3], float* const db[3], char* ws,

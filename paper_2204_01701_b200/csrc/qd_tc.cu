@@ -1246,8 +1246,21 @@ void launch_bwd_prologue_vec(const Plan& P, const void* dy, const void* a, const
 
 __device__ float g_zero_bias[3 * 2048];  // zero-initialised at module load, never written
 
+// rows of BN statistics the forward epilogue can write for P (0: the forward takes
+// a path without them -- the caller then reduces y separately)
+int tc_stat_rows(const Plan& P, int path) {
+  if (P.kind != QD_KIND_CONV || P.s != 1 || (P.flags & QD_FLAG_TC_V1)) return 0;
+  if (P.family != QD_FAM_PROPOSED && P.family != QD_FAM_T4) return 0;
+  GemmCfg c = fprop_cfg(P);
+  if (path == 1)
+    return conv2_stat_rows(P.N, P.C, P.W, P.H, P.OW, P.OH, P.p, P.r, 0, c.nbk, c.nout, c.tiles_nn, P.F, c.nbias);
+  if (path == 3)
+    return conv2_stat_rows(P.N, P.C, P.W, P.H, P.OW, P.OH, P.p, P.r, 2, c.nbk, c.nout, c.tiles_nn, P.F, c.nbias);
+  return 0;
+}
+
 int tc_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
-               void* b, char* ws, const Workspace& L, cudaStream_t st) {
+               void* b, char* ws, const Workspace& L, cudaStream_t st, float* stats) {
   const void* a0 = x;
   const void* a1 = nullptr;
   if (P.sq) {
@@ -1294,9 +1307,11 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
   if (dev_skip("fprop")) return QD_OK;
   if (!(P.flags & QD_FLAG_TC_V1)) {
     int rc2 = run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
-                        P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st);
+                        P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st,
+                        1, nullptr, 0, 1, 0, stats);
     if (rc2 != QD_ERR_UNSUPPORTED) return rc2;
   }
+  if (stats) return set_error(QD_ERR_UNSUPPORTED, "BN statistics: the conv2 forward does not fit this layer");
   return run_conv(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
                   P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st,
                   (float*)(ws + L.off_SK), L.sz_SK);
@@ -1599,7 +1614,7 @@ static int run_wgrad_v1(const Plan& P, const void* x0, const void* D, float* par
 }
 
 int x3_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
-               void* b, char* ws, const Workspace& L, cudaStream_t st) {
+               void* b, char* ws, const Workspace& L, cudaStream_t st, float* stats) {
   bf16* xh = (bf16*)(ws + L.off_XS);
   bf16* xl = xh + (size_t)P.Min * P.C;
   launch_x3_split((const float*)x, xh, xl, P.Min * P.C, st);
@@ -1612,9 +1627,10 @@ int x3_forward(const Plan& P, const void* x, const void* wpack, const float* con
     // once, no raw accumulator pass
     int rc2 = run_conv2(c.epi, c.nbk, xh, xl, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 2, wpack, P.nb * P.F,
                         3 * P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, bz, nullptr, st, 1,
-                        nullptr, 0, 1, 1);
+                        nullptr, 0, 1, 1, stats);
     if (rc2 != QD_ERR_UNSUPPORTED) return rc2 ? rc2 : check_launch("x3 forward");
   }
+  if (stats) return set_error(QD_ERR_UNSUPPORTED, "BN statistics: the conv2 forward does not fit this layer");
   int S = 1;
   int rc = run_conv(c.epi, c.nbk, xh, xl, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, 2, wpack, P.nb * P.F, 3 * P.Kf,
                     c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nob, nullptr, st,

@@ -55,6 +55,12 @@ struct C2Args {
   int dual;    // extra K segments of A: 1 = [x*x | x] (segment 1 from the second map), 2 = the fp32
                // split [hi | hi | lo] (segment 2 from the second map)
   int f32out;  // fp32 outputs stored straight from registers (the fp32 split path)
+  // BN statistics of y (the batch norm that follows the layer, bn.QuadConvBN):
+  // per (tile, CTA, 32-row warp) and channel, the mean and M2 of the stored y
+  // values of the tile's valid pixels; stats = [mean: rows x Cout][M2: rows x
+  // Cout][count: rows], merged in a fixed order by bn_merge_finalize
+  float* stats;
+  int stat_rows;
   int dbg;  // QD_DEBUG bits (dev only): 1 = epilogue only releases TMEM, 2 = no MMA
   unsigned long long* trace;  // QD_TRACE (dev only): per-role clock64 timeline of cluster 0
   const float* bias0;
@@ -186,6 +192,23 @@ __device__ __forceinline__ void c2_store_rb_pre(const uint8_t* st, bf16* dst, co
     if (roff[i] >= 0) *reinterpret_cast<uint4*>(dst + roff[i]) = val;
   }
 }
+// sum over the warp's 32 lanes of v[c] for 32 channels at once: recursive halving
+// (each lane gives away the half of its vector it does not keep: 16+8+4+2+1
+// shuffles), after which lane c holds channel c's sum
+__device__ __forceinline__ float c2_lane_sums32(float (&v)[32], int lane) {
+#pragma unroll
+  for (int half = 16; half >= 1; half >>= 1) {
+    const bool up = (lane & half) != 0;
+#pragma unroll
+    for (int i = 0; i < half; ++i) {
+      const float send = up ? v[i] : v[i + half];
+      const float keep = up ? v[i + half] : v[i];
+      v[i] = keep + __shfl_xor_sync(0xffffffffu, send, half);
+    }
+  }
+  return v[0];
+}
+
 __device__ __forceinline__ void c2_pack16(const float* v, uint4& lo, uint4& hi) {
   lo = make_uint4(c2::pack2(v[0], v[1]), c2::pack2(v[2], v[3]), c2::pack2(v[4], v[5]), c2::pack2(v[6], v[7]));
   hi = make_uint4(c2::pack2(v[8], v[9]), c2::pack2(v[10], v[11]), c2::pack2(v[12], v[13]), c2::pack2(v[14], v[15]));
@@ -506,6 +529,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         // registers, the accumulator handed back, then three staged store passes
         constexpr int JJ = CW / 16;
         uint4 pk[3][JJ][2];  // [y|a|b][jj][lo|hi]
+        float ysv[CW == 32 ? 32 : 1];  // BN statistics: the stored y of this lane's pixel, 32 channels
 #pragma unroll
         for (int jj = 0; jj < JJ; ++jj) {
           const int col = eg * CW + jj * 16;
@@ -538,6 +562,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
 #pragma unroll
             for (int e = 0; e < 16; ++e) vc[e] = va[e] * vb[e];
           }
+          if constexpr (CW == 32) if (g.stats) {
+#pragma unroll
+            for (int e = 0; e < 16; ++e)
+              ysv[jj * 16 + e] = pix < 0 ? 0.f : (g.f32out ? vc[e] : __bfloat162float(__float2bfloat16_rn(vc[e])));
+          }
           if (g.f32out) {
             // fp32 y, a, b rows of this lane's pixel, straight from registers
             if (pix >= 0) {
@@ -562,6 +591,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         if (lane == 0) c2::arrive_remote(tempty0 + acs * 8);
         if (tracer) C2_TRACE(2, it, 2);
         if (tracer1) C2_TRACE(2, it, 11);
+        if constexpr (CW == 32) if (g.stats) {
+          // this warp's 32 rows: per-channel mean and M2 (the finalize merges rows
+          // with Chan's formula); the squares first, while ysv still holds y
+          float sq[32];
+#pragma unroll
+          for (int e = 0; e < 32; ++e) sq[e] = ysv[e] * ysv[e];
+          const float s2 = c2_lane_sums32(sq, lane);
+          const float s1 = c2_lane_sums32(ysv, lane);
+          const int cnt = __popc(__ballot_sync(0xffffffffu, pix >= 0));
+          const int row = (rest * 2 + (int)rank) * 4 + q;
+          const float mean = cnt ? s1 / (float)cnt : 0.f;
+          const float m2 = cnt ? fmaxf(s2 - s1 * mean, 0.f) : 0.f;
+          const int cg = c_base + eg * 32 + lane;
+          g.stats[(size_t)row * g.Cout + cg] = mean;
+          g.stats[(size_t)g.stat_rows * g.Cout + (size_t)row * g.Cout + cg] = m2;
+          if (lane == 0 && eg == 0 && j == 0) g.stats[(size_t)2 * g.stat_rows * g.Cout + row] = (float)cnt;
+        }
         if (g.f32out) continue;  // stored above
         if (g.direct) {
           // straight from registers: this lane's pixel row, CW channels per output
@@ -958,7 +1004,7 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
               const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit, int pdl_wait,
-              int f32out) {
+              int f32out, float* stats) {
   int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
   int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
   C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
@@ -972,6 +1018,9 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   g.ss = ss;
   g.dual = dual;
   g.f32out = f32out;
+  g.stats = stats;
+  g.stat_rows = ((N + 1) / 2) * g.T_img * 8;
+  if (stats && !(epi == E2_PROPOSED || epi == E2_T4)) return QD_ERR_UNSUPPORTED;
   if (f32out && (ss != 1 || epi == E2_SQ)) return QD_ERR_UNSUPPORTED;
   {
     const char* e = getenv("QD_C2_DIRECT");
@@ -1827,6 +1876,13 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
   launch_pdl(wgrad3_kernel, grid, dim3(256), pl.smem, st, X0, X1, Dm, Dm1, g);
   count_launch(st, "wgrad3");
   return check_launch("wgrad3");
+}
+
+// rows of BN statistics the conv2 fprop epilogue writes for this geometry (0: not eligible)
+int conv2_stat_rows(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
+                    int tiles_nn, int Cout, int nbias) {
+  C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, nout, tiles_nn, Cout, nbias);
+  return pl.ok ? ((N + 1) / 2) * pl.g.T_img * 8 : 0;
 }
 
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,

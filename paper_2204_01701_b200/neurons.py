@@ -198,11 +198,20 @@ def split_opts(dtype):
     return dtype, False
 
 
-def forward(spec, params, x, *, dtype=None, flags=0, recompute=False):
+def bn_stats_rows(spec, x_shape, dtype, flags=0):
+    """Rows of BN statistics the forward epilogue writes for this layer (0: none;
+    the BN that follows then reduces y itself). C ABI qd_bn_stats_rows."""
+    desc = make_desc(spec, x_shape, dtype, flags)
+    return int(_lib.load().qd_bn_stats_rows(ctypes.byref(desc)))
+
+
+def forward(spec, params, x, *, dtype=None, flags=0, recompute=False, bn_stats=None):
     """Evaluate one layer on the GPU; returns (y, LayerCache). neurons.py:235-276.
 
     recompute=True: the cache keeps x only (the a, b buffers the kernels write are
-    not retained); the backward rebuilds a, b with one more forward GEMM."""
+    not retained); the backward rebuilds a, b with one more forward GEMM.
+    bn_stats: an fp32 buffer of ``bn_stats_rows * (2 F + 1)`` floats the fprop
+    epilogue fills with the BN statistics of y (bn.QuadConvBN)."""
     validate_device_spec(spec)
     lib = _lib.load()
     x = _as_device(x)
@@ -226,12 +235,20 @@ def forward(spec, params, x, *, dtype=None, flags=0, recompute=False):
     if spec.family in ("proposed", "t4", "t2and4"):
         a, b = mk(), mk()
     ws = _workspace(desc, x.device)
-    st = lib.qd_forward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
-                        _lib.ptr3(*[t.data_ptr() for t in biases]), y.data_ptr(),
-                        a.data_ptr() if a is not None else None,
-                        b.data_ptr() if b is not None else None, ws.data_ptr(),
-                        torch.cuda.current_stream().cuda_stream)
-    _lib.raise_for(st, "qd_forward")
+    if bn_stats is not None:
+        st = lib.qd_forward_bnstats(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
+                                    _lib.ptr3(*[t.data_ptr() for t in biases]), y.data_ptr(),
+                                    a.data_ptr() if a is not None else None,
+                                    b.data_ptr() if b is not None else None, ws.data_ptr(), bn_stats.data_ptr(),
+                                    torch.cuda.current_stream().cuda_stream)
+        _lib.raise_for(st, "qd_forward_bnstats")
+    else:
+        st = lib.qd_forward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(),
+                            _lib.ptr3(*[t.data_ptr() for t in biases]), y.data_ptr(),
+                            a.data_ptr() if a is not None else None,
+                            b.data_ptr() if b is not None else None, ws.data_ptr(),
+                            torch.cuda.current_stream().cuda_stream)
+        _lib.raise_for(st, "qd_forward")
     if recompute and a is not None:
         return y, LayerCache(spec.family, spec.kind, x, None, None, tuple(y.shape), desc, wpack, key, True)
     return y, LayerCache(spec.family, spec.kind, x, a, b, tuple(y.shape), desc, wpack, key)

@@ -786,3 +786,36 @@ def test_concurrent_host_threads_same_results():
         assert torch.equal(alone[i][0], conc[i][0]) and torch.equal(alone[i][1], conc[i][1])
         for k in alone[i][2]:
             assert torch.equal(alone[i][2][k], conc[i][2][k]), (i, k)
+
+
+@pytest.mark.parametrize("shape,dtype", [((8, 64, 32, 32), torch.bfloat16), ((5, 128, 14, 14), torch.bfloat16),
+                                         ((4, 64, 16, 16), torch.float32)])
+def test_bn_statistics_from_fprop_epilogue(shape, dtype, monkeypatch):
+    """BN forward statistics written by the layer's fprop epilogue (per 32-pixel
+    warp mean / M2, Chan merge) vs the separate reduction pass over y: same batch
+    mean / biased variance (running buffers) to fp32 round-off, same output z;
+    the epilogue path launches no reduction kernel."""
+    import copy
+    from paper_2204_01701_b200.bn import QuadConvBN
+    from paper_2204_01701_b200.nn import QuadConv2d
+    from paper_2204_01701_b200 import neurons
+    torch.manual_seed(8)
+    n, c, h, w = shape
+    m1 = QuadConvBN(QuadConv2d(c, c, 3, 1, 1, device="cuda", compute_dtype=dtype), relu=True)
+    with torch.no_grad():
+        for r in ("ba", "bb", "bc"):
+            getattr(m1.layer, r).uniform_(-0.5, 1.5)  # non-zero channel means
+    m2 = copy.deepcopy(m1)
+    x = torch.randn(shape, device="cuda").to(dtype).contiguous(memory_format=torch.channels_last)
+    assert neurons.bn_stats_rows(m1.layer.spec, shape, dtype) > 0
+    monkeypatch.setenv("QD_BN_EPI", "1")
+    z1, names1 = _kernel_names(lambda: m1(x))
+    monkeypatch.setenv("QD_BN_EPI", "0")
+    z2, names2 = _kernel_names(lambda: m2(x))
+    assert "bn_stats_merge" in names1 and "bn_stats" not in names1, names1
+    assert "bn_stats" in names2
+    assert torch.allclose(m1.bn.running_mean, m2.bn.running_mean, rtol=1e-4, atol=1e-5)
+    assert torch.allclose(m1.bn.running_var, m2.bn.running_var, rtol=1e-4, atol=1e-5)
+    d = (z1.float() - z2.float()).abs()
+    tol = 2e-2 if dtype == torch.bfloat16 else 1e-4
+    assert float(d.max()) <= tol * float(z2.float().abs().max()), float(d.max())
