@@ -558,9 +558,15 @@ __global__ void __launch_bounds__(256, 4) bn_bwd_reduce_c4_kernel(long long M, i
   }
 }
 
+// workspace: [reduction partial rows][2C] then [D-emission partial rows][Jd]
+// (the register-streaming emit: S rows; the streaming emit: <= bn_stream_rows(),
+// its fold group rows included)
+static size_t bn_emit_rows(long long M, int C) {
+  const size_t a = (size_t)bn_splits(M, C), b = bn_stream_rows();
+  return a > b ? a : b;
+}
 size_t bn_workspace_bytes(long long M, int C, int Jd) {
-  const int S = bn_splits(M, C);
-  return (size_t)S * 2 * C * 4 + (size_t)S * Jd * 4 + 256;
+  return (size_t)bn_splits(M, C) * 2 * C * 4 + bn_emit_rows(M, C) * Jd * 4 + 256;
 }
 
 // per-block partials over rows [r0, r1): thread = (channel c = tid % C? no: strided)
@@ -825,6 +831,8 @@ static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, c
   count_launch(st, "bn_bwd_reduce");
   launch_pdl(bn_grad_finalize, dim3((C + 31) / 32), dim3(1024), 0, st, C, S, (const float*)part, dgamma, dbeta);
   count_launch(st, "bn_bwd_finalize");
+  if (bn_stream_ok(M, C, P.dtype))  // qd_bnstream.cu: bulk-copy streaming emit, bias folded in-kernel
+    return bn_emit_stream(P, dz, y, a, b, gamma, beta, sm, si, relu, D, dgamma, dbeta, db, bpart, st);
   if (bn_c4(C) && getenv("QD_BN_C4"))  // dev: the 4-channel emit (slower, measured)
     launch_pdl(bn_emit_D_c4_kernel<T>, dim3(S), dim3(256), 0, st, P, dz, y, a, b, sm, si, gamma, beta,
                (const float*)dgamma, (const float*)dbeta, relu, D, bpart);

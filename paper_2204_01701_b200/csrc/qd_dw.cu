@@ -484,7 +484,7 @@ static bool dw_vec(const Plan& P) {
 }
 template <typename K>
 static void dw_smem_attr(K kernel, size_t smem) {
-  if (smem > 48 * 1024) cudaFuncSetAttribute((const void*)kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  raise_smem_attr((const void*)kernel, smem);
 }
 
 int dw_wgrad_split(const Plan& P) {

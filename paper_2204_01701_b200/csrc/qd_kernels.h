@@ -4,15 +4,17 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 #include <string.h>
+#include <mutex>
 #include <utility>
 #include "qd_common.cuh"
 
 namespace qd {
 
 // ---- per-(thread, device) host state ------------------------------------------
-// Kernel attributes are per device, and the side stream / fork-join events of the
-// concurrent backward are per host thread: caches are thread_local arrays indexed
-// by the current device, so threads and devices never share them.
+// The side stream / fork-join events of the concurrent backward are per host
+// thread: those caches are thread_local arrays indexed by the current device.
+// Kernel attributes are per (function, device) for the whole process: see
+// raise_smem_attr.
 constexpr int kMaxDev = 16;
 inline int cur_device() {
   int d = 0;
@@ -21,6 +23,36 @@ inline int cur_device() {
     d = 0;
   }
   return d < 0 ? 0 : (d >= kMaxDev ? kMaxDev - 1 : d);
+}
+
+// Raise a kernel's opt-in dynamic shared memory on the current device to at
+// least `bytes`; never lowers it. The attribute is process-wide, so the record
+// of what was set is too (one mutex): a per-thread "largest so far" let the
+// autograd thread set a smaller value under a launch of the main thread's larger
+// plan (conv2 launch: invalid argument).
+inline cudaError_t raise_smem_attr(const void* fn, size_t bytes) {
+  struct Rec {
+    const void* fn;
+    int dev;
+    size_t bytes;
+  };
+  static std::mutex mu;
+  static Rec recs[512];
+  static int n = 0;
+  if (bytes <= 48 * 1024) return cudaSuccess;
+  const int d = cur_device();
+  std::lock_guard<std::mutex> lock(mu);
+  int i = 0;
+  for (; i < n; ++i)
+    if (recs[i].fn == fn && recs[i].dev == d) break;
+  if (i < n && recs[i].bytes >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e != cudaSuccess) return e;
+  if (i < n)
+    recs[i].bytes = bytes;
+  else if (n < 512)
+    recs[n++] = Rec{fn, d, bytes};
+  return cudaSuccess;
 }
 
 // ---- bookkeeping -----------------------------------------------------------
@@ -157,6 +189,14 @@ void launch_sgd_pack(const Plan& P, float* const w[3], float* const mom[3], cons
 
 // ---- BN (+ReLU) around the quadratic conv (qd_bn.cu) ------------------------
 size_t bn_workspace_bytes(long long M, int C, int Jd);
+// the streaming D emission of the BN backward (qd_bnstream.cu): persistent CTAs,
+// bulk-copy staged tiles, bias gradients folded in-kernel
+bool bn_stream_ok(long long M, int C, int dtype);
+size_t bn_stream_rows();
+int bn_emit_stream(const Plan& P, const void* dz, const void* y, const void* a, const void* b, const float* gamma,
+                   const float* beta, const float* sm, const float* si, int relu, void* D, const float* dgamma,
+                   const float* dbeta, float* const db[3], float* bpart, cudaStream_t st);
+int tc_num_sms();
 int bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta, float* rm,
                float* rv, float momentum, float eps, int relu, int training, void* z, float* sm, float* si, char* ws,
                cudaStream_t st, const void* res = nullptr);

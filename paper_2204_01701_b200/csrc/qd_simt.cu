@@ -176,12 +176,7 @@ __global__ void __launch_bounds__(256) pack_conv_kernel(Plan P, const float* w0,
 
 template <typename T>
 static void launch_pack_conv(const Plan& P, const float* const w[3], T* out, size_t smem, cudaStream_t st) {
-  thread_local size_t attr[kMaxDev] = {};
-  const int dv = cur_device();
-  if (smem > 48 * 1024 && smem > attr[dv]) {
-    cudaFuncSetAttribute(pack_conv_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr[dv] = smem;
-  }
+  raise_smem_attr((const void*)pack_conv_kernel<T>, smem);
   pack_conv_kernel<T><<<P.nb * P.F + P.C, 256, smem, st>>>(P, w[0], w[1], w[2], out);
 }
 
@@ -386,13 +381,7 @@ static void launch_sgd_tiled(const Plan& P, float* const w[3], float* const mom[
                                                                     first, out);
     return;
   }
-  thread_local size_t attr_[kMaxDev] = {};
-  size_t& attr = attr_[cur_device()];
-  if (smem > 48 * 1024 && smem > attr) {
-    cudaFuncSetAttribute(sgd_pack_tiled_kernel<T, TF, TC, 0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = smem;
-  }
+  raise_smem_attr((const void*)sgd_pack_tiled_kernel<T, TF, TC, 0, true>, smem);
   sgd_pack_tiled_kernel<T, TF, TC, 0, true><<<blocks, QD_SGD_THREADS, smem, st>>>(P, w[0], w[1], w[2], mom[0], mom[1], mom[2],
                                                                   grad[0], grad[1], grad[2], lr, momentum, wd,
                                                                   first, out);
@@ -1166,12 +1155,7 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
     const int G = S >= 8 ? 8 : (S >= 4 ? 4 : (S >= 2 ? 2 : 1)), NJ = 8 / G;  // as in the kernel
     const int nwc = dW[0] ? (P.Jd + NJ - 1) / NJ * (P.Kf / P.K0) * (P.C / 64) : 0;
     const size_t smem = (size_t)8 * P.r * P.r * 17 * sizeof(float4);
-    thread_local size_t attr_[kMaxDev] = {};
-  size_t& attr = attr_[cur_device()];
-    if (smem > 48 * 1024 && smem > attr) {
-      cudaFuncSetAttribute(wfinish_conv_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-      attr = smem;
-    }
+    raise_smem_attr((const void*)wfinish_conv_kernel<0>, smem);  // r = 3 / 1 stay under 48 KB
     if (P.r == 3)
       wfinish_conv_kernel<9><<<nwc + nbb, 256, smem, st>>>(P, wpart, S, ws1, dW[0], dW[1], dW[2], bpart, SB, db[0],
                                                            db[1], db[2], nwc);

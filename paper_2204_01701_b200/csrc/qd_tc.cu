@@ -999,12 +999,7 @@ template <int EPI, int NB>
 static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const CUtensorMap& O0,
                        const CUtensorMap& O1, const CUtensorMap& O2, const ConvArgs& args, cudaStream_t st) {
   using Cfg = ConvCfg<EPI, NB>;
-  thread_local bool attr_[kMaxDev] = {};
-  bool& attr = attr_[cur_device()];
-  if (!attr) {
-    cudaFuncSetAttribute(conv_gemm_kernel<EPI, NB>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr = true;
-  }
+  raise_smem_attr((const void*)conv_gemm_kernel<EPI, NB>, Cfg::SMEM);
   const int nwork = args.cls ? 4 * args.cls_tiles : args.total_tiles * args.ksplit;
   int grid = nwork < g_num_sms ? nwork : g_num_sms;
   conv_gemm_kernel<EPI, NB><<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
@@ -1040,12 +1035,7 @@ template <int NBLK>
 static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUtensorMap& Dm, const WgArgs& args,
                         cudaStream_t st) {
   using Cfg = WgCfg<NBLK>;
-  thread_local bool attr_[kMaxDev] = {};
-  bool& attr = attr_[cur_device()];
-  if (!attr) {
-    cudaFuncSetAttribute(wgrad_kernel<NBLK>, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    attr = true;
-  }
+  raise_smem_attr((const void*)wgrad_kernel<NBLK>, Cfg::SMEM);
   int grid = args.mtiles * args.ntiles * args.splits;
   wgrad_kernel<NBLK><<<grid, 256, Cfg::SMEM, st>>>(X0, X1, Dm, args);
   count_launch(st, "wgrad_v1");

@@ -966,12 +966,7 @@ void set_conv2_cap(int pairs) { g_conv2_cap = pairs; }
 template <int EPI, int NB, int R>
 static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
                        cudaStream_t st) {
-  thread_local int attr_smem_[kMaxDev] = {};
-  int& attr_smem = attr_smem_[cur_device()];
-  if ((int)pl.smem > attr_smem) {
-    cudaFuncSetAttribute(conv2_kernel<EPI, NB, R>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    attr_smem = (int)pl.smem;
-  }
+  raise_smem_attr((const void*)conv2_kernel<EPI, NB, R>, pl.smem);
   // persistent grid: only as many pairs as can be co-resident (GPCs with an odd
   // number of free SMs cannot host a pair; a second wave would double the time)
   thread_local int maxc_[kMaxDev] = {};
@@ -986,8 +981,23 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   if (maxc > 0 && maxc < clusters) clusters = maxc;
   if (pl.g.total < clusters) clusters = pl.g.total;
   if (g_conv2_cap > 0 && g_conv2_cap < clusters) clusters = g_conv2_cap;
-  launch_pdl(conv2_kernel<EPI, NB, R>, dim3(2 * clusters), dim3(C2Threads<EPI, NB>::THREADS), pl.smem, st, A0, A1, B,
-             pl.g);
+  const cudaError_t le = launch_pdl(conv2_kernel<EPI, NB, R>, dim3(2 * clusters), dim3(C2Threads<EPI, NB>::THREADS),
+                                    pl.smem, st, A0, A1, B, pl.g);
+  if (le != cudaSuccess) {
+    cudaGetLastError();
+    cudaFuncAttributes fa;
+    memset(&fa, 0, sizeof(fa));
+    const cudaError_t fe = cudaFuncGetAttributes(&fa, conv2_kernel<EPI, NB, R>);
+    const int again = max_pair_clusters(conv2_kernel<EPI, NB, R>, C2Threads<EPI, NB>::THREADS, pl.smem);
+    int dev = -1;
+    cudaGetDevice(&dev);
+    return set_error(QD_ERR_CUDA,
+                     "conv2 launch (%d CTAs, %d threads, %zu B smem, maxc %d, tiles %d; function: "
+                     "max dyn smem %d static %zu (%s), clusters now %d, device %d): %s",
+                     2 * clusters, C2Threads<EPI, NB>::THREADS, pl.smem, maxc, (int)pl.g.total,
+                     fa.maxDynamicSharedSizeBytes, fa.sharedSizeBytes, cudaGetErrorString(fe), again, dev,
+                     cudaGetErrorString(le));
+  }
   count_launch(st, "conv2");
   return check_launch("conv2");
 }
@@ -1789,7 +1799,7 @@ static W3Plan w3_plan(const Plan& P) {
   int& maxc = maxc_[cur_device()];
   size_t& maxc_smem = maxc_smem_[cur_device()];
   if (maxc == 0 || maxc_smem != pl.smem) {
-    cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+    raise_smem_attr((const void*)wgrad3_kernel, pl.smem);
     maxc = max_pair_clusters(wgrad3_kernel, 256, pl.smem);
     maxc_smem = pl.smem;
   }
@@ -1856,9 +1866,7 @@ int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cuuint64_t d1[4] = {(cuuint64_t)(P.Jd - 64 * g.jsplit), (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
     if ((rc = c2_map(&Dm1, Dtail, 4, d1, bD))) return rc;
   }
-  // the attribute follows the plan being launched (w3_plan sets it for occupancy
-  // queries of other shapes too, so a cached "largest so far" could be stale)
-  cudaFuncSetAttribute(wgrad3_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
+  raise_smem_attr((const void*)wgrad3_kernel, pl.smem);
   const dim3 grid(2 * g.jtiles * g.ablocks * g.nsplit);
   if (g.fold_slot >= 0) {
     // in-kernel fold: cooperative launch (co-residency guaranteed by the driver);
@@ -1929,12 +1937,7 @@ int run_wgrad2(const Plan& P, const void* x0, const void* x1, const void* D, flo
     cuuint64_t d1[4] = {(cuuint64_t)(P.Jd - 64 * g.jsplit), (cuuint64_t)P.OW, (cuuint64_t)P.OH, (cuuint64_t)P.N};
     if ((rc = c2_map(&Dm1, Dtail, 4, d1, bD))) return rc;
   }
-  thread_local int attr_[kMaxDev] = {};
-  int& attr = attr_[cur_device()];
-  if ((int)pl.smem > attr) {
-    cudaFuncSetAttribute(wgrad2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl.smem);
-    attr = (int)pl.smem;
-  }
+  raise_smem_attr((const void*)wgrad2_kernel, pl.smem);
   launch_pdl(wgrad2_kernel, dim3(g.jtiles * g.ablocks * g.gstart[g.tgroups]), dim3(256), pl.smem, st, X0, X1, Dm,
              Dm1, g);
   count_launch(st, "wgrad2");

@@ -552,6 +552,48 @@ def test_quadconvbn_fused_matches_reference_bn(family, kind, relu):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("family,relu", [("proposed", True), ("proposed", False), ("t4", True),
+                                         ("first_order", True)])
+def test_streaming_emit_matches_register_emit(family, relu, monkeypatch):
+    """Large fused layers take the bulk-copy streaming D emission (bias gradients
+    folded in-kernel): the same D as the register-streaming emit bit for bit
+    (so dx and the weight gradients are identical), bias gradients to fp32
+    summation-order round-off."""
+    from paper_2204_01701_b200.bn import QuadConvBN
+    from paper_2204_01701_b200.nn import QuadConv2d
+    from paper_2204_01701_b200.spec import param_shapes
+    torch.manual_seed(5)
+    mod = QuadConvBN(QuadConv2d(64, 64, 3, 1, 1, family=family, device="cuda"), relu=relu)
+    with torch.no_grad():
+        mod.weight.uniform_(0.5, 1.5)
+        mod.bias.uniform_(-0.2, 0.2)
+        for r in param_shapes(mod.layer.spec):
+            if r.startswith("b"):
+                getattr(mod.layer, r).uniform_(-0.1, 0.1)
+    x0 = torch.randn(64, 64, 64, 64, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    gz = torch.randn(64, 64, 64, 64, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
+    out = []
+    for old in (False, True):
+        if old:
+            monkeypatch.setenv("QD_BN_OLD", "1")
+        x1 = x0.clone().requires_grad_(True)
+        for p in mod.parameters():
+            p.grad = None
+        mod(x1).backward(gz)
+        out.append((x1.grad, {n: p.grad.clone() for n, p in mod.named_parameters()}))
+    torch.cuda.synchronize()
+    assert torch.equal(out[0][0], out[1][0])
+    wmax = max(float(g.abs().max()) for n, g in out[0][1].items() if n.startswith("layer.W"))
+    for n, g in out[0][1].items():
+        if n in ("layer.bc", "layer.b"):  # exactly zero through BN: fold-order round-off only
+            assert float(g.abs().max()) <= 1e-3 * wmax and float(out[1][1][n].abs().max()) <= 1e-3 * wmax, n
+        elif n.startswith("layer.b"):  # bias: in-kernel fold vs bias_finish order
+            assert torch.allclose(g, out[1][1][n], rtol=1e-4, atol=1e-5 * float(g.abs().max())), n
+        else:
+            assert torch.equal(g, out[1][1][n]), n
+
+
+@pytest.mark.gpu
 def test_quadconvbn_add_relu_matches_composition():
     """ResNet block tail relu(BN(layer(x)) + res) as one fused node (residual add
     and ReLU on the BN apply pass, mask z > 0 in the backward) vs the module's
@@ -707,6 +749,62 @@ def test_bnact_matches_reference_bn(relu):
     assert Q.rel_err(m.weight.grad.double().cpu().numpy(), w2.grad.double().cpu().numpy()) <= 2e-2
     assert Q.rel_err(m.bias.grad.double().cpu().numpy(), b2.grad.double().cpu().numpy()) <= 2e-2
     assert int(m.num_batches_tracked) == 1
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,c,hw,dtype", [(2, 8, 3, torch.bfloat16), (4, 64, 9, torch.bfloat16),
+                                          (128, 64, 56, torch.bfloat16), (32, 512, 7, torch.bfloat16),
+                                          (3, 2048, 5, torch.bfloat16), (16, 256, 14, torch.float32),
+                                          (5, 96, 7, torch.bfloat16), (2, 4096, 2, torch.bfloat16),
+                                          (64, 64, 64, torch.float32)],
+                         ids=["tiny", "small", "r18_64x56", "r18_512x7", "c2048", "fp32", "c96", "c4096", "fp32_big"])
+def test_bn_kernels_vs_fp64_and_deterministic(n, c, hw, dtype):
+    """BN (+ReLU) forward / backward across shapes and dtypes (the large ones take
+    the streaming D emission, C = 96 / 4096 the scalar any-C kernels) against
+    the fp64 composition: z, dx, dgamma, dbeta, running statistics; and
+    bit-identical results on a second run (fixed-order folds)."""
+    from paper_2204_01701_b200.bn import BNAct2d
+    g = torch.Generator(device="cuda").manual_seed(n * c + hw)
+    x = (torch.randn(n, c, hw, hw, device="cuda", generator=g) * 2 + 0.5).to(dtype)
+    x = x.contiguous(memory_format=torch.channels_last)
+    gz = torch.randn(x.shape, device="cuda", generator=g).to(dtype)
+    m = BNAct2d(c, relu=True).cuda()
+    with torch.no_grad():
+        m.weight.uniform_(0.5, 1.5, generator=g)
+        m.bias.uniform_(-0.5, 0.5, generator=g)
+    rm0, rv0 = m.running_mean.clone(), m.running_var.clone()
+    runs = []
+    for _ in range(2):
+        with torch.no_grad():
+            m.running_mean.copy_(rm0)
+            m.running_var.copy_(rv0)
+        x1 = x.clone().requires_grad_(True)
+        m.weight.grad = m.bias.grad = None
+        z = m(x1)
+        z.backward(gz)
+        runs.append((z.detach(), x1.grad, m.weight.grad.clone(), m.bias.grad.clone(), m.running_mean.clone(),
+                     m.running_var.clone()))
+    for a, b in zip(*runs):
+        assert torch.equal(a, b)
+    z, dx, dw, db, rm, rv = runs[0]
+    xd = x.double().requires_grad_(True)
+    wd = m.weight.detach().double().requires_grad_(True)
+    bd = m.bias.detach().double().requires_grad_(True)
+    mean = xd.mean(dim=(0, 2, 3))
+    var = xd.var(dim=(0, 2, 3), unbiased=False)
+    t = wd.view(1, -1, 1, 1) * (xd - mean.view(1, -1, 1, 1)) * torch.rsqrt(var + 1e-5).view(1, -1, 1, 1) + \
+        bd.view(1, -1, 1, 1)
+    mask = (z > 0).double()  # the device's own ReLU mask (ties at 0 go either way)
+    zr = t * mask
+    zr.backward(gz.double())
+    tol = 2e-2 if dtype == torch.bfloat16 else 1e-4
+    rel = lambda a, b: float((a.double() - b.double()).norm() / b.double().norm().clamp_min(1e-30))  # noqa
+    assert rel(z, zr.detach()) <= (1e-2 if dtype == torch.bfloat16 else 1e-5)
+    assert rel(dx, xd.grad) <= tol, rel(dx, xd.grad)
+    assert rel(dw, wd.grad) <= tol, rel(dw, wd.grad)
+    assert rel(db, bd.grad) <= tol, rel(db, bd.grad)
+    assert torch.allclose(rm.double(), 0.9 * rm0.double() + 0.1 * mean.detach(), rtol=1e-4, atol=1e-5)
+    assert torch.allclose(rv.double(), 0.9 * rv0.double() + 0.1 * var.detach(), rtol=1e-4, atol=1e-5)
 
 
 @pytest.mark.gpu
