@@ -628,39 +628,51 @@ __global__ void __launch_bounds__(256) bn_reduce_kernel(long long M, int C, cons
   }
 }
 
-// fold the S x (2, C) partials: block = 32 channels x both sums (64 columns) x 16
-// split groups; group g sums splits g, g+16, ... in order, then one thread per
-// column adds the 16 group totals in order (deterministic, ~S/16 loads deep)
+// fold the S x (2, C) partials: block = 8 channels x both sums (16 columns) x 64
+// row groups; group g sums rows g, g + 64, ... in order (~S/64 <= 10 loads, all
+// issued before use: the fold is L2-latency bound, and 32 channels x 16 groups
+// took five dependent rounds, ~10 us per finalize), then 8 threads per column
+// add 8 group totals each and one adds those 8, in order (deterministic).
+constexpr int kFoldCh = 8;
 __device__ __forceinline__ bool bn_fold2(int C, int S, const float* part, float& s1, float& s2) {
-  __shared__ float red[16][65];
-  const int col = threadIdx.x % 64, grp = threadIdx.x / 64;
-  const int k = col / 32, c = blockIdx.x * 32 + col % 32;
-  // eight independent chains per thread (8 partial loads in flight: the fold
-  // is L2-latency bound -- two chains took ~7 us for S ~ 600), combined in order
-  float a[8];
-#pragma unroll
-  for (int u = 0; u < 8; ++u) a[u] = 0.f;
+  __shared__ float red[64][2 * kFoldCh + 1];
+  __shared__ float red8[8][2 * kFoldCh + 1];
+  const int col = threadIdx.x % (2 * kFoldCh), grp = threadIdx.x / (2 * kFoldCh);
+  const int k = col / kFoldCh, c = blockIdx.x * kFoldCh + col % kFoldCh;
+  float acc = 0.f;
   if (c < C) {
     const float* p = part + (size_t)k * C + c;
     const size_t step = (size_t)2 * C;
     int sp = grp;
-    for (; sp + 7 * 16 < S; sp += 8 * 16) {
+    for (; sp + 7 * 64 < S; sp += 8 * 64) {
       float v[8];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) v[u] = p[(size_t)(sp + 16 * u) * step];
+      for (int u = 0; u < 8; ++u) v[u] = p[(size_t)(sp + 64 * u) * step];
 #pragma unroll
-      for (int u = 0; u < 8; ++u) a[u] += v[u];
+      for (int u = 0; u < 8; ++u) acc += v[u];
     }
-    for (; sp < S; sp += 16) a[0] += p[(size_t)sp * step];
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = sp + 64 * u < S ? p[(size_t)(sp + 64 * u) * step] : 0.f;
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
   }
-  red[grp][col] = ((a[0] + a[1]) + (a[2] + a[3])) + ((a[4] + a[5]) + (a[6] + a[7]));
+  red[grp][col] = acc;
   __syncthreads();
-  if (grp != 0 || col >= 32 || c >= C) return false;
+  if (grp < 8) {
+    float t = 0.f;
+#pragma unroll
+    for (int g = 0; g < 8; ++g) t += red[grp * 8 + g][col];
+    red8[grp][col] = t;
+  }
+  __syncthreads();
+  if (threadIdx.x >= kFoldCh || blockIdx.x * kFoldCh + (int)threadIdx.x >= C) return false;
   s1 = 0.f;
   s2 = 0.f;
-  for (int g = 0; g < 16; ++g) {
-    s1 += red[g][col];
-    s2 += red[g][col + 32];
+#pragma unroll
+  for (int g = 0; g < 8; ++g) {
+    s1 += red8[g][threadIdx.x];
+    s2 += red8[g][threadIdx.x + kFoldCh];
   }
   return true;
 }
@@ -673,7 +685,7 @@ __global__ void __launch_bounds__(1024) bn_stats_finalize(long long M, int C, in
   ptx::pdl_launch();
   float s1, s2;
   if (!bn_fold2(C, S, part, s1, s2)) return;
-  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.x * kFoldCh + threadIdx.x;
   const float inv_m = 1.f / (float)M;
   const float dm = s1 * inv_m;
   float var = s2 * inv_m - dm * dm;  // biased (tensor.py:444)
@@ -705,7 +717,7 @@ __global__ void __launch_bounds__(1024) bn_grad_finalize(int C, int S, const flo
   ptx::pdl_launch();
   float s1, s2;
   if (!bn_fold2(C, S, part, s1, s2)) return;
-  const int c = blockIdx.x * 32 + threadIdx.x;
+  const int c = blockIdx.x * kFoldCh + threadIdx.x;
   dbeta[c] = s1;
   dgamma[c] = s2;
 }
@@ -796,7 +808,7 @@ static int bn_forward_t(long long M, int C, const T* y, const float* gamma, cons
     else
       bn_reduce_kernel<T, 0><<<S, 256, 0, st>>>(M, C, y, nullptr, nullptr, nullptr, nullptr, nullptr, 0, part);
     count_launch(st, "bn_stats");
-    launch_pdl(bn_stats_finalize<T>, dim3((C + 31) / 32), dim3(1024), 0, st, M, C, S, y, (const float*)part, eps,
+    launch_pdl(bn_stats_finalize<T>, dim3((C + kFoldCh - 1) / kFoldCh), dim3(1024), 0, st, M, C, S, y, (const float*)part, eps,
                momentum, 1, rm, rv, sm, si);
     count_launch(st, "bn_stats_finalize");
   }
@@ -829,7 +841,8 @@ static int bn_backward_D_t(const Plan& P, const T* dz, const T* y, const T* a, c
   else
     bn_reduce_kernel<T, 1><<<S, 256, 0, st>>>(M, C, y, dz, sm, si, gamma, beta, relu, part);
   count_launch(st, "bn_bwd_reduce");
-  launch_pdl(bn_grad_finalize, dim3((C + 31) / 32), dim3(1024), 0, st, C, S, (const float*)part, dgamma, dbeta);
+  launch_pdl(bn_grad_finalize, dim3((C + kFoldCh - 1) / kFoldCh), dim3(1024), 0, st, C, S, (const float*)part, dgamma,
+             dbeta);
   count_launch(st, "bn_bwd_finalize");
   if (bn_stream_ok(M, C, P.dtype))  // qd_bnstream.cu: bulk-copy streaming emit, bias folded in-kernel
     return bn_emit_stream(P, dz, y, a, b, gamma, beta, sm, si, relu, D, dgamma, dbeta, db, bpart, st);
