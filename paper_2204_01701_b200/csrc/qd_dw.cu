@@ -15,33 +15,9 @@
 //            pixel ranges folded in a fixed order (deterministic).
 #include <stdio.h>
 #include "qd_kernels.h"
+#include "qd_dw.cuh"
 
 namespace qd {
-
-// role table: which D block and which input (x or x*x) each weight role uses
-struct DwFam {
-  int nroles;
-  int din[3];  // D block of role r (backward)
-  int sq[3];   // role r reads x*x
-};
-__host__ __device__ inline DwFam dw_fam(int family) {
-  DwFam f = {1, {0, 0, 0}, {0, 0, 0}};
-  switch (family) {
-    case QD_FAM_T2: f.sq[0] = 1; break;
-    case QD_FAM_T4: f.nroles = 2; f.din[1] = 1; break;
-    case QD_FAM_PROPOSED: f.nroles = 3; f.din[1] = 1; f.din[2] = 2; break;
-    case QD_FAM_T2_LINEAR: f.nroles = 2; f.sq[0] = 1; break;  // Wa on x*x, Wc on x, both with D = g
-    case QD_FAM_T2AND4: f.nroles = 3; f.din[1] = 1; f.din[2] = 2; f.sq[2] = 1; break;
-    default: break;  // first_order, t3 (D = 2 g a)
-  }
-  return f;
-}
-
-struct DwArgs {
-  int family, N, C, H, W, OH, OW, r, s, p;
-  long long Min, Mout;
-  int Jd;
-};
 
 static DwArgs dw_args(const Plan& P) {
   DwArgs a;
@@ -450,7 +426,15 @@ __global__ void dw_wgrad_finish_kernel(int nrc, int S, const float* part, int rr
   const int id = blockIdx.x * blockDim.x + threadIdx.x;
   if (id >= nrc) return;
   float acc = 0.f;
-  for (int s = 0; s < S; ++s) acc += part[(size_t)s * nrc + id];
+  int s = 0;
+  for (; s + 8 <= S; s += 8) {  // eight rows in flight, added in row order
+    float v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = part[(size_t)(s + u) * nrc + id];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) acc += v[u];
+  }
+  for (; s < S; ++s) acc += part[(size_t)s * nrc + id];
   const int c = id % C, rt = id / C, tap = rt % rr, ro = rt / rr;
   float* dst = ro == 0 ? w0 : (ro == 1 ? w1 : w2);
   if (dst) dst[(size_t)c * rr + tap] = acc;  // reference layout (C, r, r)
@@ -488,6 +472,7 @@ static void dw_smem_attr(K kernel, size_t smem) {
 }
 
 int dw_wgrad_split(const Plan& P) {
+  if (dw_tile_ok(P)) return dw_tile_wgrad_split(P);
   if (dw_vec(P)) {  // grid (taps, ranges) ~ 4 blocks per SM
     const int rr = P.r * P.r;
     long long S = (4LL * 148 + rr - 1) / rr;
@@ -509,6 +494,7 @@ template <typename T>
 static int dw_forward_t(const Plan& P, const T* x, const float* Wp, const float* const bias[3], T* y, T* a, T* b,
                         cudaStream_t st) {
   DwArgs A = dw_args(P);
+  if (dw_tile_ok(P)) return dw_tile_forward<T>(P, A, x, Wp, bias, y, a, b, 0, st);
   if (dw_vec(P)) {
     dw_smem_attr(dw_fwd_vec_kernel<T>, dw_wsmem(P));
     dw_fwd_vec_kernel<T><<<dw_grid(P.Mout * (P.C / 8)), 256, dw_wsmem(P), st>>>(A, x, Wp, bias[0], bias[1], bias[2], y,
@@ -537,7 +523,10 @@ static int dw_backward_t(const Plan& P, const T* x, const float* Wp, const T* a,
   if (P.family == QD_FAM_T3) {
     T* Dw = (T*)(ws + L.off_D);
     const float* nob[3] = {nullptr, nullptr, nullptr};
-    if (dw_vec(P)) {
+    if (dw_tile_ok(P)) {
+      int rc = dw_tile_forward<T>(P, A, x, Wp, nob, Dw, nullptr, nullptr, 1, st);
+      if (rc) return rc;
+    } else if (dw_vec(P)) {
       dw_smem_attr(dw_fwd_vec_kernel<T>, dw_wsmem(P));
       dw_fwd_vec_kernel<T><<<dw_grid(P.Mout * (P.C / 8)), 256, dw_wsmem(P), st>>>(A, x, Wp, nob[0], nob[1], nob[2], Dw,
                                                                                  nullptr, nullptr, 1);
@@ -545,7 +534,7 @@ static int dw_backward_t(const Plan& P, const T* x, const float* Wp, const T* a,
     else
       dw_fwd_kernel<T><<<dw_grid(P.Mout * P.C), 256, 0, st>>>(A, x, Wp, nob[0], nob[1], nob[2], Dw, nullptr,
                                                               nullptr, 1);
-    count_launch(st, "dw_fwd_plain");
+    if (!dw_tile_ok(P)) count_launch(st, "dw_fwd_plain");
     launch_t3_prologue(P, dy, Dw, false, Dw, st);
     D = Dw;
   } else {
@@ -555,6 +544,19 @@ static int dw_backward_t(const Plan& P, const T* x, const float* Wp, const T* a,
     else
       launch_bwd_prologue(P, dy, a, b, (void*)D, bpart, L.bs_split, st);
     if (db[0]) launch_bias_finish(P, bpart, L.bs_split, db, st);
+  }
+  if (dw_tile_ok(P)) {  // tiled wgrad + dgrad, then the fixed-order fold of the wgrad rows
+    const DwFam fm = dw_fam(P.family);
+    const int nrc = fm.nroles * P.r * P.r * P.C;
+    float* part = dW[0] ? (float*)(ws + L.off_WG) : nullptr;
+    int rc = dw_tile_backward<T>(P, A, x, D, Wp, dx, part, L.wg_split, st);
+    if (rc) return rc;
+    if (part) {
+      dw_wgrad_finish_kernel<<<(nrc + 255) / 256, 256, 0, st>>>(nrc, L.wg_split, part, P.r * P.r * P.C, dW[0], dW[1],
+                                                                dW[2], P.r * P.r, P.C);
+      count_launch(st, "dw_wgrad_finish");
+    }
+    return check_launch("dwconv backward");
   }
   if (dW[0]) {
     const DwFam fm = dw_fam(P.family);

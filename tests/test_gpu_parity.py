@@ -414,7 +414,8 @@ def test_kernels_launch_counter():
     assert _lib.launch_count() > before
 
 
-# depth-wise kind: direct kernels (qd_path == 2), every family that allows it
+# depth-wise kind (qd_path == 2), every family that allows it: direct kernels and the
+# shared-memory tiled ones
 DW_CASES = [
     ("proposed", 4, 32, 14, 14, 3, 1, 1),
     ("proposed", 3, 24, 15, 13, 3, 2, 1),
@@ -424,12 +425,21 @@ DW_CASES = [
     ("t2_linear", 2, 16, 9, 9, 3, 1, 1),
     ("t2and4", 2, 16, 10, 10, 3, 2, 1),
     ("first_order", 2, 16, 9, 9, 3, 1, 1),
+    # shared-memory tiled kernels (r = 3, C % 32 == 0): tile edges, stride 2, pads 0 / 2
+    ("proposed", 2, 64, 19, 37, 3, 1, 1),
+    ("proposed", 2, 32, 17, 35, 3, 2, 1),
+    ("t4", 2, 32, 9, 20, 3, 1, 1),
+    ("t2", 2, 32, 11, 11, 3, 2, 1),
+    ("t3", 2, 32, 9, 9, 3, 1, 1),
+    ("t2_linear", 2, 32, 12, 18, 3, 1, 0),
+    ("t2and4", 2, 32, 10, 10, 3, 2, 1),
+    ("first_order", 2, 32, 9, 9, 3, 1, 2),
 ]
 
 
 @pytest.mark.gpu
 @pytest.mark.parametrize("dtype", [torch.float32, torch.bfloat16], ids=["fp32", "bf16"])
-@pytest.mark.parametrize("case", DW_CASES, ids=[f"{c[0]}-{c[2]}x{c[3]}-k{c[5]}s{c[6]}" for c in DW_CASES])
+@pytest.mark.parametrize("case", DW_CASES, ids=[f"{c[0]}-c{c[2]}-{c[3]}x{c[4]}-k{c[5]}s{c[6]}p{c[7]}" for c in DW_CASES])
 def test_dwconv_parity(case, dtype):
     fam, n, c, h, w, k, s, p = case
     x, P, g = Q.synthetic_layer(fam, "dwconv", n, c, c, h, w, k, s, p, seed=11, random_bias=True)
