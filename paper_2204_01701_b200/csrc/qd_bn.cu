@@ -120,7 +120,7 @@ __global__ void __launch_bounds__(256) bn_reduce_vec_kernel(long long M, int C, 
       }
     }
     long long r = r0 + lane;
-    constexpr int U = MODE == 0 ? 4 : 2;  // rows whose loads are issued before any use
+    constexpr int U = MODE == 0 ? 8 : 2;  // rows whose loads are issued before any use
     for (; r + (U - 1) * lanes < r1; r += U * lanes) {
       float v[U][8], gv[U][8];
 #pragma unroll
@@ -190,54 +190,82 @@ __global__ void __launch_bounds__(256) bn_reduce_vec_kernel(long long M, int C, 
 }
 
 // thread = (8-channel chunk q, row lane) with 256 % (C / 8) == 0: the chunk's
-// BN constants stay in registers and rows stride by the grid's lane count
-template <typename T>
-__global__ void __launch_bounds__(256) bn_apply_vec_kernel(long long rows, int C, const T* __restrict__ y,
-                                                           const float* mean, const float* invstd,
-                                                           const float* gamma, const float* beta, int relu,
-                                                           T* __restrict__ z, const T* __restrict__ res) {
+// BN constants stay in registers (packed fp32 pairs) and rows stride by the
+// grid's lane count; residual and ReLU are template parameters, so the
+// no-residual instantiation keeps only 4 rows x 16 B of loads in registers
+// (4 blocks per SM, one wave of a 4-per-SM grid)
+template <typename T, bool RES, bool RELU>
+__global__ void __launch_bounds__(256, 4) bn_apply_vec_kernel(long long rows, int C, const T* __restrict__ y,
+                                                              const float* mean, const float* invstd,
+                                                              const float* gamma, const float* beta,
+                                                              T* __restrict__ z, const T* __restrict__ res) {
   ptx::pdl_wait();  // predecessor outputs complete (PDL launch)
   ptx::pdl_launch();
   const int CQ = C / 8, lanes = 256 / CQ;
   const int q = threadIdx.x % CQ, c0 = q * 8;
-  float sc[8], sh[8];
+  float2 sc[4], sh[4];
 #pragma unroll
-  for (int e = 0; e < 8; ++e) {  // z = sc * y + sh
-    sc[e] = gamma[c0 + e] * invstd[c0 + e];
-    sh[e] = beta[c0 + e] - sc[e] * mean[c0 + e];
+  for (int h = 0; h < 4; ++h) {  // z = sc * y + sh (the backward's mask uses the same fmaf)
+    float a[2], b[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int c = c0 + 2 * h + u;
+      a[u] = gamma[c] * invstd[c];
+      b[u] = beta[c] - a[u] * mean[c];
+    }
+    sc[h] = make_float2(a[0], a[1]);
+    sh[h] = make_float2(b[0], b[1]);
   }
   const long long step = (long long)gridDim.x * lanes;
   long long r = (long long)blockIdx.x * lanes + threadIdx.x / CQ;
-  // main loop: 4 rows whose loads are all issued before any use (a guarded
-  // single-row loop keeps one load in flight per thread: ~2.4 TB/s)
+  auto emit = [&](long long rr, float (&v)[8], const float (&rv)[8]) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      float2 t = __ffma2_rn(sc[h], make_float2(v[2 * h], v[2 * h + 1]), sh[h]);
+      if (RES) t = __fadd2_rn(t, make_float2(rv[2 * h], rv[2 * h + 1]));
+      if (RELU) {
+        t.x = t.x < 0.f ? 0.f : t.x;
+        t.y = t.y < 0.f ? 0.f : t.y;
+      }
+      v[2 * h] = t.x;
+      v[2 * h + 1] = t.y;
+    }
+    BV<T>::st8(z + (size_t)rr * C + c0, v);
+  };
+  // main loop: 4 rows whose loads are all issued before any use
   for (; r + 3 * step < rows; r += 4 * step) {
     float v[4][8], rv[4][8];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       BV<T>::ld8(y + (size_t)(r + u * step) * C + c0, v[u]);
-      if (res) BV<T>::ld8(res + (size_t)(r + u * step) * C + c0, rv[u]);
+      if (RES) BV<T>::ld8(res + (size_t)(r + u * step) * C + c0, rv[u]);
     }
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const float t = fmaf(sc[e], v[u][e], sh[e]) + (res ? rv[u][e] : 0.f);
-        v[u][e] = (relu && t < 0.f) ? 0.f : t;
-      }
-      BV<T>::st8(z + (size_t)(r + u * step) * C + c0, v[u]);
-    }
+    for (int u = 0; u < 4; ++u) emit(r + u * step, v[u], rv[u]);
   }
   for (; r < rows; r += step) {
     float v[8], rv[8];
     BV<T>::ld8(y + (size_t)r * C + c0, v);
-    if (res) BV<T>::ld8(res + (size_t)r * C + c0, rv);
-#pragma unroll
-    for (int e = 0; e < 8; ++e) {
-      const float t = fmaf(sc[e], v[e], sh[e]) + (res ? rv[e] : 0.f);
-      v[e] = (relu && t < 0.f) ? 0.f : t;
-    }
-    BV<T>::st8(z + (size_t)r * C + c0, v);
+    if (RES) BV<T>::ld8(res + (size_t)r * C + c0, rv);
+    emit(r, v, rv);
   }
+}
+
+template <typename T>
+static void launch_apply_vec(long long M, int C, const T* y, const float* sm, const float* si, const float* gamma,
+                             const float* beta, int relu, T* z, const T* res, cudaStream_t st) {
+  long long g = ((M * C / 8) + 255) / 256;
+  g = (g + 3) / 4;  // each thread takes >= 4 rows (the unguarded batch)
+  const long long cap = 4LL * tc_num_sms();
+  if (g > cap) g = cap;
+#define QD_APPLY(R_, L_)                                                                                         \
+  launch_pdl(bn_apply_vec_kernel<T, R_, L_>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, sm, si, gamma, beta, z, \
+             res)
+  if (res)
+    relu ? QD_APPLY(true, true) : QD_APPLY(true, false);
+  else
+    relu ? QD_APPLY(false, true) : QD_APPLY(false, false);
+#undef QD_APPLY
 }
 
 template <typename T>
@@ -813,14 +841,13 @@ static int bn_forward_t(long long M, int C, const T* y, const float* gamma, cons
     count_launch(st, "bn_stats_finalize");
   }
   const long long n = M * C;
-  long long g = ((bn_vec(C) ? n / 8 : n) + 255) / 256;
-  if (bn_vec(C)) g = (g + 3) / 4;  // each thread takes >= 4 rows (the unguarded batch)
-  if (g > 148 * 8) g = 148 * 8;
-  if (bn_vec(C))
-    launch_pdl(bn_apply_vec_kernel<T>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, (const float*)sm, (const float*)si,
-               gamma, beta, relu, z, res);
-  else
+  if (bn_vec(C)) {
+    launch_apply_vec<T>(M, C, y, sm, si, gamma, beta, relu, z, res, st);
+  } else {
+    long long g = (n + 255) / 256;
+    if (g > 148 * 8) g = 148 * 8;
     bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z, res);
+  }
   count_launch(st, "bn_apply");
   return check_launch("bn forward");
 }
@@ -924,14 +951,13 @@ static int bn_forward_stats_t(long long M, int C, const T* y, const T* res, cons
              sm, si);
   count_launch(st, "bn_stats_merge");
   const long long n = M * C;
-  long long g = ((bn_vec(C) ? n / 8 : n) + 255) / 256;
-  if (bn_vec(C)) g = (g + 3) / 4;
-  if (g > 148 * 8) g = 148 * 8;
-  if (bn_vec(C))
-    launch_pdl(bn_apply_vec_kernel<T>, dim3((unsigned)g), dim3(256), 0, st, M, C, y, (const float*)sm, (const float*)si,
-               gamma, beta, relu, z, res);
-  else
+  if (bn_vec(C)) {
+    launch_apply_vec<T>(M, C, y, sm, si, gamma, beta, relu, z, res, st);
+  } else {
+    long long g = (n + 255) / 256;
+    if (g > 148 * 8) g = 148 * 8;
     bn_apply_kernel<T><<<(int)g, 256, 0, st>>>(n, C, y, sm, si, gamma, beta, relu, z, res);
+  }
   count_launch(st, "bn_apply");
   return check_launch("bn forward (epilogue statistics)");
 }
