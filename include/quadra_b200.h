@@ -104,7 +104,11 @@ int qd_pack_weights(const qd_desc* d, const float* const w[3], void* wpack,
  * in the running update). NHWC tensors of M = N*OH*OW rows and C channels.
  * Forward: z = relu?(gamma (y - mean) inv_std + beta); training computes the
  * batch statistics (save_mean / save_invstd out) and folds them into
- * run_mean / run_var; eval uses save_mean / save_invstd as given. */
+ * run_mean / run_var; eval uses save_mean / save_invstd as given.
+ * Workspace: qd_bn_workspace_bytes of caller memory, any content, one call at a
+ * time. Reductions are deterministic (fixed-order partial rows); the streaming
+ * D emission of large tensors folds its bias sums in-kernel with arrival
+ * counters from a library-owned device ring (1024 slots, re-armed by each use). */
 size_t qd_bn_workspace_bytes(long long M, int C, int Jd);
 int qd_bn_forward(long long M, int C, int dtype, const void* y, const float* gamma, const float* beta,
                   float* run_mean, float* run_var, float momentum, float eps, int relu, int training,
