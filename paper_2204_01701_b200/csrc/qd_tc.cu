@@ -1057,6 +1057,10 @@ static long long wgrad_split_for(long long tiles, long long ptiles, int sms) {
 
 static int wgrad_ntile_blocks(const Plan& P, long long ptiles) {
   const int nb = P.Jd / 64, mtiles = (P.Kf / 64 + 1) / 2, sms = tc_num_sms();
+  if (const char* e = getenv("QD_WG_NBLK")) {  // dev: pin the N tile (64-column blocks)
+    const int c = atoi(e);
+    if (c >= 1 && c <= 4 && nb % c == 0) return c;
+  }
   int best = 1;
   double best_eff = -1.0;
   for (int c = 4; c >= 1; --c) {
