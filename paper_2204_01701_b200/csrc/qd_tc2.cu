@@ -935,8 +935,13 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
       slots = KBtot;
       aslots = (int)(rest / halo);
       if (aslots > 4) aslots = 4;
-      const char* e = getenv("QD_ASLOTS");  // dev knob
-      if (e && atoi(e) >= 1 && atoi(e) < aslots) aslots = atoi(e);
+      // two halo buffers: the smaller footprint lets the next PDL-launched kernel's
+      // CTAs land beside this one's tail (C2 step 115.7 -> 113.0 us, t4 64@56 +5%;
+      // neutral on the other C5 shapes and both nets; tools/aslot_ab.sh)
+      int want = 2;
+      const char* e = getenv("QD_ASLOTS");  // dev knob: 1..4
+      if (e && atoi(e) >= 1) want = atoi(e);
+      if (want < aslots) aslots = want;
     }
   }
   if (!resident) {
