@@ -935,11 +935,12 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
       slots = KBtot;
       aslots = (int)(rest / halo);
       if (aslots > 4) aslots = 4;
-      // two halo buffers: the smaller footprint lets the next PDL-launched kernel's
-      // CTAs land beside this one's tail (C2 step 115.7 -> 113.0 us, t4 64@56 +5%;
-      // neutral on the other C5 shapes and both nets; tools/aslot_ab.sh)
-      int want = 2;
-      const char* e = getenv("QD_ASLOTS");  // dev knob: 1..4
+      // fprop: two halo buffers -- the smaller footprint lets the next PDL-launched
+      // kernel's CTAs land beside this one's tail (C2 step 115.7 -> 113.0 us, t4
+      // 64@56 +5%; neutral on the other C5 shapes and both nets; tools/aslot_ab.sh);
+      // dgrad: four (112.1 us)
+      int want = NOUT == 3 ? 2 : 4;
+      const char* e = getenv(NOUT == 3 ? "QD_ASLOTS" : "QD_ASLOTS_DG");  // dev knobs: 1..4 (fprop / other)
       if (e && atoi(e) >= 1) want = atoi(e);
       if (want < aslots) aslots = want;
     }
