@@ -267,12 +267,21 @@ int wgrad3_split(const Plan& P);
 int run_wgrad3(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
                cudaStream_t st, const void* Dtail = nullptr, int jsplit = 0, float* const* dW = nullptr,
                const float* bpart = nullptr, int SB = 0, float* const* db = nullptr, bool* folded = nullptr);
+// operand transform of the conv2 A operand (C2Args::xf): mode 1 = x * x for the
+// first K half (x = the layer input), 2 = the dgrad's D blocks dy * b, dy * a
+// (x = dy; cs = channels of dy / a / b, fb = F / 64)
+struct C2Xform {
+  int mode, cs, fb;
+  const void* x;
+  const void* a;
+  const void* b;
+};
 // v2 stride-1 conv on CTA pairs (qd_tc2.cu); QD_ERR_UNSUPPORTED if the shape does not fit
 int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win, int Hin, int N, int OWg, int OHg,
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
               const void* xres, cudaStream_t st, int ss = 1, const void* a_tail = nullptr, int csplit = 0,
-              int pdl_wait = 1, int f32out = 0, float* stats = nullptr);
+              int pdl_wait = 1, int f32out = 0, float* stats = nullptr, const C2Xform* xf = nullptr);
 int conv2_stat_rows(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,
                     int tiles_nn, int Cout, int nbias);
 bool conv2_fits(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe, int r, int dual, int nbk, int nout,

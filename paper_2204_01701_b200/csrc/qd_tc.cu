@@ -685,6 +685,170 @@ __global__ void __launch_bounds__(256, 1)
   }
 }
 
+// K4 v1 on CTA pairs. The v1 wgrad is bound by TMA delivery (every stage brings
+// 16 KB of x boxes and NBLK x 8 KB of D boxes for 128 x 64 NBLK x 64 MACs; the
+// chip-wide TMA throughput, ~6300 B/cycle, caps it at ~30% tensor-pipe use on the
+// 512-channel layers). The two CTAs of a cluster take M tiles 2m and 2m + 1 of the
+// same N tile and pixel range and issue M = 256 MMAs (cta_group::2): each holds its
+// own x boxes but only HALF of the D boxes (its NBLK / 2 64-column blocks), so every
+// D byte reaches one SM instead of two: 16 + 4 NBLK KB per SM and stage instead of
+// 16 + 8 NBLK. Same partial-slot output as wgrad_kernel.
+template <int NBLK>
+struct WpCfg {
+  static constexpr int HB = NBLK / 2;  // D boxes per CTA
+  static constexpr int A_BYTES = 2 * 8192;
+  static constexpr int B_BYTES = HB * 8192;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int S0 = (220 * 1024 - 2048) / STAGE;
+  static constexpr int STAGES = S0 > 8 ? 8 : S0;
+  static constexpr int SMEM = 1024 + STAGES * STAGE + 1024;
+  static constexpr int TCOLS = NBLK * 64 <= 128 ? 128 : 256;
+};
+
+template <int NBLK>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    wgrad_pair_kernel(const __grid_constant__ CUtensorMap mapX0, const __grid_constant__ CUtensorMap mapX1,
+                      const __grid_constant__ CUtensorMap mapD, const WgArgs args) {
+  using Cfg = WpCfg<NBLK>;
+  constexpr int STAGES = Cfg::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint8_t* sA = smem;
+  uint8_t* sB = smem + STAGES * Cfg::A_BYTES;
+  uint64_t* full = (uint64_t*)(sB + STAGES * Cfg::B_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = (uint32_t*)(done + 1);
+
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = ptx::cluster_rank();
+  int b = blockIdx.x >> 1;
+  const int ntile = b % args.ntiles;
+  b /= args.ntiles;
+  const int mpairs = (args.mtiles + 1) / 2;
+  const int mpair = b % mpairs;
+  const int split = b / mpairs;
+  const int mtile = 2 * mpair + (int)rank;
+  const int p_beg = (int)((long long)split * args.ptiles / args.splits);
+  const int p_end = (int)((long long)(split + 1) * args.ptiles / args.splits);
+  // 64-row k-blocks of x this CTA loads (a missing second M tile loads none: its
+  // TMEM rows are computed from stale smem and never stored)
+  auto n_a = [&](int mt) { return mt >= args.mtiles ? 0 : ((2 * mt + 1 < args.nkb) ? 2 : 1); };
+  const int nA = n_a(mtile);
+
+  if (threadIdx.x == 0) {
+    ptx::prefetch_tmap(&mapX0);
+    ptx::prefetch_tmap(&mapX1);
+    ptx::prefetch_tmap(&mapD);
+    for (int i = 0; i < STAGES; ++i) {
+      ptx::mbar_init(&full[i], 1);
+      ptx::mbar_init(&empty[i], 1);
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_barrier_init();
+  }
+  if (warp == 2) ptx::tmem_alloc2(tmem_slot, Cfg::TCOLS);
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // both CTAs' boxes complete on CTA0's full barrier; CTA0 expects the pair's bytes
+      int stage = 0;
+      uint32_t phase = 0;
+      const uint32_t bytes = (uint32_t)((n_a(2 * mpair) + n_a(2 * mpair + 1)) * 8192 + 2 * Cfg::B_BYTES);
+      for (int pt = p_beg; pt < p_end; ++pt) {
+        int tw = pt % args.pt_w, th = (pt / args.pt_w) % args.pt_h, tn = pt / (args.pt_w * args.pt_h);
+        int w0 = tw * args.pb_w, h0 = th * args.pb_h, n0 = tn * args.pb_n;
+        ptx::mbar_wait(&empty[stage], phase ^ 1);
+        if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+        const uint32_t fb = ptx::peer0(&full[stage]);
+        for (int a = 0; a < nA; ++a) {
+          int kb = 2 * mtile + a;
+          int half = kb / args.kb_half, kk = kb % args.kb_half;
+          int tap = kk / args.cblks, cb = kk % args.cblks;
+          int ey = tap / args.r, ex = tap % args.r;
+          ptx::tma4_cg2(half ? &mapX1 : &mapX0, fb, sA + stage * Cfg::A_BYTES + a * 8192, cb * 64,
+                        args.sstride * w0 + ex - args.pad, args.sstride * h0 + ey - args.pad, n0);
+        }
+#pragma unroll
+        for (int i = 0; i < Cfg::HB; ++i)
+          ptx::tma4_cg2(&mapD, fb, sB + stage * Cfg::B_BYTES + i * 8192, (ntile * NBLK + (int)rank * Cfg::HB + i) * 64,
+                        w0, h0, n0);
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+    }
+  } else if (warp == 1) {
+    if (rank == 0) {
+      // M = 256 over the pair (CTA r: rows of M tile 2m + r), N = NBLK x 64 (CTA r
+      // holds columns [r N/2, (r+1) N/2) of B); commits reach both CTAs' barriers
+      constexpr uint32_t IDESC = ptx::idesc_bf16(256, NBLK * 64, true, true);
+      constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
+      const bool leader = ptx::elect_one();
+      const uint32_t a_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sA), 8192);
+      const uint32_t b_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sB), 8192);
+      int stage = 0;
+      uint32_t phase = 0;
+      uint32_t accum = 0;
+      for (int pt = p_beg; pt < p_end; ++pt) {
+        ptx::mbar_wait(&full[stage], phase);
+        ptx::tc_fence_after();
+        const uint32_t a_lo = a_lo0 + stage * (Cfg::A_BYTES >> 4);
+        const uint32_t b_lo = b_lo0 + stage * (Cfg::B_BYTES >> 4);
+        if (leader) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            ptx::mma_cg2(tmem_base, ptx::mk_desc(DHI, a_lo + 128 * k), ptx::mk_desc(DHI, b_lo + 128 * k), IDESC,
+                         accum | (uint32_t)k);
+          ptx::commit_mc(&empty[stage]);
+        }
+        accum = 1;
+        __syncwarp();
+        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+      }
+      if (leader) ptx::commit_mc(done);
+      __syncwarp();
+    }
+  } else if (warp >= 4) {
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int kglob = mtile * 128 + row;
+    const bool has_work = p_end > p_beg;
+    if (has_work) {
+      ptx::mbar_wait(done, 0);
+      ptx::tc_fence_after();
+    }
+    const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16);
+    float* dst = args.part + (size_t)split * args.Jd * args.Kf;
+#pragma unroll 1
+    for (int c = 0; c < NBLK * 64; c += 16) {
+      float v[16];
+      if (has_work) {
+        ptx::tmem_ld16(tbase + c, v);
+        ptx::tmem_wait_ld();
+      } else {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+      }
+      if (kglob < args.Kf && row < nA * 64) {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          int j = ntile * NBLK * 64 + c + e;
+          dst[(size_t)j * args.Kf + kglob] = v[e];
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  ptx::cluster_sync();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc2(tmem_base, Cfg::TCOLS);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // vectorised backward prologue for the tcgen05 path:
 // D = [dy*b | dy*a | dy] (proposed) / [dy*b | dy*a] (t4) in bf16 plus
@@ -1041,6 +1205,16 @@ static int launch_wgrad(const CUtensorMap& X0, const CUtensorMap& X1, const CUte
   count_launch(st, "wgrad_v1");
   return check_launch("wgrad");
 }
+template <int NBLK>
+static int launch_wgrad_pair(const CUtensorMap& X0, const CUtensorMap& X1, const CUtensorMap& Dm,
+                             const WgArgs& args, cudaStream_t st) {
+  using Cfg = WpCfg<NBLK>;
+  raise_smem_attr((const void*)wgrad_pair_kernel<NBLK>, Cfg::SMEM);
+  int grid = 2 * ((args.mtiles + 1) / 2) * args.ntiles * args.splits;
+  wgrad_pair_kernel<NBLK><<<grid, 256, Cfg::SMEM, st>>>(X0, X1, Dm, args);
+  count_launch(st, "wgrad_v1");
+  return check_launch("wgrad pair");
+}
 
 // v1 wgrad shape: N tile (64-column blocks: 4 / 3 / 2 / 1 dividing Jd) and the
 // pixel split S. One CTA per SM, so the grid (tiles x S) should fill whole waves:
@@ -1080,6 +1254,43 @@ static long long wgrad_ptiles(const Plan& P) {
   return (long long)pb.tw * pb.th * pb.tn;
 }
 
+// v1 wgrad launch shape: CTA pairs or single CTAs, the N tile (64-column blocks)
+// and the pixel split S. Pairs (wgrad_pair_kernel) need an even block count and
+// two M tiles; they are taken when a small cost model says so: per tile, MACs /
+// (per-SM MMA rate x TMA factor) with the factor min(1, 7 / operand KB per
+// 64-pixel k-step and 8K MACs) -- the single kernel at N = 256 delivers 48 KB per
+// 16 x 8K MACs, the pair 32 -- times whole waves of the grid, plus the fold's
+// S x Jd x Kf x 8 bytes of partial traffic. Only with QD_WPAIR=1.
+struct WgShape { int pair, nblk, S; };
+static WgShape wgrad_v1_shape(const Plan& P) {
+  const long long ptiles = wgrad_ptiles(P);
+  const int sms = tc_num_sms(), nb = P.Jd / 64, mtiles = (P.Kf / 64 + 1) / 2;
+  WgShape s{0, wgrad_ntile_blocks(P, ptiles), 1};
+  s.S = (int)wgrad_split_for((long long)mtiles * (nb / s.nblk), ptiles, sms);
+  const char* on = getenv("QD_WPAIR");  // opt-in: measured no faster with its fold
+  if (!(on && atoi(on)) || mtiles < 2 || nb % 2) return s;
+  const double px = (double)ptiles * 64;
+  auto cost = [&](int pair, int c, int S) {
+    const long long units = (long long)(pair ? (mtiles + 1) / 2 : mtiles) * (nb / c) * S;
+    const int slots = pair ? sms / 2 : sms;
+    const long long waves = (units + slots - 1) / slots;
+    const double kb = pair ? (16.0 + 4.0 * c) / c : (16.0 + 8.0 * c) / c;  // KB per k-step and 8K MACs
+    const double rate = kb > 7.0 ? 7.0 / kb : 1.0;
+    const double tile_us = 128.0 * 64 * c * (px / S) / 5.5e6 / rate;
+    const double fold_us = (double)S * P.Jd * P.Kf * 8 / 6.0e6;
+    return waves * tile_us + fold_us;
+  };
+  double best = cost(0, s.nblk, s.S);
+  for (int c = 4; c >= 2; c -= 2) {
+    if (nb % c) continue;
+    for (int S = 1; S <= 4 && ptiles / S >= 4; ++S) {
+      const double t = cost(1, c, S);
+      if (t < best * 0.97) { best = t; s = WgShape{1, c, S}; }
+    }
+  }
+  return s;
+}
+
 int tc_wgrad_split(const Plan& P) {
   if (!(P.flags & QD_FLAG_TC_V1)) {
     int s3 = wgrad3_split(P);
@@ -1087,10 +1298,7 @@ int tc_wgrad_split(const Plan& P) {
     int s2 = wgrad2_split(P);
     if (s2 > 0) return s2;
   }
-  const long long ptiles = wgrad_ptiles(P);
-  const int mtiles = (P.Kf / 64 + 1) / 2;
-  const int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P, ptiles);
-  return (int)wgrad_split_for((long long)mtiles * ntiles, ptiles, tc_num_sms());
+  return wgrad_v1_shape(P).S;
 }
 
 // generic conv-GEMM launch (fprop or dgrad)
@@ -1257,12 +1465,19 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
                void* b, char* ws, const Workspace& L, cudaStream_t st, float* stats) {
   const void* a0 = x;
   const void* a1 = nullptr;
-  if (P.sq) {
+  // squared-input families: x * x into the workspace by one vectorised pass, the
+  // GEMM reads it as its first K half. QD_XFS=1 (measured slower):
+  // the conv2 kernels square x in their transform warps instead (C2Args::xf = 1)
+  const bool xfs = P.sq && getenv("QD_XFS") && atoi(getenv("QD_XFS"));
+  const C2Xform xsq{xfs ? 1 : 0, P.C, 0, x, nullptr, nullptr};
+  auto square_x = [&]() {
+    if (!P.sq) return;
     void* xs = ws + L.off_XS;
     launch_square(P, x, xs, st);
     a0 = xs;
-    if (P.sq == 2) a1 = x;
-  }
+  };
+  if (P.sq == 2) a1 = x;
+  if (P.sq && !xfs) square_x();
   const float* nb3[3] = {bias[0], bias[1], bias[2]};
   GemmCfg c = fprop_cfg(P);
   if (c.nbias == 0) nb3[0] = nb3[1] = nb3[2] = nullptr;
@@ -1282,6 +1497,7 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
   }
   if (P.family == QD_FAM_T3) {
     // y = (Wa x)^2: the plain GEMM, then the square in place
+    if (xfs) square_x();
     int rc = tc_fprop_plain(P, a0, a1, wpack, y, st);
     if (rc) return rc;
     launch_square_out(P, y, st);
@@ -1296,16 +1512,18 @@ int tc_forward(const Plan& P, const void* x, const void* wpack, const float* con
     // stride-1 grid, epilogue keeps the even positions
     Plan P1 = stride1_plan(P);
     return run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P1.OW, P1.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
-                     P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st, 2);
+                     P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st, 2,
+                     nullptr, 0, 1, 0, nullptr, &xsq);
   }
   if (dev_skip("fprop")) return QD_OK;
   if (!(P.flags & QD_FLAG_TC_V1)) {
     int rc2 = run_conv2(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
                         P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st,
-                        1, nullptr, 0, 1, 0, stats);
+                        1, nullptr, 0, 1, 0, stats, &xsq);
     if (rc2 != QD_ERR_UNSUPPORTED) return rc2;
   }
   if (stats) return set_error(QD_ERR_UNSUPPORTED, "BN statistics: the conv2 forward does not fit this layer");
+  if (xfs) square_x();
   return run_conv(c.epi, c.nbk, a0, a1, P.C, P.W, P.H, P.N, P.OW, P.OH, P.p, P.r, P.sq == 2 ? 1 : 0, wpack,
                   P.nb * P.F, P.Kf, c.b_rs_tile, 64, c.tiles_nn, c.out_c_tile, y, a, b, P.F, nb3, nullptr, st,
                   (float*)(ws + L.off_SK), L.sz_SK);
@@ -1344,6 +1562,39 @@ static void join_side(cudaStream_t st, cudaStream_t side) {
   cudaStreamWaitEvent(st, s.join, 0);
 }
 
+// one v1 wgrad product (x taps from x0 / x1 by K half, D) into `splits` fp32
+// partial slots at `part`; single CTAs or CTA pairs per wgrad_v1_shape
+static int run_wgrad_v1(const Plan& P, const void* x0, const void* x1, const void* D, float* part, int splits,
+                        cudaStream_t st) {
+  Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
+  CUtensorMap X0, X1, Dm;
+  int rc;
+  if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
+  if ((rc = map_act(&X1, x1 ? x1 : x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
+  if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
+  const WgShape sh = wgrad_v1_shape(P);
+  WgArgs g;
+  memset(&g, 0, sizeof(g));
+  g.nkb = P.Kf / 64;
+  g.mtiles = (g.nkb + 1) / 2;
+  g.ntiles = (P.Jd / 64) / sh.nblk;
+  g.splits = splits;
+  g.pb_w = pb.Wb; g.pb_h = pb.Hb; g.pb_n = pb.Nb;
+  g.pt_w = pb.tw; g.pt_h = pb.th; g.ptiles = pb.tw * pb.th * pb.tn;
+  g.r = P.r; g.pad = P.p; g.cblks = P.C / 64; g.kb_half = P.K0 / 64;
+  g.Jd = P.Jd; g.Kf = P.Kf;
+  g.sstride = P.s;
+  g.part = part;
+  if (sh.pair) {
+    if (sh.nblk == 4) return launch_wgrad_pair<4>(X0, X1, Dm, g, st);
+    return launch_wgrad_pair<2>(X0, X1, Dm, g, st);
+  }
+  if (sh.nblk == 4) return launch_wgrad<4>(X0, X1, Dm, g, st);
+  if (sh.nblk == 3) return launch_wgrad<3>(X0, X1, Dm, g, st);
+  if (sh.nblk == 2) return launch_wgrad<2>(X0, X1, Dm, g, st);
+  return launch_wgrad<1>(X0, X1, Dm, g, st);
+}
+
 int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a, const void* b, const void* dy,
                 void* dx, float* const dW[3], float* const db[3], char* ws, const Workspace& L,
                 cudaStream_t st) {
@@ -1368,6 +1619,32 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     d2 = conv2_fits(P.N, P.Jd, P.OW, P.OH, P.W, P.H, P.r - 1 - P.p, P.r, 0, c.nbk, c.nout, c.tiles_nn, P.C, 0);
   }
   const int dsplit = d2 ? 2 * P.F / 64 : 0;
+  int rc;
+  // SM partition: the v3 wgrad runs on ~54% of the SM pairs (side stream) while
+  // the dgrad runs on the rest, both persistent and concurrent -- their tails
+  // (partial-store drain, last-tile imbalance) overlap instead of adding up.
+  // 54% balances the two on the measured C2 step (DESIGN.md); QD_PART=K pins
+  // K pairs, QD_NO_PART=1 runs them back to back on all SMs.
+  int part = 0, dg_pairs = 0;
+  if (w3 && dx && dW[0] && !P.sq && !getenv("QD_NO_PART") && !getenv("QD_BR2")) {
+    const int per = wgrad3_pairs_per_split(P);
+    const int total = L.wg_split * per;  // pairs the wgrad alone would fill
+    part = getenv("QD_PART") ? atoi(getenv("QD_PART")) : (total * 54 / per + 50) / 100;
+    dg_pairs = total - part * per;
+    // one pair per split only: with several (wide C) the split granularity is too
+    // coarse to balance the two (measured: 256x14 loses 15%, DESIGN.md)
+    if (per != 1 || part < 1 || part >= L.wg_split || dg_pairs < total / 4) part = 0;
+  }
+  // QD_XFD=1 (measured slower): the dgrad forms its own D blocks
+  // (dy * b, dy * a) in its transform warps (C2Args::xf = 2) and no longer waits
+  // for the backward prologue, which then runs on the side stream ahead of the
+  // wgrad, beside the dgrad
+  const bool xfd = d2 && dx && part > 0 && P.kind == QD_KIND_CONV && getenv("QD_XFD") && atoi(getenv("QD_XFD"));
+  if (xfd) {
+    side = fork_side(st);
+    if (!side) return set_error(QD_ERR_CUDA, "side stream");
+  }
+  cudaStream_t pst = xfd ? side : st;  // the prologue's stream
   bool wg_pdl = false;  // a PDL-launched v2/v3 wgrad immediately precedes the dgrad on `st`
   if (dgiven) {
     D = (const bf16*)dy;
@@ -1384,26 +1661,10 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     long long rows = up ? P.Mout : P0.Mout;
     long long rows_per = (rows + L.bs_split - 1) / L.bs_split;
     bf16* Dw = (mat || up) ? (bf16*)(ws + L.off_D) : nullptr;
-    if (!dev_skip("prologue")) launch_pdl(bwd_prologue_vec_kernel, dim3(L.bs_split), dim3(256), 0, st, P0, (const bf16*)dy, (const bf16*)a,
+    if (!dev_skip("prologue")) launch_pdl(bwd_prologue_vec_kernel, dim3(L.bs_split), dim3(256), 0, pst, P0, (const bf16*)dy, (const bf16*)a,
                (const bf16*)b, Dw, bpart, rows_per, up ? 1 : 0, P.OH, P.OW, d2 ? 2 * P.F : P.Jd);
-    count_launch(st, "prologue");
+    count_launch(pst, "prologue");
     if (mat || up) D = Dw;
-  }
-  int rc;
-  // SM partition: the v3 wgrad runs on ~54% of the SM pairs (side stream) while
-  // the dgrad runs on the rest, both persistent and concurrent -- their tails
-  // (partial-store drain, last-tile imbalance) overlap instead of adding up.
-  // 54% balances the two on the measured C2 step (DESIGN.md); QD_PART=K pins
-  // K pairs, QD_NO_PART=1 runs them back to back on all SMs.
-  int part = 0, dg_pairs = 0;
-  if (w3 && dx && dW[0] && !P.sq && !getenv("QD_NO_PART") && !getenv("QD_BR2")) {
-    const int per = wgrad3_pairs_per_split(P);
-    const int total = L.wg_split * per;  // pairs the wgrad alone would fill
-    part = getenv("QD_PART") ? atoi(getenv("QD_PART")) : (total * 54 / per + 50) / 100;
-    dg_pairs = total - part * per;
-    // one pair per split only: with several (wide C) the split granularity is too
-    // coarse to balance the two (measured: 256x14 loses 15%, DESIGN.md)
-    if (per != 1 || part < 1 || part >= L.wg_split || dg_pairs < total / 4) part = 0;
   }
   // ---- wgrad ----
   if (dW[0]) {
@@ -1422,7 +1683,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     const bool br2 = (w2 || w3) && dx && !P.sq && getenv("QD_BR2") && atoi(getenv("QD_BR2"));
     cudaStream_t wst = st;
     if (br2 || part) {
-      side = fork_side(st);
+      if (!side) side = fork_side(st);
       if (side) wst = side;
       else part = 0;
     }
@@ -1462,32 +1723,11 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     } else if (rc != QD_ERR_UNSUPPORTED) {
       return rc;
     } else {
-    Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
-    CUtensorMap X0, X1, Dm;
-    if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
-    if ((rc = map_act(&X1, x1, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
-    if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
-    WgArgs g;
-    memset(&g, 0, sizeof(g));
-    int nblk = wgrad_ntile_blocks(P, wgrad_ptiles(P));
-    g.nkb = P.Kf / 64;
-    g.mtiles = (g.nkb + 1) / 2;
-    g.ntiles = (P.Jd / 64) / nblk;
-    g.splits = L.wg_split;
-    g.pb_w = pb.Wb; g.pb_h = pb.Hb; g.pb_n = pb.Nb;
-    g.pt_w = pb.tw; g.pt_h = pb.th; g.ptiles = pb.tw * pb.th * pb.tn;
-    g.r = P.r; g.pad = P.p; g.cblks = P.C / 64; g.kb_half = P.K0 / 64;
-    g.Jd = P.Jd; g.Kf = P.Kf;
-    g.sstride = P.s;
-    g.part = (float*)(ws + L.off_WG);
-    if (nblk == 4) rc = launch_wgrad<4>(X0, X1, Dm, g, st);
-    else if (nblk == 3) rc = launch_wgrad<3>(X0, X1, Dm, g, st);
-    else if (nblk == 2) rc = launch_wgrad<2>(X0, X1, Dm, g, st);
-    else rc = launch_wgrad<1>(X0, X1, Dm, g, st);
+    rc = run_wgrad_v1(P, x0, x1, D, (float*)(ws + L.off_WG), L.wg_split, st);
     if (rc) return rc;
     WSplits uni;
     memset(&uni, 0, sizeof(uni));
-    launch_bwd_finish(P, g.part, g.splits, uni, dW, bpart, L.bs_split, db, st);
+    launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, uni, dW, bpart, L.bs_split, db, st);
     }
   } else if (db[0] && (mat || P.nbias)) {
     launch_bias_finish(P, bpart, L.bs_split, db, st);
@@ -1509,9 +1749,12 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     else if (!(P.flags & QD_FLAG_TC_V1))
       // D is complete once the (PDL-launched) v2/v3 wgrad is running, and nothing
       // the dgrad reads is written by it: the dgrad need not wait for the wgrad
+    {
+      C2Xform xfm{xfd ? 2 : 0, P.F, P.F / 64, dy, a, b};
       rc = run_conv2(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
                      c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st, 1,
-                     dy, dsplit, wg_pdl ? 0 : 1);
+                     dy, dsplit, (wg_pdl && !xfd) ? 0 : 1, 0, nullptr, &xfm);
+    }
     if (part) set_conv2_cap(0);
     if (d2 && rc == QD_ERR_UNSUPPORTED) return set_error(QD_ERR_UNSUPPORTED, "dgrad conv2 plan changed");
     if (rc == QD_ERR_UNSUPPORTED && !up)
@@ -1575,36 +1818,7 @@ int x3_wgrad_split(const Plan& P) {
     const int s3 = wgrad3_split(P);  // r = 3 on CTA pairs (one product per launch, no in-kernel fold)
     if (s3 > 0) return s3;
   }
-  const long long ptiles = wgrad_ptiles(P);
-  const int mtiles = (P.Kf / 64 + 1) / 2;
-  const int ntiles = (P.Jd / 64) / wgrad_ntile_blocks(P, ptiles);
-  return (int)wgrad_split_for((long long)mtiles * ntiles, ptiles, tc_num_sms());
-}
-
-// one v1 wgrad product (x0 taps, D) into `splits` fp32 partial slots at `part`
-static int run_wgrad_v1(const Plan& P, const void* x0, const void* D, float* part, int splits, cudaStream_t st) {
-  Box pb = choose_box(P.OW, P.OH, P.N, 64, true);
-  CUtensorMap X0, Dm;
-  int rc;
-  if ((rc = map_act(&X0, x0, P.C, P.W, P.H, P.N, pb.Wb, pb.Hb, pb.Nb, P.s))) return rc;
-  if ((rc = map_act(&Dm, D, P.Jd, P.OW, P.OH, P.N, pb.Wb, pb.Hb, pb.Nb))) return rc;
-  WgArgs g;
-  memset(&g, 0, sizeof(g));
-  int nblk = wgrad_ntile_blocks(P, wgrad_ptiles(P));
-  g.nkb = P.Kf / 64;
-  g.mtiles = (g.nkb + 1) / 2;
-  g.ntiles = (P.Jd / 64) / nblk;
-  g.splits = splits;
-  g.pb_w = pb.Wb; g.pb_h = pb.Hb; g.pb_n = pb.Nb;
-  g.pt_w = pb.tw; g.pt_h = pb.th; g.ptiles = pb.tw * pb.th * pb.tn;
-  g.r = P.r; g.pad = P.p; g.cblks = P.C / 64; g.kb_half = P.K0 / 64;
-  g.Jd = P.Jd; g.Kf = P.Kf;
-  g.sstride = P.s;
-  g.part = part;
-  if (nblk == 4) return launch_wgrad<4>(X0, X0, Dm, g, st);
-  if (nblk == 3) return launch_wgrad<3>(X0, X0, Dm, g, st);
-  if (nblk == 2) return launch_wgrad<2>(X0, X0, Dm, g, st);
-  return launch_wgrad<1>(X0, X0, Dm, g, st);
+  return wgrad_v1_shape(P).S;
 }
 
 int x3_forward(const Plan& P, const void* x, const void* wpack, const float* const bias[3], void* y, void* a,
@@ -1683,7 +1897,7 @@ int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
     const bf16* da[3] = {Dh, Dl, Dh};
     for (int i = 0; i < 3; ++i) {
       float* pi = part + (size_t)i * S * slot;  // 3 S contiguous slots
-      rc = w3 ? run_wgrad3(P, xa[i], nullptr, da[i], pi, S, wst) : run_wgrad_v1(P, xa[i], da[i], pi, S, wst);
+      rc = w3 ? run_wgrad3(P, xa[i], nullptr, da[i], pi, S, wst) : run_wgrad_v1(P, xa[i], nullptr, da[i], pi, S, wst);
       if (rc) return rc;
     }
     WSplits uni;

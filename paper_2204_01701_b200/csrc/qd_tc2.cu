@@ -70,6 +70,15 @@ struct C2Args {
   bf16* out1;
   bf16* out2;
   const bf16* xres;
+  // operand transform (XF kernels): A halo slots computed by the transform warps
+  // from global tensors instead of TMA-loaded. xf = 1: x * x for the blocks of the
+  // first K half (squared-input families, neurons.py:255-256); xf = 2: the dgrad's
+  // D blocks cb < csplit, dy * b (block cb < xf_fb) and dy * a (neurons.py:437-444),
+  // bit-identical to the backward prologue's bf16(dy * b) / bf16(dy * a)
+  int xf, xf_cs, xf_fb;  // mode; channels of the source tensors; F / 64
+  const bf16* xf_x;      // x (xf 1) or dy (xf 2)
+  const bf16* xf_a;
+  const bf16* xf_b;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -90,56 +99,19 @@ namespace c2 {
     if (g.trace && blockIdx.x == (blk) && (tile) < 64)                                            \
       g.trace[((role) * 64 + (tile)) * 16 + (ev)] = (unsigned long long)clock64();                \
   } while (0)
-__device__ __forceinline__ uint32_t cluster_rank() {
-  uint32_t r;
-  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
-  return r;
-}
-__device__ __forceinline__ void cluster_sync() {
-  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
-}
-__device__ __forceinline__ uint32_t peer0(const void* p) { return ptx::smem_u32(p) & 0xFEFFFFFFu; }
-__device__ __forceinline__ void tma4_cg2(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1, int c2,
-                                         int c3) {
-  asm volatile(
-      "cp.async.bulk.tensor.4d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(ptx::smem_u32(dst)),
-      "l"(m), "r"(bar), "r"(c0), "r"(c1), "r"(c2), "r"(c3)
-      : "memory");
-}
+using ptx::cluster_rank;
+using ptx::cluster_sync;
+using ptx::peer0;
+using ptx::tma4_cg2;
+using ptx::tma2_cg2;
+using ptx::mma_cg2;
+using ptx::commit_mc;
+using ptx::arrive_remote;
 // L2 prefetch of a future box (fire and forget; the later load then hits L2)
 __device__ __forceinline__ void tma4_prefetch(const CUtensorMap* m, int c0, int c1, int c2, int c3) {
   asm volatile("cp.async.bulk.prefetch.tensor.4d.L2.global.tile [%0, {%1, %2, %3, %4}];" ::"l"(m), "r"(c0), "r"(c1),
                "r"(c2), "r"(c3)
                : "memory");
-}
-__device__ __forceinline__ void tma2_cg2(const CUtensorMap* m, uint32_t bar, void* dst, int c0, int c1) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%3, %4}], [%2];" ::"r"(ptx::smem_u32(dst)),
-      "l"(m), "r"(bar), "r"(c0), "r"(c1)
-      : "memory");
-}
-__device__ __forceinline__ void mma_cg2(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
-      "l"(a), "l"(b), "r"(idesc), "r"(acc)
-      : "memory");
-}
-__device__ __forceinline__ void commit_mc(uint64_t* bar) {
-  asm volatile(
-      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
-          ptx::smem_u32(bar)),
-      "h"((uint16_t)3)
-      : "memory");
-}
-// TMEM hand-back: no memory is published through this barrier (the TMEM
-// reads are ordered by tcgen05.wait::ld + fence::before_thread_sync), so a
-// relaxed arrive -- a release would first drain this warp's outstanding
-// global stores of the previous tile (profiled: the MMA warp stalled on it).
-__device__ __forceinline__ void arrive_remote(uint32_t addr) {
-  asm volatile("mbarrier.arrive.relaxed.cluster.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
 }
 __device__ __forceinline__ uint32_t pack2(float a, float b) {
   __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -232,21 +204,49 @@ __device__ __forceinline__ void c2_store_pass(const C2Args& g, const uint8_t* st
 #ifndef C2_EPW
 #define C2_EPW 2
 #endif
-template <int EPI, int NB>
+
+// transform warps' slot wait: polls with a back-off so the spinning warps leave
+// the issue slots to the MMA warp on their sub-partition
+__device__ __forceinline__ void c2_wait_sleep(uint64_t* bar, uint32_t parity) {
+  const uint32_t addr = ptx::smem_u32(bar);
+  while (!ptx::mbar_try_wait(addr, parity)) __nanosleep(200);
+}
+template <int EPI, int NB, int XF = 0>
 struct C2Threads {
   static constexpr int NPASS = (EPI == E2_PROPOSED || EPI == E2_T4) ? 3 : (EPI == E2_PLAIN ? NB : 1);
   // proposed / t4: C2_EPW epilogue warpgroups, each owning 64 / C2_EPW channels of y, a, b
   static constexpr int NEPI = NPASS == 3 ? 4 * C2_EPW : 4;
-  static constexpr int THREADS = 128 + NEPI * 32;
+  // operand-transform warps (XF kernels): 8 beside one epilogue warpgroup, else 4
+  static constexpr int XW = XF ? (NEPI == 4 ? 8 : 4) : 0;
+  static constexpr int THREADS = 128 + NEPI * 32 + XW * 32;
 };
 
-template <int EPI, int NB, int R>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::THREADS, 1)
+// release arrive on a (possibly remote) cluster barrier: publishes this warp's
+// shared-memory writes (after fence.proxy.async) to the MMA that waits on it
+// (CTA-scope release, as the usual 2-SM producer pattern: a cluster-scope release
+// compiles to MEMBAR.ALL.GPU + ERRBAR per arrival, profiled)
+__device__ __forceinline__ void c2_arrive_release(uint32_t addr) {
+  asm volatile("mbarrier.arrive.release.cta.shared::cluster.b64 _, [%0];" ::"r"(addr) : "memory");
+}
+__device__ __forceinline__ uint4 c2_bf16_mul(uint4 u, uint4 v) {
+  __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&u);
+  const __nv_bfloat162* k = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float2 a = __bfloat1622float2(h[e]), b = __bfloat1622float2(k[e]);
+    h[e] = __floats2bfloat162_rn(a.x * b.x, a.y * b.y);
+  }
+  return u;
+}
+
+template <int EPI, int NB, int R, int XF = 0>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB, XF>::THREADS, 1)
     conv2_kernel(const __grid_constant__ CUtensorMap mA0, const __grid_constant__ CUtensorMap mA1,
                  const __grid_constant__ CUtensorMap mB, const C2Args g) {
   // output "passes": proposed/t4 write y, a, b; plain writes NB 64-channel blocks
-  constexpr int NPASS = C2Threads<EPI, NB>::NPASS;
-  constexpr int NEPI = C2Threads<EPI, NB>::NEPI;
+  constexpr int NPASS = C2Threads<EPI, NB, XF>::NPASS;
+  constexpr int NEPI = C2Threads<EPI, NB, XF>::NEPI;
+  constexpr int XW = C2Threads<EPI, NB, XF>::XW;
   constexpr int ACC = NB * 64;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -278,7 +278,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
     ptx::prefetch_tmap(&mA1);
     ptx::prefetch_tmap(&mB);
     for (int i = 0; i < 4; ++i) {
-      ptx::mbar_init(&afull[i], 1);
+      ptx::mbar_init(&afull[i], 1 + 2 * XW);  // XF: every transform warp of both CTAs arrives per slot use
       ptx::mbar_init(&aempty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -331,7 +331,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         if (leader) C2_TRACE(0, it, 2 * ab);
         if (leader) C2_TRACE_B(1, 0, it, 8 + 2 * ab);
         ptx::mbar_wait(&aempty[as], aph ^ 1);
-        if (leader) {
+        const bool xblk = XF && (g.xf == 1 ? half == 0 : (g.xf == 2 && cb < g.csplit));  // filled by the transform warps
+        if (xblk) {
+          if (leader && rank == 0) ptx::mbar_arrive(&afull[as]);
+        } else if (leader) {
           C2_TRACE(0, it, 2 * ab + 1);
           C2_TRACE_B(1, 0, it, 9 + 2 * ab);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&afull[as], 2u * g.halo_tx);
@@ -468,7 +471,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
         __syncwarp();
       }
     }
-  } else if (warp >= 4) {
+  } else if (warp >= 4 && warp < 4 + NEPI) {
     // ===== epilogue (both CTAs, own TMEM rows); one 4 KB staging tile per warp,
     // one output pass at a time =====
     const int q = warp & 3;
@@ -796,6 +799,99 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB>::
       if (tracer) C2_TRACE(2, it, 3);
       if (tracer1) C2_TRACE(2, it, 12);
     }
+  } else if (XF && warp >= 4 + NEPI) {
+    // ===== operand transform (XF): the A halo slots of the transformed blocks are
+    // written here -- 16-B chunks of the source rows loaded (ld.global.nc), the
+    // elementwise op in fp32, bf16 stored at the SWIZZLE_128B position the TMA
+    // would use (chunk c of halo row ri at c ^ (ri & 7)); out-of-image rows and
+    // columns are zeros (the TMA's OOB fill = the padding). Each warp then
+    // fences the generic-proxy writes for the tensor core and arrives (release)
+    // on CTA0's full barrier; it also arrives for TMA-loaded blocks so the
+    // barrier count stays fixed.
+    constexpr int U = 8;
+    const int xt = threadIdx.x - (128 + NEPI * 32);
+    const int nchunk = g.Wp * g.HR * 8;
+    const size_t img = (size_t)g.Hin * g.Win;
+    int as = 0;
+    uint32_t aph = 0;
+    const bool xtr = xt == 0;  // dev trace: role 3 = transform warp 0 of CTA 0
+    int it = 0;
+    for (int w = cluster; w < g.total; w += nclusters, ++it) {
+      const int rest = ptx::fdiv(w, g.fd_nn);
+      const int p = ptx::fdiv(rest, g.fd_T), t = rest - p * g.T_img;
+      const int n = 2 * p + (int)rank;
+      const int h0 = ptx::fdiv(128 * t, g.fd_Wp) - g.pe;
+      for (int ab = 0; ab < g.ablocks; ++ab) {
+        const int half = ab / g.cblks, cb = ab % g.cblks;
+        const bool xblk = g.xf == 1 ? half == 0 : (g.xf == 2 && cb < g.csplit);  // 3: none (dev)
+        if (xblk) {
+          const bf16* s0 = g.xf_x;
+          const bf16* s1 = nullptr;
+          int ch = cb * 64;
+          if (g.xf == 2) {
+            const int seg = cb >= g.xf_fb ? 1 : 0;
+            ch = (cb - seg * g.xf_fb) * 64;
+            s1 = seg == 0 ? g.xf_b : g.xf_a;
+          }
+          uint8_t* slot = sHalo + as * g.halo_bytes;
+          // the first pass's loads go out before the wait for the slot (registers
+          // only), so their latency overlaps the MMAs still reading it. Thread xt
+          // owns 16-B chunk (xt & 7) of halo rows (xt >> 3) + 32 k (XW = 8: 256
+          // threads = 32 rows per step): the row -> (image row, column) walk and
+          // the source offsets advance incrementally (the transform is issue-bound)
+          bool waited = false;
+          constexpr int RSTEP = XW * 32 / 8;  // halo rows per step of all transform threads
+          const int cc = xt & 7;
+          int r_ = xt >> 3;
+          int hi = ptx::fdiv(r_, g.fd_Wp), wc = r_ - hi * g.Wp;
+          const size_t rowpix = (size_t)g.Win * g.xf_cs;
+          const bf16* b0 = s0 + (size_t)n * img * g.xf_cs + ch + cc * 8;
+          const bf16* b1 = s1 ? s1 + (size_t)n * img * g.xf_cs + ch + cc * 8 : nullptr;
+          const int nrows = g.Wp * g.HR;
+          const bool nok = n < g.N && !(g.dbg & 8);
+          while (r_ < nrows) {
+            uint4 v0[U], v1[U];
+            int ri[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              const int hh = h0 + hi, ww = wc - g.pe;
+              ri[u] = r_ < nrows ? r_ : -1;
+              const bool ok = r_ < nrows && nok && hh >= 0 && hh < g.Hin && ww >= 0 && ww < g.Win;
+              const size_t off = (size_t)hh * rowpix + (size_t)ww * g.xf_cs;
+              v0[u] = ok ? __ldg(reinterpret_cast<const uint4*>(b0 + off)) : make_uint4(0, 0, 0, 0);
+              if (g.xf == 2) v1[u] = ok ? __ldg(reinterpret_cast<const uint4*>(b1 + off)) : make_uint4(0, 0, 0, 0);
+              r_ += RSTEP;
+              wc += RSTEP;
+              while (wc >= g.Wp) { wc -= g.Wp; ++hi; }
+            }
+            if (!waited) {
+              if (xtr) C2_TRACE(3, it, 2 * ab);
+              if (lane == 0) c2_wait_sleep(&aempty[as], aph ^ 1);
+              if (xtr) C2_TRACE(3, it, 2 * ab + 1);
+              __syncwarp();
+              waited = true;
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+              if (ri[u] < 0) continue;
+              const uint4 val = c2_bf16_mul(v0[u], g.xf == 2 ? v1[u] : v0[u]);
+              if (!(g.dbg & 128)) *reinterpret_cast<uint4*>(slot + ri[u] * 128 + ((cc ^ (ri[u] & 7)) << 4)) = val;
+            }
+          }
+          if (!waited) {
+            if (lane == 0) c2_wait_sleep(&aempty[as], aph ^ 1);
+            __syncwarp();
+          }
+          if (!(g.dbg & 64)) ptx::fence_proxy_async_smem();
+        } else {
+          if (lane == 0) c2_wait_sleep(&aempty[as], aph ^ 1);
+        }
+        __syncwarp();
+        if (xtr) C2_TRACE(3, it, 8 + ab);
+        if (lane == 0) c2_arrive_release(c2::peer0(&afull[as]));
+        if (++as == g.a_slots) { as = 0; aph ^= 1; }
+      }
+    }
   }
   ptx::tc_fence_before();
   c2::cluster_sync();
@@ -969,10 +1065,11 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
 static thread_local int g_conv2_cap = 0;  // per host thread (set around one launch)
 void set_conv2_cap(int pairs) { g_conv2_cap = pairs; }
 
-template <int EPI, int NB, int R>
+template <int EPI, int NB, int R, int XF = 0>
 static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
                        cudaStream_t st) {
-  raise_smem_attr((const void*)conv2_kernel<EPI, NB, R>, pl.smem);
+  using Th = C2Threads<EPI, NB, XF>;
+  raise_smem_attr((const void*)conv2_kernel<EPI, NB, R, XF>, pl.smem);
   // persistent grid: only as many pairs as can be co-resident (GPCs with an odd
   // number of free SMs cannot host a pair; a second wave would double the time)
   thread_local int maxc_[kMaxDev] = {};
@@ -980,27 +1077,27 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
   int& maxc = maxc_[cur_device()];
   size_t& maxc_smem = maxc_smem_[cur_device()];
   if (maxc == 0 || maxc_smem != pl.smem) {
-    maxc = max_pair_clusters(conv2_kernel<EPI, NB, R>, C2Threads<EPI, NB>::THREADS, pl.smem);
+    maxc = max_pair_clusters(conv2_kernel<EPI, NB, R, XF>, Th::THREADS, pl.smem);
     maxc_smem = pl.smem;
   }
   int clusters = tc_num_sms() / 2;
   if (maxc > 0 && maxc < clusters) clusters = maxc;
   if (pl.g.total < clusters) clusters = pl.g.total;
   if (g_conv2_cap > 0 && g_conv2_cap < clusters) clusters = g_conv2_cap;
-  const cudaError_t le = launch_pdl(conv2_kernel<EPI, NB, R>, dim3(2 * clusters), dim3(C2Threads<EPI, NB>::THREADS),
+  const cudaError_t le = launch_pdl(conv2_kernel<EPI, NB, R, XF>, dim3(2 * clusters), dim3(Th::THREADS),
                                     pl.smem, st, A0, A1, B, pl.g);
   if (le != cudaSuccess) {
     cudaGetLastError();
     cudaFuncAttributes fa;
     memset(&fa, 0, sizeof(fa));
-    const cudaError_t fe = cudaFuncGetAttributes(&fa, conv2_kernel<EPI, NB, R>);
-    const int again = max_pair_clusters(conv2_kernel<EPI, NB, R>, C2Threads<EPI, NB>::THREADS, pl.smem);
+    const cudaError_t fe = cudaFuncGetAttributes(&fa, conv2_kernel<EPI, NB, R, XF>);
+    const int again = max_pair_clusters(conv2_kernel<EPI, NB, R, XF>, Th::THREADS, pl.smem);
     int dev = -1;
     cudaGetDevice(&dev);
     return set_error(QD_ERR_CUDA,
                      "conv2 launch (%d CTAs, %d threads, %zu B smem, maxc %d, tiles %d; function: "
                      "max dyn smem %d static %zu (%s), clusters now %d, device %d): %s",
-                     2 * clusters, C2Threads<EPI, NB>::THREADS, pl.smem, maxc, (int)pl.g.total,
+                     2 * clusters, Th::THREADS, pl.smem, maxc, (int)pl.g.total,
                      fa.maxDynamicSharedSizeBytes, fa.sharedSizeBytes, cudaGetErrorString(fe), again, dev,
                      cudaGetErrorString(le));
   }
@@ -1010,6 +1107,10 @@ static int c2_launch_r(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
 template <int EPI, int NB>
 static int c2_launch(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const C2Plan& pl,
                      cudaStream_t st) {
+  if (pl.g.xf) {
+    if (pl.g.r == 3) return c2_launch_r<EPI, NB, 3, 1>(A0, A1, B, pl, st);
+    return c2_launch_r<EPI, NB, 0, 1>(A0, A1, B, pl, st);
+  }
   if (pl.g.r == 3) return c2_launch_r<EPI, NB, 3>(A0, A1, B, pl, st);
   return c2_launch_r<EPI, NB, 0>(A0, A1, B, pl, st);
 }
@@ -1020,7 +1121,7 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
               int pe, int r, int dual, const void* wmat, int wrows, int wK, int b_rs_tile, int b_rs_blk,
               int tiles_nn, int out_c_tile, void* o0, void* o1, void* o2, int Cout, const float* const bias[3],
               const void* xres, cudaStream_t st, int ss, const void* a_tail, int csplit, int pdl_wait,
-              int f32out, float* stats) {
+              int f32out, float* stats, const C2Xform* xf) {
   int NOUT = (epi == E2_PROPOSED || epi == E2_T4) ? 3 : (epi == E2_PLAIN ? nbk : 1);
   int nbias = epi == E2_PROPOSED ? 3 : ((epi == E2_PLAIN && bias[0]) ? 1 : 0);
   C2Plan pl = c2_plan(N, Cin, Win, Hin, OWg, OHg, pe, r, dual, nbk, NOUT, tiles_nn, Cout, nbias);
@@ -1056,6 +1157,17 @@ int run_conv2(int epi, int nbk, const void* a0, const void* a1, int Cin, int Win
   g.out0 = (bf16*)o0; g.out1 = (bf16*)o1; g.out2 = (bf16*)o2;
   g.xres = (const bf16*)xres;
   g.pdl_wait = pdl_wait;
+  if (xf && xf->mode) {
+    if (f32out || (xf->mode == 1 && dual > 1) || (xf->mode == 2 && !(a_tail && csplit > 0)))
+      return QD_ERR_UNSUPPORTED;
+    g.xf = xf->mode;
+    if (getenv("QD_XF_NULL")) g.xf = 3;  // dev: transform warps present, every block TMA-loaded (timing)
+    g.xf_cs = xf->cs;
+    g.xf_fb = xf->fb;
+    g.xf_x = (const bf16*)xf->x;
+    g.xf_a = (const bf16*)xf->a;
+    g.xf_b = (const bf16*)xf->b;
+  }
   CUtensorMap A0, A1, B;
   int rc;
   cuuint32_t bA[4] = {64, (cuuint32_t)g.Wp, (cuuint32_t)g.HR, 1};

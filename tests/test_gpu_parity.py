@@ -927,3 +927,45 @@ def test_bn_statistics_from_fprop_epilogue(shape, dtype, monkeypatch):
     d = (z1.float() - z2.float()).abs()
     tol = 2e-2 if dtype == torch.bfloat16 else 1e-4
     assert float(d.max()) <= tol * float(z2.float().abs().max()), float(d.max())
+
+
+@pytest.mark.parametrize("case", [
+    ("proposed", 128, 64, 64, 32, 32, 1, "QD_XFD"),    # C2: dgrad forms dy*b, dy*a itself
+    ("proposed", 64, 128, 128, 28, 28, 1, "QD_XFD"),
+    ("t2_linear", 8, 64, 64, 56, 56, 1, "QD_XFS"),     # fprop squares x in its transform warps
+    ("t2_linear", 4, 128, 64, 20, 20, 2, "QD_XFS"),
+    ("t2", 4, 64, 128, 16, 16, 1, "QD_XFS"),
+    ("t2and4", 4, 64, 64, 24, 24, 1, "QD_XFS"),
+], ids=lambda c: f"{c[0]}_{c[1]}x{c[2]}x{c[4]}s{c[6]}" if isinstance(c, tuple) else str(c))
+def test_operand_transform_bit_identical(case, monkeypatch):
+    """The conv2 operand-transform warps (x * x for the squared-input families,
+    dy * b / dy * a for the dgrad's D blocks) write exactly the bf16 values the
+    separate passes (square_vec / backward prologue) write, in the TMA's
+    swizzled layout: every output and gradient is bit-identical to the default
+    path. (Opt-in: measured slower.)"""
+    fam, n, c, f, h, w, s, knob = case
+    x, P, g = Q.synthetic_layer(fam, "conv", n, c, f, h, w, 3, s, 1, seed=11, random_bias=True)
+    off = run_device(fam, "conv", x, P, g, torch.bfloat16, 3, s, 1)
+    monkeypatch.setenv(knob, "1")
+    on = run_device(fam, "conv", x, P, g, torch.bfloat16, 3, s, 1)
+    monkeypatch.delenv(knob)
+    assert on[5] == 1 and off[5] == 1
+    assert (on[0] == off[0]).all(), "y"
+    assert (on[4] == off[4]).all(), "dx"
+    for role in on[3]:
+        assert (on[3][role] == off[3][role]).all(), role
+
+
+@pytest.mark.parametrize("shape", [(128, 512, 512, 7), (64, 256, 512, 14), (32, 128, 256, 8)])
+def test_wgrad_pair_matches_single(shape, monkeypatch):
+    """The CTA-pair v1 wgrad (QD_WPAIR=1: M = 256 over two SMs, each holding half
+    of the D boxes) gives the single-CTA kernel's weight gradients; both are
+    checked against the oracle elsewhere."""
+    n, c, f, hw = shape
+    x, P, g = Q.synthetic_layer("proposed", "conv", n, c, f, hw, hw, 3, 1, 1, seed=3, random_bias=True)
+    base = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    monkeypatch.setenv("QD_WPAIR", "1")
+    pair = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    monkeypatch.delenv("QD_WPAIR")
+    for role in base[3]:
+        assert Q.rel_err(pair[3][role], base[3][role]) <= 1e-5, role

@@ -8,8 +8,10 @@ from oracle import quadra_oracle as Q
 from paper_2204_01701_b200 import _lib, neurons
 from paper_2204_01701_b200.spec import QuadraticLayerSpec
 which = sys.argv[1] if len(sys.argv) > 1 else "fprop"
-spec = QuadraticLayerSpec(kind="conv", family="proposed", in_dim=64, out_dim=64, kernel=3, stride=1, pad=1)
-x, P, g = Q.synthetic_layer("proposed", "conv", 128, 64, 64, 32, 32, 3, 1, 1, seed=0)
+fam = sys.argv[2] if len(sys.argv) > 2 else "proposed"
+n_, c_, hw_ = (int(v) for v in (sys.argv[3:6] if len(sys.argv) > 5 else (128, 64, 32)))
+spec = QuadraticLayerSpec(kind="conv", family=fam, in_dim=c_, out_dim=c_, kernel=3, stride=1, pad=1)
+x, P, g = Q.synthetic_layer(fam, "conv", n_, c_, c_, hw_, hw_, 3, 1, 1, seed=0)
 xt = torch.as_tensor(x, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
 gt = torch.as_tensor(g, device="cuda").bfloat16().contiguous(memory_format=torch.channels_last)
 params = {k: torch.as_tensor(v, dtype=torch.float32, device="cuda") for k, v in P.items()}
@@ -22,12 +24,12 @@ for _ in range(3):
 torch.cuda.synchronize()
 buf = np.zeros(8192, dtype=np.uint64)
 lib.qd_debug_trace_copy(buf.ctypes.data)
-T = buf[:3072].reshape(3, 64, 16).astype(np.int64)
+T = buf[:4096].reshape(4, 64, 16).astype(np.int64)
 t0 = T[T > 0].min()
-names = {0: "producer", 1: "mma", 2: "epilogue"}
+names = {0: "producer", 1: "mma", 2: "epilogue", 3: "xform"}
 for tile in range(10):
     row = []
-    for role in range(3):
+    for role in range(4):
         ev = T[role, tile]
         nz = [(i, int(v - t0)) for i, v in enumerate(ev) if v > 0]
         row.append(f"{names[role]}: " + " ".join(f"{i}@{v}" for i, v in nz))
