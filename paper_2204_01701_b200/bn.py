@@ -29,7 +29,7 @@ import torch
 from torch import nn
 
 from . import _lib, neurons
-from .nn import QuadFunction, _QuadBase
+from .nn import QuadFunction, _QuadBase, grad_sinks, settle_sinks
 from .spec import QuadraticLayerSpec, param_shapes
 
 
@@ -120,8 +120,16 @@ def _forward_with_stats(spec, params, x, dtype, recompute):
     return y, cache, stats, rows
 
 
-def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu, params=None):
-    """(D, dgamma, dbeta, {bias role: grad}) for the layer's backward from D."""
+def _f32(C, dev, t=None):
+    """a caller-owned fp32 (C,) output (e.g. a data-parallel bucket view) or a fresh one"""
+    if t is not None and tuple(t.shape) == (C,) and t.dtype == torch.float32 and t.is_contiguous():
+        return t
+    return torch.empty(C, dtype=torch.float32, device=dev)
+
+
+def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu, params=None, out=None):
+    """(D, dgamma, dbeta, {bias role: grad}) for the layer's backward from D;
+    ``out`` may hold caller-owned outputs for "gamma", "beta" and the bias roles."""
     lib = _lib.load()
     desc = neurons.make_desc(spec, cache.x.shape, cache.x.dtype)
     pl = lib  # noqa: F841
@@ -131,10 +139,11 @@ def bn_backward_D(spec, cache, dz, y, gamma, beta, save_mean, save_invstd, relu,
     yr = _rows(y)
     M = yr.shape[0]
     D = torch.empty((M, nblk * C), dtype=y.dtype, device=y.device)
-    dgamma = torch.empty(C, dtype=torch.float32, device=y.device)
-    dbeta = torch.empty(C, dtype=torch.float32, device=y.device)
+    out = out or {}
+    dgamma = _f32(C, y.device, out.get("gamma"))
+    dbeta = _f32(C, y.device, out.get("beta"))
     broles = neurons.BIAS_ROLES.get(fam, ())
-    db = {r: torch.empty(C, dtype=torch.float32, device=y.device) for r in broles}
+    db = {r: _f32(C, y.device, out.get(r)) for r in broles}
     ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, nblk * C), dtype=torch.uint8, device=y.device)
     dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
     ca, cb = (cache.a, cache.b) if params is None else neurons.restore_ab(spec, params, cache)
@@ -162,6 +171,7 @@ class _QuadBNFunction(torch.autograd.Function):
         else:
             z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
         ctx.spec, ctx.roles, ctx.params, ctx.cache, ctx.relu = spec, roles, params, cache, relu
+        ctx.gamma, ctx.beta = gamma, beta  # the parameters themselves (gradient sinks)
         ctx.x_dtype = x.dtype
         ctx.save_for_backward(y, gamma, beta, sm, si)
         return z
@@ -169,14 +179,21 @@ class _QuadBNFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dz):
         y, gamma, beta, sm, si = ctx.saved_tensors
-        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, dz, y, gamma, beta, sm, si, ctx.relu, ctx.params)
+        named = dict(ctx.params, gamma=ctx.gamma, beta=ctx.beta)
+        needs = dict({r: ctx.needs_input_grad[7 + i] for i, r in enumerate(ctx.roles)},
+                     gamma=ctx.needs_input_grad[5], beta=ctx.needs_input_grad[6])
+        sinks = grad_sinks(named, needs)
+        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, dz, y, gamma, beta, sm, si, ctx.relu, ctx.params,
+                                             out=sinks)
         want_dx = ctx.needs_input_grad[4]
-        grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx)
+        grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx, out=sinks)
         grads.update(db)
+        grads.update(gamma=dgamma, beta=dbeta)
+        grads = settle_sinks(named, sinks, grads)
         if dx is not None and dx.dtype != ctx.x_dtype:
             dx = dx.to(ctx.x_dtype)
         ctx.cache = None
-        return (None, None, None, None, dx, dgamma, dbeta) + tuple(grads[r] for r in ctx.roles)
+        return (None, None, None, None, dx, grads["gamma"], grads["beta"]) + tuple(grads[r] for r in ctx.roles)
 
 
 class _QuadBNAddReLUFunction(torch.autograd.Function):
@@ -201,6 +218,7 @@ class _QuadBNAddReLUFunction(torch.autograd.Function):
             z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, True, True,
                                    res=res)
         ctx.spec, ctx.roles, ctx.params, ctx.cache = spec, roles, params, cache
+        ctx.gamma, ctx.beta = gamma, beta
         ctx.x_dtype, ctx.res_dtype = x.dtype, res.dtype
         ctx.save_for_backward(y, z, gamma, beta, sm, si)
         return z
@@ -209,15 +227,22 @@ class _QuadBNAddReLUFunction(torch.autograd.Function):
     def backward(ctx, dz):
         y, z, gamma, beta, sm, si = ctx.saved_tensors
         g = torch.ops.aten.threshold_backward(dz.to(z.dtype), z, 0)
-        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, g, y, gamma, beta, sm, si, False, ctx.params)
+        named = dict(ctx.params, gamma=ctx.gamma, beta=ctx.beta)
+        needs = dict({r: ctx.needs_input_grad[7 + i] for i, r in enumerate(ctx.roles)},
+                     gamma=ctx.needs_input_grad[5], beta=ctx.needs_input_grad[6])
+        sinks = grad_sinks(named, needs)
+        D, dgamma, dbeta, db = bn_backward_D(ctx.spec, ctx.cache, g, y, gamma, beta, sm, si, False, ctx.params,
+                                             out=sinks)
         want_dx = ctx.needs_input_grad[3]
-        grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx)
+        grads, dx = neurons.backward_from_D(ctx.spec, ctx.params, ctx.cache, D, want_dx=want_dx, out=sinks)
         grads.update(db)
+        grads.update(gamma=dgamma, beta=dbeta)
+        grads = settle_sinks(named, sinks, grads)
         if dx is not None and dx.dtype != ctx.x_dtype:
             dx = dx.to(ctx.x_dtype)
         ctx.cache = None
         dres = g if ctx.needs_input_grad[4] else None
-        return (None, None, None, dx, dres, dgamma, dbeta) + tuple(grads[r] for r in ctx.roles)
+        return (None, None, None, dx, dres, grads["gamma"], grads["beta"]) + tuple(grads[r] for r in ctx.roles)
 
 
 class _BNFunction(torch.autograd.Function):
@@ -228,6 +253,7 @@ class _BNFunction(torch.autograd.Function):
     def forward(ctx, y, gamma, beta, bn, relu):
         z, sm, si = bn_forward(y, gamma, beta, bn.running_mean, bn.running_var, bn.momentum, bn.eps, relu, True)
         ctx.relu = relu
+        ctx.gamma, ctx.beta = gamma, beta
         ctx.save_for_backward(y, gamma, beta, sm, si)
         return z
 
@@ -243,8 +269,10 @@ class _BNFunction(torch.autograd.Function):
         desc.N, desc.C, desc.H, desc.W, desc.F = M, C, 1, 1, C
         desc.r, desc.stride, desc.pad, desc.flags = 1, 1, 0, 0
         dy = torch.empty_like(y)
-        dgamma = torch.empty(C, dtype=torch.float32, device=y.device)
-        dbeta = torch.empty(C, dtype=torch.float32, device=y.device)
+        named = {"gamma": ctx.gamma, "beta": ctx.beta}
+        sinks = grad_sinks(named, {"gamma": ctx.needs_input_grad[1], "beta": ctx.needs_input_grad[2]})
+        dgamma = _f32(C, y.device, sinks.get("gamma"))
+        dbeta = _f32(C, y.device, sinks.get("beta"))
         ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, C), dtype=torch.uint8, device=y.device)
         dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
         st = lib.qd_bn_backward_D(ctypes.byref(desc), dzr.data_ptr(), y.data_ptr(), None, None, gamma.data_ptr(),
@@ -252,7 +280,8 @@ class _BNFunction(torch.autograd.Function):
                                   dgamma.data_ptr(), dbeta.data_ptr(), _lib.ptr3(), ws.data_ptr(),
                                   torch.cuda.current_stream().cuda_stream)
         _lib.raise_for(st, "qd_bn_backward_D (bn only)")
-        return dy, dgamma, dbeta, None, None
+        gr = settle_sinks(named, sinks, {"gamma": dgamma, "beta": dbeta})
+        return dy, gr["gamma"], gr["beta"], None, None
 
 
 def _ref_batchnorm(y, gamma, beta, running_mean, running_var, momentum, eps, training):

@@ -17,6 +17,15 @@ NVSwitch; gloo on CPU for the tests):
   NCCL transfer of the deep layers overlaps the backward of the shallow ones;
 * ``finish()`` waits for the outstanding buckets before the optimizer step.
 
+Direct gradient sink: the library's backward kernels (quadratic layers, their
+BN, first-order BN) fold their weight / bias gradients straight into the
+bucket views (``take_grad``) instead of fresh tensors, and the autograd
+function returns None for those parameters -- no AccumulateGrad add pass
+over the ~135 MB of gradients (ResNet-18) per step; the function then marks
+the parameter ready (``grad_ready``), which is what the post-accumulate hook
+does for every other parameter. A parameter is taken at most once between
+``reset()`` calls (a second gradient in the same step accumulates as usual).
+
 The update itself is the reference's ``sgd_step`` (trainer.py:50-61:
 v <- m v + g + wd p; p <- p - lr v), which is exactly
 ``torch.optim.SGD(momentum=0.9, weight_decay=5e-4, dampening=0)``.
@@ -28,9 +37,27 @@ import torch
 import torch.distributed as dist
 
 
+import os as _os
+
+_DEBUG = bool(_os.environ.get("QD_DP_DEBUG"))
+
+
+def take_grad(p):
+    """The tensor a library backward may overwrite with ``p``'s gradient this step
+    (its bucket view), or None (then the gradient goes through autograd)."""
+    red = getattr(p, "_qd_red", None)
+    return red.take(p) if red is not None else None
+
+
+def grad_ready(p):
+    """``p``'s gradient is complete in its bucket (after a ``take_grad`` write)."""
+    p._qd_red.ready(p)
+
+
 class BucketedAllReduce:
-    def __init__(self, params, bucket_mb=25.0, group=None, reduce_dtype=torch.float32):
+    def __init__(self, params, bucket_mb=25.0, group=None, reduce_dtype=torch.float32, direct=True):
         self.group = group
+        self.direct = direct and reduce_dtype == torch.float32
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         params = [p for p in params if p.requires_grad]
         order = list(reversed(params))
@@ -48,9 +75,18 @@ class BucketedAllReduce:
         self.pending = [0] * len(self.buckets)
         self.handles = [None] * len(self.buckets)
         self.hooks = []
+        self.bucket_of = {}
+        self.view_ptr = {}
+        self.taken = set()
+        self.sunk = set()
+        self._log = []
         for bi, (_, ps) in enumerate(self.buckets):
             for p in ps:
                 self.hooks.append(p.register_post_accumulate_grad_hook(self._hook(bi)))
+                self.bucket_of[id(p)] = bi
+                self.view_ptr[id(p)] = p.grad.data_ptr()
+                if self.direct:
+                    p._qd_red = self
         self.reset()
 
     def _make_bucket(self, ps, n, dtype):
@@ -61,14 +97,37 @@ class BucketedAllReduce:
             off += p.numel()
         self.buckets.append((flat, ps))
 
+    def _ready(self, bi):
+        self.pending[bi] -= 1
+        if self.pending[bi] == 0 and self.world > 1:
+            op = dist.ReduceOp.AVG if dist.get_backend(self.group) == "nccl" else dist.ReduceOp.SUM
+            self.handles[bi] = dist.all_reduce(self.buckets[bi][0], op=op, group=self.group, async_op=True)
+
     def _hook(self, bi):
-        def fire(_p):
-            self.pending[bi] -= 1
-            if self.pending[bi] == 0 and self.world > 1:
-                op = dist.ReduceOp.AVG if dist.get_backend(self.group) == "nccl" else dist.ReduceOp.SUM
-                self.handles[bi] = dist.all_reduce(self.buckets[bi][0], op=op, group=self.group,
-                                                   async_op=True)
+        def fire(p):
+            # the hook also runs for a parameter whose function returned None (a
+            # direct write already reported it through ready())
+            if id(p) in self.sunk:
+                return
+            if _DEBUG:
+                self._log.append(("hook", id(p), bi, self.pending[bi]))
+            self._ready(bi)
         return fire
+
+    def take(self, p):
+        """p's bucket view for a direct write, once per step (None if p.grad is no
+        longer the bucket view, or p already received a gradient this step)"""
+        k = id(p)
+        if not self.direct or k in self.taken or p.grad is None or p.grad.data_ptr() != self.view_ptr.get(k):
+            return None
+        self.taken.add(k)
+        return p.grad
+
+    def ready(self, p):
+        self.sunk.add(id(p))
+        if _DEBUG:
+            self._log.append(("sink", id(p), self.bucket_of[id(p)], self.pending[self.bucket_of[id(p)]]))
+        self._ready(self.bucket_of[id(p)])
 
     def reset(self):
         """zero the buckets (the grads) and re-arm the per-bucket counters"""
@@ -76,6 +135,8 @@ class BucketedAllReduce:
             flat.zero_()
             self.pending[bi] = len(ps)
             self.handles[bi] = None
+        self.taken.clear()
+        self.sunk.clear()
 
     def finish(self):
         """wait for every bucket's all-reduce; gradients are then the rank mean"""
@@ -91,6 +152,10 @@ class BucketedAllReduce:
     def remove(self):
         for h in self.hooks:
             h.remove()
+        for flat, ps in self.buckets:
+            for p in ps:
+                if getattr(p, "_qd_red", None) is self:
+                    del p._qd_red
 
 
 def broadcast_module(module, src=0, group=None):

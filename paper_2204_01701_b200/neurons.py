@@ -265,7 +265,19 @@ def restore_ab(spec, params, cache):
     return c2.a, c2.b
 
 
-def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, want_db=True):
+def _grad_buffers(shapes, roles, dev, out):
+    """fp32 gradient outputs: ``out[role]`` (a caller-owned contiguous fp32 tensor of
+    the role's shape, e.g. a data-parallel bucket view) or a fresh tensor"""
+    res = {}
+    for r in roles:
+        t = (out or {}).get(r)
+        if t is None or tuple(t.shape) != tuple(shapes[r]) or t.dtype != torch.float32 or not t.is_contiguous():
+            t = torch.empty(shapes[r], dtype=torch.float32, device=dev)
+        res[r] = t
+    return res
+
+
+def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, want_db=True, out=None):
     """Closed-form gradients on the GPU; returns ({role: grad}, dx).
 
     neurons.py:295-445 -- same checks (IntegrityError for a cache of another
@@ -301,8 +313,8 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, wa
     dev = x.device
     shapes = param_shapes(spec)
     broles = BIAS_ROLES.get(spec.family, ()) if want_db else ()  # want_db=False: no bias grads (constant bias)
-    grads = {role: torch.empty(shapes[role], dtype=torch.float32, device=dev)
-             for role in GRAD_ORDER[spec.family] if want_db or role not in BIAS_ROLES.get(spec.family, ())}
+    grads = _grad_buffers(shapes, [role for role in GRAD_ORDER[spec.family]
+                                   if want_db or role not in BIAS_ROLES.get(spec.family, ())], dev, out)
     dx = torch.empty_like(x) if want_dx else None  # preserves channels_last
     ws = _workspace(desc, dev)
     ca, cb = restore_ab(spec, params, cache)
@@ -317,7 +329,7 @@ def symbolic_backward(spec, params, cache, dy, *, want_dx=True, want_dw=True, wa
     return grads, dx
 
 
-def backward_from_D(spec, params, cache, D, *, want_dx=True, want_dw=True):
+def backward_from_D(spec, params, cache, D, *, want_dx=True, want_dw=True, out=None):
     """Layer backward from a precomputed operand D ([M, Jd] rows, e.g. from the
     fused BN backward ``bn.bn_backward_D``); weight gradients and dx only (the
     bias gradients come with D). Stride-1 fc / conv layers."""
@@ -338,7 +350,7 @@ def backward_from_D(spec, params, cache, D, *, want_dx=True, want_dw=True):
         wpack = _pack(spec, desc, params)[0]
     dev = x.device
     shapes = param_shapes(spec)
-    grads = {role: torch.empty(shapes[role], dtype=torch.float32, device=dev) for role in roles}
+    grads = _grad_buffers(shapes, roles, dev, out)
     dx = torch.empty_like(x) if want_dx else None
     ws = _workspace(desc, dev)
     st = lib.qd_backward(ctypes.byref(desc), x.data_ptr(), wpack.data_ptr(), None, None, D.data_ptr(),

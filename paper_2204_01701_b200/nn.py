@@ -17,7 +17,37 @@ import torch
 from torch import nn
 
 from . import neurons
+from .dp import grad_ready, take_grad
 from .spec import QuadraticLayerSpec, fan_in, param_shapes, validate_device_spec
+
+
+def grad_sinks(named, needs):
+    """{name: bucket view} for the parameters whose gradients the library may write
+    straight into their data-parallel buckets (dp.take_grad); ``named`` maps
+    name -> parameter, ``needs`` name -> whether autograd wants its gradient"""
+    out = {}
+    for k, p in named.items():
+        if needs.get(k):
+            t = take_grad(p)
+            if t is not None:
+                out[k] = t
+    return out
+
+
+def settle_sinks(named, sinks, grads):
+    """After the kernels that wrote them are enqueued: mark the sunk parameters
+    ready and return the gradients autograd still has to accumulate (None for a
+    sunk one). A sink the library did not use (its buffer was replaced) goes back
+    through autograd, which adds into the zeroed bucket and fires the hook."""
+    res = {}
+    for k, g in grads.items():
+        t = sinks.get(k)
+        if t is not None and g is t:
+            grad_ready(named[k])
+            res[k] = None
+        else:
+            res[k] = g
+    return res
 
 
 class QuadFunction(torch.autograd.Function):
@@ -40,8 +70,10 @@ class QuadFunction(torch.autograd.Function):
         # a bias-free first-order stem, skips the bias reduction pass)
         bro = neurons.BIAS_ROLES.get(ctx.spec.family, ())
         want_db = any(ctx.needs_input_grad[3 + i] for i, r in enumerate(ctx.roles) if r in bro)
+        sinks = grad_sinks(ctx.params, {r: ctx.needs_input_grad[3 + i] for i, r in enumerate(ctx.roles)})
         grads, dx = neurons.symbolic_backward(ctx.spec, ctx.params, ctx.cache, gy,
-                                              want_dx=want_dx, want_db=want_db)
+                                              want_dx=want_dx, want_db=want_db, out=sinks)
+        grads = settle_sinks(ctx.params, sinks, grads)
         if dx is not None and dx.dtype != ctx.x_dtype:
             dx = dx.to(ctx.x_dtype)
         ctx.cache = None

@@ -111,3 +111,54 @@ def test_sgd_matches_reference_sgd_step():
         v = upd if v is None else 0.9 * v + upd
         p_ref = p_ref - 0.1 * v
         assert torch.allclose(p.detach(), p_ref, atol=1e-6)
+
+
+def test_direct_gradient_sink_reports_each_parameter_once():
+    """A function that writes its weight gradient straight into the bucket view
+    (dp.take_grad) and returns None: the parameter is reported once (ready(),
+    not again by the post-accumulate hook, which still fires), every bucket's
+    counter reaches exactly zero, and the gradients equal autograd's."""
+    from paper_2204_01701_b200.dp import BucketedAllReduce, grad_ready, take_grad
+
+    class SinkLinear(torch.autograd.Function):
+        @staticmethod
+        def forward(ctx, x, w, b):
+            ctx.save_for_backward(x)
+            ctx.w, ctx.b = w, b
+            return x @ w.t() + b
+
+        @staticmethod
+        def backward(ctx, g):
+            (x,) = ctx.saved_tensors
+            out = []
+            for p, grad in ((ctx.w, g.t() @ x), (ctx.b, g.sum(0))):
+                t = take_grad(p)
+                if t is None:
+                    out.append(grad)
+                else:
+                    t.copy_(grad)
+                    grad_ready(p)
+                    out.append(None)
+            return (g @ ctx.w, *out)
+
+    torch.manual_seed(0)
+    l1, l2 = torch.nn.Linear(5, 4), torch.nn.Linear(4, 3)
+    ref1, ref2 = torch.nn.Linear(5, 4), torch.nn.Linear(4, 3)
+    ref1.load_state_dict(l1.state_dict())
+    ref2.load_state_dict(l2.state_dict())
+    params = list(l1.parameters()) + list(l2.parameters())
+    red = BucketedAllReduce(params, bucket_mb=4e-5)  # several buckets
+    assert len(red.buckets) >= 2
+    x = torch.randn(6, 5)
+    for _ in range(2):  # the counters re-arm on reset()
+        red.reset()
+        h = SinkLinear.apply(x, l1.weight, l1.bias)
+        y = l2(torch.relu(h))  # l2 through autograd (AccumulateGrad + hook)
+        y.square().sum().backward()
+        assert red.pending == [0] * len(red.buckets)
+        red.finish()
+    for r in (ref1, ref2):
+        r.zero_grad()
+    ref2(torch.relu(ref1(x))).square().sum().backward()
+    for p, q in zip(params, list(ref1.parameters()) + list(ref2.parameters())):
+        assert torch.allclose(p.grad, q.grad, atol=1e-6)

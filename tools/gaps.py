@@ -53,3 +53,12 @@ print(f"{name}: span {(t1 - t0) / 1e3:.3f} ms, {len(evs)} kernels, idle {sum(g[0
       f"in {len(gaps)} gaps")
 for g, a, b in sorted(gaps, reverse=True)[:top]:
     print(f"  {g:8.1f} us  after {a}  before {b}")
+# per-kernel totals of the same replay
+tot = {}
+for e in evs:
+    k = e.name[:90]
+    t, c = tot.get(k, (0.0, 0))
+    tot[k] = (t + (e.time_range.end - e.time_range.start), c + 1)
+print(f"kernel time {sum(t for t, _ in tot.values()) / 1e3:.3f} ms (overlapping streams counted twice)")
+for k, (t, c) in sorted(tot.items(), key=lambda kv: -kv[1][0])[:int(os.environ.get("GAPS_TOP", "45"))]:
+    print(f"  {t / 1e3:7.3f} ms  x{c:<4d} {k}")
