@@ -1727,7 +1727,12 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     if (rc) return rc;
     WSplits uni;
     memset(&uni, 0, sizeof(uni));
-    launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, uni, dW, bpart, L.bs_split, db, st);
+    // the HBM-bound fold beside the dgrad (side stream, joined below) when there
+    // is one: the v1 dgrad grid often leaves SMs free (512@7: 98 of 148 CTAs)
+    const bool fold_main = !dx || (getenv("QD_FOLD_MAIN") && atoi(getenv("QD_FOLD_MAIN")));
+    if (!fold_main && !side) side = fork_side(st);
+    launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, uni, dW, bpart, L.bs_split, db,
+                      (!fold_main && side) ? side : st);
     }
   } else if (db[0] && (mat || P.nbias)) {
     launch_bias_finish(P, bpart, L.bs_split, db, st);
