@@ -1666,6 +1666,17 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     count_launch(pst, "prologue");
     if (mat || up) D = Dw;
   }
+  // v1 wgrad + fold on stream `ws_`, x operands chosen below
+  bool v1_side = false;
+  const void* v1_x0 = x;
+  auto run_v1_wgrad_and_fold = [&](cudaStream_t ws_) -> int {
+    int rc1 = run_wgrad_v1(P, v1_x0, x, D, (float*)(ws + L.off_WG), L.wg_split, ws_);
+    if (rc1) return rc1;
+    WSplits uni;
+    memset(&uni, 0, sizeof(uni));
+    launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, uni, dW, bpart, L.bs_split, db, ws_);
+    return QD_OK;
+  };
   // ---- wgrad ----
   if (dW[0]) {
     const void* x0 = x;
@@ -1675,6 +1686,7 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       launch_square(P, x, xs, st);
       x0 = xs;
     }
+    v1_x0 = x0;
     rc = QD_ERR_UNSUPPORTED;
     WSplits wsp;
     memset(&wsp, 0, sizeof(wsp));
@@ -1723,16 +1735,17 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
     } else if (rc != QD_ERR_UNSUPPORTED) {
       return rc;
     } else {
-    rc = run_wgrad_v1(P, x0, x1, D, (float*)(ws + L.off_WG), L.wg_split, st);
-    if (rc) return rc;
-    WSplits uni;
-    memset(&uni, 0, sizeof(uni));
-    // the HBM-bound fold beside the dgrad (side stream, joined below) when there
-    // is one: the v1 dgrad grid often leaves SMs free (512@7: 98 of 148 CTAs)
-    const bool fold_main = !dx || (getenv("QD_FOLD_MAIN") && atoi(getenv("QD_FOLD_MAIN")));
-    if (!fold_main && !side) side = fork_side(st);
-    launch_bwd_finish(P, (float*)(ws + L.off_WG), L.wg_split, uni, dW, bpart, L.bs_split, db,
-                      (!fold_main && side) ? side : st);
+      // v1 wgrad + its fold: with a dgrad, on the side stream AFTER the dgrad is
+      // enqueued (below), so the persistent dgrad takes its SMs first and the
+      // wgrad's CTAs fill the ones it leaves (512@7: 98 of 148) and then the rest;
+      // QD_V1_SERIAL=1: wgrad, fold, dgrad in order on `st`
+      v1_side = dx && !(getenv("QD_V1_SERIAL") && atoi(getenv("QD_V1_SERIAL")));
+      if (v1_side && !side) side = fork_side(st);
+      if (!side) v1_side = false;
+      if (!v1_side) {
+        rc = run_v1_wgrad_and_fold(st);
+        if (rc) return rc;
+      }
     }
   } else if (db[0] && (mat || P.nbias)) {
     launch_bias_finish(P, bpart, L.bs_split, db, st);
@@ -1766,6 +1779,10 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
       rc = run_conv(c.epi, c.nbk, D, nullptr, P.Jd, P.OW, P.OH, P.N, P.W, P.H, pad_eff, P.r, 0, wd, P.Cd, P.Kd,
                     c.b_rs_tile, c.b_rs_blk, c.tiles_nn, c.out_c_tile, dx, nullptr, nullptr, P.C, nob, xr, st,
                     (float*)(ws + L.off_SK), L.sz_SK);
+    if (rc) return rc;
+  }
+  if (v1_side) {
+    rc = run_v1_wgrad_and_fold(side);
     if (rc) return rc;
   }
   if (side) join_side(st, side);
