@@ -317,6 +317,13 @@ def config_of(wl, name, ngpu):
 # ---------------------------------------------------------------------------
 # GPU side
 # ---------------------------------------------------------------------------
+def _dist(world):
+    """a process group is up: world > 1, or QD_DIST_FORCE=1 (dev: the NCCL path --
+    process group, collectives, graph-captured bucket all-reduces -- exercised by
+    a single-rank torchrun on one GPU)"""
+    return world > 1 or os.environ.get("QD_DIST_FORCE") == "1"
+
+
 def run_ours(args, wl, wl_name):
     import torch
     import torch.distributed as dist
@@ -328,7 +335,7 @@ def run_ours(args, wl, wl_name):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if _dist(world):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
     fam, kind, n, c, f, h, w, r, s, p, dts = wl
@@ -348,18 +355,30 @@ def run_ours(args, wl, wl_name):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
 
-    def compute(want_dx=True, want_dw=True):
+    # the layer's weight / bias gradients land in one flat fp32 buffer (the
+    # library writes them there directly), so the data-parallel exchange is one
+    # all-reduce with no gather copy; captured into the step's graph below
+    gorder = [r_ for r_ in neurons.GRAD_ORDER[fam] if r_ in params]
+    gflat = torch.zeros(sum(params[r_].numel() for r_ in gorder), dtype=torch.float32, device=dev)
+    gviews, o_ = {}, 0
+    for r_ in gorder:
+        gviews[r_] = gflat[o_:o_ + params[r_].numel()].view(params[r_].shape)
+        o_ += params[r_].numel()
+
+    def compute(want_dx=True, want_dw=True, out=gviews):
         y, cache = neurons.forward(spec, params, x, dtype=dt)
         grads, dx = neurons.symbolic_backward(spec, params, cache, gy, want_dx=want_dx,
-                                              want_dw=want_dw)
+                                              want_dw=want_dw, out=out)
         return y, grads, dx
 
     def exchange(grads):
-        # the one data-parallel exchange: rank mean of dW / db.
-        # Kept outside the captured graph: NCCL runs eagerly after each replay.
-        if world > 1:
-            flat = torch.cat([t_.reshape(-1) for t_ in grads.values()])
-            dist.all_reduce(flat, op=dist.ReduceOp.AVG)
+        # the one data-parallel exchange: rank mean of dW / db
+        if _dist(world):
+            if all(grads[r_] is gviews[r_] for r_ in gorder if r_ in grads):
+                dist.all_reduce(gflat, op=dist.ReduceOp.AVG)
+            else:
+                flat = torch.cat([t_.reshape(-1) for t_ in grads.values()])
+                dist.all_reduce(flat, op=dist.ReduceOp.AVG)
 
     def step():
         y, grads, dx = compute()
@@ -397,24 +416,24 @@ def run_ours(args, wl, wl_name):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             _, g_static, _ = compute()
+            exchange(g_static)  # the NCCL all-reduce is part of the replayed step
 
         def run():
             graph.replay()
-            exchange(g_static)
         for _ in range(args.warmup):
             run()
     torch.cuda.synchronize()
-    if world > 1:
+    if _dist(world):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ms = timed(run, args.steps)
     launches = per_step_launches * args.steps
-    if world > 1:
+    if _dist(world):
         dist.barrier()
     torch.cuda.synchronize()
     total_ms = sum(ms)
-    if world > 1:
+    if _dist(world):
         tt = torch.tensor([total_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         total_ms = float(tt.item())
@@ -560,7 +579,7 @@ def run_ours(args, wl, wl_name):
 
     pipelined_e2e(3, h2d_in, compute_e2e, d2h_out)  # warm-up
     e2e_step_ms = pipelined_e2e(args.steps, h2d_in, compute_e2e, d2h_out)
-    if world > 1:
+    if _dist(world):
         tt = torch.tensor([e2e_step_ms], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e2e_step_ms = float(tt.item())
@@ -574,10 +593,10 @@ def run_ours(args, wl, wl_name):
     for net in args.nets:
         nets[net] = measure_net(args, net, world, rank, local, dev)
 
-    if world > 1:
+    if _dist(world):
         dist.barrier()
     if rank != 0:
-        if world > 1:
+        if _dist(world):
             dist.destroy_process_group()
         return 0
 
@@ -609,7 +628,7 @@ def run_ours(args, wl, wl_name):
            "path": {0: "cuda-core", 1: "tcgen05", 2: "depth-wise", 3: "tcgen05 fp32 (split bf16 x3)"}[
                neurons.device_path(spec, x.shape, dt)]}
     print(json.dumps(out), flush=True)
-    if world > 1:
+    if _dist(world):
         dist.destroy_process_group()
     return 0
 
@@ -707,13 +726,13 @@ def run_net(args, name):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
+    if _dist(world):
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         dist.init_process_group("nccl", device_id=dev)
     out = measure_net(args, name, world, rank, local, dev)
     if rank == 0:
         print(json.dumps(out), flush=True)
-    if world > 1:
+    if _dist(world):
         dist.destroy_process_group()
     return 0
 
@@ -774,7 +793,7 @@ def measure_net(args, name, world, rank, local, dev):
             print(f"[bench] CUDA-graph capture failed ({type(e).__name__}: {e}); timing the eager step",
                   file=sys.stderr)
             ok = 0
-        if world > 1:  # every rank must take the same path
+        if _dist(world):  # every rank must take the same path
             t = torch.tensor([ok], device=dev, dtype=torch.int32)
             dist.all_reduce(t, op=dist.ReduceOp.MIN)
             ok = int(t.item())
@@ -803,13 +822,13 @@ def measure_net(args, name, world, rank, local, dev):
     step()
     torch.cuda.synchronize()
     per_step = launches_graph if graph is not None else _lib.launch_count() - l0
-    if world > 1:
+    if _dist(world):
         dist.barrier()
     torch.cuda.synchronize()
     with ClockSampler(local) as clk:
         ms = timed(step, args.steps)
     tot = sum(ms)
-    if world > 1:
+    if _dist(world):
         tt = torch.tensor([tot], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         tot = float(tt.item())
@@ -839,11 +858,11 @@ def measure_net(args, name, world, rank, local, dev):
 
     pipelined_e2e(3, h2d_in, compute_e2e, d2h_out)  # warm-up
     e_step = pipelined_e2e(args.steps, h2d_in, compute_e2e, d2h_out)
-    if world > 1:
+    if _dist(world):
         tt = torch.tensor([e_step], device=dev, dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         e_step = float(tt.item())
-    if world > 1:
+    if _dist(world):
         dist.barrier()
     red.remove()
     if rank != 0:

@@ -59,6 +59,8 @@ class BucketedAllReduce:
         self.group = group
         self.direct = direct and reduce_dtype == torch.float32
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        # collectives at world > 1 (QD_DIST_FORCE=1: also on a single-rank group, dev)
+        self.collective = self.world > 1 or (_os.environ.get("QD_DIST_FORCE") == "1" and dist.is_initialized())
         params = [p for p in params if p.requires_grad]
         order = list(reversed(params))
         cap = int(bucket_mb * (1 << 20) / 4)
@@ -99,7 +101,7 @@ class BucketedAllReduce:
 
     def _ready(self, bi):
         self.pending[bi] -= 1
-        if self.pending[bi] == 0 and self.world > 1:
+        if self.pending[bi] == 0 and self.collective:
             op = dist.ReduceOp.AVG if dist.get_backend(self.group) == "nccl" else dist.ReduceOp.SUM
             self.handles[bi] = dist.all_reduce(self.buckets[bi][0], op=op, group=self.group, async_op=True)
 
@@ -141,7 +143,7 @@ class BucketedAllReduce:
     def finish(self):
         """wait for every bucket's all-reduce; gradients are then the rank mean"""
         for bi, h in enumerate(self.handles):
-            if self.world > 1:
+            if self.collective:
                 if h is None:  # a bucket whose params got no gradient this step
                     op = dist.ReduceOp.AVG if dist.get_backend(self.group) == "nccl" else dist.ReduceOp.SUM
                     h = dist.all_reduce(self.buckets[bi][0], op=op, group=self.group, async_op=True)
