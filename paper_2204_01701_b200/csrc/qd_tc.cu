@@ -1019,6 +1019,23 @@ static bool init_driver() {
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn() { return g_encode; }
+
+// the driver call needs a current context: a host thread whose first CUDA call is
+// ours (e.g. torch's autograd worker running a backward) has none yet
+// (CUDA_ERROR_INVALID_CONTEXT); binding the device's primary context through the
+// runtime and retrying fixes that
+CUresult tc_encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* ptr, const cuuint64_t* dims,
+                         const cuuint64_t* strides, const cuuint32_t* box, const cuuint32_t* es,
+                         CUtensorMapInterleave il, CUtensorMapSwizzle sw, CUtensorMapL2promotion l2,
+                         CUtensorMapFloatOOBfill oob) {
+  CUresult r = g_encode(m, dt, rank, ptr, dims, strides, box, es, il, sw, l2, oob);
+  if (r == CUDA_ERROR_INVALID_CONTEXT) {
+    cudaFree(nullptr);  // binds the current device's primary context to this thread
+    cudaGetLastError();
+    r = g_encode(m, dt, rank, ptr, dims, strides, box, es, il, sw, l2, oob);
+  }
+  return r;
+}
 int tc_num_sms() { return g_num_sms > 0 ? g_num_sms : 148; }
 
 static int plain_blocks(int ch);
@@ -1100,9 +1117,9 @@ static int make_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t*
   }
   // trav > 1: traversal stride along W and H (the box spans trav x the pixels it loads)
   cuuint32_t es[5] = {1, (cuuint32_t)trav, (cuuint32_t)trav, 1, 1};
-  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = tc_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box,
+                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(QD_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d)", (int)r);
   return QD_OK;
 }

@@ -965,6 +965,10 @@ static int max_pair_clusters(K kernel, int threads, size_t smem) {
   return n;
 }
 extern PFN_cuTensorMapEncodeTiled_v12000 tc_encode_fn();
+extern CUresult tc_encode_tiled(CUtensorMap* m, CUtensorMapDataType dt, cuuint32_t rank, void* ptr,
+                                const cuuint64_t* dims, const cuuint64_t* strides, const cuuint32_t* box,
+                                const cuuint32_t* es, CUtensorMapInterleave il, CUtensorMapSwizzle sw,
+                                CUtensorMapL2promotion l2, CUtensorMapFloatOOBfill oob);
 extern int tc_num_sms();
 
 struct C2Plan {
@@ -981,7 +985,7 @@ static int c2_map(CUtensorMap* m, const void* ptr, int rank, const cuuint64_t* d
     acc *= dims[i];
   }
   cuuint32_t es[5] = {1, 1, 1, 1, 1};
-  CUresult r = tc_encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box,
+  CUresult r = tc_encode_tiled(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(ptr), dims, strides, box,
                               es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) return set_error(QD_ERR_CUDA, "cuTensorMapEncodeTiled (conv2) failed (%d)", (int)r);

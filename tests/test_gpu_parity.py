@@ -969,3 +969,34 @@ def test_wgrad_pair_matches_single(shape, monkeypatch):
     monkeypatch.delenv("QD_WPAIR")
     for role in base[3]:
         assert Q.rel_err(pair[3][role], base[3][role]) <= 1e-5, role
+
+
+def test_backward_on_a_fresh_host_thread():
+    """The C ABI from a host thread whose first CUDA call it is (torch's autograd
+    worker runs backward passes on such threads): the tensor-map encode binds the
+    device's primary context instead of failing with CUDA_ERROR_INVALID_CONTEXT."""
+    import threading
+    from paper_2204_01701_b200 import neurons
+    x, P, g = Q.synthetic_layer("proposed", "conv", 4, 64, 64, 16, 16, 3, 1, 1, seed=2)
+    ref = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
+    spec = _spec("proposed", "conv", 64, 64, 3, 1, 1)
+    dev = torch.device("cuda")
+    params = {r: torch.as_tensor(v, dtype=torch.float32, device=dev) for r, v in P.items()}
+    y, cache = neurons.forward(spec, params, torch.as_tensor(x, device=dev).bfloat16())
+    gt = torch.as_tensor(g, device=dev).bfloat16()
+    out, err = {}, []
+
+    def work():
+        try:
+            grads, dx = neurons.symbolic_backward(spec, params, cache, gt)
+            torch.cuda.synchronize()
+            out.update(grads=grads, dx=dx)
+        except Exception as e:  # noqa: BLE001 - reported below
+            err.append(e)
+    t = threading.Thread(target=work)
+    t.start()
+    t.join()
+    assert not err, err
+    assert (out["dx"].double().cpu().numpy() == ref[4]).all()
+    for role in ref[3]:
+        assert (out["grads"][role].double().cpu().numpy() == ref[3][role]).all(), role
