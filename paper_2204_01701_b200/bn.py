@@ -260,28 +260,36 @@ class _BNFunction(torch.autograd.Function):
     @staticmethod
     def backward(ctx, dz):
         y, gamma, beta, sm, si = ctx.saved_tensors
-        lib = _lib.load()
-        yr = _rows(y)
-        M, C = yr.shape
-        desc = _lib.QdDesc()
-        desc.family, desc.kind = _lib.FAMILY_CODE["first_order"], _lib.KIND_CODE["fc"]
-        desc.dtype = _dtype_code(y)
-        desc.N, desc.C, desc.H, desc.W, desc.F = M, C, 1, 1, C
-        desc.r, desc.stride, desc.pad, desc.flags = 1, 1, 0, 0
-        dy = torch.empty_like(y)
-        named = {"gamma": ctx.gamma, "beta": ctx.beta}
-        sinks = grad_sinks(named, {"gamma": ctx.needs_input_grad[1], "beta": ctx.needs_input_grad[2]})
-        dgamma = _f32(C, y.device, sinks.get("gamma"))
-        dbeta = _f32(C, y.device, sinks.get("beta"))
-        ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, C), dtype=torch.uint8, device=y.device)
-        dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
-        st = lib.qd_bn_backward_D(ctypes.byref(desc), dzr.data_ptr(), y.data_ptr(), None, None, gamma.data_ptr(),
-                                  beta.data_ptr(), sm.data_ptr(), si.data_ptr(), int(ctx.relu), dy.data_ptr(),
-                                  dgamma.data_ptr(), dbeta.data_ptr(), _lib.ptr3(), ws.data_ptr(),
-                                  torch.cuda.current_stream().cuda_stream)
-        _lib.raise_for(st, "qd_bn_backward_D (bn only)")
-        gr = settle_sinks(named, sinks, {"gamma": dgamma, "beta": dbeta})
-        return dy, gr["gamma"], gr["beta"], None, None
+        dy, dgamma, dbeta = _bn_backward_only(y, dz, gamma, beta, sm, si, ctx.relu,
+                                              {"gamma": ctx.gamma, "beta": ctx.beta},
+                                              {"gamma": ctx.needs_input_grad[1], "beta": ctx.needs_input_grad[2]})
+        return dy, dgamma, dbeta, None, None
+
+
+def _bn_backward_only(y, dz, gamma, beta, sm, si, relu, named, needs):
+    """dL/dy, dgamma, dbeta of a BN (+ReLU) from dz (the mask recomputed from y);
+    gamma / beta gradients sunk into their data-parallel buckets when allowed"""
+    lib = _lib.load()
+    yr = _rows(y)
+    M, C = yr.shape
+    desc = _lib.QdDesc()
+    desc.family, desc.kind = _lib.FAMILY_CODE["first_order"], _lib.KIND_CODE["fc"]
+    desc.dtype = _dtype_code(y)
+    desc.N, desc.C, desc.H, desc.W, desc.F = M, C, 1, 1, C
+    desc.r, desc.stride, desc.pad, desc.flags = 1, 1, 0, 0
+    dy = torch.empty_like(y)
+    sinks = grad_sinks(named, needs)
+    dgamma = _f32(C, y.device, sinks.get("gamma"))
+    dbeta = _f32(C, y.device, sinks.get("beta"))
+    ws = torch.empty(lib.qd_bn_workspace_bytes(M, C, C), dtype=torch.uint8, device=y.device)
+    dzr = _rows(dz.contiguous(memory_format=torch.channels_last) if dz.dim() == 4 else dz.contiguous())
+    st = lib.qd_bn_backward_D(ctypes.byref(desc), dzr.data_ptr(), y.data_ptr(), None, None, gamma.data_ptr(),
+                              beta.data_ptr(), sm.data_ptr(), si.data_ptr(), int(relu), dy.data_ptr(),
+                              dgamma.data_ptr(), dbeta.data_ptr(), _lib.ptr3(), ws.data_ptr(),
+                              torch.cuda.current_stream().cuda_stream)
+    _lib.raise_for(st, "qd_bn_backward_D (bn only)")
+    gr = settle_sinks(named, sinks, {"gamma": dgamma, "beta": dbeta})
+    return dy, gr["gamma"], gr["beta"]
 
 
 def _ref_batchnorm(y, gamma, beta, running_mean, running_var, momentum, eps, training):

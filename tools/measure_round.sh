@@ -31,3 +31,8 @@ python bench.py --steps 2 --warmup 3 --nets "" --no-cpu > ${o}_plain_launch.log 
   ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file ${o}_launches.csv \
       python bench.py --steps 2 --warmup 3 --nets "" --no-cpu > ${o}_ncu_launch.log 2>&1
 echo measure done
+# single-rank torchrun with every collective on (NCCL process group, graph-captured all-reduces)
+QD_DIST_FORCE=1 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29531 \
+    bench.py --gpus 1 --steps 20 --warmup 5 --no-cpu > ${o}_bench_dist1.json 2> ${o}_bench_dist1.err
+python tools/gaps.py qresnet18 10 > ${o}_resnet_kernels.txt 2>&1
+echo measure2 done
