@@ -81,10 +81,12 @@ __device__ __forceinline__ ConvWork conv_work(const ConvArgs& a, int wi, int KB)
   return w;
 }
 
-template <int EPI, int NB>
+// PAIR: the CTA-pair form (cta_group::2, M = 256 over two SMs), each CTA holding
+// its own A tile but only half of B (NB x 32 rows)
+template <int EPI, int NB, int PAIR = 0>
 struct ConvCfg {
   static constexpr int A_BYTES = 128 * 128;
-  static constexpr int B_BYTES = NB * 64 * 128;
+  static constexpr int B_BYTES = NB * 64 * 128 / (PAIR ? 2 : 1);
   static constexpr int STAGE = A_BYTES + B_BYTES;
   static constexpr int NOUT = (EPI == EPI_PROPOSED || EPI == EPI_T4) ? 3 : (EPI == EPI_PLAIN ? NB : 1);
   static constexpr int STG = NOUT * 128 * 128;
@@ -114,13 +116,13 @@ __device__ __forceinline__ void stage_store16(uint8_t* tile, int row, int j, con
   *reinterpret_cast<uint4*>(rowp + ((q1 ^ (row & 7)) << 4)) = hi;
 }
 
-template <int EPI, int NB>
+template <int EPI, int NB, int PAIR = 0>
 __global__ void __launch_bounds__(256, 1)
     conv_gemm_kernel(const __grid_constant__ CUtensorMap mapA0, const __grid_constant__ CUtensorMap mapA1,
                      const __grid_constant__ CUtensorMap mapB, const __grid_constant__ CUtensorMap mapO0,
                      const __grid_constant__ CUtensorMap mapO1, const __grid_constant__ CUtensorMap mapO2,
                      const ConvArgs args) {
-  using Cfg = ConvCfg<EPI, NB>;
+  using Cfg = ConvCfg<EPI, NB, PAIR>;
   constexpr int STAGES = Cfg::STAGES;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -134,6 +136,18 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tmem_slot = (uint32_t*)(tempty + 2);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // PAIR: CTA r of a cluster takes M tile 2 m + r of the pair's work item; every
+  // stage completes on CTA0's full barrier, the MMA (CTA0) commits to both CTAs
+  const uint32_t rank = PAIR ? ptx::cluster_rank() : 0;
+  const int wstart = PAIR ? (int)(blockIdx.x >> 1) : (int)blockIdx.x;
+  const int wstep = PAIR ? (int)(gridDim.x >> 1) : (int)gridDim.x;
+  auto tile_of = [&](int t, int& ntile, int& w0, int& h0, int& n0) {
+    ntile = t % args.tiles_nn;
+    const int mt = PAIR ? 2 * (t / args.tiles_nn) + (int)rank : t / args.tiles_nn;
+    const int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
+    const int tn = mt / (args.tiles_w * args.tiles_h);  // >= tiles_n: an empty tile (all OOB)
+    w0 = tw * args.Wb; h0 = th * args.Hb; n0 = tn * args.Nb;
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&mapA0);
@@ -145,16 +159,21 @@ __global__ void __launch_bounds__(256, 1)
     }
     for (int i = 0; i < 2; ++i) {
       ptx::mbar_init(&tfull[i], 1);
-      ptx::mbar_init(&tempty[i], 4);
+      ptx::mbar_init(&tempty[i], PAIR ? 8 : 4);
     }
     ptx::fence_barrier_init();
   }
   if (warp == 2) {
-    ptx::tmem_alloc(tmem_slot, 512);
-    ptx::tmem_relinquish();
+    if (PAIR) {
+      ptx::tmem_alloc2(tmem_slot, 512);
+    } else {
+      ptx::tmem_alloc(tmem_slot, 512);
+      ptx::tmem_relinquish();
+    }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (PAIR) ptx::cluster_sync();
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_slot;
 
@@ -168,21 +187,19 @@ __global__ void __launch_bounds__(256, 1)
       // ===== TMA producer =====
       int stage = 0;
       uint32_t phase = 0;
-      const uint32_t bytes = (uint32_t)(args.box_rows * 128 + Cfg::B_BYTES);
+      const uint32_t bytes = (uint32_t)(args.box_rows * 128 + Cfg::B_BYTES) * (PAIR ? 2 : 1);
       const int ss = args.sstride;
-      for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x) {
+      for (int wi = wstart; wi < NWORK; wi += wstep) {
         const ConvWork cw = conv_work(args, wi, KB);
         const int t = cw.t;
-        int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
-        int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
-        int tn = mt / (args.tiles_w * args.tiles_h);
-        int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
+        int ntile, w0, h0, n0;
+        tile_of(t, ntile, w0, h0, n0);
         // class mode: first tap of the class's parity and its tap count along x
         const int ey0 = (args.pad_eff - cw.ph) & 1, ex0 = (args.pad_eff - cw.pw) & 1;
         const int ntx = (args.r - ex0 + 1) >> 1;
         for (int kb = cw.kb0; kb < cw.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
-          ptx::mbar_arrive_expect_tx(&full[stage], bytes);
+          if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], bytes);
           int half = kb / args.kb_half, kk = kb % args.kb_half;
           int tap = kk / args.cblks, cb = kk % args.cblks;
           int ax, ay, bk = kb;
@@ -197,18 +214,30 @@ __global__ void __launch_bounds__(256, 1)
             ay = ss * h0 + ey - args.pad_eff;
           }
           const CUtensorMap* ma = (half > 0 && half == args.dual) ? &mapA1 : &mapA0;
-          ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
+          if (PAIR) {
+            // this CTA's half of the B tile: rows j in [rank NB 32, (rank + 1) NB 32) as 32-row boxes
+            const uint32_t fb = ptx::peer0(&full[stage]);
+            ptx::tma4_cg2(ma, fb, sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
 #pragma unroll
-          for (int i = 0; i < NB; ++i)
-            ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, bk * 64,
-                             ntile * args.b_rs_tile + i * args.b_rs_blk);
+            for (int i = 0; i < NB; ++i) {
+              const int j0 = (int)rank * NB * 32 + i * 32;
+              ptx::tma2_cg2(&mapB, fb, sB + stage * Cfg::B_BYTES + i * 4096, bk * 64,
+                            ntile * args.b_rs_tile + (j0 / 64) * args.b_rs_blk + j0 % 64);
+            }
+          } else {
+            ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
+#pragma unroll
+            for (int i = 0; i < NB; ++i)
+              ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, bk * 64,
+                               ntile * args.b_rs_tile + i * args.b_rs_blk);
+          }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
         }
       }
     }
-  } else if (warp == 1) {
+  } else if (warp == 1 && rank == 0) {
     // ===== MMA issuer: warp-wide loop (uniform datapath), one elected lane issues =====
-    constexpr uint32_t IDESC = ptx::idesc_bf16(128, NB * 64, false, false);
+    constexpr uint32_t IDESC = ptx::idesc_bf16(PAIR ? 256 : 128, NB * 64, false, false);
     constexpr uint32_t DHI = ptx::sw128_desc_hi(1024);
     const bool leader = ptx::elect_one();
     const uint32_t a_lo0 = ptx::sw128_desc_lo(ptx::smem_u32(sA), 16);
@@ -216,7 +245,7 @@ __global__ void __launch_bounds__(256, 1)
     int stage = 0;
     uint32_t phase = 0;
     int it = 0;
-    for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x, ++it) {
+    for (int wi = wstart; wi < NWORK; wi += wstep, ++it) {
       const ConvWork cw = conv_work(args, wi, KB);
       const int kb0 = cw.kb0, kb1 = cw.kb1;
       int as = it & 1;
@@ -231,15 +260,24 @@ __global__ void __launch_bounds__(256, 1)
         const uint32_t b_lo = b_lo0 + stage * (Cfg::B_BYTES >> 4);
         if (leader) {
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            ptx::mma_bf16(d_tmem, ptx::mk_desc(DHI, a_lo + 2 * k), ptx::mk_desc(DHI, b_lo + 2 * k), IDESC,
-                          (kb != kb0) || (k != 0));
-          ptx::mma_commit(&empty[stage]);
+          for (int k = 0; k < 4; ++k) {
+            if (PAIR)
+              ptx::mma_cg2(d_tmem, ptx::mk_desc(DHI, a_lo + 2 * k), ptx::mk_desc(DHI, b_lo + 2 * k), IDESC,
+                           ((kb != kb0) || (k != 0)) ? 1u : 0u);
+            else
+              ptx::mma_bf16(d_tmem, ptx::mk_desc(DHI, a_lo + 2 * k), ptx::mk_desc(DHI, b_lo + 2 * k), IDESC,
+                            (kb != kb0) || (k != 0));
+          }
+          if (PAIR) ptx::commit_mc(&empty[stage]);
+          else ptx::mma_commit(&empty[stage]);
         }
         __syncwarp();
         if (++stage == STAGES) { stage = 0; phase ^= 1; }
       }
-      if (leader) ptx::mma_commit(&tfull[as]);
+      if (leader) {
+        if (PAIR) ptx::commit_mc(&tfull[as]);
+        else ptx::mma_commit(&tfull[as]);
+      }
       __syncwarp();
     }
   } else if (warp >= 4) {
@@ -247,14 +285,18 @@ __global__ void __launch_bounds__(256, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const int etid = threadIdx.x - 128;
+    // TMEM hand-back: PAIR -> CTA0's barrier (count 8: both CTAs' epilogue warps)
+    const uint32_t tempty0 = PAIR ? ptx::peer0(&tempty[0]) : 0u;
+    auto hand_back = [&](int as_) {
+      if (PAIR) ptx::arrive_remote(tempty0 + as_ * 8);
+      else ptx::mbar_arrive(&tempty[as_]);
+    };
     int it = 0;
-    for (int wi = blockIdx.x; wi < NWORK; wi += gridDim.x, ++it) {
+    for (int wi = wstart; wi < NWORK; wi += wstep, ++it) {
       const ConvWork cw = conv_work(args, wi, KB);
       const int t = cw.t, ks = cw.ks;
-      int ntile = t % args.tiles_nn, mt = t / args.tiles_nn;
-      int tw = mt % args.tiles_w, th = (mt / args.tiles_w) % args.tiles_h;
-      int tn = mt / (args.tiles_w * args.tiles_h);
-      int w0 = tw * args.Wb, h0 = th * args.Hb, n0 = tn * args.Nb;
+      int ntile, w0, h0, n0;
+      tile_of(t, ntile, w0, h0, n0);
       int as = it & 1;
       uint32_t aph = (it >> 1) & 1;
       if (EPI == EPI_PLAIN && args.cls) {
@@ -298,7 +340,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+        if (lane == 0) hand_back(as);
         continue;
       }
       if (args.part) {
@@ -328,7 +370,7 @@ __global__ void __launch_bounds__(256, 1)
         }
         ptx::tc_fence_before();
         __syncwarp();
-        if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+        if (lane == 0) hand_back(as);
         continue;
       }
       // previous tile's TMA stores must have finished reading the staging tiles
@@ -411,7 +453,7 @@ __global__ void __launch_bounds__(256, 1)
       // accumulator drained: hand it back to the MMA warp
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(&tempty[as]);
+      if (lane == 0) hand_back(as);
       ptx::fence_proxy_async_smem();
       ptx::named_bar_sync(1, 128);
       if (etid == 0) {
@@ -431,10 +473,18 @@ __global__ void __launch_bounds__(256, 1)
     if (etid == 0) ptx::bulk_wait0();
   }
   ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, 512);
+  if (PAIR) {
+    ptx::cluster_sync();
+    if (warp == 2) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc2(tmem_base, 512);
+    }
+  } else {
+    __syncthreads();
+    if (warp == 2) {
+      ptx::tc_fence_after();
+      ptx::tmem_dealloc(tmem_base, 512);
+    }
   }
 }
 
@@ -1132,9 +1182,9 @@ static int map_act(CUtensorMap* m, const void* p, int Cch, int W, int H, int N, 
   cuuint32_t box[4] = {64, (cuuint32_t)(Wb * trav), (cuuint32_t)(Hb * trav), (cuuint32_t)Nb};
   return make_map(m, p, 4, dims, box, trav);
 }
-static int map_rows(CUtensorMap* m, const void* p, int K, int rows) {
+static int map_rows(CUtensorMap* m, const void* p, int K, int rows, int box_rows = 64) {
   cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)rows};
-  cuuint32_t box[2] = {64, 64};
+  cuuint32_t box[2] = {64, (cuuint32_t)box_rows};
   return make_map(m, p, 2, dims, box);
 }
 
@@ -1176,14 +1226,62 @@ static Box choose_box(int W, int H, int N, int cap, bool exact) {
   return best;
 }
 
-template <int EPI, int NB>
+// co-resident 2-CTA clusters of a kernel at this smem (cached per kernel / device)
+template <typename K>
+static int conv_pair_clusters(K kernel, size_t smem) {
+  thread_local int maxc_[kMaxDev] = {};
+  int& maxc = maxc_[cur_device()];
+  if (maxc == 0) {
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(2 * 148, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = smem;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int n = 0;
+    if (cudaOccupancyMaxActiveClusters(&n, (void*)kernel, &cfg) != cudaSuccess) {
+      cudaGetLastError();
+      n = 0;
+    }
+    maxc = n > 0 ? n : g_num_sms / 2;
+  }
+  return maxc;
+}
+
+template <int EPI, int NB, int PAIR = 0>
 static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B, const CUtensorMap& O0,
                        const CUtensorMap& O1, const CUtensorMap& O2, const ConvArgs& args, cudaStream_t st) {
-  using Cfg = ConvCfg<EPI, NB>;
-  raise_smem_attr((const void*)conv_gemm_kernel<EPI, NB>, Cfg::SMEM);
+  using Cfg = ConvCfg<EPI, NB, PAIR>;
+  auto kernel = conv_gemm_kernel<EPI, NB, PAIR>;
+  raise_smem_attr((const void*)kernel, Cfg::SMEM);
   const int nwork = args.cls ? 4 * args.cls_tiles : args.total_tiles * args.ksplit;
-  int grid = nwork < g_num_sms ? nwork : g_num_sms;
-  conv_gemm_kernel<EPI, NB><<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
+  if (!PAIR) {
+    int grid = nwork < g_num_sms ? nwork : g_num_sms;
+    kernel<<<grid, 256, Cfg::SMEM, st>>>(A0, A1, B, O0, O1, O2, args);
+  } else {
+    int clusters = conv_pair_clusters(kernel, Cfg::SMEM);
+    if (nwork < clusters) clusters = nwork;
+    cudaLaunchConfig_t cfg;
+    memset(&cfg, 0, sizeof(cfg));
+    cfg.gridDim = dim3(2 * clusters, 1, 1);
+    cfg.blockDim = dim3(256, 1, 1);
+    cfg.dynamicSmemBytes = Cfg::SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    cudaLaunchKernelEx(&cfg, kernel, A0, A1, B, O0, O1, O2, args);
+  }
   count_launch(st, "conv_gemm");
   return check_launch("conv_gemm");
 }
@@ -1191,8 +1289,9 @@ static int launch_conv(const CUtensorMap& A0, const CUtensorMap& A1, const CUten
 template <int EPI, int NB>
 static int launch_conv_split(const CUtensorMap& A0, const CUtensorMap& A1, const CUtensorMap& B,
                              const CUtensorMap& O0, const CUtensorMap& O1, const CUtensorMap& O2,
-                             const ConvArgs& args, void* o0, void* o1, void* o2, cudaStream_t st) {
-  int rc = launch_conv<EPI, NB>(A0, A1, B, O0, O1, O2, args, st);
+                             const ConvArgs& args, void* o0, void* o1, void* o2, cudaStream_t st, bool pair) {
+  int rc = pair ? launch_conv<EPI, NB, 1>(A0, A1, B, O0, O1, O2, args, st)
+                : launch_conv<EPI, NB>(A0, A1, B, O0, O1, O2, args, st);
   if (rc || args.ksplit <= 1) return rc;
   const long long n = args.Mpix * (args.Cout / 8);
   splitk_finish_kernel<EPI, NB><<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
@@ -1204,8 +1303,8 @@ static int launch_conv_split(const CUtensorMap& A0, const CUtensorMap& A1, const
 
 // K slices for a conv_gemm launch: only when the output grid leaves most SMs idle,
 // each slice >= 8 k-blocks (K 512); QD_NO_SPLITK=1 disables
-static int conv_ksplit(long long tiles, int KB) {
-  const int sms = tc_num_sms();
+static int conv_ksplit(long long tiles, int KB, int sms = 0) {
+  if (sms <= 0) sms = tc_num_sms();
   if (getenv("QD_NO_SPLITK") || tiles * 2 > sms) return 1;
   long long S = sms / tiles;
   if (S > KB / 8) S = KB / 8;
@@ -1326,18 +1425,23 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
                     float* skpart = nullptr, size_t skbytes = 0, int trav = 1, int cls = 0, int Hx = 0,
                     int Wx = 0, int force_part = 0, int* ksplit_out = nullptr) {
   Box bx = choose_box(OWg, OHg, N, 128, false);
+  const long long mtiles = (long long)bx.tw * bx.th * bx.tn;
+  // CTA pairs (M = 256 over two SMs, each holding half of the weight tile): only
+  // with QD_CPAIR=1 while being measured, never for the raw-accumulator modes
+  const char* cp = getenv("QD_CPAIR");
+  const bool pair = cp && atoi(cp) && mtiles >= 2 && !force_part;
   CUtensorMap A0, A1, B, O0, O1, O2;
   int rc;
   if ((rc = map_act(&A0, a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb, trav))) return rc;
   if ((rc = map_act(&A1, a1 ? a1 : a0, Cin, Win, Hin, N, bx.Wb, bx.Hb, bx.Nb, trav))) return rc;
-  if ((rc = map_rows(&B, wmat, wK, wrows))) return rc;
+  if ((rc = map_rows(&B, wmat, wK, wrows, pair ? 32 : 64))) return rc;
   if ((rc = map_act(&O0, o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
   if ((rc = map_act(&O1, o1 ? o1 : o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
   if ((rc = map_act(&O2, o2 ? o2 : o0, Cout, OWg, OHg, N, bx.Wb, bx.Hb, bx.Nb))) return rc;
   ConvArgs g;
   memset(&g, 0, sizeof(g));
   g.tiles_w = bx.tw; g.tiles_h = bx.th; g.tiles_nn = tiles_nn;
-  g.total_tiles = bx.tw * bx.th * bx.tn * tiles_nn;
+  g.total_tiles = (int)((pair ? (mtiles + 1) / 2 : mtiles) * tiles_nn);  // PAIR: pair tiles
   g.Wb = bx.Wb; g.Hb = bx.Hb; g.Nb = bx.Nb; g.box_rows = bx.Wb * bx.Hb * bx.Nb;
   g.OHg = OHg; g.OWg = OWg; g.Ng = N;
   g.r = r; g.pad_eff = pad_eff; g.cblks = Cin / 64;
@@ -1350,7 +1454,7 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
   g.kb_per = KB;
   g.Mpix = (long long)N * OHg * OWg;
   g.part_ld = tiles_nn * nbk * 64;
-  const int S = conv_ksplit(g.total_tiles, KB);
+  const int S = conv_ksplit(g.total_tiles, KB, pair ? tc_num_sms() / 2 : 0);
   if (S > 1 && skpart && (size_t)S * g.Mpix * g.part_ld * 4 <= skbytes) {
     g.kb_per = (KB + S - 1) / S;
     g.ksplit = (KB + g.kb_per - 1) / g.kb_per;
@@ -1396,7 +1500,7 @@ static int run_conv(int epi, int nbk, const void* a0, const void* a1, int Cin, i
     g.Hx = Hx; g.Wx = Wx;
     g.out = (bf16*)o0;
   }
-#define QD_LC(E, NBV) launch_conv_split<E, NBV>(A0, A1, B, O0, O1, O2, g, o0, o1, o2, st)
+#define QD_LC(E, NBV) launch_conv_split<E, NBV>(A0, A1, B, O0, O1, O2, g, o0, o1, o2, st, pair)
   if (epi == EPI_PROPOSED) return QD_LC(EPI_PROPOSED, 3);
   if (epi == EPI_T4) return QD_LC(EPI_T4, 2);
   if (epi == EPI_PLAIN) {

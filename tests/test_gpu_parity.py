@@ -1000,3 +1000,27 @@ def test_backward_on_a_fresh_host_thread():
     assert (out["dx"].double().cpu().numpy() == ref[4]).all()
     for role in ref[3]:
         assert (out["grads"][role].double().cpu().numpy() == ref[3][role]).all(), role
+
+
+@pytest.mark.parametrize("case", [("proposed", 64, 512, 512, 7, 1), ("t4", 32, 256, 512, 14, 2),
+                                  ("first_order", 16, 128, 256, 28, 2), ("proposed", 4, 64, 64, 9, 1)],
+                         ids=lambda c: f"{c[0]}_{c[1]}x{c[2]}x{c[4]}s{c[5]}")
+def test_conv_gemm_pair_matches_single(case, monkeypatch):
+    """The CTA-pair v1 conv GEMM (QD_CPAIR=1: M = 256 over two SMs, each holding
+    half of the weight tile; fprop, stride-1 dgrad, stride-2 parity-class dgrad,
+    split-K) reproduces the single-CTA kernel bit for bit (same MMAs per output
+    row, same accumulation order)."""
+    fam, n, c, f, hw, s = case
+    x, P, g = Q.synthetic_layer(fam, "conv", n, c, f, hw, hw, 3, s, 1, seed=4, random_bias=True)
+    base = run_device(fam, "conv", x, P, g, torch.bfloat16, 3, s, 1, flags=_lib_flag_v1())
+    monkeypatch.setenv("QD_CPAIR", "1")
+    pair = run_device(fam, "conv", x, P, g, torch.bfloat16, 3, s, 1, flags=_lib_flag_v1())
+    monkeypatch.delenv("QD_CPAIR")
+    assert (pair[0] == base[0]).all() and (pair[4] == base[4]).all()
+    for role in base[3]:
+        assert (pair[3][role] == base[3][role]).all(), role
+
+
+def _lib_flag_v1():
+    from paper_2204_01701_b200 import _lib
+    return _lib.FLAG_TC_V1
