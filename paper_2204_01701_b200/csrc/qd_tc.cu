@@ -197,21 +197,33 @@ __global__ void __launch_bounds__(256, 1)
         // class mode: first tap of the class's parity and its tap count along x
         const int ey0 = (args.pad_eff - cw.ph) & 1, ex0 = (args.pad_eff - cw.pw) & 1;
         const int ntx = (args.r - ex0 + 1) >> 1;
+        // k-block -> (K half, tap, channel block) walked incrementally: the divisions
+        // run once per work item, not per k-block (the single producer thread issues
+        // 1 + NB boxes per ~400 MMA cycles and was the limiter with them, ncu)
+        int half = cw.kb0 / args.kb_half, kk0 = cw.kb0 - half * args.kb_half;
+        int tap = kk0 / args.cblks, cb = kk0 - tap * args.cblks;
+        int ty = args.cls ? tap / ntx : tap / args.r;  // class: tap row in the class; else ey
+        int tx = args.cls ? tap - ty * ntx : tap - ty * args.r;
+        int kk = kk0;
+        int brow[NB];
+#pragma unroll
+        for (int i = 0; i < NB; ++i) {
+          const int j0 = (int)rank * NB * 32 + i * 32;
+          brow[i] = PAIR ? ntile * args.b_rs_tile + (j0 / 64) * args.b_rs_blk + j0 % 64
+                         : ntile * args.b_rs_tile + i * args.b_rs_blk;
+        }
         for (int kb = cw.kb0; kb < cw.kb1; ++kb) {
           ptx::mbar_wait(&empty[stage], phase ^ 1);
           if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], bytes);
-          int half = kb / args.kb_half, kk = kb % args.kb_half;
-          int tap = kk / args.cblks, cb = kk % args.cblks;
           int ax, ay, bk = kb;
           if (args.cls) {
-            const int ty = tap / ntx, ey = ey0 + 2 * ty, ex = ex0 + 2 * (tap - ty * ntx);
+            const int ey = ey0 + 2 * ty, ex = ex0 + 2 * tx;
             ay = h0 + ((cw.ph + ey - args.pad_eff) >> 1);  // even numerator: exact
             ax = w0 + ((cw.pw + ex - args.pad_eff) >> 1);
             bk = (ey * args.r + ex) * args.cblks + cb;
           } else {
-            int ey = tap / args.r, ex = tap % args.r;
-            ax = ss * w0 + ex - args.pad_eff;
-            ay = ss * h0 + ey - args.pad_eff;
+            ax = ss * w0 + tx - args.pad_eff;
+            ay = ss * h0 + ty - args.pad_eff;
           }
           const CUtensorMap* ma = (half > 0 && half == args.dual) ? &mapA1 : &mapA0;
           if (PAIR) {
@@ -219,19 +231,21 @@ __global__ void __launch_bounds__(256, 1)
             const uint32_t fb = ptx::peer0(&full[stage]);
             ptx::tma4_cg2(ma, fb, sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
 #pragma unroll
-            for (int i = 0; i < NB; ++i) {
-              const int j0 = (int)rank * NB * 32 + i * 32;
-              ptx::tma2_cg2(&mapB, fb, sB + stage * Cfg::B_BYTES + i * 4096, bk * 64,
-                            ntile * args.b_rs_tile + (j0 / 64) * args.b_rs_blk + j0 % 64);
-            }
+            for (int i = 0; i < NB; ++i)
+              ptx::tma2_cg2(&mapB, fb, sB + stage * Cfg::B_BYTES + i * 4096, bk * 64, brow[i]);
           } else {
             ptx::tma_load_4d(ma, &full[stage], sA + stage * Cfg::A_BYTES, cb * 64, ax, ay, n0);
 #pragma unroll
             for (int i = 0; i < NB; ++i)
-              ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, bk * 64,
-                               ntile * args.b_rs_tile + i * args.b_rs_blk);
+              ptx::tma_load_2d(&mapB, &full[stage], sB + stage * Cfg::B_BYTES + i * 8192, bk * 64, brow[i]);
           }
           if (++stage == STAGES) { stage = 0; phase ^= 1; }
+          // next k-block: channel block, then tap (x, then y), then K half
+          if (++cb == args.cblks) {
+            cb = 0;
+            if (++tx == (args.cls ? ntx : args.r)) { tx = 0; ++ty; }
+          }
+          if (++kk == args.kb_half) { kk = 0; ++half; ty = 0; tx = 0; cb = 0; }
         }
       }
     }
@@ -649,18 +663,29 @@ __global__ void __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t bytes = (uint32_t)(nA * 8192 + Cfg::B_BYTES);
+      // the CTA's two x k-blocks are fixed: decoded once; the pixel tile walks
+      // (w, h, n) incrementally (no divisions per stage in the producer thread)
+      int a_c[2] = {0, 0}, a_dx[2] = {0, 0}, a_dy[2] = {0, 0}, a_h[2] = {0, 0};
+      for (int a = 0; a < nA; ++a) {
+        const int kb = 2 * mtile + a;
+        const int half = kb / args.kb_half, kk = kb % args.kb_half;
+        const int tap = kk / args.cblks, cb = kk % args.cblks;
+        a_h[a] = half;
+        a_c[a] = cb * 64;
+        a_dx[a] = tap % args.r - args.pad;
+        a_dy[a] = tap / args.r - args.pad;
+      }
+      int tw = p_beg % args.pt_w, th = (p_beg / args.pt_w) % args.pt_h, tn = p_beg / (args.pt_w * args.pt_h);
       for (int pt = p_beg; pt < p_end; ++pt) {
-        int tw = pt % args.pt_w, th = (pt / args.pt_w) % args.pt_h, tn = pt / (args.pt_w * args.pt_h);
-        int w0 = tw * args.pb_w, h0 = th * args.pb_h, n0 = tn * args.pb_n;
+        const int w0 = tw * args.pb_w, h0 = th * args.pb_h, n0 = tn * args.pb_n;
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         ptx::mbar_arrive_expect_tx(&full[stage], bytes);
-        for (int a = 0; a < nA; ++a) {
-          int kb = 2 * mtile + a;
-          int half = kb / args.kb_half, kk = kb % args.kb_half;
-          int tap = kk / args.cblks, cb = kk % args.cblks;
-          int ey = tap / args.r, ex = tap % args.r;
-          ptx::tma_load_4d(half ? &mapX1 : &mapX0, &full[stage], sA + stage * Cfg::A_BYTES + a * 8192, cb * 64,
-                           args.sstride * w0 + ex - args.pad, args.sstride * h0 + ey - args.pad, n0);
+        for (int a = 0; a < nA; ++a)
+          ptx::tma_load_4d(a_h[a] ? &mapX1 : &mapX0, &full[stage], sA + stage * Cfg::A_BYTES + a * 8192, a_c[a],
+                           args.sstride * w0 + a_dx[a], args.sstride * h0 + a_dy[a], n0);
+        if (++tw == args.pt_w) {
+          tw = 0;
+          if (++th == args.pt_h) { th = 0; ++tn; }
         }
 #pragma unroll
         for (int i = 0; i < NBLK; ++i)
@@ -809,19 +834,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
       int stage = 0;
       uint32_t phase = 0;
       const uint32_t bytes = (uint32_t)((n_a(2 * mpair) + n_a(2 * mpair + 1)) * 8192 + 2 * Cfg::B_BYTES);
+      int a_c[2] = {0, 0}, a_dx[2] = {0, 0}, a_dy[2] = {0, 0}, a_h[2] = {0, 0};
+      for (int a = 0; a < nA; ++a) {
+        const int kb = 2 * mtile + a;
+        const int half = kb / args.kb_half, kk = kb % args.kb_half;
+        const int tap = kk / args.cblks, cb = kk % args.cblks;
+        a_h[a] = half;
+        a_c[a] = cb * 64;
+        a_dx[a] = tap % args.r - args.pad;
+        a_dy[a] = tap / args.r - args.pad;
+      }
+      int tw = p_beg % args.pt_w, th = (p_beg / args.pt_w) % args.pt_h, tn = p_beg / (args.pt_w * args.pt_h);
       for (int pt = p_beg; pt < p_end; ++pt) {
-        int tw = pt % args.pt_w, th = (pt / args.pt_w) % args.pt_h, tn = pt / (args.pt_w * args.pt_h);
-        int w0 = tw * args.pb_w, h0 = th * args.pb_h, n0 = tn * args.pb_n;
+        const int w0 = tw * args.pb_w, h0 = th * args.pb_h, n0 = tn * args.pb_n;
         ptx::mbar_wait(&empty[stage], phase ^ 1);
         if (rank == 0) ptx::mbar_arrive_expect_tx(&full[stage], bytes);
         const uint32_t fb = ptx::peer0(&full[stage]);
-        for (int a = 0; a < nA; ++a) {
-          int kb = 2 * mtile + a;
-          int half = kb / args.kb_half, kk = kb % args.kb_half;
-          int tap = kk / args.cblks, cb = kk % args.cblks;
-          int ey = tap / args.r, ex = tap % args.r;
-          ptx::tma4_cg2(half ? &mapX1 : &mapX0, fb, sA + stage * Cfg::A_BYTES + a * 8192, cb * 64,
-                        args.sstride * w0 + ex - args.pad, args.sstride * h0 + ey - args.pad, n0);
+        for (int a = 0; a < nA; ++a)
+          ptx::tma4_cg2(a_h[a] ? &mapX1 : &mapX0, fb, sA + stage * Cfg::A_BYTES + a * 8192, a_c[a],
+                        args.sstride * w0 + a_dx[a], args.sstride * h0 + a_dy[a], n0);
+        if (++tw == args.pt_w) {
+          tw = 0;
+          if (++th == args.pt_h) { th = 0; ++tn; }
         }
 #pragma unroll
         for (int i = 0; i < Cfg::HB; ++i)
