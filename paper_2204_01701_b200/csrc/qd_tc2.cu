@@ -1286,8 +1286,8 @@ __global__ void __launch_bounds__(256, 1)
     const bool leader = ptx::elect_one();
     int st = 0;
     uint32_t ph = 0;
-    for (int qb = q_beg; qb < q_end; ++qb) {
-      int n = qb / g.T_img, t = qb % g.T_img;
+    int n = q_beg / g.T_img, t = q_beg % g.T_img;  // walked incrementally below
+    for (int qb = q_beg; qb < q_end; ++qb, (++t == g.T_img ? (t = 0, ++n) : 0)) {
       int hq_lo = (128 * t) / g.Wp;
       if (leader) C2_TRACE(0, qb - q_beg, 0);
       ptx::mbar_wait(&empty[st], ph ^ 1);
@@ -1318,8 +1318,8 @@ __global__ void __launch_bounds__(256, 1)
     int st = 0;
     uint32_t ph = 0;
     uint32_t accum = 0;
-    for (int qb = q_beg; qb < q_end; ++qb) {
-      int t = qb % g.T_img;
+    int t = q_beg % g.T_img;
+    for (int qb = q_beg; qb < q_end; ++qb, (++t == g.T_img ? (t = 0) : 0)) {
       int q0 = 128 * t;
       int row_off = q0 - (q0 / g.Wp) * g.Wp;
       if (leader) C2_TRACE(1, qb - q_beg, 0);
@@ -1629,8 +1629,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     uint32_t ph = 0;
     // box i < ntb: D box i; i == ntb: the x halo. CTA0 issues [0, nsh), CTA1 the rest.
     const int nsh = (g.ntb + 1) / 2;
-    for (int qb = q_beg; qb < q_end; ++qb) {
-      int n = qb / g.T_img, t = qb % g.T_img;
+    int n = q_beg / g.T_img, t = q_beg % g.T_img;  // walked incrementally below
+    for (int qb = q_beg; qb < q_end; ++qb, (++t == g.T_img ? (t = 0, ++n) : 0)) {
       int hq_lo = g.R * t;
       if (leader) C2_TRACE(0, qb - q_beg, 0);
       ptx::mbar_wait(&empty[st], ph ^ 1);
