@@ -133,13 +133,34 @@ __global__ void __launch_bounds__(256) x3_pack_fc_kernel(Plan P, const float* w0
   }
 }
 
+// fc dgrad rows [hi | lo | hi] of the split pack: row cp = input channel, column j =
+// D channel (one tap); block (x, cp) covers 256 consecutive j -- the fc weights
+// are read along f (coalesced) and no per-element 64-bit index division remains
+__global__ void __launch_bounds__(256) x3_pack_fc_dgrad_kernel(Plan P, const float* w0, const float* w1,
+                                                               const float* w2, bf16* out) {
+  const int cp = blockIdx.y, j = blockIdx.x * 256 + threadIdx.x;
+  if (j >= P.Kd) return;
+  int role, c, f;
+  const bool nz = dgrad_src(P, cp, j, role, c, f);
+  const float* w = role == 0 ? w0 : (role == 1 ? w1 : w2);
+  const float v = nz ? __ldg(w + (size_t)c * P.F + f) : 0.f;
+  bf16 hi, lo;
+  x3_split1(v, hi, lo);
+  bf16* row = out + 3 * (size_t)P.nb * P.F * P.Kf + (size_t)cp * 3 * P.Kd;
+  row[j] = hi;
+  row[P.Kd + j] = lo;
+  row[2 * P.Kd + j] = hi;
+}
+
 void launch_x3_pack(const Plan& P, const float* const w[3], void* wpack, cudaStream_t st) {
   const long long nf = (long long)P.nb * P.F * P.Kf;
   long long i0 = 0;
   if (P.kind == QD_KIND_FC && P.sq == 0) {
     x3_pack_fc_kernel<<<dim3((P.F + 31) / 32, (P.C + 31) / 32, P.nroles), 256, 0, st>>>(P, w[0], w[1], w[2],
                                                                                          (bf16*)wpack);
-    i0 = nf;  // the dgrad rows read the fc weights along f: coalesced in the generic kernel
+    x3_pack_fc_dgrad_kernel<<<dim3((P.Kd + 255) / 256, P.Cd), 256, 0, st>>>(P, w[0], w[1], w[2], (bf16*)wpack);
+    count_launch(st, "x3_pack");
+    return;
   }
   const long long n = nf + (long long)P.Cd * P.Kd - i0;
   long long g = (n + 255) / 256;
