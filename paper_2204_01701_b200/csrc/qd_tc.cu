@@ -1410,15 +1410,15 @@ static long long wgrad_ptiles(const Plan& P) {
 // (per-SM MMA rate x TMA factor) with the factor min(1, 7 / operand KB per
 // 64-pixel k-step and 8K MACs) -- the single kernel at N = 256 delivers 48 KB per
 // 16 x 8K MACs, the pair 32 -- times whole waves of the grid, plus the fold's
-// S x Jd x Kf x 8 bytes of partial traffic. Only with QD_WPAIR=1.
+// S x Jd x Kf x 8 bytes of partial traffic; pairs take S = 1 (QD_WPAIR=0: never).
 struct WgShape { int pair, nblk, S; };
 static WgShape wgrad_v1_shape(const Plan& P) {
   const long long ptiles = wgrad_ptiles(P);
   const int sms = tc_num_sms(), nb = P.Jd / 64, mtiles = (P.Kf / 64 + 1) / 2;
   WgShape s{0, wgrad_ntile_blocks(P, ptiles), 1};
   s.S = (int)wgrad_split_for((long long)mtiles * (nb / s.nblk), ptiles, sms);
-  const char* on = getenv("QD_WPAIR");  // opt-in: measured no faster with its fold
-  if (!(on && atoi(on)) || mtiles < 2 || nb % 2) return s;
+  const char* on = getenv("QD_WPAIR");  // QD_WPAIR=0: single CTAs only
+  if ((on && !atoi(on)) || mtiles < 2 || nb % 2) return s;
   const double px = (double)ptiles * 64;
   auto cost = [&](int pair, int c, int S) {
     const long long units = (long long)(pair ? (mtiles + 1) / 2 : mtiles) * (nb / c) * S;
@@ -1431,9 +1431,12 @@ static WgShape wgrad_v1_shape(const Plan& P) {
     return waves * tile_us + fold_us;
   };
   double best = cost(0, s.nblk, s.S);
+  // pairs without extra pixel splits: an S = 2 pair's partial fold (~22 µs at
+  // 512@7) costs more than the split saves (measured); QD_WPAIR_SMAX=K (dev) allows K
+  const int smax = getenv("QD_WPAIR_SMAX") ? atoi(getenv("QD_WPAIR_SMAX")) : 1;
   for (int c = 4; c >= 2; c -= 2) {
     if (nb % c) continue;
-    for (int S = 1; S <= 4 && ptiles / S >= 4; ++S) {
+    for (int S = 1; S <= smax && ptiles / S >= 4; ++S) {
       const double t = cost(1, c, S);
       if (t < best * 0.97) { best = t; s = WgShape{1, c, S}; }
     }

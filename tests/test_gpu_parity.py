@@ -958,15 +958,19 @@ def test_operand_transform_bit_identical(case, monkeypatch):
 
 @pytest.mark.parametrize("shape", [(128, 512, 512, 7), (64, 256, 512, 14), (32, 128, 256, 8)])
 def test_wgrad_pair_matches_single(shape, monkeypatch):
-    """The CTA-pair v1 wgrad (QD_WPAIR=1: M = 256 over two SMs, each holding half
-    of the D boxes) gives the single-CTA kernel's weight gradients; both are
-    checked against the oracle elsewhere."""
+    """The CTA-pair v1 wgrad (M = 256 over two SMs, each holding half of the D
+    boxes; the default where its cost model picks it) gives the single-CTA
+    kernel's weight gradients (QD_WPAIR=0); both are checked against the oracle
+    elsewhere."""
     n, c, f, hw = shape
     x, P, g = Q.synthetic_layer("proposed", "conv", n, c, f, hw, hw, 3, 1, 1, seed=3, random_bias=True)
+    monkeypatch.setenv("QD_WPAIR", "0")
     base = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
     monkeypatch.setenv("QD_WPAIR", "1")
+    monkeypatch.setenv("QD_WPAIR_SMAX", "4")  # the split variants too
     pair = run_device("proposed", "conv", x, P, g, torch.bfloat16, 3, 1, 1)
     monkeypatch.delenv("QD_WPAIR")
+    monkeypatch.delenv("QD_WPAIR_SMAX")
     for role in base[3]:
         assert Q.rel_err(pair[3][role], base[3][role]) <= 1e-5, role
 
