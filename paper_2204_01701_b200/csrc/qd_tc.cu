@@ -1787,7 +1787,10 @@ int tc_backward(const Plan& P0, const void* x, const void* wpack, const void* a,
   if (w3 && dx && dW[0] && !P.sq && !getenv("QD_NO_PART") && !getenv("QD_BR2")) {
     const int per = wgrad3_pairs_per_split(P);
     const int total = L.wg_split * per;  // pairs the wgrad alone would fill
-    part = getenv("QD_PART") ? atoi(getenv("QD_PART")) : (total * 54 / per + 50) / 100;
+    // measured best: 54% of the pairs on the C2 step (32x32 images), 50% on the
+    // ResNet 64@56 layers (287.5 vs 299.2 us at 37 vs 40 pairs); QD_PART pins
+    const int pct = P.OH >= 48 ? 50 : 54;
+    part = getenv("QD_PART") ? atoi(getenv("QD_PART")) : (total * pct / per + 50) / 100;
     dg_pairs = total - part * per;
     // one pair per split only: with several (wide C) the split granularity is too
     // coarse to balance the two (measured: 256x14 loses 15%)
