@@ -1170,6 +1170,9 @@ void launch_bwd_finish(const Plan& P, const float* wpart, int S, const WSplits& 
     wfinish_fc_kernel<<<ntile + nbb, 256, 0, st>>>(P, wpart, S, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1], db[2],
                                                    ntile);
   } else {
+    if (getenv("QD_VERBOSE"))
+      fprintf(stderr, "[qd] generic bwd_finish: kind %d fam %d C %d F %d r %d Jd %d Kf %d S %d ng %d SB %d nbb %d\n", P.kind,
+              P.family, P.C, P.F, P.r, P.Jd, P.Kf, S, ws.ng, SB, nbb);
     bwd_finish_kernel<<<nwb + nbb, 256, 0, st>>>(P, wpart, S, ws, dW[0], dW[1], dW[2], bpart, SB, db[0], db[1],
                                                   db[2], nwb);
   }

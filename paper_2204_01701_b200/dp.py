@@ -54,6 +54,13 @@ def grad_ready(p):
     p._qd_red.ready(p)
 
 
+def _padded(n, align=32):
+    """elements a gradient view occupies in its bucket: rounded up to 32 fp32
+    (128 B), so every view starts aligned -- the library's folds write dW with
+    16-B vector stores and take a scalar fallback otherwise (4x slower, measured)"""
+    return (n + align - 1) // align * align
+
+
 class BucketedAllReduce:
     def __init__(self, params, bucket_mb=25.0, group=None, reduce_dtype=torch.float32, direct=True):
         self.group = group
@@ -71,7 +78,7 @@ class BucketedAllReduce:
                 self._make_bucket(cur, cur_n, reduce_dtype)
                 cur, cur_n = [], 0
             cur.append(p)
-            cur_n += p.numel()
+            cur_n += _padded(p.numel())
         if cur:
             self._make_bucket(cur, cur_n, reduce_dtype)
         self.pending = [0] * len(self.buckets)
@@ -96,7 +103,7 @@ class BucketedAllReduce:
         off = 0
         for p in ps:
             p.grad = flat[off:off + p.numel()].view_as(p)
-            off += p.numel()
+            off += _padded(p.numel())  # every view 128-B aligned (the library's vectorised folds)
         self.buckets.append((flat, ps))
 
     def _ready(self, bi):
