@@ -61,6 +61,8 @@ class QuadSGD(torch.optim.Optimizer):
         self._rest = torch.optim.SGD(rest, lr=lr, momentum=momentum, weight_decay=weight_decay,
                                      dampening=0.0, foreach=True) if rest else None
         self._packs = {}
+        self._streams = []
+        self.nstreams = 4  # streams the per-layer update + pack kernels are spread over
 
     @torch.no_grad()
     def step(self, closure=None):
@@ -68,7 +70,10 @@ class QuadSGD(torch.optim.Optimizer):
         g = self.param_groups[0]
         lr, mom, wd = g["lr"], g["momentum"], g["weight_decay"]
         lib = _lib.load()
-        stream = torch.cuda.current_stream().cuda_stream
+        # pass 1 on the current stream: state, packs and descriptors (allocations and
+        # first-time packs are ordered on it)
+        cur = torch.cuda.current_stream()
+        work = []
         for m in self.quad:
             roles = neurons.WEIGHT_ROLES[m.spec.family]
             ws = [getattr(m, r) for r in roles]
@@ -89,6 +94,18 @@ class QuadSGD(torch.optim.Optimizer):
             if not all(w.is_contiguous() for w in ws):
                 raise RuntimeError("QuadSGD: quadratic weights must stay in the standard contiguous layout")
             grads = [w.grad.contiguous() for w in ws]
+            work.append((ws, states, first, desc, wpack, grads))
+        # pass 2: the per-layer update + pack kernels are independent; spread over a
+        # few streams forked from the current one (most layers are small and
+        # latency-bound), joined back before the rest of the step
+        nstreams = min(self.nstreams, len(work))
+        if nstreams > 1:
+            if len(self._streams) < nstreams:
+                self._streams = [torch.cuda.Stream(device=cur.device) for _ in range(nstreams)]
+            for sx in self._streams[:nstreams]:
+                sx.wait_stream(cur)
+        for li, (ws, states, first, desc, wpack, grads) in enumerate(work):
+            stream = (self._streams[li % nstreams] if nstreams > 1 else cur).cuda_stream
             st = lib.qd_sgd_pack(ctypes.byref(desc), _lib.ptr3(*[w.data_ptr() for w in ws]),
                                  _lib.ptr3(*[s_["momentum_buffer"].data_ptr() for s_ in states]),
                                  _lib.ptr3(*[gr.data_ptr() for gr in grads]), float(lr), float(mom),
@@ -97,6 +114,9 @@ class QuadSGD(torch.optim.Optimizer):
             for w in ws:  # the kernel changed the weights in place: bump their version counters
                 torch.autograd.graph.increment_version(w)
             neurons.register_pack(desc, ws, wpack)
+        if nstreams > 1:
+            for sx in self._streams[:nstreams]:
+                cur.wait_stream(sx)
         if self._rest is not None:
             self._sync_rest()
             self._rest.step()
