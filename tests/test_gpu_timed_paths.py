@@ -174,3 +174,19 @@ def test_resnet_stride2_layers_batch128_vs_oracle(c, f, hw):
     names, _ = check_full("proposed", "conv", 128, c, f, hw, hw, 3, 2, 1, torch.bfloat16, seed=0,
                           random_bias=True, chunk=8)
     assert "conv_gemm" in names or "conv2" in names, names
+
+
+# ---- C5 cross product off the diagonal (SURVEY.md §8(d) "full 4 x 4") ---------
+# The kernel plan (halo tiles, resident weights, wgrad form, split-K) follows the
+# layer shape (C, H, W), so every off-diagonal point of the measured grid
+# (profiles/r2f_c5_grid.txt) is checked here at a small batch the fp64 oracle
+# finishes in seconds; the diagonal runs at the full N = 64 above.
+C5_OFF = [(c, hw) for c in (64, 128, 256, 512) for hw in (56, 28, 14, 7)
+          if (c, hw) not in ((64, 56), (128, 28), (256, 14), (512, 7))]
+C5_OFF_CASES = [(fam, c, hw) for fam in ("proposed", "t4", "t2_linear") for c, hw in C5_OFF]
+
+
+@pytest.mark.parametrize("fam,c,hw", C5_OFF_CASES, ids=[f"{a}-{b}x{d}" for a, b, d in C5_OFF_CASES])
+def test_c5_grid_off_diagonal_vs_oracle(fam, c, hw):
+    n = 4 if hw >= 28 else 8
+    check_full(fam, "conv", n, c, c, hw, hw, 3, 1, 1, torch.bfloat16, seed=0, random_bias=True, chunk=1)
