@@ -1050,7 +1050,14 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
     while (aslots > 2 && fixed0 + (size_t)aslots * halo + 4 * (size_t)bstage > limit) --aslots;
     if (fixed0 + (size_t)aslots * halo + 2 * (size_t)bstage > limit) return pl;
     slots = (int)((limit - fixed0 - (size_t)aslots * halo) / bstage);
-    if (slots > 8) slots = 8;
+    // ring depth cap 8: deeper rings for the small (4 / 8 KB) stages were measured neutral
+    // to slower (the larger footprint delays the next PDL-launched kernel's CTAs)
+    int cap = 8;
+    {
+      const char* e = getenv("QD_C2_BSLOTS");  // dev knob: B ring depth cap (2..48)
+      if (e && atoi(e) >= 2 && atoi(e) <= 48) cap = atoi(e);
+    }
+    if (slots > cap) slots = cap;
   }
   const size_t fixed = fixed0 + (size_t)aslots * halo;
   g.N = N; g.Cin = Cin; g.Win = Win; g.Hin = Hin; g.OHg = OHg; g.OWg = OWg;
