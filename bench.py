@@ -39,6 +39,8 @@ WORKLOADS = {
     "c2": ("proposed", "conv", 128, 64, 64, 32, 32, 3, 1, 1, "bf16"),
     "c2_fp32": ("proposed", "conv", 128, 64, 64, 32, 32, 3, 1, 1, "fp32"),
     "c1": ("proposed", "fc", 256, 512, 512, 1, 1, 1, 1, 0, "fp32"),
+    "x3_128x28": ("proposed", "conv", 64, 128, 128, 28, 28, 3, 1, 1, "fp32"),
+    "x3_64x56": ("proposed", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "fp32"),
     "c5_proposed_64x56": ("proposed", "conv", 64, 64, 64, 56, 56, 3, 1, 1, "bf16"),
     "c5_proposed_128x28": ("proposed", "conv", 64, 128, 128, 28, 28, 3, 1, 1, "bf16"),
     "c5_proposed_256x14": ("proposed", "conv", 64, 256, 256, 14, 14, 3, 1, 1, "bf16"),

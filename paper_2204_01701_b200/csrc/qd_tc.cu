@@ -2063,7 +2063,10 @@ int x3_backward(const Plan& P, const void* x, const void* wpack, const void* a, 
   // on ~half of the pairs on the side stream, the persistent dgrad capped to the rest
   int S = L.wg_split, dg_pairs = 0;
   if (w3 && c2d && !getenv("QD_NO_PART")) {
-    const int part = getenv("QD_X3_PART") ? atoi(getenv("QD_X3_PART")) : (L.wg_split * 35 + 50) / 100;  // measured best on C2-fp32 (26 of 74)
+    // measured on C2-fp32 (tools/x3_part_sweep.sh): 39 of 74 pairs with the grouped B stream
+    // of the 64-channel dgrad (254 vs 222 TFLOP/s at the old 26, the best for the per-tap ring)
+    const int pct = P.C == 64 ? 53 : 35;
+    const int part = getenv("QD_X3_PART") ? atoi(getenv("QD_X3_PART")) : (L.wg_split * pct + 50) / 100;
     if (part >= 1 && part < L.wg_split) {
       S = part;
       dg_pairs = L.wg_split - part;

@@ -46,6 +46,7 @@ struct C2Args {
   int Cout, out_c_tile;
   uint32_t halo_bytes, halo_tx, b_stage_bytes;
   int b_slots, a_slots, stg_tiles;
+  int b_group;  // streamed B: taps per ring slot (1, or r*r = one barrier per channel block)
   int nbias;  // bias vectors staged in smem (3 proposed, 1 first_order, else 0), Cout floats each
   int direct;  // epilogue stores straight from registers (no smem staging)
   int pf;      // L2 prefetch distance of the A halo boxes, in this cluster's tiles (0 = off)
@@ -252,7 +253,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB, X
   uint8_t* sm = (uint8_t*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
   uint8_t* sHalo = sm;
   uint8_t* sB = sHalo + g.a_slots * g.halo_bytes;
-  uint8_t* sStg = sB + g.b_slots * g.b_stage_bytes;
+  uint8_t* sStg = sB + g.b_slots * g.b_group * g.b_stage_bytes;
   float* sBias = (float*)(sStg + 4 * g.stg_tiles * 4096);
   uint64_t* afull = (uint64_t*)(sBias + g.nbias * g.Cout);
   uint64_t* aempty = afull + 4;
@@ -353,7 +354,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB, X
           }
         }
         if (++as == g.a_slots) { as = 0; aph ^= 1; }
-        if (!g.resident) {
+        if (!g.resident && g.b_group > 1) {
+          // all taps of this channel block on one barrier (one wait / commit per block on the MMA side)
+          ptx::mbar_wait(&bempty[bs], bph ^ 1);
+          if (leader) {
+            if (rank == 0) ptx::mbar_arrive_expect_tx(&bfull[bs], 2u * rr * g.b_stage_bytes);
+            for (int tap = 0; tap < rr; ++tap)
+              c2::tma2_cg2(&mB, c2::peer0(&bfull[bs]), sB + (bs * rr + tap) * g.b_stage_bytes,
+                           ((half * rr + tap) * g.cblks + cb) * 64, brow(j));
+          }
+          if (++bs == g.b_slots) { bs = 0; bph ^= 1; }
+        } else if (!g.resident) {
           for (int tap = 0; tap < rr; ++tap) {
             int kbi = (half * rr + tap) * g.cblks + cb;
             ptx::mbar_wait(&bempty[bs], bph ^ 1);
@@ -405,10 +416,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB, X
           if (leader) C2_TRACE(1, it, 2 + ab);
           ptx::tc_fence_after();
           const uint32_t a_lo = halo_lo0 + as * halo_step + row_off * 8;
-          if (g.resident && !(g.dbg & 2)) {
-            // all taps of this channel block back to back (B resident: no waits)
-            const uint32_t bb = b_lo0 + (half * rr * g.cblks + cb) * b_step;
-            const uint32_t tap_b = g.cblks * b_step;
+          const bool grouped = !g.resident && g.b_group > 1;
+          if ((g.resident && !(g.dbg & 2)) || grouped) {
+            // all taps of this channel block back to back (B resident: no waits;
+            // grouped stream: one wait and one commit per block)
+            if (grouped) {
+              ptx::mbar_wait(&bfull[bs], bph);
+              ptx::tc_fence_after();
+            }
+            const uint32_t bb = grouped ? b_lo0 + bs * rr * b_step : b_lo0 + (half * rr * g.cblks + cb) * b_step;
+            const uint32_t tap_b = grouped ? b_step : g.cblks * b_step;
             if (leader) {
               if (R > 0) {
 #pragma unroll
@@ -436,6 +453,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(C2Threads<EPI, NB, X
             }
             accum = 1;
             __syncwarp();
+            if (grouped) {
+              if (leader) c2::commit_mc(&bempty[bs]);
+              if (++bs == g.b_slots) { bs = 0; bph ^= 1; }
+            }
           } else {
             for (int ey = 0; ey < r; ++ey) {
               for (int ex = 0; ex < r; ++ex) {
@@ -1026,7 +1047,7 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   const size_t bias_bytes = (size_t)nbias * Cout * 4;
   const size_t fixed0 = 1024 + 4 * (size_t)stg_tiles * 4096 + bias_bytes + 1024;  // slack, staging, biases, barriers
   const size_t limit = 227 * 1024;
-  int resident = 0, slots, aslots = 0;
+  int resident = 0, slots, aslots = 0, bgroup = 1;
   // prefer resident B with >= 3 halo buffers; else stream B with a 4-deep halo ring
   if (tiles_nn == 1 && KBtot <= 48) {
     size_t rest = limit - fixed0 - (size_t)KBtot * bstage;
@@ -1058,6 +1079,22 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
       if (e && atoi(e) >= 2 && atoi(e) <= 48) cap = atoi(e);
     }
     if (slots > cap) slots = cap;
+    // grouped stream (all r*r taps of a channel block per ring slot) where two groups fit
+    // beside the halo ring: the MMA warp then waits / commits once per block, not per tap
+    const char* eg = getenv("QD_C2_BGROUP");  // dev knob: 0 = per-tap ring, 1 = grouped wherever it fits
+    const int gmode = eg ? atoi(eg) : -1;
+    const size_t gbytes = (size_t)r * r * bstage;
+    const bool gwant = gmode == 1 || (gmode < 0 && bstage <= 4096);
+    if (gwant) {
+      int ga = aslots;
+      while (ga > 2 && fixed0 + (size_t)ga * halo + 2 * gbytes > limit) --ga;
+      if (fixed0 + (size_t)ga * halo + 2 * gbytes <= limit) {
+        aslots = ga;
+        bgroup = r * r;
+        slots = (int)((limit - fixed0 - (size_t)aslots * halo) / gbytes);
+        if (slots > 3) slots = 3;
+      }
+    }
   }
   const size_t fixed = fixed0 + (size_t)aslots * halo;
   g.N = N; g.Cin = Cin; g.Win = Win; g.Hin = Hin; g.OHg = OHg; g.OWg = OWg;
@@ -1065,9 +1102,9 @@ static C2Plan c2_plan(int N, int Cin, int Win, int Hin, int OWg, int OHg, int pe
   g.T_img = T_img; g.tiles_nn = tiles_nn; g.total = ((N + 1) / 2) * T_img * tiles_nn;
   g.fd_nn = ptx::make_fastdiv(tiles_nn); g.fd_T = ptx::make_fastdiv(T_img); g.fd_Wp = ptx::make_fastdiv(Wp);
   g.cblks = cblks; g.ablocks = ablocks; g.KBtot = KBtot; g.resident = resident;
-  g.halo_bytes = halo; g.halo_tx = halo_tx; g.b_stage_bytes = bstage; g.b_slots = slots; g.a_slots = aslots; g.stg_tiles = stg_tiles; g.nbias = nbias;
+  g.halo_bytes = halo; g.halo_tx = halo_tx; g.b_stage_bytes = bstage; g.b_slots = slots; g.b_group = bgroup; g.a_slots = aslots; g.stg_tiles = stg_tiles; g.nbias = nbias;
   g.Cout = Cout;
-  pl.smem = fixed + (size_t)slots * bstage;
+  pl.smem = fixed + (size_t)slots * bgroup * bstage;
   pl.ok = true;
   return pl;
 }

@@ -1,5 +1,6 @@
 #!/bin/bash
-# A/B of the conv2 B-ring depth cap (QD_C2_BSLOTS=8 = the old cap) on the workloads whose
+# A/B of the conv2 streamed-B ring: per-tap slots (QD_C2_BGROUP=0) vs one slot per channel block
+# (all r*r taps on one barrier); QD_C2_BSLOTS caps the per-tap ring depth on the workloads whose
 # conv2 kernels stream B. Run under gpurun from the repo root; output gpurun_out/<tag>_bslots_ab.txt
 tag=${1:-rx}
 out=gpurun_out/${tag}_bslots_ab.txt
@@ -12,9 +13,8 @@ k = d['roofline']['kernels']
 print('%8.1f TFLOP/s %8.4f ms  ' % (d['value'], d['ms_per_step']) + ' '.join('%s=%.1f' % (n, v['ms'] * 1e3) for n, v in k.items() if 'conv' in n))")
   echo "$3 [$1] $v" | tee -a $out
 }
-for w in c5_proposed_128x28 c5_proposed_256x14 r18_128x28 r18_256x14 c5_proposed_512x7; do
-  for c in 3 4 6 8 12; do one cap$c QD_C2_BSLOTS=$c $w; done
-done
-for c in 4 6 8; do
-  echo "qresnet18 [cap$c] $(QD_C2_BSLOTS=$c python bench.py --workload qresnet18 --steps 20 --warmup 5 --no-cpu 2>/dev/null | python -c "import sys,json; d=json.loads(sys.stdin.read().strip().splitlines()[-1]); print(d['value'], d['ms_per_step'])")" | tee -a $out
+for w in c2_fp32 c5_proposed_128x28 c5_proposed_256x14 r18_128x28 r18_256x14 c5_t4_64x56; do
+  one pertap QD_C2_BGROUP=0 $w
+  one default QD_NOOP=1 $w
+  one grouped QD_C2_BGROUP=1 $w
 done
