@@ -1028,3 +1028,30 @@ def test_conv_gemm_pair_matches_single(case, monkeypatch):
 def _lib_flag_v1():
     from paper_2204_01701_b200 import _lib
     return _lib.FLAG_TC_V1
+
+
+@pytest.mark.parametrize("case", [("proposed", 6, 64, 64, 32, 32, 3), ("t4", 3, 64, 128, 17, 23, 3),
+                                  ("proposed", 2, 64, 64, 20, 20, 5), ("proposed", 4, 128, 128, 14, 14, 3)],
+                         ids=lambda c: f"{c[0]}_{c[1]}x{c[2]}x{c[4]}x{c[5]}k{c[6]}")
+def test_grouped_b_stream_bit_identical(case, monkeypatch):
+    """conv2 with streamed weights: one ring slot / barrier per channel block (all
+    r*r taps, the default for 4 KB stages -- the fp32 split dgrad of 64-channel
+    layers; QD_C2_BGROUP=1 everywhere it fits) issues the same MMAs in the same
+    order as the per-tap ring (QD_C2_BGROUP=0), so every output is bit-identical;
+    the grouped form is also checked against the fp64 oracle at 1e-4."""
+    fam, n, c, f, h, w, k = case
+    p = k // 2
+    x, P, g = Q.synthetic_layer(fam, "conv", n, c, f, h, w, k, 1, p, seed=31, random_bias=True)
+    monkeypatch.setenv("QD_C2_BGROUP", "0")
+    base = run_device(fam, "conv", x, P, g, torch.float32, k, 1, p)
+    monkeypatch.setenv("QD_C2_BGROUP", "1")
+    grp = run_device(fam, "conv", x, P, g, torch.float32, k, 1, p)
+    monkeypatch.delenv("QD_C2_BGROUP")
+    dflt = run_device(fam, "conv", x, P, g, torch.float32, k, 1, p)
+    assert base[5] == 3 and grp[5] == 3
+    for other in (grp, dflt):
+        assert (other[0] == base[0]).all() and (other[4] == base[4]).all()
+        for role in base[3]:
+            assert (other[3][role] == base[3][role]).all(), role
+    monkeypatch.setenv("QD_C2_BGROUP", "1")
+    assert check_against_oracle(fam, "conv", x, P, g, torch.float32, k, 1, p) == 3
